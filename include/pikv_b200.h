@@ -1,0 +1,283 @@
+/* SPDX-License-Identifier: Apache-2.0
+ *
+ * pikv_b200.h — C-ABI of the B200-native PiKV decode engine.
+ *
+ * This is the drop-in boundary for the reference's decode path
+ * (`pikv::Engine::step`, /root/reference/proj/src/pipeline.cpp:213-351) and
+ * the free functions it is built from.  Every entry point names the reference
+ * interface it replaces.  Signatures use plain pointers and sizes only; all
+ * device buffers are caller-owned CUDA device pointers unless the name ends
+ * in `_host`.  Store memory (paged KV pool, slot metadata) is owned by the
+ * engine.
+ *
+ * Error convention: every call returns an int status.  0 is success; the
+ * non-zero codes map 1:1 onto the reference's exception classes
+ * (/root/reference/proj/include/pikv/errors.hpp:9-47) plus CUDA/NCCL/OOM.
+ * `pikv_last_error()` returns the message of the last failure on the calling
+ * thread.  A failing step leaves no partial state (pipeline.cpp:153-154).
+ *
+ * Threading: an engine is single-writer; calls are
+ * stream-ordered on the engine's CUDA stream and not thread-safe per engine.
+ */
+#ifndef PIKV_B200_H
+#define PIKV_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (errors.hpp:9-47) ---------------------------------- */
+#define PIKV_OK 0
+#define PIKV_ERR_INVALID_ARGUMENT 1        /* pikv::InvalidArgument  errors.hpp:13 */
+#define PIKV_ERR_INVALID_CONFIG 2          /* pikv::InvalidConfig    errors.hpp:17 */
+#define PIKV_ERR_INVALID_ENTRY 3           /* pikv::InvalidEntry     errors.hpp:21 */
+#define PIKV_ERR_NUMERICAL 4               /* pikv::NumericalError   errors.hpp:25 */
+#define PIKV_ERR_CODEC_MISMATCH 5          /* pikv::CodecMismatch    errors.hpp:29 */
+#define PIKV_ERR_NOT_FITTED 6              /* pikv::NotFitted        errors.hpp:33 */
+#define PIKV_ERR_INSUFFICIENT_CALIBRATION 7
+#define PIKV_ERR_INVALID_COMPARISON 8
+#define PIKV_ERR_IO 9
+#define PIKV_ERR_CUDA 10
+#define PIKV_ERR_NCCL 11
+#define PIKV_ERR_OUT_OF_MEMORY 12          /* KV page pool exhausted */
+
+/* ---- enums (same order as the reference enums) ------------------------ */
+/* RouterStrategy, router.hpp:11-19 */
+#define PIKV_ROUTER_BASE 0
+#define PIKV_ROUTER_TOPK 1
+#define PIKV_ROUTER_LOAD_BALANCED 2
+#define PIKV_ROUTER_CACHE_AWARE 3
+#define PIKV_ROUTER_ENTROPY_LB 4
+#define PIKV_ROUTER_ADAPTIVE 5
+#define PIKV_ROUTER_HIERARCHICAL 6
+/* SchedStrategy, scheduler.hpp:16-25 (QUEST is out of scope: needs an Eigen fit) */
+#define PIKV_SCHED_H2O 0
+#define PIKV_SCHED_SL 1
+#define PIKV_SCHED_QUEST 2
+#define PIKV_SCHED_FLEX 3
+#define PIKV_SCHED_LRU 4
+#define PIKV_SCHED_LRU_PLUS 5
+#define PIKV_SCHED_ADAKV 6
+#define PIKV_SCHED_DUO 7
+/* EvictReason, scheduler.hpp:87 */
+#define PIKV_EVICT_BUDGET 0
+#define PIKV_EVICT_THRESHOLD 1
+#define PIKV_EVICT_OVERWRITE 2
+/* Stored-entry codecs.  IDENTITY/LOWRANK/LORAPLUS/FASTV/PRUNE follow the
+ * reference's projection schemes (compressor.cpp:318-474) with one basis per
+ * head; INT8/INT4 are this engine's quantizers (not in the reference,
+ * SPEC.md:331). */
+#define PIKV_CODEC_IDENTITY 0
+#define PIKV_CODEC_LOWRANK 1   /* Scheme::SVD / Scheme::LoRA: y = B^T x     */
+#define PIKV_CODEC_LORAPLUS 2  /* Scheme::LoRAPlus: y = B^T (x - bias)      */
+#define PIKV_CODEC_FASTV 3     /* Scheme::FastV: keep the first r coords     */
+#define PIKV_CODEC_PRUNE 4     /* Scheme::Prune: keep sorted coords `kept`   */
+#define PIKV_CODEC_INT8 5      /* symmetric absmax per (entry, head)         */
+#define PIKV_CODEC_INT4 6      /* symmetric absmax per (entry, head), packed */
+/* input / storage dtypes */
+#define PIKV_DTYPE_F32 0
+#define PIKV_DTYPE_BF16 1
+
+/* ---- configuration ------------------------------------------------------
+ * One flat POD mirroring EngineConfig (pipeline.hpp:87-98) and the configs
+ * it aggregates.  Field meanings follow the reference; extra fields are the
+ * batch/multi-head/runtime knobs the reference does not have.             */
+typedef struct pikv_config {
+    /* ModelConfig, config.hpp:23-55 */
+    int32_t d;            /* query/key/value width before compression       */
+    int32_t head_width;   /* h: fetch-cost model only (pipeline.cpp:22-26)  */
+    int32_t E;            /* experts                                         */
+    int32_t k;            /* active experts per token (RouterConfig.k too)   */
+    int64_t L;            /* token budget (cost model only)                  */
+    int32_t G;            /* devices of shard_assign (kvstore.cpp:14-30)     */
+    int32_t S;            /* shard ring capacity                             */
+    int32_t K;            /* ModelConfig.K (cost model only)                 */
+    int32_t elem_bytes;   /* bytes per stored scalar for memory_bytes()      */
+    double rho;           /* d / d'                                          */
+    /* multi-head convention: H independent heads of width
+     * d/H; attention is per head, attn_mass += mean over heads of alpha.   */
+    int32_t n_heads;
+    /* StoreConfig, kvstore.hpp:63-72 */
+    int32_t n_tok, n_exp, additive, shards_per_device;
+    /* RouterConfig, router.hpp:24-37 */
+    int32_t router_strategy, groups, stride;
+    double alpha, lambda_miss, beta_ent, bandit_step, bias_cap, load_decay;
+    /* SchedulerConfig, scheduler.hpp:30-47 */
+    int32_t sched_strategy, budget_pages, page_size, sink, flex_bucket;
+    int32_t n_adakv_weights, n_flex_plan;
+    double tau, lambda_freq, adakv_step, target_hit, gamma_sim, theta0, hit_decay;
+    double adakv_weights[8];
+    double flex_plan[32];
+    /* CompressorConfig, compressor.hpp:28-41 (runtime part only) */
+    int32_t codec;        /* PIKV_CODEC_*                                    */
+    int32_t rank;         /* r per head for LOWRANK/LORAPLUS/FASTV/PRUNE     */
+    /* EngineConfig, pipeline.hpp:87-98 */
+    int32_t unbounded_budget;
+    int32_t n_layers;     /* width of per_layer_scores (TokenInput.layer_saliency) */
+    /* B200 runtime (no reference counterpart) */
+    int32_t batch;        /* B independent decode streams     */
+    int32_t kv_dtype;     /* PIKV_DTYPE_*: dtype of q/k/v inputs and of the
+                             stored identity/low-rank payload               */
+    int32_t world_size;   /* ranks; rank r owns devices g with g % world == r */
+    int32_t rank_id;
+    int64_t pool_entries; /* KV page pool capacity in entries (0 = auto)     */
+    uint64_t seed;        /* EngineConfig.seed: W_r = Rng(seed ^ kRouterSalt) */
+} pikv_config;
+
+/* One eviction record, scheduler.hpp:90-98 (+ the stream it belongs to). */
+typedef struct pikv_evict_record {
+    uint64_t step;
+    uint64_t entry_id;
+    int64_t token_id;
+    int32_t expert_id;
+    int32_t device;
+    double score;
+    int32_t reason;     /* PIKV_EVICT_* */
+    int32_t stream;
+} pikv_evict_record;
+
+/* Per-stream summary of the last step (StepResult, pipeline.hpp:68-80). */
+typedef struct pikv_step_summary {
+    uint64_t step;
+    int32_t inserts;
+    int32_t hits;
+    int32_t lookups;
+    int32_t n_attended;      /* attn.retrieved                              */
+    int64_t fetch_elements;  /* pipeline.cpp:262-264                         */
+    int32_t n_evictions;     /* overwrite + scheduled                         */
+    int32_t pages_before;    /* EvictionReport, scheduler.hpp:100-104        */
+    int32_t pages_after;
+    int32_t error;           /* per-stream PIKV_ERR_* raised on device        */
+} pikv_step_summary;
+
+typedef struct pikv_engine pikv_engine;
+
+/* ---- library --------------------------------------------------------- */
+const char* pikv_version(void);
+const char* pikv_last_error(void);
+int pikv_config_size(void);                 /* sizeof(pikv_config) for FFI checks */
+/* Fills `cfg` with the reference defaults (config.hpp, kvstore.hpp:63-72,
+ * router.hpp:24-37, scheduler.hpp:30-47, compressor.hpp:28-41). */
+void pikv_config_default(pikv_config* cfg);
+
+/* ---- pure functions (device kernels over arrays) ----------------------- */
+/* shard_assign, kvstore.cpp:14-30, for n (t, e) pairs; outputs device/shard/raw. */
+int pikv_shard_assign(const int64_t* t, const int32_t* e, int32_t n, int32_t n_tok,
+                      int32_t n_exp, int32_t devices, int32_t additive,
+                      int32_t* device_out, int32_t* shard_out, int32_t* raw_out);
+/* select_evictions, scheduler.cpp:231-260, on one device's page list.
+ * Writes up to n victims (page index, reason) in eviction order. */
+int pikv_select_evictions(const double* aggregate, const uint64_t* oldest_id,
+                          int32_t n, int32_t budget_pages, int32_t use_theta,
+                          double theta, int32_t* idx_out, int32_t* reason_out,
+                          int32_t* n_out);
+/* attention, pipeline.cpp:59-85, for `n_queries` independent single-head
+ * problems of width w over n entries each (fp32 in/out; fp64 not used). */
+int pikv_attention(const float* q, const float* keys, const float* values,
+                   int32_t n_queries, int32_t n, int32_t w, float* y_out,
+                   float* weights_out);
+/* int8/int4 codes (this engine's quantizer; oracle/pikv_oracle.c restates it). */
+int pikv_quantize(const void* x, int32_t dtype, int32_t rows, int32_t width,
+                  int32_t bits, uint8_t* codes_out, float* scales_out);
+int pikv_dequantize(const uint8_t* codes, const float* scales, int32_t rows,
+                    int32_t width, int32_t bits, float* x_out);
+/* Codec::project_encode / project_decode, compressor.cpp:318-340, per head:
+ * x [rows][H*hd] -> y [rows][H*r] with basis [H][r][hd] (column j of the
+ * reference's col-major d x r basis is basis[h][j][:]). */
+int pikv_lowrank_encode(const float* x, const float* basis, const float* bias,
+                        int32_t rows, int32_t heads, int32_t hd, int32_t r, float* y_out);
+int pikv_lowrank_decode(const float* y, const float* basis, const float* bias,
+                        int32_t rows, int32_t heads, int32_t hd, int32_t r, float* x_out);
+
+/* ---- engine (Engine, pipeline.hpp:101-145) ------------------------------ */
+int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine** out);
+int pikv_engine_destroy(pikv_engine* eng);
+/* The engine's CUDA stream (cudaStream_t) all calls are ordered on. */
+void* pikv_engine_stream(pikv_engine* eng);
+/* RouterState::init(E, d, seed ^ kRouterSalt) (router.cpp:54-67,
+ * pipeline.cpp:16,91) is done at create; this overrides W_r (E x d, fp64,
+ * host, row-major) for all streams. */
+int pikv_set_router_matrix_host(pikv_engine* eng, const double* w_r);
+/* Codec parameters (host): basis [H][r][hd] fp32, bias [d] fp32 (LoRAPlus),
+ * kept [H][r] int32 (Prune). Pass NULL for unused ones. */
+int pikv_set_codec_host(pikv_engine* eng, const float* basis, const float* bias,
+                        const int32_t* kept);
+
+/* Engine::step for all B streams.  q/k/v: device [B][d] in cfg.kv_dtype;
+ * saliency: device [B][n_layers] fp64 or NULL; y_out: device [B][d'] fp32
+ * (attention output in compressed space, pipeline.cpp:295-299).  Enqueued on
+ * the engine stream; no host synchronisation. */
+int pikv_step(pikv_engine* eng, const void* q, const void* k, const void* v,
+              const double* saliency, float* y_out);
+/* Same step through HOST buffers (pinned or pageable): copies the inputs in,
+ * runs the step and copies y back, synchronising before returning. */
+int pikv_step_host(pikv_engine* eng, const void* q, const void* k, const void* v,
+                   const double* saliency, float* y_out);
+/* Multi-rank step: run the rank-local part, exchange the merge records with
+ * an all-gather (caller-provided, e.g. NCCL), then finish.  The exchange
+ * buffer is device memory of pikv_exchange_bytes() per rank. */
+int64_t pikv_exchange_bytes(pikv_engine* eng);
+int pikv_step_local(pikv_engine* eng, const void* q, const void* k, const void* v,
+                    const double* saliency, void** exchange_out);
+int pikv_step_finish(pikv_engine* eng, const void* gathered /* [world][exchange] */,
+                     float* y_out);
+/* Prefill `tokens` decode steps without attention (store synthesis for
+ * benchmarks): synthetic q/k/v ~ N(0,1) rounded to kv_dtype, generated on the
+ * device from `seed`.  Route/insert/evict/retrieve all run as in step(). */
+int pikv_prefill_synthetic(pikv_engine* eng, int64_t tokens, uint64_t seed);
+/* Device-side synthetic inputs for one step ([B][d] each, kv_dtype). */
+int pikv_fill_synthetic(pikv_engine* eng, void* q, void* k, void* v, uint64_t seed);
+int pikv_sync(pikv_engine* eng);
+
+/* ---- results / state readback (host) -------------------------------- */
+/* experts [B][k] int32, gates [B][k] f64, logits [B][E] f64, summary [B].
+ * Any pointer may be NULL.  Synchronises. */
+int pikv_read_step_host(pikv_engine* eng, int32_t* experts, double* gates,
+                        double* logits, pikv_step_summary* summary);
+/* Eviction records of the last step for all streams, reference order per
+ * stream (overwrites, then per device the scheduled victims). */
+int pikv_read_evictions_host(pikv_engine* eng, pikv_evict_record* out, int32_t cap,
+                             int32_t* n_out);
+/* Attended entries of the last step of `stream`: (token, expert, alpha) in
+ * this engine's (ring, slot) order; the reference orders by (token, expert). */
+int pikv_read_attended_host(pikv_engine* eng, int32_t stream, int64_t* token,
+                            int32_t* expert, double* alpha, int32_t cap,
+                            int32_t* n_out);
+/* Slot metadata of `stream` for its owned devices:
+ * [G_local][SPD][S] arrays; id 0 marks an empty slot.  Any pointer may be NULL. */
+int64_t pikv_slot_count(pikv_engine* eng);
+int pikv_read_slots_host(pikv_engine* eng, int32_t stream, uint64_t* id,
+                         uint64_t* shard_seq, int64_t* token, int32_t* expert,
+                         uint64_t* insert_step, uint64_t* last_access,
+                         uint64_t* freq, double* attn_mass, double* per_layer);
+/* Overwrite attn_mass (and optionally per_layer) of `stream`'s slots, to
+ * inject identical metadata for step-local parity of H2O/AdaKV/Duo. */
+int pikv_write_attn_mass_host(pikv_engine* eng, int32_t stream,
+                              const double* attn_mass, const double* per_layer);
+/* RouterState (router.hpp:41-56) and SchedulerState (scheduler.hpp:49-56). */
+int pikv_read_router_state_host(pikv_engine* eng, int32_t stream, double* load,
+                                uint64_t* usage, uint64_t* miss, double* bias,
+                                uint64_t* step, uint64_t* total_usage);
+int pikv_read_sched_state_host(pikv_engine* eng, int32_t stream, double* theta,
+                               double* running_hit, uint64_t* step);
+/* KVStore::live_entries / memory_bytes (kvstore.cpp:187-196) per stream,
+ * and the pool's allocated page count. */
+int pikv_store_stats_host(pikv_engine* eng, int32_t stream, uint64_t* live,
+                          uint64_t* memory_bytes, uint64_t* inserts,
+                          uint64_t* overwrites);
+int64_t pikv_pool_pages_in_use(pikv_engine* eng);
+/* Bytes of one stored entry (K + V payload + scales) and entries per page. */
+int64_t pikv_entry_bytes(pikv_engine* eng);
+/* Launch statistics: number of kernels this engine enqueued so far. */
+int64_t pikv_kernel_launches(pikv_engine* eng);
+/* Per-kernel timing of the last step on the engine stream (CUDA events). */
+int pikv_set_profiling(pikv_engine* eng, int32_t on);
+int pikv_read_profile_host(pikv_engine* eng, float* attend_ms, float* step_ms,
+                           int64_t* attended_total);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PIKV_B200_H */
