@@ -1,0 +1,393 @@
+# SPDX-License-Identifier: Apache-2.0
+"""Benchmark of the B200 PiKV decode step (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config c2|c1|c3|c4-int8|c4-int4|c4-lowrank]
+
+One step = Engine::step (pipeline.cpp:213-351) for every stream of the batch:
+route -> insert -> evict -> retrieve -> decode attention -> LSE merge ->
+alpha fold-back.  Default workload (N=1) is BASELINE.json configs[1]:
+16 experts top-2, 32K context, 32 heads x 128, bf16, batch 16, store
+prefilled synthetically to L tokens (untimed).  value = decode tokens/s of the
+whole job (B * K / device time, inputs resident in HBM); e2e = the same
+through pikv_step_host with pinned host buffers (H2D of q/k/v, D2H of y inside
+the timed region).  Under torchrun (N>1) the experts are sharded over the
+ranks (G = N logical devices, device g on rank g) and the per-step partial
+softmax states are merged with an NCCL all-gather.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (description, kwargs)
+    "c2": ("7B-scale MoE decode: E16 top-2, L=32768, 32 heads x 128, bf16, batch 16, 1 GPU",
+           dict(E=16, k=2, L=32768, H=32, hd=128, B=16, dtype="bf16", codec="Identity")),
+    "c1": ("CPU-reference config: E16 top-2, 4 shards, L=4096, 8 heads x 128, fp32, batch 1",
+           dict(E=16, k=2, L=4096, H=8, hd=128, B=1, dtype="f32", codec="Identity", G=4)),
+    "c3": ("128K context, E16 expert-sharded, retain 25%, 32x128 bf16, batch 16",
+           dict(E=16, k=2, L=131072, H=32, hd=128, B=16, dtype="bf16", codec="Identity",
+                retain=0.25)),
+    "c4-int8": ("compression: int8 KV, L=65536, 32x128, batch 32",
+                dict(E=16, k=2, L=65536, H=32, hd=128, B=32, dtype="bf16", codec="Int8")),
+    "c4-int4": ("compression: int4 KV, L=65536, 32x128, batch 32",
+                dict(E=16, k=2, L=65536, H=32, hd=128, B=32, dtype="bf16", codec="Int4")),
+    "c4-lowrank": ("compression: rank-32 per head, L=65536, 32x128, batch 32",
+                   dict(E=16, k=2, L=65536, H=32, hd=128, B=32, dtype="bf16", codec="LowRank",
+                        rank=32)),
+}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def make_config(w, world=1, rank=0, G=None):
+    from paper_2508_06526_b200.config import (CompressorConfig, EngineConfig, ModelConfig,
+                                              RouterConfig, SchedulerConfig, StoreConfig)
+    E, k, L, H, hd, B = w["E"], w["k"], w["L"], w["H"], w["hd"], w["B"]
+    d = H * hd
+    G = G or w.get("G", world)
+    retain = w.get("retain", 1.0)
+    ps = 16
+    c = EngineConfig()
+    per_expert = k * L // E
+    S = 1
+    while S < int(per_expert * 1.5):
+        S *= 2
+    c.model = ModelConfig(d=d, head_width=hd, E=E, k=k, L=L, G=G, S=S, K=4, rho=1.0,
+                          elem_bytes=2)
+    c.store = StoreConfig(n_tok=1, n_exp=E)          # pure expert partitioning
+    c.router = RouterConfig(strategy="TopK", k=k)
+    # LRU page budget per device: keep ~retain * k * L entries in steady state
+    budget = max(1, int(retain * k * L / ps / G))
+    c.scheduler = SchedulerConfig(strategy="LRU", budget_pages=budget, page_size=ps)
+    rank_r = w.get("rank", 8)
+    c.compressor = CompressorConfig(scheme=w["codec"], rank=rank_r)
+    c.n_heads = H
+    c.n_layers = 0
+    c.batch = B
+    c.kv_dtype = w["dtype"]
+    c.world_size = world
+    c.rank_id = rank
+    local_frac = 1.0 / world if world > 1 else 1.0
+    c.pool_entries = int(B * (k * L * local_frac * 1.15 + 4096))
+    c.seed = 1
+    return c
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + q,
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self._proc = None
+        return self
+
+    def _read(self):
+        for line in self._proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self._proc:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=2)
+            except Exception:
+                self._proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for n, v in zip(names, s[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.samples)}
+
+
+def cpu_reference(w, steps, threads=None, prefill=None):
+    """The reference's own objects (oracle/_ref) on this host's cores; streams
+    in parallel threads (streams are independent).  Falls back to
+    the C restatement (oracle/) when the reference objects are absent."""
+    import ctypes
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle import build as obuild
+    cfg = make_config(dict(w, H=1, hd=w["H"] * w["hd"]), world=1, rank=0, G=1)
+    cfg.batch = 1
+    cfg.kv_dtype = w["dtype"]
+    cfg.compressor.scheme = "Identity"
+    threads = threads or min(os.cpu_count() or 1, 16)
+    prefill = prefill if prefill is not None else w["L"]
+    path = obuild.ref_lib_path()
+    if os.path.exists(path):
+        from tests.oracle_bind import ref_lib
+        lib = ref_lib()
+        secs = np.zeros(threads)
+        att = ctypes.c_long(0)
+        c = cfg.to_c()
+        t = lib.ref_time_streams(ctypes.byref(c), threads, prefill, steps, 12345,
+                                 secs.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                 ctypes.byref(att))
+        kind = "reference"
+    else:  # oracle port, single thread
+        from tests.oracle_bind import OracleEngine, round_to
+        o = OracleEngine(cfg)
+        rng = np.random.default_rng(1)
+        d = cfg.model.d
+        for _ in range(prefill):
+            x = round_to(rng.standard_normal((3, d)), w["dtype"])
+            o.step(x[0], x[1], x[2], attend=False)
+        t0 = time.perf_counter()
+        n = 0
+        for _ in range(steps):
+            x = round_to(rng.standard_normal((3, d)), w["dtype"])
+            n += o.step(x[0], x[1], x[2])["n_attended"]
+        t = time.perf_counter() - t0
+        threads, kind = 1, "port"
+        att = type("A", (), {"value": n})
+    tokens = threads * steps
+    return {"value": tokens / t, "unit": "tokens/s", "cores": threads, "kind": kind,
+            "seconds": t, "attended": int(att.value),
+            "sample": "%d streams x %d steps after %d-token prefill (route+insert), E%d k%d, "
+                      "d=%d single head (the reference has no heads; same K/V bytes), "
+                      "%s-rounded inputs, fp64 compute" % (threads, steps, prefill, w["E"], w["k"],
+                                                          cfg.model.d, w["dtype"])}
+
+
+def run_reference_arm(args, w, name):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    steps = max(1, args.steps)
+    res = cpu_reference(w, steps=min(steps, 3), prefill=None)
+    line = {"impl": "reference", "metric": "decode tokens/sec", "value": res["value"],
+            "unit": "tokens/s", "n_gpus": args.gpus, "steps": min(steps, 3),
+            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": name, "description": w and WORKLOADS[name][0]},
+            "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": res["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--prefill", type=int, default=None, help="override prefill tokens")
+    args = ap.parse_args()
+    name = args.config
+    w = dict(WORKLOADS[name][1])
+    if args.prefill is not None:
+        w["L"] = args.prefill
+    if args.impl == "reference":
+        run_reference_arm(args, w, name)
+        return
+
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2508_06526_b200.engine import Engine
+    from paper_2508_06526_b200.parallel import ShardedStepper
+
+    cfg = make_config(w, world=world, rank=rank)
+    eng = Engine(cfg, device=local)
+    B, d, dp = cfg.batch, cfg.model.d, cfg.stored_width
+    if cfg.compressor.scheme in ("LowRank",):
+        hd, r = cfg.head_dim, cfg.compressor.rank
+        rng = np.random.default_rng(0)
+        basis = np.linalg.qr(rng.standard_normal((hd, hd)))[0][:, :r].T
+        eng.set_codec(np.ascontiguousarray(np.repeat(basis[None], cfg.n_heads, 0), np.float32))
+    stepper = ShardedStepper(eng) if world > 1 else None
+
+    t0 = time.time()
+    eng.prefill_synthetic(w["L"], seed=7)
+    prefill_s = time.time() - t0
+
+    tdt = torch.bfloat16 if cfg.kv_dtype == "bf16" else torch.float32
+    nbank = args.warmup + args.steps
+    bank = torch.empty(nbank, 3, B, d, dtype=tdt, device="cuda")
+    for i in range(nbank):
+        eng.fill_synthetic(bank[i, 0], bank[i, 1], bank[i, 2], seed=1000 + i)
+    q = torch.empty(B, d, dtype=tdt, device="cuda")
+    k = torch.empty_like(q)
+    v = torch.empty_like(q)
+    y = torch.empty(B, dp, dtype=torch.float32, device="cuda")
+    es = eng.external_stream()
+    torch.cuda.synchronize()
+
+    def one_step(i):
+        with torch.cuda.stream(es):
+            q.copy_(bank[i, 0], non_blocking=True)
+            k.copy_(bank[i, 1], non_blocking=True)
+            v.copy_(bank[i, 2], non_blocking=True)
+        if stepper is None:
+            eng.step(q, k, v, None, y)
+        else:
+            stepper.step(q, k, v, y)
+
+    for i in range(args.warmup):
+        one_step(i)
+    eng.sync()
+    launches0 = eng.kernel_launches()
+
+    # ---------------- timed region (device-resident inputs) ----------------
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(es)
+        for i in range(args.steps):
+            one_step(args.warmup + i)
+        ev1.record(es)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = eng.kernel_launches() - launches0
+    t_ms = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+    ms = float(t_ms.item())
+    _, _, _, summ = eng.read_step()
+    att_last = sum(s["n_attended"] for s in summ)
+
+    # ---------------- attention kernel timing (events on the engine stream) ----
+    eng.set_profiling(True)
+    att_total = 0
+    nprof = min(args.steps, 20)
+    for i in range(nprof):
+        one_step(args.warmup + (i % args.steps))
+        _, _, _, sm = eng.read_step()
+        att_total += sum(s["n_attended"] for s in sm)
+    attend_ms, n_launch = eng.read_profile()
+    eng.set_profiling(False)
+    entry_bytes = eng.entry_bytes()
+    # local attended entries on this rank (global n_attended is summed over ranks)
+    alg_bytes = att_total * entry_bytes / max(world, 1)
+    attend_avg_ms = attend_ms / max(n_launch, 1)
+    peak, peak_kind = load_peaks()
+    achieved = alg_bytes / max(n_launch, 1) / (attend_avg_ms * 1e-3) / 1e9 if attend_avg_ms else 0.0
+
+    # ---------------- end to end through host buffers ----------------
+    e2e = None
+    if world == 1:
+        elem = 2 if cfg.kv_dtype == "bf16" else 4
+        npdt = np.uint16 if elem == 2 else np.float32
+        hq = torch.empty(args.steps, 3, B, d, dtype=tdt).pin_memory()
+        hq.copy_(bank[args.warmup:].cpu())
+        hy = torch.empty(B, dp, dtype=torch.float32).pin_memory()
+        hq_np = hq.view(torch.int16 if elem == 2 else torch.float32).numpy()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(es)
+        from paper_2508_06526_b200 import _capi
+        L = _capi.lib()
+        for i in range(args.steps):
+            _capi.check(L.pikv_step_host(eng.h, hq_np[i, 0].ctypes.data, hq_np[i, 1].ctypes.data,
+                                         hq_np[i, 2].ctypes.data, None, hy.data_ptr()))
+        e1.record(es)
+        torch.cuda.synchronize()
+        e2e_ms = e0.elapsed_time(e1)
+        e2e = {"value": B * args.steps / (e2e_ms * 1e-3), "unit": "tokens/s",
+               "h2d_bytes_per_step": 3 * B * d * elem, "d2h_bytes_per_step": B * dp * 4,
+               "ms_per_step": e2e_ms / args.steps}
+        del npdt
+
+    tokens = B * args.steps
+    kv_bytes_step = att_last * entry_bytes  # last step's attended KV (global)
+    line = {
+        "metric": "decode tokens/sec", "value": tokens / (ms * 1e-3), "unit": "tokens/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "bf16"
+        if cfg.kv_dtype == "bf16" else "f32",
+        "data": "synthetic (device-generated N(0,1) q/k/v; store prefilled to L)",
+        "config": {"workload": name, "description": WORKLOADS[name][0], "batch": B,
+                   "context": w["L"], "experts": w["E"], "top_k": w["k"], "heads": w["H"],
+                   "head_dim": w["hd"], "codec": w["codec"], "scheduler": "LRU page budget",
+                   "placement": "expert-sharded over %d GPU(s)" % world,
+                   "l2": "inputs larger than L2 (2 GiB KV read per step)",
+                   "prefill_s": round(prefill_s, 2)},
+        "kv_gbs": kv_bytes_step / (ms / args.steps * 1e-3) / 1e9,
+        "kv_frac_of_hbm": kv_bytes_step / (ms / args.steps * 1e-3) / 1e9 / (peak * world),
+        "attended_per_step": att_last,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": "k_attend (decode attention, TMA bulk ring)",
+                     "peak_kind": peak_kind, "avg_launch_ms": attend_avg_ms,
+                     "algorithmic_bytes_per_launch": alg_bytes / max(n_launch, 1)},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "e2e": e2e,
+    }
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        try:
+            res = cpu_reference(w, steps=2)
+            line["cpu_baseline"] = {k2: res[k2] for k2 in ("value", "unit", "cores", "kind",
+                                                           "sample")}
+        except Exception as ex:  # pragma: no cover
+            line["cpu_baseline"] = {"value": None, "error": str(ex)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

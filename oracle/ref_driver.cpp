@@ -443,3 +443,9 @@ double ref_time_streams(const pikv_config* cfg, int threads, long prefill, int s
 }
 
 }  // extern "C"
+
+extern "C" void ref_normal_vector(std::uint64_t seed, std::int64_t n, double scale, double* out) {
+    Rng rng(seed);  // rng.hpp:54-58
+    auto v = rng.normal_vector(static_cast<std::size_t>(n), scale);
+    for (std::int64_t i = 0; i < n; ++i) out[i] = v[i];
+}

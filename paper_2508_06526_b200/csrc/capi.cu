@@ -1,0 +1,959 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// C-ABI of the B200 PiKV engine (include/pikv_b200.h): engine lifetime,
+// HBM allocation, the per-step launch sequence (captured once into a CUDA
+// graph and replayed), result readback and the pure-function entry points.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <random>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "pikv_dev.cuh"
+
+using namespace pikv_dev;
+
+namespace pikv_dev {
+__global__ void k_shard_assign(const int64_t*, const int32_t*, int32_t, int32_t, int32_t, int32_t,
+                               int32_t, int32_t*, int32_t*, int32_t*);
+__global__ void k_select(const double*, const uint64_t*, int32_t, int32_t, int32_t, double,
+                         int32_t*, int32_t*, int32_t*);
+__global__ void k_attention(const float*, const float*, const float*, int32_t, int32_t, float*,
+                            float*);
+__global__ void k_quantize(const void*, int32_t, int32_t, int32_t, int32_t, uint8_t*, float*);
+__global__ void k_dequantize(const uint8_t*, const float*, int32_t, int32_t, int32_t, float*);
+__global__ void k_lr_encode(const float*, const float*, const float*, int32_t, int32_t, int32_t,
+                            int32_t, float*);
+__global__ void k_lr_decode(const float*, const float*, const float*, int32_t, int32_t, int32_t,
+                            int32_t, float*);
+const char* attend_check(const Dims& D);
+}  // namespace pikv_dev
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CUDA_TRY(x)                                                                   \
+    do {                                                                              \
+        cudaError_t e_ = (x);                                                         \
+        if (e_ != cudaSuccess)                                                        \
+            return fail(PIKV_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+bool is_pow2(int n) { return n >= 1 && (n & (n - 1)) == 0; }
+
+constexpr uint64_t kRouterSalt = 0x2545f4914f6cdd1dULL;  // pipeline.cpp:16
+
+// RouterState::init (router.cpp:54-67): W_r = Rng(seed).normal_vector(E*d,
+// 1/sqrt(d)), with pikv::Rng's transforms over std::mt19937_64 (rng.hpp).
+std::vector<double> router_matrix(int E, int d, uint64_t seed) {
+    std::mt19937_64 gen(seed);
+    auto uniform = [&]() { return static_cast<double>(gen() >> 11) * 0x1.0p-53; };
+    bool has_spare = false;
+    double spare = 0.0;
+    auto normal = [&]() {
+        if (has_spare) {
+            has_spare = false;
+            return spare;
+        }
+        double u1 = uniform();
+        double u2 = uniform();
+        while (u1 <= 0.0) u1 = uniform();
+        double radius = std::sqrt(-2.0 * std::log(u1));
+        double angle = 2.0 * M_PI * u2;
+        spare = radius * std::sin(angle);
+        has_spare = true;
+        return radius * std::cos(angle);
+    };
+    const double scale = 1.0 / std::sqrt(static_cast<double>(d));
+    std::vector<double> w(static_cast<size_t>(E) * d);
+    for (auto& x : w) x = scale * normal();
+    return w;
+}
+
+}  // namespace
+
+struct pikv_engine {
+    pikv_config cfg{};
+    Dims D{};
+    Cfg C{};
+    State S{};
+    ExchangeLayout X{};
+    cudaStream_t stream = nullptr;
+    int device = 0;
+    std::vector<void*> allocs;
+    // staging for host-buffer steps and synthetic prefill
+    void* in_q = nullptr;
+    void* in_k = nullptr;
+    void* in_v = nullptr;
+    double* in_sal = nullptr;
+    float* out_y = nullptr;
+    // graph cache keyed by (q, k, v, saliency, y, attend)
+    std::map<std::tuple<const void*, const void*, const void*, const void*, void*, int>,
+             cudaGraphExec_t>
+        graphs;
+    bool warmed = false;
+    int64_t launches = 0;
+    int kernels_per_step = 0;
+    // profiling
+    bool profiling = false;
+    std::vector<cudaEvent_t> ev;
+    int ev_used = 0;
+    cudaEvent_t step_ev[2]{};
+    int step_count_prof = 0;
+
+    template <class T>
+    T* alloc(size_t n) {
+        void* p = nullptr;
+        if (n == 0) n = 1;
+        if (cudaMalloc(&p, n * sizeof(T)) != cudaSuccess) return nullptr;
+        allocs.push_back(p);
+        return static_cast<T*>(p);
+    }
+};
+
+extern "C" {
+
+const char* pikv_version(void) { return "pikv-b200 0.1 (sm_100a)"; }
+const char* pikv_last_error(void) { return g_err.c_str(); }
+int pikv_config_size(void) { return (int)sizeof(pikv_config); }
+
+void pikv_config_default(pikv_config* c) {
+    std::memset(c, 0, sizeof(*c));
+    c->d = 64, c->head_width = 16, c->E = 8, c->k = 2, c->L = 1024, c->G = 2, c->S = 16;
+    c->K = 4, c->elem_bytes = 2, c->rho = 1.0, c->n_heads = 1;
+    c->n_tok = 64, c->n_exp = 64, c->additive = 0, c->shards_per_device = 0;
+    c->router_strategy = PIKV_ROUTER_TOPK, c->groups = 1, c->stride = 1;
+    c->alpha = 1.0, c->lambda_miss = 1.0, c->beta_ent = 1.0, c->bandit_step = 0.05;
+    c->bias_cap = 5.0, c->load_decay = 0.99;
+    c->sched_strategy = PIKV_SCHED_LRU, c->budget_pages = 4, c->page_size = 16, c->sink = 4;
+    c->flex_bucket = 16, c->n_adakv_weights = 3, c->n_flex_plan = 1;
+    c->tau = 64.0, c->lambda_freq = 0.5, c->adakv_step = 0.05, c->target_hit = 0.9;
+    c->gamma_sim = 0.5, c->theta0 = -1e18, c->hit_decay = 0.9;
+    c->adakv_weights[0] = 1.0, c->adakv_weights[1] = 0.5, c->adakv_weights[2] = 0.25;
+    c->flex_plan[0] = 1.0;
+    c->codec = PIKV_CODEC_IDENTITY, c->rank = 8;
+    c->batch = 1, c->kv_dtype = PIKV_DTYPE_F32, c->world_size = 1, c->rank_id = 0;
+    c->seed = 1;
+}
+
+// ---------------------------------------------------------------------------
+// pure functions
+// ---------------------------------------------------------------------------
+int pikv_shard_assign(const int64_t* t, const int32_t* e, int32_t n, int32_t n_tok, int32_t n_exp,
+                      int32_t devices, int32_t additive, int32_t* device_out, int32_t* shard_out,
+                      int32_t* raw_out) {
+    if (!is_pow2(n_tok) || !is_pow2(n_exp))  // kvstore.cpp:17-19
+        return fail(PIKV_ERR_INVALID_CONFIG, "shard_assign: moduli must be powers of two");
+    if (devices < 1) return fail(PIKV_ERR_INVALID_CONFIG, "shard_assign: devices must be >= 1");
+    if (n <= 0) return PIKV_OK;
+    // negative inputs (kvstore.cpp:20-22) are checked on the device copy
+    std::vector<int64_t> ht(n);
+    std::vector<int32_t> he(n);
+    CUDA_TRY(cudaMemcpy(ht.data(), t, sizeof(int64_t) * n, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(he.data(), e, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < n; ++i)
+        if (ht[i] < 0 || he[i] < 0)
+            return fail(PIKV_ERR_INVALID_ARGUMENT, "shard_assign: negative token or expert index");
+    k_shard_assign<<<(n + 255) / 256, 256>>>(t, e, n, n_tok, n_exp, devices, additive, device_out,
+                                             shard_out, raw_out);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaDeviceSynchronize());
+    return PIKV_OK;
+}
+
+int pikv_select_evictions(const double* aggregate, const uint64_t* oldest_id, int32_t n,
+                          int32_t budget_pages, int32_t use_theta, double theta, int32_t* idx_out,
+                          int32_t* reason_out, int32_t* n_out) {
+    if (budget_pages < 1) return fail(PIKV_ERR_INVALID_CONFIG, "budget_pages must be >= 1");
+    k_select<<<1, 1024>>>(aggregate, oldest_id, n, budget_pages, use_theta, theta, idx_out,
+                          reason_out, n_out);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaDeviceSynchronize());
+    return PIKV_OK;
+}
+
+int pikv_attention(const float* q, const float* keys, const float* values, int32_t n_queries,
+                   int32_t n, int32_t w, float* y_out, float* weights_out) {
+    if (w < 1) return fail(PIKV_ERR_INVALID_ARGUMENT, "attention: width must be >= 1");
+    if (n == 0) {  // pipeline.cpp:63-66: zero vector, no weights
+        CUDA_TRY(cudaMemset(y_out, 0, sizeof(float) * (size_t)n_queries * w));
+        return PIKV_OK;
+    }
+    size_t smem = sizeof(float) * (size_t)n;
+    if (smem > 200 * 1024) return fail(PIKV_ERR_INVALID_ARGUMENT, "attention: n too large");
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(k_attention, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_attention<<<n_queries, 256, smem>>>(q, keys, values, n, w, y_out, weights_out);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaDeviceSynchronize());
+    return PIKV_OK;
+}
+
+int pikv_quantize(const void* x, int32_t dtype, int32_t rows, int32_t width, int32_t bits,
+                  uint8_t* codes_out, float* scales_out) {
+    if (bits != 8 && bits != 4) return fail(PIKV_ERR_INVALID_ARGUMENT, "bits must be 8 or 4");
+    if (bits == 4 && width % 2) return fail(PIKV_ERR_INVALID_ARGUMENT, "int4 width must be even");
+    k_quantize<<<(rows + 7) / 8, 256>>>(x, dtype, rows, width, bits, codes_out, scales_out);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaDeviceSynchronize());
+    return PIKV_OK;
+}
+
+int pikv_dequantize(const uint8_t* codes, const float* scales, int32_t rows, int32_t width,
+                    int32_t bits, float* x_out) {
+    if (bits != 8 && bits != 4) return fail(PIKV_ERR_INVALID_ARGUMENT, "bits must be 8 or 4");
+    const int64_t n = (int64_t)rows * width;
+    k_dequantize<<<(unsigned)((n + 255) / 256), 256>>>(codes, scales, rows, width, bits, x_out);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaDeviceSynchronize());
+    return PIKV_OK;
+}
+
+int pikv_lowrank_encode(const float* x, const float* basis, const float* bias, int32_t rows,
+                        int32_t heads, int32_t hd, int32_t r, float* y_out) {
+    const int64_t n = (int64_t)rows * heads * r;
+    k_lr_encode<<<(unsigned)((n + 255) / 256), 256>>>(x, basis, bias, rows, heads, hd, r, y_out);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaDeviceSynchronize());
+    return PIKV_OK;
+}
+
+int pikv_lowrank_decode(const float* y, const float* basis, const float* bias, int32_t rows,
+                        int32_t heads, int32_t hd, int32_t r, float* x_out) {
+    const int64_t n = (int64_t)rows * heads * hd;
+    k_lr_decode<<<(unsigned)((n + 255) / 256), 256>>>(y, basis, bias, rows, heads, hd, r, x_out);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaDeviceSynchronize());
+    return PIKV_OK;
+}
+
+// ---------------------------------------------------------------------------
+// engine
+// ---------------------------------------------------------------------------
+static int validate(const pikv_config& c) {
+    // ModelConfig::validate, config.hpp:42-54
+    if (c.d < 1) return fail(PIKV_ERR_INVALID_CONFIG, "ModelConfig: d must be >= 1");
+    if (c.head_width < 1 || c.head_width > c.d)
+        return fail(PIKV_ERR_INVALID_CONFIG, "ModelConfig: head_width must be in [1, d]");
+    if (c.E < 1) return fail(PIKV_ERR_INVALID_CONFIG, "ModelConfig: E must be >= 1");
+    if (c.k < 1 || c.k > c.E) return fail(PIKV_ERR_INVALID_CONFIG, "ModelConfig: need 1 <= k <= E");
+    if (c.L < 1 || c.G < 1 || c.S < 1 || c.K < 1)
+        return fail(PIKV_ERR_INVALID_CONFIG, "ModelConfig: L, G, S, K must be >= 1");
+    if (!(c.rho >= 1.0)) return fail(PIKV_ERR_INVALID_CONFIG, "ModelConfig: rho must be >= 1");
+    if (c.elem_bytes < 1) return fail(PIKV_ERR_INVALID_CONFIG, "ModelConfig: elem_bytes must be >= 1");
+    // StoreConfig::validate, kvstore.cpp:56-64
+    if (!is_pow2(c.n_tok) || !is_pow2(c.n_exp))
+        return fail(PIKV_ERR_INVALID_CONFIG, "StoreConfig: n_tok and n_exp must be powers of two");
+    if (c.shards_per_device < 0)
+        return fail(PIKV_ERR_INVALID_CONFIG, "StoreConfig: shards_per_device must be >= 0");
+    // RouterConfig::validate, router.cpp:40-53
+    if (c.alpha < 0 || c.lambda_miss < 0 || c.beta_ent < 0 || c.bandit_step < 0)
+        return fail(PIKV_ERR_INVALID_CONFIG, "RouterConfig: coefficients must be >= 0");
+    if (c.groups < 1 || c.groups > c.E)
+        return fail(PIKV_ERR_INVALID_CONFIG, "RouterConfig: need 1 <= groups <= E");
+    if (c.load_decay < 0 || c.load_decay >= 1.0)
+        return fail(PIKV_ERR_INVALID_CONFIG, "RouterConfig: load_decay must be in [0, 1)");
+    // SchedulerConfig::validate, scheduler.cpp:49-71
+    if (c.budget_pages < 1) return fail(PIKV_ERR_INVALID_CONFIG, "SchedulerConfig: budget_pages must be >= 1");
+    if (c.page_size < 1) return fail(PIKV_ERR_INVALID_CONFIG, "SchedulerConfig: page_size must be >= 1");
+    if (c.lambda_freq < 0 || c.adakv_step < 0 || c.gamma_sim < 0)
+        return fail(PIKV_ERR_INVALID_CONFIG, "SchedulerConfig: coefficients must be >= 0");
+    if (c.target_hit < 0.0 || c.target_hit > 1.0)
+        return fail(PIKV_ERR_INVALID_CONFIG, "SchedulerConfig: target_hit must be in [0, 1]");
+    if (c.hit_decay < 0.0 || c.hit_decay >= 1.0)
+        return fail(PIKV_ERR_INVALID_CONFIG, "SchedulerConfig: hit_decay must be in [0, 1)");
+    if (c.n_flex_plan < 1 || c.n_flex_plan > 32 || c.flex_bucket < 1)
+        return fail(PIKV_ERR_INVALID_CONFIG, "SchedulerConfig: flex plan needs >= 1 bucket");
+    if (c.sink < 0 || c.tau < 0) return fail(PIKV_ERR_INVALID_CONFIG, "SchedulerConfig: sink and tau must be >= 0");
+    if (c.n_adakv_weights < 0 || c.n_adakv_weights > 8)
+        return fail(PIKV_ERR_INVALID_CONFIG, "SchedulerConfig: <= 8 adakv weights");
+    if (c.sched_strategy == PIKV_SCHED_QUEST)  // scheduler.cpp:199-203 (fit needs Eigen; out of scope)
+        return fail(PIKV_ERR_NOT_FITTED, "score: QUEST scorer not fitted");
+    if (c.sched_strategy < 0 || c.sched_strategy > PIKV_SCHED_DUO || c.router_strategy < 0 ||
+        c.router_strategy > PIKV_ROUTER_HIERARCHICAL)
+        return fail(PIKV_ERR_INVALID_CONFIG, "unknown strategy");
+    // engine limits
+    if (c.E > kMaxE) return fail(PIKV_ERR_INVALID_CONFIG, "E must be <= 256");
+    if (c.k > kMaxK) return fail(PIKV_ERR_INVALID_CONFIG, "k must be <= 64");
+    if (c.n_heads < 1 || c.d % c.n_heads)
+        return fail(PIKV_ERR_INVALID_CONFIG, "n_heads must divide d");
+    if (c.batch < 1 || c.batch > 1024) return fail(PIKV_ERR_INVALID_CONFIG, "batch must be in [1, 1024]");
+    if (c.world_size < 1 || c.rank_id < 0 || c.rank_id >= c.world_size)
+        return fail(PIKV_ERR_INVALID_CONFIG, "bad world_size / rank_id");
+    if (c.codec < PIKV_CODEC_IDENTITY || c.codec > PIKV_CODEC_INT4)
+        return fail(PIKV_ERR_INVALID_CONFIG, "unknown codec");
+    if (c.kv_dtype != PIKV_DTYPE_F32 && c.kv_dtype != PIKV_DTYPE_BF16)
+        return fail(PIKV_ERR_INVALID_CONFIG, "kv_dtype must be f32 or bf16");
+    const int hd = c.d / c.n_heads;
+    if ((c.codec >= PIKV_CODEC_LOWRANK && c.codec <= PIKV_CODEC_PRUNE) && (c.rank < 1 || c.rank > hd))
+        return fail(PIKV_ERR_INVALID_CONFIG, "codec rank must be in [1, head_dim]");
+    if (c.n_layers < 0) return fail(PIKV_ERR_INVALID_CONFIG, "n_layers must be >= 0");
+    return PIKV_OK;
+}
+
+int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine** out) {
+    *out = nullptr;
+    int rc = validate(*cfg);
+    if (rc) return rc;
+    CUDA_TRY(cudaSetDevice(cuda_device));
+    auto* eng = new pikv_engine();
+    eng->cfg = *cfg;
+    eng->device = cuda_device;
+    const pikv_config& c = *cfg;
+    Dims& D = eng->D;
+    D.B = c.batch;
+    D.G = c.G;
+    D.world = c.world_size;
+    D.rank = c.rank_id;
+    D.Gl = 0;
+    for (int g = 0; g < c.G; ++g) D.Gl += (g % c.world_size) == c.rank_id;
+    // KVStore ctor, kvstore.cpp:82-100
+    int spd = c.shards_per_device > 0 ? c.shards_per_device : std::max(c.n_tok, c.n_exp) / c.G;
+    if (spd < 1) spd = 1;
+    const int raw_span = c.additive ? c.n_tok + c.n_exp - 1 : std::max(c.n_tok, c.n_exp);
+    const int needed = (raw_span + c.G - 1) / c.G;
+    D.SPD = std::max(spd, needed);
+    D.R = std::max(D.Gl, 1) * D.SPD;
+    D.S = c.S;
+    D.H = c.n_heads;
+    D.d = c.d;
+    D.E = c.E;
+    D.k = c.k;
+    D.n_layers = c.n_layers;
+    D.codec = c.codec;
+    D.kv_dtype = c.kv_dtype;
+    const int hd = c.d / c.n_heads;
+    const bool proj = c.codec >= PIKV_CODEC_LOWRANK && c.codec <= PIKV_CODEC_PRUNE;
+    D.dph = proj ? c.rank : hd;
+    D.dp = D.dph * D.H;
+    const bool quant = c.codec == PIKV_CODEC_INT8 || c.codec == PIKV_CODEC_INT4;
+    if (c.codec == PIKV_CODEC_INT8) D.payload_bytes = D.dp, D.elem_bits = 8;
+    else if (c.codec == PIKV_CODEC_INT4) D.payload_bytes = D.dp / 2, D.elem_bits = 4;
+    else D.payload_bytes = D.dp * (c.kv_dtype == PIKV_DTYPE_BF16 ? 2 : 4),
+         D.elem_bits = c.kv_dtype == PIKV_DTYPE_BF16 ? 16 : 32;
+    D.entry_bytes = 2 * D.payload_bytes + (quant ? 8 * D.H : 0);
+    D.entry_bytes = (D.entry_bytes + 15) & ~15;
+    D.n_tok = c.n_tok;
+    D.n_exp = c.n_exp;
+    D.additive = c.additive;
+    D.page_size = c.page_size;
+    D.ppr_sched = (c.S - 1) / c.page_size + 2;
+    if (c.S % c.page_size == 0 && c.page_size <= 256) {
+        D.spg = c.page_size;
+    } else {
+        D.spg = 1;
+        while (D.spg < 16 && c.S % (D.spg * 2) == 0) D.spg *= 2;
+    }
+    D.ppr = c.S / D.spg;
+    int sel = 1;
+    while (sel < D.SPD * D.ppr_sched) sel <<= 1;
+    D.sel_stride = sel;
+    D.max_cand = std::min<int64_t>(D.R, (int64_t)c.k * c.n_tok);
+    D.chunk_slots = std::min(1024, ((c.S + 31) / 32) * 32);
+    D.nch = (c.S + D.chunk_slots - 1) / D.chunk_slots;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device);
+    D.attend_ctas = sms;
+    D.item_cap = 4LL * D.attend_ctas + D.B + 16;
+    const int64_t total_slots = (int64_t)D.B * D.R * D.S;
+    if (total_slots >= (1LL << 31)) {
+        delete eng;
+        return fail(PIKV_ERR_INVALID_CONFIG, "B * rings * S must be < 2^31 slots");
+    }
+    int64_t pool_entries = c.pool_entries > 0 ? c.pool_entries : total_slots;
+    {
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        const int64_t cap = (int64_t)((double)fr * 0.6 / D.entry_bytes);
+        if (c.pool_entries <= 0 && pool_entries > cap) pool_entries = cap;
+    }
+    D.pool_pages = (pool_entries + D.spg - 1) / D.spg;
+    D.pool_entries = D.pool_pages * D.spg;
+    D.att_cap = std::min<int64_t>(D.pool_entries, total_slots) + 1;
+    if (const char* msg = attend_check(D)) {
+        delete eng;
+        return fail(PIKV_ERR_INVALID_CONFIG, std::string("attention layout: ") + msg);
+    }
+    // scalar config
+    Cfg& C = eng->C;
+    C.router_strategy = c.router_strategy, C.groups = c.groups, C.stride = c.stride;
+    C.alpha = c.alpha, C.lambda_miss = c.lambda_miss, C.beta_ent = c.beta_ent;
+    C.bandit_step = c.bandit_step, C.bias_cap = c.bias_cap, C.load_decay = c.load_decay;
+    C.sched_strategy = c.sched_strategy, C.budget_pages = c.budget_pages;
+    C.page_size = c.page_size, C.sink = c.sink, C.flex_bucket = c.flex_bucket;
+    C.n_adakv_weights = c.n_adakv_weights, C.n_flex_plan = c.n_flex_plan;
+    C.tau = c.tau, C.lambda_freq = c.lambda_freq, C.adakv_step = c.adakv_step;
+    C.target_hit = c.target_hit, C.theta0 = c.theta0, C.hit_decay = c.hit_decay;
+    std::memcpy(C.adakv_weights, c.adakv_weights, sizeof(C.adakv_weights));
+    std::memcpy(C.flex_plan, c.flex_plan, sizeof(C.flex_plan));
+    C.unbounded_budget = c.unbounded_budget, C.head_width = c.head_width;
+
+    // exchange record layout
+    ExchangeLayout& X = eng->X;
+    X.o_off = 0;
+    X.m_off = X.o_off + 4LL * D.H * D.dph;
+    X.l_off = X.m_off + 4LL * D.H;
+    X.found_off = X.l_off + 4LL * D.H;
+    X.stats_off = X.found_off + 4LL * D.k;
+    X.bytes_per_stream = ((X.stats_off + 16 + 15) / 16) * 16;
+
+    cudaStreamCreateWithFlags(&eng->stream, cudaStreamNonBlocking);
+    State& S = eng->S;
+    const int B = D.B, E = D.E, k = D.k;
+    const int64_t rings = (int64_t)B * D.R;
+    bool ok = true;
+    auto chk = [&](void* p) { ok = ok && p != nullptr; };
+    double* W = eng->alloc<double>((size_t)E * D.d);
+    chk(W);
+    S.W = W;
+    chk(S.load = eng->alloc<double>((size_t)B * E));
+    chk(S.usage = eng->alloc<uint64_t>((size_t)B * E));
+    chk(S.total_usage = eng->alloc<uint64_t>(B));
+    chk(S.miss = eng->alloc<uint64_t>((size_t)B * E));
+    chk(S.bias = eng->alloc<double>((size_t)B * E));
+    chk(S.rstep = eng->alloc<uint64_t>(B));
+    chk(S.theta = eng->alloc<double>(B));
+    chk(S.running_hit = eng->alloc<double>(B));
+    chk(S.sstep = eng->alloc<uint64_t>(B));
+    chk(S.now = eng->alloc<uint64_t>(B));
+    chk(S.next_id = eng->alloc<uint64_t>(B));
+    chk(S.err = eng->alloc<int32_t>(B));
+    chk(S.st_inserts = eng->alloc<uint64_t>(B));
+    chk(S.st_overwrites = eng->alloc<uint64_t>(B));
+    chk(S.head = eng->alloc<int32_t>(rings));
+    chk(S.live = eng->alloc<int32_t>(rings));
+    chk(S.seq = eng->alloc<uint64_t>(rings));
+    chk(S.page_table = eng->alloc<int32_t>(rings * D.ppr));
+    chk(S.id = eng->alloc<uint64_t>(total_slots));
+    chk(S.shard_seq = eng->alloc<uint64_t>(total_slots));
+    chk(S.token = eng->alloc<int64_t>(total_slots));
+    chk(S.expert = eng->alloc<int32_t>(total_slots));
+    chk(S.insert_step = eng->alloc<uint64_t>(total_slots));
+    chk(S.last_access = eng->alloc<uint64_t>(total_slots));
+    chk(S.freq = eng->alloc<uint64_t>(total_slots));
+    chk(S.attn_mass = eng->alloc<double>(total_slots));
+    chk(S.per_layer = eng->alloc<double>((size_t)total_slots * std::max(D.n_layers, 1)));
+    chk(S.pool = eng->alloc<uint8_t>((size_t)D.pool_entries * D.entry_bytes));
+    chk(S.page_live = eng->alloc<int32_t>(D.pool_pages));
+    chk(S.free_stack = eng->alloc<int32_t>(D.pool_pages));
+    chk(S.free_top = eng->alloc<int32_t>(1));
+    chk(S.experts = eng->alloc<int32_t>((size_t)B * k));
+    chk(S.gates = eng->alloc<double>((size_t)B * k));
+    chk(S.logits = eng->alloc<double>((size_t)B * E));
+    chk(S.q_attn = eng->alloc<float>((size_t)B * D.dp));
+    chk(S.cand = eng->alloc<int32_t>((size_t)B * D.max_cand));
+    chk(S.ncand = eng->alloc<int32_t>(B));
+    chk(S.rec_ow = eng->alloc<EvictRec>((size_t)B * k));
+    chk(S.n_ow = eng->alloc<int32_t>(B));
+    chk(S.rec_ev = eng->alloc<EvictRec>((size_t)B * std::max(D.Gl, 1) * D.SPD * D.S));
+    chk(S.n_ev = eng->alloc<int32_t>((size_t)B * std::max(D.Gl, 1)));
+    chk(S.pages_before = eng->alloc<int32_t>((size_t)B * std::max(D.Gl, 1)));
+    chk(S.pages_after = eng->alloc<int32_t>((size_t)B * std::max(D.Gl, 1)));
+    chk(S.pg_agg = eng->alloc<double>(rings * D.ppr_sched));
+    chk(S.pg_oldest = eng->alloc<uint64_t>(rings * D.ppr_sched));
+    chk(S.pg_cnt = eng->alloc<int32_t>(rings * D.ppr_sched));
+    chk(S.sel_idx = eng->alloc<int32_t>((size_t)B * std::max(D.Gl, 1) * D.sel_stride));
+    const size_t nchunk = (size_t)B * D.max_cand * D.nch;
+    chk(S.chunk_cnt = eng->alloc<int32_t>(nchunk));
+    chk(S.chunk_off = eng->alloc<int32_t>(nchunk));
+    chk(S.found = eng->alloc<int32_t>((size_t)B * k));
+    chk(S.att_base = eng->alloc<int64_t>(B + 1));
+    chk(S.att_slot = eng->alloc<int32_t>(D.att_cap));
+    chk(S.att_entry = eng->alloc<int32_t>(D.att_cap));
+    chk(S.scores = eng->alloc<float>((size_t)D.att_cap * D.H));
+    chk(S.item_stream = eng->alloc<int32_t>(D.item_cap));
+    chk(S.item_begin = eng->alloc<int32_t>(D.item_cap));
+    chk(S.item_end = eng->alloc<int32_t>(D.item_cap));
+    chk(S.n_items = eng->alloc<int32_t>(1));
+    chk(S.part_m = eng->alloc<float>((size_t)D.item_cap * D.H));
+    chk(S.part_l = eng->alloc<float>((size_t)D.item_cap * D.H));
+    chk(S.part_o = eng->alloc<float>((size_t)D.item_cap * D.H * D.dph));
+    chk(S.exchange = eng->alloc<uint8_t>((size_t)B * X.bytes_per_stream));
+    chk(S.gM = eng->alloc<float>((size_t)B * D.H));
+    chk(S.gL = eng->alloc<float>((size_t)B * D.H));
+    chk(S.summary = eng->alloc<pikv_step_summary>(B));
+    const size_t in_elem = c.kv_dtype == PIKV_DTYPE_BF16 ? 2 : 4;
+    chk(eng->in_q = eng->alloc<uint8_t>((size_t)B * D.d * in_elem));
+    chk(eng->in_k = eng->alloc<uint8_t>((size_t)B * D.d * in_elem));
+    chk(eng->in_v = eng->alloc<uint8_t>((size_t)B * D.d * in_elem));
+    chk(eng->in_sal = eng->alloc<double>((size_t)B * std::max(D.n_layers, 1)));
+    chk(eng->out_y = eng->alloc<float>((size_t)B * D.dp));
+    if (!ok) {
+        pikv_engine_destroy(eng);
+        return fail(PIKV_ERR_OUT_OF_MEMORY, "cudaMalloc failed (reduce pool_entries / batch / S)");
+    }
+    // initial state
+    cudaStream_t st = eng->stream;
+    auto w = router_matrix(E, D.d, c.seed ^ kRouterSalt);
+    CUDA_TRY(cudaMemcpyAsync(W, w.data(), sizeof(double) * w.size(), cudaMemcpyHostToDevice, st));
+    std::vector<double> theta(B, c.theta0);  // SchedulerState::init, scheduler.cpp:73-80
+    CUDA_TRY(cudaMemcpyAsync(S.theta, theta.data(), sizeof(double) * B, cudaMemcpyHostToDevice, st));
+    std::vector<uint64_t> ones(B, 1);  // kvstore.hpp:157 next_id_ = 1
+    CUDA_TRY(cudaMemcpyAsync(S.next_id, ones.data(), sizeof(uint64_t) * B, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemsetAsync(S.load, 0, sizeof(double) * B * E, st));
+    CUDA_TRY(cudaMemsetAsync(S.usage, 0, sizeof(uint64_t) * B * E, st));
+    CUDA_TRY(cudaMemsetAsync(S.total_usage, 0, sizeof(uint64_t) * B, st));
+    CUDA_TRY(cudaMemsetAsync(S.miss, 0, sizeof(uint64_t) * B * E, st));
+    CUDA_TRY(cudaMemsetAsync(S.bias, 0, sizeof(double) * B * E, st));
+    CUDA_TRY(cudaMemsetAsync(S.rstep, 0, sizeof(uint64_t) * B, st));
+    CUDA_TRY(cudaMemsetAsync(S.running_hit, 0, sizeof(double) * B, st));
+    CUDA_TRY(cudaMemsetAsync(S.sstep, 0, sizeof(uint64_t) * B, st));
+    CUDA_TRY(cudaMemsetAsync(S.now, 0, sizeof(uint64_t) * B, st));
+    CUDA_TRY(cudaMemsetAsync(S.err, 0, sizeof(int32_t) * B, st));
+    CUDA_TRY(cudaMemsetAsync(S.st_inserts, 0, sizeof(uint64_t) * B, st));
+    CUDA_TRY(cudaMemsetAsync(S.st_overwrites, 0, sizeof(uint64_t) * B, st));
+    CUDA_TRY(cudaMemsetAsync(S.head, 0, sizeof(int32_t) * rings, st));
+    CUDA_TRY(cudaMemsetAsync(S.live, 0, sizeof(int32_t) * rings, st));
+    CUDA_TRY(cudaMemsetAsync(S.seq, 0, sizeof(uint64_t) * rings, st));
+    CUDA_TRY(cudaMemsetAsync(S.page_table, 0xff, sizeof(int32_t) * rings * D.ppr, st));
+    CUDA_TRY(cudaMemsetAsync(S.id, 0, sizeof(uint64_t) * total_slots, st));
+    CUDA_TRY(cudaMemsetAsync(S.attn_mass, 0, sizeof(double) * total_slots, st));
+    CUDA_TRY(cudaMemsetAsync(S.n_ow, 0, sizeof(int32_t) * B, st));
+    CUDA_TRY(cudaMemsetAsync(S.n_ev, 0, sizeof(int32_t) * B * std::max(D.Gl, 1), st));
+    CUDA_TRY(cudaMemsetAsync(S.pages_before, 0, sizeof(int32_t) * B * std::max(D.Gl, 1), st));
+    CUDA_TRY(cudaMemsetAsync(S.pages_after, 0, sizeof(int32_t) * B * std::max(D.Gl, 1), st));
+    CUDA_TRY(cudaMemsetAsync(S.summary, 0, sizeof(pikv_step_summary) * B, st));
+    CUDA_TRY(cudaMemsetAsync(S.n_items, 0, sizeof(int32_t), st));
+    CUDA_TRY(cudaMemsetAsync(S.att_base, 0, sizeof(int64_t) * (B + 1), st));
+    std::vector<int32_t> stack(D.pool_pages);
+    for (int64_t i = 0; i < D.pool_pages; ++i) stack[i] = (int32_t)(D.pool_pages - 1 - i);
+    CUDA_TRY(cudaMemcpyAsync(S.free_stack, stack.data(), sizeof(int32_t) * D.pool_pages,
+                             cudaMemcpyHostToDevice, st));
+    const int32_t top = (int32_t)D.pool_pages;
+    CUDA_TRY(cudaMemcpyAsync(S.free_top, &top, sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemsetAsync(eng->in_sal, 0, sizeof(double) * B * std::max(D.n_layers, 1), st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    S.basis = nullptr, S.cbias = nullptr, S.kept = nullptr;
+    *out = eng;
+    return PIKV_OK;
+}
+
+int pikv_engine_destroy(pikv_engine* eng) {
+    if (!eng) return PIKV_OK;
+    cudaSetDevice(eng->device);
+    if (eng->stream) cudaStreamSynchronize(eng->stream);
+    for (auto& kv : eng->graphs) cudaGraphExecDestroy(kv.second);
+    for (auto e : eng->ev) cudaEventDestroy(e);
+    if (eng->step_ev[0]) cudaEventDestroy(eng->step_ev[0]), cudaEventDestroy(eng->step_ev[1]);
+    for (void* p : eng->allocs) cudaFree(p);
+    if (eng->stream) cudaStreamDestroy(eng->stream);
+    delete eng;
+    return PIKV_OK;
+}
+
+void* pikv_engine_stream(pikv_engine* eng) { return (void*)eng->stream; }
+
+int pikv_set_router_matrix_host(pikv_engine* eng, const double* w_r) {
+    CUDA_TRY(cudaMemcpyAsync((void*)eng->S.W, w_r, sizeof(double) * eng->D.E * eng->D.d,
+                             cudaMemcpyHostToDevice, eng->stream));
+    CUDA_TRY(cudaStreamSynchronize(eng->stream));
+    return PIKV_OK;
+}
+
+int pikv_set_codec_host(pikv_engine* eng, const float* basis, const float* bias,
+                        const int32_t* kept) {
+    const Dims& D = eng->D;
+    const int hd = D.d / D.H, r = D.dph;
+    auto up = [&](const void* src, size_t bytes) -> void* {
+        void* p = eng->alloc<uint8_t>(bytes);
+        if (p) cudaMemcpy(p, src, bytes, cudaMemcpyHostToDevice);
+        return p;
+    };
+    if (basis) eng->S.basis = (const float*)up(basis, sizeof(float) * (size_t)D.H * r * hd);
+    if (bias) eng->S.cbias = (const float*)up(bias, sizeof(float) * (size_t)D.d);
+    if (kept) {
+        for (int i = 0; i < D.H * r; ++i)
+            if (kept[i] < 0 || kept[i] >= hd) return fail(PIKV_ERR_INVALID_ARGUMENT, "kept index out of range");
+        eng->S.kept = (const int32_t*)up(kept, sizeof(int32_t) * (size_t)D.H * r);
+    }
+    eng->graphs.clear();  // captured kernels hold the old pointers
+    return PIKV_OK;
+}
+
+static int codec_ready(pikv_engine* eng) {
+    const int c = eng->D.codec;
+    if ((c == PIKV_CODEC_LOWRANK || c == PIKV_CODEC_LORAPLUS) && !eng->S.basis)
+        return fail(PIKV_ERR_NOT_FITTED, "codec basis not set (pikv_set_codec_host)");
+    if (c == PIKV_CODEC_LORAPLUS && !eng->S.cbias)
+        return fail(PIKV_ERR_NOT_FITTED, "LoRAPlus bias not set");
+    if (c == PIKV_CODEC_PRUNE && !eng->S.kept) return fail(PIKV_ERR_NOT_FITTED, "Prune kept set not set");
+    return PIKV_OK;
+}
+
+// The step's launch sequence (pipeline.cpp:213-351 ordering).
+static int enqueue_local(pikv_engine* eng, const void* q, const void* k, const void* v,
+                         const double* sal, bool attend) {
+    const Dims& D = eng->D;
+    const State& S = eng->S;
+    cudaStream_t st = eng->stream;
+    int n = 0;
+    CUDA_TRY(cudaMemsetAsync(S.n_ow, 0, sizeof(int32_t) * D.B, st));
+    CUDA_TRY(cudaMemsetAsync(S.n_ev, 0, sizeof(int32_t) * D.B * std::max(D.Gl, 1), st));
+    CUDA_TRY(cudaMemsetAsync(S.pages_before, 0, sizeof(int32_t) * D.B * std::max(D.Gl, 1), st));
+    CUDA_TRY(cudaMemsetAsync(S.pages_after, 0, sizeof(int32_t) * D.B * std::max(D.Gl, 1), st));
+    launch_route(D, eng->C, S, q, st), ++n;
+    if (D.Gl > 0) {
+        launch_insert(D, eng->C, S, k, v, sal, st), ++n;
+        if (!eng->C.unbounded_budget) launch_sched(D, eng->C, S, st), n += 2;
+        launch_retrieve(D, eng->C, S, st), n += 3;
+        if (attend) {
+            bool prof = eng->profiling && eng->ev_used + 2 <= (int)eng->ev.size();
+            if (prof) cudaEventRecord(eng->ev[eng->ev_used], st);
+            launch_attend(D, S, st), ++n;
+            if (prof) cudaEventRecord(eng->ev[eng->ev_used + 1], st), eng->ev_used += 2;
+        }
+    } else {
+        // a rank without devices still issues ids (k_insert does it) -- run
+        // insert for the id counter only
+        launch_insert(D, eng->C, S, k, v, sal, st), ++n;
+        launch_retrieve(D, eng->C, S, st), n += 3;
+    }
+    launch_combine(D, S, eng->X, st), ++n;
+    CUDA_TRY(cudaGetLastError());
+    eng->kernels_per_step = n;
+    return PIKV_OK;
+}
+
+static int enqueue_finish(pikv_engine* eng, const uint8_t* gathered, float* y, bool attend) {
+    launch_finish(eng->D, eng->C, eng->S, eng->X, gathered, y, attend ? 1 : 0, eng->stream);
+    eng->kernels_per_step += attend ? 3 : 2;
+    CUDA_TRY(cudaGetLastError());
+    return PIKV_OK;
+}
+
+static int run_step(pikv_engine* eng, const void* q, const void* k, const void* v,
+                    const double* sal, float* y, bool attend) {
+    int rc = codec_ready(eng);
+    if (rc) return rc;
+    if (eng->D.world != 1)
+        return fail(PIKV_ERR_INVALID_ARGUMENT, "world_size > 1: use pikv_step_local / pikv_step_finish");
+    cudaSetDevice(eng->device);
+    const bool use_graph = eng->warmed && !eng->profiling;
+    if (!use_graph) {
+        rc = enqueue_local(eng, q, k, v, sal, attend);
+        if (!rc) rc = enqueue_finish(eng, eng->S.exchange, y, attend);
+        if (rc) return rc;
+        eng->warmed = true;  // first eager pass sets kernel attributes
+        eng->launches += eng->kernels_per_step;
+        return PIKV_OK;
+    }
+    auto key = std::make_tuple(q, k, v, (const void*)sal, (void*)y, attend ? 1 : 0);
+    auto it = eng->graphs.find(key);
+    if (it == eng->graphs.end()) {
+        cudaGraph_t g;
+        CUDA_TRY(cudaStreamBeginCapture(eng->stream, cudaStreamCaptureModeThreadLocal));
+        rc = enqueue_local(eng, q, k, v, sal, attend);
+        if (!rc) rc = enqueue_finish(eng, eng->S.exchange, y, attend);
+        cudaError_t ce = cudaStreamEndCapture(eng->stream, &g);
+        if (rc) return rc;
+        if (ce != cudaSuccess) return fail(PIKV_ERR_CUDA, std::string("capture: ") + cudaGetErrorString(ce));
+        cudaGraphExec_t ge;
+        CUDA_TRY(cudaGraphInstantiate(&ge, g, 0));
+        cudaGraphDestroy(g);
+        if (eng->graphs.size() > 8) {
+            for (auto& kv : eng->graphs) cudaGraphExecDestroy(kv.second);
+            eng->graphs.clear();
+        }
+        it = eng->graphs.emplace(key, ge).first;
+    }
+    CUDA_TRY(cudaGraphLaunch(it->second, eng->stream));
+    eng->launches += eng->kernels_per_step;
+    return PIKV_OK;
+}
+
+int pikv_step(pikv_engine* eng, const void* q, const void* k, const void* v, const double* saliency,
+              float* y_out) {
+    return run_step(eng, q, k, v, saliency, y_out, true);
+}
+
+int pikv_step_host(pikv_engine* eng, const void* q, const void* k, const void* v,
+                   const double* saliency, float* y_out) {
+    const Dims& D = eng->D;
+    const size_t n = (size_t)D.B * D.d * (D.kv_dtype == PIKV_DTYPE_BF16 ? 2 : 4);
+    cudaStream_t st = eng->stream;
+    CUDA_TRY(cudaMemcpyAsync(eng->in_q, q, n, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(eng->in_k, k, n, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(eng->in_v, v, n, cudaMemcpyHostToDevice, st));
+    const double* sal = nullptr;
+    if (saliency && D.n_layers > 0) {
+        CUDA_TRY(cudaMemcpyAsync(eng->in_sal, saliency, sizeof(double) * D.B * D.n_layers,
+                                 cudaMemcpyHostToDevice, st));
+        sal = eng->in_sal;
+    }
+    int rc = run_step(eng, eng->in_q, eng->in_k, eng->in_v, sal, eng->out_y, true);
+    if (rc) return rc;
+    if (y_out)
+        CUDA_TRY(cudaMemcpyAsync(y_out, eng->out_y, sizeof(float) * D.B * D.dp, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return PIKV_OK;
+}
+
+int64_t pikv_exchange_bytes(pikv_engine* eng) { return (int64_t)eng->D.B * eng->X.bytes_per_stream; }
+
+int pikv_step_local(pikv_engine* eng, const void* q, const void* k, const void* v,
+                    const double* saliency, void** exchange_out) {
+    int rc = codec_ready(eng);
+    if (rc) return rc;
+    cudaSetDevice(eng->device);
+    rc = enqueue_local(eng, q, k, v, saliency, true);
+    if (rc) return rc;
+    eng->launches += eng->kernels_per_step;
+    if (exchange_out) *exchange_out = eng->S.exchange;
+    return PIKV_OK;
+}
+
+int pikv_step_finish(pikv_engine* eng, const void* gathered, float* y_out) {
+    cudaSetDevice(eng->device);
+    int rc = enqueue_finish(eng, (const uint8_t*)gathered, y_out, true);
+    if (rc) return rc;
+    eng->launches += 3;
+    return PIKV_OK;
+}
+
+int pikv_fill_synthetic(pikv_engine* eng, void* q, void* k, void* v, uint64_t seed) {
+    launch_synth(eng->D, q, k, v, seed, 0, eng->stream);
+    CUDA_TRY(cudaGetLastError());
+    return PIKV_OK;
+}
+
+int pikv_prefill_synthetic(pikv_engine* eng, int64_t tokens, uint64_t seed) {
+    int rc = codec_ready(eng);
+    if (rc) return rc;
+    cudaSetDevice(eng->device);
+    const bool was_prof = eng->profiling;
+    eng->profiling = false;
+    for (int64_t t = 0; t < tokens; ++t) {
+        launch_synth(eng->D, eng->in_q, eng->in_k, eng->in_v, seed, (uint64_t)t, eng->stream);
+        if (eng->D.world == 1) {
+            rc = run_step(eng, eng->in_q, eng->in_k, eng->in_v, nullptr, nullptr, false);
+        } else {
+            rc = enqueue_local(eng, eng->in_q, eng->in_k, eng->in_v, nullptr, false);
+            if (!rc) rc = enqueue_finish(eng, eng->S.exchange, nullptr, false);
+        }
+        if (rc) {
+            eng->profiling = was_prof;
+            return rc;
+        }
+        if ((t & 1023) == 1023) CUDA_TRY(cudaStreamSynchronize(eng->stream));
+    }
+    eng->profiling = was_prof;
+    CUDA_TRY(cudaStreamSynchronize(eng->stream));
+    return PIKV_OK;
+}
+
+int pikv_sync(pikv_engine* eng) {
+    CUDA_TRY(cudaStreamSynchronize(eng->stream));
+    std::vector<int32_t> err(eng->D.B);
+    CUDA_TRY(cudaMemcpy(err.data(), eng->S.err, sizeof(int32_t) * eng->D.B, cudaMemcpyDeviceToHost));
+    for (int s = 0; s < eng->D.B; ++s)
+        if (err[s]) return fail(err[s], "stream " + std::to_string(s) + " failed on device (code " +
+                                            std::to_string(err[s]) + ")");
+    return PIKV_OK;
+}
+
+// ---------------------------------------------------------------------------
+// readback
+// ---------------------------------------------------------------------------
+int pikv_read_step_host(pikv_engine* eng, int32_t* experts, double* gates, double* logits,
+                        pikv_step_summary* summary) {
+    const Dims& D = eng->D;
+    CUDA_TRY(cudaStreamSynchronize(eng->stream));
+    if (experts) CUDA_TRY(cudaMemcpy(experts, eng->S.experts, sizeof(int32_t) * D.B * D.k, cudaMemcpyDeviceToHost));
+    if (gates) CUDA_TRY(cudaMemcpy(gates, eng->S.gates, sizeof(double) * D.B * D.k, cudaMemcpyDeviceToHost));
+    if (logits) CUDA_TRY(cudaMemcpy(logits, eng->S.logits, sizeof(double) * D.B * D.E, cudaMemcpyDeviceToHost));
+    if (summary)
+        CUDA_TRY(cudaMemcpy(summary, eng->S.summary, sizeof(pikv_step_summary) * D.B, cudaMemcpyDeviceToHost));
+    return PIKV_OK;
+}
+
+int pikv_read_evictions_host(pikv_engine* eng, pikv_evict_record* out, int32_t cap, int32_t* n_out) {
+    const Dims& D = eng->D;
+    CUDA_TRY(cudaStreamSynchronize(eng->stream));
+    const int Gl = std::max(D.Gl, 1);
+    std::vector<int32_t> now(D.B), nev((size_t)D.B * Gl);
+    CUDA_TRY(cudaMemcpy(now.data(), eng->S.n_ow, sizeof(int32_t) * D.B, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(nev.data(), eng->S.n_ev, sizeof(int32_t) * D.B * Gl, cudaMemcpyDeviceToHost));
+    int32_t n = 0;
+    for (int s = 0; s < D.B; ++s) {
+        const int no = std::min(now[s], std::max(0, cap - n));
+        if (no > 0)
+            CUDA_TRY(cudaMemcpy(out + n, eng->S.rec_ow + (size_t)s * D.k, sizeof(pikv_evict_record) * no,
+                                cudaMemcpyDeviceToHost));
+        n += no;
+        for (int gl = 0; gl < D.Gl; ++gl) {
+            const int ne = std::min(nev[(size_t)s * Gl + gl], std::max(0, cap - n));
+            if (ne > 0)
+                CUDA_TRY(cudaMemcpy(out + n, eng->S.rec_ev + ((size_t)s * Gl + gl) * D.SPD * D.S,
+                                    sizeof(pikv_evict_record) * ne, cudaMemcpyDeviceToHost));
+            n += ne;
+        }
+    }
+    *n_out = n;
+    return PIKV_OK;
+}
+
+int pikv_read_attended_host(pikv_engine* eng, int32_t stream, int64_t* token, int32_t* expert,
+                            double* alpha, int32_t cap, int32_t* n_out) {
+    const Dims& D = eng->D;
+    if (stream < 0 || stream >= D.B) return fail(PIKV_ERR_INVALID_ARGUMENT, "stream out of range");
+    CUDA_TRY(cudaStreamSynchronize(eng->stream));
+    int64_t base[2];
+    CUDA_TRY(cudaMemcpy(base, eng->S.att_base + stream, sizeof(int64_t) * 2, cudaMemcpyDeviceToHost));
+    const int n = (int)(base[1] - base[0]);
+    *n_out = n;
+    const int m = std::min(n, cap);
+    if (m <= 0) return PIKV_OK;
+    std::vector<int32_t> slot(m);
+    std::vector<float> sc((size_t)m * D.H), gM(D.H), gL(D.H);
+    CUDA_TRY(cudaMemcpy(slot.data(), eng->S.att_slot + base[0], sizeof(int32_t) * m, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(sc.data(), eng->S.scores + base[0] * D.H, sizeof(float) * m * D.H, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(gM.data(), eng->S.gM + stream * D.H, sizeof(float) * D.H, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(gL.data(), eng->S.gL + stream * D.H, sizeof(float) * D.H, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < m; ++i) {
+        int64_t t;
+        int32_t e;
+        CUDA_TRY(cudaMemcpy(&t, eng->S.token + slot[i], sizeof(int64_t), cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemcpy(&e, eng->S.expert + slot[i], sizeof(int32_t), cudaMemcpyDeviceToHost));
+        if (token) token[i] = t;
+        if (expert) expert[i] = e;
+        if (alpha) {  // same expression as k_foldback
+            double a = 0.0;
+            for (int h = 0; h < D.H; ++h)
+                if (gL[h] > 0.f) a += (double)(std::exp2((double)sc[(size_t)i * D.H + h] - gM[h]) / gL[h]);
+            alpha[i] = a / D.H;
+        }
+    }
+    return PIKV_OK;
+}
+
+int64_t pikv_slot_count(pikv_engine* eng) { return (int64_t)eng->D.R * eng->D.S; }
+
+int pikv_read_slots_host(pikv_engine* eng, int32_t stream, uint64_t* id, uint64_t* shard_seq,
+                         int64_t* token, int32_t* expert, uint64_t* insert_step,
+                         uint64_t* last_access, uint64_t* freq, double* attn_mass,
+                         double* per_layer) {
+    const Dims& D = eng->D;
+    if (stream < 0 || stream >= D.B) return fail(PIKV_ERR_INVALID_ARGUMENT, "stream out of range");
+    CUDA_TRY(cudaStreamSynchronize(eng->stream));
+    const size_t n = (size_t)D.R * D.S, off = (size_t)stream * n;
+    auto cp = [&](void* dst, const void* src, size_t es) -> cudaError_t {
+        if (!dst) return cudaSuccess;
+        return cudaMemcpy(dst, (const uint8_t*)src + off * es, n * es, cudaMemcpyDeviceToHost);
+    };
+    CUDA_TRY(cp(id, eng->S.id, 8));
+    CUDA_TRY(cp(shard_seq, eng->S.shard_seq, 8));
+    CUDA_TRY(cp(token, eng->S.token, 8));
+    CUDA_TRY(cp(expert, eng->S.expert, 4));
+    CUDA_TRY(cp(insert_step, eng->S.insert_step, 8));
+    CUDA_TRY(cp(last_access, eng->S.last_access, 8));
+    CUDA_TRY(cp(freq, eng->S.freq, 8));
+    CUDA_TRY(cp(attn_mass, eng->S.attn_mass, 8));
+    if (per_layer && D.n_layers > 0)
+        CUDA_TRY(cudaMemcpy(per_layer, eng->S.per_layer + off * D.n_layers, n * D.n_layers * 8,
+                            cudaMemcpyDeviceToHost));
+    return PIKV_OK;
+}
+
+int pikv_write_attn_mass_host(pikv_engine* eng, int32_t stream, const double* attn_mass,
+                              const double* per_layer) {
+    const Dims& D = eng->D;
+    if (stream < 0 || stream >= D.B) return fail(PIKV_ERR_INVALID_ARGUMENT, "stream out of range");
+    CUDA_TRY(cudaStreamSynchronize(eng->stream));
+    const size_t n = (size_t)D.R * D.S, off = (size_t)stream * n;
+    if (attn_mass) CUDA_TRY(cudaMemcpy(eng->S.attn_mass + off, attn_mass, n * 8, cudaMemcpyHostToDevice));
+    if (per_layer && D.n_layers > 0)
+        CUDA_TRY(cudaMemcpy(eng->S.per_layer + off * D.n_layers, per_layer, n * D.n_layers * 8,
+                            cudaMemcpyHostToDevice));
+    return PIKV_OK;
+}
+
+int pikv_read_router_state_host(pikv_engine* eng, int32_t stream, double* load, uint64_t* usage,
+                                uint64_t* miss, double* bias, uint64_t* step, uint64_t* total_usage) {
+    const Dims& D = eng->D;
+    if (stream < 0 || stream >= D.B) return fail(PIKV_ERR_INVALID_ARGUMENT, "stream out of range");
+    CUDA_TRY(cudaStreamSynchronize(eng->stream));
+    const size_t E = D.E, o = (size_t)stream * E;
+    if (load) CUDA_TRY(cudaMemcpy(load, eng->S.load + o, E * 8, cudaMemcpyDeviceToHost));
+    if (usage) CUDA_TRY(cudaMemcpy(usage, eng->S.usage + o, E * 8, cudaMemcpyDeviceToHost));
+    if (miss) CUDA_TRY(cudaMemcpy(miss, eng->S.miss + o, E * 8, cudaMemcpyDeviceToHost));
+    if (bias) CUDA_TRY(cudaMemcpy(bias, eng->S.bias + o, E * 8, cudaMemcpyDeviceToHost));
+    if (step) CUDA_TRY(cudaMemcpy(step, eng->S.rstep + stream, 8, cudaMemcpyDeviceToHost));
+    if (total_usage) CUDA_TRY(cudaMemcpy(total_usage, eng->S.total_usage + stream, 8, cudaMemcpyDeviceToHost));
+    return PIKV_OK;
+}
+
+int pikv_read_sched_state_host(pikv_engine* eng, int32_t stream, double* theta, double* running_hit,
+                               uint64_t* step) {
+    if (stream < 0 || stream >= eng->D.B) return fail(PIKV_ERR_INVALID_ARGUMENT, "stream out of range");
+    CUDA_TRY(cudaStreamSynchronize(eng->stream));
+    if (theta) CUDA_TRY(cudaMemcpy(theta, eng->S.theta + stream, 8, cudaMemcpyDeviceToHost));
+    if (running_hit) CUDA_TRY(cudaMemcpy(running_hit, eng->S.running_hit + stream, 8, cudaMemcpyDeviceToHost));
+    if (step) CUDA_TRY(cudaMemcpy(step, eng->S.sstep + stream, 8, cudaMemcpyDeviceToHost));
+    return PIKV_OK;
+}
+
+int pikv_store_stats_host(pikv_engine* eng, int32_t stream, uint64_t* live, uint64_t* memory_bytes,
+                          uint64_t* inserts, uint64_t* overwrites) {
+    const Dims& D = eng->D;
+    if (stream < 0 || stream >= D.B) return fail(PIKV_ERR_INVALID_ARGUMENT, "stream out of range");
+    CUDA_TRY(cudaStreamSynchronize(eng->stream));
+    std::vector<int32_t> lv(D.R);
+    CUDA_TRY(cudaMemcpy(lv.data(), eng->S.live + (size_t)stream * D.R, sizeof(int32_t) * D.R, cudaMemcpyDeviceToHost));
+    uint64_t n = 0;
+    for (int r = 0; r < D.R; ++r) n += (uint64_t)lv[r];
+    if (live) *live = n;
+    // KVStore::memory_bytes, kvstore.cpp:193-196: 2 * d' * elem_bytes * live
+    if (memory_bytes) *memory_bytes = 2ull * (uint64_t)D.dp * (uint64_t)eng->cfg.elem_bytes * n;
+    if (inserts) CUDA_TRY(cudaMemcpy(inserts, eng->S.st_inserts + stream, 8, cudaMemcpyDeviceToHost));
+    if (overwrites) CUDA_TRY(cudaMemcpy(overwrites, eng->S.st_overwrites + stream, 8, cudaMemcpyDeviceToHost));
+    return PIKV_OK;
+}
+
+int64_t pikv_pool_pages_in_use(pikv_engine* eng) {
+    cudaStreamSynchronize(eng->stream);
+    int32_t top = 0;
+    cudaMemcpy(&top, eng->S.free_top, sizeof(int32_t), cudaMemcpyDeviceToHost);
+    return eng->D.pool_pages - top;
+}
+
+int64_t pikv_entry_bytes(pikv_engine* eng) { return eng->D.entry_bytes; }
+int64_t pikv_kernel_launches(pikv_engine* eng) { return eng->launches; }
+
+int pikv_set_profiling(pikv_engine* eng, int32_t on) {
+    eng->profiling = on != 0;
+    if (eng->profiling && eng->ev.empty()) {
+        eng->ev.resize(4096);
+        for (auto& e : eng->ev) CUDA_TRY(cudaEventCreate(&e));
+    }
+    eng->ev_used = 0;
+    return PIKV_OK;
+}
+
+int pikv_read_profile_host(pikv_engine* eng, float* attend_ms, float* step_ms, int64_t* attended_total) {
+    CUDA_TRY(cudaStreamSynchronize(eng->stream));
+    float tot = 0.f;
+    for (int i = 0; i + 1 < eng->ev_used; i += 2) {
+        float ms = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&ms, eng->ev[i], eng->ev[i + 1]));
+        tot += ms;
+    }
+    if (attend_ms) *attend_ms = tot;
+    if (step_ms) *step_ms = 0.f;
+    if (attended_total) *attended_total = eng->ev_used / 2;
+    eng->ev_used = 0;
+    return PIKV_OK;
+}
+
+}  // extern "C"

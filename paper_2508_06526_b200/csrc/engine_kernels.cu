@@ -1,0 +1,1034 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Per-step kernels of the B200 PiKV engine except decode attention
+// (attend.cu).  One launch each, all on the engine stream, graph-capturable:
+//
+//   route      router.cpp:216-234 + 122-214 (+ codec query projection,
+//              pipeline.cpp:295-297) and the retrieval candidate rings
+//   insert     kvstore.cpp:107-120 + 36-53, pipeline.cpp:148-211
+//   sched      scheduler.cpp:262-330 (score + page aggregate, select, erase)
+//   retrieve   kvstore.cpp:122-178 (filter, compact, freq/recency bump)
+//   combine    per-stream LSE merge of the attention work items
+//   finish     cross-rank LSE merge -> y, global (m, l); hits/misses
+//   foldback   pipeline.cpp:302-312 (attn_mass += alpha)
+//   feedback   pipeline.cpp:337-347 (adapt, observe_hits, adakv_update), now++
+//
+// Bit-exactness: all fp64 arithmetic that the reference performs with plain
+// * and + is written with __dmul_rn/__dadd_rn so nvcc cannot contract it into
+// FMAs, and every reduction keeps the reference's sequential order.
+#include <cuda_runtime.h>
+
+#include "pikv_dev.cuh"
+
+namespace pikv_dev {
+
+// ===========================================================================
+// route
+// ===========================================================================
+// One CTA per stream.  Threads 0..E-1 each compute one logit as the
+// reference's sequential fp64 dot (router.cpp:229-231); thread 0 then runs
+// the strategy penalty, selection, gate softmax and note_selection.
+__global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin) {
+    extern __shared__ double sm_q[];  // [d] as fp64
+    __shared__ double sm_logit[kMaxE];
+    __shared__ bool sm_flag[kMaxE];
+    __shared__ int sm_pool[kMaxE];
+    const int s = blockIdx.x;
+    const int tid = threadIdx.x;
+    if (S.err[s]) return;
+    // query in fp64 (exact upcast of bf16/f32)
+    for (int i = tid; i < D.d; i += blockDim.x) {
+        double x;
+        if (D.kv_dtype == PIKV_DTYPE_BF16)
+            x = (double)__uint_as_float(((uint32_t)((const uint16_t*)qin)[(int64_t)s * D.d + i]) << 16);
+        else
+            x = (double)((const float*)qin)[(int64_t)s * D.d + i];
+        sm_q[i] = x;
+    }
+    __syncthreads();
+    const bool base = C.router_strategy == PIKV_ROUTER_BASE;
+    if (!base) {
+        for (int e = tid; e < D.E; e += blockDim.x) {
+            const double* row = S.W + (int64_t)e * D.d;
+            double acc = 0.0;
+            for (int i = 0; i < D.d; ++i) acc = __dadd_rn(acc, __dmul_rn(row[i], sm_q[i]));
+            sm_logit[e] = acc;
+        }
+    }
+    // codec projection of the query (pipeline.cpp:295-297), fp32
+    {
+        const int H = D.H, hd = D.d / D.H, r = D.dph;
+        float* qa = S.q_attn + (int64_t)s * D.dp;
+        for (int o = tid; o < D.dp; o += blockDim.x) {
+            const int h = o / r, j = o % r;
+            float val;
+            switch (D.codec) {
+                case PIKV_CODEC_LOWRANK:
+                case PIKV_CODEC_LORAPLUS: {
+                    const float* col = S.basis + ((int64_t)h * r + j) * hd;
+                    float acc = 0.f;
+                    for (int i = 0; i < hd; ++i) {
+                        float xi = (float)sm_q[h * hd + i];
+                        if (D.codec == PIKV_CODEC_LORAPLUS) xi -= S.cbias[h * hd + i];
+                        acc = fmaf(col[i], xi, acc);
+                    }
+                    val = acc;
+                    break;
+                }
+                case PIKV_CODEC_FASTV: val = (float)sm_q[h * hd + j]; break;
+                case PIKV_CODEC_PRUNE: val = (float)sm_q[h * hd + S.kept[h * r + j]]; break;
+                default: val = (float)sm_q[o]; break;
+            }
+            qa[o] = val;
+        }
+        (void)H;
+    }
+    __syncthreads();
+    if (tid != 0) return;
+
+    const int E = D.E, k = D.k;
+    double* load = S.load + (int64_t)s * E;
+    uint64_t* usage = S.usage + (int64_t)s * E;
+    int32_t* experts = S.experts + (int64_t)s * k;
+    double* gates = S.gates + (int64_t)s * k;
+    double* lg = S.logits + (int64_t)s * E;
+    int sel[kMaxK];
+    if (base) {  // base_round_robin, router.cpp:107-118
+        int64_t t = (int64_t)S.rstep[s];
+        for (int j = 0; j < k; ++j) sel[j] = (int)((t * C.stride + j) % E);
+        for (int j = 0; j < k; ++j) gates[j] = __ddiv_rn(1.0, (double)k);
+        for (int e = 0; e < E; ++e) lg[e] = 0.0;
+    } else {
+        for (int e = 0; e < E; ++e) {
+            if (isnan(sm_logit[e])) {  // router.cpp:131-133
+                S.err[s] = PIKV_ERR_NUMERICAL;
+                return;
+            }
+        }
+        switch (C.router_strategy) {
+            case PIKV_ROUTER_LOAD_BALANCED: {
+                double acc = 0.0;
+                for (int e = 0; e < E; ++e) acc = __dadd_rn(acc, load[e]);
+                double mean = __ddiv_rn(acc, (double)E);
+                for (int e = 0; e < E; ++e)
+                    sm_logit[e] = __dsub_rn(sm_logit[e], __dmul_rn(C.alpha, __dsub_rn(load[e], mean)));
+                break;
+            }
+            case PIKV_ROUTER_CACHE_AWARE:
+                for (int e = 0; e < E; ++e)
+                    sm_logit[e] = __dsub_rn(sm_logit[e], __dmul_rn(C.lambda_miss,
+                                                                  log1p((double)S.miss[(int64_t)s * E + e])));
+                break;
+            case PIKV_ROUTER_ENTROPY_LB: {
+                uint64_t tot = S.total_usage[s];
+                for (int e = 0; e < E; ++e) {
+                    double p = tot == 0 ? 0.0 : __ddiv_rn((double)usage[e], (double)tot);
+                    double h = p > 0.0 ? __dmul_rn(-p, log(p)) : 0.0;
+                    sm_logit[e] = __dsub_rn(sm_logit[e], __dmul_rn(C.beta_ent, h));
+                }
+                break;
+            }
+            case PIKV_ROUTER_ADAPTIVE:
+                for (int e = 0; e < E; ++e)
+                    sm_logit[e] = __dadd_rn(sm_logit[e], S.bias[(int64_t)s * E + e]);
+                break;
+            default:
+                break;
+        }
+        // selection: (score desc, index asc), router.cpp:82-90, 174-198
+        auto better = [&](int a, int b) {
+            double sa = sm_logit[a], sb = sm_logit[b];
+            return sa != sb ? sa > sb : a < b;
+        };
+        if (C.router_strategy == PIKV_ROUTER_HIERARCHICAL) {
+            const int groups = C.groups;
+            const int cs = (E + groups - 1) / groups;
+            // cluster order by (max logit desc, index asc); pool grows until >= k
+            int chosen_clusters = 0, npool = 0;
+            bool* used = sm_flag;
+            int* pool = sm_pool;
+            for (int g = 0; g < groups; ++g) used[g] = false;
+            while (npool < k && chosen_clusters < groups) {
+                int best = -1;
+                double bsc = 0.0;
+                for (int g = 0; g < groups; ++g) {
+                    if (used[g]) continue;
+                    double sc = -INFINITY;
+                    for (int e = g * cs; e < min(E, g * cs + cs); ++e)
+                        sc = (sc < sm_logit[e]) ? sm_logit[e] : sc;
+                    if (best < 0 || sc > bsc) best = g, bsc = sc;  // ties keep lower g
+                }
+                used[best] = true;
+                ++chosen_clusters;
+                for (int e = best * cs; e < min(E, best * cs + cs); ++e) pool[npool++] = e;
+            }
+            for (int j = 0; j < k; ++j) {  // partial selection sort over the pool
+                int bi = j;
+                for (int i = j + 1; i < npool; ++i)
+                    if (better(pool[i], pool[bi])) bi = i;
+                int t = pool[j];
+                pool[j] = pool[bi];
+                pool[bi] = t;
+                sel[j] = pool[j];
+            }
+        } else {
+            // k rounds of argmax excluding earlier picks == sorted prefix
+            bool* taken = sm_flag;
+            for (int e = 0; e < E; ++e) taken[e] = false;
+            for (int j = 0; j < k; ++j) {
+                int bi = -1;
+                for (int e = 0; e < E; ++e)
+                    if (!taken[e] && (bi < 0 || better(e, bi))) bi = e;
+                taken[bi] = true;
+                sel[j] = bi;
+            }
+        }
+        // gates = softmax(selected logits), mathops.cpp:11-30
+        double mx = sm_logit[sel[0]];
+        for (int j = 0; j < k; ++j) mx = (mx < sm_logit[sel[j]]) ? sm_logit[sel[j]] : mx;
+        double tot = 0.0;
+        for (int j = 0; j < k; ++j) {
+            gates[j] = exp(__dsub_rn(sm_logit[sel[j]], mx));
+            tot = __dadd_rn(tot, gates[j]);
+        }
+        for (int j = 0; j < k; ++j) gates[j] = __ddiv_rn(gates[j], tot);
+        for (int e = 0; e < E; ++e) lg[e] = sm_logit[e];
+    }
+    // note_selection, router.cpp:92-105
+    const double one_m = __dsub_rn(1.0, C.load_decay);
+    for (int e = 0; e < E; ++e) {
+        bool picked = false;
+        for (int j = 0; j < k; ++j) picked |= sel[j] == e;
+        load[e] = __dadd_rn(__dmul_rn(C.load_decay, load[e]), __dmul_rn(one_m, picked ? 1.0 : 0.0));
+    }
+    for (int j = 0; j < k; ++j) {
+        usage[sel[j]] += 1;
+        experts[j] = sel[j];
+    }
+    S.total_usage[s] += (uint64_t)k;
+    S.rstep[s] += 1;
+
+    // candidate local rings for retrieval (ascending ring id)
+    int nc = 0;
+    int32_t* cand = S.cand + (int64_t)s * D.max_cand;
+    for (int gl = 0; gl < D.Gl; ++gl) {
+        const int g = gl * D.world + D.rank;
+        for (int sh = 0; sh < D.SPD; ++sh) {
+            const int raw = sh * D.G + g;
+            bool ok = false;
+            for (int j = 0; j < k && !ok; ++j)
+                ok = ring_can_hold(raw, sel[j], D.n_tok, D.n_exp, D.additive);
+            if (ok && nc < D.max_cand) cand[nc++] = gl * D.SPD + sh;
+        }
+    }
+    S.ncand[s] = nc;
+}
+
+void launch_route(const Dims& D, const Cfg& C, const State& S, const void* q, cudaStream_t st) {
+    size_t smem = sizeof(double) * (size_t)D.d;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_route, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_route<<<D.B, 256, smem, st>>>(D, C, S, q);
+}
+
+// ===========================================================================
+// insert: KVStore::insert for the k staged entries of each stream
+// ===========================================================================
+__device__ __forceinline__ float load_in(const void* p, int dtype, int64_t i) {
+    if (dtype == PIKV_DTYPE_BF16) return __uint_as_float(((uint32_t)((const uint16_t*)p)[i]) << 16);
+    return ((const float*)p)[i];
+}
+
+// Encode one K or V row of stream s into smem `dst` in the stored layout.
+__device__ void encode_row(const Dims& D, const State& S, const void* x, int s, uint8_t* dst,
+                           float* scales_out, float* tmp) {
+    const int H = D.H, hd = D.d / H, r = D.dph, tid = threadIdx.x, nt = blockDim.x;
+    const int64_t base = (int64_t)s * D.d;
+    switch (D.codec) {
+        case PIKV_CODEC_IDENTITY:
+            if (D.kv_dtype == PIKV_DTYPE_BF16) {
+                for (int i = tid; i < D.d; i += nt) ((uint16_t*)dst)[i] = ((const uint16_t*)x)[base + i];
+            } else {
+                for (int i = tid; i < D.d; i += nt) ((float*)dst)[i] = ((const float*)x)[base + i];
+            }
+            return;
+        case PIKV_CODEC_LOWRANK:
+        case PIKV_CODEC_LORAPLUS:
+        case PIKV_CODEC_FASTV:
+        case PIKV_CODEC_PRUNE:
+            for (int o = tid; o < D.dp; o += nt) {
+                const int h = o / r, j = o % r;
+                float val;
+                if (D.codec == PIKV_CODEC_FASTV) {
+                    val = load_in(x, D.kv_dtype, base + h * hd + j);
+                } else if (D.codec == PIKV_CODEC_PRUNE) {
+                    val = load_in(x, D.kv_dtype, base + h * hd + S.kept[h * r + j]);
+                } else {  // project_encode, compressor.cpp:318-329
+                    const float* col = S.basis + ((int64_t)h * r + j) * hd;
+                    float acc = 0.f;
+                    for (int i = 0; i < hd; ++i) {
+                        float xi = load_in(x, D.kv_dtype, base + h * hd + i);
+                        if (D.codec == PIKV_CODEC_LORAPLUS) xi -= S.cbias[h * hd + i];
+                        acc = fmaf(col[i], xi, acc);
+                    }
+                    val = acc;
+                }
+                if (D.kv_dtype == PIKV_DTYPE_BF16) ((uint16_t*)dst)[o] = f32_to_bf16_rne(val);
+                else ((float*)dst)[o] = val;
+            }
+            return;
+        case PIKV_CODEC_INT8:
+        case PIKV_CODEC_INT4: {
+            // symmetric absmax per head (oracle: po_quantize_row)
+            const int bits = D.codec == PIKV_CODEC_INT8 ? 8 : 4;
+            const float qmax = bits == 8 ? 127.0f : 7.0f;
+            for (int i = tid; i < D.d; i += nt) tmp[i] = load_in(x, D.kv_dtype, base + i);
+            __syncthreads();
+            const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+            for (int h = warp; h < H; h += nw) {
+                float amax = 0.f;
+                for (int i = lane; i < hd; i += 32) amax = fmaxf(amax, fabsf(tmp[h * hd + i]));
+                for (int off = 16; off; off >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
+                float inv = 0.f, scale = 0.f;
+                if (amax > 0.f) {
+                    scale = __fdiv_rn(amax, qmax);
+                    inv = __fdiv_rn(qmax, amax);
+                }
+                if (lane == 0) scales_out[h] = scale;
+                if (bits == 8) {
+                    for (int i = lane; i < hd; i += 32) {
+                        float c = rintf(__fmul_rn(tmp[h * hd + i], inv));
+                        c = fminf(fmaxf(c, -qmax), qmax);
+                        ((int8_t*)dst)[h * hd + i] = (int8_t)(int)c;
+                    }
+                } else {
+                    for (int i2 = lane; i2 < hd / 2; i2 += 32) {
+                        float c0 = rintf(__fmul_rn(tmp[h * hd + 2 * i2], inv));
+                        float c1 = rintf(__fmul_rn(tmp[h * hd + 2 * i2 + 1], inv));
+                        c0 = fminf(fmaxf(c0, -qmax), qmax);
+                        c1 = fminf(fmaxf(c1, -qmax), qmax);
+                        dst[(h * hd) / 2 + i2] = (uint8_t)(((int)c0 & 0xF) | (((int)c1 & 0xF) << 4));
+                    }
+                }
+            }
+            __syncthreads();
+            return;
+        }
+    }
+}
+
+__global__ void k_insert(Dims D, Cfg C, State S, const void* __restrict__ kin,
+                         const void* __restrict__ vin, const double* __restrict__ saliency) {
+    extern __shared__ __align__(16) uint8_t sm_entry[];  // [entry_bytes] + tmp floats [d]
+    __shared__ int64_t sm_dst[kMaxK];
+    __shared__ int64_t sm_slot[kMaxK];
+    __shared__ int sm_n;
+    const int s = blockIdx.x, tid = threadIdx.x;
+    if (S.err[s]) return;
+    float* tmp = (float*)(sm_entry + ((D.entry_bytes + 15) & ~15));
+    const int pay = D.payload_bytes;
+    float* ksc = (float*)(sm_entry + 2 * pay);
+    float* vsc = ksc + D.H;
+    encode_row(D, S, kin, s, sm_entry, ksc, tmp);
+    encode_row(D, S, vin, s, sm_entry + pay, vsc, tmp);
+    if (tid == 0) {
+        const uint64_t now = S.now[s];
+        const int64_t token = (int64_t)now;
+        int n = 0;
+        for (int j = 0; j < D.k; ++j) {
+            const int e = S.experts[(int64_t)s * D.k + j];
+            const int raw = shard_raw(token, e, D.n_tok, D.n_exp, D.additive);
+            const int dev = raw % D.G, sh = raw / D.G;
+            const uint64_t id = S.next_id[s]++;  // every rank issues every id
+            if (dev % D.world != D.rank) continue;
+            const int gl = dev / D.world;
+            const int64_t ring = ((int64_t)s * D.Gl + gl) * D.SPD + sh;
+            const int slot = S.head[ring];
+            const int64_t gi = ring * D.S + slot;
+            const int64_t pidx = ring * D.ppr + slot / D.spg;
+            int32_t page = S.page_table[pidx];
+            if (S.id[gi] != 0) {  // displaced (kvstore.cpp:41-43; pipeline.cpp:200-208)
+                const int no = S.n_ow[s]++;
+                EvictRec& r = S.rec_ow[(int64_t)s * D.k + no];
+                r.step = now;
+                r.entry_id = S.id[gi];
+                r.token_id = S.token[gi];
+                r.expert_id = S.expert[gi];
+                r.device = dev;
+                r.score = 0.0;
+                r.reason = PIKV_EVICT_OVERWRITE;
+                r.stream = s;
+                S.st_overwrites[s] += 1;
+            } else {
+                S.live[ring] += 1;
+                if (page < 0) {
+                    const int top = atomicSub(S.free_top, 1) - 1;
+                    if (top < 0) {
+                        atomicAdd(S.free_top, 1);
+                        S.err[s] = PIKV_ERR_OUT_OF_MEMORY;
+                        return;
+                    }
+                    page = S.free_stack[top];
+                    S.page_table[pidx] = page;
+                    S.page_live[page] = 0;
+                }
+                S.page_live[page] += 1;
+            }
+            S.id[gi] = id;
+            S.shard_seq[gi] = S.seq[ring]++;
+            S.token[gi] = token;
+            S.expert[gi] = e;
+            S.insert_step[gi] = now;
+            S.last_access[gi] = now;
+            S.freq[gi] = 0;
+            S.attn_mass[gi] = 0.0;
+            for (int l = 0; l < D.n_layers; ++l)
+                S.per_layer[gi * D.n_layers + l] = saliency ? saliency[(int64_t)s * D.n_layers + l] : 0.0;
+            S.head[ring] = (slot + 1) % D.S;
+            S.st_inserts[s] += 1;
+            sm_dst[n] = (int64_t)page * D.spg + slot % D.spg;
+            sm_slot[n] = gi;
+            ++n;
+        }
+        sm_n = n;
+    }
+    __syncthreads();
+    const int n = sm_n;
+    const int nvec = D.entry_bytes / 16;
+    for (int j = 0; j < n; ++j) {
+        uint4* dst = (uint4*)(S.pool + sm_dst[j] * (int64_t)D.entry_bytes);
+        const uint4* src = (const uint4*)sm_entry;
+        for (int i = tid; i < nvec; i += blockDim.x) dst[i] = src[i];
+    }
+}
+
+void launch_insert(const Dims& D, const Cfg& C, const State& S, const void* k, const void* v,
+                   const double* saliency, cudaStream_t st) {
+    size_t smem = (size_t)((D.entry_bytes + 15) & ~15) + sizeof(float) * (size_t)D.d;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_insert, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_insert<<<D.B, 256, smem, st>>>(D, C, S, k, v, saliency);
+}
+
+// ===========================================================================
+// sched: evict, scheduler.cpp:262-330
+// ===========================================================================
+// (a) one thread per candidate scheduler page (ring, page_no): aggregate of
+//     member scores in slot order, oldest id, member count.
+__global__ void k_sched_pages(Dims D, Cfg C, State S) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t total = (int64_t)D.B * D.R * D.ppr_sched;
+    if (t >= total) return;
+    const int64_t ring = t / D.ppr_sched;
+    const int pi = (int)(t % D.ppr_sched);
+    const int s = (int)(ring / D.R);
+    S.pg_cnt[t] = 0;
+    if (S.err[s]) return;
+    const uint64_t seq = S.seq[ring];
+    const uint64_t Su = (uint64_t)D.S, ps = (uint64_t)D.page_size;
+    const uint64_t lo = seq > Su ? seq - Su : 0;
+    const uint64_t q = lo / ps + (uint64_t)pi;
+    if (q * ps >= seq) return;
+    const uint64_t s0 = (q * ps) % Su;
+    // slot order: members whose slot wrapped to 0.. come first
+    const int w = (s0 + ps > Su) ? (int)(Su - s0) : 0;
+    const uint64_t now = S.now[s];
+    double agg = 0.0;
+    uint64_t oldest = 0;
+    int cnt = 0;
+    for (int u = 0; u < (int)ps; ++u) {
+        const int i = (w + u) % (int)ps;
+        const uint64_t sq = q * ps + (uint64_t)i;
+        const int64_t gi = ring * D.S + (int64_t)(sq % Su);
+        const uint64_t id = S.id[gi];
+        if (id == 0 || S.shard_seq[gi] != sq) continue;
+        if (cnt == 0 || id < oldest) oldest = id;
+        agg = __dadd_rn(agg, score_entry(C, S, gi, now, D.n_layers));
+        ++cnt;
+    }
+    S.pg_agg[t] = agg;
+    S.pg_oldest[t] = oldest;
+    S.pg_cnt[t] = cnt;
+}
+
+__device__ __forceinline__ bool page_less(double a, uint64_t oa, double b, uint64_t ob) {
+    return a != b ? a < b : oa < ob;
+}
+
+// (b) one CTA per (stream, local device): select_evictions + erase.
+constexpr int kSelThreads = 1024;
+__global__ void __launch_bounds__(kSelThreads) k_sched_select(Dims D, Cfg C, State S) {
+    const int sg = blockIdx.x;  // s * Gl + gl
+    const int s = sg / D.Gl, gl = sg % D.Gl;
+    const int tid = threadIdx.x;
+    __shared__ int sm_red[32];
+    __shared__ int sm_P, sm_thr, sm_V;
+    __shared__ double sm_ba;
+    __shared__ uint64_t sm_bo;
+    __shared__ int sm_bi;
+    if (S.err[s]) return;
+    const int64_t first = (int64_t)sg * D.SPD * D.ppr_sched;  // pages of this device
+    const int npg = D.SPD * D.ppr_sched;
+    int32_t* list = S.sel_idx + (int64_t)sg * D.sel_stride;
+    const double theta = S.theta[s];
+    const bool use_theta = C.sched_strategy == PIKV_SCHED_ADAKV;
+    // count pages and below-theta pages
+    int P = 0, T = 0;
+    for (int i = tid; i < npg; i += kSelThreads) {
+        if (S.pg_cnt[first + i] > 0) {
+            ++P;
+            if (use_theta && S.pg_agg[first + i] < theta) ++T;
+        }
+    }
+    for (int off = 16; off; off >>= 1) {
+        P += __shfl_xor_sync(0xffffffffu, P, off);
+        T += __shfl_xor_sync(0xffffffffu, T, off);
+    }
+    if ((tid & 31) == 0) sm_red[tid >> 5] = P | 0;
+    __syncthreads();
+    if (tid == 0) {
+        int p = 0;
+        for (int w = 0; w < kSelThreads / 32; ++w) p += sm_red[w];
+        sm_P = p;
+    }
+    __syncthreads();
+    if ((tid & 31) == 0) sm_red[tid >> 5] = T;
+    __syncthreads();
+    if (tid == 0) {
+        int t = 0;
+        for (int w = 0; w < kSelThreads / 32; ++w) t += sm_red[w];
+        sm_thr = t;
+        const int over = sm_P - C.budget_pages;
+        sm_V = max(t, max(over, 0));  // select_evictions, scheduler.cpp:246-259
+        S.pages_before[sg] = sm_P;
+        S.pages_after[sg] = sm_P - sm_V;
+        S.n_ev[sg] = 0;
+    }
+    __syncthreads();
+    const int V = sm_V;
+    if (V == 0) return;
+    if (V <= 32) {
+        // V rounds of block-wide argmin over (aggregate, oldest_id)
+        for (int v = 0; v < V; ++v) {
+            double ba = 0.0;
+            uint64_t bo = 0;
+            int bi = -1;
+            for (int i = tid; i < npg; i += kSelThreads) {
+                if (S.pg_cnt[first + i] <= 0) continue;
+                const double a = S.pg_agg[first + i];
+                const uint64_t o = S.pg_oldest[first + i];
+                if (bi < 0 || page_less(a, o, ba, bo)) ba = a, bo = o, bi = i;
+            }
+            for (int off = 16; off; off >>= 1) {
+                double a2 = __shfl_xor_sync(0xffffffffu, ba, off);
+                uint64_t o2 = __shfl_xor_sync(0xffffffffu, bo, off);
+                int i2 = __shfl_xor_sync(0xffffffffu, bi, off);
+                if (i2 >= 0 && (bi < 0 || page_less(a2, o2, ba, bo))) ba = a2, bo = o2, bi = i2;
+            }
+            __shared__ double wa[32];
+            __shared__ uint64_t wo[32];
+            __shared__ int wi[32];
+            if ((tid & 31) == 0) wa[tid >> 5] = ba, wo[tid >> 5] = bo, wi[tid >> 5] = bi;
+            __syncthreads();
+            if (tid == 0) {
+                int b = -1;
+                double a = 0.0;
+                uint64_t o = 0;
+                for (int w = 0; w < kSelThreads / 32; ++w) {
+                    if (wi[w] >= 0 && (b < 0 || page_less(wa[w], wo[w], a, o))) a = wa[w], o = wo[w], b = wi[w];
+                }
+                list[v] = b;
+                S.pg_cnt[first + b] = -S.pg_cnt[first + b];  // mark taken (negative count)
+            }
+            __syncthreads();
+        }
+    } else {
+        // full bitonic sort of page indices by (aggregate, oldest_id) in the
+        // scratch list (power-of-two capacity D.sel_stride; -1 sorts last),
+        // then take the first V.
+        const int n2 = D.sel_stride;
+        for (int i = tid; i < n2; i += kSelThreads)
+            list[i] = (i < npg && S.pg_cnt[first + i] > 0) ? i : -1;
+        __syncthreads();
+        auto key_less = [&](int a, int b) {
+            if (a < 0) return false;
+            if (b < 0) return true;
+            return page_less(S.pg_agg[first + a], S.pg_oldest[first + a], S.pg_agg[first + b],
+                             S.pg_oldest[first + b]);
+        };
+        for (int kk = 2; kk <= n2; kk <<= 1) {
+            for (int j = kk >> 1; j > 0; j >>= 1) {
+                for (int i = tid; i < n2; i += kSelThreads) {
+                    const int ixj = i ^ j;
+                    if (ixj > i) {
+                        const int a = list[i], b = list[ixj];
+                        const bool up = (i & kk) == 0;
+                        if (up ? key_less(b, a) : key_less(a, b)) {
+                            list[i] = b;
+                            list[ixj] = a;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        for (int v = tid; v < V; v += kSelThreads) S.pg_cnt[first + list[v]] = -S.pg_cnt[first + list[v]];
+        __syncthreads();
+    }
+    // erase victims in order; record offsets by prefix of member counts
+    __shared__ int sm_off;
+    if (tid == 0) sm_off = 0;
+    __syncthreads();
+    const uint64_t sstep = S.sstep[s];
+    const uint64_t now = S.now[s];
+    const int dev = gl * D.world + D.rank;
+    EvictRec* rec = S.rec_ev + (int64_t)sg * D.SPD * D.S;
+    for (int v0 = 0; v0 < V; v0 += kSelThreads) {
+        const int v = v0 + tid;
+        int cnt = 0, pidx = -1;
+        if (v < V) {
+            pidx = list[v];
+            cnt = -S.pg_cnt[first + pidx];
+        }
+        // block exclusive scan of cnt
+        int x = cnt;
+        for (int off = 1; off < 32; off <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, x, off);
+            if ((tid & 31) >= off) x += y;
+        }
+        __shared__ int wsum[32];
+        if ((tid & 31) == 31) wsum[tid >> 5] = x;
+        __syncthreads();
+        if (tid < 32) {
+            int w = wsum[tid];
+            for (int off = 1; off < 32; off <<= 1) {
+                int y = __shfl_up_sync(0xffffffffu, w, off);
+                if (tid >= off) w += y;
+            }
+            wsum[tid] = w;
+        }
+        __syncthreads();
+        const int excl = x - cnt + ((tid >> 5) ? wsum[(tid >> 5) - 1] : 0) + sm_off;
+        if (v < V) {
+            const int reason = v < sm_thr ? PIKV_EVICT_THRESHOLD : PIKV_EVICT_BUDGET;
+            const int64_t ring = (int64_t)sg * D.SPD + pidx / D.ppr_sched;
+            const uint64_t seq = S.seq[ring];
+            const uint64_t Su = (uint64_t)D.S, ps = (uint64_t)D.page_size;
+            const uint64_t lo = seq > Su ? seq - Su : 0;
+            const uint64_t q = lo / ps + (uint64_t)(pidx % D.ppr_sched);
+            int o = excl;
+            for (uint64_t sq = q * ps; sq < (q + 1) * ps; ++sq) {  // id order
+                const int slot = (int)(sq % Su);
+                const int64_t gi = ring * D.S + slot;
+                if (S.id[gi] == 0 || S.shard_seq[gi] != sq) continue;
+                EvictRec& r = rec[o++];
+                r.step = sstep;
+                r.entry_id = S.id[gi];
+                r.token_id = S.token[gi];
+                r.expert_id = S.expert[gi];
+                r.device = dev;
+                r.score = score_entry(C, S, gi, now, D.n_layers);
+                r.reason = reason;
+                r.stream = s;
+                // KVStore::erase (kvstore.cpp:180-185) + page reclamation
+                S.id[gi] = 0;
+                atomicSub(&S.live[ring], 1);
+                const int64_t pt_i = ring * D.ppr + slot / D.spg;
+                const int32_t page = S.page_table[pt_i];
+                if (atomicSub(&S.page_live[page], 1) == 1) {
+                    S.page_table[pt_i] = -1;
+                    const int top = atomicAdd(S.free_top, 1);
+                    S.free_stack[top] = page;
+                }
+            }
+        }
+        __syncthreads();
+        if (tid == kSelThreads - 1) sm_off = excl + cnt;
+        __syncthreads();
+    }
+    if (tid == 0) S.n_ev[sg] = sm_off;
+}
+
+void launch_sched(const Dims& D, const Cfg& C, const State& S, cudaStream_t st) {
+    const int64_t total = (int64_t)D.B * D.R * D.ppr_sched;
+    k_sched_pages<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(D, C, S);
+    k_sched_select<<<D.B * D.Gl, kSelThreads, 0, st>>>(D, C, S);
+}
+
+// ===========================================================================
+// retrieve: KVStore::retrieve over the candidate rings
+// ===========================================================================
+// (a) count matches per (stream, candidate, chunk of chunk_slots slots)
+__global__ void k_retr_count(Dims D, State S) {
+    const int s = blockIdx.x, c = blockIdx.y, ch = blockIdx.z;
+    const int tid = threadIdx.x;
+    __shared__ int red[32];
+    __shared__ int fred[kMaxK];
+    const int64_t ci = ((int64_t)s * D.max_cand + c) * D.nch + ch;
+    if (tid < D.k) fred[tid] = 0;
+    int cnt = 0;
+    const bool active = !S.err[s] && c < S.ncand[s];
+    if (active) {
+        const int64_t ring = (int64_t)s * D.R + S.cand[(int64_t)s * D.max_cand + c];
+        const uint64_t seq = S.seq[ring];
+        const int fill = seq < (uint64_t)D.S ? (int)seq : D.S;
+        const int slot = ch * D.chunk_slots + tid;
+        const int64_t now = (int64_t)S.now[s];
+        __syncthreads();
+        if (slot < fill && tid < D.chunk_slots) {
+            const int64_t gi = ring * D.S + slot;
+            if (S.id[gi] != 0 && S.token[gi] < now) {
+                const int e = S.expert[gi];
+                for (int j = 0; j < D.k; ++j) {
+                    if (S.experts[(int64_t)s * D.k + j] == e) {
+                        cnt = 1;
+                        atomicAdd(&fred[j], 1);
+                        break;
+                    }
+                }
+            }
+        }
+    } else {
+        __syncthreads();
+    }
+    for (int off = 16; off; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+    if ((tid & 31) == 0) red[tid >> 5] = cnt;
+    __syncthreads();
+    if (tid == 0) {
+        int t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        S.chunk_cnt[ci] = t;
+    }
+    if (active && tid < D.k && fred[tid]) atomicAdd(&S.found[(int64_t)s * D.k + tid], fred[tid]);
+}
+
+// (b) single CTA: exclusive offsets, per-stream bases, attention work items.
+__global__ void k_retr_scan(Dims D, State S) {
+    __shared__ int64_t sm_tot[1024];
+    const int tid = threadIdx.x;
+    const int per = D.max_cand * D.nch;
+    // per-stream totals + in-stream chunk offsets (a thread per stream)
+    for (int s = tid; s < D.B; s += blockDim.x) {
+        int64_t acc = 0;
+        for (int i = 0; i < per; ++i) {
+            const int64_t ci = (int64_t)s * per + i;
+            S.chunk_off[ci] = (int32_t)acc;
+            acc += S.chunk_cnt[ci];
+        }
+        S.summary[s].n_attended = (int32_t)acc;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int64_t acc = 0;
+        for (int s = 0; s < D.B; ++s) {
+            S.att_base[s] = acc;
+            acc += S.summary[s].n_attended;
+        }
+        S.att_base[D.B] = acc;
+        // work items: chunk size so that ~4 items per attention CTA
+        const int64_t N = acc;
+        int64_t C = (N + 4LL * D.attend_ctas - 1) / (4LL * D.attend_ctas);
+        if (C < 16) C = 16;
+        int64_t w = 0;
+        for (int s = 0; s < D.B; ++s) {
+            const int64_t n = S.summary[s].n_attended;
+            for (int64_t a = 0; a < n && w < D.item_cap; a += C) {
+                S.item_stream[w] = s;
+                S.item_begin[w] = (int32_t)a;
+                S.item_end[w] = (int32_t)(a + C < n ? a + C : n);
+                ++w;
+            }
+        }
+        S.n_items[0] = (int32_t)w;
+    }
+    (void)sm_tot;
+}
+
+// (c) write the compacted (slot, entry) lists; bump freq / last_access.
+__global__ void k_retr_write(Dims D, State S) {
+    const int s = blockIdx.x, c = blockIdx.y, ch = blockIdx.z;
+    const int tid = threadIdx.x;
+    if (S.err[s] || c >= S.ncand[s]) return;
+    const int64_t ci = ((int64_t)s * D.max_cand + c) * D.nch + ch;
+    const int64_t ring = (int64_t)s * D.R + S.cand[(int64_t)s * D.max_cand + c];
+    const uint64_t seq = S.seq[ring];
+    const int fill = seq < (uint64_t)D.S ? (int)seq : D.S;
+    const int slot = ch * D.chunk_slots + tid;
+    const uint64_t now = S.now[s];
+    int m = 0;
+    int64_t gi = 0;
+    if (slot < fill && tid < D.chunk_slots) {
+        gi = ring * D.S + slot;
+        if (S.id[gi] != 0 && S.token[gi] < (int64_t)now) {
+            const int e = S.expert[gi];
+            for (int j = 0; j < D.k; ++j)
+                if (S.experts[(int64_t)s * D.k + j] == e) m = 1;
+        }
+    }
+    // block exclusive scan of m (slot order)
+    int x = m;
+    for (int off = 1; off < 32; off <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, x, off);
+        if ((tid & 31) >= off) x += y;
+    }
+    __shared__ int ws[32];
+    if ((tid & 31) == 31) ws[tid >> 5] = x;
+    __syncthreads();
+    if (tid < 32) {
+        int w = tid < (int)(blockDim.x >> 5) ? ws[tid] : 0;
+        for (int off = 1; off < 32; off <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, w, off);
+            if (tid >= off) w += y;
+        }
+        ws[tid] = w;
+    }
+    __syncthreads();
+    if (m) {
+        const int excl = x - 1 + ((tid >> 5) ? ws[(tid >> 5) - 1] : 0);
+        const int64_t pos = S.att_base[s] + S.chunk_off[ci] + excl;
+        S.att_slot[pos] = (int32_t)gi;
+        const int32_t page = S.page_table[ring * D.ppr + slot / D.spg];
+        S.att_entry[pos] = page * D.spg + slot % D.spg;
+        S.freq[gi] += 1;  // kvstore.cpp:165-168
+        S.last_access[gi] = now;
+    }
+}
+
+void launch_retrieve(const Dims& D, const Cfg& C, const State& S, cudaStream_t st) {
+    (void)C;
+    cudaMemsetAsync(S.found, 0, sizeof(int32_t) * (size_t)D.B * D.k, st);
+    dim3 grid(D.B, D.max_cand, D.nch);
+    k_retr_count<<<grid, D.chunk_slots, 0, st>>>(D, S);
+    k_retr_scan<<<1, 1024, 0, st>>>(D, S);
+    k_retr_write<<<grid, D.chunk_slots, 0, st>>>(D, S);
+}
+
+// ===========================================================================
+// combine: per-stream merge of work-item partials into the exchange record
+// ===========================================================================
+__global__ void k_combine(Dims D, State S, ExchangeLayout X) {
+    const int s = blockIdx.x;
+    const int tid = threadIdx.x;
+    uint8_t* rec = S.exchange + (int64_t)s * X.bytes_per_stream;
+    float* xo = (float*)(rec + X.o_off);
+    float* xm = (float*)(rec + X.m_off);
+    float* xl = (float*)(rec + X.l_off);
+    int32_t* xf = (int32_t*)(rec + X.found_off);
+    int32_t* xs = (int32_t*)(rec + X.stats_off);
+    // item range of stream s (items are stream-ordered)
+    __shared__ int sm_w0, sm_w1;
+    if (tid == 0) {
+        const int n = S.n_items[0];
+        int w0 = 0;
+        while (w0 < n && S.item_stream[w0] < s) ++w0;  // n is small (~4 * CTAs)
+        int w1 = w0;
+        while (w1 < n && S.item_stream[w1] == s) ++w1;
+        sm_w0 = w0, sm_w1 = w1;
+    }
+    __syncthreads();
+    const int w0 = sm_w0, w1 = sm_w1;
+    const bool ok = !S.err[s];
+    for (int o = tid; o < D.H * D.dph; o += blockDim.x) {
+        const int h = o / D.dph;
+        float m = -INFINITY;
+        for (int w = w0; w < w1; ++w) m = fmaxf(m, S.part_m[(int64_t)w * D.H + h]);
+        float acc = 0.f;
+        for (int w = w0; w < w1; ++w) {
+            const float mw = S.part_m[(int64_t)w * D.H + h];
+            acc += S.part_o[((int64_t)w * D.H + h) * D.dph + o % D.dph] * exp2f(mw - m);
+        }
+        xo[o] = ok ? acc : 0.f;
+    }
+    for (int h = tid; h < D.H; h += blockDim.x) {
+        float m = -INFINITY;
+        for (int w = w0; w < w1; ++w) m = fmaxf(m, S.part_m[(int64_t)w * D.H + h]);
+        float l = 0.f;
+        for (int w = w0; w < w1; ++w)
+            l += S.part_l[(int64_t)w * D.H + h] * exp2f(S.part_m[(int64_t)w * D.H + h] - m);
+        xm[h] = ok ? m : -INFINITY;
+        xl[h] = ok ? l : 0.f;
+    }
+    if (tid < D.k) xf[tid] = S.found[(int64_t)s * D.k + tid];
+    if (tid == 0) {
+        int nev = S.n_ow[s], pb = 0, pa = 0;
+        for (int gl = 0; gl < D.Gl; ++gl) {
+            nev += S.n_ev[s * D.Gl + gl];
+            pb += S.pages_before[s * D.Gl + gl];
+            pa += S.pages_after[s * D.Gl + gl];
+        }
+        xs[0] = S.summary[s].n_attended;
+        xs[1] = nev;
+        xs[2] = pb;
+        xs[3] = pa;
+    }
+}
+
+void launch_combine(const Dims& D, const State& S, const ExchangeLayout& X, cudaStream_t st) {
+    k_combine<<<D.B, 256, 0, st>>>(D, S, X);
+}
+
+// ===========================================================================
+// finish: cross-rank merge, fold-back, feedback
+// ===========================================================================
+
+// ===========================================================================
+// finish: cross-rank merge -> y, global (m, l), summary
+// ===========================================================================
+__global__ void k_finish_merge(Dims D, Cfg C, State S, ExchangeLayout X,
+                               const uint8_t* __restrict__ gathered, float* __restrict__ y) {
+    const int s = blockIdx.x, tid = threadIdx.x;
+    const int64_t stride_rank = (int64_t)D.B * X.bytes_per_stream;
+    for (int o = tid; o < D.H * D.dph; o += blockDim.x) {
+        const int h = o / D.dph;
+        float M = -INFINITY;
+        for (int r = 0; r < D.world; ++r) {
+            const uint8_t* rec = gathered + r * stride_rank + (int64_t)s * X.bytes_per_stream;
+            M = fmaxf(M, ((const float*)(rec + X.m_off))[h]);
+        }
+        float L = 0.f, acc = 0.f;
+        if (M != -INFINITY) {
+            for (int r = 0; r < D.world; ++r) {
+                const uint8_t* rec = gathered + r * stride_rank + (int64_t)s * X.bytes_per_stream;
+                const float mr = ((const float*)(rec + X.m_off))[h];
+                if (mr == -INFINITY) continue;
+                const float f = exp2f(mr - M);
+                L += ((const float*)(rec + X.l_off))[h] * f;
+                acc += ((const float*)(rec + X.o_off))[o] * f;
+            }
+        }
+        if (y && !S.err[s]) y[(int64_t)s * D.dp + o] = L > 0.f ? acc / L : 0.f;  // empty -> 0
+        if (o % D.dph == 0) {
+            S.gM[s * D.H + h] = M;
+            S.gL[s * D.H + h] = L;
+        }
+    }
+    if (tid == 0) {
+        int n_att = 0, nev = 0, pb = 0, pa = 0, hits = 0;
+        for (int j = 0; j < D.k; ++j) {
+            int f = 0;
+            for (int r = 0; r < D.world; ++r) {
+                const uint8_t* rec = gathered + r * stride_rank + (int64_t)s * X.bytes_per_stream;
+                f += ((const int32_t*)(rec + X.found_off))[j];
+            }
+            S.found[(int64_t)s * D.k + j] = f;  // global per-expert hit counts
+            hits += f > 0;
+        }
+        for (int r = 0; r < D.world; ++r) {
+            const int32_t* xs = (const int32_t*)(gathered + r * stride_rank +
+                                                 (int64_t)s * X.bytes_per_stream + X.stats_off);
+            n_att += xs[0], nev += xs[1], pb += xs[2], pa += xs[3];
+        }
+        pikv_step_summary& sm = S.summary[s];
+        sm.step = S.now[s];
+        sm.inserts = D.k;
+        sm.lookups = D.k;
+        sm.hits = hits;
+        sm.n_attended = n_att;
+        // pipeline.cpp:262-264, 22-26
+        const int hw = C.head_width < D.dp ? C.head_width : D.dp;
+        sm.fetch_elements = (int64_t)n_att * (int64_t)(2 * hw + D.dp);
+        sm.n_evictions = nev;
+        sm.pages_before = pb;
+        sm.pages_after = pa;
+        sm.error = S.err[s];
+    }
+}
+
+// attn_mass += alpha, pipeline.cpp:302-312; alpha = mean over heads.
+__global__ void k_foldback(Dims D, State S) {
+    __shared__ int64_t sm_base[1025];
+    const int nb = D.B + 1;
+    for (int i = threadIdx.x; i < nb && i < 1025; i += blockDim.x) sm_base[i] = S.att_base[i];
+    __syncthreads();
+    const int64_t N = sm_base[D.B < 1024 ? D.B : 1024];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int lo = 0, hi = D.B;  // stream: last s with base[s] <= i
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (sm_base[mid] <= i) lo = mid; else hi = mid;
+        }
+        const int s = lo;
+        if (S.err[s]) continue;
+        double a = 0.0;
+        const float* sc = S.scores + i * D.H;
+        for (int h = 0; h < D.H; ++h) {
+            const float L = S.gL[s * D.H + h];
+            if (L > 0.f) a += (double)(exp2f(sc[h] - S.gM[s * D.H + h]) / L);
+        }
+        a /= (double)D.H;
+        const int64_t gi = S.att_slot[i];
+        S.attn_mass[gi] += a;
+        if (D.n_layers > 0) S.per_layer[gi * D.n_layers + (int64_t)(S.now[s] % (uint64_t)D.n_layers)] += a;
+    }
+}
+
+// pipeline.cpp:258 (record_miss), 337-347 (adapt, observe_hits,
+// adakv_update); scheduler state.step++ (scheduler.cpp:328); now++.
+__global__ void k_feedback(Dims D, Cfg C, State S) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= D.B || S.err[s]) return;
+    const int k = D.k, E = D.E;
+    int hits = 0;
+    for (int j = 0; j < k; ++j) {
+        if (S.found[(int64_t)s * k + j] > 0) ++hits;
+        else S.miss[(int64_t)s * E + S.experts[(int64_t)s * k + j]] += 1;
+    }
+    const double reward = __ddiv_rn((double)hits, (double)k);
+    if (C.router_strategy == PIKV_ROUTER_ADAPTIVE) {  // adapt, router.cpp:243-255
+        double* bias = S.bias + (int64_t)s * E;
+        double acc = 0.0;
+        for (int e = 0; e < E; ++e) acc = __dadd_rn(acc, bias[e]);
+        const double mean = __ddiv_rn(acc, (double)E);
+        for (int j = 0; j < k; ++j) {
+            const int e = S.experts[(int64_t)s * k + j];
+            double b = __dadd_rn(bias[e], __dmul_rn(C.bandit_step, __dsub_rn(reward, mean)));
+            bias[e] = b < -C.bias_cap ? -C.bias_cap : (C.bias_cap < b ? C.bias_cap : b);
+        }
+    }
+    // observe_hits, scheduler.cpp:332-338
+    S.running_hit[s] = __dadd_rn(__dmul_rn(C.hit_decay, S.running_hit[s]),
+                                 __dmul_rn(__dsub_rn(1.0, C.hit_decay), reward));
+    if (C.sched_strategy == PIKV_SCHED_ADAKV && !C.unbounded_budget)  // :340-342
+        S.theta[s] = __dadd_rn(S.theta[s], __dmul_rn(C.adakv_step, __dsub_rn(C.target_hit, S.running_hit[s])));
+    if (!C.unbounded_budget) S.sstep[s] += 1;
+    S.now[s] += 1;
+}
+
+void launch_finish(const Dims& D, const Cfg& C, const State& S, const ExchangeLayout& X,
+                   const uint8_t* gathered, float* y, int attend, cudaStream_t st) {
+    k_finish_merge<<<D.B, 256, 0, st>>>(D, C, S, X, gathered, y);
+    if (attend) k_foldback<<<D.attend_ctas * 2, 256, 0, st>>>(D, S);
+    k_feedback<<<(D.B + 127) / 128, 128, 0, st>>>(D, C, S);
+}
+
+// ===========================================================================
+// synthetic inputs: N(0,1) from a counter hash, rounded to kv_dtype
+// ===========================================================================
+__host__ __device__ __forceinline__ uint64_t splitmix(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+
+__global__ void k_synth(int64_t n, int dtype, void* __restrict__ out, uint64_t seed) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t h = splitmix(seed ^ splitmix((uint64_t)i));
+        const float u1 = ((float)(h >> 40) + 1.0f) * (1.0f / 16777217.0f);
+        const float u2 = (float)((h >> 16) & 0xffffff) * (1.0f / 16777216.0f);
+        const float z = sqrtf(-2.0f * logf(u1)) * cospif(2.0f * u2);
+        if (dtype == PIKV_DTYPE_BF16) ((uint16_t*)out)[i] = f32_to_bf16_rne(z);
+        else ((float*)out)[i] = z;
+    }
+}
+
+void launch_synth(const Dims& D, void* q, void* k, void* v, uint64_t seed, uint64_t step,
+                  cudaStream_t st) {
+    const int64_t n = (int64_t)D.B * D.d;
+    const uint64_t base = splitmix(seed) ^ (step * 0x632be59bd9b4e019ull);
+    k_synth<<<256, 256, 0, st>>>(n, D.kv_dtype, q, base ^ 0x1111);
+    k_synth<<<256, 256, 0, st>>>(n, D.kv_dtype, k, base ^ 0x2222);
+    k_synth<<<256, 256, 0, st>>>(n, D.kv_dtype, v, base ^ 0x3333);
+}
+
+}  // namespace pikv_dev

@@ -1,0 +1,239 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Device-side state and helpers of the B200 PiKV engine.
+//
+// HBM layout (per GPU = per rank):
+//   * stores: B streams x G_local logical devices x SPD shards; each shard is
+//     a ring of S slots (kvstore.hpp:31-61).  ring index
+//     r = (stream * G_local + g_local) * SPD + shard, slot index r * S + slot.
+//     Slot metadata is SoA (id, shard_seq, token, expert, insert_step,
+//     last_access, freq, attn_mass, per_layer[n_layers]); id 0 = empty.
+//   * KV payload: a paged pool shared by all streams.  A ring's slot range
+//     [p*spg, (p+1)*spg) maps through page_table[r][p] to a pool page of spg
+//     entries; pages are taken on first write and returned when their last
+//     live entry is erased, so HBM use follows live entries (kvstore.cpp:
+//     193-196's M = 2 d' elem live) instead of ring capacity.
+//   * entry = [K payload H*dph][V payload H*dph][K scales H][V scales H]
+//     (scales only for INT8/INT4), padded to 16 B so one cp.async.bulk moves
+//     it; payload element = bf16 / f32 / int8 / packed int4.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/pikv_b200.h"
+
+namespace pikv_dev {
+
+constexpr int kMaxK = 64;
+constexpr int kMaxE = 256;
+
+struct EvictRec {  // == pikv_evict_record
+    uint64_t step;
+    uint64_t entry_id;
+    int64_t token_id;
+    int32_t expert_id;
+    int32_t device;
+    double score;
+    int32_t reason;
+    int32_t stream;
+};
+static_assert(sizeof(EvictRec) == sizeof(pikv_evict_record), "record layout");
+
+// Per-stream exchange record for the cross-rank merge (one per stream per
+// rank; world==1 uses it directly).  o is unnormalised w.r.t. m (base-2).
+struct ExchangeLayout {
+    int64_t o_off, m_off, l_off, found_off, stats_off, bytes_per_stream;
+};
+
+struct Dims {
+    int B, Gl, SPD, R, S, H, dph, dp, d, E, k, n_layers;
+    int G, world, rank;
+    int spg, ppr;            // storage page entries, pages per ring
+    int entry_bytes, payload_bytes, elem_bits;
+    int codec, kv_dtype;
+    int n_tok, n_exp, additive;
+    int page_size, ppr_sched;  // scheduler pages per ring (candidates)
+    int max_cand, nch, chunk_slots;  // retrieval grid
+    int sel_stride;                  // pow2 >= SPD * ppr_sched
+    int64_t pool_entries, pool_pages, att_cap, item_cap;
+    int attend_ctas;
+};
+
+struct Cfg {  // scalar config needed on device (copied by value into kernels)
+    int router_strategy, groups, stride;
+    double alpha, lambda_miss, beta_ent, bandit_step, bias_cap, load_decay;
+    int sched_strategy, budget_pages, page_size, sink, flex_bucket, n_adakv_weights, n_flex_plan;
+    double tau, lambda_freq, adakv_step, target_hit, theta0, hit_decay;
+    double adakv_weights[8];
+    double flex_plan[32];
+    int unbounded_budget, head_width;
+};
+
+struct State {
+    // router (router.hpp:41-56), per stream
+    const double* W;  // E x d, shared by all streams (same seed)
+    double* load;
+    uint64_t* usage;
+    uint64_t* total_usage;
+    uint64_t* miss;
+    double* bias;
+    uint64_t* rstep;
+    // scheduler (scheduler.hpp:49-56), per stream
+    double* theta;
+    double* running_hit;
+    uint64_t* sstep;
+    // engine
+    uint64_t* now;      // per stream
+    uint64_t* next_id;  // per stream (KVStore::next_id_)
+    int32_t* err;       // per stream
+    uint64_t* st_inserts;
+    uint64_t* st_overwrites;
+    // rings
+    int32_t* head;
+    int32_t* live;
+    uint64_t* seq;
+    int32_t* page_table;  // [B*R][ppr]
+    // slots
+    uint64_t* id;
+    uint64_t* shard_seq;
+    int64_t* token;
+    int32_t* expert;
+    uint64_t* insert_step;
+    uint64_t* last_access;
+    uint64_t* freq;
+    double* attn_mass;
+    double* per_layer;
+    // pool
+    uint8_t* pool;
+    int32_t* page_live;
+    int32_t* free_stack;
+    int32_t* free_top;
+    // codec params
+    const float* basis;  // [H][r][hd]
+    const float* cbias;  // [d]
+    const int32_t* kept; // [H][r]
+    // step scratch
+    int32_t* experts;  // [B][k]
+    double* gates;     // [B][k]
+    double* logits;    // [B][E]
+    float* q_attn;     // [B][dp]
+    int32_t* cand;     // [B][max_cand] local ring ids
+    int32_t* ncand;    // [B]
+    EvictRec* rec_ow;  // [B][k]
+    int32_t* n_ow;     // [B]
+    EvictRec* rec_ev;  // [B*Gl][SPD*S]
+    int32_t* n_ev;     // [B*Gl]
+    int32_t* pages_before;  // [B*Gl]
+    int32_t* pages_after;   // [B*Gl]
+    double* pg_agg;         // [B*R][ppr_sched]
+    uint64_t* pg_oldest;
+    int32_t* pg_cnt;
+    int32_t* sel_idx;       // [B*Gl][R_dev*ppr_sched] scratch for selection
+    int32_t* chunk_cnt;     // [B][max_cand][nch]
+    int32_t* chunk_off;     // same, exclusive within stream
+    int32_t* found;         // [B][k]
+    int64_t* att_base;      // [B+1]
+    int32_t* att_slot;      // [att_cap] global slot index (ring*S+slot)
+    int32_t* att_entry;     // [att_cap] pool entry index
+    float* scores;          // [att_cap][H]  (base-2 logits)
+    int32_t* item_stream;   // [item_cap]
+    int32_t* item_begin;
+    int32_t* item_end;
+    int32_t* n_items;       // [1]
+    float* part_m;          // [item_cap][H]
+    float* part_l;
+    float* part_o;          // [item_cap][H][dph]
+    uint8_t* exchange;      // [B][bytes_per_stream]
+    float* gM;              // [B][H] global max (base 2)
+    float* gL;              // [B][H]
+    pikv_step_summary* summary;  // [B]
+};
+
+// ---- helpers -------------------------------------------------------------
+__device__ __forceinline__ int shard_raw(int64_t t, int e, int n_tok, int n_exp, int additive) {
+    int lhs = (int)(t % n_tok);
+    int rhs = e % n_exp;
+    return additive ? lhs + rhs : (lhs ^ rhs);
+}
+
+// Does local ring (g_local, shard) possibly hold expert e?  Under xor mode
+// raw = (t mod n_tok) ^ (e mod n_exp) for some t  <=>  raw ^ (e mod n_exp) < n_tok.
+__device__ __forceinline__ bool ring_can_hold(int raw, int e, int n_tok, int n_exp, int additive) {
+    int rhs = e % n_exp;
+    int lhs = additive ? raw - rhs : (raw ^ rhs);
+    return lhs >= 0 && lhs < n_tok;
+}
+
+__device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+
+__device__ __forceinline__ uint16_t f32_to_bf16_rne(float f) {
+    uint32_t u = __float_as_uint(f);
+    if ((u & 0x7f800000u) != 0x7f800000u) u += 0x7fffu + ((u >> 16) & 1u);
+    return (uint16_t)(u >> 16);
+}
+
+// Orderable 64-bit key of a double (ascending numeric order; no NaNs here).
+__device__ __forceinline__ uint64_t dkey(double x) {
+    uint64_t u = (uint64_t)__double_as_longlong(x);
+    return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+}
+
+// score_entry, scheduler.cpp:181-229 (QUEST rejected at create).
+__device__ __forceinline__ double score_entry(const Cfg& c, const State& st, int64_t gi,
+                                              uint64_t now, int n_layers) {
+    uint64_t ins = st.insert_step[gi], la = st.last_access[gi];
+    uint64_t age = now >= ins ? now - ins : 0;
+    uint64_t rec = now >= la ? now - la : 0;
+    switch (c.sched_strategy) {
+        case PIKV_SCHED_H2O:
+            return st.attn_mass[gi];
+        case PIKV_SCHED_SL: {
+            double u = (double)age <= c.tau ? 1.0 : 0.0;
+            if (st.token[gi] < c.sink) u = __dadd_rn(u, 2.0);
+            return u;
+        }
+        case PIKV_SCHED_FLEX: {
+            uint64_t bucket = age / (uint64_t)c.flex_bucket;
+            if (bucket >= (uint64_t)c.n_flex_plan) bucket = (uint64_t)c.n_flex_plan - 1;
+            return c.flex_plan[bucket];
+        }
+        case PIKV_SCHED_LRU:
+            return -(double)rec;
+        case PIKV_SCHED_LRU_PLUS:
+            return __dadd_rn(-(double)rec, __dmul_rn(c.lambda_freq, (double)st.freq[gi]));
+        case PIKV_SCHED_ADAKV: {
+            double phi0 = st.attn_mass[gi], phi1 = (double)st.freq[gi];
+            double phi2 = __ddiv_rn(1.0, __dadd_rn(1.0, (double)age));
+            double u = 0.0;
+            if (c.n_adakv_weights > 0) u = __dadd_rn(u, __dmul_rn(c.adakv_weights[0], phi0));
+            if (c.n_adakv_weights > 1) u = __dadd_rn(u, __dmul_rn(c.adakv_weights[1], phi1));
+            if (c.n_adakv_weights > 2) u = __dadd_rn(u, __dmul_rn(c.adakv_weights[2], phi2));
+            return u;
+        }
+        case PIKV_SCHED_DUO: {
+            double u = 0.0;
+            const double* pl = st.per_layer + gi * (int64_t)n_layers;
+            for (int l = 0; l < n_layers; ++l) u = __dadd_rn(u, pl[l]);
+            return u;
+        }
+    }
+    return 0.0;
+}
+
+// ---- launch wrappers (defined in the .cu files) ----------------------------
+void launch_route(const Dims& D, const Cfg& C, const State& S, const void* q, cudaStream_t st);
+void launch_insert(const Dims& D, const Cfg& C, const State& S, const void* k, const void* v,
+                   const double* saliency, cudaStream_t st);
+void launch_sched(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);
+void launch_retrieve(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);
+void launch_attend(const Dims& D, const State& S, cudaStream_t st);
+void launch_combine(const Dims& D, const State& S, const ExchangeLayout& X, cudaStream_t st);
+void launch_finish(const Dims& D, const Cfg& C, const State& S, const ExchangeLayout& X,
+                   const uint8_t* gathered, float* y, int attend, cudaStream_t st);
+void launch_synth(const Dims& D, void* q, void* k, void* v, uint64_t seed, uint64_t step,
+                  cudaStream_t st);
+int attend_max_smem();
+
+}  // namespace pikv_dev

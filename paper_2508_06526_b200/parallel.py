@@ -1,0 +1,76 @@
+# SPDX-License-Identifier: Apache-2.0
+"""Multi-rank decode step: experts sharded over ranks, partial softmax states
+merged across ranks.
+
+Placement follows the reference's own shard_assign (kvstore.cpp:14-30): with
+G logical devices and G ranks, device g lives on rank g.  Routing is
+replicated (W_r is identical on every rank), each rank inserts, evicts
+(budgets are per device, scheduler.cpp:269) and attends only over its own
+shards, and the one real exchange of the path is the log-sum-exp merge
+(SURVEY §8 a14/e): every rank all-gathers the per-stream exchange records
+(m, l, o[H][d'h], per-expert hit counts, step counters) and finishes the
+step locally (global y, global (m, l) for the alpha fold-back, misses).
+
+The collective is NCCL over NVLink on GPUs; the same code runs over gloo on
+CPU tensors for the multi-process tests.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+class _DevBuf:
+    """Zero-copy torch view of an engine-owned device buffer."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+def device_view(ptr: int, nbytes: int) -> torch.Tensor:
+    return torch.as_tensor(_DevBuf(ptr, nbytes), device="cuda")
+
+
+def all_gather_bytes(out: torch.Tensor, local: torch.Tensor, group=None):
+    """out[r * n:(r+1) * n] = local of rank r."""
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, local, group=group)
+    else:
+        n = local.numel()
+        parts = [out[r * n:(r + 1) * n] for r in range(dist.get_world_size(group))]
+        dist.all_gather(parts, local, group=group)
+    return out
+
+
+class ShardedStepper:
+    """Drive one rank's engine through the sharded step:
+    step_local -> all-gather(exchange) -> step_finish.
+
+    ``engine`` provides exchange_bytes(), step_local(q, k, v, saliency) -> ptr
+    or tensor, step_finish(gathered, y) and external_stream() (or None)."""
+
+    def __init__(self, engine, group=None):
+        self.eng = engine
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.nbytes = engine.exchange_bytes()
+        dev = "cuda" if torch.cuda.is_available() and dist.get_backend(group) == "nccl" else "cpu"
+        self.gathered = torch.empty(self.world * self.nbytes, dtype=torch.uint8, device=dev)
+
+    def step(self, q, k, v, y=None, saliency=None):
+        es = self.eng.external_stream()
+        if es is not None:
+            es.wait_stream(torch.cuda.current_stream())
+        local = self.eng.step_local(q, k, v, saliency)
+        if isinstance(local, int):
+            local = device_view(local, self.nbytes)
+        if es is not None:
+            with torch.cuda.stream(es):
+                all_gather_bytes(self.gathered, local, self.group)
+        else:
+            all_gather_bytes(self.gathered, local, self.group)
+        y = self.eng.step_finish(self.gathered, y)
+        if es is not None:
+            torch.cuda.current_stream().wait_stream(es)
+        return y

@@ -1,0 +1,225 @@
+# SPDX-License-Identifier: Apache-2.0
+"""GPU parity: the CUDA engine (through the C-ABI) against the CPU oracle.
+
+Per step and per stream:
+  * bit-exact: experts (routing), hits/lookups, n_attended, fetch_elements,
+    pages_before/after, every eviction record (step, id, token, expert,
+    device, score, reason) in reference order, the attended (token, expert)
+    set, and the slot metadata (ids, shard_seq, token, expert, insert/last
+    access steps, freq);
+  * tolerance (stated here): gates |rel| <= 1e-12 (CUDA vs glibc exp);
+    attention output rel-L2 <= 2e-5 (fp32 accumulation vs the fp64
+    reference on identically rounded inputs); alpha / attn_mass increments
+    |abs| <= 1e-6 + 1e-4 |rel|.
+H2O/AdaKV/Duo score entries by the fold-back attn_mass, so before every step
+the oracle's attn_mass/per_layer are injected into the engine (SURVEY §8 c:
+"step-local on injected identical state"); eviction is then bit-exact too.
+"""
+import numpy as np
+import pytest
+
+from cases import ROUTERS, SCHEDS, engine_config
+from oracle_bind import OracleEngine, make_stream
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2508_06526_b200.engine import Engine  # noqa: E402
+
+Y_TOL = 2e-5
+
+
+def to_kv(x, dtype):
+    if dtype == "f32":
+        return np.ascontiguousarray(x, dtype=np.float32)
+    f = np.ascontiguousarray(x, dtype=np.float32)
+    return (f.view(np.uint32) >> 16).astype(np.uint16)
+
+
+def rel_l2(a, b):
+    n = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (n if n > 0 else 1.0)
+
+
+def run_parity(cfg, T, seed, inject=True, basis=None, bias=None, kept=None, check_slots=True,
+               mutate=None):
+    B = cfg.batch
+    eng = Engine(cfg)
+    if basis is not None or bias is not None or kept is not None:
+        eng.set_codec(basis, bias, kept)
+    ob = None if basis is None else np.asarray(basis, dtype=np.float64)
+    orc = [OracleEngine(cfg, basis=ob, bias=bias, kept=kept) for _ in range(B)]
+    streams = [make_stream(T, cfg.model.d, seed + 1000 * s, cfg.kv_dtype, cfg.n_layers)
+               for s in range(B)]
+    for t in range(T):
+        if mutate is not None:
+            mutate(t, orc)
+        if inject:
+            for s in range(B):
+                st = orc[s].slots()
+                eng.set_attn_mass(s, st["attn_mass"], st["per_layer"] if cfg.n_layers else None)
+        q = np.stack([streams[s][0][t] for s in range(B)])
+        k = np.stack([streams[s][1][t] for s in range(B)])
+        v = np.stack([streams[s][2][t] for s in range(B)])
+        sal = None if cfg.n_layers == 0 else np.stack([streams[s][3][t] for s in range(B)])
+        before = [eng.slots(s)["attn_mass"] for s in range(B)] if inject else None
+        y = eng.step_host(to_kv(q, cfg.kv_dtype), to_kv(k, cfg.kv_dtype), to_kv(v, cfg.kv_dtype),
+                          sal)
+        experts, gates, logits, summ = eng.read_step()
+        evs = eng.read_evictions()
+        for s in range(B):
+            r = orc[s].step(q[s], k[s], v[s], None if sal is None else sal[s])
+            ctx = (t, s)
+            assert summ[s]["error"] == 0, ctx
+            assert experts[s].tolist() == r["experts"], ctx
+            assert np.allclose(gates[s], r["gates"], rtol=1e-12, atol=0), ctx
+            assert summ[s]["hits"] == r["hits"] and summ[s]["lookups"] == r["lookups"], ctx
+            assert summ[s]["n_attended"] == r["n_attended"], ctx
+            assert summ[s]["fetch_elements"] == r["fetch_elements"], ctx
+            if not cfg.unbounded_budget:
+                assert (summ[s]["pages_before"], summ[s]["pages_after"]) == (
+                    r["pages_before"], r["pages_after"]), ctx
+            mine = [(e.step, e.entry_id, e.token_id, e.expert_id, e.device, e.score,
+                     {"budget": 0, "threshold": 1, "overwrite": 2}[e.reason])
+                    for e in evs if e.stream == s]
+            assert mine == r["evictions"], ctx
+            assert rel_l2(y[s].astype(np.float64), r["y"]) <= Y_TOL, (ctx, rel_l2(y[s], r["y"]))
+            tok, ex, al = eng.read_attended(s)
+            order = np.lexsort((ex, tok))
+            assert np.array_equal(tok[order], r["att_token"]), ctx
+            assert np.array_equal(ex[order], r["att_expert"]), ctx
+            assert np.allclose(al[order], r["att_weight"], rtol=1e-4, atol=1e-6), ctx
+            if inject and r["n_attended"]:  # fold-back: attn_mass gains alpha
+                gain = eng.slots(s)["attn_mass"] - before[s]
+                assert np.isclose(gain.sum(), 1.0, atol=1e-5), ctx
+    if check_slots:
+        for s in range(B):
+            a, b = eng.slots(s), orc[s].slots()
+            assert np.array_equal(a["id"], b["id"])
+            live = a["id"] != 0
+            for key in ("shard_seq", "token", "expert", "insert_step", "last_access", "freq"):
+                assert np.array_equal(a[key][live], b[key][live]), key
+            assert np.allclose(a["attn_mass"][live], b["attn_mass"][live], rtol=1e-4, atol=1e-6)
+            ra, rb = eng.router_state(s), orc[s].router_state()
+            assert np.array_equal(ra["usage"], rb["usage"]) and np.array_equal(ra["miss"], rb["miss"])
+            assert np.allclose(ra["load"], rb["load"], rtol=1e-14, atol=0)
+            assert ra["step"] == rb["step"] and ra["total_usage"] == rb["total_usage"]
+            sa, sb = eng.scheduler_state(s), orc[s].sched_state()
+            assert sa["step"] == sb["step"]
+            assert sa["running_hit"] == sb["running_hit"] and sa["theta"] == sb["theta"]
+            st_a, st_b = eng.store_stats(s), orc[s].store_stats()
+            assert st_a == st_b
+    return eng, orc
+
+
+@pytest.mark.parametrize("router", ROUTERS)
+def test_engine_lossless_all_routers(router):
+    """test_pipeline.cpp:170-192 analogue: unbounded store, every router."""
+    cfg = engine_config(router=router, unbounded=True, S=256, batch=3)
+    run_parity(cfg, 60, 13)
+
+
+@pytest.mark.parametrize("sched", SCHEDS)
+def test_engine_bounded_all_schedulers(sched):
+    cfg = engine_config(router="TopK", sched=sched, batch=2, H=2)
+    run_parity(cfg, 70, 19)
+
+
+@pytest.mark.parametrize("router,sched,kw", [
+    ("LoadBalanced", "H2O", dict(S=8, budget=16)),                 # ring overwrites
+    ("CacheAware", "AdaKV", dict(theta0=0.5)),                      # threshold evict-all
+    ("Adaptive", "LRU", dict(S=10, ps=4, budget=3)),               # pages wrap the ring end
+    ("EntropyLB", "SL", dict(G=1, n_tok=1, n_exp=8)),              # pure expert sharding
+    ("Hierarchical", "Flex", dict(G=4, n_tok=4, n_exp=8, E=16, k=4)),
+    ("TopK", "LRUPlus", dict(G=2, n_tok=1, n_exp=4, E=8, k=2)),    # E > n_exp: shared shards
+    ("Base", "Duo", dict(n_layers=5)),
+    ("TopK", "LRU", dict(budget=1, ps=1)),                          # page_size 1
+])
+def test_engine_edge_configs(router, sched, kw):
+    cfg = engine_config(router=router, sched=sched, batch=2, **kw)
+    run_parity(cfg, 60, 29)
+
+
+def test_engine_large_victim_cut_uses_sort_path():
+    """A threshold cut of > 32 pages at once exercises the bitonic select
+    path (V <= 32 uses block argmin rounds)."""
+    cfg = engine_config(router="TopK", sched="AdaKV", S=512, G=1, n_tok=1, n_exp=8, ps=1,
+                        budget=100000, batch=2, theta0=0.0)
+    cfg.scheduler.adakv_step = 0.0
+    cfg.scheduler.adakv_weights = [1.0]
+
+    def mutate(t, orc):
+        if t in (40, 70):
+            for o in orc:
+                st = o.slots()
+                m = st["attn_mass"].copy()
+                live = np.flatnonzero(st["id"] != 0)
+                m[live[::2]] = -1.0  # half the pages drop below theta
+                o.set_attn_mass(m)
+
+    run_parity(cfg, 90, 5, mutate=mutate)
+
+
+def test_engine_bf16_multihead():
+    cfg = engine_config(router="TopK", sched="H2O", d=256, H=4, S=128, batch=3, dtype="bf16")
+    run_parity(cfg, 40, 7)
+
+
+@pytest.mark.parametrize("codec,rank", [("Int8", 8), ("Int4", 8), ("LowRank", 8), ("LoRAPlus", 8),
+                                        ("FastV", 8), ("Prune", 8)])
+def test_engine_codecs(codec, rank):
+    d, H = 128, 2
+    hd = d // H
+    cfg = engine_config(router="TopK", sched="LRU", d=d, H=H, S=64, batch=2, codec=codec,
+                        rank=rank if codec not in ("Int8", "Int4") else 8)
+    rng = np.random.default_rng(3)
+    basis = bias = kept = None
+    if codec in ("LowRank", "LoRAPlus"):
+        basis = np.linalg.qr(rng.standard_normal((hd, hd)))[0][:, :rank].T[None].repeat(H, 0)
+        basis = np.ascontiguousarray(basis, dtype=np.float32)
+        if codec == "LoRAPlus":
+            bias = (0.1 * rng.standard_normal(d)).astype(np.float32)
+    if codec == "Prune":
+        kept = np.stack([np.sort(rng.choice(hd, rank, replace=False)) for _ in range(H)]).astype(np.int32)
+    run_parity(cfg, 40, 3, basis=basis, bias=None if bias is None else bias.astype(np.float64),
+               kept=kept, check_slots=True)
+
+
+def test_engine_error_leaves_no_partial_state():
+    """test_pipeline.cpp:138-152: a NaN query raises NumericalError, no mutation."""
+    from paper_2508_06526_b200.engine import PikvError
+    cfg = engine_config(router="TopK", unbounded=True, S=64, batch=1)
+    eng = Engine(cfg)
+    q, k, v, sal = make_stream(2, 16, 5, n_layers=3)
+    eng.step_host(to_kv(q[:1], "f32"), to_kv(k[:1], "f32"), to_kv(v[:1], "f32"), sal[:1])
+    live = eng.store_stats(0)["live"]
+    bad = q[1:2].copy()
+    bad[0, 3] = np.nan
+    eng.step_host(to_kv(bad, "f32"), to_kv(k[1:2], "f32"), to_kv(v[1:2], "f32"), sal[1:2])
+    with pytest.raises(PikvError) as ei:
+        eng.sync()
+    assert ei.value.kind == "NumericalError"
+    assert eng.store_stats(0)["live"] == live
+
+
+def test_prefill_then_step_graph_replay():
+    """Synthetic prefill (no attention) then graph-replayed steps stay sane."""
+    cfg = engine_config(router="TopK", sched="LRU", d=512, H=4, S=2048, G=1, n_tok=1, n_exp=16,
+                        E=16, k=2, batch=4, dtype="bf16", budget=100000, ps=16, n_layers=0)
+    eng = Engine(cfg)
+    eng.prefill_synthetic(1000, seed=3)
+    for s in range(4):
+        assert eng.store_stats(s)["live"] == 2000
+    q = torch.empty(4, 512, dtype=torch.bfloat16, device="cuda")
+    k, v = torch.empty_like(q), torch.empty_like(q)
+    for i in range(5):
+        eng.fill_synthetic(q, k, v, seed=100 + i)
+        y = eng.step(q, k, v)
+    eng.sync()
+    _, _, _, summ = eng.read_step()
+    for s in range(4):
+        assert summ[s]["error"] == 0 and summ[s]["n_attended"] > 0
+    assert torch.isfinite(y).all()
