@@ -65,7 +65,7 @@ def run_parity(cfg, T, seed, inject=True, basis=None, bias=None, kept=None, chec
         k = np.stack([streams[s][1][t] for s in range(B)])
         v = np.stack([streams[s][2][t] for s in range(B)])
         sal = None if cfg.n_layers == 0 else np.stack([streams[s][3][t] for s in range(B)])
-        before = [eng.slots(s)["attn_mass"] for s in range(B)] if inject else None
+        before = [eng.slots(s) for s in range(B)] if inject else None
         y = eng.step_host(to_kv(q, cfg.kv_dtype), to_kv(k, cfg.kv_dtype), to_kv(v, cfg.kv_dtype),
                           sal)
         experts, gates, logits, summ = eng.read_step()
@@ -93,7 +93,9 @@ def run_parity(cfg, T, seed, inject=True, basis=None, bias=None, kept=None, chec
             assert np.array_equal(ex[order], r["att_expert"]), ctx
             assert np.allclose(al[order], r["att_weight"], rtol=1e-4, atol=1e-6), ctx
             if inject and r["n_attended"]:  # fold-back: attn_mass gains alpha
-                gain = eng.slots(s)["attn_mass"] - before[s]
+                after = eng.slots(s)
+                same = (after["id"] == before[s]["id"]) & (after["id"] != 0)
+                gain = after["attn_mass"][same] - before[s]["attn_mass"][same]
                 assert np.isclose(gain.sum(), 1.0, atol=1e-5), ctx
     if check_slots:
         for s in range(B):
