@@ -93,13 +93,16 @@ def make_config(w, world=1, rank=0, G=None):
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region
+    (written to a file by nvidia-smi itself: piped output is block-buffered)."""
+
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index=0):
         self.index = index
-        self.samples = []
-        self._stop = threading.Event()
+        self.path = "/tmp/pikv_clocks_%d_%d.csv" % (os.getpid(), index)
         self._proc = None
+        self.samples = []
 
     def __enter__(self):
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -108,42 +111,50 @@ class ClockSampler:
         try:
             self._proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + q,
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._t = threading.Thread(target=self._read, daemon=True)
-            self._t.start()
+                 "--format=csv,noheader,nounits", "-lms", "100", "-f", self.path],
+                stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
         except Exception:
             self._proc = None
         return self
 
-    def _read(self):
-        for line in self._proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 8:
-                self.samples.append(parts)
-
     def __exit__(self, *a):
         if self._proc:
+            time.sleep(0.25)
             self._proc.terminate()
             try:
-                self._proc.wait(timeout=2)
+                self._proc.wait(timeout=3)
             except Exception:
                 self._proc.kill()
+            try:
+                with open(self.path) as f:
+                    for line in f:
+                        parts = [p.strip() for p in line.split(",")]
+                        if len(parts) >= 8:
+                            self.samples.append(parts)
+                os.unlink(self.path)
+            except OSError:
+                pass
 
     def summary(self):
-        if not self.samples:
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [v for v in (num(s[0]) for s in self.samples) if v is not None]
+        mx = [v for v in (num(s[1]) for s in self.samples) if v is not None]
+        if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
         for s in self.samples:
-            for n, v in zip(names, s[4:8]):
+            for n, v in zip(self.NAMES, s[4:8]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(self.samples)}
+        # under load: samples above half of max (the sampler brackets idle edges)
+        load = [v for v in sm if v >= 0.5 * max(mx)] or sm
+        return {"sm_mhz": float(np.median(load)), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
 
 
 def cpu_reference(w, steps, threads=None, prefill=None):
@@ -305,7 +316,7 @@ def main():
     _, _, _, summ = eng.read_step()
     att_last = sum(s["n_attended"] for s in summ)
 
-    # ---------------- attention kernel timing (events on the engine stream) ----
+    # ---------------- per-phase timing (CUDA events on the engine stream) ----
     eng.set_profiling(True)
     att_total = 0
     nprof = min(args.steps, 20)
@@ -313,14 +324,15 @@ def main():
         one_step(args.warmup + (i % args.steps))
         _, _, _, sm = eng.read_step()
         att_total += sum(s["n_attended"] for s in sm)
-    attend_ms, n_launch = eng.read_profile()
+    phases, n_launch = eng.read_profile()
     eng.set_profiling(False)
     entry_bytes = eng.entry_bytes()
-    # local attended entries on this rank (global n_attended is summed over ranks)
+    # KV bytes this rank's attention kernel must read (global count / ranks)
     alg_bytes = att_total * entry_bytes / max(world, 1)
-    attend_avg_ms = attend_ms / max(n_launch, 1)
+    attend_avg_ms = phases["attend"] / max(n_launch, 1)
     peak, peak_kind = load_peaks()
     achieved = alg_bytes / max(n_launch, 1) / (attend_avg_ms * 1e-3) / 1e9 if attend_avg_ms else 0.0
+    phase_avg = {k2: round(v / max(n_launch, 1), 4) for k2, v in phases.items()}
 
     # ---------------- end to end through host buffers ----------------
     e2e = None
@@ -371,6 +383,7 @@ def main():
                      "kernel": "k_attend (decode attention, TMA bulk ring)",
                      "peak_kind": peak_kind, "avg_launch_ms": attend_avg_ms,
                      "algorithmic_bytes_per_launch": alg_bytes / max(n_launch, 1)},
+        "phase_ms": phase_avg,
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "e2e": e2e,

@@ -272,10 +272,13 @@ int64_t pikv_pool_pages_in_use(pikv_engine* eng);
 int64_t pikv_entry_bytes(pikv_engine* eng);
 /* Launch statistics: number of kernels this engine enqueued so far. */
 int64_t pikv_kernel_launches(pikv_engine* eng);
-/* Per-kernel timing of the last step on the engine stream (CUDA events). */
+/* Profiling mode: steps run eagerly (no graph) with CUDA events on the engine
+ * stream between phases.  pikv_read_profile_host returns the summed ms of
+ * each phase over the profiled steps: [route, insert, sched, retrieve,
+ * attend, combine, finish] (n_phases <= 7) and resets the counters. */
 int pikv_set_profiling(pikv_engine* eng, int32_t on);
-int pikv_read_profile_host(pikv_engine* eng, float* attend_ms, float* step_ms,
-                           int64_t* attended_total);
+int pikv_read_profile_host(pikv_engine* eng, float* phase_ms, int32_t n_phases,
+                           int32_t* n_steps);
 
 #ifdef __cplusplus
 }

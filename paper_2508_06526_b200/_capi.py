@@ -77,8 +77,7 @@ SIGNATURES = {
     "pikv_entry_bytes": (c_i64, [c_vp]),
     "pikv_kernel_launches": (c_i64, [c_vp]),
     "pikv_set_profiling": (ctypes.c_int, [c_vp, c_i32]),
-    "pikv_read_profile_host": (ctypes.c_int, [c_vp, P(ctypes.c_float), P(ctypes.c_float),
-                                              P(c_i64)]),
+    "pikv_read_profile_host": (ctypes.c_int, [c_vp, c_vp, c_i32, P(c_i32)]),
 }
 
 _LIB = None

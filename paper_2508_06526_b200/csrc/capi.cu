@@ -106,12 +106,11 @@ struct pikv_engine {
     bool warmed = false;
     int64_t launches = 0;
     int kernels_per_step = 0;
-    // profiling
+    // profiling: per step kPhases+1 events on the engine stream
     bool profiling = false;
     std::vector<cudaEvent_t> ev;
-    int ev_used = 0;
-    cudaEvent_t step_ev[2]{};
-    int step_count_prof = 0;
+    int prof_steps = 0;
+    int cur = -1;  // event slot base of the step being enqueued
 
     template <class T>
     T* alloc(size_t n) {
@@ -546,7 +545,6 @@ int pikv_engine_destroy(pikv_engine* eng) {
     if (eng->stream) cudaStreamSynchronize(eng->stream);
     for (auto& kv : eng->graphs) cudaGraphExecDestroy(kv.second);
     for (auto e : eng->ev) cudaEventDestroy(e);
-    if (eng->step_ev[0]) cudaEventDestroy(eng->step_ev[0]), cudaEventDestroy(eng->step_ev[1]);
     for (void* p : eng->allocs) cudaFree(p);
     if (eng->stream) cudaStreamDestroy(eng->stream);
     delete eng;
@@ -592,6 +590,16 @@ static int codec_ready(pikv_engine* eng) {
     return PIKV_OK;
 }
 
+// Phases timed in profiling mode: route, insert, sched, retrieve, attend,
+// combine, finish (merge + fold-back + feedback).
+constexpr int kPhases = 7;
+constexpr int kProfSteps = 512;
+
+static void mark(pikv_engine* eng, int phase) {
+    if (eng->cur < 0) return;
+    cudaEventRecord(eng->ev[eng->cur + phase], eng->stream);
+}
+
 // The step's launch sequence (pipeline.cpp:213-351 ordering).
 static int enqueue_local(pikv_engine* eng, const void* q, const void* k, const void* v,
                          const double* sal, bool attend) {
@@ -599,21 +607,24 @@ static int enqueue_local(pikv_engine* eng, const void* q, const void* k, const v
     const State& S = eng->S;
     cudaStream_t st = eng->stream;
     int n = 0;
+    eng->cur = -1;
+    if (eng->profiling && eng->prof_steps < kProfSteps) eng->cur = eng->prof_steps++ * (kPhases + 1);
+    mark(eng, 0);
     CUDA_TRY(cudaMemsetAsync(S.n_ow, 0, sizeof(int32_t) * D.B, st));
     CUDA_TRY(cudaMemsetAsync(S.n_ev, 0, sizeof(int32_t) * D.B * std::max(D.Gl, 1), st));
     CUDA_TRY(cudaMemsetAsync(S.pages_before, 0, sizeof(int32_t) * D.B * std::max(D.Gl, 1), st));
     CUDA_TRY(cudaMemsetAsync(S.pages_after, 0, sizeof(int32_t) * D.B * std::max(D.Gl, 1), st));
     launch_route(D, eng->C, S, q, st), ++n;
+    mark(eng, 1);
     if (D.Gl > 0) {
         launch_insert(D, eng->C, S, k, v, sal, st), ++n;
+        mark(eng, 2);
         if (!eng->C.unbounded_budget) launch_sched(D, eng->C, S, st), n += 2;
+        mark(eng, 3);
         launch_retrieve(D, eng->C, S, st), n += 3;
-        if (attend) {
-            bool prof = eng->profiling && eng->ev_used + 2 <= (int)eng->ev.size();
-            if (prof) cudaEventRecord(eng->ev[eng->ev_used], st);
-            launch_attend(D, S, st), ++n;
-            if (prof) cudaEventRecord(eng->ev[eng->ev_used + 1], st), eng->ev_used += 2;
-        }
+        mark(eng, 4);
+        if (attend) launch_attend(D, S, st), ++n;
+        mark(eng, 5);
     } else {
         // a rank without devices still issues ids (k_insert does it) -- run
         // insert for the id counter only
@@ -621,6 +632,7 @@ static int enqueue_local(pikv_engine* eng, const void* q, const void* k, const v
         launch_retrieve(D, eng->C, S, st), n += 3;
     }
     launch_combine(D, S, eng->X, st), ++n;
+    mark(eng, 6);
     CUDA_TRY(cudaGetLastError());
     eng->kernels_per_step = n;
     return PIKV_OK;
@@ -628,6 +640,8 @@ static int enqueue_local(pikv_engine* eng, const void* q, const void* k, const v
 
 static int enqueue_finish(pikv_engine* eng, const uint8_t* gathered, float* y, bool attend) {
     launch_finish(eng->D, eng->C, eng->S, eng->X, gathered, y, attend ? 1 : 0, eng->stream);
+    mark(eng, 7);
+    eng->cur = -1;
     eng->kernels_per_step += attend ? 3 : 2;
     CUDA_TRY(cudaGetLastError());
     return PIKV_OK;
@@ -934,25 +948,27 @@ int64_t pikv_kernel_launches(pikv_engine* eng) { return eng->launches; }
 int pikv_set_profiling(pikv_engine* eng, int32_t on) {
     eng->profiling = on != 0;
     if (eng->profiling && eng->ev.empty()) {
-        eng->ev.resize(4096);
+        eng->ev.resize((size_t)kProfSteps * (kPhases + 1));
         for (auto& e : eng->ev) CUDA_TRY(cudaEventCreate(&e));
     }
-    eng->ev_used = 0;
+    eng->prof_steps = 0;
     return PIKV_OK;
 }
 
-int pikv_read_profile_host(pikv_engine* eng, float* attend_ms, float* step_ms, int64_t* attended_total) {
+int pikv_read_profile_host(pikv_engine* eng, float* phase_ms, int32_t n_phases, int32_t* n_steps) {
     CUDA_TRY(cudaStreamSynchronize(eng->stream));
-    float tot = 0.f;
-    for (int i = 0; i + 1 < eng->ev_used; i += 2) {
-        float ms = 0.f;
-        CUDA_TRY(cudaEventElapsedTime(&ms, eng->ev[i], eng->ev[i + 1]));
-        tot += ms;
+    std::vector<float> acc(kPhases, 0.f);
+    for (int st = 0; st < eng->prof_steps; ++st) {
+        const int b = st * (kPhases + 1);
+        for (int p = 0; p < kPhases; ++p) {
+            float ms = 0.f;
+            CUDA_TRY(cudaEventElapsedTime(&ms, eng->ev[b + p], eng->ev[b + p + 1]));
+            acc[p] += ms;
+        }
     }
-    if (attend_ms) *attend_ms = tot;
-    if (step_ms) *step_ms = 0.f;
-    if (attended_total) *attended_total = eng->ev_used / 2;
-    eng->ev_used = 0;
+    for (int p = 0; p < n_phases && p < kPhases; ++p) phase_ms[p] = acc[p];
+    if (n_steps) *n_steps = eng->prof_steps;
+    eng->prof_steps = 0;
     return PIKV_OK;
 }
 

@@ -319,13 +319,15 @@ class Engine:
     def set_profiling(self, on: bool):
         check(lib().pikv_set_profiling(self.h, int(on)))
 
+    PHASES = ("route", "insert", "sched", "retrieve", "attend", "combine", "finish")
+
     def read_profile(self):
-        a = ctypes.c_float(0)
-        s = ctypes.c_float(0)
-        n = ctypes.c_int64(0)
-        check(lib().pikv_read_profile_host(self.h, ctypes.byref(a), ctypes.byref(s),
+        """{phase: summed ms} over the steps run since set_profiling(True), and the count."""
+        ms = np.zeros(len(self.PHASES), dtype=np.float32)
+        n = ctypes.c_int32(0)
+        check(lib().pikv_read_profile_host(self.h, _np_ptr(ms), len(self.PHASES),
                                            ctypes.byref(n)))
-        return a.value, int(n.value)
+        return dict(zip(self.PHASES, ms.tolist())), int(n.value)
 
     # ---- multi-rank (see parallel.py) --------------------------------------
     def exchange_bytes(self) -> int:
