@@ -172,7 +172,7 @@ def cpu_reference(w, steps, threads=None, prefill=None):
     prefill = prefill if prefill is not None else w["L"]
     path = obuild.ref_lib_path()
     if os.path.exists(path):
-        from tests.oracle_bind import ref_lib
+        from oracle_bind import ref_lib
         lib = ref_lib()
         secs = np.zeros(threads)
         att = ctypes.c_long(0)
@@ -182,7 +182,7 @@ def cpu_reference(w, steps, threads=None, prefill=None):
                                  ctypes.byref(att))
         kind = "reference"
     else:  # oracle port, single thread
-        from tests.oracle_bind import OracleEngine, round_to
+        from oracle_bind import OracleEngine, round_to
         o = OracleEngine(cfg)
         rng = np.random.default_rng(1)
         d = cfg.model.d

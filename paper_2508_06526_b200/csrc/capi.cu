@@ -299,6 +299,7 @@ static int validate(const pikv_config& c) {
     if ((c.codec >= PIKV_CODEC_LOWRANK && c.codec <= PIKV_CODEC_PRUNE) && (c.rank < 1 || c.rank > hd))
         return fail(PIKV_ERR_INVALID_CONFIG, "codec rank must be in [1, head_dim]");
     if (c.n_layers < 0) return fail(PIKV_ERR_INVALID_CONFIG, "n_layers must be >= 0");
+    if (c.d > 16384) return fail(PIKV_ERR_INVALID_CONFIG, "d must be <= 16384 (router stages q in smem)");
     return PIKV_OK;
 }
 
@@ -476,6 +477,7 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
     chk(S.item_begin = eng->alloc<int32_t>(D.item_cap));
     chk(S.item_end = eng->alloc<int32_t>(D.item_cap));
     chk(S.n_items = eng->alloc<int32_t>(1));
+    chk(S.item_first = eng->alloc<int32_t>(B + 1));
     chk(S.part_m = eng->alloc<float>((size_t)D.item_cap * D.H));
     chk(S.part_l = eng->alloc<float>((size_t)D.item_cap * D.H));
     chk(S.part_o = eng->alloc<float>((size_t)D.item_cap * D.H * D.dph));
@@ -525,6 +527,7 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
     CUDA_TRY(cudaMemsetAsync(S.pages_after, 0, sizeof(int32_t) * B * std::max(D.Gl, 1), st));
     CUDA_TRY(cudaMemsetAsync(S.summary, 0, sizeof(pikv_step_summary) * B, st));
     CUDA_TRY(cudaMemsetAsync(S.n_items, 0, sizeof(int32_t), st));
+    CUDA_TRY(cudaMemsetAsync(S.item_first, 0, sizeof(int32_t) * (B + 1), st));
     CUDA_TRY(cudaMemsetAsync(S.att_base, 0, sizeof(int64_t) * (B + 1), st));
     std::vector<int32_t> stack(D.pool_pages);
     for (int64_t i = 0; i < D.pool_pages; ++i) stack[i] = (int32_t)(D.pool_pages - 1 - i);

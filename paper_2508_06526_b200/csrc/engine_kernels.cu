@@ -25,11 +25,16 @@ namespace pikv_dev {
 // ===========================================================================
 // route
 // ===========================================================================
-// One CTA per stream.  Threads 0..E-1 each compute one logit as the
-// reference's sequential fp64 dot (router.cpp:229-231); thread 0 then runs
-// the strategy penalty, selection, gate softmax and note_selection.
-__global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin) {
-    extern __shared__ double sm_q[];  // [d] as fp64
+// One CTA per stream.  The logits are the reference's sequential fp64 dot
+// (router.cpp:229-231): s = ((0 + w0 q0) + w1 q1) + ...  Each product is an
+// independent, correctly rounded DMUL, so all threads compute the products of
+// a chunk of kRouteChunk columns for every expert into shared memory (double
+// buffered, coalesced W loads) while thread e < E runs the dependent DADD
+// chain over the previous chunk in column order -- the only part the
+// rounding semantics force to be sequential.  Thread 0 then runs the
+// strategy penalty, selection, gate softmax and note_selection.
+__global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin, int kRouteChunk) {
+    extern __shared__ double sm_q[];  // [d] fp64, then 2 x [E][kRouteChunk + 1] products
     __shared__ double sm_logit[kMaxE];
     __shared__ bool sm_flag[kMaxE];
     __shared__ int sm_pool[kMaxE];
@@ -48,12 +53,31 @@ __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin) {
     __syncthreads();
     const bool base = C.router_strategy == PIKV_ROUTER_BASE;
     if (!base) {
-        for (int e = tid; e < D.E; e += blockDim.x) {
-            const double* row = S.W + (int64_t)e * D.d;
-            double acc = 0.0;
-            for (int i = 0; i < D.d; ++i) acc = __dadd_rn(acc, __dmul_rn(row[i], sm_q[i]));
-            sm_logit[e] = acc;
+        const int E = D.E, CH = kRouteChunk, ld = CH + 1;  // +1: conflict-free column reads
+        double* prod = sm_q + D.d;
+        const int nchunk = (D.d + CH - 1) / CH;
+        auto fill = [&](int c, double* buf) {
+            const int c0 = c * CH, w = min(CH, D.d - c0);
+            for (int t = tid; t < E * CH; t += blockDim.x) {
+                const int e = t / CH, i = t % CH;
+                if (i < w) buf[e * ld + i] = __dmul_rn(S.W[(int64_t)e * D.d + c0 + i], sm_q[c0 + i]);
+            }
+        };
+        double acc = 0.0;
+        fill(0, prod);
+        __syncthreads();
+        for (int c = 0; c < nchunk; ++c) {
+            double* cur = prod + (c & 1) * E * ld;
+            if (c + 1 < nchunk) fill(c + 1, prod + ((c + 1) & 1) * E * ld);
+            if (tid < E) {
+                const int w = min(CH, D.d - c * CH);
+                const double* row = cur + tid * ld;
+#pragma unroll 8
+                for (int i = 0; i < w; ++i) acc = __dadd_rn(acc, row[i]);
+            }
+            __syncthreads();
         }
+        if (tid < E) sm_logit[tid] = acc;
     }
     // codec projection of the query (pipeline.cpp:295-297), fp32
     {
@@ -225,9 +249,12 @@ __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin) {
 }
 
 void launch_route(const Dims& D, const Cfg& C, const State& S, const void* q, cudaStream_t st) {
-    size_t smem = sizeof(double) * (size_t)D.d;
+    int ch = 256;
+    auto bytes = [&](int c) { return sizeof(double) * ((size_t)D.d + 2 * (size_t)D.E * (c + 1)); };
+    while (ch > 8 && bytes(ch) > 200 * 1024) ch >>= 1;
+    size_t smem = bytes(ch);
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_route, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_route<<<D.B, 256, smem, st>>>(D, C, S, q);
+    k_route<<<D.B, 256, smem, st>>>(D, C, S, q, ch);
 }
 
 // ===========================================================================
@@ -659,45 +686,47 @@ void launch_sched(const Dims& D, const Cfg& C, const State& S, cudaStream_t st) 
 // (a) count matches per (stream, candidate, chunk of chunk_slots slots)
 __global__ void k_retr_count(Dims D, State S) {
     const int s = blockIdx.x, c = blockIdx.y, ch = blockIdx.z;
-    const int tid = threadIdx.x;
-    __shared__ int red[32];
-    __shared__ int fred[kMaxK];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __shared__ int red[32][kMaxK + 1];
     const int64_t ci = ((int64_t)s * D.max_cand + c) * D.nch + ch;
-    if (tid < D.k) fred[tid] = 0;
-    int cnt = 0;
     const bool active = !S.err[s] && c < S.ncand[s];
+    int j_hit = -1;
     if (active) {
         const int64_t ring = (int64_t)s * D.R + S.cand[(int64_t)s * D.max_cand + c];
         const uint64_t seq = S.seq[ring];
         const int fill = seq < (uint64_t)D.S ? (int)seq : D.S;
         const int slot = ch * D.chunk_slots + tid;
-        const int64_t now = (int64_t)S.now[s];
-        __syncthreads();
         if (slot < fill && tid < D.chunk_slots) {
             const int64_t gi = ring * D.S + slot;
-            if (S.id[gi] != 0 && S.token[gi] < now) {
+            if (S.id[gi] != 0 && S.token[gi] < (int64_t)S.now[s]) {
                 const int e = S.expert[gi];
-                for (int j = 0; j < D.k; ++j) {
+                for (int j = 0; j < D.k; ++j)
                     if (S.experts[(int64_t)s * D.k + j] == e) {
-                        cnt = 1;
-                        atomicAdd(&fred[j], 1);
+                        j_hit = j;
                         break;
                     }
-                }
             }
         }
-    } else {
-        __syncthreads();
     }
-    for (int off = 16; off; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
-    if ((tid & 31) == 0) red[tid >> 5] = cnt;
+    // per-warp counts: total and per selected expert
+    const int nw = (int)(blockDim.x >> 5);
+    const int tot = __popc(__ballot_sync(0xffffffffu, j_hit >= 0));
+    if (lane == 0) red[warp][kMaxK] = tot;
+    for (int j = 0; j < D.k; ++j) {
+        const int cj = __popc(__ballot_sync(0xffffffffu, j_hit == j));
+        if (lane == 0) red[warp][j] = cj;
+    }
     __syncthreads();
     if (tid == 0) {
         int t = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        for (int w = 0; w < nw; ++w) t += red[w][kMaxK];
         S.chunk_cnt[ci] = t;
     }
-    if (active && tid < D.k && fred[tid]) atomicAdd(&S.found[(int64_t)s * D.k + tid], fred[tid]);
+    if (active && tid < D.k) {
+        int f = 0;
+        for (int w = 0; w < nw; ++w) f += red[w][tid];
+        if (f) atomicAdd(&S.found[(int64_t)s * D.k + tid], f);
+    }
 }
 
 // (b) single CTA: exclusive offsets, per-stream bases, attention work items.
@@ -729,6 +758,7 @@ __global__ void k_retr_scan(Dims D, State S) {
         if (C < 16) C = 16;
         int64_t w = 0;
         for (int s = 0; s < D.B; ++s) {
+            S.item_first[s] = (int32_t)w;
             const int64_t n = S.summary[s].n_attended;
             for (int64_t a = 0; a < n && w < D.item_cap; a += C) {
                 S.item_stream[w] = s;
@@ -738,6 +768,7 @@ __global__ void k_retr_scan(Dims D, State S) {
             }
         }
         S.n_items[0] = (int32_t)w;
+        S.item_first[D.B] = (int32_t)w;
     }
     (void)sm_tot;
 }
@@ -805,49 +836,41 @@ void launch_retrieve(const Dims& D, const Cfg& C, const State& S, cudaStream_t s
 // combine: per-stream merge of work-item partials into the exchange record
 // ===========================================================================
 __global__ void k_combine(Dims D, State S, ExchangeLayout X) {
-    const int s = blockIdx.x;
+    const int s = blockIdx.x, h = blockIdx.y;
     const int tid = threadIdx.x;
+    extern __shared__ float sm_f[];  // [n_items of stream s] scale factors
+    __shared__ float sm_M, sm_L;
     uint8_t* rec = S.exchange + (int64_t)s * X.bytes_per_stream;
     float* xo = (float*)(rec + X.o_off);
     float* xm = (float*)(rec + X.m_off);
     float* xl = (float*)(rec + X.l_off);
-    int32_t* xf = (int32_t*)(rec + X.found_off);
-    int32_t* xs = (int32_t*)(rec + X.stats_off);
-    // item range of stream s (items are stream-ordered)
-    __shared__ int sm_w0, sm_w1;
+    const int w0 = S.item_first[s], w1 = S.item_first[s + 1];
+    const int nw = w1 - w0;
+    const bool ok = !S.err[s];
     if (tid == 0) {
-        const int n = S.n_items[0];
-        int w0 = 0;
-        while (w0 < n && S.item_stream[w0] < s) ++w0;  // n is small (~4 * CTAs)
-        int w1 = w0;
-        while (w1 < n && S.item_stream[w1] == s) ++w1;
-        sm_w0 = w0, sm_w1 = w1;
+        float M = -INFINITY;
+        for (int w = w0; w < w1; ++w) M = fmaxf(M, S.part_m[(int64_t)w * D.H + h]);
+        float L = 0.f;
+        for (int w = w0; w < w1; ++w) {
+            const float f = M == -INFINITY ? 0.f : exp2f(S.part_m[(int64_t)w * D.H + h] - M);
+            sm_f[w - w0] = f;
+            L += S.part_l[(int64_t)w * D.H + h] * f;
+        }
+        sm_M = M, sm_L = L;
+        xm[h] = ok ? M : -INFINITY;
+        xl[h] = ok ? L : 0.f;
     }
     __syncthreads();
-    const int w0 = sm_w0, w1 = sm_w1;
-    const bool ok = !S.err[s];
-    for (int o = tid; o < D.H * D.dph; o += blockDim.x) {
-        const int h = o / D.dph;
-        float m = -INFINITY;
-        for (int w = w0; w < w1; ++w) m = fmaxf(m, S.part_m[(int64_t)w * D.H + h]);
+    for (int o = tid; o < D.dph; o += blockDim.x) {
         float acc = 0.f;
-        for (int w = w0; w < w1; ++w) {
-            const float mw = S.part_m[(int64_t)w * D.H + h];
-            acc += S.part_o[((int64_t)w * D.H + h) * D.dph + o % D.dph] * exp2f(mw - m);
-        }
-        xo[o] = ok ? acc : 0.f;
+        for (int i = 0; i < nw; ++i)
+            acc = fmaf(S.part_o[((int64_t)(w0 + i) * D.H + h) * D.dph + o], sm_f[i], acc);
+        xo[h * D.dph + o] = ok ? acc : 0.f;
     }
-    for (int h = tid; h < D.H; h += blockDim.x) {
-        float m = -INFINITY;
-        for (int w = w0; w < w1; ++w) m = fmaxf(m, S.part_m[(int64_t)w * D.H + h]);
-        float l = 0.f;
-        for (int w = w0; w < w1; ++w)
-            l += S.part_l[(int64_t)w * D.H + h] * exp2f(S.part_m[(int64_t)w * D.H + h] - m);
-        xm[h] = ok ? m : -INFINITY;
-        xl[h] = ok ? l : 0.f;
-    }
-    if (tid < D.k) xf[tid] = S.found[(int64_t)s * D.k + tid];
-    if (tid == 0) {
+    if (h == 0 && tid == 0) {
+        int32_t* xf = (int32_t*)(rec + X.found_off);
+        int32_t* xs = (int32_t*)(rec + X.stats_off);
+        for (int j = 0; j < D.k; ++j) xf[j] = S.found[(int64_t)s * D.k + j];
         int nev = S.n_ow[s], pb = 0, pa = 0;
         for (int gl = 0; gl < D.Gl; ++gl) {
             nev += S.n_ev[s * D.Gl + gl];
@@ -862,7 +885,8 @@ __global__ void k_combine(Dims D, State S, ExchangeLayout X) {
 }
 
 void launch_combine(const Dims& D, const State& S, const ExchangeLayout& X, cudaStream_t st) {
-    k_combine<<<D.B, 256, 0, st>>>(D, S, X);
+    const int threads = D.dph >= 128 ? 128 : (D.dph >= 64 ? 64 : 32);
+    k_combine<<<dim3(D.B, D.H), threads, sizeof(float) * (size_t)D.item_cap, st>>>(D, S, X);
 }
 
 // ===========================================================================

@@ -141,6 +141,7 @@ struct State {
     int32_t* item_begin;
     int32_t* item_end;
     int32_t* n_items;       // [1]
+    int32_t* item_first;    // [B+1] first work item of each stream
     float* part_m;          // [item_cap][H]
     float* part_l;
     float* part_o;          // [item_cap][H][dph]
