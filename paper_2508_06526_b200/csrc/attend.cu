@@ -22,6 +22,8 @@
 //    the tensor-core ridge, so CUDA cores are the right unit.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "pikv_dev.cuh"
 
 namespace pikv_dev {
@@ -30,7 +32,7 @@ namespace {
 
 constexpr int kConsumers = 256;
 constexpr int kThreads = kConsumers + 32;
-constexpr int kSmemBudget = 220 * 1024;
+constexpr int kSmemBudget = 110 * 1024;  // two CTAs per SM
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -75,46 +77,72 @@ __device__ __forceinline__ void consumer_bar() {
     asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
 }
 
-// ---- 16-byte chunk decoders ------------------------------------------------
+// ---- packed fp32x2 math (Blackwell FFMA2 / FMUL2) ------------------------
+struct f2 {
+    float x, y;
+};
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;"
+        : "=l"(d)
+        : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+          "l"(*reinterpret_cast<unsigned long long*>(&c)));
+    return *reinterpret_cast<f2*>(&d);
+}
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+    unsigned long long d;
+    asm("mul.rn.f32x2 %0, %1, %2;"
+        : "=l"(d)
+        : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
+    return *reinterpret_cast<f2*>(&d);
+}
+
+// ---- 16-byte chunk decoders: N values as N/2 pairs -------------------------
 struct DecBF16 {
     static constexpr int N = 8;
-    __device__ static void dec(const uint4& w, float* x) {
-        x[0] = bf16_lo(w.x), x[1] = bf16_hi(w.x), x[2] = bf16_lo(w.y), x[3] = bf16_hi(w.y);
-        x[4] = bf16_lo(w.z), x[5] = bf16_hi(w.z), x[6] = bf16_lo(w.w), x[7] = bf16_hi(w.w);
+    __device__ static void dec(const uint4& w, f2* x) {
+        x[0] = {bf16_lo(w.x), bf16_hi(w.x)};
+        x[1] = {bf16_lo(w.y), bf16_hi(w.y)};
+        x[2] = {bf16_lo(w.z), bf16_hi(w.z)};
+        x[3] = {bf16_lo(w.w), bf16_hi(w.w)};
     }
 };
 struct DecF32 {
     static constexpr int N = 4;
-    __device__ static void dec(const uint4& w, float* x) {
-        x[0] = __uint_as_float(w.x), x[1] = __uint_as_float(w.y);
-        x[2] = __uint_as_float(w.z), x[3] = __uint_as_float(w.w);
+    __device__ static void dec(const uint4& w, f2* x) {
+        x[0] = {__uint_as_float(w.x), __uint_as_float(w.y)};
+        x[1] = {__uint_as_float(w.z), __uint_as_float(w.w)};
     }
 };
 struct DecI8 {
     static constexpr int N = 16;
-    __device__ static void dec(const uint4& w, float* x) {
+    __device__ static void dec(const uint4& w, f2* x) {
         const uint32_t v[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) x[i * 4 + j] = (float)((int32_t)(v[i] << (24 - 8 * j)) >> 24);
+        for (int i = 0; i < 4; ++i) {
+            x[2 * i] = {(float)((int32_t)(v[i] << 24) >> 24), (float)((int32_t)(v[i] << 16) >> 24)};
+            x[2 * i + 1] = {(float)((int32_t)(v[i] << 8) >> 24), (float)((int32_t)v[i] >> 24)};
+        }
     }
 };
 struct DecI4 {
     static constexpr int N = 32;
-    __device__ static void dec(const uint4& w, float* x) {
+    __device__ static void dec(const uint4& w, f2* x) {
         const uint32_t v[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 8; ++j) x[i * 8 + j] = (float)((int32_t)(v[i] << (28 - 4 * j)) >> 28);
+            for (int j = 0; j < 4; ++j)
+                x[4 * i + j] = {(float)((int32_t)(v[i] << (28 - 8 * j)) >> 28),
+                                (float)((int32_t)(v[i] << (24 - 8 * j)) >> 28)};
     }
 };
 
 struct AttParams {
     int CPH;          // 16-byte chunks per head (K payload)
-    int cpe;          // chunks per entry (K payload) = H * CPH
-    int EP;           // entries processed in parallel by sub-groups
+    int LPH;          // lanes per head = CPH / CPT
+    int TPE;          // threads per entry = H * LPH
+    int EP;           // entries processed in parallel by sub-groups (256 / TPE)
     int EPS;          // entries per stage
     int NST;          // stages
     int stage_bytes;
@@ -122,10 +150,13 @@ struct AttParams {
     float scale2;     // log2(e) / sqrt(dph)
 };
 
-template <class Dec, int VPT, int NB>
-__global__ void __launch_bounds__(kThreads, 1) k_attend(Dims D, State S, AttParams P) {
+// Thread (sub, head, j) owns chunks j + i*LPH (i < CPT) of one head: the
+// q.k partial is reduced over the head's LPH lanes (xor shuffles), so every
+// lane of the group holds the head's score and its own slice of o.
+template <class Dec, int CPT, int NB>
+__global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttParams P) {
     extern __shared__ __align__(128) uint8_t smem[];
-    constexpr int N = Dec::N;
+    constexpr int N = Dec::N, NP = N / 2;
     uint64_t* full = (uint64_t*)smem;
     uint64_t* empty = full + 16;
     uint8_t* stages = smem + 256;
@@ -172,117 +203,95 @@ __global__ void __launch_bounds__(kThreads, 1) k_attend(Dims D, State S, AttPara
     }
 
     // ================= consumer warps =================
-    int sub, cbase;
-    if (P.EP > 1) {
-        sub = tid / P.cpe;
-        cbase = tid % P.cpe;
-    } else {
-        sub = 0;
-        cbase = tid;
-    }
-    int head[VPT], cc[VPT];
+    const int sub = tid / P.TPE;
+    const int r = tid % P.TPE;
+    const int head = r / P.LPH, j = r % P.LPH;
+    const bool active_sub = sub < P.EP;
+    int coff[CPT];  // byte offset of chunk i inside the K (or V) payload
 #pragma unroll
-    for (int i = 0; i < VPT; ++i) {
-        const int c = cbase + i * kConsumers;
-        head[i] = c / P.CPH;
-        cc[i] = c % P.CPH;
-    }
+    for (int i = 0; i < CPT; ++i) coff[i] = (head * P.CPH + j + i * P.LPH) * 16;
     int stage = 0;
     uint32_t phase = 0;
     for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
         const int s = S.item_stream[w];
         const int64_t pos0 = S.att_base[s] + S.item_begin[w];
         const int cnt = S.item_end[w] - S.item_begin[w];
-        float q[VPT][N], o[VPT][N], m[VPT], l[VPT];
+        f2 q[CPT][NP], o[CPT][NP];
+        float m = -INFINITY, l = 0.f;
 #pragma unroll
-        for (int i = 0; i < VPT; ++i) {
-            const float* qs = S.q_attn + (int64_t)s * D.dp + head[i] * dph + cc[i] * N;
+        for (int i = 0; i < CPT; ++i) {
+            const float* qs = S.q_attn + (int64_t)s * D.dp + head * dph + (j + i * P.LPH) * N;
 #pragma unroll
-            for (int j = 0; j < N; ++j) {
-                q[i][j] = qs[j];
-                o[i][j] = 0.f;
+            for (int t = 0; t < NP; ++t) {
+                q[i][t] = {qs[2 * t], qs[2 * t + 1]};
+                o[i][t] = {0.f, 0.f};
             }
-            m[i] = -INFINITY;
-            l[i] = 0.f;
         }
         for (int b = 0; b < cnt; b += P.EPS) {
             const int n = min(P.EPS, cnt - b);
             mbar_wait(&full[stage], phase);
             const uint8_t* sb = stages + (size_t)stage * P.stage_bytes;
-            // warp-uniform trip count: sub-groups of one warp may see
-            // different entries, never different loop counts (shuffles below)
+            // warp-uniform trip count (sub-groups of a warp see different entries)
             for (int e0 = 0; e0 < n; e0 += P.EP * NB) {
-                float sc[NB][VPT];
+                float sc[NB];
 #pragma unroll
                 for (int bb = 0; bb < NB; ++bb) {
                     const int e = e0 + sub + bb * P.EP;
-                    const bool valid = e < n;
-                    const uint8_t* ent = sb + (size_t)(valid ? e : 0) * eb;
+                    const uint8_t* ent = sb + (size_t)((active_sub && e < n) ? e : 0) * eb;
+                    f2 acc = {0.f, 0.f};
 #pragma unroll
-                    for (int i = 0; i < VPT; ++i) {
-                        const uint4 kw = *(const uint4*)(ent + (size_t)(cbase + i * kConsumers) * 16);
-                        float kx[N];
-                        Dec::dec(kw, kx);
-                        float acc = 0.f;
+                    for (int i = 0; i < CPT; ++i) {
+                        f2 kx[NP];
+                        Dec::dec(*(const uint4*)(ent + coff[i]), kx);
 #pragma unroll
-                        for (int j = 0; j < N; ++j) acc = fmaf(q[i][j], kx[j], acc);
-                        sc[bb][i] = acc;
+                        for (int t = 0; t < NP; ++t) acc = fma2(q[i][t], kx[t], acc);
                     }
+                    sc[bb] = acc.x + acc.y;
                 }
 #pragma unroll
                 for (int off = 16; off; off >>= 1) {
-                    if (off < P.CPH) {
+                    if (off < P.LPH) {
 #pragma unroll
-                        for (int bb = 0; bb < NB; ++bb)
-#pragma unroll
-                            for (int i = 0; i < VPT; ++i)
-                                sc[bb][i] += __shfl_xor_sync(0xffffffffu, sc[bb][i], off);
+                        for (int bb = 0; bb < NB; ++bb) sc[bb] += __shfl_xor_sync(0xffffffffu, sc[bb], off);
                     }
+                }
+                float mx = m;
+#pragma unroll
+                for (int bb = 0; bb < NB; ++bb) {
+                    const int e = e0 + sub + bb * P.EP;
+                    const bool valid = active_sub && e < n;
+                    const uint8_t* ent = sb + (size_t)(valid ? e : 0) * eb;
+                    float x = sc[bb] * P.scale2;
+                    if (P.quant) x *= ((const float*)(ent + 2 * pay))[head];
+                    sc[bb] = valid ? x : -INFINITY;
+                    if (valid && j == 0) S.scores[(pos0 + b + e) * H + head] = x;
+                    mx = fmaxf(mx, sc[bb]);
+                }
+                if (mx > m) {  // lazy rescale: only when the running max moves
+                    const float corr = exp2f(m - mx);  // m = -inf -> 0
+                    l *= corr;
+                    const f2 c2 = {corr, corr};
+#pragma unroll
+                    for (int i = 0; i < CPT; ++i)
+#pragma unroll
+                        for (int t = 0; t < NP; ++t) o[i][t] = mul2(o[i][t], c2);
+                    m = mx;
                 }
 #pragma unroll
                 for (int bb = 0; bb < NB; ++bb) {
                     const int e = e0 + sub + bb * P.EP;
-                    const bool valid = e < n;
-                    const uint8_t* ent = sb + (size_t)(valid ? e : 0) * eb;
+                    if (active_sub && e < n) {
+                        const uint8_t* ent = sb + (size_t)e * eb;
+                        float pp = exp2f(sc[bb] - m);
+                        l += pp;
+                        if (P.quant) pp *= ((const float*)(ent + 2 * pay))[H + head];
+                        const f2 p2 = {pp, pp};
 #pragma unroll
-                    for (int i = 0; i < VPT; ++i) {
-                        float x = sc[bb][i] * P.scale2;
-                        if (P.quant) x *= ((const float*)(ent + 2 * pay))[head[i]];
-                        sc[bb][i] = valid ? x : -INFINITY;
-                        if (valid && cc[i] == 0)
-                            S.scores[(pos0 + b + e) * H + head[i]] = x;
-                    }
-                }
+                        for (int i = 0; i < CPT; ++i) {
+                            f2 vx[NP];
+                            Dec::dec(*(const uint4*)(ent + pay + coff[i]), vx);
 #pragma unroll
-                for (int i = 0; i < VPT; ++i) {
-                    float mx = m[i];
-#pragma unroll
-                    for (int bb = 0; bb < NB; ++bb) mx = fmaxf(mx, sc[bb][i]);
-                    const bool none = mx == -INFINITY;  // no entry yet for this lane
-                    const float corr = none ? 1.f : exp2f(m[i] - mx);
-                    float p[NB];
-                    float psum = 0.f;
-#pragma unroll
-                    for (int bb = 0; bb < NB; ++bb) {
-                        p[bb] = none ? 0.f : exp2f(sc[bb][i] - mx);
-                        psum += p[bb];
-                    }
-                    l[i] = fmaf(l[i], corr, psum);
-                    m[i] = mx;
-#pragma unroll
-                    for (int j = 0; j < N; ++j) o[i][j] *= corr;
-#pragma unroll
-                    for (int bb = 0; bb < NB; ++bb) {
-                        const int e = e0 + sub + bb * P.EP;
-                        if (e < n) {
-                            const uint8_t* ent = sb + (size_t)e * eb;
-                            const uint4 vw = *(const uint4*)(ent + pay + (size_t)(cbase + i * kConsumers) * 16);
-                            float vx[N];
-                            Dec::dec(vw, vx);
-                            float pp = p[bb];
-                            if (P.quant) pp *= ((const float*)(ent + 2 * pay))[H + head[i]];
-#pragma unroll
-                            for (int j = 0; j < N; ++j) o[i][j] = fmaf(pp, vx[j], o[i][j]);
+                            for (int t = 0; t < NP; ++t) o[i][t] = fma2(p2, vx[t], o[i][t]);
                         }
                     }
                 }
@@ -294,51 +303,65 @@ __global__ void __launch_bounds__(kThreads, 1) k_attend(Dims D, State S, AttPara
         // ---- write the item's partial (m, l, o), merging sub-groups ----
         if (P.EP == 1) {
 #pragma unroll
-            for (int i = 0; i < VPT; ++i) {
-                float* po = S.part_o + ((int64_t)w * H + head[i]) * dph + cc[i] * N;
+            for (int i = 0; i < CPT; ++i) {
+                float* po = S.part_o + ((int64_t)w * H + head) * dph + (j + i * P.LPH) * N;
 #pragma unroll
-                for (int j = 0; j < N; ++j) po[j] = o[i][j];
-                if (cc[i] == 0) {
-                    S.part_m[(int64_t)w * H + head[i]] = m[i];
-                    S.part_l[(int64_t)w * H + head[i]] = l[i];
-                }
+                for (int t = 0; t < NP; ++t) po[2 * t] = o[i][t].x, po[2 * t + 1] = o[i][t].y;
+            }
+            if (j == 0) {
+                S.part_m[(int64_t)w * H + head] = m;
+                S.part_l[(int64_t)w * H + head] = l;
             }
         } else {
             // red layout: [EP][H*dph] o, then [EP][H] m, [EP][H] l
             float* ro = red;
             float* rm = red + (size_t)P.EP * H * dph;
             float* rl = rm + (size_t)P.EP * H;
-            {
-                float* dst = ro + (size_t)sub * H * dph + head[0] * dph + cc[0] * N;
+            if (active_sub) {
 #pragma unroll
-                for (int j = 0; j < N; ++j) dst[j] = o[0][j];
-                if (cc[0] == 0) {
-                    rm[sub * H + head[0]] = m[0];
-                    rl[sub * H + head[0]] = l[0];
+                for (int i = 0; i < CPT; ++i) {
+                    float* dst = ro + (size_t)sub * H * dph + head * dph + (j + i * P.LPH) * N;
+#pragma unroll
+                    for (int t = 0; t < NP; ++t) dst[2 * t] = o[i][t].x, dst[2 * t + 1] = o[i][t].y;
+                }
+                if (j == 0) {
+                    rm[sub * H + head] = m;
+                    rl[sub * H + head] = l;
                 }
             }
             consumer_bar();
             if (sub == 0) {
-                const int h = head[0];
                 float M = -INFINITY;
-                for (int g = 0; g < P.EP; ++g) M = fmaxf(M, rm[g * H + h]);
-                float L = 0.f, acc[N];
+                for (int g = 0; g < P.EP; ++g) M = fmaxf(M, rm[g * H + head]);
+                float L = 0.f;
+                f2 acc[CPT][NP];
 #pragma unroll
-                for (int j = 0; j < N; ++j) acc[j] = 0.f;
+                for (int i = 0; i < CPT; ++i)
+#pragma unroll
+                    for (int t = 0; t < NP; ++t) acc[i][t] = {0.f, 0.f};
                 for (int g = 0; g < P.EP; ++g) {
-                    const float mg = rm[g * H + h];
+                    const float mg = rm[g * H + head];
                     const float f = mg == -INFINITY ? 0.f : exp2f(mg - M);
-                    L += rl[g * H + h] * f;
-                    const float* src = ro + (size_t)g * H * dph + h * dph + cc[0] * N;
+                    L += rl[g * H + head] * f;
 #pragma unroll
-                    for (int j = 0; j < N; ++j) acc[j] += src[j] * f;
+                    for (int i = 0; i < CPT; ++i) {
+                        const float* src = ro + (size_t)g * H * dph + head * dph + (j + i * P.LPH) * N;
+#pragma unroll
+                        for (int t = 0; t < NP; ++t) {
+                            acc[i][t].x += src[2 * t] * f;
+                            acc[i][t].y += src[2 * t + 1] * f;
+                        }
+                    }
                 }
-                float* po = S.part_o + ((int64_t)w * H + h) * dph + cc[0] * N;
 #pragma unroll
-                for (int j = 0; j < N; ++j) po[j] = acc[j];
-                if (cc[0] == 0) {
-                    S.part_m[(int64_t)w * H + h] = M;
-                    S.part_l[(int64_t)w * H + h] = L;
+                for (int i = 0; i < CPT; ++i) {
+                    float* po = S.part_o + ((int64_t)w * H + head) * dph + (j + i * P.LPH) * N;
+#pragma unroll
+                    for (int t = 0; t < NP; ++t) po[2 * t] = acc[i][t].x, po[2 * t + 1] = acc[i][t].y;
+                }
+                if (j == 0) {
+                    S.part_m[(int64_t)w * H + head] = M;
+                    S.part_l[(int64_t)w * H + head] = L;
                 }
             }
             consumer_bar();
@@ -348,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_attend(Dims D, State S, AttPara
 
 struct Plan {
     AttParams P;
-    int vpt;
+    int cpt;
     size_t smem;
 };
 
@@ -362,16 +385,17 @@ Plan make_plan(const Dims& D) {
     }
     const int head_bytes = D.dph * elem_bytes_x2 / 2;
     pl.P.CPH = head_bytes / 16;
-    pl.P.cpe = pl.P.CPH * D.H;
-    if (pl.P.cpe >= kConsumers) {
-        pl.vpt = pl.P.cpe / kConsumers;
-        pl.P.EP = 1;
-    } else {
-        pl.vpt = 1;
-        pl.P.EP = kConsumers / pl.P.cpe;
-    }
+    // chunks per thread: aim for 8 lanes per head, and a whole entry within
+    // the 256 consumer threads
+    int cpt = pl.P.CPH >= 8 ? pl.P.CPH / 8 : 1;
+    while (cpt < 8 && cpt < pl.P.CPH && D.H * (pl.P.CPH / cpt) > kConsumers) cpt *= 2;
+    pl.cpt = cpt;
+    pl.P.LPH = pl.P.CPH / cpt;
+    pl.P.TPE = D.H * pl.P.LPH;
+    pl.P.EP = pl.P.TPE > 0 ? kConsumers / pl.P.TPE : 0;
     int eps = (32 * 1024) / D.entry_bytes;
     eps = eps < 1 ? 1 : (eps > 32 ? 32 : eps);
+    if (eps < 2 * pl.P.EP) eps = std::min(32, 2 * pl.P.EP);
     pl.P.EPS = eps;
     pl.P.stage_bytes = eps * D.entry_bytes;
     const size_t redb = pl.P.EP > 1 ? sizeof(float) * (size_t)pl.P.EP * D.H * (D.dph + 2) : 0;
@@ -383,19 +407,20 @@ Plan make_plan(const Dims& D) {
     return pl;
 }
 
-template <class Dec, int VPT>
+template <class Dec, int CPT>
 void launch_t(const Dims& D, const State& S, const Plan& pl, cudaStream_t st) {
-    auto kern = k_attend<Dec, VPT, 2>;
+    auto kern = k_attend<Dec, CPT, 2>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
     kern<<<D.attend_ctas, kThreads, pl.smem, st>>>(D, S, pl.P);
 }
 
 template <class Dec>
 void launch_dec(const Dims& D, const State& S, const Plan& pl, cudaStream_t st) {
-    switch (pl.vpt) {
+    switch (pl.cpt) {
         case 1: launch_t<Dec, 1>(D, S, pl, st); break;
         case 2: launch_t<Dec, 2>(D, S, pl, st); break;
         case 4: launch_t<Dec, 4>(D, S, pl, st); break;
+        case 8: launch_t<Dec, 8>(D, S, pl, st); break;
         default: break;
     }
 }
@@ -409,13 +434,11 @@ const char* attend_check(const Dims& D) {
     Plan pl = make_plan(D);
     int elem_x2 = D.codec == PIKV_CODEC_INT8 ? 2 : D.codec == PIKV_CODEC_INT4 ? 1
                                                  : (D.kv_dtype == PIKV_DTYPE_BF16 ? 4 : 8);
-    if ((D.dph * elem_x2 / 2) % 16 != 0 || D.dph * elem_x2 % 2)
-        return "stored head width must be a multiple of 16 bytes";
+    if (D.dph * elem_x2 % 32 != 0) return "stored head width must be a multiple of 16 bytes";
     const int cph = pl.P.CPH;
-    if (cph < 1 || cph > 32 || (cph & (cph - 1))) return "stored head width must be 16..512 B, power of 2";
-    if (pl.P.cpe >= kConsumers && (pl.P.cpe % kConsumers || pl.vpt > 4 || pl.vpt == 3))
-        return "H * head bytes must be <= 16 KiB and a multiple of 4 KiB above 4 KiB";
-    if (pl.P.cpe < kConsumers && kConsumers % pl.P.cpe) return "H * head chunks must divide 256";
+    if (cph < 1 || cph > 64 || (cph & (cph - 1))) return "stored head width must be 16..1024 B, power of 2";
+    if (pl.P.LPH > 32 || pl.P.TPE > kConsumers || kConsumers % pl.P.TPE)
+        return "heads x lanes-per-head must divide 256 (reduce heads or head width)";
     if (pl.P.NST < 2) return "KV entry too large for the shared-memory ring";
     return nullptr;
 }

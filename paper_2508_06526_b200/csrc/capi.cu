@@ -365,7 +365,7 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
     D.nch = (c.S + D.chunk_slots - 1) / D.chunk_slots;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device);
-    D.attend_ctas = sms;
+    D.attend_ctas = 2 * sms;  // k_attend runs two CTAs per SM
     D.item_cap = 4LL * D.attend_ctas + D.B + 16;
     const int64_t total_slots = (int64_t)D.B * D.R * D.S;
     if (total_slots >= (1LL << 31)) {
