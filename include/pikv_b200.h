@@ -273,9 +273,10 @@ int64_t pikv_entry_bytes(pikv_engine* eng);
 /* Launch statistics: number of kernels this engine enqueued so far. */
 int64_t pikv_kernel_launches(pikv_engine* eng);
 /* Profiling mode: steps run eagerly (no graph) with CUDA events on the engine
- * stream between phases.  pikv_read_profile_host returns the summed ms of
- * each phase over the profiled steps: [route, insert, sched, retrieve,
- * attend, combine, finish] (n_phases <= 7) and resets the counters. */
+ * stream between kernels.  pikv_read_profile_host returns the summed ms of
+ * each kernel over the profiled steps: [route, insert, sched_pages,
+ * sched_select, retr_count, retr_scan, retr_write, attend, combine,
+ * finish_merge, foldback, feedback] (n_phases <= 12) and resets them. */
 int pikv_set_profiling(pikv_engine* eng, int32_t on);
 int pikv_read_profile_host(pikv_engine* eng, float* phase_ms, int32_t n_phases,
                            int32_t* n_steps);

@@ -593,9 +593,9 @@ static int codec_ready(pikv_engine* eng) {
     return PIKV_OK;
 }
 
-// Phases timed in profiling mode: route, insert, sched, retrieve, attend,
-// combine, finish (merge + fold-back + feedback).
-constexpr int kPhases = 7;
+// Kernels timed in profiling mode (one event after each).
+constexpr int kPhases = 12;  // route insert sched_pages sched_select retr_count retr_scan
+                             // retr_write attend combine finish_merge foldback feedback
 constexpr int kProfSteps = 512;
 
 static void mark(pikv_engine* eng, int phase) {
@@ -619,31 +619,37 @@ static int enqueue_local(pikv_engine* eng, const void* q, const void* k, const v
     CUDA_TRY(cudaMemsetAsync(S.pages_after, 0, sizeof(int32_t) * D.B * std::max(D.Gl, 1), st));
     launch_route(D, eng->C, S, q, st), ++n;
     mark(eng, 1);
-    if (D.Gl > 0) {
-        launch_insert(D, eng->C, S, k, v, sal, st), ++n;
-        mark(eng, 2);
-        if (!eng->C.unbounded_budget) launch_sched(D, eng->C, S, st), n += 2;
-        mark(eng, 3);
-        launch_retrieve(D, eng->C, S, st), n += 3;
-        mark(eng, 4);
-        if (attend) launch_attend(D, S, st), ++n;
-        mark(eng, 5);
-    } else {
-        // a rank without devices still issues ids (k_insert does it) -- run
-        // insert for the id counter only
-        launch_insert(D, eng->C, S, k, v, sal, st), ++n;
-        launch_retrieve(D, eng->C, S, st), n += 3;
-    }
-    launch_combine(D, S, eng->X, st), ++n;
+    // a rank that owns no device still issues entry ids (k_insert) and joins
+    // the merge with an empty record
+    launch_insert(D, eng->C, S, k, v, sal, st), ++n;
+    mark(eng, 2);
+    const bool sched = D.Gl > 0 && !eng->C.unbounded_budget;
+    if (sched) launch_sched_pages(D, eng->C, S, st), ++n;
+    mark(eng, 3);
+    if (sched) launch_sched_select(D, eng->C, S, st), ++n;
+    mark(eng, 4);
+    launch_retr_count(D, S, st), ++n;
+    mark(eng, 5);
+    launch_retr_scan(D, S, st), ++n;
     mark(eng, 6);
+    launch_retr_write(D, S, st), ++n;
+    mark(eng, 7);
+    if (attend && D.Gl > 0) launch_attend(D, S, st), ++n;
+    mark(eng, 8);
+    launch_combine(D, S, eng->X, st), ++n;
+    mark(eng, 9);
     CUDA_TRY(cudaGetLastError());
     eng->kernels_per_step = n;
     return PIKV_OK;
 }
 
 static int enqueue_finish(pikv_engine* eng, const uint8_t* gathered, float* y, bool attend) {
-    launch_finish(eng->D, eng->C, eng->S, eng->X, gathered, y, attend ? 1 : 0, eng->stream);
-    mark(eng, 7);
+    launch_finish_merge(eng->D, eng->C, eng->S, eng->X, gathered, y, eng->stream);
+    mark(eng, 10);
+    if (attend) launch_foldback(eng->D, eng->S, eng->stream);
+    mark(eng, 11);
+    launch_feedback(eng->D, eng->C, eng->S, eng->stream);
+    mark(eng, 12);
     eng->cur = -1;
     eng->kernels_per_step += attend ? 3 : 2;
     CUDA_TRY(cudaGetLastError());

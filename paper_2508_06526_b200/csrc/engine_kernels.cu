@@ -57,10 +57,24 @@ __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin, in
         double* prod = sm_q + D.d;
         const int nchunk = (D.d + CH - 1) / CH;
         auto fill = [&](int c, double* buf) {
-            const int c0 = c * CH, w = min(CH, D.d - c0);
-            for (int t = tid; t < E * CH; t += blockDim.x) {
-                const int e = t / CH, i = t % CH;
-                if (i < w) buf[e * ld + i] = __dmul_rn(S.W[(int64_t)e * D.d + c0 + i], sm_q[c0 + i]);
+            const int c0 = c * CH, w = min(CH, D.d - c0), total = E * CH;
+            constexpr int U = 8;  // keep U independent W loads in flight per thread
+            for (int t0 = tid; t0 < total; t0 += U * (int)blockDim.x) {
+                double wv[U], qv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int t = t0 + u * (int)blockDim.x;
+                    const int e = t / CH, i = t % CH;
+                    const bool ok = t < total && i < w;
+                    wv[u] = ok ? __ldg(S.W + (int64_t)e * D.d + c0 + i) : 0.0;
+                    qv[u] = ok ? sm_q[c0 + i] : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int t = t0 + u * (int)blockDim.x;
+                    const int e = t / CH, i = t % CH;
+                    if (t < total && i < w) buf[e * ld + i] = __dmul_rn(wv[u], qv[u]);
+                }
             }
         };
         double acc = 0.0;
@@ -438,42 +452,62 @@ void launch_insert(const Dims& D, const Cfg& C, const State& S, const void* k, c
 // ===========================================================================
 // sched: evict, scheduler.cpp:262-330
 // ===========================================================================
-// (a) one thread per candidate scheduler page (ring, page_no): aggregate of
-//     member scores in slot order, oldest id, member count.
-__global__ void k_sched_pages(Dims D, Cfg C, State S) {
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// (a) one group of G = min(32, pow2 >= page_size) lanes per candidate
+//     scheduler page (ring, page_no): lane u loads the u-th member in slot
+//     order (coalesced), lane 0 sums the member scores in that order in fp64
+//     (for_each_live order, kvstore.hpp:43-48; scheduler.cpp:276-289).
+__global__ void k_sched_pages(Dims D, Cfg C, State S, int lanes) {
+    const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int sub = lane / lanes, u0 = lane % lanes;
+    const unsigned gmask = (lanes == 32 ? 0xffffffffu : ((1u << lanes) - 1u)) << (sub * lanes);
+    const int64_t t = gt / lanes;  // page candidate index
     const int64_t total = (int64_t)D.B * D.R * D.ppr_sched;
-    if (t >= total) return;
-    const int64_t ring = t / D.ppr_sched;
-    const int pi = (int)(t % D.ppr_sched);
+    const bool in = t < total;
+    const int64_t ring = in ? t / D.ppr_sched : 0;
+    const int pi = in ? (int)(t % D.ppr_sched) : 0;
     const int s = (int)(ring / D.R);
-    S.pg_cnt[t] = 0;
-    if (S.err[s]) return;
-    const uint64_t seq = S.seq[ring];
+    const uint64_t seq = in ? S.seq[ring] : 0;
     const uint64_t Su = (uint64_t)D.S, ps = (uint64_t)D.page_size;
     const uint64_t lo = seq > Su ? seq - Su : 0;
     const uint64_t q = lo / ps + (uint64_t)pi;
-    if (q * ps >= seq) return;
+    const bool live_page = in && !S.err[s] && q * ps < seq;
     const uint64_t s0 = (q * ps) % Su;
-    // slot order: members whose slot wrapped to 0.. come first
-    const int w = (s0 + ps > Su) ? (int)(Su - s0) : 0;
-    const uint64_t now = S.now[s];
+    const int w = (s0 + ps > Su) ? (int)(Su - s0) : 0;  // members wrapping to slot 0 first
+    const uint64_t now = in ? S.now[s] : 0;
     double agg = 0.0;
-    uint64_t oldest = 0;
+    uint64_t oldest = ~0ull;
     int cnt = 0;
-    for (int u = 0; u < (int)ps; ++u) {
-        const int i = (w + u) % (int)ps;
-        const uint64_t sq = q * ps + (uint64_t)i;
-        const int64_t gi = ring * D.S + (int64_t)(sq % Su);
-        const uint64_t id = S.id[gi];
-        if (id == 0 || S.shard_seq[gi] != sq) continue;
-        if (cnt == 0 || id < oldest) oldest = id;
-        agg = __dadd_rn(agg, score_entry(C, S, gi, now, D.n_layers));
-        ++cnt;
+    for (int base = 0; base < (int)ps; base += lanes) {
+        const int u = base + u0;
+        bool mem = false;
+        double sc = 0.0;
+        uint64_t id = 0;
+        if (live_page && u < (int)ps) {
+            const int i = (w + u) % (int)ps;
+            const uint64_t sq = q * ps + (uint64_t)i;
+            const int64_t gi = ring * D.S + (int64_t)(sq % Su);
+            id = S.id[gi];
+            mem = id != 0 && S.shard_seq[gi] == sq;
+            if (mem) sc = score_entry(C, S, gi, now, D.n_layers);
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, mem) & gmask;
+        cnt += __popc(bal);
+        if (mem && id < oldest) oldest = id;
+        for (int v = 0; v < lanes; ++v) {  // sequential fp64 sum in slot order
+            const double x = __shfl_sync(0xffffffffu, sc, sub * lanes + v);
+            if (bal & (1u << (sub * lanes + v))) agg = __dadd_rn(agg, x);
+        }
     }
-    S.pg_agg[t] = agg;
-    S.pg_oldest[t] = oldest;
-    S.pg_cnt[t] = cnt;
+    for (int off = lanes >> 1; off; off >>= 1) {
+        const uint64_t o2 = __shfl_xor_sync(0xffffffffu, oldest, off);
+        oldest = o2 < oldest ? o2 : oldest;
+    }
+    if (in && u0 == 0) {
+        S.pg_cnt[t] = cnt;
+        S.pg_agg[t] = agg;
+        S.pg_oldest[t] = cnt ? oldest : 0;
+    }
 }
 
 __device__ __forceinline__ bool page_less(double a, uint64_t oa, double b, uint64_t ob) {
@@ -674,9 +708,13 @@ __global__ void __launch_bounds__(kSelThreads) k_sched_select(Dims D, Cfg C, Sta
     if (tid == 0) S.n_ev[sg] = sm_off;
 }
 
-void launch_sched(const Dims& D, const Cfg& C, const State& S, cudaStream_t st) {
-    const int64_t total = (int64_t)D.B * D.R * D.ppr_sched;
-    k_sched_pages<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(D, C, S);
+void launch_sched_pages(const Dims& D, const Cfg& C, const State& S, cudaStream_t st) {
+    int lanes = 1;
+    while (lanes < D.page_size && lanes < 32) lanes <<= 1;
+    const int64_t threads = (int64_t)D.B * D.R * D.ppr_sched * lanes;
+    k_sched_pages<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(D, C, S, lanes);
+}
+void launch_sched_select(const Dims& D, const Cfg& C, const State& S, cudaStream_t st) {
     k_sched_select<<<D.B * D.Gl, kSelThreads, 0, st>>>(D, C, S);
 }
 
@@ -823,13 +861,15 @@ __global__ void k_retr_write(Dims D, State S) {
     }
 }
 
-void launch_retrieve(const Dims& D, const Cfg& C, const State& S, cudaStream_t st) {
-    (void)C;
+void launch_retr_count(const Dims& D, const State& S, cudaStream_t st) {
     cudaMemsetAsync(S.found, 0, sizeof(int32_t) * (size_t)D.B * D.k, st);
-    dim3 grid(D.B, D.max_cand, D.nch);
-    k_retr_count<<<grid, D.chunk_slots, 0, st>>>(D, S);
+    k_retr_count<<<dim3(D.B, D.max_cand, D.nch), D.chunk_slots, 0, st>>>(D, S);
+}
+void launch_retr_scan(const Dims& D, const State& S, cudaStream_t st) {
     k_retr_scan<<<1, 1024, 0, st>>>(D, S);
-    k_retr_write<<<grid, D.chunk_slots, 0, st>>>(D, S);
+}
+void launch_retr_write(const Dims& D, const State& S, cudaStream_t st) {
+    k_retr_write<<<dim3(D.B, D.max_cand, D.nch), D.chunk_slots, 0, st>>>(D, S);
 }
 
 // ===========================================================================
@@ -1017,10 +1057,14 @@ __global__ void k_feedback(Dims D, Cfg C, State S) {
     S.now[s] += 1;
 }
 
-void launch_finish(const Dims& D, const Cfg& C, const State& S, const ExchangeLayout& X,
-                   const uint8_t* gathered, float* y, int attend, cudaStream_t st) {
+void launch_finish_merge(const Dims& D, const Cfg& C, const State& S, const ExchangeLayout& X,
+                         const uint8_t* gathered, float* y, cudaStream_t st) {
     k_finish_merge<<<D.B, 256, 0, st>>>(D, C, S, X, gathered, y);
-    if (attend) k_foldback<<<D.attend_ctas * 2, 256, 0, st>>>(D, S);
+}
+void launch_foldback(const Dims& D, const State& S, cudaStream_t st) {
+    k_foldback<<<D.attend_ctas, 256, 0, st>>>(D, S);
+}
+void launch_feedback(const Dims& D, const Cfg& C, const State& S, cudaStream_t st) {
     k_feedback<<<(D.B + 127) / 128, 128, 0, st>>>(D, C, S);
 }
 

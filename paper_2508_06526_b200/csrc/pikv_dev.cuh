@@ -227,12 +227,17 @@ __device__ __forceinline__ double score_entry(const Cfg& c, const State& st, int
 void launch_route(const Dims& D, const Cfg& C, const State& S, const void* q, cudaStream_t st);
 void launch_insert(const Dims& D, const Cfg& C, const State& S, const void* k, const void* v,
                    const double* saliency, cudaStream_t st);
-void launch_sched(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);
-void launch_retrieve(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);
+void launch_sched_pages(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);
+void launch_sched_select(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);
+void launch_retr_count(const Dims& D, const State& S, cudaStream_t st);
+void launch_retr_scan(const Dims& D, const State& S, cudaStream_t st);
+void launch_retr_write(const Dims& D, const State& S, cudaStream_t st);
 void launch_attend(const Dims& D, const State& S, cudaStream_t st);
 void launch_combine(const Dims& D, const State& S, const ExchangeLayout& X, cudaStream_t st);
-void launch_finish(const Dims& D, const Cfg& C, const State& S, const ExchangeLayout& X,
-                   const uint8_t* gathered, float* y, int attend, cudaStream_t st);
+void launch_finish_merge(const Dims& D, const Cfg& C, const State& S, const ExchangeLayout& X,
+                         const uint8_t* gathered, float* y, cudaStream_t st);
+void launch_foldback(const Dims& D, const State& S, cudaStream_t st);
+void launch_feedback(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);
 void launch_synth(const Dims& D, void* q, void* k, void* v, uint64_t seed, uint64_t step,
                   cudaStream_t st);
 int attend_max_smem();

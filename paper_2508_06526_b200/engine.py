@@ -319,7 +319,8 @@ class Engine:
     def set_profiling(self, on: bool):
         check(lib().pikv_set_profiling(self.h, int(on)))
 
-    PHASES = ("route", "insert", "sched", "retrieve", "attend", "combine", "finish")
+    PHASES = ("route", "insert", "sched_pages", "sched_select", "retr_count", "retr_scan",
+              "retr_write", "attend", "combine", "finish_merge", "foldback", "feedback")
 
     def read_profile(self):
         """{phase: summed ms} over the steps run since set_profiling(True), and the count."""
