@@ -605,7 +605,7 @@ static void mark(pikv_engine* eng, int phase) {
 
 // The step's launch sequence (pipeline.cpp:213-351 ordering).
 static int enqueue_local(pikv_engine* eng, const void* q, const void* k, const void* v,
-                         const double* sal, bool attend) {
+                         const double* sal, bool attend, float* y) {
     const Dims& D = eng->D;
     const State& S = eng->S;
     cudaStream_t st = eng->stream;
@@ -613,10 +613,6 @@ static int enqueue_local(pikv_engine* eng, const void* q, const void* k, const v
     eng->cur = -1;
     if (eng->profiling && eng->prof_steps < kProfSteps) eng->cur = eng->prof_steps++ * (kPhases + 1);
     mark(eng, 0);
-    CUDA_TRY(cudaMemsetAsync(S.n_ow, 0, sizeof(int32_t) * D.B, st));
-    CUDA_TRY(cudaMemsetAsync(S.n_ev, 0, sizeof(int32_t) * D.B * std::max(D.Gl, 1), st));
-    CUDA_TRY(cudaMemsetAsync(S.pages_before, 0, sizeof(int32_t) * D.B * std::max(D.Gl, 1), st));
-    CUDA_TRY(cudaMemsetAsync(S.pages_after, 0, sizeof(int32_t) * D.B * std::max(D.Gl, 1), st));
     launch_route(D, eng->C, S, q, st), ++n;
     mark(eng, 1);
     // a rank that owns no device still issues entry ids (k_insert) and joins
@@ -636,7 +632,8 @@ static int enqueue_local(pikv_engine* eng, const void* q, const void* k, const v
     mark(eng, 7);
     if (attend && D.Gl > 0) launch_attend(D, S, st), ++n;
     mark(eng, 8);
-    launch_combine(D, S, eng->X, st), ++n;
+    const int direct = D.world == 1;  // single rank: combine writes y and the global (m, l)
+    launch_combine(D, eng->C, S, eng->X, y, direct, st), ++n;
     mark(eng, 9);
     CUDA_TRY(cudaGetLastError());
     eng->kernels_per_step = n;
@@ -644,14 +641,14 @@ static int enqueue_local(pikv_engine* eng, const void* q, const void* k, const v
 }
 
 static int enqueue_finish(pikv_engine* eng, const uint8_t* gathered, float* y, bool attend) {
-    launch_finish_merge(eng->D, eng->C, eng->S, eng->X, gathered, y, eng->stream);
+    if (eng->D.world > 1) launch_finish_merge(eng->D, eng->C, eng->S, eng->X, gathered, y, eng->stream);
     mark(eng, 10);
     if (attend) launch_foldback(eng->D, eng->S, eng->stream);
     mark(eng, 11);
     launch_feedback(eng->D, eng->C, eng->S, eng->stream);
     mark(eng, 12);
     eng->cur = -1;
-    eng->kernels_per_step += attend ? 3 : 2;
+    eng->kernels_per_step += (attend ? 2 : 1) + (eng->D.world > 1 ? 1 : 0);
     CUDA_TRY(cudaGetLastError());
     return PIKV_OK;
 }
@@ -665,7 +662,7 @@ static int run_step(pikv_engine* eng, const void* q, const void* k, const void* 
     cudaSetDevice(eng->device);
     const bool use_graph = eng->warmed && !eng->profiling;
     if (!use_graph) {
-        rc = enqueue_local(eng, q, k, v, sal, attend);
+        rc = enqueue_local(eng, q, k, v, sal, attend, y);
         if (!rc) rc = enqueue_finish(eng, eng->S.exchange, y, attend);
         if (rc) return rc;
         eng->warmed = true;  // first eager pass sets kernel attributes
@@ -677,7 +674,7 @@ static int run_step(pikv_engine* eng, const void* q, const void* k, const void* 
     if (it == eng->graphs.end()) {
         cudaGraph_t g;
         CUDA_TRY(cudaStreamBeginCapture(eng->stream, cudaStreamCaptureModeThreadLocal));
-        rc = enqueue_local(eng, q, k, v, sal, attend);
+        rc = enqueue_local(eng, q, k, v, sal, attend, y);
         if (!rc) rc = enqueue_finish(eng, eng->S.exchange, y, attend);
         cudaError_t ce = cudaStreamEndCapture(eng->stream, &g);
         if (rc) return rc;
@@ -730,7 +727,7 @@ int pikv_step_local(pikv_engine* eng, const void* q, const void* k, const void* 
     int rc = codec_ready(eng);
     if (rc) return rc;
     cudaSetDevice(eng->device);
-    rc = enqueue_local(eng, q, k, v, saliency, true);
+    rc = enqueue_local(eng, q, k, v, saliency, true, nullptr);
     if (rc) return rc;
     eng->launches += eng->kernels_per_step;
     if (exchange_out) *exchange_out = eng->S.exchange;
@@ -741,7 +738,7 @@ int pikv_step_finish(pikv_engine* eng, const void* gathered, float* y_out) {
     cudaSetDevice(eng->device);
     int rc = enqueue_finish(eng, (const uint8_t*)gathered, y_out, true);
     if (rc) return rc;
-    eng->launches += 3;
+    eng->launches += 3;  // finish_merge, foldback, feedback
     return PIKV_OK;
 }
 
@@ -762,7 +759,7 @@ int pikv_prefill_synthetic(pikv_engine* eng, int64_t tokens, uint64_t seed) {
         if (eng->D.world == 1) {
             rc = run_step(eng, eng->in_q, eng->in_k, eng->in_v, nullptr, nullptr, false);
         } else {
-            rc = enqueue_local(eng, eng->in_q, eng->in_k, eng->in_v, nullptr, false);
+            rc = enqueue_local(eng, eng->in_q, eng->in_k, eng->in_v, nullptr, false, nullptr);
             if (!rc) rc = enqueue_finish(eng, eng->S.exchange, nullptr, false);
         }
         if (rc) {

@@ -27,19 +27,31 @@ namespace pikv_dev {
 // ===========================================================================
 // One CTA per stream.  The logits are the reference's sequential fp64 dot
 // (router.cpp:229-231): s = ((0 + w0 q0) + w1 q1) + ...  Each product is an
-// independent, correctly rounded DMUL, so all threads compute the products of
-// a chunk of kRouteChunk columns for every expert into shared memory (double
-// buffered, coalesced W loads) while thread e < E runs the dependent DADD
-// chain over the previous chunk in column order -- the only part the
-// rounding semantics force to be sequential.  Thread 0 then runs the
-// strategy penalty, selection, gate softmax and note_selection.
-__global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin, int kRouteChunk) {
-    extern __shared__ double sm_q[];  // [d] fp64, then 2 x [E][kRouteChunk + 1] products
+// independent, correctly rounded DMUL, so the "filler" warps compute the
+// products of a chunk of CH columns for every expert into shared memory
+// (double buffered; the W loads of chunk c+2 are in flight in registers while
+// chunk c+1 is stored), while the summing warps (thread e < E) run the
+// dependent DADD chain over chunk c in column order -- the only part the
+// rounding semantics force to be sequential.  Thread 0 then runs the strategy
+// penalty, selection, gate softmax and note_selection.
+constexpr int kRouteFillers = 224;
+constexpr int kRouteMaxP = 20;  // products per filler thread per chunk
+
+__global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin, int CH) {
+    extern __shared__ double sm_q[];  // [d] fp64, then 2 x [E][CH + 1] products
     __shared__ double sm_logit[kMaxE];
     __shared__ bool sm_flag[kMaxE];
     __shared__ int sm_pool[kMaxE];
     const int s = blockIdx.x;
     const int tid = threadIdx.x;
+    // per-step scratch counters of this stream (replaces memset nodes)
+    if (tid == 0) S.n_ow[s] = 0;
+    for (int g = tid; g < D.Gl; g += blockDim.x) {
+        S.n_ev[s * D.Gl + g] = 0;
+        S.pages_before[s * D.Gl + g] = 0;
+        S.pages_after[s * D.Gl + g] = 0;
+    }
+    for (int j = tid; j < D.k; j += blockDim.x) S.found[(int64_t)s * D.k + j] = 0;
     if (S.err[s]) return;
     // query in fp64 (exact upcast of bf16/f32)
     for (int i = tid; i < D.d; i += blockDim.x) {
@@ -53,39 +65,46 @@ __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin, in
     __syncthreads();
     const bool base = C.router_strategy == PIKV_ROUTER_BASE;
     if (!base) {
-        const int E = D.E, CH = kRouteChunk, ld = CH + 1;  // +1: conflict-free column reads
+        const int E = D.E, ld = CH + 1;  // +1: conflict-free column reads
         double* prod = sm_q + D.d;
         const int nchunk = (D.d + CH - 1) / CH;
-        auto fill = [&](int c, double* buf) {
-            const int c0 = c * CH, w = min(CH, D.d - c0), total = E * CH;
-            constexpr int U = 8;  // keep U independent W loads in flight per thread
-            for (int t0 = tid; t0 < total; t0 += U * (int)blockDim.x) {
-                double wv[U], qv[U];
+        const int fill_lo = (int)blockDim.x - kRouteFillers;  // summers: warps below
+        const int ftid = tid - fill_lo;
+        const bool filler = ftid >= 0;
+        const int total = E * CH;
+        double wreg[kRouteMaxP];
+        auto load = [&](int c) {
+            const int c0 = c * CH, w = min(CH, D.d - c0);
 #pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int t = t0 + u * (int)blockDim.x;
-                    const int e = t / CH, i = t % CH;
-                    const bool ok = t < total && i < w;
-                    wv[u] = ok ? __ldg(S.W + (int64_t)e * D.d + c0 + i) : 0.0;
-                    qv[u] = ok ? sm_q[c0 + i] : 0.0;
-                }
+            for (int u = 0; u < kRouteMaxP; ++u) {
+                const int t = ftid + u * kRouteFillers;
+                const int e = t / CH, i = t % CH;
+                wreg[u] = (c < nchunk && t < total && i < w) ? __ldg(S.W + (int64_t)e * D.d + c0 + i) : 0.0;
+            }
+        };
+        auto store = [&](int c, double* buf) {
+            const int c0 = c * CH, w = min(CH, D.d - c0);
 #pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int t = t0 + u * (int)blockDim.x;
-                    const int e = t / CH, i = t % CH;
-                    if (t < total && i < w) buf[e * ld + i] = __dmul_rn(wv[u], qv[u]);
-                }
+            for (int u = 0; u < kRouteMaxP; ++u) {
+                const int t = ftid + u * kRouteFillers;
+                const int e = t / CH, i = t % CH;
+                if (c < nchunk && t < total && i < w) buf[e * ld + i] = __dmul_rn(wreg[u], sm_q[c0 + i]);
             }
         };
         double acc = 0.0;
-        fill(0, prod);
+        if (filler) {
+            load(0);
+            store(0, prod);
+            load(1);
+        }
         __syncthreads();
         for (int c = 0; c < nchunk; ++c) {
-            double* cur = prod + (c & 1) * E * ld;
-            if (c + 1 < nchunk) fill(c + 1, prod + ((c + 1) & 1) * E * ld);
-            if (tid < E) {
+            if (filler) {
+                store(c + 1, prod + ((c + 1) & 1) * E * ld);
+                load(c + 2);
+            } else if (tid < E) {
                 const int w = min(CH, D.d - c * CH);
-                const double* row = cur + tid * ld;
+                const double* row = prod + (c & 1) * E * ld + tid * ld;
 #pragma unroll 8
                 for (int i = 0; i < w; ++i) acc = __dadd_rn(acc, row[i]);
             }
@@ -265,10 +284,11 @@ __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin, in
 void launch_route(const Dims& D, const Cfg& C, const State& S, const void* q, cudaStream_t st) {
     int ch = 256;
     auto bytes = [&](int c) { return sizeof(double) * ((size_t)D.d + 2 * (size_t)D.E * (c + 1)); };
-    while (ch > 8 && bytes(ch) > 200 * 1024) ch >>= 1;
+    while (ch > 8 && (bytes(ch) > 200 * 1024 || D.E * ch > kRouteMaxP * kRouteFillers)) ch >>= 1;
     size_t smem = bytes(ch);
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_route, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_route<<<D.B, 256, smem, st>>>(D, C, S, q, ch);
+    const int summers = ((D.E + 31) / 32) * 32;
+    k_route<<<D.B, summers + kRouteFillers, smem, st>>>(D, C, S, q, ch);
 }
 
 // ===========================================================================
@@ -767,48 +787,81 @@ __global__ void k_retr_count(Dims D, State S) {
     }
 }
 
-// (b) single CTA: exclusive offsets, per-stream bases, attention work items.
-__global__ void k_retr_scan(Dims D, State S) {
-    __shared__ int64_t sm_tot[1024];
-    const int tid = threadIdx.x;
-    const int per = D.max_cand * D.nch;
-    // per-stream totals + in-stream chunk offsets (a thread per stream)
-    for (int s = tid; s < D.B; s += blockDim.x) {
-        int64_t acc = 0;
-        for (int i = 0; i < per; ++i) {
-            const int64_t ci = (int64_t)s * per + i;
-            S.chunk_off[ci] = (int32_t)acc;
-            acc += S.chunk_cnt[ci];
+// (b) single CTA: in-stream chunk offsets (warp per stream), per-stream
+//     bases and attention work items (block scans over streams).
+__device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t* wsum, int64_t* total) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    int64_t x = v;
+    for (int off = 1; off < 32; off <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, x, off);
+        if (lane >= off) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        int64_t w = lane < nw ? wsum[lane] : 0;
+        for (int off = 1; off < 32; off <<= 1) {
+            const int64_t y = __shfl_up_sync(0xffffffffu, w, off);
+            if (lane >= off) w += y;
         }
-        S.summary[s].n_attended = (int32_t)acc;
+        wsum[lane] = w;
     }
     __syncthreads();
-    if (tid == 0) {
-        int64_t acc = 0;
-        for (int s = 0; s < D.B; ++s) {
-            S.att_base[s] = acc;
-            acc += S.summary[s].n_attended;
-        }
-        S.att_base[D.B] = acc;
-        // work items: chunk size so that ~4 items per attention CTA
-        const int64_t N = acc;
-        int64_t C = (N + 4LL * D.attend_ctas - 1) / (4LL * D.attend_ctas);
-        if (C < 16) C = 16;
-        int64_t w = 0;
-        for (int s = 0; s < D.B; ++s) {
-            S.item_first[s] = (int32_t)w;
-            const int64_t n = S.summary[s].n_attended;
-            for (int64_t a = 0; a < n && w < D.item_cap; a += C) {
-                S.item_stream[w] = s;
-                S.item_begin[w] = (int32_t)a;
-                S.item_end[w] = (int32_t)(a + C < n ? a + C : n);
-                ++w;
+    const int64_t excl = x - v + (warp ? wsum[warp - 1] : 0);
+    *total = wsum[nw - 1];
+    __syncthreads();
+    return excl;
+}
+
+__global__ void __launch_bounds__(1024) k_retr_scan(Dims D, State S) {
+    __shared__ int64_t sm_n[1024];
+    __shared__ int64_t wsum[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    const int per = D.max_cand * D.nch;
+    for (int s = warp; s < D.B; s += nw) {
+        int64_t run = 0;
+        for (int b0 = 0; b0 < per; b0 += 32) {
+            const int64_t ci = (int64_t)s * per + b0 + lane;
+            const int c = b0 + lane < per ? S.chunk_cnt[ci] : 0;
+            int x = c;
+            for (int off = 1; off < 32; off <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x, off);
+                if (lane >= off) x += y;
             }
+            if (b0 + lane < per) S.chunk_off[ci] = (int32_t)(run + x - c);
+            run += __shfl_sync(0xffffffffu, x, 31);
         }
-        S.n_items[0] = (int32_t)w;
-        S.item_first[D.B] = (int32_t)w;
+        if (lane == 0) sm_n[s] = run;
     }
-    (void)sm_tot;
+    __syncthreads();
+    const int64_t n = tid < D.B ? sm_n[tid] : 0;
+    int64_t N;
+    const int64_t base = block_excl_scan(n, wsum, &N);
+    int64_t C = (N + 4LL * D.attend_ctas - 1) / (4LL * D.attend_ctas);
+    if (C < 16) C = 16;
+    const int64_t items = (n + C - 1) / C;
+    int64_t W;
+    const int64_t first = block_excl_scan(items, wsum, &W);
+    if (tid < D.B) {
+        S.summary[tid].n_attended = (int32_t)n;
+        S.att_base[tid] = base;
+        S.item_first[tid] = (int32_t)first;
+    }
+    if (tid == 0) {
+        S.att_base[D.B] = N;
+        S.item_first[D.B] = (int32_t)W;
+        S.n_items[0] = (int32_t)W;
+    }
+    __syncthreads();
+    for (int s = warp; s < D.B; s += nw) {
+        const int64_t ns = sm_n[s];
+        const int64_t f = S.item_first[s];
+        for (int64_t j = lane; j * C < ns; j += 32) {
+            S.item_stream[f + j] = s;
+            S.item_begin[f + j] = (int32_t)(j * C);
+            S.item_end[f + j] = (int32_t)min(ns, (j + 1) * C);
+        }
+    }
 }
 
 // (c) write the compacted (slot, entry) lists; bump freq / last_access.
@@ -862,7 +915,6 @@ __global__ void k_retr_write(Dims D, State S) {
 }
 
 void launch_retr_count(const Dims& D, const State& S, cudaStream_t st) {
-    cudaMemsetAsync(S.found, 0, sizeof(int32_t) * (size_t)D.B * D.k, st);
     k_retr_count<<<dim3(D.B, D.max_cand, D.nch), D.chunk_slots, 0, st>>>(D, S);
 }
 void launch_retr_scan(const Dims& D, const State& S, cudaStream_t st) {
@@ -875,11 +927,11 @@ void launch_retr_write(const Dims& D, const State& S, cudaStream_t st) {
 // ===========================================================================
 // combine: per-stream merge of work-item partials into the exchange record
 // ===========================================================================
-__global__ void k_combine(Dims D, State S, ExchangeLayout X) {
+__global__ void k_combine(Dims D, Cfg C, State S, ExchangeLayout X, float* __restrict__ y, int direct) {
     const int s = blockIdx.x, h = blockIdx.y;
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
     extern __shared__ float sm_f[];  // [n_items of stream s] scale factors
-    __shared__ float sm_M, sm_L;
+    __shared__ float red[32];
     uint8_t* rec = S.exchange + (int64_t)s * X.bytes_per_stream;
     float* xo = (float*)(rec + X.o_off);
     float* xm = (float*)(rec + X.m_off);
@@ -887,46 +939,83 @@ __global__ void k_combine(Dims D, State S, ExchangeLayout X) {
     const int w0 = S.item_first[s], w1 = S.item_first[s + 1];
     const int nw = w1 - w0;
     const bool ok = !S.err[s];
-    if (tid == 0) {
-        float M = -INFINITY;
-        for (int w = w0; w < w1; ++w) M = fmaxf(M, S.part_m[(int64_t)w * D.H + h]);
-        float L = 0.f;
-        for (int w = w0; w < w1; ++w) {
-            const float f = M == -INFINITY ? 0.f : exp2f(S.part_m[(int64_t)w * D.H + h] - M);
-            sm_f[w - w0] = f;
-            L += S.part_l[(int64_t)w * D.H + h] * f;
-        }
-        sm_M = M, sm_L = L;
-        xm[h] = ok ? M : -INFINITY;
-        xl[h] = ok ? L : 0.f;
-    }
+    float M = -INFINITY;
+    for (int i = tid; i < nw; i += blockDim.x) M = fmaxf(M, S.part_m[(int64_t)(w0 + i) * D.H + h]);
+    for (int off = 16; off; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+    if (lane == 0) red[warp] = M;
     __syncthreads();
+    M = -INFINITY;
+    for (int w = 0; w < nwarp; ++w) M = fmaxf(M, red[w]);
+    __syncthreads();
+    float L = 0.f;
+    for (int i = tid; i < nw; i += blockDim.x) {
+        const float f = M == -INFINITY ? 0.f : exp2f(S.part_m[(int64_t)(w0 + i) * D.H + h] - M);
+        sm_f[i] = f;
+        L += S.part_l[(int64_t)(w0 + i) * D.H + h] * f;
+    }
+    for (int off = 16; off; off >>= 1) L += __shfl_xor_sync(0xffffffffu, L, off);
+    if (lane == 0) red[warp] = L;
+    __syncthreads();
+    L = 0.f;
+    for (int w = 0; w < nwarp; ++w) L += red[w];
     for (int o = tid; o < D.dph; o += blockDim.x) {
         float acc = 0.f;
         for (int i = 0; i < nw; ++i)
             acc = fmaf(S.part_o[((int64_t)(w0 + i) * D.H + h) * D.dph + o], sm_f[i], acc);
-        xo[h * D.dph + o] = ok ? acc : 0.f;
+        if (direct) {
+            if (y && ok) y[(int64_t)s * D.dp + h * D.dph + o] = L > 0.f ? acc / L : 0.f;
+        } else {
+            xo[h * D.dph + o] = ok ? acc : 0.f;
+        }
+    }
+    if (tid == 0) {
+        if (direct) {
+            S.gM[s * D.H + h] = M;
+            S.gL[s * D.H + h] = L;
+        } else {
+            xm[h] = ok ? M : -INFINITY;
+            xl[h] = ok ? L : 0.f;
+        }
     }
     if (h == 0 && tid == 0) {
-        int32_t* xf = (int32_t*)(rec + X.found_off);
-        int32_t* xs = (int32_t*)(rec + X.stats_off);
-        for (int j = 0; j < D.k; ++j) xf[j] = S.found[(int64_t)s * D.k + j];
         int nev = S.n_ow[s], pb = 0, pa = 0;
         for (int gl = 0; gl < D.Gl; ++gl) {
             nev += S.n_ev[s * D.Gl + gl];
             pb += S.pages_before[s * D.Gl + gl];
             pa += S.pages_after[s * D.Gl + gl];
         }
-        xs[0] = S.summary[s].n_attended;
-        xs[1] = nev;
-        xs[2] = pb;
-        xs[3] = pa;
+        const int n_att = S.summary[s].n_attended;
+        if (direct) {  // world == 1: this rank's counts are the global ones
+            int hits = 0;
+            for (int j = 0; j < D.k; ++j) hits += S.found[(int64_t)s * D.k + j] > 0;
+            pikv_step_summary& sm = S.summary[s];
+            sm.step = S.now[s];
+            sm.inserts = D.k;
+            sm.lookups = D.k;
+            sm.hits = hits;
+            const int hw = C.head_width < D.dp ? C.head_width : D.dp;  // pipeline.cpp:22-26
+            sm.fetch_elements = (int64_t)n_att * (int64_t)(2 * hw + D.dp);
+            sm.n_evictions = nev;
+            sm.pages_before = pb;
+            sm.pages_after = pa;
+            sm.error = S.err[s];
+        } else {
+            int32_t* xf = (int32_t*)(rec + X.found_off);
+            int32_t* xs = (int32_t*)(rec + X.stats_off);
+            for (int j = 0; j < D.k; ++j) xf[j] = S.found[(int64_t)s * D.k + j];
+            xs[0] = n_att;
+            xs[1] = nev;
+            xs[2] = pb;
+            xs[3] = pa;
+        }
     }
 }
 
-void launch_combine(const Dims& D, const State& S, const ExchangeLayout& X, cudaStream_t st) {
+void launch_combine(const Dims& D, const Cfg& C, const State& S, const ExchangeLayout& X, float* y,
+                    int direct, cudaStream_t st) {
     const int threads = D.dph >= 128 ? 128 : (D.dph >= 64 ? 64 : 32);
-    k_combine<<<dim3(D.B, D.H), threads, sizeof(float) * (size_t)D.item_cap, st>>>(D, S, X);
+    k_combine<<<dim3(D.B, D.H), threads, sizeof(float) * (size_t)D.item_cap, st>>>(D, C, S, X, y,
+                                                                                 direct);
 }
 
 // ===========================================================================
@@ -996,15 +1085,18 @@ __global__ void k_finish_merge(Dims D, Cfg C, State S, ExchangeLayout X,
     }
 }
 
-// attn_mass += alpha, pipeline.cpp:302-312; alpha = mean over heads.
+// attn_mass += alpha, pipeline.cpp:302-312; alpha = mean over heads.  One
+// warp per retrieved entry, lanes over heads (coalesced score reads).
 __global__ void k_foldback(Dims D, State S) {
     __shared__ int64_t sm_base[1025];
     const int nb = D.B + 1;
-    for (int i = threadIdx.x; i < nb && i < 1025; i += blockDim.x) sm_base[i] = S.att_base[i];
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) sm_base[i] = S.att_base[i];
     __syncthreads();
-    const int64_t N = sm_base[D.B < 1024 ? D.B : 1024];
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N;
-         i += (int64_t)gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    const int64_t N = sm_base[D.B];
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = gw; i < N; i += nwarps) {
         int lo = 0, hi = D.B;  // stream: last s with base[s] <= i
         while (hi - lo > 1) {
             const int mid = (lo + hi) >> 1;
@@ -1012,16 +1104,19 @@ __global__ void k_foldback(Dims D, State S) {
         }
         const int s = lo;
         if (S.err[s]) continue;
-        double a = 0.0;
-        const float* sc = S.scores + i * D.H;
-        for (int h = 0; h < D.H; ++h) {
+        float a = 0.f;
+        for (int h = lane; h < D.H; h += 32) {
             const float L = S.gL[s * D.H + h];
-            if (L > 0.f) a += (double)(exp2f(sc[h] - S.gM[s * D.H + h]) / L);
+            if (L > 0.f) a += exp2f(S.scores[i * D.H + h] - S.gM[s * D.H + h]) / L;
         }
-        a /= (double)D.H;
-        const int64_t gi = S.att_slot[i];
-        S.attn_mass[gi] += a;
-        if (D.n_layers > 0) S.per_layer[gi * D.n_layers + (int64_t)(S.now[s] % (uint64_t)D.n_layers)] += a;
+        for (int off = 16; off; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+        if (lane == 0) {
+            const double al = (double)a / (double)D.H;
+            const int64_t gi = S.att_slot[i];
+            S.attn_mass[gi] += al;
+            if (D.n_layers > 0)
+                S.per_layer[gi * D.n_layers + (int64_t)(S.now[s] % (uint64_t)D.n_layers)] += al;
+        }
     }
 }
 
@@ -1062,7 +1157,7 @@ void launch_finish_merge(const Dims& D, const Cfg& C, const State& S, const Exch
     k_finish_merge<<<D.B, 256, 0, st>>>(D, C, S, X, gathered, y);
 }
 void launch_foldback(const Dims& D, const State& S, cudaStream_t st) {
-    k_foldback<<<D.attend_ctas, 256, 0, st>>>(D, S);
+    k_foldback<<<D.attend_ctas * 2, 256, 0, st>>>(D, S);
 }
 void launch_feedback(const Dims& D, const Cfg& C, const State& S, cudaStream_t st) {
     k_feedback<<<(D.B + 127) / 128, 128, 0, st>>>(D, C, S);

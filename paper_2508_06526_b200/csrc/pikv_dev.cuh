@@ -233,7 +233,8 @@ void launch_retr_count(const Dims& D, const State& S, cudaStream_t st);
 void launch_retr_scan(const Dims& D, const State& S, cudaStream_t st);
 void launch_retr_write(const Dims& D, const State& S, cudaStream_t st);
 void launch_attend(const Dims& D, const State& S, cudaStream_t st);
-void launch_combine(const Dims& D, const State& S, const ExchangeLayout& X, cudaStream_t st);
+void launch_combine(const Dims& D, const Cfg& C, const State& S, const ExchangeLayout& X, float* y,
+                    int direct, cudaStream_t st);
 void launch_finish_merge(const Dims& D, const Cfg& C, const State& S, const ExchangeLayout& X,
                          const uint8_t* gathered, float* y, cudaStream_t st);
 void launch_foldback(const Dims& D, const State& S, cudaStream_t st);
