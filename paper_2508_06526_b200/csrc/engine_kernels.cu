@@ -26,24 +26,30 @@ namespace pikv_dev {
 // route
 // ===========================================================================
 // One CTA per stream.  The logits are the reference's sequential fp64 dot
-// (router.cpp:229-231): s = ((0 + w0 q0) + w1 q1) + ...  Each product is an
-// independent, correctly rounded DMUL, so the "filler" warps compute the
-// products of a chunk of CH columns for every expert into shared memory
-// (double buffered; the W loads of chunk c+2 are in flight in registers while
-// chunk c+1 is stored), while the summing warps (thread e < E) run the
-// dependent DADD chain over chunk c in column order -- the only part the
-// rounding semantics force to be sequential.  Thread 0 then runs the strategy
-// penalty, selection, gate softmax and note_selection.
-constexpr int kRouteFillers = 224;
-constexpr int kRouteMaxP = 20;  // products per filler thread per chunk
+// (router.cpp:229-231): s = ((0 + w0 q0) + w1 q1) + ...; thread e < E runs
+// that dependent DMUL/DADD chain for expert e in column order (the rounding
+// semantics make it sequential; __dmul_rn/__dadd_rn forbid FMA contraction).
+// W_r rows stream through an NST-stage shared-memory ring filled by TMA bulk
+// copies (one per expert row segment, issued by the producer lane of the
+// last warp), so the chain never waits on L2.  Thread 0 then runs the
+// strategy penalty, selection, gate softmax and note_selection.
+constexpr int kRouteCH = 256;    // columns per stage
+constexpr int kRouteStages = 3;
 
-__global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin, int CH) {
-    extern __shared__ double sm_q[];  // [d] fp64, then 2 x [E][CH + 1] products
+__global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin) {
+    extern __shared__ __align__(128) uint8_t sm_raw[];
+    uint64_t* full = (uint64_t*)sm_raw;
+    uint64_t* empty = full + kRouteStages;
+    double* sm_q = (double*)(sm_raw + 128);
+    const int rowb = kRouteCH * 8 + 16;  // padded row: 2-way bank conflicts at worst
+    uint8_t* ring = (uint8_t*)(sm_q + D.d);
     __shared__ double sm_logit[kMaxE];
     __shared__ bool sm_flag[kMaxE];
     __shared__ int sm_pool[kMaxE];
     const int s = blockIdx.x;
     const int tid = threadIdx.x;
+    const int nsum_warps = (D.E + 31) / 32;
+    const int prod_warp = nsum_warps;  // last warp
     // per-step scratch counters of this stream (replaces memset nodes)
     if (tid == 0) S.n_ow[s] = 0;
     for (int g = tid; g < D.Gl; g += blockDim.x) {
@@ -53,6 +59,13 @@ __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin, in
     }
     for (int j = tid; j < D.k; j += blockDim.x) S.found[(int64_t)s * D.k + j] = 0;
     if (S.err[s]) return;
+    if (tid == 0) {
+        for (int i = 0; i < kRouteStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], nsum_warps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     // query in fp64 (exact upcast of bf16/f32)
     for (int i = tid; i < D.d; i += blockDim.x) {
         double x;
@@ -65,52 +78,45 @@ __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin, in
     __syncthreads();
     const bool base = C.router_strategy == PIKV_ROUTER_BASE;
     if (!base) {
-        const int E = D.E, ld = CH + 1;  // +1: conflict-free column reads
-        double* prod = sm_q + D.d;
+        const int E = D.E, CH = kRouteCH;
         const int nchunk = (D.d + CH - 1) / CH;
-        const int fill_lo = (int)blockDim.x - kRouteFillers;  // summers: warps below
-        const int ftid = tid - fill_lo;
-        const bool filler = ftid >= 0;
-        const int total = E * CH;
-        double wreg[kRouteMaxP];
-        auto load = [&](int c) {
-            const int c0 = c * CH, w = min(CH, D.d - c0);
-#pragma unroll
-            for (int u = 0; u < kRouteMaxP; ++u) {
-                const int t = ftid + u * kRouteFillers;
-                const int e = t / CH, i = t % CH;
-                wreg[u] = (c < nchunk && t < total && i < w) ? __ldg(S.W + (int64_t)e * D.d + c0 + i) : 0.0;
+        const int warp = tid >> 5, lane = tid & 31;
+        if (warp == prod_warp) {
+            if (lane == 0) {
+                int stage = 0;
+                uint32_t phase = 0;
+                for (int c = 0; c < nchunk; ++c) {
+                    const int c0 = c * CH, w = min(CH, D.d - c0);
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_expect_tx(&full[stage], (uint32_t)(E * w * 8));
+                    uint8_t* dst = ring + (size_t)stage * E * rowb;
+                    for (int e = 0; e < E; ++e)
+                        bulk_g2s_plain(dst + (size_t)e * rowb, S.W + (int64_t)e * D.d + c0,
+                                       (uint32_t)(w * 8), &full[stage]);
+                    if (++stage == kRouteStages) stage = 0, phase ^= 1;
+                }
             }
-        };
-        auto store = [&](int c, double* buf) {
-            const int c0 = c * CH, w = min(CH, D.d - c0);
-#pragma unroll
-            for (int u = 0; u < kRouteMaxP; ++u) {
-                const int t = ftid + u * kRouteFillers;
-                const int e = t / CH, i = t % CH;
-                if (c < nchunk && t < total && i < w) buf[e * ld + i] = __dmul_rn(wreg[u], sm_q[c0 + i]);
+        } else if (warp < nsum_warps) {
+            double acc = 0.0;
+            int stage = 0;
+            uint32_t phase = 0;
+            const int e = tid;
+            for (int c = 0; c < nchunk; ++c) {
+                const int c0 = c * CH, w = min(CH, D.d - c0);
+                mbar_wait(&full[stage], phase);
+                if (e < E) {
+                    const double* row = (const double*)(ring + (size_t)stage * E * rowb + (size_t)e * rowb);
+                    const double* qq = sm_q + c0;
+#pragma unroll 8
+                    for (int i = 0; i < w; ++i) acc = __dadd_rn(acc, __dmul_rn(row[i], qq[i]));
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[stage]);
+                if (++stage == kRouteStages) stage = 0, phase ^= 1;
             }
-        };
-        double acc = 0.0;
-        if (filler) {
-            load(0);
-            store(0, prod);
-            load(1);
+            if (e < E) sm_logit[e] = acc;
         }
         __syncthreads();
-        for (int c = 0; c < nchunk; ++c) {
-            if (filler) {
-                store(c + 1, prod + ((c + 1) & 1) * E * ld);
-                load(c + 2);
-            } else if (tid < E) {
-                const int w = min(CH, D.d - c * CH);
-                const double* row = prod + (c & 1) * E * ld + tid * ld;
-#pragma unroll 8
-                for (int i = 0; i < w; ++i) acc = __dadd_rn(acc, row[i]);
-            }
-            __syncthreads();
-        }
-        if (tid < E) sm_logit[tid] = acc;
     }
     // codec projection of the query (pipeline.cpp:295-297), fp32
     {
@@ -282,13 +288,11 @@ __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin, in
 }
 
 void launch_route(const Dims& D, const Cfg& C, const State& S, const void* q, cudaStream_t st) {
-    int ch = 256;
-    auto bytes = [&](int c) { return sizeof(double) * ((size_t)D.d + 2 * (size_t)D.E * (c + 1)); };
-    while (ch > 8 && (bytes(ch) > 200 * 1024 || D.E * ch > kRouteMaxP * kRouteFillers)) ch >>= 1;
-    size_t smem = bytes(ch);
+    const size_t smem = 128 + sizeof(double) * (size_t)D.d +
+                        (size_t)kRouteStages * D.E * (kRouteCH * 8 + 16);
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_route, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const int summers = ((D.E + 31) / 32) * 32;
-    k_route<<<D.B, summers + kRouteFillers, smem, st>>>(D, C, S, q, ch);
+    const int threads = ((D.E + 31) / 32) * 32 + 32;
+    k_route<<<D.B, threads, smem, st>>>(D, C, S, q);
 }
 
 // ===========================================================================
@@ -306,7 +310,12 @@ __device__ void encode_row(const Dims& D, const State& S, const void* x, int s, 
     const int64_t base = (int64_t)s * D.d;
     switch (D.codec) {
         case PIKV_CODEC_IDENTITY:
-            if (D.kv_dtype == PIKV_DTYPE_BF16) {
+            if ((D.d * (D.kv_dtype == PIKV_DTYPE_BF16 ? 2 : 4)) % 16 == 0) {
+                const int nv = D.d * (D.kv_dtype == PIKV_DTYPE_BF16 ? 2 : 4) / 16;
+                const uint4* src = (const uint4*)((const uint8_t*)x +
+                                                  base * (D.kv_dtype == PIKV_DTYPE_BF16 ? 2 : 4));
+                for (int i = tid; i < nv; i += nt) ((uint4*)dst)[i] = src[i];
+            } else if (D.kv_dtype == PIKV_DTYPE_BF16) {
                 for (int i = tid; i < D.d; i += nt) ((uint16_t*)dst)[i] = ((const uint16_t*)x)[base + i];
             } else {
                 for (int i = tid; i < D.d; i += nt) ((float*)dst)[i] = ((const float*)x)[base + i];
@@ -391,9 +400,102 @@ __global__ void k_insert(Dims D, Cfg C, State S, const void* __restrict__ kin,
     float* vsc = ksc + D.H;
     encode_row(D, S, kin, s, sm_entry, ksc, tmp);
     encode_row(D, S, vin, s, sm_entry + pay, vsc, tmp);
-    if (tid == 0) {
-        const uint64_t now = S.now[s];
-        const int64_t token = (int64_t)now;
+    // Bookkeeping.  Entry ids are issued in selection order on every rank
+    // (kvstore.cpp:114).  When the k entries hit k distinct rings (the common
+    // case) lanes j < k do their KVStore::insert concurrently; otherwise
+    // thread 0 runs them in order.
+    __shared__ int sm_ring[kMaxK];
+    __shared__ int sm_distinct;
+    const uint64_t now = S.now[s];
+    const int64_t token = (int64_t)now;
+    if (tid < D.k) {
+        const int e = S.experts[(int64_t)s * D.k + tid];
+        const int raw = shard_raw(token, e, D.n_tok, D.n_exp, D.additive);
+        const int dev = raw % D.G;
+        sm_ring[tid] = dev % D.world == D.rank ? (dev / D.world) * D.SPD + raw / D.G : -1 - tid;
+    }
+    if (tid == 0) sm_distinct = 1;
+    __syncthreads();
+    if (tid < D.k)
+        for (int j2 = 0; j2 < tid; ++j2)
+            if (sm_ring[j2] == sm_ring[tid]) sm_distinct = 0;
+    __syncthreads();
+    if (sm_distinct && D.k <= 32) {
+        if (tid < 32) {
+            const int j = tid;
+            const bool act = j < D.k && sm_ring[j] >= 0;
+            bool disp = false;
+            int64_t gi = 0;
+            int32_t page = -1;
+            EvictRec rec{};
+            bool oom = false;
+            if (act) {
+                const int e = S.experts[(int64_t)s * D.k + j];
+                const int raw = shard_raw(token, e, D.n_tok, D.n_exp, D.additive);
+                const int dev = raw % D.G;
+                const int64_t ring = (int64_t)s * D.R + sm_ring[j];
+                const int slot = S.head[ring];
+                gi = ring * D.S + slot;
+                const int64_t pidx = ring * D.ppr + slot / D.spg;
+                page = S.page_table[pidx];
+                const uint64_t old = S.id[gi];
+                if (old != 0) {  // displaced (kvstore.cpp:41-43; pipeline.cpp:200-208)
+                    disp = true;
+                    rec.step = now;
+                    rec.entry_id = old;
+                    rec.token_id = S.token[gi];
+                    rec.expert_id = S.expert[gi];
+                    rec.device = dev;
+                    rec.score = 0.0;
+                    rec.reason = PIKV_EVICT_OVERWRITE;
+                    rec.stream = s;
+                } else {
+                    S.live[ring] += 1;
+                    if (page < 0) {
+                        const int top = atomicSub(S.free_top, 1) - 1;
+                        if (top < 0) {
+                            atomicAdd(S.free_top, 1);
+                            oom = true;
+                        } else {
+                            page = S.free_stack[top];
+                            S.page_table[pidx] = page;
+                            S.page_live[page] = 0;
+                        }
+                    }
+                    if (!oom) S.page_live[page] += 1;
+                }
+                if (!oom) {
+                    S.id[gi] = S.next_id[s] + (uint64_t)j;
+                    S.shard_seq[gi] = S.seq[ring]++;
+                    S.token[gi] = token;
+                    S.expert[gi] = e;
+                    S.insert_step[gi] = now;
+                    S.last_access[gi] = now;
+                    S.freq[gi] = 0;
+                    S.attn_mass[gi] = 0.0;
+                    for (int l = 0; l < D.n_layers; ++l)
+                        S.per_layer[gi * D.n_layers + l] = saliency ? saliency[(int64_t)s * D.n_layers + l] : 0.0;
+                    S.head[ring] = (slot + 1) % D.S;
+                }
+            }
+            const unsigned dm = __ballot_sync(0xffffffffu, disp);
+            const unsigned am = __ballot_sync(0xffffffffu, act && !oom);
+            if (__any_sync(0xffffffffu, oom) && j == 0) S.err[s] = PIKV_ERR_OUT_OF_MEMORY;
+            if (disp) S.rec_ow[(int64_t)s * D.k + __popc(dm & ((1u << j) - 1u))] = rec;
+            if (act && !oom) {
+                const int pos = __popc(am & ((1u << j) - 1u));
+                sm_dst[pos] = (int64_t)page * D.spg + (gi % D.S) % D.spg;
+                sm_slot[pos] = gi;
+            }
+            if (j == 0) {
+                S.n_ow[s] = __popc(dm);
+                S.st_overwrites[s] += (uint64_t)__popc(dm);
+                S.st_inserts[s] += (uint64_t)__popc(am);
+                S.next_id[s] += (uint64_t)D.k;
+                sm_n = __popc(am);
+            }
+        }
+    } else     if (tid == 0) {
         int n = 0;
         for (int j = 0; j < D.k; ++j) {
             const int e = S.experts[(int64_t)s * D.k + j];
@@ -426,7 +528,7 @@ __global__ void k_insert(Dims D, Cfg C, State S, const void* __restrict__ kin,
                     if (top < 0) {
                         atomicAdd(S.free_top, 1);
                         S.err[s] = PIKV_ERR_OUT_OF_MEMORY;
-                        return;
+                        break;
                     }
                     page = S.free_stack[top];
                     S.page_table[pidx] = page;
@@ -960,8 +1062,10 @@ __global__ void k_combine(Dims D, Cfg C, State S, ExchangeLayout X, float* __res
     for (int w = 0; w < nwarp; ++w) L += red[w];
     for (int o = tid; o < D.dph; o += blockDim.x) {
         float acc = 0.f;
-        for (int i = 0; i < nw; ++i)
-            acc = fmaf(S.part_o[((int64_t)(w0 + i) * D.H + h) * D.dph + o], sm_f[i], acc);
+        const float* po = S.part_o + ((int64_t)w0 * D.H + h) * D.dph + o;
+        const int64_t stride = (int64_t)D.H * D.dph;
+#pragma unroll 8
+        for (int i = 0; i < nw; ++i) acc = fmaf(po[i * stride], sm_f[i], acc);
         if (direct) {
             if (y && ok) y[(int64_t)s * D.dp + h * D.dph + o] = L > 0.f ? acc / L : 0.f;
         } else {
@@ -1085,8 +1189,10 @@ __global__ void k_finish_merge(Dims D, Cfg C, State S, ExchangeLayout X,
     }
 }
 
-// attn_mass += alpha, pipeline.cpp:302-312; alpha = mean over heads.  One
-// warp per retrieved entry, lanes over heads (coalesced score reads).
+// attn_mass += alpha, pipeline.cpp:302-312; alpha = mean over heads.  A
+// warp takes 32 retrieved entries: for each, lanes read the per-head logits
+// (coalesced) and reduce alpha; lane j keeps entry j's alpha, then all 32
+// read-modify-writes of attn_mass go out in parallel.
 __global__ void k_foldback(Dims D, State S) {
     __shared__ int64_t sm_base[1025];
     const int nb = D.B + 1;
@@ -1096,26 +1202,34 @@ __global__ void k_foldback(Dims D, State S) {
     const int64_t N = sm_base[D.B];
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t i = gw; i < N; i += nwarps) {
-        int lo = 0, hi = D.B;  // stream: last s with base[s] <= i
+    for (int64_t g0 = gw * 32; g0 < N; g0 += nwarps * 32) {
+        // stream of this lane's entry
+        const int64_t my = g0 + lane;
+        int lo = 0, hi = D.B;
         while (hi - lo > 1) {
             const int mid = (lo + hi) >> 1;
-            if (sm_base[mid] <= i) lo = mid; else hi = mid;
+            if (sm_base[mid] <= my) lo = mid; else hi = mid;
         }
-        const int s = lo;
-        if (S.err[s]) continue;
-        float a = 0.f;
-        for (int h = lane; h < D.H; h += 32) {
-            const float L = S.gL[s * D.H + h];
-            if (L > 0.f) a += exp2f(S.scores[i * D.H + h] - S.gM[s * D.H + h]) / L;
+        const int my_s = lo;
+        float mine = 0.f;
+        const int cnt = (int)min((int64_t)32, N - g0);
+        for (int j = 0; j < cnt; ++j) {
+            const int64_t i = g0 + j;
+            const int s = __shfl_sync(0xffffffffu, my_s, j);
+            float a = 0.f;
+            for (int h = lane; h < D.H; h += 32) {
+                const float L = S.gL[s * D.H + h];
+                if (L > 0.f) a += exp2f(S.scores[i * D.H + h] - S.gM[s * D.H + h]) / L;
+            }
+            for (int off = 16; off; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+            if (lane == j) mine = a;
         }
-        for (int off = 16; off; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
-        if (lane == 0) {
-            const double al = (double)a / (double)D.H;
-            const int64_t gi = S.att_slot[i];
+        if (lane < cnt && !S.err[my_s]) {
+            const double al = (double)mine / (double)D.H;
+            const int64_t gi = S.att_slot[my];
             S.attn_mass[gi] += al;
             if (D.n_layers > 0)
-                S.per_layer[gi * D.n_layers + (int64_t)(S.now[s] % (uint64_t)D.n_layers)] += al;
+                S.per_layer[gi * D.n_layers + (int64_t)(S.now[my_s] % (uint64_t)D.n_layers)] += al;
         }
     }
 }
