@@ -66,14 +66,46 @@ __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin) {
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    // query in fp64 (exact upcast of bf16/f32)
-    for (int i = tid; i < D.d; i += blockDim.x) {
-        double x;
-        if (D.kv_dtype == PIKV_DTYPE_BF16)
-            x = (double)__uint_as_float(((uint32_t)((const uint16_t*)qin)[(int64_t)s * D.d + i]) << 16);
-        else
-            x = (double)((const float*)qin)[(int64_t)s * D.d + i];
-        sm_q[i] = x;
+    // query in fp64 (exact upcast of bf16/f32); 16-byte loads, all in flight
+    {
+        const int esz = D.kv_dtype == PIKV_DTYPE_BF16 ? 2 : 4;
+        const int nvec = (D.d * esz) / 16;
+        const uint8_t* qb = (const uint8_t*)qin + (int64_t)s * D.d * esz;
+        if ((D.d * esz) % 16 == 0) {
+            for (int v0 = tid; v0 < nvec; v0 += 8 * blockDim.x) {
+                uint4 w[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int v = v0 + u * blockDim.x;
+                    if (v < nvec) w[u] = ((const uint4*)qb)[v];
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int v = v0 + u * blockDim.x;
+                    if (v >= nvec) continue;
+                    const uint32_t ww[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
+                    if (esz == 2) {
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) {
+                            sm_q[v * 8 + 2 * t] = (double)bf16_lo(ww[t]);
+                            sm_q[v * 8 + 2 * t + 1] = (double)bf16_hi(ww[t]);
+                        }
+                    } else {
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) sm_q[v * 4 + t] = (double)__uint_as_float(ww[t]);
+                    }
+                }
+            }
+        } else {
+            for (int i = tid; i < D.d; i += blockDim.x) {
+                double x;
+                if (esz == 2)
+                    x = (double)__uint_as_float(((uint32_t)((const uint16_t*)qin)[(int64_t)s * D.d + i]) << 16);
+                else
+                    x = (double)((const float*)qin)[(int64_t)s * D.d + i];
+                sm_q[i] = x;
+            }
+        }
     }
     __syncthreads();
     const bool base = C.router_strategy == PIKV_ROUTER_BASE;
@@ -655,6 +687,7 @@ __global__ void __launch_bounds__(kSelThreads) k_sched_select(Dims D, Cfg C, Sta
     const bool use_theta = C.sched_strategy == PIKV_SCHED_ADAKV;
     // count pages and below-theta pages
     int P = 0, T = 0;
+#pragma unroll 4
     for (int i = tid; i < npg; i += kSelThreads) {
         if (S.pg_cnt[first + i] > 0) {
             ++P;
@@ -694,6 +727,7 @@ __global__ void __launch_bounds__(kSelThreads) k_sched_select(Dims D, Cfg C, Sta
             double ba = 0.0;
             uint64_t bo = 0;
             int bi = -1;
+#pragma unroll 4
             for (int i = tid; i < npg; i += kSelThreads) {
                 if (S.pg_cnt[first + i] <= 0) continue;
                 const double a = S.pg_agg[first + i];
@@ -756,29 +790,29 @@ __global__ void __launch_bounds__(kSelThreads) k_sched_select(Dims D, Cfg C, Sta
         for (int v = tid; v < V; v += kSelThreads) S.pg_cnt[first + list[v]] = -S.pg_cnt[first + list[v]];
         __syncthreads();
     }
-    // erase victims in order; record offsets by prefix of member counts
+    // erase victims in order (scheduler.cpp:305-326): a warp per victim page,
+    // lanes over its members in id (= shard_seq) order; record offsets are the
+    // exclusive prefix of member counts over victims (block scan) plus the
+    // ballot rank inside the page.
     __shared__ int sm_off;
+    __shared__ int vcnt_off[kSelThreads];
     if (tid == 0) sm_off = 0;
     __syncthreads();
     const uint64_t sstep = S.sstep[s];
     const uint64_t now = S.now[s];
     const int dev = gl * D.world + D.rank;
     EvictRec* rec = S.rec_ev + (int64_t)sg * D.SPD * D.S;
+    const int lane = tid & 31, warp = tid >> 5;
     for (int v0 = 0; v0 < V; v0 += kSelThreads) {
         const int v = v0 + tid;
-        int cnt = 0, pidx = -1;
-        if (v < V) {
-            pidx = list[v];
-            cnt = -S.pg_cnt[first + pidx];
-        }
-        // block exclusive scan of cnt
+        const int cnt = v < V ? -S.pg_cnt[first + list[v]] : 0;
         int x = cnt;
         for (int off = 1; off < 32; off <<= 1) {
             int y = __shfl_up_sync(0xffffffffu, x, off);
-            if ((tid & 31) >= off) x += y;
+            if (lane >= off) x += y;
         }
         __shared__ int wsum[32];
-        if ((tid & 31) == 31) wsum[tid >> 5] = x;
+        if (lane == 31) wsum[warp] = x;
         __syncthreads();
         if (tid < 32) {
             int w = wsum[tid];
@@ -789,42 +823,54 @@ __global__ void __launch_bounds__(kSelThreads) k_sched_select(Dims D, Cfg C, Sta
             wsum[tid] = w;
         }
         __syncthreads();
-        const int excl = x - cnt + ((tid >> 5) ? wsum[(tid >> 5) - 1] : 0) + sm_off;
-        if (v < V) {
-            const int reason = v < sm_thr ? PIKV_EVICT_THRESHOLD : PIKV_EVICT_BUDGET;
+        vcnt_off[tid] = x - cnt + (warp ? wsum[warp - 1] : 0) + sm_off;
+        __syncthreads();
+        const int nv = min(kSelThreads, V - v0);
+        for (int vv = warp; vv < nv; vv += kSelThreads / 32) {
+            const int pidx = list[v0 + vv];
+            const int reason = (v0 + vv) < sm_thr ? PIKV_EVICT_THRESHOLD : PIKV_EVICT_BUDGET;
             const int64_t ring = (int64_t)sg * D.SPD + pidx / D.ppr_sched;
             const uint64_t seq = S.seq[ring];
             const uint64_t Su = (uint64_t)D.S, ps = (uint64_t)D.page_size;
             const uint64_t lo = seq > Su ? seq - Su : 0;
             const uint64_t q = lo / ps + (uint64_t)(pidx % D.ppr_sched);
-            int o = excl;
-            for (uint64_t sq = q * ps; sq < (q + 1) * ps; ++sq) {  // id order
-                const int slot = (int)(sq % Su);
-                const int64_t gi = ring * D.S + slot;
-                if (S.id[gi] == 0 || S.shard_seq[gi] != sq) continue;
-                EvictRec& r = rec[o++];
-                r.step = sstep;
-                r.entry_id = S.id[gi];
-                r.token_id = S.token[gi];
-                r.expert_id = S.expert[gi];
-                r.device = dev;
-                r.score = score_entry(C, S, gi, now, D.n_layers);
-                r.reason = reason;
-                r.stream = s;
-                // KVStore::erase (kvstore.cpp:180-185) + page reclamation
-                S.id[gi] = 0;
-                atomicSub(&S.live[ring], 1);
-                const int64_t pt_i = ring * D.ppr + slot / D.spg;
-                const int32_t page = S.page_table[pt_i];
-                if (atomicSub(&S.page_live[page], 1) == 1) {
-                    S.page_table[pt_i] = -1;
-                    const int top = atomicAdd(S.free_top, 1);
-                    S.free_stack[top] = page;
+            int o = vcnt_off[vv];
+            for (uint64_t b = 0; b < ps; b += 32) {
+                const uint64_t sq = q * ps + b + lane;
+                bool mem = false;
+                int64_t gi = 0;
+                if (b + lane < ps) {
+                    gi = ring * D.S + (int64_t)(sq % Su);
+                    mem = S.id[gi] != 0 && S.shard_seq[gi] == sq;
                 }
+                const unsigned bal = __ballot_sync(0xffffffffu, mem);
+                if (mem) {
+                    EvictRec& r = rec[o + __popc(bal & ((1u << lane) - 1u))];
+                    r.step = sstep;
+                    r.entry_id = S.id[gi];
+                    r.token_id = S.token[gi];
+                    r.expert_id = S.expert[gi];
+                    r.device = dev;
+                    r.score = score_entry(C, S, gi, now, D.n_layers);
+                    r.reason = reason;
+                    r.stream = s;
+                    // KVStore::erase (kvstore.cpp:180-185) + page reclamation
+                    S.id[gi] = 0;
+                    atomicSub(&S.live[ring], 1);
+                    const int slot = (int)(sq % Su);
+                    const int64_t pt_i = ring * D.ppr + slot / D.spg;
+                    const int32_t page = S.page_table[pt_i];
+                    if (atomicSub(&S.page_live[page], 1) == 1) {
+                        S.page_table[pt_i] = -1;
+                        const int top = atomicAdd(S.free_top, 1);
+                        S.free_stack[top] = page;
+                    }
+                }
+                o += __popc(bal);
             }
         }
         __syncthreads();
-        if (tid == kSelThreads - 1) sm_off = excl + cnt;
+        if (tid == kSelThreads - 1) sm_off = vcnt_off[tid] + cnt;
         __syncthreads();
     }
     if (tid == 0) S.n_ev[sg] = sm_off;
@@ -1213,6 +1259,7 @@ __global__ void k_foldback(Dims D, State S) {
         const int my_s = lo;
         float mine = 0.f;
         const int cnt = (int)min((int64_t)32, N - g0);
+#pragma unroll 8
         for (int j = 0; j < cnt; ++j) {
             const int64_t i = g0 + j;
             const int s = __shfl_sync(0xffffffffu, my_s, j);
