@@ -399,6 +399,27 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
     std::memcpy(C.adakv_weights, c.adakv_weights, sizeof(C.adakv_weights));
     std::memcpy(C.flex_plan, c.flex_plan, sizeof(C.flex_plan));
     C.unbounded_budget = c.unbounded_budget, C.head_width = c.head_width;
+    // Page aggregates (scheduler.cpp:276-289) are summed in slot order.  When
+    // every score is an integer multiple of 2^-10 and the page sum stays below
+    // 2^42 in magnitude, each partial sum is exact, so any summation order is
+    // bit-identical and the kernel may use a tree reduction.  True for LRU
+    // (-recency) and SL ({0,1,2,3}) always, for LRUPlus when lambda*1024 is an
+    // integer, and for Flex when every plan value is such a multiple.  With
+    // step counters < 2^31: LRU |sum| <= ps 2^31 < 2^53; LRUPlus needs
+    // ps (1 + |lambda|) 2^31 2^10 <= 2^53; Flex |plan| < 2^20 -> ps 2^30 <= 2^53.
+    {
+        auto dyadic = [](double x) { return std::isfinite(x) && std::fabs(x) < 1048576.0 &&
+                                            std::nearbyint(x * 1024.0) == x * 1024.0; };
+        bool ex = false;
+        if (c.sched_strategy == PIKV_SCHED_LRU || c.sched_strategy == PIKV_SCHED_SL) ex = true;
+        if (c.sched_strategy == PIKV_SCHED_LRU_PLUS)
+            ex = dyadic(c.lambda_freq) && (double)c.page_size * (1.0 + std::fabs(c.lambda_freq)) <= 4096.0;
+        if (c.sched_strategy == PIKV_SCHED_FLEX) {
+            ex = true;
+            for (int i = 0; i < c.n_flex_plan; ++i) ex = ex && dyadic(c.flex_plan[i]);
+        }
+        C.exact_sum = ex && c.page_size <= 1024 ? 1 : 0;
+    }
 
     // exchange record layout
     ExchangeLayout& X = eng->X;

@@ -137,10 +137,29 @@ __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin) {
                 const int c0 = c * CH, w = min(CH, D.d - c0);
                 mbar_wait(&full[stage], phase);
                 if (e < E) {
+                    // software pipeline: the 16 products of batch b+1 are
+                    // loaded and multiplied while batch b runs the DADD chain
                     const double* row = (const double*)(ring + (size_t)stage * E * rowb + (size_t)e * rowb);
                     const double* qq = sm_q + c0;
-#pragma unroll 8
-                    for (int i = 0; i < w; ++i) acc = __dadd_rn(acc, __dmul_rn(row[i], qq[i]));
+                    constexpr int NBt = 16;
+                    double pa[NBt], pb[NBt];
+                    auto prod = [&](int i0, double* p) {
+#pragma unroll
+                        for (int u = 0; u < NBt; ++u)
+                            p[u] = (i0 + u < w) ? __dmul_rn(row[i0 + u], qq[i0 + u]) : 0.0;
+                    };
+                    auto chain = [&](int i0, const double* p) {
+#pragma unroll
+                        for (int u = 0; u < NBt; ++u)
+                            if (i0 + u < w) acc = __dadd_rn(acc, p[u]);
+                    };
+                    prod(0, pa);
+                    for (int i0 = 0; i0 < w; i0 += 2 * NBt) {
+                        prod(i0 + NBt, pb);
+                        chain(i0, pa);
+                        prod(i0 + 2 * NBt, pa);
+                        chain(i0 + NBt, pb);
+                    }
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[stage]);
@@ -648,9 +667,17 @@ __global__ void k_sched_pages(Dims D, Cfg C, State S, int lanes) {
         const unsigned bal = __ballot_sync(0xffffffffu, mem) & gmask;
         cnt += __popc(bal);
         if (mem && id < oldest) oldest = id;
-        for (int v = 0; v < lanes; ++v) {  // sequential fp64 sum in slot order
-            const double x = __shfl_sync(0xffffffffu, sc, sub * lanes + v);
-            if (bal & (1u << (sub * lanes + v))) agg = __dadd_rn(agg, x);
+        if (C.exact_sum) {
+            // every score and partial sum is exactly representable (integer /
+            // dyadic scores, host-checked bound), so any order is bit-identical
+            double x = mem ? sc : 0.0;
+            for (int off = lanes >> 1; off; off >>= 1) x = __dadd_rn(x, __shfl_xor_sync(0xffffffffu, x, off));
+            if (bal) agg = __dadd_rn(agg, x);
+        } else {
+            for (int v = 0; v < lanes; ++v) {  // sequential fp64 sum in slot order
+                const double x = __shfl_sync(0xffffffffu, sc, sub * lanes + v);
+                if (bal & (1u << (sub * lanes + v))) agg = __dadd_rn(agg, x);
+            }
         }
     }
     for (int off = lanes >> 1; off; off >>= 1) {
@@ -1235,49 +1262,49 @@ __global__ void k_finish_merge(Dims D, Cfg C, State S, ExchangeLayout X,
     }
 }
 
-// attn_mass += alpha, pipeline.cpp:302-312; alpha = mean over heads.  A
-// warp takes 32 retrieved entries: for each, lanes read the per-head logits
-// (coalesced) and reduce alpha; lane j keeps entry j's alpha, then all 32
-// read-modify-writes of attn_mass go out in parallel.
+// attn_mass += alpha, pipeline.cpp:302-312; alpha = mean over heads.  One
+// thread per retrieved entry (its H logits are contiguous: 16-byte loads);
+// the global (M, 1/L) of every (stream, head) are staged in shared memory.
 __global__ void k_foldback(Dims D, State S) {
+    extern __shared__ float sm_ml[];  // [B*H] M, then [B*H] 1/L (0 when empty)
     __shared__ int64_t sm_base[1025];
     const int nb = D.B + 1;
+    const int BH = D.B * D.H;
     for (int i = threadIdx.x; i < nb; i += blockDim.x) sm_base[i] = S.att_base[i];
+    for (int i = threadIdx.x; i < BH; i += blockDim.x) {
+        sm_ml[i] = S.gM[i];
+        const float L = S.gL[i];
+        sm_ml[BH + i] = L > 0.f ? 1.f / L : 0.f;
+    }
     __syncthreads();
-    const int lane = threadIdx.x & 31;
     const int64_t N = sm_base[D.B];
-    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t g0 = gw * 32; g0 < N; g0 += nwarps * 32) {
-        // stream of this lane's entry
-        const int64_t my = g0 + lane;
-        int lo = 0, hi = D.B;
+    const bool vec = (D.H % 4) == 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int lo = 0, hi = D.B;  // stream: last s with base[s] <= i
         while (hi - lo > 1) {
             const int mid = (lo + hi) >> 1;
-            if (sm_base[mid] <= my) lo = mid; else hi = mid;
+            if (sm_base[mid] <= i) lo = mid; else hi = mid;
         }
-        const int my_s = lo;
-        float mine = 0.f;
-        const int cnt = (int)min((int64_t)32, N - g0);
-#pragma unroll 8
-        for (int j = 0; j < cnt; ++j) {
-            const int64_t i = g0 + j;
-            const int s = __shfl_sync(0xffffffffu, my_s, j);
-            float a = 0.f;
-            for (int h = lane; h < D.H; h += 32) {
-                const float L = S.gL[s * D.H + h];
-                if (L > 0.f) a += exp2f(S.scores[i * D.H + h] - S.gM[s * D.H + h]) / L;
+        const int s = lo;
+        if (S.err[s]) continue;
+        const float* M = sm_ml + s * D.H;
+        const float* iL = sm_ml + BH + s * D.H;
+        const float* sc = S.scores + i * D.H;
+        float a = 0.f;
+        if (vec) {
+            for (int h = 0; h < D.H; h += 4) {
+                const float4 v = *(const float4*)(sc + h);
+                a += exp2f(v.x - M[h]) * iL[h] + exp2f(v.y - M[h + 1]) * iL[h + 1] +
+                     exp2f(v.z - M[h + 2]) * iL[h + 2] + exp2f(v.w - M[h + 3]) * iL[h + 3];
             }
-            for (int off = 16; off; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
-            if (lane == j) mine = a;
+        } else {
+            for (int h = 0; h < D.H; ++h) a += exp2f(sc[h] - M[h]) * iL[h];
         }
-        if (lane < cnt && !S.err[my_s]) {
-            const double al = (double)mine / (double)D.H;
-            const int64_t gi = S.att_slot[my];
-            S.attn_mass[gi] += al;
-            if (D.n_layers > 0)
-                S.per_layer[gi * D.n_layers + (int64_t)(S.now[my_s] % (uint64_t)D.n_layers)] += al;
-        }
+        const double al = (double)a / (double)D.H;
+        const int64_t gi = S.att_slot[i];
+        S.attn_mass[gi] += al;
+        if (D.n_layers > 0) S.per_layer[gi * D.n_layers + (int64_t)(S.now[s] % (uint64_t)D.n_layers)] += al;
     }
 }
 
@@ -1318,7 +1345,9 @@ void launch_finish_merge(const Dims& D, const Cfg& C, const State& S, const Exch
     k_finish_merge<<<D.B, 256, 0, st>>>(D, C, S, X, gathered, y);
 }
 void launch_foldback(const Dims& D, const State& S, cudaStream_t st) {
-    k_foldback<<<D.attend_ctas * 2, 256, 0, st>>>(D, S);
+    const size_t smem = sizeof(float) * 2 * (size_t)D.B * D.H;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_foldback, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_foldback<<<D.attend_ctas * 2, 256, smem, st>>>(D, S);
 }
 void launch_feedback(const Dims& D, const Cfg& C, const State& S, cudaStream_t st) {
     k_feedback<<<(D.B + 127) / 128, 128, 0, st>>>(D, C, S);

@@ -68,6 +68,7 @@ struct Cfg {  // scalar config needed on device (copied by value into kernels)
     double adakv_weights[8];
     double flex_plan[32];
     int unbounded_budget, head_width;
+    int exact_sum;  // page aggregates are exact in any order (see capi.cu)
 };
 
 struct State {
