@@ -506,6 +506,7 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
     chk(S.gM = eng->alloc<float>((size_t)B * D.H));
     chk(S.gL = eng->alloc<float>((size_t)B * D.H));
     chk(S.summary = eng->alloc<pikv_step_summary>(B));
+    chk(S.dbg = eng->alloc<long long>(64));
     const size_t in_elem = c.kv_dtype == PIKV_DTYPE_BF16 ? 2 : 4;
     chk(eng->in_q = eng->alloc<uint8_t>((size_t)B * D.d * in_elem));
     chk(eng->in_k = eng->alloc<uint8_t>((size_t)B * D.d * in_elem));
@@ -638,7 +639,7 @@ static int enqueue_local(pikv_engine* eng, const void* q, const void* k, const v
     mark(eng, 1);
     // a rank that owns no device still issues entry ids (k_insert) and joins
     // the merge with an empty record
-    launch_insert(D, eng->C, S, k, v, sal, st), ++n;
+    launch_insert(D, eng->C, S, q, k, v, sal, st), ++n;
     mark(eng, 2);
     const bool sched = D.Gl > 0 && !eng->C.unbounded_budget;
     if (sched) launch_sched_pages(D, eng->C, S, st), ++n;
@@ -970,6 +971,13 @@ int64_t pikv_pool_pages_in_use(pikv_engine* eng) {
 }
 
 int64_t pikv_entry_bytes(pikv_engine* eng) { return eng->D.entry_bytes; }
+
+// Not part of the public header: debug timestamps written by kernels.
+int pikv_debug_read(pikv_engine* eng, long long* out, int n) {
+    CUDA_TRY(cudaStreamSynchronize(eng->stream));
+    CUDA_TRY(cudaMemcpy(out, eng->S.dbg, sizeof(long long) * std::min(n, 64), cudaMemcpyDeviceToHost));
+    return PIKV_OK;
+}
 int64_t pikv_kernel_launches(pikv_engine* eng) { return eng->launches; }
 
 int pikv_set_profiling(pikv_engine* eng, int32_t on) {

@@ -33,8 +33,13 @@ namespace pikv_dev {
 // copies (one per expert row segment, issued by the producer lane of the
 // last warp), so the chain never waits on L2.  Thread 0 then runs the
 // strategy penalty, selection, gate softmax and note_selection.
+__device__ __noinline__ void route_select(const Dims& D, const Cfg& C, const State& S, int s,
+                                          double* sm_logit, bool* sm_flag, int* sm_pool,
+                                          double* load, uint64_t* usage, const uint64_t* miss,
+                                          const double* bias, int* sel);
+
 constexpr int kRouteCH = 256;    // columns per stage
-constexpr int kRouteStages = 3;
+constexpr int kRouteStages = 5;
 
 __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin) {
     extern __shared__ __align__(128) uint8_t sm_raw[];
@@ -46,6 +51,9 @@ __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin) {
     __shared__ double sm_logit[kMaxE];
     __shared__ bool sm_flag[kMaxE];
     __shared__ int sm_pool[kMaxE];
+    __shared__ double sm_load[kMaxE], sm_bias[kMaxE];
+    __shared__ uint64_t sm_usage[kMaxE], sm_miss[kMaxE];
+    __shared__ int sm_sel[kMaxK];
     const int s = blockIdx.x;
     const int tid = threadIdx.x;
     const int nsum_warps = (D.E + 31) / 32;
@@ -59,6 +67,16 @@ __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin) {
     }
     for (int j = tid; j < D.k; j += blockDim.x) S.found[(int64_t)s * D.k + j] = 0;
     if (S.err[s]) return;
+    // router state of this stream -> smem (thread 0's serial part reads it
+    // without dependent global round trips)
+    for (int e = tid; e < D.E; e += blockDim.x) {
+        sm_load[e] = S.load[(int64_t)s * D.E + e];
+        sm_usage[e] = S.usage[(int64_t)s * D.E + e];
+        sm_miss[e] = S.miss[(int64_t)s * D.E + e];
+        sm_bias[e] = S.bias[(int64_t)s * D.E + e];
+    }
+    const bool dbg = s == 0 && tid == 0 && S.dbg;
+    if (dbg) S.dbg[0] = clock64();
     if (tid == 0) {
         for (int i = 0; i < kRouteStages; ++i) {
             mbar_init(&full[i], 1);
@@ -108,6 +126,7 @@ __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin) {
         }
     }
     __syncthreads();
+    if (dbg) S.dbg[1] = clock64();
     const bool base = C.router_strategy == PIKV_ROUTER_BASE;
     if (!base) {
         const int E = D.E, CH = kRouteCH;
@@ -133,9 +152,12 @@ __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin) {
             int stage = 0;
             uint32_t phase = 0;
             const int e = tid;
+            long long t_wait = 0;
             for (int c = 0; c < nchunk; ++c) {
                 const int c0 = c * CH, w = min(CH, D.d - c0);
+                const long long tw0 = clock64();
                 mbar_wait(&full[stage], phase);
+                t_wait += clock64() - tw0;
                 if (e < E) {
                     // software pipeline: the 16 products of batch b+1 are
                     // loaded and multiplied while batch b runs the DADD chain
@@ -166,47 +188,34 @@ __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin) {
                 if (++stage == kRouteStages) stage = 0, phase ^= 1;
             }
             if (e < E) sm_logit[e] = acc;
+            if (dbg) S.dbg[5] = t_wait;
         }
         __syncthreads();
     }
-    // codec projection of the query (pipeline.cpp:295-297), fp32
-    {
-        const int H = D.H, hd = D.d / D.H, r = D.dph;
-        float* qa = S.q_attn + (int64_t)s * D.dp;
-        for (int o = tid; o < D.dp; o += blockDim.x) {
-            const int h = o / r, j = o % r;
-            float val;
-            switch (D.codec) {
-                case PIKV_CODEC_LOWRANK:
-                case PIKV_CODEC_LORAPLUS: {
-                    const float* col = S.basis + ((int64_t)h * r + j) * hd;
-                    float acc = 0.f;
-                    for (int i = 0; i < hd; ++i) {
-                        float xi = (float)sm_q[h * hd + i];
-                        if (D.codec == PIKV_CODEC_LORAPLUS) xi -= S.cbias[h * hd + i];
-                        acc = fmaf(col[i], xi, acc);
-                    }
-                    val = acc;
-                    break;
-                }
-                case PIKV_CODEC_FASTV: val = (float)sm_q[h * hd + j]; break;
-                case PIKV_CODEC_PRUNE: val = (float)sm_q[h * hd + S.kept[h * r + j]]; break;
-                default: val = (float)sm_q[o]; break;
-            }
-            qa[o] = val;
-        }
-        (void)H;
-    }
+    if (dbg) S.dbg[2] = clock64();
+    if (dbg) S.dbg[3] = clock64();
+    if (tid == 0) route_select(D, C, S, s, sm_logit, sm_flag, sm_pool, sm_load, sm_usage, sm_miss,
+                               sm_bias, sm_sel);
     __syncthreads();
-    if (tid != 0) return;
+    if (S.err[s]) return;
+    for (int e = tid; e < D.E; e += blockDim.x) S.load[(int64_t)s * D.E + e] = sm_load[e];
+    for (int j = tid; j < D.k; j += blockDim.x) {
+        S.usage[(int64_t)s * D.E + sm_sel[j]] = sm_usage[sm_sel[j]];
+        S.experts[(int64_t)s * D.k + j] = sm_sel[j];
+    }
+    if (dbg) S.dbg[4] = clock64();
+}
 
+// Thread 0 of k_route: penalties, selection, gates, note_selection and the
+// retrieval candidate rings, on the smem copy of RouterState.
+__device__ __noinline__ void route_select(const Dims& D, const Cfg& C, const State& S, int s,
+                                          double* sm_logit, bool* sm_flag, int* sm_pool,
+                                          double* load, uint64_t* usage, const uint64_t* miss,
+                                          const double* bias, int* sel) {
     const int E = D.E, k = D.k;
-    double* load = S.load + (int64_t)s * E;
-    uint64_t* usage = S.usage + (int64_t)s * E;
-    int32_t* experts = S.experts + (int64_t)s * k;
     double* gates = S.gates + (int64_t)s * k;
     double* lg = S.logits + (int64_t)s * E;
-    int sel[kMaxK];
+    const bool base = C.router_strategy == PIKV_ROUTER_BASE;
     if (base) {  // base_round_robin, router.cpp:107-118
         int64_t t = (int64_t)S.rstep[s];
         for (int j = 0; j < k; ++j) sel[j] = (int)((t * C.stride + j) % E);
@@ -230,8 +239,7 @@ __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin) {
             }
             case PIKV_ROUTER_CACHE_AWARE:
                 for (int e = 0; e < E; ++e)
-                    sm_logit[e] = __dsub_rn(sm_logit[e], __dmul_rn(C.lambda_miss,
-                                                                  log1p((double)S.miss[(int64_t)s * E + e])));
+                    sm_logit[e] = __dsub_rn(sm_logit[e], __dmul_rn(C.lambda_miss, log1p((double)miss[e])));
                 break;
             case PIKV_ROUTER_ENTROPY_LB: {
                 uint64_t tot = S.total_usage[s];
@@ -244,7 +252,7 @@ __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin) {
             }
             case PIKV_ROUTER_ADAPTIVE:
                 for (int e = 0; e < E; ++e)
-                    sm_logit[e] = __dadd_rn(sm_logit[e], S.bias[(int64_t)s * E + e]);
+                    sm_logit[e] = __dadd_rn(sm_logit[e], bias[e]);
                 break;
             default:
                 break;
@@ -315,10 +323,7 @@ __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin) {
         for (int j = 0; j < k; ++j) picked |= sel[j] == e;
         load[e] = __dadd_rn(__dmul_rn(C.load_decay, load[e]), __dmul_rn(one_m, picked ? 1.0 : 0.0));
     }
-    for (int j = 0; j < k; ++j) {
-        usage[sel[j]] += 1;
-        experts[j] = sel[j];
-    }
+    for (int j = 0; j < k; ++j) usage[sel[j]] += 1;
     S.total_usage[s] += (uint64_t)k;
     S.rstep[s] += 1;
 
@@ -437,8 +442,9 @@ __device__ void encode_row(const Dims& D, const State& S, const void* x, int s, 
     }
 }
 
-__global__ void k_insert(Dims D, Cfg C, State S, const void* __restrict__ kin,
-                         const void* __restrict__ vin, const double* __restrict__ saliency) {
+__global__ void k_insert(Dims D, Cfg C, State S, const void* __restrict__ qin,
+                         const void* __restrict__ kin, const void* __restrict__ vin,
+                         const double* __restrict__ saliency) {
     extern __shared__ __align__(16) uint8_t sm_entry[];  // [entry_bytes] + tmp floats [d]
     __shared__ int64_t sm_dst[kMaxK];
     __shared__ int64_t sm_slot[kMaxK];
@@ -451,6 +457,34 @@ __global__ void k_insert(Dims D, Cfg C, State S, const void* __restrict__ kin,
     float* vsc = ksc + D.H;
     encode_row(D, S, kin, s, sm_entry, ksc, tmp);
     encode_row(D, S, vin, s, sm_entry + pay, vsc, tmp);
+    // the query in the stored (compressed) space, fp32 (pipeline.cpp:295-297)
+    {
+        const int hd = D.d / D.H, r = D.dph;
+        const int64_t base = (int64_t)s * D.d;
+        float* qa = S.q_attn + (int64_t)s * D.dp;
+        for (int o = tid; o < D.dp; o += blockDim.x) {
+            const int h = o / r, j = o % r;
+            float val;
+            switch (D.codec) {
+                case PIKV_CODEC_LOWRANK:
+                case PIKV_CODEC_LORAPLUS: {
+                    const float* col = S.basis + ((int64_t)h * r + j) * hd;
+                    float acc = 0.f;
+                    for (int i = 0; i < hd; ++i) {
+                        float xi = load_in(qin, D.kv_dtype, base + h * hd + i);
+                        if (D.codec == PIKV_CODEC_LORAPLUS) xi -= S.cbias[h * hd + i];
+                        acc = fmaf(col[i], xi, acc);
+                    }
+                    val = acc;
+                    break;
+                }
+                case PIKV_CODEC_FASTV: val = load_in(qin, D.kv_dtype, base + h * hd + j); break;
+                case PIKV_CODEC_PRUNE: val = load_in(qin, D.kv_dtype, base + h * hd + S.kept[h * r + j]); break;
+                default: val = load_in(qin, D.kv_dtype, base + o); break;
+            }
+            qa[o] = val;
+        }
+    }
     // Bookkeeping.  Entry ids are issued in selection order on every rank
     // (kvstore.cpp:114).  When the k entries hit k distinct rings (the common
     // case) lanes j < k do their KVStore::insert concurrently; otherwise
@@ -615,11 +649,11 @@ __global__ void k_insert(Dims D, Cfg C, State S, const void* __restrict__ kin,
     }
 }
 
-void launch_insert(const Dims& D, const Cfg& C, const State& S, const void* k, const void* v,
-                   const double* saliency, cudaStream_t st) {
+void launch_insert(const Dims& D, const Cfg& C, const State& S, const void* q, const void* k,
+                   const void* v, const double* saliency, cudaStream_t st) {
     size_t smem = (size_t)((D.entry_bytes + 15) & ~15) + sizeof(float) * (size_t)D.d;
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_insert, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_insert<<<D.B, 256, smem, st>>>(D, C, S, k, v, saliency);
+    k_insert<<<D.B, 256, smem, st>>>(D, C, S, q, k, v, saliency);
 }
 
 // ===========================================================================

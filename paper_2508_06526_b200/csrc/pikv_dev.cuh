@@ -150,6 +150,7 @@ struct State {
     float* gM;              // [B][H] global max (base 2)
     float* gL;              // [B][H]
     pikv_step_summary* summary;  // [B]
+    long long* dbg;              // [64] debug timestamps (k_route, stream 0)
 };
 
 // ---- helpers -------------------------------------------------------------
@@ -275,8 +276,8 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
 
 // ---- launch wrappers (defined in the .cu files) ----------------------------
 void launch_route(const Dims& D, const Cfg& C, const State& S, const void* q, cudaStream_t st);
-void launch_insert(const Dims& D, const Cfg& C, const State& S, const void* k, const void* v,
-                   const double* saliency, cudaStream_t st);
+void launch_insert(const Dims& D, const Cfg& C, const State& S, const void* q, const void* k,
+                   const void* v, const double* saliency, cudaStream_t st);
 void launch_sched_pages(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);
 void launch_sched_select(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);
 void launch_retr_count(const Dims& D, const State& S, cudaStream_t st);
