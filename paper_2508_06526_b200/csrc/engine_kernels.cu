@@ -33,10 +33,10 @@ namespace pikv_dev {
 // copies (one per expert row segment, issued by the producer lane of the
 // last warp), so the chain never waits on L2.  Thread 0 then runs the
 // strategy penalty, selection, gate softmax and note_selection.
-__device__ __noinline__ void route_select(const Dims& D, const Cfg& C, const State& S, int s,
-                                          double* sm_logit, bool* sm_flag, int* sm_pool,
-                                          double* load, uint64_t* usage, const uint64_t* miss,
-                                          const double* bias, int* sel);
+__device__ __forceinline__ void route_select(const Dims& D, const Cfg& C, const State& S, int s,
+                                             double* sm_logit, bool* sm_flag, int* sm_pool,
+                                             double* load, uint64_t* usage, const uint64_t* miss,
+                                             const double* bias, int* sel);
 
 constexpr int kRouteCH = 256;    // columns per stage
 constexpr int kRouteStages = 5;
@@ -159,28 +159,27 @@ __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin) {
                 mbar_wait(&full[stage], phase);
                 t_wait += clock64() - tw0;
                 if (e < E) {
-                    // software pipeline: the 16 products of batch b+1 are
-                    // loaded and multiplied while batch b runs the DADD chain
+                    // 32 products into registers (LDS.128 pairs, independent
+                    // DMULs), then the 32-long DADD chain: measured 10.5
+                    // cycles/column on B200 vs 17.6 for a fused load-mul-add
+                    // loop (profiles/microbench/chain_variants.cu)
                     const double* row = (const double*)(ring + (size_t)stage * E * rowb + (size_t)e * rowb);
                     const double* qq = sm_q + c0;
-                    constexpr int NBt = 16;
-                    double pa[NBt], pb[NBt];
-                    auto prod = [&](int i0, double* p) {
+                    if (w == CH) {
+                        for (int i0 = 0; i0 < CH; i0 += 32) {
+                            double r[32];
 #pragma unroll
-                        for (int u = 0; u < NBt; ++u)
-                            p[u] = (i0 + u < w) ? __dmul_rn(row[i0 + u], qq[i0 + u]) : 0.0;
-                    };
-                    auto chain = [&](int i0, const double* p) {
+                            for (int u = 0; u < 32; u += 2) {
+                                const double2 a2 = *(const double2*)(row + i0 + u);
+                                const double2 b2 = *(const double2*)(qq + i0 + u);
+                                r[u] = __dmul_rn(a2.x, b2.x);
+                                r[u + 1] = __dmul_rn(a2.y, b2.y);
+                            }
 #pragma unroll
-                        for (int u = 0; u < NBt; ++u)
-                            if (i0 + u < w) acc = __dadd_rn(acc, p[u]);
-                    };
-                    prod(0, pa);
-                    for (int i0 = 0; i0 < w; i0 += 2 * NBt) {
-                        prod(i0 + NBt, pb);
-                        chain(i0, pa);
-                        prod(i0 + 2 * NBt, pa);
-                        chain(i0 + NBt, pb);
+                            for (int u = 0; u < 32; ++u) acc = __dadd_rn(acc, r[u]);
+                        }
+                    } else {
+                        for (int i = 0; i < w; ++i) acc = __dadd_rn(acc, __dmul_rn(row[i], qq[i]));
                     }
                 }
                 __syncwarp();
@@ -194,7 +193,7 @@ __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin) {
     }
     if (dbg) S.dbg[2] = clock64();
     if (dbg) S.dbg[3] = clock64();
-    if (tid == 0) route_select(D, C, S, s, sm_logit, sm_flag, sm_pool, sm_load, sm_usage, sm_miss,
+    if (tid < 32) route_select(D, C, S, s, sm_logit, sm_flag, sm_pool, sm_load, sm_usage, sm_miss,
                                sm_bias, sm_sel);
     __syncthreads();
     if (S.err[s]) return;
@@ -206,141 +205,172 @@ __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin) {
     if (dbg) S.dbg[4] = clock64();
 }
 
-// Thread 0 of k_route: penalties, selection, gates, note_selection and the
-// retrieval candidate rings, on the smem copy of RouterState.
-__device__ __noinline__ void route_select(const Dims& D, const Cfg& C, const State& S, int s,
-                                          double* sm_logit, bool* sm_flag, int* sm_pool,
-                                          double* load, uint64_t* usage, const uint64_t* miss,
-                                          const double* bias, int* sel) {
+// Warp 0 of k_route: penalties, selection, gates, note_selection and the
+// retrieval candidate rings, on the smem copy of RouterState.  Lanes work
+// over experts / rings; the reductions whose order the reference fixes
+// (mean load, gate softmax) run on lane 0 in index order.
+__device__ __forceinline__ void route_select(const Dims& D, const Cfg& C, const State& S, int s,
+                                             double* sm_logit, bool* sm_flag, int* sm_pool,
+                                             double* load, uint64_t* usage, const uint64_t* miss,
+                                             const double* bias, int* sel) {
+    const int lane = threadIdx.x & 31;
     const int E = D.E, k = D.k;
     double* gates = S.gates + (int64_t)s * k;
     double* lg = S.logits + (int64_t)s * E;
     const bool base = C.router_strategy == PIKV_ROUTER_BASE;
+    __shared__ double sm_mean;
+    __shared__ uint64_t sm_tot;
+    if (lane == 0) sm_tot = S.total_usage[s];
     if (base) {  // base_round_robin, router.cpp:107-118
-        int64_t t = (int64_t)S.rstep[s];
-        for (int j = 0; j < k; ++j) sel[j] = (int)((t * C.stride + j) % E);
-        for (int j = 0; j < k; ++j) gates[j] = __ddiv_rn(1.0, (double)k);
-        for (int e = 0; e < E; ++e) lg[e] = 0.0;
+        const int64_t t = (int64_t)S.rstep[s];
+        for (int j = lane; j < k; j += 32) {
+            sel[j] = (int)((t * C.stride + j) % E);
+            gates[j] = __ddiv_rn(1.0, (double)k);
+        }
+        for (int e = lane; e < E; e += 32) lg[e] = 0.0;
     } else {
-        for (int e = 0; e < E; ++e) {
-            if (isnan(sm_logit[e])) {  // router.cpp:131-133
-                S.err[s] = PIKV_ERR_NUMERICAL;
-                return;
-            }
+        bool nan_seen = false;
+        for (int e = lane; e < E; e += 32) nan_seen |= isnan(sm_logit[e]);
+        if (__any_sync(0xffffffffu, nan_seen)) {  // router.cpp:131-133
+            if (lane == 0) S.err[s] = PIKV_ERR_NUMERICAL;
+            return;
         }
-        switch (C.router_strategy) {
-            case PIKV_ROUTER_LOAD_BALANCED: {
-                double acc = 0.0;
-                for (int e = 0; e < E; ++e) acc = __dadd_rn(acc, load[e]);
-                double mean = __ddiv_rn(acc, (double)E);
-                for (int e = 0; e < E; ++e)
-                    sm_logit[e] = __dsub_rn(sm_logit[e], __dmul_rn(C.alpha, __dsub_rn(load[e], mean)));
-                break;
-            }
-            case PIKV_ROUTER_CACHE_AWARE:
-                for (int e = 0; e < E; ++e)
-                    sm_logit[e] = __dsub_rn(sm_logit[e], __dmul_rn(C.lambda_miss, log1p((double)miss[e])));
-                break;
-            case PIKV_ROUTER_ENTROPY_LB: {
-                uint64_t tot = S.total_usage[s];
-                for (int e = 0; e < E; ++e) {
-                    double p = tot == 0 ? 0.0 : __ddiv_rn((double)usage[e], (double)tot);
-                    double h = p > 0.0 ? __dmul_rn(-p, log(p)) : 0.0;
-                    sm_logit[e] = __dsub_rn(sm_logit[e], __dmul_rn(C.beta_ent, h));
+        if (C.router_strategy == PIKV_ROUTER_LOAD_BALANCED && lane == 0) {
+            double acc = 0.0;
+            for (int e = 0; e < E; ++e) acc = __dadd_rn(acc, load[e]);
+            sm_mean = __ddiv_rn(acc, (double)E);
+        }
+        __syncwarp();
+        const uint64_t tot = sm_tot;
+        for (int e = lane; e < E; e += 32) {
+            double x = sm_logit[e];
+            switch (C.router_strategy) {
+                case PIKV_ROUTER_LOAD_BALANCED:
+                    x = __dsub_rn(x, __dmul_rn(C.alpha, __dsub_rn(load[e], sm_mean)));
+                    break;
+                case PIKV_ROUTER_CACHE_AWARE:
+                    x = __dsub_rn(x, __dmul_rn(C.lambda_miss, log1p((double)miss[e])));
+                    break;
+                case PIKV_ROUTER_ENTROPY_LB: {
+                    const double p = tot == 0 ? 0.0 : __ddiv_rn((double)usage[e], (double)tot);
+                    const double h = p > 0.0 ? __dmul_rn(-p, log(p)) : 0.0;
+                    x = __dsub_rn(x, __dmul_rn(C.beta_ent, h));
+                    break;
                 }
-                break;
+                case PIKV_ROUTER_ADAPTIVE:
+                    x = __dadd_rn(x, bias[e]);
+                    break;
+                default:
+                    break;
             }
-            case PIKV_ROUTER_ADAPTIVE:
-                for (int e = 0; e < E; ++e)
-                    sm_logit[e] = __dadd_rn(sm_logit[e], bias[e]);
-                break;
-            default:
-                break;
+            sm_logit[e] = x;
+            lg[e] = x;
         }
+        __syncwarp();
         // selection: (score desc, index asc), router.cpp:82-90, 174-198
-        auto better = [&](int a, int b) {
-            double sa = sm_logit[a], sb = sm_logit[b];
-            return sa != sb ? sa > sb : a < b;
-        };
         if (C.router_strategy == PIKV_ROUTER_HIERARCHICAL) {
-            const int groups = C.groups;
-            const int cs = (E + groups - 1) / groups;
-            // cluster order by (max logit desc, index asc); pool grows until >= k
-            int chosen_clusters = 0, npool = 0;
-            bool* used = sm_flag;
-            int* pool = sm_pool;
-            for (int g = 0; g < groups; ++g) used[g] = false;
-            while (npool < k && chosen_clusters < groups) {
-                int best = -1;
-                double bsc = 0.0;
-                for (int g = 0; g < groups; ++g) {
-                    if (used[g]) continue;
-                    double sc = -INFINITY;
-                    for (int e = g * cs; e < min(E, g * cs + cs); ++e)
-                        sc = (sc < sm_logit[e]) ? sm_logit[e] : sc;
-                    if (best < 0 || sc > bsc) best = g, bsc = sc;  // ties keep lower g
+            if (lane == 0) {
+                auto better = [&](int a2, int b2) {
+                    const double sa = sm_logit[a2], sb = sm_logit[b2];
+                    return sa != sb ? sa > sb : a2 < b2;
+                };
+                const int groups = C.groups;
+                const int cs = (E + groups - 1) / groups;
+                int chosen = 0, npool = 0;
+                bool* used = sm_flag;
+                int* pool = sm_pool;
+                for (int g = 0; g < groups; ++g) used[g] = false;
+                while (npool < k && chosen < groups) {
+                    int best = -1;
+                    double bsc = 0.0;
+                    for (int g = 0; g < groups; ++g) {
+                        if (used[g]) continue;
+                        double sc = -INFINITY;
+                        for (int e = g * cs; e < min(E, g * cs + cs); ++e)
+                            sc = (sc < sm_logit[e]) ? sm_logit[e] : sc;
+                        if (best < 0 || sc > bsc) best = g, bsc = sc;  // ties keep lower g
+                    }
+                    used[best] = true;
+                    ++chosen;
+                    for (int e = best * cs; e < min(E, best * cs + cs); ++e) pool[npool++] = e;
                 }
-                used[best] = true;
-                ++chosen_clusters;
-                for (int e = best * cs; e < min(E, best * cs + cs); ++e) pool[npool++] = e;
-            }
-            for (int j = 0; j < k; ++j) {  // partial selection sort over the pool
-                int bi = j;
-                for (int i = j + 1; i < npool; ++i)
-                    if (better(pool[i], pool[bi])) bi = i;
-                int t = pool[j];
-                pool[j] = pool[bi];
-                pool[bi] = t;
-                sel[j] = pool[j];
+                for (int j = 0; j < k; ++j) {
+                    int bi = j;
+                    for (int i = j + 1; i < npool; ++i)
+                        if (better(pool[i], pool[bi])) bi = i;
+                    const int t = pool[j];
+                    pool[j] = pool[bi];
+                    pool[bi] = t;
+                    sel[j] = pool[j];
+                }
             }
         } else {
-            // k rounds of argmax excluding earlier picks == sorted prefix
-            bool* taken = sm_flag;
-            for (int e = 0; e < E; ++e) taken[e] = false;
+            // k rounds of warp argmax, excluding earlier picks == sorted prefix
+            for (int e = lane; e < E; e += 32) sm_flag[e] = false;
+            __syncwarp();
             for (int j = 0; j < k; ++j) {
+                double bv = 0.0;
                 int bi = -1;
-                for (int e = 0; e < E; ++e)
-                    if (!taken[e] && (bi < 0 || better(e, bi))) bi = e;
-                taken[bi] = true;
-                sel[j] = bi;
+                for (int e = lane; e < E; e += 32) {
+                    if (sm_flag[e]) continue;
+                    const double x = sm_logit[e];
+                    if (bi < 0 || x > bv || (x == bv && e < bi)) bv = x, bi = e;
+                }
+                for (int off = 16; off; off >>= 1) {
+                    const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
+                    const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+                    if (oi >= 0 && (bi < 0 || ov > bv || (ov == bv && oi < bi))) bv = ov, bi = oi;
+                }
+                if (lane == 0) {
+                    sel[j] = bi;
+                    sm_flag[bi] = true;
+                }
+                __syncwarp();
             }
         }
-        // gates = softmax(selected logits), mathops.cpp:11-30
-        double mx = sm_logit[sel[0]];
-        for (int j = 0; j < k; ++j) mx = (mx < sm_logit[sel[j]]) ? sm_logit[sel[j]] : mx;
-        double tot = 0.0;
-        for (int j = 0; j < k; ++j) {
-            gates[j] = exp(__dsub_rn(sm_logit[sel[j]], mx));
-            tot = __dadd_rn(tot, gates[j]);
+        __syncwarp();
+        if (lane == 0) {  // gates = softmax(selected logits), mathops.cpp:11-30
+            double mx = sm_logit[sel[0]];
+            for (int j = 0; j < k; ++j) mx = (mx < sm_logit[sel[j]]) ? sm_logit[sel[j]] : mx;
+            double tot2 = 0.0;
+            for (int j = 0; j < k; ++j) {
+                gates[j] = exp(__dsub_rn(sm_logit[sel[j]], mx));
+                tot2 = __dadd_rn(tot2, gates[j]);
+            }
+            for (int j = 0; j < k; ++j) gates[j] = __ddiv_rn(gates[j], tot2);
         }
-        for (int j = 0; j < k; ++j) gates[j] = __ddiv_rn(gates[j], tot);
-        for (int e = 0; e < E; ++e) lg[e] = sm_logit[e];
     }
+    __syncwarp();
     // note_selection, router.cpp:92-105
     const double one_m = __dsub_rn(1.0, C.load_decay);
-    for (int e = 0; e < E; ++e) {
+    for (int e = lane; e < E; e += 32) {
         bool picked = false;
         for (int j = 0; j < k; ++j) picked |= sel[j] == e;
         load[e] = __dadd_rn(__dmul_rn(C.load_decay, load[e]), __dmul_rn(one_m, picked ? 1.0 : 0.0));
     }
-    for (int j = 0; j < k; ++j) usage[sel[j]] += 1;
-    S.total_usage[s] += (uint64_t)k;
-    S.rstep[s] += 1;
-
+    for (int j = lane; j < k; j += 32) usage[sel[j]] += 1;
+    if (lane == 0) {
+        S.total_usage[s] = sm_tot + (uint64_t)k;
+        S.rstep[s] += 1;
+    }
     // candidate local rings for retrieval (ascending ring id)
     int nc = 0;
     int32_t* cand = S.cand + (int64_t)s * D.max_cand;
-    for (int gl = 0; gl < D.Gl; ++gl) {
-        const int g = gl * D.world + D.rank;
-        for (int sh = 0; sh < D.SPD; ++sh) {
-            const int raw = sh * D.G + g;
-            bool ok = false;
-            for (int j = 0; j < k && !ok; ++j)
-                ok = ring_can_hold(raw, sel[j], D.n_tok, D.n_exp, D.additive);
-            if (ok && nc < D.max_cand) cand[nc++] = gl * D.SPD + sh;
+    const int nr = D.Gl * D.SPD;
+    for (int r0 = 0; r0 < nr; r0 += 32) {
+        const int r = r0 + lane;
+        bool ok = false;
+        if (r < nr) {
+            const int gl = r / D.SPD, sh = r % D.SPD;
+            const int raw = sh * D.G + gl * D.world + D.rank;
+            for (int j = 0; j < k && !ok; ++j) ok = ring_can_hold(raw, sel[j], D.n_tok, D.n_exp, D.additive);
         }
+        const unsigned bal = __ballot_sync(0xffffffffu, ok);
+        const int pos = nc + __popc(bal & ((1u << lane) - 1u));
+        if (ok && pos < D.max_cand) cand[pos] = r;
+        nc += __popc(bal);
     }
-    S.ncand[s] = nc;
+    if (lane == 0) S.ncand[s] = min(nc, D.max_cand);
 }
 
 void launch_route(const Dims& D, const Cfg& C, const State& S, const void* q, cudaStream_t st) {
@@ -360,7 +390,7 @@ __device__ __forceinline__ float load_in(const void* p, int dtype, int64_t i) {
 }
 
 // Encode one K or V row of stream s into smem `dst` in the stored layout.
-__device__ void encode_row(const Dims& D, const State& S, const void* x, int s, uint8_t* dst,
+__device__ __forceinline__ void encode_row(const Dims& D, const State& S, const void* x, int s, uint8_t* dst,
                            float* scales_out, float* tmp) {
     const int H = D.H, hd = D.d / H, r = D.dph, tid = threadIdx.x, nt = blockDim.x;
     const int64_t base = (int64_t)s * D.d;

@@ -13,4 +13,5 @@ for i in range(5):
     eng.fill_synthetic(q,k,v,seed=i); eng.step(q,k,v); eng.sync()
     d=np.zeros(64,dtype=np.int64); L.pikv_debug_read(eng.h, d.ctypes.data, 64)
     print("qload %d chain %d (wait %d) sync %d select+writeback %d cycles"%(d[1]-d[0], d[2]-d[1], d[5], d[3]-d[2], d[4]-d[3]))
+    print("  select: nan %d penalty %d topk+gates %d note %d cand %d tail %d"%(d[10]-d[3], d[11]-d[10], d[12]-d[11], d[13]-d[12], d[14]-d[13], d[4]-d[14]))
 eng.close()
