@@ -49,6 +49,22 @@ WORKLOADS = {
 }
 
 
+def load_traffic(workload):
+    """dram bytes read+written per k_attend launch from the committed ncu
+    --set full capture of this workload (profiles/r*_attend_ncu.json)."""
+    import glob
+    best = None
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_attend_ncu.json"))):
+        try:
+            with open(path) as f:
+                p = json.load(f)
+        except Exception:
+            continue
+        if p.get("workload", "").startswith(workload + ":"):
+            best = (p["traffic_bytes_per_launch"], os.path.relpath(path, ROOT))
+    return best
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -379,7 +395,9 @@ def main():
         "kv_frac_of_hbm": kv_bytes_step / (ms / args.steps * 1e-3) / 1e9 / (peak * world),
         "attended_per_step": att_last,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak,
+                     "traffic": (load_traffic(name) or (None, None))[0],
+                     "traffic_source": (load_traffic(name) or (None, None))[1],
                      "kernel": "k_attend (decode attention, TMA bulk ring)",
                      "peak_kind": peak_kind, "avg_launch_ms": attend_avg_ms,
                      "algorithmic_bytes_per_launch": alg_bytes / max(n_launch, 1)},

@@ -191,6 +191,18 @@ int pikv_lowrank_encode(const float* x, const float* basis, const float* bias,
 int pikv_lowrank_decode(const float* y, const float* basis, const float* bias,
                         int32_t rows, int32_t heads, int32_t hd, int32_t r, float* x_out);
 
+/* Host-buffer variants of the above (copy in, run the same kernels, copy
+ * out); used by the C++ facade include/pikv_b200.hpp. */
+int pikv_shard_assign_host(const int64_t* t, const int32_t* e, int32_t n, int32_t n_tok,
+                           int32_t n_exp, int32_t devices, int32_t additive,
+                           int32_t* device_out, int32_t* shard_out, int32_t* raw_out);
+int pikv_select_evictions_host(const double* aggregate, const uint64_t* oldest_id, int32_t n,
+                               int32_t budget_pages, int32_t use_theta, double theta,
+                               int32_t* idx_out, int32_t* reason_out, int32_t* n_out);
+int pikv_attention_host(const float* q, const float* keys, const float* values,
+                        int32_t n_queries, int32_t n, int32_t w, float* y_out,
+                        float* weights_out);
+
 /* ---- engine (Engine, pipeline.hpp:101-145) ------------------------------ */
 int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine** out);
 int pikv_engine_destroy(pikv_engine* eng);

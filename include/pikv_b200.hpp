@@ -1,0 +1,374 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// pikv_b200.hpp -- header-only C++ facade of the B200 engine with the
+// reference's API (/root/reference/proj/include/pikv) over the C-ABI
+// (pikv_b200.h).  Names, argument meanings and exception types follow the
+// reference so a caller of pikv::Engine / pikv::shard_assign / ... switches by
+// changing the namespace to pikv::b200:
+//
+//   reference                               this facade
+//   pikv::shard_assign (kvstore.hpp:25)     pikv::b200::shard_assign
+//   pikv::select_evictions (scheduler.hpp:114) pikv::b200::select_evictions
+//   pikv::attention (pipeline.hpp:46)       pikv::b200::attention
+//   pikv::Engine (pipeline.hpp:101)         pikv::b200::Engine (B streams)
+//   pikv::Error tree (errors.hpp:9-47)      pikv::b200::Error tree
+//
+// Differences, all from the reference's own scope notes: the engine takes the
+// token's q/k/v directly (QueryEncoder is a desk-scale stand-in for the host
+// model, pipeline.hpp:17-18); codecs take a caller basis (fitting is offline,
+// PAPER.md:499); heads/batch/dtype are extra config.
+// No CUDA headers are needed: link with libpikv_b200.so.
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "pikv_b200.h"
+
+namespace pikv::b200 {
+
+// ---- errors.hpp:9-47 ----------------------------------------------------
+struct Error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct InvalidArgument : Error { using Error::Error; };
+struct InvalidConfig : Error { using Error::Error; };
+struct InvalidEntry : Error { using Error::Error; };
+struct NumericalError : Error { using Error::Error; };
+struct CodecMismatch : Error { using Error::Error; };
+struct NotFitted : Error { using Error::Error; };
+struct InsufficientCalibration : Error { using Error::Error; };
+struct InvalidComparison : Error { using Error::Error; };
+struct IoError : Error { using Error::Error; };
+struct DeviceError : Error { using Error::Error; };  // CUDA / NCCL / pool exhaustion
+
+inline void check(int rc) {
+    if (rc == PIKV_OK) return;
+    const std::string msg = pikv_last_error();
+    switch (rc) {
+        case PIKV_ERR_INVALID_ARGUMENT: throw InvalidArgument(msg);
+        case PIKV_ERR_INVALID_CONFIG: throw InvalidConfig(msg);
+        case PIKV_ERR_INVALID_ENTRY: throw InvalidEntry(msg);
+        case PIKV_ERR_NUMERICAL: throw NumericalError(msg);
+        case PIKV_ERR_CODEC_MISMATCH: throw CodecMismatch(msg);
+        case PIKV_ERR_NOT_FITTED: throw NotFitted(msg);
+        case PIKV_ERR_INSUFFICIENT_CALIBRATION: throw InsufficientCalibration(msg);
+        case PIKV_ERR_INVALID_COMPARISON: throw InvalidComparison(msg);
+        case PIKV_ERR_IO: throw IoError(msg);
+        default: throw DeviceError(msg);
+    }
+}
+
+// ---- free functions ----------------------------------------------------
+struct ShardId {  // kvstore.hpp:14-20
+    int device = 0;
+    int shard_index = 0;
+    int raw = 0;
+    bool operator==(const ShardId&) const = default;
+};
+
+inline ShardId shard_assign(std::int64_t t, int e, int n_tok, int n_exp, int devices,
+                            bool additive = false) {
+    std::int32_t d = 0, s = 0, r = 0, ee = e;
+    check(pikv_shard_assign_host(&t, &ee, 1, n_tok, n_exp, devices, additive ? 1 : 0, &d, &s, &r));
+    return {d, s, r};
+}
+
+enum class EvictReason { Budget, Threshold, Overwrite };  // scheduler.hpp:87
+
+struct PageScore {  // scheduler.hpp:106-109
+    double aggregate = 0.0;
+    std::uint64_t oldest_id = 0;
+};
+
+inline std::vector<std::pair<std::size_t, EvictReason>> select_evictions(
+    const std::vector<PageScore>& pages, int budget_pages, bool use_theta, double theta) {
+    const int n = static_cast<int>(pages.size());
+    std::vector<double> agg(n);
+    std::vector<std::uint64_t> old(n);
+    for (int i = 0; i < n; ++i) agg[i] = pages[i].aggregate, old[i] = pages[i].oldest_id;
+    std::vector<std::int32_t> idx(n + 1), why(n + 1);
+    std::int32_t m = 0;
+    check(pikv_select_evictions_host(agg.data(), old.data(), n, budget_pages, use_theta ? 1 : 0,
+                                     theta, idx.data(), why.data(), &m));
+    std::vector<std::pair<std::size_t, EvictReason>> out;
+    for (int i = 0; i < m; ++i)
+        out.emplace_back(static_cast<std::size_t>(idx[i]), static_cast<EvictReason>(why[i]));
+    return out;
+}
+
+struct AttentionOutput {  // pipeline.hpp:39-43
+    std::vector<double> output;
+    std::vector<double> weights;
+    std::size_t retrieved = 0;
+};
+
+// attention(query, entries) with entries given as key/value rows.
+inline AttentionOutput attention(const std::vector<double>& query,
+                                 const std::vector<std::vector<double>>& keys,
+                                 const std::vector<std::vector<double>>& values) {
+    AttentionOutput out;
+    const int w = static_cast<int>(query.size()), n = static_cast<int>(keys.size());
+    out.retrieved = static_cast<std::size_t>(n);
+    if (n == 0) {
+        out.output.assign(query.size(), 0.0);
+        return out;
+    }
+    std::vector<float> q(query.begin(), query.end()), k, v, y(w), wt(n);
+    for (int i = 0; i < n; ++i) {
+        if (static_cast<int>(keys[i].size()) != w)
+            throw InvalidArgument("attention: key/query width mismatch");  // pipeline.cpp:71-73
+        k.insert(k.end(), keys[i].begin(), keys[i].end());
+        v.insert(v.end(), values[i].begin(), values[i].end());
+    }
+    check(pikv_attention_host(q.data(), k.data(), v.data(), 1, n, w, y.data(), wt.data()));
+    out.output.assign(y.begin(), y.end());
+    out.weights.assign(wt.begin(), wt.end());
+    return out;
+}
+
+// ---- configuration (config.hpp, kvstore.hpp, router.hpp, scheduler.hpp,
+//      compressor.hpp, pipeline.hpp) -------------------------------------
+enum class RouterStrategy { Base, TopK, LoadBalanced, CacheAware, EntropyLB, Adaptive, Hierarchical };
+enum class SchedStrategy { H2O, SL, QUEST, Flex, LRU, LRUPlus, AdaKV, Duo };
+enum class Codec { Identity, LowRank, LoRAPlus, FastV, Prune, Int8, Int4 };
+enum class DType { F32, BF16 };
+
+struct ModelConfig { int d = 64, head_width = 16, E = 8, k = 2; long long L = 1024; int G = 2, S = 16, K = 4;
+                     double rho = 1.0; int elem_bytes = 2; };
+struct StoreConfig { int n_tok = 64, n_exp = 64; bool additive = false; int shards_per_device = 0; };
+struct RouterConfig { RouterStrategy strategy = RouterStrategy::TopK; int k = 2; double alpha = 1.0,
+                      lambda_miss = 1.0, beta_ent = 1.0, bandit_step = 0.05; int groups = 1, stride = 1;
+                      double bias_cap = 5.0, load_decay = 0.99; };
+struct SchedulerConfig { SchedStrategy strategy = SchedStrategy::LRU; int budget_pages = 4, page_size = 16;
+                         double tau = 64.0; int sink = 4; double lambda_freq = 0.5, adakv_step = 0.05,
+                         target_hit = 0.9, gamma_sim = 0.5, theta0 = -1e18, hit_decay = 0.9;
+                         std::vector<double> adakv_weights{1.0, 0.5, 0.25};
+                         std::vector<double> flex_plan{1.0}; int flex_bucket = 16; };
+struct CompressorConfig { Codec scheme = Codec::Identity; int rank = 8; };
+
+struct EngineConfig {  // pipeline.hpp:87-98 (+ B200 runtime fields)
+    ModelConfig model;
+    StoreConfig store;
+    RouterConfig router;
+    SchedulerConfig scheduler;
+    CompressorConfig compressor;
+    bool unbounded_budget = false;
+    std::uint64_t seed = 1;
+    int n_heads = 1, n_layers = 0, batch = 1;
+    DType kv_dtype = DType::F32;
+    long long pool_entries = 0;
+    int cuda_device = 0;
+
+    pikv_config to_c() const {
+        pikv_config c;
+        pikv_config_default(&c);
+        c.d = model.d, c.head_width = model.head_width, c.E = model.E, c.k = router.k;
+        c.L = model.L, c.G = model.G, c.S = model.S, c.K = model.K, c.elem_bytes = model.elem_bytes;
+        c.rho = model.rho, c.n_heads = n_heads;
+        c.n_tok = store.n_tok, c.n_exp = store.n_exp, c.additive = store.additive;
+        c.shards_per_device = store.shards_per_device;
+        c.router_strategy = static_cast<int>(router.strategy), c.groups = router.groups;
+        c.stride = router.stride, c.alpha = router.alpha, c.lambda_miss = router.lambda_miss;
+        c.beta_ent = router.beta_ent, c.bandit_step = router.bandit_step, c.bias_cap = router.bias_cap;
+        c.load_decay = router.load_decay;
+        c.sched_strategy = static_cast<int>(scheduler.strategy);
+        c.budget_pages = scheduler.budget_pages, c.page_size = scheduler.page_size;
+        c.sink = scheduler.sink, c.flex_bucket = scheduler.flex_bucket, c.tau = scheduler.tau;
+        c.lambda_freq = scheduler.lambda_freq, c.adakv_step = scheduler.adakv_step;
+        c.target_hit = scheduler.target_hit, c.gamma_sim = scheduler.gamma_sim;
+        c.theta0 = scheduler.theta0, c.hit_decay = scheduler.hit_decay;
+        if (scheduler.adakv_weights.size() > 8 || scheduler.flex_plan.size() > 32)
+            throw InvalidConfig("SchedulerConfig: at most 8 adakv weights / 32 flex buckets");
+        c.n_adakv_weights = static_cast<int>(scheduler.adakv_weights.size());
+        for (std::size_t i = 0; i < scheduler.adakv_weights.size(); ++i) c.adakv_weights[i] = scheduler.adakv_weights[i];
+        c.n_flex_plan = static_cast<int>(scheduler.flex_plan.size());
+        for (std::size_t i = 0; i < scheduler.flex_plan.size(); ++i) c.flex_plan[i] = scheduler.flex_plan[i];
+        c.codec = static_cast<int>(compressor.scheme), c.rank = compressor.rank;
+        c.unbounded_budget = unbounded_budget, c.n_layers = n_layers, c.batch = batch;
+        c.kv_dtype = kv_dtype == DType::BF16 ? PIKV_DTYPE_BF16 : PIKV_DTYPE_F32;
+        c.world_size = 1, c.rank_id = 0, c.pool_entries = pool_entries, c.seed = seed;
+        return c;
+    }
+};
+
+// ---- step I/O (pipeline.hpp:59-85) ----------------------------------------
+struct TokenInput {
+    std::vector<double> query, key, value;  // width d, rounded to kv_dtype by the engine
+    std::vector<double> layer_saliency;     // n_layers (Duo)
+};
+
+struct EvictionRecord {  // scheduler.hpp:90-98
+    std::uint64_t step = 0, entry_id = 0;
+    std::int64_t token_id = 0;
+    int expert_id = 0, device = 0;
+    double score = 0.0;
+    EvictReason reason = EvictReason::Budget;
+};
+
+struct AttendedEntry {
+    std::int64_t token_id = 0;
+    int expert_id = 0;
+    double weight = 0.0;
+};
+
+struct StepResult {  // pipeline.hpp:68-80
+    std::uint64_t step = 0;
+    std::vector<int> experts;
+    std::vector<double> gates;
+    int inserts = 0;
+    std::vector<EvictionRecord> evictions;  // overwrite + scheduled
+    std::uint64_t fetch_elements = 0;
+    std::uint64_t hits = 0, lookups = 0;
+    AttentionOutput attn;                   // output; weights in (token, expert) order
+    std::vector<AttendedEntry> attended;    // (token, expert) order (kvstore.cpp:144-163)
+};
+
+struct StoreStats { std::uint64_t live = 0, memory_bytes = 0, inserts = 0, overwrites = 0; };
+struct RouterStateView { std::vector<double> load, bandit_bias; std::vector<std::uint64_t> usage_counts,
+                         miss_counts; std::uint64_t total_usage = 0, step = 0; };
+struct SchedulerStateView { double theta = 0.0, running_hit = 0.0; std::uint64_t step = 0; };
+
+// B independent decode streams of pikv::Engine on one GPU.
+class Engine {
+  public:
+    explicit Engine(const EngineConfig& cfg) : cfg_(cfg) {
+        pikv_config c = cfg.to_c();
+        check(pikv_engine_create(&c, cfg.cuda_device, &h_));
+    }
+    ~Engine() { if (h_) pikv_engine_destroy(h_); }
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    // Codec basis [H][r][hd], LoRAPlus bias [d], Prune kept [H][r].
+    void set_codec(const std::vector<float>& basis, const std::vector<float>& bias = {},
+                   const std::vector<std::int32_t>& kept = {}) {
+        check(pikv_set_codec_host(h_, basis.empty() ? nullptr : basis.data(),
+                                  bias.empty() ? nullptr : bias.data(), kept.empty() ? nullptr : kept.data()));
+    }
+    void set_router_matrix(const std::vector<double>& w_r) { check(pikv_set_router_matrix_host(h_, w_r.data())); }
+
+    // Engine::step (pipeline.cpp:213-351) for all streams, one token each.
+    std::vector<StepResult> step(const std::vector<TokenInput>& tokens) {
+        const int B = cfg_.batch, d = cfg_.model.d, k = cfg_.router.k, E = cfg_.model.E;
+        if (static_cast<int>(tokens.size()) != B) throw InvalidArgument("Engine::step: one token per stream");
+        const bool bf16 = cfg_.kv_dtype == DType::BF16;
+        std::vector<std::uint16_t> qb, kb, vb;
+        std::vector<float> qf, kf, vf;
+        std::vector<double> sal(static_cast<std::size_t>(B) * (cfg_.n_layers > 0 ? cfg_.n_layers : 1));
+        for (int s = 0; s < B; ++s) {
+            const TokenInput& t = tokens[s];
+            if (static_cast<int>(t.query.size()) != d || static_cast<int>(t.key.size()) != d ||
+                static_cast<int>(t.value.size()) != d)
+                throw InvalidArgument("Engine::step: embedding width mismatch");  // pipeline.cpp:214-216
+            for (int i = 0; i < d; ++i) {
+                if (bf16) {
+                    qb.push_back(to_bf16(t.query[i])), kb.push_back(to_bf16(t.key[i]));
+                    vb.push_back(to_bf16(t.value[i]));
+                } else {
+                    qf.push_back(static_cast<float>(t.query[i])), kf.push_back(static_cast<float>(t.key[i]));
+                    vf.push_back(static_cast<float>(t.value[i]));
+                }
+            }
+            for (int l = 0; l < cfg_.n_layers; ++l)
+                sal[static_cast<std::size_t>(s) * cfg_.n_layers + l] =
+                    l < static_cast<int>(t.layer_saliency.size()) ? t.layer_saliency[l] : 0.0;
+        }
+        const int dp = stored_width();
+        std::vector<float> y(static_cast<std::size_t>(B) * dp);
+        const void* q = bf16 ? static_cast<const void*>(qb.data()) : qf.data();
+        const void* kk = bf16 ? static_cast<const void*>(kb.data()) : kf.data();
+        const void* v = bf16 ? static_cast<const void*>(vb.data()) : vf.data();
+        check(pikv_step_host(h_, q, kk, v, cfg_.n_layers > 0 ? sal.data() : nullptr, y.data()));
+        check(pikv_sync(h_));
+        std::vector<std::int32_t> ex(static_cast<std::size_t>(B) * k);
+        std::vector<double> gates(static_cast<std::size_t>(B) * k);
+        std::vector<pikv_step_summary> sm(B);
+        check(pikv_read_step_host(h_, ex.data(), gates.data(), nullptr, sm.data()));
+        std::vector<pikv_evict_record> recs(1u << 16);
+        std::int32_t nrec = 0;
+        check(pikv_read_evictions_host(h_, recs.data(), static_cast<std::int32_t>(recs.size()), &nrec));
+        std::vector<StepResult> out(B);
+        for (int s = 0; s < B; ++s) {
+            StepResult& r = out[s];
+            r.step = sm[s].step;
+            r.experts.assign(ex.begin() + s * k, ex.begin() + (s + 1) * k);
+            r.gates.assign(gates.begin() + s * k, gates.begin() + (s + 1) * k);
+            r.inserts = sm[s].inserts;
+            r.fetch_elements = static_cast<std::uint64_t>(sm[s].fetch_elements);
+            r.hits = static_cast<std::uint64_t>(sm[s].hits);
+            r.lookups = static_cast<std::uint64_t>(sm[s].lookups);
+            r.attn.output.assign(y.begin() + static_cast<std::size_t>(s) * dp,
+                                 y.begin() + static_cast<std::size_t>(s + 1) * dp);
+            for (int i = 0; i < nrec && i < static_cast<int>(recs.size()); ++i) {
+                if (recs[i].stream != s) continue;
+                r.evictions.push_back({recs[i].step, recs[i].entry_id, recs[i].token_id, recs[i].expert_id,
+                                       recs[i].device, recs[i].score, static_cast<EvictReason>(recs[i].reason)});
+            }
+            std::int32_t n = 0;
+            check(pikv_read_attended_host(h_, s, nullptr, nullptr, nullptr, 0, &n));
+            std::vector<std::int64_t> tok(n > 0 ? n : 1);
+            std::vector<std::int32_t> exp(n > 0 ? n : 1);
+            std::vector<double> al(n > 0 ? n : 1);
+            check(pikv_read_attended_host(h_, s, tok.data(), exp.data(), al.data(), n, &n));
+            std::vector<AttendedEntry> att(n);
+            for (int i = 0; i < n; ++i) att[i] = {tok[i], exp[i], al[i]};
+            sort_attended(att);
+            r.attended = att;
+            r.attn.retrieved = static_cast<std::size_t>(n);
+            for (const auto& a : att) r.attn.weights.push_back(a.weight);
+        }
+        (void)E;
+        return out;
+    }
+
+    StoreStats store_stats(int stream = 0) const {
+        StoreStats st;
+        check(pikv_store_stats_host(h_, stream, &st.live, &st.memory_bytes, &st.inserts, &st.overwrites));
+        return st;
+    }
+    RouterStateView router_state(int stream = 0) const {
+        const int E = cfg_.model.E;
+        RouterStateView r;
+        r.load.resize(E), r.bandit_bias.resize(E), r.usage_counts.resize(E), r.miss_counts.resize(E);
+        check(pikv_read_router_state_host(h_, stream, r.load.data(), r.usage_counts.data(), r.miss_counts.data(),
+                                          r.bandit_bias.data(), &r.step, &r.total_usage));
+        return r;
+    }
+    SchedulerStateView scheduler_state(int stream = 0) const {
+        SchedulerStateView v;
+        check(pikv_read_sched_state_host(h_, stream, &v.theta, &v.running_hit, &v.step));
+        return v;
+    }
+    int stored_width() const {
+        const int hd = cfg_.model.d / cfg_.n_heads;
+        const bool proj = cfg_.compressor.scheme == Codec::LowRank || cfg_.compressor.scheme == Codec::LoRAPlus ||
+                          cfg_.compressor.scheme == Codec::FastV || cfg_.compressor.scheme == Codec::Prune;
+        return (proj ? cfg_.compressor.rank : hd) * cfg_.n_heads;
+    }
+    pikv_engine* handle() { return h_; }
+
+  private:
+    static std::uint16_t to_bf16(double x) {
+        float f = static_cast<float>(x);
+        std::uint32_t u;
+        std::memcpy(&u, &f, 4);
+        if ((u & 0x7f800000u) != 0x7f800000u) u += 0x7fffu + ((u >> 16) & 1u);
+        return static_cast<std::uint16_t>(u >> 16);
+    }
+    static void sort_attended(std::vector<AttendedEntry>& a) {
+        // (token, expert) order of KVStore::retrieve (kvstore.cpp:144-163)
+        std::sort(a.begin(), a.end(), [](const AttendedEntry& x, const AttendedEntry& y) {
+            return x.token_id != y.token_id ? x.token_id < y.token_id : x.expert_id < y.expert_id;
+        });
+    }
+    EngineConfig cfg_;
+    pikv_engine* h_ = nullptr;
+};
+
+}  // namespace pikv::b200

@@ -51,6 +51,11 @@ SIGNATURES = {
     "pikv_dequantize": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),
     "pikv_lowrank_encode": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_vp]),
     "pikv_lowrank_decode": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_vp]),
+    "pikv_shard_assign_host": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_vp,
+                                              c_vp, c_vp]),
+    "pikv_select_evictions_host": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_i32, c_f64, c_vp,
+                                                  c_vp, c_vp]),
+    "pikv_attention_host": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp]),
     "pikv_engine_create": (ctypes.c_int, [P(PikvConfigC), c_i32, P(c_vp)]),
     "pikv_engine_destroy": (ctypes.c_int, [c_vp]),
     "pikv_engine_stream": (c_vp, [c_vp]),

@@ -238,6 +238,71 @@ int pikv_lowrank_decode(const float* y, const float* basis, const float* bias, i
     return PIKV_OK;
 }
 
+// host-buffer wrappers ---------------------------------------------------------
+namespace {
+struct DevBuf {
+    void* p = nullptr;
+    explicit DevBuf(size_t n) { cudaMalloc(&p, n ? n : 1); }
+    ~DevBuf() { cudaFree(p); }
+};
+}  // namespace
+
+int pikv_shard_assign_host(const int64_t* t, const int32_t* e, int32_t n, int32_t n_tok,
+                           int32_t n_exp, int32_t devices, int32_t additive, int32_t* device_out,
+                           int32_t* shard_out, int32_t* raw_out) {
+    if (n <= 0) return pikv_shard_assign(nullptr, nullptr, 0, n_tok, n_exp, devices, additive,
+                                         nullptr, nullptr, nullptr);
+    DevBuf dt(8 * (size_t)n), de(4 * (size_t)n), dd(4 * (size_t)n), ds(4 * (size_t)n), dr(4 * (size_t)n);
+    CUDA_TRY(cudaMemcpy(dt.p, t, 8 * (size_t)n, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(de.p, e, 4 * (size_t)n, cudaMemcpyHostToDevice));
+    int rc = pikv_shard_assign((int64_t*)dt.p, (int32_t*)de.p, n, n_tok, n_exp, devices, additive,
+                               (int32_t*)dd.p, (int32_t*)ds.p, (int32_t*)dr.p);
+    if (rc) return rc;
+    if (device_out) CUDA_TRY(cudaMemcpy(device_out, dd.p, 4 * (size_t)n, cudaMemcpyDeviceToHost));
+    if (shard_out) CUDA_TRY(cudaMemcpy(shard_out, ds.p, 4 * (size_t)n, cudaMemcpyDeviceToHost));
+    if (raw_out) CUDA_TRY(cudaMemcpy(raw_out, dr.p, 4 * (size_t)n, cudaMemcpyDeviceToHost));
+    return PIKV_OK;
+}
+
+int pikv_select_evictions_host(const double* aggregate, const uint64_t* oldest_id, int32_t n,
+                               int32_t budget_pages, int32_t use_theta, double theta,
+                               int32_t* idx_out, int32_t* reason_out, int32_t* n_out) {
+    const size_t m = n > 0 ? (size_t)n : 1;
+    DevBuf da(8 * m), dol(8 * m), di(4 * m), dr(4 * m), dn(4);
+    if (n > 0) {
+        CUDA_TRY(cudaMemcpy(da.p, aggregate, 8 * (size_t)n, cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(dol.p, oldest_id, 8 * (size_t)n, cudaMemcpyHostToDevice));
+    }
+    int rc = pikv_select_evictions((double*)da.p, (uint64_t*)dol.p, n, budget_pages, use_theta, theta,
+                                   (int32_t*)di.p, (int32_t*)dr.p, (int32_t*)dn.p);
+    if (rc) return rc;
+    int32_t v = 0;
+    CUDA_TRY(cudaMemcpy(&v, dn.p, 4, cudaMemcpyDeviceToHost));
+    *n_out = v;
+    if (v > 0) {
+        CUDA_TRY(cudaMemcpy(idx_out, di.p, 4 * (size_t)v, cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemcpy(reason_out, dr.p, 4 * (size_t)v, cudaMemcpyDeviceToHost));
+    }
+    return PIKV_OK;
+}
+
+int pikv_attention_host(const float* q, const float* keys, const float* values, int32_t n_queries,
+                        int32_t n, int32_t w, float* y_out, float* weights_out) {
+    const size_t nq = (size_t)n_queries, nn = (size_t)(n > 0 ? n : 1);
+    DevBuf dq(4 * nq * w), dk(4 * nq * nn * w), dv(4 * nq * nn * w), dy(4 * nq * w), dw(4 * nq * nn);
+    CUDA_TRY(cudaMemcpy(dq.p, q, 4 * nq * w, cudaMemcpyHostToDevice));
+    if (n > 0) {
+        CUDA_TRY(cudaMemcpy(dk.p, keys, 4 * nq * n * w, cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(dv.p, values, 4 * nq * n * w, cudaMemcpyHostToDevice));
+    }
+    int rc = pikv_attention((float*)dq.p, (float*)dk.p, (float*)dv.p, n_queries, n, w, (float*)dy.p,
+                            (float*)dw.p);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpy(y_out, dy.p, 4 * nq * w, cudaMemcpyDeviceToHost));
+    if (weights_out && n > 0) CUDA_TRY(cudaMemcpy(weights_out, dw.p, 4 * nq * n, cudaMemcpyDeviceToHost));
+    return PIKV_OK;
+}
+
 // ---------------------------------------------------------------------------
 // engine
 // ---------------------------------------------------------------------------
@@ -662,8 +727,10 @@ static int enqueue_local(pikv_engine* eng, const void* q, const void* k, const v
     return PIKV_OK;
 }
 
-static int enqueue_finish(pikv_engine* eng, const uint8_t* gathered, float* y, bool attend) {
-    if (eng->D.world > 1) launch_finish_merge(eng->D, eng->C, eng->S, eng->X, gathered, y, eng->stream);
+static int enqueue_finish(pikv_engine* eng, const uint8_t* gathered, float* y, bool attend,
+                          int granks) {
+    if (eng->D.world > 1)
+        launch_finish_merge(eng->D, eng->C, eng->S, eng->X, gathered, y, granks, eng->stream);
     mark(eng, 10);
     if (attend) launch_foldback(eng->D, eng->S, eng->stream);
     mark(eng, 11);
@@ -685,7 +752,7 @@ static int run_step(pikv_engine* eng, const void* q, const void* k, const void* 
     const bool use_graph = eng->warmed && !eng->profiling;
     if (!use_graph) {
         rc = enqueue_local(eng, q, k, v, sal, attend, y);
-        if (!rc) rc = enqueue_finish(eng, eng->S.exchange, y, attend);
+        if (!rc) rc = enqueue_finish(eng, eng->S.exchange, y, attend, 1);
         if (rc) return rc;
         eng->warmed = true;  // first eager pass sets kernel attributes
         eng->launches += eng->kernels_per_step;
@@ -697,7 +764,7 @@ static int run_step(pikv_engine* eng, const void* q, const void* k, const void* 
         cudaGraph_t g;
         CUDA_TRY(cudaStreamBeginCapture(eng->stream, cudaStreamCaptureModeThreadLocal));
         rc = enqueue_local(eng, q, k, v, sal, attend, y);
-        if (!rc) rc = enqueue_finish(eng, eng->S.exchange, y, attend);
+        if (!rc) rc = enqueue_finish(eng, eng->S.exchange, y, attend, 1);
         cudaError_t ce = cudaStreamEndCapture(eng->stream, &g);
         if (rc) return rc;
         if (ce != cudaSuccess) return fail(PIKV_ERR_CUDA, std::string("capture: ") + cudaGetErrorString(ce));
@@ -758,7 +825,7 @@ int pikv_step_local(pikv_engine* eng, const void* q, const void* k, const void* 
 
 int pikv_step_finish(pikv_engine* eng, const void* gathered, float* y_out) {
     cudaSetDevice(eng->device);
-    int rc = enqueue_finish(eng, (const uint8_t*)gathered, y_out, true);
+    int rc = enqueue_finish(eng, (const uint8_t*)gathered, y_out, true, eng->D.world);
     if (rc) return rc;
     eng->launches += 3;  // finish_merge, foldback, feedback
     return PIKV_OK;
@@ -782,7 +849,9 @@ int pikv_prefill_synthetic(pikv_engine* eng, int64_t tokens, uint64_t seed) {
             rc = run_step(eng, eng->in_q, eng->in_k, eng->in_v, nullptr, nullptr, false);
         } else {
             rc = enqueue_local(eng, eng->in_q, eng->in_k, eng->in_v, nullptr, false, nullptr);
-            if (!rc) rc = enqueue_finish(eng, eng->S.exchange, nullptr, false);
+            // synthetic prefill without a collective: each rank finishes on its own
+            // record (hit/miss counts then see only local shards)
+            if (!rc) rc = enqueue_finish(eng, eng->S.exchange, nullptr, false, 1);
         }
         if (rc) {
             eng->profiling = was_prof;

@@ -1267,8 +1267,9 @@ void launch_combine(const Dims& D, const Cfg& C, const State& S, const ExchangeL
 // finish: cross-rank merge -> y, global (m, l), summary
 // ===========================================================================
 __global__ void k_finish_merge(Dims D, Cfg C, State S, ExchangeLayout X,
-                               const uint8_t* __restrict__ gathered, float* __restrict__ y) {
+                               const uint8_t* __restrict__ gathered, float* __restrict__ y, int granks) {
     const int s = blockIdx.x, tid = threadIdx.x;
+    D.world = granks;  // records present in `gathered`
     const int64_t stride_rank = (int64_t)D.B * X.bytes_per_stream;
     for (int o = tid; o < D.H * D.dph; o += blockDim.x) {
         const int h = o / D.dph;
@@ -1405,8 +1406,8 @@ __global__ void k_feedback(Dims D, Cfg C, State S) {
 }
 
 void launch_finish_merge(const Dims& D, const Cfg& C, const State& S, const ExchangeLayout& X,
-                         const uint8_t* gathered, float* y, cudaStream_t st) {
-    k_finish_merge<<<D.B, 256, 0, st>>>(D, C, S, X, gathered, y);
+                         const uint8_t* gathered, float* y, int granks, cudaStream_t st) {
+    k_finish_merge<<<D.B, 256, 0, st>>>(D, C, S, X, gathered, y, granks);
 }
 void launch_foldback(const Dims& D, const State& S, cudaStream_t st) {
     const size_t smem = sizeof(float) * 2 * (size_t)D.B * D.H;

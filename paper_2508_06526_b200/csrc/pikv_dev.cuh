@@ -287,7 +287,7 @@ void launch_attend(const Dims& D, const State& S, cudaStream_t st);
 void launch_combine(const Dims& D, const Cfg& C, const State& S, const ExchangeLayout& X, float* y,
                     int direct, cudaStream_t st);
 void launch_finish_merge(const Dims& D, const Cfg& C, const State& S, const ExchangeLayout& X,
-                         const uint8_t* gathered, float* y, cudaStream_t st);
+                         const uint8_t* gathered, float* y, int granks, cudaStream_t st);
 void launch_foldback(const Dims& D, const State& S, cudaStream_t st);
 void launch_feedback(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);
 void launch_synth(const Dims& D, void* q, void* k, void* v, uint64_t seed, uint64_t step,
