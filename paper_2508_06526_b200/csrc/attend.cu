@@ -116,6 +116,7 @@ struct AttParams {
 // lane of the group holds the head's score and its own slice of o.
 template <class Dec, int CPT, int NB>
 __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttParams P) {
+    griddep_enter();
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr int N = Dec::N, NP = N / 2;
     uint64_t* full = (uint64_t*)smem;
@@ -372,7 +373,7 @@ template <class Dec, int CPT>
 void launch_t(const Dims& D, const State& S, const Plan& pl, cudaStream_t st) {
     auto kern = k_attend<Dec, CPT, 2>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
-    kern<<<D.attend_ctas, kThreads, pl.smem, st>>>(D, S, pl.P);
+    launch_pdl(kern, dim3(D.attend_ctas), dim3(kThreads), pl.smem, st, D, S, pl.P);
 }
 
 template <class Dec>

@@ -42,6 +42,7 @@ constexpr int kRouteCH = 256;    // columns per stage
 constexpr int kRouteStages = 5;
 
 __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin) {
+    griddep_enter();
     extern __shared__ __align__(128) uint8_t sm_raw[];
     uint64_t* full = (uint64_t*)sm_raw;
     uint64_t* empty = full + kRouteStages;
@@ -378,7 +379,7 @@ void launch_route(const Dims& D, const Cfg& C, const State& S, const void* q, cu
                         (size_t)kRouteStages * D.E * (kRouteCH * 8 + 16);
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_route, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int threads = ((D.E + 31) / 32) * 32 + 32;
-    k_route<<<D.B, threads, smem, st>>>(D, C, S, q);
+    launch_pdl(k_route, dim3(D.B), dim3(threads), smem, st, D, C, S, q);
 }
 
 // ===========================================================================
@@ -475,6 +476,7 @@ __device__ __forceinline__ void encode_row(const Dims& D, const State& S, const 
 __global__ void k_insert(Dims D, Cfg C, State S, const void* __restrict__ qin,
                          const void* __restrict__ kin, const void* __restrict__ vin,
                          const double* __restrict__ saliency) {
+    griddep_enter();
     extern __shared__ __align__(16) uint8_t sm_entry[];  // [entry_bytes] + tmp floats [d]
     __shared__ int64_t sm_dst[kMaxK];
     __shared__ int64_t sm_slot[kMaxK];
@@ -683,7 +685,7 @@ void launch_insert(const Dims& D, const Cfg& C, const State& S, const void* q, c
                    const void* v, const double* saliency, cudaStream_t st) {
     size_t smem = (size_t)((D.entry_bytes + 15) & ~15) + sizeof(float) * (size_t)D.d;
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_insert, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_insert<<<D.B, 256, smem, st>>>(D, C, S, q, k, v, saliency);
+    launch_pdl(k_insert, dim3(D.B), dim3(256), smem, st, D, C, S, q, k, v, saliency);
 }
 
 // ===========================================================================
@@ -694,6 +696,7 @@ void launch_insert(const Dims& D, const Cfg& C, const State& S, const void* q, c
 //     order (coalesced), lane 0 sums the member scores in that order in fp64
 //     (for_each_live order, kvstore.hpp:43-48; scheduler.cpp:276-289).
 __global__ void k_sched_pages(Dims D, Cfg C, State S, int lanes) {
+    griddep_enter();
     const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const int sub = lane / lanes, u0 = lane % lanes;
@@ -724,9 +727,13 @@ __global__ void k_sched_pages(Dims D, Cfg C, State S, int lanes) {
             const int i = (w + u) % (int)ps;
             const uint64_t sq = q * ps + (uint64_t)i;
             const int64_t gi = ring * D.S + (int64_t)(sq % Su);
+            // all loads of the slot in one round: score inputs are read even
+            // for non-members (discarded below) so they do not wait on id
             id = S.id[gi];
-            mem = id != 0 && S.shard_seq[gi] == sq;
-            if (mem) sc = score_entry(C, S, gi, now, D.n_layers);
+            const uint64_t ssq = S.shard_seq[gi];
+            sc = score_entry(C, S, gi, now, D.n_layers);
+            mem = id != 0 && ssq == sq;
+            if (!mem) sc = 0.0;
         }
         const unsigned bal = __ballot_sync(0xffffffffu, mem) & gmask;
         cnt += __popc(bal);
@@ -762,6 +769,7 @@ __device__ __forceinline__ bool page_less(double a, uint64_t oa, double b, uint6
 // (b) one CTA per (stream, local device): select_evictions + erase.
 constexpr int kSelThreads = 1024;
 __global__ void __launch_bounds__(kSelThreads) k_sched_select(Dims D, Cfg C, State S) {
+    griddep_enter();
     const int sg = blockIdx.x;  // s * Gl + gl
     const int s = sg / D.Gl, gl = sg % D.Gl;
     const int tid = threadIdx.x;
@@ -971,10 +979,10 @@ void launch_sched_pages(const Dims& D, const Cfg& C, const State& S, cudaStream_
     int lanes = 1;
     while (lanes < D.page_size && lanes < 32) lanes <<= 1;
     const int64_t threads = (int64_t)D.B * D.R * D.ppr_sched * lanes;
-    k_sched_pages<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(D, C, S, lanes);
+    launch_pdl(k_sched_pages, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0, st, D, C, S, lanes);
 }
 void launch_sched_select(const Dims& D, const Cfg& C, const State& S, cudaStream_t st) {
-    k_sched_select<<<D.B * D.Gl, kSelThreads, 0, st>>>(D, C, S);
+    launch_pdl(k_sched_select, dim3(D.B * D.Gl), dim3(kSelThreads), 0, st, D, C, S);
 }
 
 // ===========================================================================
@@ -982,6 +990,7 @@ void launch_sched_select(const Dims& D, const Cfg& C, const State& S, cudaStream
 // ===========================================================================
 // (a) count matches per (stream, candidate, chunk of chunk_slots slots)
 __global__ void k_retr_count(Dims D, State S) {
+    griddep_enter();
     const int s = blockIdx.x, c = blockIdx.y, ch = blockIdx.z;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     __shared__ int red[32][kMaxK + 1];
@@ -1053,6 +1062,7 @@ __device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t* wsum, int
 }
 
 __global__ void __launch_bounds__(1024) k_retr_scan(Dims D, State S) {
+    griddep_enter();
     __shared__ int64_t sm_n[1024];
     __shared__ int64_t wsum[32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
@@ -1105,6 +1115,7 @@ __global__ void __launch_bounds__(1024) k_retr_scan(Dims D, State S) {
 
 // (c) write the compacted (slot, entry) lists; bump freq / last_access.
 __global__ void k_retr_write(Dims D, State S) {
+    griddep_enter();
     const int s = blockIdx.x, c = blockIdx.y, ch = blockIdx.z;
     const int tid = threadIdx.x;
     if (S.err[s] || c >= S.ncand[s]) return;
@@ -1154,19 +1165,20 @@ __global__ void k_retr_write(Dims D, State S) {
 }
 
 void launch_retr_count(const Dims& D, const State& S, cudaStream_t st) {
-    k_retr_count<<<dim3(D.B, D.max_cand, D.nch), D.chunk_slots, 0, st>>>(D, S);
+    launch_pdl(k_retr_count, dim3(D.B, D.max_cand, D.nch), dim3(D.chunk_slots), 0, st, D, S);
 }
 void launch_retr_scan(const Dims& D, const State& S, cudaStream_t st) {
-    k_retr_scan<<<1, 1024, 0, st>>>(D, S);
+    launch_pdl(k_retr_scan, dim3(1), dim3(1024), 0, st, D, S);
 }
 void launch_retr_write(const Dims& D, const State& S, cudaStream_t st) {
-    k_retr_write<<<dim3(D.B, D.max_cand, D.nch), D.chunk_slots, 0, st>>>(D, S);
+    launch_pdl(k_retr_write, dim3(D.B, D.max_cand, D.nch), dim3(D.chunk_slots), 0, st, D, S);
 }
 
 // ===========================================================================
 // combine: per-stream merge of work-item partials into the exchange record
 // ===========================================================================
 __global__ void k_combine(Dims D, Cfg C, State S, ExchangeLayout X, float* __restrict__ y, int direct) {
+    griddep_enter();
     const int s = blockIdx.x, h = blockIdx.y;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
     extern __shared__ float sm_f[];  // [n_items of stream s] scale factors
@@ -1255,8 +1267,8 @@ __global__ void k_combine(Dims D, Cfg C, State S, ExchangeLayout X, float* __res
 void launch_combine(const Dims& D, const Cfg& C, const State& S, const ExchangeLayout& X, float* y,
                     int direct, cudaStream_t st) {
     const int threads = D.dph >= 128 ? 128 : (D.dph >= 64 ? 64 : 32);
-    k_combine<<<dim3(D.B, D.H), threads, sizeof(float) * (size_t)D.item_cap, st>>>(D, C, S, X, y,
-                                                                                 direct);
+    launch_pdl(k_combine, dim3(D.B, D.H), dim3(threads), sizeof(float) * (size_t)D.item_cap, st, D, C, S, X, y,
+               direct);
 }
 
 // ===========================================================================
@@ -1268,6 +1280,7 @@ void launch_combine(const Dims& D, const Cfg& C, const State& S, const ExchangeL
 // ===========================================================================
 __global__ void k_finish_merge(Dims D, Cfg C, State S, ExchangeLayout X,
                                const uint8_t* __restrict__ gathered, float* __restrict__ y, int granks) {
+    griddep_enter();
     const int s = blockIdx.x, tid = threadIdx.x;
     D.world = granks;  // records present in `gathered`
     const int64_t stride_rank = (int64_t)D.B * X.bytes_per_stream;
@@ -1331,6 +1344,7 @@ __global__ void k_finish_merge(Dims D, Cfg C, State S, ExchangeLayout X,
 // thread per retrieved entry (its H logits are contiguous: 16-byte loads);
 // the global (M, 1/L) of every (stream, head) are staged in shared memory.
 __global__ void k_foldback(Dims D, State S) {
+    griddep_enter();
     extern __shared__ float sm_ml[];  // [B*H] M, then [B*H] 1/L (0 when empty)
     __shared__ int64_t sm_base[1025];
     const int nb = D.B + 1;
@@ -1376,6 +1390,7 @@ __global__ void k_foldback(Dims D, State S) {
 // pipeline.cpp:258 (record_miss), 337-347 (adapt, observe_hits,
 // adakv_update); scheduler state.step++ (scheduler.cpp:328); now++.
 __global__ void k_feedback(Dims D, Cfg C, State S) {
+    griddep_enter();
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= D.B || S.err[s]) return;
     const int k = D.k, E = D.E;
@@ -1407,15 +1422,15 @@ __global__ void k_feedback(Dims D, Cfg C, State S) {
 
 void launch_finish_merge(const Dims& D, const Cfg& C, const State& S, const ExchangeLayout& X,
                          const uint8_t* gathered, float* y, int granks, cudaStream_t st) {
-    k_finish_merge<<<D.B, 256, 0, st>>>(D, C, S, X, gathered, y, granks);
+    launch_pdl(k_finish_merge, dim3(D.B), dim3(256), 0, st, D, C, S, X, gathered, y, granks);
 }
 void launch_foldback(const Dims& D, const State& S, cudaStream_t st) {
     const size_t smem = sizeof(float) * 2 * (size_t)D.B * D.H;
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_foldback, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_foldback<<<D.attend_ctas * 2, 256, smem, st>>>(D, S);
+    launch_pdl(k_foldback, dim3(D.attend_ctas * 2), dim3(256), smem, st, D, S);
 }
 void launch_feedback(const Dims& D, const Cfg& C, const State& S, cudaStream_t st) {
-    k_feedback<<<(D.B + 127) / 128, 128, 0, st>>>(D, C, S);
+    launch_pdl(k_feedback, dim3((D.B + 127) / 128), dim3(128), 0, st, D, C, S);
 }
 
 // ===========================================================================
@@ -1429,6 +1444,7 @@ __host__ __device__ __forceinline__ uint64_t splitmix(uint64_t x) {
 }
 
 __global__ void k_synth(int64_t n, int dtype, void* __restrict__ out, uint64_t seed) {
+    griddep_enter();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const uint64_t h = splitmix(seed ^ splitmix((uint64_t)i));
@@ -1444,9 +1460,9 @@ void launch_synth(const Dims& D, void* q, void* k, void* v, uint64_t seed, uint6
                   cudaStream_t st) {
     const int64_t n = (int64_t)D.B * D.d;
     const uint64_t base = splitmix(seed) ^ (step * 0x632be59bd9b4e019ull);
-    k_synth<<<256, 256, 0, st>>>(n, D.kv_dtype, q, base ^ 0x1111);
-    k_synth<<<256, 256, 0, st>>>(n, D.kv_dtype, k, base ^ 0x2222);
-    k_synth<<<256, 256, 0, st>>>(n, D.kv_dtype, v, base ^ 0x3333);
+    launch_pdl(k_synth, dim3(256), dim3(256), 0, st, n, D.kv_dtype, q, base ^ 0x1111);
+    launch_pdl(k_synth, dim3(256), dim3(256), 0, st, n, D.kv_dtype, k, base ^ 0x2222);
+    launch_pdl(k_synth, dim3(256), dim3(256), 0, st, n, D.kv_dtype, v, base ^ 0x3333);
 }
 
 }  // namespace pikv_dev

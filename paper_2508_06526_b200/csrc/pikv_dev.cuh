@@ -274,6 +274,33 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
     return p;
 }
 
+// ---- programmatic dependent launch ------------------------------------------
+// Every step kernel is launched with programmatic stream serialization and
+// starts with griddep_enter(): wait for the predecessor grid (and therefore,
+// transitively, every earlier kernel of the step) to complete and flush, then
+// allow the successor grid to be scheduled.  The wait must precede any early
+// return so that a kernel's completion still implies its predecessors'.
+__device__ __forceinline__ void griddep_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // ---- launch wrappers (defined in the .cu files) ----------------------------
 void launch_route(const Dims& D, const Cfg& C, const State& S, const void* q, cudaStream_t st);
 void launch_insert(const Dims& D, const Cfg& C, const State& S, const void* q, const void* k,
