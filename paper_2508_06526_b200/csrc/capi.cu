@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <random>
@@ -20,6 +21,14 @@
 using namespace pikv_dev;
 
 namespace pikv_dev {
+bool pdl_enabled() {
+    static const bool on = [] {
+        // measured neutral on c2 with graph replay (profiles/README.md); opt in
+        const char* v = std::getenv("PIKV_PDL");
+        return v && v[0] == '1';
+    }();
+    return on;
+}
 __global__ void k_shard_assign(const int64_t*, const int32_t*, int32_t, int32_t, int32_t, int32_t,
                                int32_t, int32_t*, int32_t*, int32_t*);
 __global__ void k_select(const double*, const uint64_t*, int32_t, int32_t, int32_t, double,
