@@ -355,12 +355,16 @@ Plan make_plan(const Dims& D) {
     pl.P.LPH = pl.P.CPH / cpt;
     pl.P.TPE = D.H * pl.P.LPH;
     pl.P.EP = pl.P.TPE > 0 ? kConsumers / pl.P.TPE : 0;
+    // entries per stage: ~32 KiB, at least one per sub-group when possible,
+    // and small enough that the ring keeps >= 3 stages in flight
+    const size_t redb = pl.P.EP > 1 ? sizeof(float) * (size_t)pl.P.EP * D.H * (D.dph + 2) : 0;
+    const int ring_max = (int)((kSmemBudget - 256 - redb) / D.entry_bytes);  // entries that fit
     int eps = (32 * 1024) / D.entry_bytes;
+    eps = std::max(eps, std::min(2 * pl.P.EP, 32));
+    eps = std::min(eps, std::max(1, ring_max / 3));
     eps = eps < 1 ? 1 : (eps > 32 ? 32 : eps);
-    if (eps < 2 * pl.P.EP) eps = std::min(32, 2 * pl.P.EP);
     pl.P.EPS = eps;
     pl.P.stage_bytes = eps * D.entry_bytes;
-    const size_t redb = pl.P.EP > 1 ? sizeof(float) * (size_t)pl.P.EP * D.H * (D.dph + 2) : 0;
     int nst = (int)((kSmemBudget - 256 - redb) / pl.P.stage_bytes);
     pl.P.NST = nst > 8 ? 8 : nst;
     pl.P.quant = D.codec == PIKV_CODEC_INT8 || D.codec == PIKV_CODEC_INT4;

@@ -411,28 +411,36 @@ __device__ __forceinline__ void encode_row(const Dims& D, const State& S, const 
         case PIKV_CODEC_LOWRANK:
         case PIKV_CODEC_LORAPLUS:
         case PIKV_CODEC_FASTV:
-        case PIKV_CODEC_PRUNE:
+        case PIKV_CODEC_PRUNE: {
+            // stage the row in smem (fp32), then one output per thread with the
+            // basis column read through the read-only path, 8 loads in flight
+            for (int i = tid; i < D.d; i += nt) {
+                float xi = load_in(x, D.kv_dtype, base + i);
+                if (D.codec == PIKV_CODEC_LORAPLUS) xi -= S.cbias[i];
+                tmp[i] = xi;
+            }
+            __syncthreads();
             for (int o = tid; o < D.dp; o += nt) {
                 const int h = o / r, j = o % r;
                 float val;
                 if (D.codec == PIKV_CODEC_FASTV) {
-                    val = load_in(x, D.kv_dtype, base + h * hd + j);
+                    val = tmp[h * hd + j];
                 } else if (D.codec == PIKV_CODEC_PRUNE) {
-                    val = load_in(x, D.kv_dtype, base + h * hd + S.kept[h * r + j]);
+                    val = tmp[h * hd + S.kept[h * r + j]];
                 } else {  // project_encode, compressor.cpp:318-329
                     const float* col = S.basis + ((int64_t)h * r + j) * hd;
+                    const float* xh = tmp + h * hd;
                     float acc = 0.f;
-                    for (int i = 0; i < hd; ++i) {
-                        float xi = load_in(x, D.kv_dtype, base + h * hd + i);
-                        if (D.codec == PIKV_CODEC_LORAPLUS) xi -= S.cbias[h * hd + i];
-                        acc = fmaf(col[i], xi, acc);
-                    }
+#pragma unroll 8
+                    for (int i = 0; i < hd; ++i) acc = fmaf(__ldg(col + i), xh[i], acc);
                     val = acc;
                 }
                 if (D.kv_dtype == PIKV_DTYPE_BF16) ((uint16_t*)dst)[o] = f32_to_bf16_rne(val);
                 else ((float*)dst)[o] = val;
             }
+            __syncthreads();
             return;
+        }
         case PIKV_CODEC_INT8:
         case PIKV_CODEC_INT4: {
             // symmetric absmax per head (oracle: po_quantize_row)
@@ -494,27 +502,43 @@ __global__ void k_insert(Dims D, Cfg C, State S, const void* __restrict__ qin,
         const int hd = D.d / D.H, r = D.dph;
         const int64_t base = (int64_t)s * D.d;
         float* qa = S.q_attn + (int64_t)s * D.dp;
-        for (int o = tid; o < D.dp; o += blockDim.x) {
-            const int h = o / r, j = o % r;
-            float val;
-            switch (D.codec) {
-                case PIKV_CODEC_LOWRANK:
-                case PIKV_CODEC_LORAPLUS: {
-                    const float* col = S.basis + ((int64_t)h * r + j) * hd;
-                    float acc = 0.f;
-                    for (int i = 0; i < hd; ++i) {
-                        float xi = load_in(qin, D.kv_dtype, base + h * hd + i);
-                        if (D.codec == PIKV_CODEC_LORAPLUS) xi -= S.cbias[h * hd + i];
-                        acc = fmaf(col[i], xi, acc);
-                    }
-                    val = acc;
-                    break;
-                }
-                case PIKV_CODEC_FASTV: val = load_in(qin, D.kv_dtype, base + h * hd + j); break;
-                case PIKV_CODEC_PRUNE: val = load_in(qin, D.kv_dtype, base + h * hd + S.kept[h * r + j]); break;
-                default: val = load_in(qin, D.kv_dtype, base + o); break;
+        const bool proj = D.codec == PIKV_CODEC_LOWRANK || D.codec == PIKV_CODEC_LORAPLUS ||
+                          D.codec == PIKV_CODEC_FASTV || D.codec == PIKV_CODEC_PRUNE;
+        if (!proj && D.kv_dtype == PIKV_DTYPE_BF16 && D.d % 8 == 0) {
+            const uint4* src = (const uint4*)((const uint16_t*)qin + base);
+            for (int v = tid; v < D.d / 8; v += blockDim.x) {
+                const uint4 w = src[v];
+                float4* dq = (float4*)(qa + v * 8);
+                dq[0] = make_float4(bf16_lo(w.x), bf16_hi(w.x), bf16_lo(w.y), bf16_hi(w.y));
+                dq[1] = make_float4(bf16_lo(w.z), bf16_hi(w.z), bf16_lo(w.w), bf16_hi(w.w));
             }
-            qa[o] = val;
+        } else if (!proj) {
+            for (int o = tid; o < D.d; o += blockDim.x) qa[o] = load_in(qin, D.kv_dtype, base + o);
+        } else {
+            __syncthreads();
+            for (int i = tid; i < D.d; i += blockDim.x) {
+                float xi = load_in(qin, D.kv_dtype, base + i);
+                if (D.codec == PIKV_CODEC_LORAPLUS) xi -= S.cbias[i];
+                tmp[i] = xi;
+            }
+            __syncthreads();
+            for (int o = tid; o < D.dp; o += blockDim.x) {
+                const int h = o / r, j = o % r;
+                float val;
+                if (D.codec == PIKV_CODEC_FASTV) {
+                    val = tmp[h * hd + j];
+                } else if (D.codec == PIKV_CODEC_PRUNE) {
+                    val = tmp[h * hd + S.kept[h * r + j]];
+                } else {
+                    const float* col = S.basis + ((int64_t)h * r + j) * hd;
+                    const float* xh = tmp + h * hd;
+                    float acc = 0.f;
+#pragma unroll 8
+                    for (int i = 0; i < hd; ++i) acc = fmaf(__ldg(col + i), xh[i], acc);
+                    val = acc;
+                }
+                qa[o] = val;
+            }
         }
     }
     // Bookkeeping.  Entry ids are issued in selection order on every rank
