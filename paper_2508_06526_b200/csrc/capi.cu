@@ -493,6 +493,8 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
             for (int i = 0; i < c.n_flex_plan; ++i) ex = ex && dyadic(c.flex_plan[i]);
         }
         C.exact_sum = ex && c.page_size <= 1024 ? 1 : 0;
+        C.record_agg = C.exact_sum && (c.sched_strategy == PIKV_SCHED_LRU ||
+                                       c.sched_strategy == PIKV_SCHED_LRU_PLUS) ? 1 : 0;
     }
 
     // exchange record layout
@@ -556,6 +558,10 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
     chk(S.n_ev = eng->alloc<int32_t>((size_t)B * std::max(D.Gl, 1)));
     chk(S.pages_before = eng->alloc<int32_t>((size_t)B * std::max(D.Gl, 1)));
     chk(S.pages_after = eng->alloc<int32_t>((size_t)B * std::max(D.Gl, 1)));
+    chk(S.pr_cnt = eng->alloc<int32_t>(rings * D.ppr_sched));
+    chk(S.pr_first = eng->alloc<int32_t>(rings * D.ppr_sched));
+    chk(S.pr_sla = eng->alloc<uint64_t>(rings * D.ppr_sched));
+    chk(S.pr_sf = eng->alloc<uint64_t>(rings * D.ppr_sched));
     chk(S.pg_agg = eng->alloc<double>(rings * D.ppr_sched));
     chk(S.pg_oldest = eng->alloc<uint64_t>(rings * D.ppr_sched));
     chk(S.pg_cnt = eng->alloc<int32_t>(rings * D.ppr_sched));
@@ -617,6 +623,10 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
     CUDA_TRY(cudaMemsetAsync(S.page_table, 0xff, sizeof(int32_t) * rings * D.ppr, st));
     CUDA_TRY(cudaMemsetAsync(S.id, 0, sizeof(uint64_t) * total_slots, st));
     CUDA_TRY(cudaMemsetAsync(S.attn_mass, 0, sizeof(double) * total_slots, st));
+    CUDA_TRY(cudaMemsetAsync(S.pr_cnt, 0, sizeof(int32_t) * rings * D.ppr_sched, st));
+    CUDA_TRY(cudaMemsetAsync(S.pr_first, 0, sizeof(int32_t) * rings * D.ppr_sched, st));
+    CUDA_TRY(cudaMemsetAsync(S.pr_sla, 0, sizeof(uint64_t) * rings * D.ppr_sched, st));
+    CUDA_TRY(cudaMemsetAsync(S.pr_sf, 0, sizeof(uint64_t) * rings * D.ppr_sched, st));
     CUDA_TRY(cudaMemsetAsync(S.n_ow, 0, sizeof(int32_t) * B, st));
     CUDA_TRY(cudaMemsetAsync(S.n_ev, 0, sizeof(int32_t) * B * std::max(D.Gl, 1), st));
     CUDA_TRY(cudaMemsetAsync(S.pages_before, 0, sizeof(int32_t) * B * std::max(D.Gl, 1), st));

@@ -382,6 +382,32 @@ void launch_route(const Dims& D, const Cfg& C, const State& S, const void* q, cu
     launch_pdl(k_route, dim3(D.B), dim3(threads), smem, st, D, C, S, q);
 }
 
+// page-record maintenance (see State::pr_*)
+__device__ __forceinline__ int64_t page_rec(const Dims& D, int64_t ring, uint64_t shard_seq) {
+    return ring * D.ppr_sched + (int64_t)((shard_seq / (uint64_t)D.page_size) % (uint64_t)D.ppr_sched);
+}
+__device__ __forceinline__ void rec_append(const Dims& D, const State& S, int64_t ring, uint64_t sq,
+                                           uint64_t now) {
+    const int64_t r = page_rec(D, ring, sq);
+    if (S.pr_cnt[r] == 0) {
+        S.pr_cnt[r] = 1;
+        S.pr_first[r] = (int)(sq % (uint64_t)D.page_size);
+        S.pr_sla[r] = now;
+        S.pr_sf[r] = 0;
+    } else {
+        S.pr_cnt[r] += 1;
+        S.pr_sla[r] += now;
+    }
+}
+__device__ __forceinline__ void rec_drop_front(const Dims& D, const State& S, int64_t ring, uint64_t sq,
+                                               uint64_t la, uint64_t fr) {
+    const int64_t r = page_rec(D, ring, sq);
+    S.pr_cnt[r] -= 1;
+    S.pr_first[r] += 1;
+    S.pr_sla[r] -= la;
+    S.pr_sf[r] -= fr;
+}
+
 // ===========================================================================
 // insert: KVStore::insert for the k staged entries of each stream
 // ===========================================================================
@@ -582,6 +608,7 @@ __global__ void k_insert(Dims D, Cfg C, State S, const void* __restrict__ qin,
                 const uint64_t old = S.id[gi];
                 if (old != 0) {  // displaced (kvstore.cpp:41-43; pipeline.cpp:200-208)
                     disp = true;
+                    rec_drop_front(D, S, ring, S.shard_seq[gi], S.last_access[gi], S.freq[gi]);
                     rec.step = now;
                     rec.entry_id = old;
                     rec.token_id = S.token[gi];
@@ -607,6 +634,7 @@ __global__ void k_insert(Dims D, Cfg C, State S, const void* __restrict__ qin,
                 }
                 if (!oom) {
                     S.id[gi] = S.next_id[s] + (uint64_t)j;
+                    rec_append(D, S, ring, S.seq[ring], now);
                     S.shard_seq[gi] = S.seq[ring]++;
                     S.token[gi] = token;
                     S.expert[gi] = e;
@@ -651,6 +679,7 @@ __global__ void k_insert(Dims D, Cfg C, State S, const void* __restrict__ qin,
             const int64_t pidx = ring * D.ppr + slot / D.spg;
             int32_t page = S.page_table[pidx];
             if (S.id[gi] != 0) {  // displaced (kvstore.cpp:41-43; pipeline.cpp:200-208)
+                rec_drop_front(D, S, ring, S.shard_seq[gi], S.last_access[gi], S.freq[gi]);
                 const int no = S.n_ow[s]++;
                 EvictRec& r = S.rec_ow[(int64_t)s * D.k + no];
                 r.step = now;
@@ -678,6 +707,7 @@ __global__ void k_insert(Dims D, Cfg C, State S, const void* __restrict__ qin,
                 S.page_live[page] += 1;
             }
             S.id[gi] = id;
+            rec_append(D, S, ring, S.seq[ring], now);
             S.shard_seq[gi] = S.seq[ring]++;
             S.token[gi] = token;
             S.expert[gi] = e;
@@ -715,10 +745,14 @@ void launch_insert(const Dims& D, const Cfg& C, const State& S, const void* q, c
 // ===========================================================================
 // sched: evict, scheduler.cpp:262-330
 // ===========================================================================
-// (a) one group of G = min(32, pow2 >= page_size) lanes per candidate
-//     scheduler page (ring, page_no): lane u loads the u-th member in slot
-//     order (coalesced), lane 0 sums the member scores in that order in fp64
-//     (for_each_live order, kvstore.hpp:43-48; scheduler.cpp:276-289).
+// (a) page keys (aggregate, oldest id, live count) for every candidate
+//     scheduler page (ring, page_no).  Dead pages (record count 0) cost one
+//     load.  LRU/LRU+ with exact sums take the aggregate from the page record:
+//     -(cnt*now - sum last_access) [+ lambda*sum freq] is the exact value of the
+//     reference's slot-order sum (every term and partial sum is an integer or
+//     dyadic below 2^53).  Other strategies score the live member range: lane u
+//     takes the u-th member in slot order (scheduler.cpp:276-289), lane 0 sums
+//     in that order (or a tree sum when exact in any order).
 __global__ void k_sched_pages(Dims D, Cfg C, State S, int lanes) {
     griddep_enter();
     const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -735,32 +769,47 @@ __global__ void k_sched_pages(Dims D, Cfg C, State S, int lanes) {
     const uint64_t Su = (uint64_t)D.S, ps = (uint64_t)D.page_size;
     const uint64_t lo = seq > Su ? seq - Su : 0;
     const uint64_t q = lo / ps + (uint64_t)pi;
-    const bool live_page = in && !S.err[s] && q * ps < seq;
-    const uint64_t s0 = (q * ps) % Su;
-    const int w = (s0 + ps > Su) ? (int)(Su - s0) : 0;  // members wrapping to slot 0 first
+    const int64_t rec = ring * D.ppr_sched + (int64_t)(q % (uint64_t)D.ppr_sched);
+    const int cnt = (in && q * ps < seq) ? S.pr_cnt[rec] : 0;
+    const bool live_page = cnt > 0 && !S.err[s];
     const uint64_t now = in ? S.now[s] : 0;
+    if (C.record_agg) {  // lanes == 1
+        if (!in) return;
+        double agg = 0.0;
+        uint64_t oldest = 0;
+        if (live_page) {
+            const int first = S.pr_first[rec];
+            const uint64_t sla = S.pr_sla[rec];
+            agg = -(double)((uint64_t)cnt * now - sla);
+            if (C.sched_strategy == PIKV_SCHED_LRU_PLUS)
+                agg = __dadd_rn(agg, __dmul_rn(C.lambda_freq, (double)S.pr_sf[rec]));
+            oldest = S.id[ring * D.S + (int64_t)((q * ps + (uint64_t)first) % Su)];
+        }
+        S.pg_cnt[t] = live_page ? cnt : 0;
+        S.pg_agg[t] = agg;
+        S.pg_oldest[t] = oldest;
+        return;
+    }
+    const int first = live_page ? S.pr_first[rec] : 0;
+    const uint64_t s0 = (q * ps) % Su;
+    const int w = (s0 + ps > Su) ? (int)(Su - s0) : 0;  // offsets wrapping to slot 0 come first
     double agg = 0.0;
     uint64_t oldest = ~0ull;
-    int cnt = 0;
     for (int base = 0; base < (int)ps; base += lanes) {
         const int u = base + u0;
         bool mem = false;
         double sc = 0.0;
         uint64_t id = 0;
         if (live_page && u < (int)ps) {
-            const int i = (w + u) % (int)ps;
-            const uint64_t sq = q * ps + (uint64_t)i;
-            const int64_t gi = ring * D.S + (int64_t)(sq % Su);
-            // all loads of the slot in one round: score inputs are read even
-            // for non-members (discarded below) so they do not wait on id
-            id = S.id[gi];
-            const uint64_t ssq = S.shard_seq[gi];
-            sc = score_entry(C, S, gi, now, D.n_layers);
-            mem = id != 0 && ssq == sq;
-            if (!mem) sc = 0.0;
+            const int i = (w + u) % (int)ps;  // member offset in slot order
+            if (i >= first && i < first + cnt) {
+                const int64_t gi = ring * D.S + (int64_t)((q * ps + (uint64_t)i) % Su);
+                id = S.id[gi];
+                sc = score_entry(C, S, gi, now, D.n_layers);
+                mem = true;
+            }
         }
         const unsigned bal = __ballot_sync(0xffffffffu, mem) & gmask;
-        cnt += __popc(bal);
         if (mem && id < oldest) oldest = id;
         if (C.exact_sum) {
             // every score and partial sum is exactly representable (integer /
@@ -780,9 +829,9 @@ __global__ void k_sched_pages(Dims D, Cfg C, State S, int lanes) {
         oldest = o2 < oldest ? o2 : oldest;
     }
     if (in && u0 == 0) {
-        S.pg_cnt[t] = cnt;
+        S.pg_cnt[t] = live_page ? cnt : 0;
         S.pg_agg[t] = agg;
-        S.pg_oldest[t] = cnt ? oldest : 0;
+        S.pg_oldest[t] = live_page ? oldest : 0;
     }
 }
 
@@ -991,6 +1040,13 @@ __global__ void __launch_bounds__(kSelThreads) k_sched_select(Dims D, Cfg C, Sta
                 }
                 o += __popc(bal);
             }
+            if (lane == 0) {  // the page is gone: reset its record
+                const int64_t r = ring * D.ppr_sched + (int64_t)(q % (uint64_t)D.ppr_sched);
+                S.pr_cnt[r] = 0;
+                S.pr_first[r] = 0;
+                S.pr_sla[r] = 0;
+                S.pr_sf[r] = 0;
+            }
         }
         __syncthreads();
         if (tid == kSelThreads - 1) sm_off = vcnt_off[tid] + cnt;
@@ -1001,7 +1057,7 @@ __global__ void __launch_bounds__(kSelThreads) k_sched_select(Dims D, Cfg C, Sta
 
 void launch_sched_pages(const Dims& D, const Cfg& C, const State& S, cudaStream_t st) {
     int lanes = 1;
-    while (lanes < D.page_size && lanes < 32) lanes <<= 1;
+    while (!C.record_agg && lanes < D.page_size && lanes < 32) lanes <<= 1;
     const int64_t threads = (int64_t)D.B * D.R * D.ppr_sched * lanes;
     launch_pdl(k_sched_pages, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0, st, D, C, S, lanes);
 }
@@ -1183,6 +1239,9 @@ __global__ void k_retr_write(Dims D, State S) {
         S.att_slot[pos] = (int32_t)gi;
         const int32_t page = S.page_table[ring * D.ppr + slot / D.spg];
         S.att_entry[pos] = page * D.spg + slot % D.spg;
+        const int64_t prec = page_rec(D, ring, S.shard_seq[gi]);
+        atomicAdd((unsigned long long*)&S.pr_sla[prec], (unsigned long long)(now - S.last_access[gi]));
+        atomicAdd((unsigned long long*)&S.pr_sf[prec], 1ull);
         S.freq[gi] += 1;  // kvstore.cpp:165-168
         S.last_access[gi] = now;
     }

@@ -69,6 +69,7 @@ struct Cfg {  // scalar config needed on device (copied by value into kernels)
     double flex_plan[32];
     int unbounded_budget, head_width;
     int exact_sum;  // page aggregates are exact in any order (see capi.cu)
+    int record_agg; // LRU / LRU+ with exact sums: aggregates from page records
 };
 
 struct State {
@@ -127,6 +128,14 @@ struct State {
     int32_t* n_ev;     // [B*Gl]
     int32_t* pages_before;  // [B*Gl]
     int32_t* pages_after;   // [B*Gl]
+    // per-page records, [B*R][ppr_sched] indexed by page_no % ppr_sched:
+    // live members of a scheduler page are the contiguous shard_seq range
+    // [q*ps + pr_first, q*ps + pr_first + pr_cnt) (erasure is whole pages or a
+    // ring overwrite of the page's front member)
+    int32_t* pr_cnt;
+    int32_t* pr_first;
+    uint64_t* pr_sla;       // sum of last_access over live members
+    uint64_t* pr_sf;        // sum of freq over live members
     double* pg_agg;         // [B*R][ppr_sched]
     uint64_t* pg_oldest;
     int32_t* pg_cnt;
