@@ -416,6 +416,29 @@ __device__ __forceinline__ float load_in(const void* p, int dtype, int64_t i) {
     return ((const float*)p)[i];
 }
 
+// Per-head projection y[h][j] = sum_i B[h][j][i] x[h*hd + i] of a row staged
+// in smem: one warp per output, lanes across i (coalesced basis reads, shared
+// by every stream through L2), warp-shuffle reduction.
+__device__ __forceinline__ float proj_out(const State& S, const float* x, int h, int j, int hd, int r) {
+    const int lane = threadIdx.x & 31;
+    const float* col = S.basis + ((int64_t)h * r + j) * hd;
+    const float* xh = x + h * hd;
+    float acc = 0.f;
+    if ((hd & 3) == 0) {
+        for (int i = lane * 4; i < hd; i += 128) {
+            const float4 b = __ldg((const float4*)(col + i));
+            acc = fmaf(b.x, xh[i], acc);
+            acc = fmaf(b.y, xh[i + 1], acc);
+            acc = fmaf(b.z, xh[i + 2], acc);
+            acc = fmaf(b.w, xh[i + 3], acc);
+        }
+    } else {
+        for (int i = lane; i < hd; i += 32) acc = fmaf(__ldg(col + i), xh[i], acc);
+    }
+    for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    return acc;
+}
+
 // Encode one K or V row of stream s into smem `dst` in the stored layout.
 __device__ __forceinline__ void encode_row(const Dims& D, const State& S, const void* x, int s, uint8_t* dst,
                            float* scales_out, float* tmp) {
@@ -446,23 +469,22 @@ __device__ __forceinline__ void encode_row(const Dims& D, const State& S, const 
                 tmp[i] = xi;
             }
             __syncthreads();
-            for (int o = tid; o < D.dp; o += nt) {
-                const int h = o / r, j = o % r;
-                float val;
-                if (D.codec == PIKV_CODEC_FASTV) {
-                    val = tmp[h * hd + j];
-                } else if (D.codec == PIKV_CODEC_PRUNE) {
-                    val = tmp[h * hd + S.kept[h * r + j]];
-                } else {  // project_encode, compressor.cpp:318-329
-                    const float* col = S.basis + ((int64_t)h * r + j) * hd;
-                    const float* xh = tmp + h * hd;
-                    float acc = 0.f;
-#pragma unroll 8
-                    for (int i = 0; i < hd; ++i) acc = fmaf(__ldg(col + i), xh[i], acc);
-                    val = acc;
+            if (D.codec == PIKV_CODEC_FASTV || D.codec == PIKV_CODEC_PRUNE) {
+                for (int o = tid; o < D.dp; o += nt) {
+                    const int h = o / r, j = o % r;
+                    const float val = D.codec == PIKV_CODEC_FASTV ? tmp[h * hd + j] : tmp[h * hd + S.kept[h * r + j]];
+                    if (D.kv_dtype == PIKV_DTYPE_BF16) ((uint16_t*)dst)[o] = f32_to_bf16_rne(val);
+                    else ((float*)dst)[o] = val;
                 }
-                if (D.kv_dtype == PIKV_DTYPE_BF16) ((uint16_t*)dst)[o] = f32_to_bf16_rne(val);
-                else ((float*)dst)[o] = val;
+            } else {  // project_encode, compressor.cpp:318-329
+                const int warp = tid >> 5, nw = nt >> 5, lane = tid & 31;
+                for (int o = warp; o < D.dp; o += nw) {
+                    const float val = proj_out(S, tmp, o / r, o % r, hd, r);
+                    if (lane == 0) {
+                        if (D.kv_dtype == PIKV_DTYPE_BF16) ((uint16_t*)dst)[o] = f32_to_bf16_rne(val);
+                        else ((float*)dst)[o] = val;
+                    }
+                }
             }
             __syncthreads();
             return;
@@ -548,22 +570,17 @@ __global__ void k_insert(Dims D, Cfg C, State S, const void* __restrict__ qin,
                 tmp[i] = xi;
             }
             __syncthreads();
-            for (int o = tid; o < D.dp; o += blockDim.x) {
-                const int h = o / r, j = o % r;
-                float val;
-                if (D.codec == PIKV_CODEC_FASTV) {
-                    val = tmp[h * hd + j];
-                } else if (D.codec == PIKV_CODEC_PRUNE) {
-                    val = tmp[h * hd + S.kept[h * r + j]];
-                } else {
-                    const float* col = S.basis + ((int64_t)h * r + j) * hd;
-                    const float* xh = tmp + h * hd;
-                    float acc = 0.f;
-#pragma unroll 8
-                    for (int i = 0; i < hd; ++i) acc = fmaf(__ldg(col + i), xh[i], acc);
-                    val = acc;
+            if (D.codec == PIKV_CODEC_FASTV || D.codec == PIKV_CODEC_PRUNE) {
+                for (int o = tid; o < D.dp; o += blockDim.x) {
+                    const int h = o / r, j = o % r;
+                    qa[o] = D.codec == PIKV_CODEC_FASTV ? tmp[h * hd + j] : tmp[h * hd + S.kept[h * r + j]];
                 }
-                qa[o] = val;
+            } else {
+                const int warp = tid >> 5, nw = blockDim.x >> 5, lane = tid & 31;
+                for (int o = warp; o < D.dp; o += nw) {
+                    const float val = proj_out(S, tmp, o / r, o % r, hd, r);
+                    if (lane == 0) qa[o] = val;
+                }
             }
         }
     }
