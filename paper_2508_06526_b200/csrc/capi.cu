@@ -643,7 +643,7 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
     CUDA_TRY(cudaMemcpyAsync(S.free_top, &top, sizeof(int32_t), cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaMemsetAsync(eng->in_sal, 0, sizeof(double) * B * std::max(D.n_layers, 1), st));
     CUDA_TRY(cudaStreamSynchronize(st));
-    S.basis = nullptr, S.cbias = nullptr, S.kept = nullptr;
+    S.basis = nullptr, S.basis_t = nullptr, S.cbias = nullptr, S.kept = nullptr;
     *out = eng;
     return PIKV_OK;
 }
@@ -678,7 +678,15 @@ int pikv_set_codec_host(pikv_engine* eng, const float* basis, const float* bias,
         if (p) cudaMemcpy(p, src, bytes, cudaMemcpyHostToDevice);
         return p;
     };
-    if (basis) eng->S.basis = (const float*)up(basis, sizeof(float) * (size_t)D.H * r * hd);
+    if (basis) {
+        eng->S.basis = (const float*)up(basis, sizeof(float) * (size_t)D.H * r * hd);
+        std::vector<float> bt((size_t)D.H * r * hd);
+        for (int h = 0; h < D.H; ++h)
+            for (int j = 0; j < r; ++j)
+                for (int i = 0; i < hd; ++i)
+                    bt[((size_t)h * hd + i) * r + j] = basis[((size_t)h * r + j) * hd + i];
+        eng->S.basis_t = (const float*)up(bt.data(), sizeof(float) * bt.size());
+    }
     if (bias) eng->S.cbias = (const float*)up(bias, sizeof(float) * (size_t)D.d);
     if (kept) {
         for (int i = 0; i < D.H * r; ++i)
@@ -726,9 +734,14 @@ static int enqueue_local(pikv_engine* eng, const void* q, const void* k, const v
     launch_insert(D, eng->C, S, q, k, v, sal, st), ++n;
     mark(eng, 2);
     const bool sched = D.Gl > 0 && !eng->C.unbounded_budget;
-    if (sched) launch_sched_pages(D, eng->C, S, st), ++n;
-    mark(eng, 3);
-    if (sched) launch_sched_select(D, eng->C, S, st), ++n;
+    if (sched && eng->C.record_agg) {
+        launch_sched_fused(D, eng->C, S, st), ++n;  // page keys from records + select, one CTA per device
+        mark(eng, 3);
+    } else {
+        if (sched) launch_sched_pages(D, eng->C, S, st), ++n;
+        mark(eng, 3);
+        if (sched) launch_sched_select(D, eng->C, S, st), ++n;
+    }
     mark(eng, 4);
     launch_retr_count(D, S, st), ++n;
     mark(eng, 5);

@@ -417,25 +417,17 @@ __device__ __forceinline__ float load_in(const void* p, int dtype, int64_t i) {
 }
 
 // Per-head projection y[h][j] = sum_i B[h][j][i] x[h*hd + i] of a row staged
-// in smem: one warp per output, lanes across i (coalesced basis reads, shared
-// by every stream through L2), warp-shuffle reduction.
+// in smem, one thread per output over the i-major basis copy B^T[h][i][j]:
+// lanes of a warp read consecutive j (coalesced, shared by every stream via
+// L2), the x[i] read is a shared-memory broadcast, and the loads are
+// independent so many are in flight.  Same summation order as
+// project_encode (compressor.cpp:318-329): i ascending.
 __device__ __forceinline__ float proj_out(const State& S, const float* x, int h, int j, int hd, int r) {
-    const int lane = threadIdx.x & 31;
-    const float* col = S.basis + ((int64_t)h * r + j) * hd;
+    const float* bt = S.basis_t + (int64_t)h * hd * r + j;
     const float* xh = x + h * hd;
     float acc = 0.f;
-    if ((hd & 3) == 0) {
-        for (int i = lane * 4; i < hd; i += 128) {
-            const float4 b = __ldg((const float4*)(col + i));
-            acc = fmaf(b.x, xh[i], acc);
-            acc = fmaf(b.y, xh[i + 1], acc);
-            acc = fmaf(b.z, xh[i + 2], acc);
-            acc = fmaf(b.w, xh[i + 3], acc);
-        }
-    } else {
-        for (int i = lane; i < hd; i += 32) acc = fmaf(__ldg(col + i), xh[i], acc);
-    }
-    for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+#pragma unroll 8
+    for (int i = 0; i < hd; ++i) acc = fmaf(__ldg(bt + (int64_t)i * r), xh[i], acc);
     return acc;
 }
 
@@ -463,10 +455,22 @@ __device__ __forceinline__ void encode_row(const Dims& D, const State& S, const 
         case PIKV_CODEC_PRUNE: {
             // stage the row in smem (fp32), then one output per thread with the
             // basis column read through the read-only path, 8 loads in flight
-            for (int i = tid; i < D.d; i += nt) {
-                float xi = load_in(x, D.kv_dtype, base + i);
-                if (D.codec == PIKV_CODEC_LORAPLUS) xi -= S.cbias[i];
-                tmp[i] = xi;
+            if (D.kv_dtype == PIKV_DTYPE_BF16 && D.d % 8 == 0) {
+                const uint4* src = (const uint4*)((const uint16_t*)x + base);
+                for (int v = tid; v < D.d / 8; v += nt) {
+                    const uint4 w = src[v];
+                    const float e[8] = {bf16_lo(w.x), bf16_hi(w.x), bf16_lo(w.y), bf16_hi(w.y),
+                                        bf16_lo(w.z), bf16_hi(w.z), bf16_lo(w.w), bf16_hi(w.w)};
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        tmp[v * 8 + u] = D.codec == PIKV_CODEC_LORAPLUS ? e[u] - S.cbias[v * 8 + u] : e[u];
+                }
+            } else {
+                for (int i = tid; i < D.d; i += nt) {
+                    float xi = load_in(x, D.kv_dtype, base + i);
+                    if (D.codec == PIKV_CODEC_LORAPLUS) xi -= S.cbias[i];
+                    tmp[i] = xi;
+                }
             }
             __syncthreads();
             if (D.codec == PIKV_CODEC_FASTV || D.codec == PIKV_CODEC_PRUNE) {
@@ -477,13 +481,10 @@ __device__ __forceinline__ void encode_row(const Dims& D, const State& S, const 
                     else ((float*)dst)[o] = val;
                 }
             } else {  // project_encode, compressor.cpp:318-329
-                const int warp = tid >> 5, nw = nt >> 5, lane = tid & 31;
-                for (int o = warp; o < D.dp; o += nw) {
+                for (int o = tid; o < D.dp; o += nt) {
                     const float val = proj_out(S, tmp, o / r, o % r, hd, r);
-                    if (lane == 0) {
-                        if (D.kv_dtype == PIKV_DTYPE_BF16) ((uint16_t*)dst)[o] = f32_to_bf16_rne(val);
-                        else ((float*)dst)[o] = val;
-                    }
+                    if (D.kv_dtype == PIKV_DTYPE_BF16) ((uint16_t*)dst)[o] = f32_to_bf16_rne(val);
+                    else ((float*)dst)[o] = val;
                 }
             }
             __syncthreads();
@@ -576,11 +577,7 @@ __global__ void k_insert(Dims D, Cfg C, State S, const void* __restrict__ qin,
                     qa[o] = D.codec == PIKV_CODEC_FASTV ? tmp[h * hd + j] : tmp[h * hd + S.kept[h * r + j]];
                 }
             } else {
-                const int warp = tid >> 5, nw = blockDim.x >> 5, lane = tid & 31;
-                for (int o = warp; o < D.dp; o += nw) {
-                    const float val = proj_out(S, tmp, o / r, o % r, hd, r);
-                    if (lane == 0) qa[o] = val;
-                }
+                for (int o = tid; o < D.dp; o += blockDim.x) qa[o] = proj_out(S, tmp, o / r, o % r, hd, r);
             }
         }
     }
@@ -858,9 +855,7 @@ __device__ __forceinline__ bool page_less(double a, uint64_t oa, double b, uint6
 
 // (b) one CTA per (stream, local device): select_evictions + erase.
 constexpr int kSelThreads = 1024;
-__global__ void __launch_bounds__(kSelThreads) k_sched_select(Dims D, Cfg C, State S) {
-    griddep_enter();
-    const int sg = blockIdx.x;  // s * Gl + gl
+__device__ __forceinline__ void select_body(const Dims& D, const Cfg& C, const State& S, const int sg) {
     const int s = sg / D.Gl, gl = sg % D.Gl;
     const int tid = threadIdx.x;
     __shared__ int sm_red[32];
@@ -1072,11 +1067,60 @@ __global__ void __launch_bounds__(kSelThreads) k_sched_select(Dims D, Cfg C, Sta
     if (tid == 0) S.n_ev[sg] = sm_off;
 }
 
+__global__ void __launch_bounds__(kSelThreads) k_sched_select(Dims D, Cfg C, State S) {
+    griddep_enter();
+    select_body(D, C, S, blockIdx.x);
+}
+
+// LRU / LRU+ with exact sums: one CTA per (stream, local device) computes the
+// keys of all its candidate pages from the page records, then selects and
+// erases in place (evict, scheduler.cpp:262-330) -- one launch, no slot scan.
+__global__ void __launch_bounds__(kSelThreads) k_sched_fused(Dims D, Cfg C, State S) {
+    griddep_enter();
+    const int sg = blockIdx.x;
+    const int s = sg / D.Gl;
+    const int tid = threadIdx.x;
+    __shared__ uint64_t sm_seq[64];
+    if (S.err[s]) return;
+    for (int sh = tid; sh < D.SPD && sh < 64; sh += kSelThreads) sm_seq[sh] = S.seq[(int64_t)sg * D.SPD + sh];
+    __syncthreads();
+    const uint64_t now = S.now[s];
+    const uint64_t Su = (uint64_t)D.S, ps = (uint64_t)D.page_size;
+    const int64_t first_t = (int64_t)sg * D.SPD * D.ppr_sched;
+    const int npg = D.SPD * D.ppr_sched;
+#pragma unroll 4
+    for (int i = tid; i < npg; i += kSelThreads) {
+        const int sh = i / D.ppr_sched, pi = i % D.ppr_sched;
+        const int64_t ring = (int64_t)sg * D.SPD + sh;
+        const uint64_t seq = sh < 64 ? sm_seq[sh] : S.seq[ring];
+        const uint64_t lo = seq > Su ? seq - Su : 0;
+        const uint64_t q = lo / ps + (uint64_t)pi;
+        const int64_t rec = ring * D.ppr_sched + (int64_t)(q % (uint64_t)D.ppr_sched);
+        const int cnt = q * ps < seq ? S.pr_cnt[rec] : 0;
+        double agg = 0.0;
+        uint64_t oldest = 0;
+        if (cnt > 0) {
+            agg = -(double)((uint64_t)cnt * now - S.pr_sla[rec]);
+            if (C.sched_strategy == PIKV_SCHED_LRU_PLUS)
+                agg = __dadd_rn(agg, __dmul_rn(C.lambda_freq, (double)S.pr_sf[rec]));
+            oldest = S.id[ring * D.S + (int64_t)((q * ps + (uint64_t)S.pr_first[rec]) % Su)];
+        }
+        S.pg_cnt[first_t + i] = cnt;
+        S.pg_agg[first_t + i] = agg;
+        S.pg_oldest[first_t + i] = oldest;
+    }
+    __syncthreads();
+    select_body(D, C, S, sg);
+}
+
 void launch_sched_pages(const Dims& D, const Cfg& C, const State& S, cudaStream_t st) {
     int lanes = 1;
     while (!C.record_agg && lanes < D.page_size && lanes < 32) lanes <<= 1;
     const int64_t threads = (int64_t)D.B * D.R * D.ppr_sched * lanes;
     launch_pdl(k_sched_pages, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0, st, D, C, S, lanes);
+}
+void launch_sched_fused(const Dims& D, const Cfg& C, const State& S, cudaStream_t st) {
+    launch_pdl(k_sched_fused, dim3(D.B * D.Gl), dim3(kSelThreads), 0, st, D, C, S);
 }
 void launch_sched_select(const Dims& D, const Cfg& C, const State& S, cudaStream_t st) {
     launch_pdl(k_sched_select, dim3(D.B * D.Gl), dim3(kSelThreads), 0, st, D, C, S);

@@ -113,6 +113,7 @@ struct State {
     int32_t* free_top;
     // codec params
     const float* basis;  // [H][r][hd]
+    const float* basis_t;  // [H][hd][r] (i-major copy for coalesced projection)
     const float* cbias;  // [d]
     const int32_t* kept; // [H][r]
     // step scratch
@@ -319,6 +320,7 @@ void launch_insert(const Dims& D, const Cfg& C, const State& S, const void* q, c
                    const void* v, const double* saliency, cudaStream_t st);
 void launch_sched_pages(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);
 void launch_sched_select(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);
+void launch_sched_fused(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);
 void launch_retr_count(const Dims& D, const State& S, cudaStream_t st);
 void launch_retr_scan(const Dims& D, const State& S, cudaStream_t st);
 void launch_retr_write(const Dims& D, const State& S, cudaStream_t st);

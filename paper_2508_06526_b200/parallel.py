@@ -33,13 +33,18 @@ def device_view(ptr: int, nbytes: int) -> torch.Tensor:
 
 
 def all_gather_bytes(out: torch.Tensor, local: torch.Tensor, group=None):
-    """out[r * n:(r+1) * n] = local of rank r."""
+    """out[r * n:(r+1) * n] = local of rank r.  NCCL gathers device buffers in
+    place; gloo (CPU tests, or a single-GPU rehearsal of the multi-rank path)
+    stages device buffers through host memory."""
     if dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(out, local, group=group)
-    else:
-        n = local.numel()
-        parts = [out[r * n:(r + 1) * n] for r in range(dist.get_world_size(group))]
-        dist.all_gather(parts, local, group=group)
+        return out
+    n = local.numel()
+    loc = local.cpu() if local.is_cuda else local
+    host = torch.empty(out.numel(), dtype=out.dtype)
+    parts = [host[r * n:(r + 1) * n] for r in range(dist.get_world_size(group))]
+    dist.all_gather(parts, loc, group=group)
+    out.copy_(host)
     return out
 
 
@@ -55,7 +60,8 @@ class ShardedStepper:
         self.group = group
         self.world = dist.get_world_size(group)
         self.nbytes = engine.exchange_bytes()
-        dev = "cuda" if torch.cuda.is_available() and dist.get_backend(group) == "nccl" else "cpu"
+        on_gpu = engine.external_stream() is not None
+        dev = "cuda" if on_gpu else "cpu"
         self.gathered = torch.empty(self.world * self.nbytes, dtype=torch.uint8, device=dev)
 
     def step(self, q, k, v, y=None, saliency=None):
