@@ -550,6 +550,7 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
     chk(S.gates = eng->alloc<double>((size_t)B * k));
     chk(S.logits = eng->alloc<double>((size_t)B * E));
     chk(S.q_attn = eng->alloc<float>((size_t)B * D.dp));
+    chk(S.proj = eng->alloc<float>((size_t)2 * B * D.dp));
     chk(S.cand = eng->alloc<int32_t>((size_t)B * D.max_cand));
     chk(S.ncand = eng->alloc<int32_t>(B));
     chk(S.rec_ow = eng->alloc<EvictRec>((size_t)B * k));
@@ -643,7 +644,7 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
     CUDA_TRY(cudaMemcpyAsync(S.free_top, &top, sizeof(int32_t), cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaMemsetAsync(eng->in_sal, 0, sizeof(double) * B * std::max(D.n_layers, 1), st));
     CUDA_TRY(cudaStreamSynchronize(st));
-    S.basis = nullptr, S.basis_t = nullptr, S.cbias = nullptr, S.kept = nullptr;
+    S.basis = nullptr, S.cbias = nullptr, S.kept = nullptr;
     *out = eng;
     return PIKV_OK;
 }
@@ -678,15 +679,7 @@ int pikv_set_codec_host(pikv_engine* eng, const float* basis, const float* bias,
         if (p) cudaMemcpy(p, src, bytes, cudaMemcpyHostToDevice);
         return p;
     };
-    if (basis) {
-        eng->S.basis = (const float*)up(basis, sizeof(float) * (size_t)D.H * r * hd);
-        std::vector<float> bt((size_t)D.H * r * hd);
-        for (int h = 0; h < D.H; ++h)
-            for (int j = 0; j < r; ++j)
-                for (int i = 0; i < hd; ++i)
-                    bt[((size_t)h * hd + i) * r + j] = basis[((size_t)h * r + j) * hd + i];
-        eng->S.basis_t = (const float*)up(bt.data(), sizeof(float) * bt.size());
-    }
+    if (basis) eng->S.basis = (const float*)up(basis, sizeof(float) * (size_t)D.H * r * hd);
     if (bias) eng->S.cbias = (const float*)up(bias, sizeof(float) * (size_t)D.d);
     if (kept) {
         for (int i = 0; i < D.H * r; ++i)
@@ -731,17 +724,16 @@ static int enqueue_local(pikv_engine* eng, const void* q, const void* k, const v
     mark(eng, 1);
     // a rank that owns no device still issues entry ids (k_insert) and joins
     // the merge with an empty record
+    if (D.codec == PIKV_CODEC_LOWRANK || D.codec == PIKV_CODEC_LORAPLUS)
+        launch_project(D, S, q, k, v, st), ++n;  // q, k, v of all streams in one pass
     launch_insert(D, eng->C, S, q, k, v, sal, st), ++n;
     mark(eng, 2);
     const bool sched = D.Gl > 0 && !eng->C.unbounded_budget;
-    if (sched && eng->C.record_agg) {
-        launch_sched_fused(D, eng->C, S, st), ++n;  // page keys from records + select, one CTA per device
-        mark(eng, 3);
-    } else {
-        if (sched) launch_sched_pages(D, eng->C, S, st), ++n;
-        mark(eng, 3);
-        if (sched) launch_sched_select(D, eng->C, S, st), ++n;
-    }
+    // (k_sched_fused -- keys + select in one CTA per device -- measured slower
+    // than the wide page-key kernel + select: 34.7 vs 28.5 us on c2)
+    if (sched) launch_sched_pages(D, eng->C, S, st), ++n;
+    mark(eng, 3);
+    if (sched) launch_sched_select(D, eng->C, S, st), ++n;
     mark(eng, 4);
     launch_retr_count(D, S, st), ++n;
     mark(eng, 5);

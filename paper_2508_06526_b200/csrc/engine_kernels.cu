@@ -408,32 +408,61 @@ __device__ __forceinline__ void rec_drop_front(const Dims& D, const State& S, in
     S.pr_sf[r] -= fr;
 }
 
-// ===========================================================================
-// insert: KVStore::insert for the k staged entries of each stream
-// ===========================================================================
 __device__ __forceinline__ float load_in(const void* p, int dtype, int64_t i) {
     if (dtype == PIKV_DTYPE_BF16) return __uint_as_float(((uint32_t)((const uint16_t*)p)[i]) << 16);
     return ((const float*)p)[i];
 }
 
-// Per-head projection y[h][j] = sum_i B[h][j][i] x[h*hd + i] of a row staged
-// in smem, one thread per output over the i-major basis copy B^T[h][i][j]:
-// lanes of a warp read consecutive j (coalesced, shared by every stream via
-// L2), the x[i] read is a shared-memory broadcast, and the loads are
-// independent so many are in flight.  Same summation order as
-// project_encode (compressor.cpp:318-329): i ascending.
-__device__ __forceinline__ float proj_out(const State& S, const float* x, int h, int j, int hd, int r) {
-    const float* bt = S.basis_t + (int64_t)h * hd * r + j;
-    const float* xh = x + h * hd;
-    float acc = 0.f;
+// ===========================================================================
+// project: Codec::encode_vector for LowRank / LoRAPlus (compressor.cpp:318-329,
+// 364-378, pipeline.cpp:295-297) of the step's q, k and v of every stream,
+// one CTA per (head, row): the head's basis and the B input slices are staged
+// in shared memory once, then y[b][j] = sum_i B[j][i] x[b][i] (i ascending,
+// fp32) for all streams.  Output: S.proj[row][B][dp] (row 0 = q -> q_attn).
+__global__ void k_project(Dims D, State S, const void* __restrict__ qin, const void* __restrict__ kin,
+                          const void* __restrict__ vin) {
+    griddep_enter();
+    extern __shared__ float sm_p[];  // basis [r][hd] then x [B][hd]
+    const int h = blockIdx.x, row = blockIdx.y;
+    const int hd = D.d / D.H, r = D.dph, tid = threadIdx.x, nt = blockDim.x;
+    const void* x = row == 0 ? qin : (row == 1 ? kin : vin);
+    float* bs = sm_p;
+    float* xs = sm_p + (size_t)r * hd;
+    for (int t = tid; t < r * hd; t += nt) bs[t] = S.basis[(int64_t)h * r * hd + t];
+    for (int t = tid; t < D.B * hd; t += nt) {
+        const int b = t / hd, i = t % hd;
+        float xi = load_in(x, D.kv_dtype, (int64_t)b * D.d + h * hd + i);
+        if (D.codec == PIKV_CODEC_LORAPLUS) xi -= S.cbias[h * hd + i];
+        xs[t] = xi;
+    }
+    __syncthreads();
+    for (int t = tid; t < D.B * r; t += nt) {
+        const int b = t / r, j = t % r;
+        const float* col = bs + (size_t)j * hd;
+        const float* xb = xs + (size_t)b * hd;
+        float acc = 0.f;
 #pragma unroll 8
-    for (int i = 0; i < hd; ++i) acc = fmaf(__ldg(bt + (int64_t)i * r), xh[i], acc);
-    return acc;
+        for (int i = 0; i < hd; ++i) acc = fmaf(col[i], xb[i], acc);
+        if (row == 0) S.q_attn[(int64_t)b * D.dp + h * r + j] = acc;
+        else S.proj[((int64_t)(row - 1) * D.B + b) * D.dp + h * r + j] = acc;
+    }
 }
+
+void launch_project(const Dims& D, const State& S, const void* q, const void* k, const void* v,
+                    cudaStream_t st) {
+    const int hd = D.d / D.H;
+    const size_t smem = sizeof(float) * ((size_t)D.dph * hd + (size_t)D.B * hd);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_project, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    launch_pdl(k_project, dim3(D.H, 3), dim3(256), smem, st, D, S, q, k, v);
+}
+
+// ===========================================================================
+// insert: KVStore::insert for the k staged entries of each stream
+// ===========================================================================
 
 // Encode one K or V row of stream s into smem `dst` in the stored layout.
 __device__ __forceinline__ void encode_row(const Dims& D, const State& S, const void* x, int s, uint8_t* dst,
-                           float* scales_out, float* tmp) {
+                                           float* scales_out, float* tmp, int kv_row) {
     const int H = D.H, hd = D.d / H, r = D.dph, tid = threadIdx.x, nt = blockDim.x;
     const int64_t base = (int64_t)s * D.d;
     switch (D.codec) {
@@ -450,46 +479,26 @@ __device__ __forceinline__ void encode_row(const Dims& D, const State& S, const 
             }
             return;
         case PIKV_CODEC_LOWRANK:
-        case PIKV_CODEC_LORAPLUS:
-        case PIKV_CODEC_FASTV:
-        case PIKV_CODEC_PRUNE: {
-            // stage the row in smem (fp32), then one output per thread with the
-            // basis column read through the read-only path, 8 loads in flight
-            if (D.kv_dtype == PIKV_DTYPE_BF16 && D.d % 8 == 0) {
-                const uint4* src = (const uint4*)((const uint16_t*)x + base);
-                for (int v = tid; v < D.d / 8; v += nt) {
-                    const uint4 w = src[v];
-                    const float e[8] = {bf16_lo(w.x), bf16_hi(w.x), bf16_lo(w.y), bf16_hi(w.y),
-                                        bf16_lo(w.z), bf16_hi(w.z), bf16_lo(w.w), bf16_hi(w.w)};
-#pragma unroll
-                    for (int u = 0; u < 8; ++u)
-                        tmp[v * 8 + u] = D.codec == PIKV_CODEC_LORAPLUS ? e[u] - S.cbias[v * 8 + u] : e[u];
-                }
-            } else {
-                for (int i = tid; i < D.d; i += nt) {
-                    float xi = load_in(x, D.kv_dtype, base + i);
-                    if (D.codec == PIKV_CODEC_LORAPLUS) xi -= S.cbias[i];
-                    tmp[i] = xi;
-                }
+        case PIKV_CODEC_LORAPLUS: {  // project_encode: computed for all streams by k_project
+            const float* pr = S.proj + ((int64_t)kv_row * D.B + s) * D.dp;
+            for (int o = tid; o < D.dp; o += nt) {
+                const float val = pr[o];
+                if (D.kv_dtype == PIKV_DTYPE_BF16) ((uint16_t*)dst)[o] = f32_to_bf16_rne(val);
+                else ((float*)dst)[o] = val;
             }
-            __syncthreads();
-            if (D.codec == PIKV_CODEC_FASTV || D.codec == PIKV_CODEC_PRUNE) {
-                for (int o = tid; o < D.dp; o += nt) {
-                    const int h = o / r, j = o % r;
-                    const float val = D.codec == PIKV_CODEC_FASTV ? tmp[h * hd + j] : tmp[h * hd + S.kept[h * r + j]];
-                    if (D.kv_dtype == PIKV_DTYPE_BF16) ((uint16_t*)dst)[o] = f32_to_bf16_rne(val);
-                    else ((float*)dst)[o] = val;
-                }
-            } else {  // project_encode, compressor.cpp:318-329
-                for (int o = tid; o < D.dp; o += nt) {
-                    const float val = proj_out(S, tmp, o / r, o % r, hd, r);
-                    if (D.kv_dtype == PIKV_DTYPE_BF16) ((uint16_t*)dst)[o] = f32_to_bf16_rne(val);
-                    else ((float*)dst)[o] = val;
-                }
-            }
-            __syncthreads();
             return;
         }
+        case PIKV_CODEC_FASTV:   // compressor.cpp:396-397
+        case PIKV_CODEC_PRUNE:   // compressor.cpp:398-402
+            for (int o = tid; o < D.dp; o += nt) {
+                const int h = o / r, j = o % r;
+                const int i = D.codec == PIKV_CODEC_FASTV ? j : S.kept[h * r + j];
+                if (D.kv_dtype == PIKV_DTYPE_BF16)
+                    ((uint16_t*)dst)[o] = ((const uint16_t*)x)[base + h * hd + i];
+                else
+                    ((float*)dst)[o] = ((const float*)x)[base + h * hd + i];
+            }
+            return;
         case PIKV_CODEC_INT8:
         case PIKV_CODEC_INT4: {
             // symmetric absmax per head (oracle: po_quantize_row)
@@ -544,8 +553,8 @@ __global__ void k_insert(Dims D, Cfg C, State S, const void* __restrict__ qin,
     const int pay = D.payload_bytes;
     float* ksc = (float*)(sm_entry + 2 * pay);
     float* vsc = ksc + D.H;
-    encode_row(D, S, kin, s, sm_entry, ksc, tmp);
-    encode_row(D, S, vin, s, sm_entry + pay, vsc, tmp);
+    encode_row(D, S, kin, s, sm_entry, ksc, tmp, 0);
+    encode_row(D, S, vin, s, sm_entry + pay, vsc, tmp, 1);
     // the query in the stored (compressed) space, fp32 (pipeline.cpp:295-297)
     {
         const int hd = D.d / D.H, r = D.dph;
@@ -563,23 +572,13 @@ __global__ void k_insert(Dims D, Cfg C, State S, const void* __restrict__ qin,
             }
         } else if (!proj) {
             for (int o = tid; o < D.d; o += blockDim.x) qa[o] = load_in(qin, D.kv_dtype, base + o);
-        } else {
-            __syncthreads();
-            for (int i = tid; i < D.d; i += blockDim.x) {
-                float xi = load_in(qin, D.kv_dtype, base + i);
-                if (D.codec == PIKV_CODEC_LORAPLUS) xi -= S.cbias[i];
-                tmp[i] = xi;
+        } else if (D.codec == PIKV_CODEC_FASTV || D.codec == PIKV_CODEC_PRUNE) {
+            for (int o = tid; o < D.dp; o += blockDim.x) {
+                const int h = o / r, j = o % r;
+                const int i = D.codec == PIKV_CODEC_FASTV ? j : S.kept[h * r + j];
+                qa[o] = load_in(qin, D.kv_dtype, base + h * hd + i);
             }
-            __syncthreads();
-            if (D.codec == PIKV_CODEC_FASTV || D.codec == PIKV_CODEC_PRUNE) {
-                for (int o = tid; o < D.dp; o += blockDim.x) {
-                    const int h = o / r, j = o % r;
-                    qa[o] = D.codec == PIKV_CODEC_FASTV ? tmp[h * hd + j] : tmp[h * hd + S.kept[h * r + j]];
-                }
-            } else {
-                for (int o = tid; o < D.dp; o += blockDim.x) qa[o] = proj_out(S, tmp, o / r, o % r, hd, r);
-            }
-        }
+        }  // LowRank / LoRAPlus: q_attn written by k_project
     }
     // Bookkeeping.  Entry ids are issued in selection order on every rank
     // (kvstore.cpp:114).  When the k entries hit k distinct rings (the common

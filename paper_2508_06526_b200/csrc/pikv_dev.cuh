@@ -113,7 +113,6 @@ struct State {
     int32_t* free_top;
     // codec params
     const float* basis;  // [H][r][hd]
-    const float* basis_t;  // [H][hd][r] (i-major copy for coalesced projection)
     const float* cbias;  // [d]
     const int32_t* kept; // [H][r]
     // step scratch
@@ -121,6 +120,7 @@ struct State {
     double* gates;     // [B][k]
     double* logits;    // [B][E]
     float* q_attn;     // [B][dp]
+    float* proj;       // [2][B][dp] LowRank/LoRAPlus encoded k, v of the step
     int32_t* cand;     // [B][max_cand] local ring ids
     int32_t* ncand;    // [B]
     EvictRec* rec_ow;  // [B][k]
@@ -316,6 +316,8 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 
 // ---- launch wrappers (defined in the .cu files) ----------------------------
 void launch_route(const Dims& D, const Cfg& C, const State& S, const void* q, cudaStream_t st);
+void launch_project(const Dims& D, const State& S, const void* q, const void* k, const void* v,
+                    cudaStream_t st);
 void launch_insert(const Dims& D, const Cfg& C, const State& S, const void* q, const void* k,
                    const void* v, const double* saliency, cudaStream_t st);
 void launch_sched_pages(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);
