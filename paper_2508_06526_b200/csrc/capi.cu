@@ -588,6 +588,7 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
     chk(S.gL = eng->alloc<float>((size_t)B * D.H));
     chk(S.summary = eng->alloc<pikv_step_summary>(B));
     chk(S.dbg = eng->alloc<long long>(64));
+    chk(S.done_ctr = eng->alloc<unsigned>(1));
     const size_t in_elem = c.kv_dtype == PIKV_DTYPE_BF16 ? 2 : 4;
     chk(eng->in_q = eng->alloc<uint8_t>((size_t)B * D.d * in_elem));
     chk(eng->in_k = eng->alloc<uint8_t>((size_t)B * D.d * in_elem));
@@ -636,6 +637,7 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
     CUDA_TRY(cudaMemsetAsync(S.n_items, 0, sizeof(int32_t), st));
     CUDA_TRY(cudaMemsetAsync(S.item_first, 0, sizeof(int32_t) * (B + 1), st));
     CUDA_TRY(cudaMemsetAsync(S.att_base, 0, sizeof(int64_t) * (B + 1), st));
+    CUDA_TRY(cudaMemsetAsync(S.done_ctr, 0, sizeof(unsigned), st));
     std::vector<int32_t> stack(D.pool_pages);
     for (int64_t i = 0; i < D.pool_pages; ++i) stack[i] = (int32_t)(D.pool_pages - 1 - i);
     CUDA_TRY(cudaMemcpyAsync(S.free_stack, stack.data(), sizeof(int32_t) * D.pool_pages,
@@ -756,12 +758,14 @@ static int enqueue_finish(pikv_engine* eng, const uint8_t* gathered, float* y, b
     if (eng->D.world > 1)
         launch_finish_merge(eng->D, eng->C, eng->S, eng->X, gathered, y, granks, eng->stream);
     mark(eng, 10);
-    if (attend) launch_foldback(eng->D, eng->S, eng->stream);
+    // fold-back + feedback in one launch (last CTA runs the feedback); the
+    // prefill (no attention) launches the feedback alone
+    if (attend) launch_foldback(eng->D, eng->C, eng->S, eng->stream);
     mark(eng, 11);
-    launch_feedback(eng->D, eng->C, eng->S, eng->stream);
+    if (!attend) launch_feedback(eng->D, eng->C, eng->S, eng->stream);
     mark(eng, 12);
     eng->cur = -1;
-    eng->kernels_per_step += (attend ? 2 : 1) + (eng->D.world > 1 ? 1 : 0);
+    eng->kernels_per_step += 1 + (eng->D.world > 1 ? 1 : 0);
     CUDA_TRY(cudaGetLastError());
     return PIKV_OK;
 }
@@ -851,7 +855,7 @@ int pikv_step_finish(pikv_engine* eng, const void* gathered, float* y_out) {
     cudaSetDevice(eng->device);
     int rc = enqueue_finish(eng, (const uint8_t*)gathered, y_out, true, eng->D.world);
     if (rc) return rc;
-    eng->launches += 3;  // finish_merge, foldback, feedback
+    eng->launches += 2;  // finish_merge, foldback(+feedback)
     return PIKV_OK;
 }
 

@@ -854,7 +854,8 @@ __device__ __forceinline__ bool page_less(double a, uint64_t oa, double b, uint6
 
 // (b) one CTA per (stream, local device): select_evictions + erase.
 constexpr int kSelThreads = 1024;
-__device__ __forceinline__ void select_body(const Dims& D, const Cfg& C, const State& S, const int sg) {
+__device__ __forceinline__ void select_body(const Dims& D, const Cfg& C, const State& S, const int sg,
+                                            const bool stage) {
     const int s = sg / D.Gl, gl = sg % D.Gl;
     const int tid = threadIdx.x;
     __shared__ int sm_red[32];
@@ -863,8 +864,28 @@ __device__ __forceinline__ void select_body(const Dims& D, const Cfg& C, const S
     __shared__ uint64_t sm_bo;
     __shared__ int sm_bi;
     if (S.err[s]) return;
-    const int64_t first = (int64_t)sg * D.SPD * D.ppr_sched;  // pages of this device
+    const int64_t first0 = (int64_t)sg * D.SPD * D.ppr_sched;  // pages of this device
     const int npg = D.SPD * D.ppr_sched;
+    // page keys of this device: staged in shared memory when they fit (every
+    // pass below then reads smem), else read in place from global memory
+    extern __shared__ __align__(16) uint8_t sm_keys[];
+    const double* KA = S.pg_agg + first0;
+    const uint64_t* KO = S.pg_oldest + first0;
+    int32_t* KC = S.pg_cnt + first0;
+    if (stage) {
+        double* a2 = (double*)sm_keys;
+        uint64_t* o2 = (uint64_t*)(a2 + npg);
+        int32_t* c2 = (int32_t*)(o2 + npg);
+#pragma unroll 4
+        for (int i = tid; i < npg; i += kSelThreads) {
+            a2[i] = KA[i];
+            o2[i] = KO[i];
+            c2[i] = KC[i];
+        }
+        __syncthreads();
+        KA = a2, KO = o2, KC = c2;
+    }
+    const int64_t first = 0;
     int32_t* list = S.sel_idx + (int64_t)sg * D.sel_stride;
     const double theta = S.theta[s];
     const bool use_theta = C.sched_strategy == PIKV_SCHED_ADAKV;
@@ -872,9 +893,9 @@ __device__ __forceinline__ void select_body(const Dims& D, const Cfg& C, const S
     int P = 0, T = 0;
 #pragma unroll 4
     for (int i = tid; i < npg; i += kSelThreads) {
-        if (S.pg_cnt[first + i] > 0) {
+        if (KC[first + i] > 0) {
             ++P;
-            if (use_theta && S.pg_agg[first + i] < theta) ++T;
+            if (use_theta && KA[first + i] < theta) ++T;
         }
     }
     for (int off = 16; off; off >>= 1) {
@@ -912,9 +933,9 @@ __device__ __forceinline__ void select_body(const Dims& D, const Cfg& C, const S
             int bi = -1;
 #pragma unroll 4
             for (int i = tid; i < npg; i += kSelThreads) {
-                if (S.pg_cnt[first + i] <= 0) continue;
-                const double a = S.pg_agg[first + i];
-                const uint64_t o = S.pg_oldest[first + i];
+                if (KC[first + i] <= 0) continue;
+                const double a = KA[first + i];
+                const uint64_t o = KO[first + i];
                 if (bi < 0 || page_less(a, o, ba, bo)) ba = a, bo = o, bi = i;
             }
             for (int off = 16; off; off >>= 1) {
@@ -936,7 +957,7 @@ __device__ __forceinline__ void select_body(const Dims& D, const Cfg& C, const S
                     if (wi[w] >= 0 && (b < 0 || page_less(wa[w], wo[w], a, o))) a = wa[w], o = wo[w], b = wi[w];
                 }
                 list[v] = b;
-                S.pg_cnt[first + b] = -S.pg_cnt[first + b];  // mark taken (negative count)
+                KC[first + b] = -KC[first + b];  // mark taken (negative count)
             }
             __syncthreads();
         }
@@ -946,13 +967,13 @@ __device__ __forceinline__ void select_body(const Dims& D, const Cfg& C, const S
         // then take the first V.
         const int n2 = D.sel_stride;
         for (int i = tid; i < n2; i += kSelThreads)
-            list[i] = (i < npg && S.pg_cnt[first + i] > 0) ? i : -1;
+            list[i] = (i < npg && KC[first + i] > 0) ? i : -1;
         __syncthreads();
         auto key_less = [&](int a, int b) {
             if (a < 0) return false;
             if (b < 0) return true;
-            return page_less(S.pg_agg[first + a], S.pg_oldest[first + a], S.pg_agg[first + b],
-                             S.pg_oldest[first + b]);
+            return page_less(KA[first + a], KO[first + a], KA[first + b],
+                             KO[first + b]);
         };
         for (int kk = 2; kk <= n2; kk <<= 1) {
             for (int j = kk >> 1; j > 0; j >>= 1) {
@@ -970,7 +991,7 @@ __device__ __forceinline__ void select_body(const Dims& D, const Cfg& C, const S
                 __syncthreads();
             }
         }
-        for (int v = tid; v < V; v += kSelThreads) S.pg_cnt[first + list[v]] = -S.pg_cnt[first + list[v]];
+        for (int v = tid; v < V; v += kSelThreads) KC[first + list[v]] = -KC[first + list[v]];
         __syncthreads();
     }
     // erase victims in order (scheduler.cpp:305-326): a warp per victim page,
@@ -988,7 +1009,7 @@ __device__ __forceinline__ void select_body(const Dims& D, const Cfg& C, const S
     const int lane = tid & 31, warp = tid >> 5;
     for (int v0 = 0; v0 < V; v0 += kSelThreads) {
         const int v = v0 + tid;
-        const int cnt = v < V ? -S.pg_cnt[first + list[v]] : 0;
+        const int cnt = v < V ? -KC[first + list[v]] : 0;
         int x = cnt;
         for (int off = 1; off < 32; off <<= 1) {
             int y = __shfl_up_sync(0xffffffffu, x, off);
@@ -1066,9 +1087,9 @@ __device__ __forceinline__ void select_body(const Dims& D, const Cfg& C, const S
     if (tid == 0) S.n_ev[sg] = sm_off;
 }
 
-__global__ void __launch_bounds__(kSelThreads) k_sched_select(Dims D, Cfg C, State S) {
+__global__ void __launch_bounds__(kSelThreads) k_sched_select(Dims D, Cfg C, State S, int stage) {
     griddep_enter();
-    select_body(D, C, S, blockIdx.x);
+    select_body(D, C, S, blockIdx.x, stage != 0);
 }
 
 // LRU / LRU+ with exact sums: one CTA per (stream, local device) computes the
@@ -1109,7 +1130,7 @@ __global__ void __launch_bounds__(kSelThreads) k_sched_fused(Dims D, Cfg C, Stat
         S.pg_oldest[first_t + i] = oldest;
     }
     __syncthreads();
-    select_body(D, C, S, sg);
+    select_body(D, C, S, sg, false);
 }
 
 void launch_sched_pages(const Dims& D, const Cfg& C, const State& S, cudaStream_t st) {
@@ -1122,7 +1143,11 @@ void launch_sched_fused(const Dims& D, const Cfg& C, const State& S, cudaStream_
     launch_pdl(k_sched_fused, dim3(D.B * D.Gl), dim3(kSelThreads), 0, st, D, C, S);
 }
 void launch_sched_select(const Dims& D, const Cfg& C, const State& S, cudaStream_t st) {
-    launch_pdl(k_sched_select, dim3(D.B * D.Gl), dim3(kSelThreads), 0, st, D, C, S);
+    const size_t keys = (size_t)D.SPD * D.ppr_sched * (8 + 8 + 4);
+    const int stage = keys <= 200 * 1024 ? 1 : 0;
+    const size_t smem = stage ? keys : 0;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_sched_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    launch_pdl(k_sched_select, dim3(D.B * D.Gl), dim3(kSelThreads), smem, st, D, C, S, stage);
 }
 
 // ===========================================================================
@@ -1483,10 +1508,40 @@ __global__ void k_finish_merge(Dims D, Cfg C, State S, ExchangeLayout X,
     }
 }
 
+// feedback for stream s (see k_feedback)
+__device__ __forceinline__ void feedback_stream(const Dims& D, const Cfg& C, const State& S, int s) {
+    if (S.err[s]) return;
+    const int k = D.k, E = D.E;
+    int hits = 0;
+    for (int j = 0; j < k; ++j) {
+        if (S.found[(int64_t)s * k + j] > 0) ++hits;
+        else S.miss[(int64_t)s * E + S.experts[(int64_t)s * k + j]] += 1;
+    }
+    const double reward = __ddiv_rn((double)hits, (double)k);
+    if (C.router_strategy == PIKV_ROUTER_ADAPTIVE) {  // adapt, router.cpp:243-255
+        double* bias = S.bias + (int64_t)s * E;
+        double acc = 0.0;
+        for (int e = 0; e < E; ++e) acc = __dadd_rn(acc, bias[e]);
+        const double mean = __ddiv_rn(acc, (double)E);
+        for (int j = 0; j < k; ++j) {
+            const int e = S.experts[(int64_t)s * k + j];
+            double b = __dadd_rn(bias[e], __dmul_rn(C.bandit_step, __dsub_rn(reward, mean)));
+            bias[e] = b < -C.bias_cap ? -C.bias_cap : (C.bias_cap < b ? C.bias_cap : b);
+        }
+    }
+    // observe_hits, scheduler.cpp:332-338
+    S.running_hit[s] = __dadd_rn(__dmul_rn(C.hit_decay, S.running_hit[s]),
+                                 __dmul_rn(__dsub_rn(1.0, C.hit_decay), reward));
+    if (C.sched_strategy == PIKV_SCHED_ADAKV && !C.unbounded_budget)  // :340-342
+        S.theta[s] = __dadd_rn(S.theta[s], __dmul_rn(C.adakv_step, __dsub_rn(C.target_hit, S.running_hit[s])));
+    if (!C.unbounded_budget) S.sstep[s] += 1;
+    S.now[s] += 1;
+}
+
 // attn_mass += alpha, pipeline.cpp:302-312; alpha = mean over heads.  One
 // thread per retrieved entry (its H logits are contiguous: 16-byte loads);
 // the global (M, 1/L) of every (stream, head) are staged in shared memory.
-__global__ void k_foldback(Dims D, State S) {
+__global__ void k_foldback(Dims D, Cfg C, State S) {
     griddep_enter();
     extern __shared__ float sm_ml[];  // [B*H] M, then [B*H] 1/L (0 when empty)
     __shared__ int64_t sm_base[1025];
@@ -1528,6 +1583,17 @@ __global__ void k_foldback(Dims D, State S) {
         S.attn_mass[gi] += al;
         if (D.n_layers > 0) S.per_layer[gi * D.n_layers + (int64_t)(S.now[s] % (uint64_t)D.n_layers)] += al;
     }
+    // the last CTA to finish runs the per-stream feedback (now++ must follow
+    // every fold-back that reads now)
+    __shared__ bool sm_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) sm_last = atomicAdd(S.done_ctr, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!sm_last) return;
+    __threadfence();
+    for (int s = threadIdx.x; s < D.B; s += blockDim.x) feedback_stream(D, C, S, s);
+    if (threadIdx.x == 0) *S.done_ctr = 0;
 }
 
 // pipeline.cpp:258 (record_miss), 337-347 (adapt, observe_hits,
@@ -1535,42 +1601,17 @@ __global__ void k_foldback(Dims D, State S) {
 __global__ void k_feedback(Dims D, Cfg C, State S) {
     griddep_enter();
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= D.B || S.err[s]) return;
-    const int k = D.k, E = D.E;
-    int hits = 0;
-    for (int j = 0; j < k; ++j) {
-        if (S.found[(int64_t)s * k + j] > 0) ++hits;
-        else S.miss[(int64_t)s * E + S.experts[(int64_t)s * k + j]] += 1;
-    }
-    const double reward = __ddiv_rn((double)hits, (double)k);
-    if (C.router_strategy == PIKV_ROUTER_ADAPTIVE) {  // adapt, router.cpp:243-255
-        double* bias = S.bias + (int64_t)s * E;
-        double acc = 0.0;
-        for (int e = 0; e < E; ++e) acc = __dadd_rn(acc, bias[e]);
-        const double mean = __ddiv_rn(acc, (double)E);
-        for (int j = 0; j < k; ++j) {
-            const int e = S.experts[(int64_t)s * k + j];
-            double b = __dadd_rn(bias[e], __dmul_rn(C.bandit_step, __dsub_rn(reward, mean)));
-            bias[e] = b < -C.bias_cap ? -C.bias_cap : (C.bias_cap < b ? C.bias_cap : b);
-        }
-    }
-    // observe_hits, scheduler.cpp:332-338
-    S.running_hit[s] = __dadd_rn(__dmul_rn(C.hit_decay, S.running_hit[s]),
-                                 __dmul_rn(__dsub_rn(1.0, C.hit_decay), reward));
-    if (C.sched_strategy == PIKV_SCHED_ADAKV && !C.unbounded_budget)  // :340-342
-        S.theta[s] = __dadd_rn(S.theta[s], __dmul_rn(C.adakv_step, __dsub_rn(C.target_hit, S.running_hit[s])));
-    if (!C.unbounded_budget) S.sstep[s] += 1;
-    S.now[s] += 1;
+    if (s < D.B) feedback_stream(D, C, S, s);
 }
 
 void launch_finish_merge(const Dims& D, const Cfg& C, const State& S, const ExchangeLayout& X,
                          const uint8_t* gathered, float* y, int granks, cudaStream_t st) {
     launch_pdl(k_finish_merge, dim3(D.B), dim3(256), 0, st, D, C, S, X, gathered, y, granks);
 }
-void launch_foldback(const Dims& D, const State& S, cudaStream_t st) {
+void launch_foldback(const Dims& D, const Cfg& C, const State& S, cudaStream_t st) {
     const size_t smem = sizeof(float) * 2 * (size_t)D.B * D.H;
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_foldback, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    launch_pdl(k_foldback, dim3(D.attend_ctas * 2), dim3(256), smem, st, D, S);
+    launch_pdl(k_foldback, dim3(D.attend_ctas * 2), dim3(256), smem, st, D, C, S);
 }
 void launch_feedback(const Dims& D, const Cfg& C, const State& S, cudaStream_t st) {
     launch_pdl(k_feedback, dim3((D.B + 127) / 128), dim3(128), 0, st, D, C, S);

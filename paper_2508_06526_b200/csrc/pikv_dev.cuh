@@ -161,6 +161,7 @@ struct State {
     float* gL;              // [B][H]
     pikv_step_summary* summary;  // [B]
     long long* dbg;              // [64] debug timestamps (k_route, stream 0)
+    unsigned* done_ctr;          // last-block counter (k_foldback)
 };
 
 // ---- helpers -------------------------------------------------------------
@@ -331,7 +332,7 @@ void launch_combine(const Dims& D, const Cfg& C, const State& S, const ExchangeL
                     int direct, cudaStream_t st);
 void launch_finish_merge(const Dims& D, const Cfg& C, const State& S, const ExchangeLayout& X,
                          const uint8_t* gathered, float* y, int granks, cudaStream_t st);
-void launch_foldback(const Dims& D, const State& S, cudaStream_t st);
+void launch_foldback(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);  // + feedback
 void launch_feedback(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);
 void launch_synth(const Dims& D, void* q, void* k, void* v, uint64_t seed, uint64_t step,
                   cudaStream_t st);
