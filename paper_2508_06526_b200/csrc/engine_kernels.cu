@@ -864,6 +864,127 @@ __device__ __forceinline__ void select_body(const Dims& D, const Cfg& C, const S
     __shared__ uint64_t sm_bo;
     __shared__ int sm_bi;
     if (S.err[s]) return;
+    // ---- fast path (the common steady state evicts 0 or 1 page): one pass
+    // over the page keys computes P, the below-theta count T and the argmin;
+    // one two-level reduction; a single victim is erased directly.
+    {
+        const int64_t f0 = (int64_t)sg * D.SPD * D.ppr_sched;
+        const int np = D.SPD * D.ppr_sched;
+        const double th = S.theta[s];
+        const bool ut = C.sched_strategy == PIKV_SCHED_ADAKV;
+        int P = 0, T = 0, bi = -1;
+        double ba = 0.0;
+        uint64_t bo = 0;
+#pragma unroll 4
+        for (int i = tid; i < np; i += kSelThreads) {
+            const int c = S.pg_cnt[f0 + i];
+            if (c <= 0) continue;
+            const double a2 = S.pg_agg[f0 + i];
+            const uint64_t o2 = S.pg_oldest[f0 + i];
+            ++P;
+            if (ut && a2 < th) ++T;
+            if (bi < 0 || page_less(a2, o2, ba, bo)) ba = a2, bo = o2, bi = i;
+        }
+        __shared__ int fP[32], fT[32], fI[32];
+        __shared__ double fA[32];
+        __shared__ uint64_t fO[32];
+        __shared__ int fV, fBest, fThr, fPall;
+        const int lane = tid & 31, warp = tid >> 5;
+        for (int off = 16; off; off >>= 1) {
+            P += __shfl_xor_sync(0xffffffffu, P, off);
+            T += __shfl_xor_sync(0xffffffffu, T, off);
+            const double a3 = __shfl_xor_sync(0xffffffffu, ba, off);
+            const uint64_t o3 = __shfl_xor_sync(0xffffffffu, bo, off);
+            const int i3 = __shfl_xor_sync(0xffffffffu, bi, off);
+            if (i3 >= 0 && (bi < 0 || page_less(a3, o3, ba, bo))) ba = a3, bo = o3, bi = i3;
+        }
+        if (lane == 0) fP[warp] = P, fT[warp] = T, fA[warp] = ba, fO[warp] = bo, fI[warp] = bi;
+        __syncthreads();
+        if (warp == 0) {
+            const int nw = kSelThreads / 32;
+            P = lane < nw ? fP[lane] : 0;
+            T = lane < nw ? fT[lane] : 0;
+            ba = lane < nw ? fA[lane] : 0.0;
+            bo = lane < nw ? fO[lane] : 0;
+            bi = lane < nw ? fI[lane] : -1;
+            for (int off = 16; off; off >>= 1) {
+                P += __shfl_xor_sync(0xffffffffu, P, off);
+                T += __shfl_xor_sync(0xffffffffu, T, off);
+                const double a3 = __shfl_xor_sync(0xffffffffu, ba, off);
+                const uint64_t o3 = __shfl_xor_sync(0xffffffffu, bo, off);
+                const int i3 = __shfl_xor_sync(0xffffffffu, bi, off);
+                if (i3 >= 0 && (bi < 0 || page_less(a3, o3, ba, bo))) ba = a3, bo = o3, bi = i3;
+            }
+            if (lane == 0) {
+                const int V0 = max(T, max(P - C.budget_pages, 0));  // scheduler.cpp:246-259
+                fV = V0, fBest = bi, fThr = T, fPall = P;
+                S.pages_before[sg] = P;
+                S.pages_after[sg] = P - V0;
+                S.n_ev[sg] = 0;
+            }
+        }
+        __syncthreads();
+        const int V0 = fV;
+        if (V0 == 0) return;
+        if (V0 == 1) {
+            if (warp == 0) {
+                const int pidx = fBest;
+                const int reason = fThr >= 1 ? PIKV_EVICT_THRESHOLD : PIKV_EVICT_BUDGET;
+                const int64_t ring = (int64_t)sg * D.SPD + pidx / D.ppr_sched;
+                const uint64_t seq = S.seq[ring];
+                const uint64_t Su = (uint64_t)D.S, ps = (uint64_t)D.page_size;
+                const uint64_t lo = seq > Su ? seq - Su : 0;
+                const uint64_t q = lo / ps + (uint64_t)(pidx % D.ppr_sched);
+                const uint64_t sstep = S.sstep[s], now = S.now[s];
+                const int dev = gl * D.world + D.rank;
+                EvictRec* rec = S.rec_ev + (int64_t)sg * D.SPD * D.S;
+                int o = 0;
+                for (uint64_t b0 = 0; b0 < ps; b0 += 32) {
+                    const uint64_t sq = q * ps + b0 + lane;
+                    bool mem = false;
+                    int64_t gi = 0;
+                    if (b0 + lane < ps) {
+                        gi = ring * D.S + (int64_t)(sq % Su);
+                        mem = S.id[gi] != 0 && S.shard_seq[gi] == sq;
+                    }
+                    const unsigned bal = __ballot_sync(0xffffffffu, mem);
+                    if (mem) {
+                        EvictRec& r = rec[o + __popc(bal & ((1u << lane) - 1u))];
+                        r.step = sstep;
+                        r.entry_id = S.id[gi];
+                        r.token_id = S.token[gi];
+                        r.expert_id = S.expert[gi];
+                        r.device = dev;
+                        r.score = score_entry(C, S, gi, now, D.n_layers);
+                        r.reason = reason;
+                        r.stream = s;
+                        S.id[gi] = 0;  // KVStore::erase, kvstore.cpp:180-185
+                        atomicSub(&S.live[ring], 1);
+                        const int slot = (int)(sq % Su);
+                        const int64_t pt_i = ring * D.ppr + slot / D.spg;
+                        const int32_t page = S.page_table[pt_i];
+                        if (atomicSub(&S.page_live[page], 1) == 1) {
+                            S.page_table[pt_i] = -1;
+                            const int top = atomicAdd(S.free_top, 1);
+                            S.free_stack[top] = page;
+                        }
+                    }
+                    o += __popc(bal);
+                }
+                if (lane == 0) {
+                    const int64_t r = ring * D.ppr_sched + (int64_t)(q % (uint64_t)D.ppr_sched);
+                    S.pr_cnt[r] = 0;
+                    S.pr_first[r] = 0;
+                    S.pr_sla[r] = 0;
+                    S.pr_sf[r] = 0;
+                    S.n_ev[sg] = o;
+                }
+            }
+            return;
+        }
+        (void)fPall;
+        __syncthreads();  // V > 1: general path below recomputes from the keys
+    }
     const int64_t first0 = (int64_t)sg * D.SPD * D.ppr_sched;  // pages of this device
     const int npg = D.SPD * D.ppr_sched;
     // page keys of this device: staged in shared memory when they fit (every
