@@ -225,3 +225,49 @@ def test_prefill_then_step_graph_replay():
     for s in range(4):
         assert summ[s]["error"] == 0 and summ[s]["n_attended"] > 0
     assert torch.isfinite(y).all()
+
+
+def test_engine_c2_shape_parity():
+    """BASELINE configs[1] shapes (d = 32 x 128, bf16, E16 top-2, pure expert
+    sharding n_tok=1/n_exp=16, LRU page budget) over 120 steps, 2 streams."""
+    cfg = engine_config(router="TopK", sched="LRU", d=4096, H=32, E=16, k=2, G=1, n_tok=1,
+                        n_exp=16, S=64, ps=16, budget=6, batch=2, dtype="bf16", n_layers=0)
+    cfg.model.head_width = 128
+    run_parity(cfg, 120, 17, inject=False)
+
+
+def test_engine_full_context_invariants():
+    """c2 at full context (32K-token synthetic prefill, B = 4): no device
+    error, live entries follow the page budget, every stream attends exactly
+    the live entries of its selected experts with token < now (recomputed from
+    the slot dump), the fold-back adds 1 per step, outputs finite."""
+    L, B = 32768, 4
+    cfg = engine_config(router="TopK", sched="LRU", d=4096, H=32, E=16, k=2, G=1, n_tok=1,
+                        n_exp=16, S=8192, ps=16, budget=(2 * L) // 16, batch=B, dtype="bf16",
+                        n_layers=0)
+    cfg.model.head_width = 128
+    cfg.pool_entries = B * (2 * L + 4096)
+    eng = Engine(cfg)
+    eng.prefill_synthetic(L, seed=11)
+    q, k, v, _ = make_stream(3, 4096, 99, "bf16", 0)
+    for t in range(3):
+        before = [eng.slots(s) for s in range(B)]
+        qq = np.repeat(q[t:t + 1], B, 0)
+        y = eng.step_host(to_kv(qq, "bf16"), to_kv(np.repeat(k[t:t + 1], B, 0), "bf16"),
+                          to_kv(np.repeat(v[t:t + 1], B, 0), "bf16"))
+        experts, _, _, summ = eng.read_step()
+        assert np.all(np.isfinite(y))
+        for s in range(B):
+            assert summ[s]["error"] == 0
+            sl = eng.slots(s)
+            now = summ[s]["step"]
+            live = sl["id"] != 0
+            want = live & np.isin(sl["expert"], experts[s]) & (sl["token"] < now)
+            assert summ[s]["n_attended"] == int(want.sum())
+            assert summ[s]["pages_after"] <= cfg.scheduler.budget_pages
+            same = (sl["id"] == before[s]["id"]) & live
+            gain = sl["attn_mass"][same] - before[s]["attn_mass"][same]
+            assert abs(gain.sum() - 1.0) < 1e-3
+            st = eng.store_stats(s)
+            assert st["live"] == int(live.sum())
+    assert eng.pool_pages_in_use() <= (B * (2 * L + 4096) + 15) // 16
