@@ -440,7 +440,11 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device);
     D.attend_ctas = 2 * sms;  // k_attend runs two CTAs per SM
-    D.item_cap = 4LL * D.attend_ctas + D.B + 16;
+    {
+        const char* v = std::getenv("PIKV_ITEMS");
+        D.items_per_cta = v ? std::max(1, std::atoi(v)) : 2;
+    }
+    D.item_cap = (int64_t)D.items_per_cta * D.attend_ctas + D.B + 16;
     const int64_t total_slots = (int64_t)D.B * D.R * D.S;
     if (total_slots >= (1LL << 31)) {
         delete eng;

@@ -1372,7 +1372,8 @@ __global__ void __launch_bounds__(1024) k_retr_scan(Dims D, State S) {
     const int64_t n = tid < D.B ? sm_n[tid] : 0;
     int64_t N;
     const int64_t base = block_excl_scan(n, wsum, &N);
-    int64_t C = (N + 4LL * D.attend_ctas - 1) / (4LL * D.attend_ctas);
+    const int64_t ipc = D.items_per_cta;  // work items per attention CTA
+    int64_t C = (N + ipc * D.attend_ctas - 1) / (ipc * D.attend_ctas);
     if (C < 16) C = 16;
     const int64_t items = (n + C - 1) / C;
     int64_t W;
