@@ -442,7 +442,7 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
     D.attend_ctas = 2 * sms;  // k_attend runs two CTAs per SM
     {
         const char* v = std::getenv("PIKV_ITEMS");
-        D.items_per_cta = v ? std::max(1, std::atoi(v)) : 2;
+        D.items_per_cta = v ? std::max(1, std::atoi(v)) : 4;
     }
     D.item_cap = (int64_t)D.items_per_cta * D.attend_ctas + D.B + 16;
     const int64_t total_slots = (int64_t)D.B * D.R * D.S;

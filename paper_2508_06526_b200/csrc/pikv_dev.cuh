@@ -58,7 +58,7 @@ struct Dims {
     int sel_stride;                  // pow2 >= SPD * ppr_sched
     int64_t pool_entries, pool_pages, att_cap, item_cap;
     int attend_ctas;
-    int items_per_cta;  // split-K work items per attention CTA (PIKV_ITEMS, default 2)
+    int items_per_cta;  // split-K work items per attention CTA (PIKV_ITEMS, default 4)
 };
 
 struct Cfg {  // scalar config needed on device (copied by value into kernels)
