@@ -259,8 +259,14 @@ struct DevBuf {
 int pikv_shard_assign_host(const int64_t* t, const int32_t* e, int32_t n, int32_t n_tok,
                            int32_t n_exp, int32_t devices, int32_t additive, int32_t* device_out,
                            int32_t* shard_out, int32_t* raw_out) {
-    if (n <= 0) return pikv_shard_assign(nullptr, nullptr, 0, n_tok, n_exp, devices, additive,
-                                         nullptr, nullptr, nullptr);
+    // same checks as shard_assign (kvstore.cpp:17-22), before touching the device
+    if (!is_pow2(n_tok) || !is_pow2(n_exp))
+        return fail(PIKV_ERR_INVALID_CONFIG, "shard_assign: moduli must be powers of two");
+    if (devices < 1) return fail(PIKV_ERR_INVALID_CONFIG, "shard_assign: devices must be >= 1");
+    for (int i = 0; i < n; ++i)
+        if (t[i] < 0 || e[i] < 0)
+            return fail(PIKV_ERR_INVALID_ARGUMENT, "shard_assign: negative token or expert index");
+    if (n <= 0) return PIKV_OK;
     DevBuf dt(8 * (size_t)n), de(4 * (size_t)n), dd(4 * (size_t)n), ds(4 * (size_t)n), dr(4 * (size_t)n);
     CUDA_TRY(cudaMemcpy(dt.p, t, 8 * (size_t)n, cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(de.p, e, 4 * (size_t)n, cudaMemcpyHostToDevice));
