@@ -393,9 +393,13 @@ Plan make_plan(const Dims& D) {
     return pl;
 }
 
+template <class Dec> struct BatchOf { static constexpr int NB = 2; };
+template <> struct BatchOf<DecI8> { static constexpr int NB = 4; };  // half/quarter-size entries:
+template <> struct BatchOf<DecI4> { static constexpr int NB = 4; };  // amortize per-entry work
+
 template <class Dec, int CPT>
 void launch_t(const Dims& D, const State& S, const Plan& pl, cudaStream_t st) {
-    auto kern = k_attend<Dec, CPT, 2>;
+    auto kern = k_attend<Dec, CPT, BatchOf<Dec>::NB>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
     launch_pdl(kern, dim3(D.attend_ctas), dim3(kThreads), pl.smem, st, D, S, pl.P);
 }
