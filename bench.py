@@ -2,7 +2,7 @@
 """Benchmark of the B200 PiKV decode step (BASELINE.json metric).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config c2|c1|c3|c4-int8|c4-int4|c4-lowrank]
+                  [--config c2|c1|c3|c4-int8|c4-int4|c4-lowrank|c5]
 
 One step = Engine::step (pipeline.cpp:213-351) for every stream of the batch:
 route -> insert -> evict -> retrieve -> decode attention -> LSE merge ->
@@ -12,7 +12,8 @@ prefilled synthetically to L tokens (untimed).  value = decode tokens/s of the
 whole job (B * K / device time, inputs resident in HBM); e2e = the same
 through pikv_step_host with pinned host buffers (H2D of q/k/v, D2H of y inside
 the timed region).  Under torchrun (N>1) the experts are sharded over the
-ranks (G = N logical devices, device g on rank g) and the per-step partial
+ranks (G = N logical devices, device g on rank g), the batch grows to 16 N
+streams (per-GPU KV work constant: weak scaling) and the per-step partial
 softmax states are merged with an NCCL all-gather.
 """
 from __future__ import annotations
@@ -43,6 +44,8 @@ WORKLOADS = {
                 dict(E=16, k=2, L=65536, H=32, hd=128, B=32, dtype="bf16", codec="Int8")),
     "c4-int4": ("compression: int4 KV, L=65536, 32x128, batch 32",
                 dict(E=16, k=2, L=65536, H=32, hd=128, B=32, dtype="bf16", codec="Int4")),
+    "c5": ("sweep point: E64 top-4, L=32768, 8 heads x 128, bf16, batch 64",
+           dict(E=64, k=4, L=32768, H=8, hd=128, B=64, dtype="bf16", codec="Identity")),
     "c4-lowrank": ("compression: rank-32 per head, L=65536, 32x128, batch 32",
                    dict(E=16, k=2, L=65536, H=32, hd=128, B=32, dtype="bf16", codec="LowRank",
                         rank=32)),
@@ -274,6 +277,11 @@ def main():
     from paper_2508_06526_b200.engine import Engine
     from paper_2508_06526_b200.parallel import ShardedStepper
 
+    if world > 1:
+        # expert-parallel + batch: B grows with N (16 streams per GPU); every
+        # GPU holds 1/N of each stream's KV (logical device g on rank g), so
+        # the per-GPU KV read per step stays that of one GPU ("weak" scaling)
+        w["B"] = w["B"] * world
     cfg = make_config(w, world=world, rank=rank)
     eng = Engine(cfg, device=local)
     B, d, dp = cfg.batch, cfg.model.d, cfg.stored_width
@@ -388,13 +396,15 @@ def main():
         "metric": "decode tokens/sec", "value": tokens / (ms * 1e-3), "unit": "tokens/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "bf16"
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16"
         if cfg.kv_dtype == "bf16" else "f32",
         "data": "synthetic (device-generated N(0,1) q/k/v; store prefilled to L)",
         "config": {"workload": name, "description": WORKLOADS[name][0], "batch": B,
                    "context": w["L"], "experts": w["E"], "top_k": w["k"], "heads": w["H"],
                    "head_dim": w["hd"], "codec": w["codec"], "scheduler": "LRU page budget",
                    "placement": "expert-sharded over %d GPU(s)" % world,
+                   "global_batch": B,
+                   "parallelism": "ep%d (experts over GPUs, LSE merge all-gather)" % world,
                    "l2": "inputs larger than L2 (2 GiB KV read per step)",
                    "prefill_s": round(prefill_s, 2)},
         "kv_gbs": kv_bytes_step / (ms / args.steps * 1e-3) / 1e9,
