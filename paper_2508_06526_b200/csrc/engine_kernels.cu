@@ -38,16 +38,16 @@ __device__ __forceinline__ void route_select(const Dims& D, const Cfg& C, const 
                                              double* load, uint64_t* usage, const uint64_t* miss,
                                              const double* bias, int* sel);
 
-constexpr int kRouteCH = 256;    // columns per stage
+constexpr int kRouteCHMax = 256;  // columns per stage (reduced so E rows x stages fit)
 constexpr int kRouteStages = 5;
 
-__global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin) {
+__global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin, int kRouteCH) {
     griddep_enter();
     extern __shared__ __align__(128) uint8_t sm_raw[];
     uint64_t* full = (uint64_t*)sm_raw;
     uint64_t* empty = full + kRouteStages;
     double* sm_q = (double*)(sm_raw + 128);
-    const int rowb = kRouteCH * 8 + 16;  // padded row: 2-way bank conflicts at worst
+    const int rowb = kRouteCH * 8 + 16;  // padded row: 2-way bank conflicts at worst (CH % 32 == 0)
     uint8_t* ring = (uint8_t*)(sm_q + D.d);
     __shared__ double sm_logit[kMaxE];
     __shared__ bool sm_flag[kMaxE];
@@ -375,11 +375,15 @@ __device__ __forceinline__ void route_select(const Dims& D, const Cfg& C, const 
 }
 
 void launch_route(const Dims& D, const Cfg& C, const State& S, const void* q, cudaStream_t st) {
-    const size_t smem = 128 + sizeof(double) * (size_t)D.d +
-                        (size_t)kRouteStages * D.E * (kRouteCH * 8 + 16);
+    int ch = kRouteCHMax;
+    auto bytes = [&](int c) {
+        return 128 + sizeof(double) * (size_t)D.d + (size_t)kRouteStages * D.E * ((size_t)c * 8 + 16);
+    };
+    while (ch > 32 && bytes(ch) > 200 * 1024) ch -= 32;
+    const size_t smem = bytes(ch);
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_route, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int threads = ((D.E + 31) / 32) * 32 + 32;
-    launch_pdl(k_route, dim3(D.B), dim3(threads), smem, st, D, C, S, q);
+    launch_pdl(k_route, dim3(D.B), dim3(threads), smem, st, D, C, S, q, ch);
 }
 
 // page-record maintenance (see State::pr_*)

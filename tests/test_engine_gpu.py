@@ -271,3 +271,12 @@ def test_engine_full_context_invariants():
             st = eng.store_stats(s)
             assert st["live"] == int(live.sum())
     assert eng.pool_pages_in_use() <= (B * (2 * L + 4096) + 15) // 16
+
+
+def test_engine_c5_shape_parity():
+    """c5 shapes: 64 experts top-4, 8 heads x 128 (router W ring with reduced
+    chunk width, 4 entries in parallel per attention CTA)."""
+    cfg = engine_config(router="TopK", sched="LRU", d=1024, H=8, E=64, k=4, G=1, n_tok=1,
+                        n_exp=64, S=32, ps=8, budget=40, batch=3, dtype="bf16", n_layers=0)
+    cfg.model.head_width = 128
+    run_parity(cfg, 80, 23, inject=False)
