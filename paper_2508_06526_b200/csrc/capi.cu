@@ -575,6 +575,7 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
     chk(S.pr_first = eng->alloc<int32_t>(rings * D.ppr_sched));
     chk(S.pr_sla = eng->alloc<uint64_t>(rings * D.ppr_sched));
     chk(S.pr_sf = eng->alloc<uint64_t>(rings * D.ppr_sched));
+    chk(S.pages_live = eng->alloc<int32_t>((size_t)B * std::max(D.Gl, 1)));
     chk(S.pg_agg = eng->alloc<double>(rings * D.ppr_sched));
     chk(S.pg_oldest = eng->alloc<uint64_t>(rings * D.ppr_sched));
     chk(S.pg_cnt = eng->alloc<int32_t>(rings * D.ppr_sched));
@@ -638,6 +639,7 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
     CUDA_TRY(cudaMemsetAsync(S.id, 0, sizeof(uint64_t) * total_slots, st));
     CUDA_TRY(cudaMemsetAsync(S.attn_mass, 0, sizeof(double) * total_slots, st));
     CUDA_TRY(cudaMemsetAsync(S.pr_cnt, 0, sizeof(int32_t) * rings * D.ppr_sched, st));
+    CUDA_TRY(cudaMemsetAsync(S.pages_live, 0, sizeof(int32_t) * B * std::max(D.Gl, 1), st));
     CUDA_TRY(cudaMemsetAsync(S.pr_first, 0, sizeof(int32_t) * rings * D.ppr_sched, st));
     CUDA_TRY(cudaMemsetAsync(S.pr_sla, 0, sizeof(uint64_t) * rings * D.ppr_sched, st));
     CUDA_TRY(cudaMemsetAsync(S.pr_sf, 0, sizeof(uint64_t) * rings * D.ppr_sched, st));
@@ -745,9 +747,14 @@ static int enqueue_local(pikv_engine* eng, const void* q, const void* k, const v
     const bool sched = D.Gl > 0 && !eng->C.unbounded_budget;
     // (k_sched_fused -- keys + select in one CTA per device -- measured slower
     // than the wide page-key kernel + select: 34.7 vs 28.5 us on c2)
-    if (sched) launch_sched_pages(D, eng->C, S, st), ++n;
-    mark(eng, 3);
-    if (sched) launch_sched_select(D, eng->C, S, st), ++n;
+    if (sched && eng->C.record_agg) {
+        launch_sched_lru(D, eng->C, S, st), ++n;  // live-page counter; keys only where P > K
+        mark(eng, 3);
+    } else {
+        if (sched) launch_sched_pages(D, eng->C, S, st), ++n;
+        mark(eng, 3);
+        if (sched) launch_sched_select(D, eng->C, S, st), ++n;
+    }
     mark(eng, 4);
     launch_retr_count(D, S, st), ++n;
     mark(eng, 5);

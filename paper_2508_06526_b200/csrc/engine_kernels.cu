@@ -394,6 +394,7 @@ __device__ __forceinline__ void rec_append(const Dims& D, const State& S, int64_
                                            uint64_t now) {
     const int64_t r = page_rec(D, ring, sq);
     if (S.pr_cnt[r] == 0) {
+        atomicAdd(&S.pages_live[ring / D.SPD], 1);  // a page comes to life
         S.pr_cnt[r] = 1;
         S.pr_first[r] = (int)(sq % (uint64_t)D.page_size);
         S.pr_sla[r] = now;
@@ -406,7 +407,7 @@ __device__ __forceinline__ void rec_append(const Dims& D, const State& S, int64_
 __device__ __forceinline__ void rec_drop_front(const Dims& D, const State& S, int64_t ring, uint64_t sq,
                                                uint64_t la, uint64_t fr) {
     const int64_t r = page_rec(D, ring, sq);
-    S.pr_cnt[r] -= 1;
+    if (--S.pr_cnt[r] == 0) atomicSub(&S.pages_live[ring / D.SPD], 1);  // last member displaced
     S.pr_first[r] += 1;
     S.pr_sla[r] -= la;
     S.pr_sf[r] -= fr;
@@ -977,6 +978,7 @@ __device__ __forceinline__ void select_body(const Dims& D, const Cfg& C, const S
                 }
                 if (lane == 0) {
                     const int64_t r = ring * D.ppr_sched + (int64_t)(q % (uint64_t)D.ppr_sched);
+                    if (S.pr_cnt[r] > 0) atomicSub(&S.pages_live[sg], 1);
                     S.pr_cnt[r] = 0;
                     S.pr_first[r] = 0;
                     S.pr_sla[r] = 0;
@@ -1199,6 +1201,7 @@ __device__ __forceinline__ void select_body(const Dims& D, const Cfg& C, const S
             }
             if (lane == 0) {  // the page is gone: reset its record
                 const int64_t r = ring * D.ppr_sched + (int64_t)(q % (uint64_t)D.ppr_sched);
+                if (S.pr_cnt[r] > 0) atomicSub(&S.pages_live[sg], 1);
                 S.pr_cnt[r] = 0;
                 S.pr_first[r] = 0;
                 S.pr_sla[r] = 0;
@@ -1264,6 +1267,61 @@ void launch_sched_pages(const Dims& D, const Cfg& C, const State& S, cudaStream_
     const int64_t threads = (int64_t)D.B * D.R * D.ppr_sched * lanes;
     launch_pdl(k_sched_pages, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0, st, D, C, S, lanes);
 }
+// LRU / LRU+ (record aggregates): the live-page counter decides whether this
+// device evicts at all (P <= K: nothing to do, one load); only evicting
+// devices compute their page keys from the records and select (fast path for
+// one victim).  Bit-identical to the full scan: the keys are the same.
+__global__ void __launch_bounds__(kSelThreads) k_sched_lru(Dims D, Cfg C, State S) {
+    griddep_enter();
+    const int sg = blockIdx.x;
+    const int s = sg / D.Gl;
+    const int tid = threadIdx.x;
+    if (S.err[s]) return;
+    const int P = S.pages_live[sg];
+    if (P <= C.budget_pages) {
+        if (tid == 0) {
+            S.pages_before[sg] = P;
+            S.pages_after[sg] = P;
+            S.n_ev[sg] = 0;
+        }
+        return;
+    }
+    __shared__ uint64_t sm_seq[64];
+    for (int sh = tid; sh < D.SPD && sh < 64; sh += kSelThreads) sm_seq[sh] = S.seq[(int64_t)sg * D.SPD + sh];
+    __syncthreads();
+    const uint64_t now = S.now[s];
+    const uint64_t Su = (uint64_t)D.S, ps = (uint64_t)D.page_size;
+    const int64_t first_t = (int64_t)sg * D.SPD * D.ppr_sched;
+    const int npg = D.SPD * D.ppr_sched;
+    for (int i = tid; i < npg; i += kSelThreads) {
+        const int sh = i / D.ppr_sched, pi = i % D.ppr_sched;
+        const int64_t ring = (int64_t)sg * D.SPD + sh;
+        const uint64_t seq = sh < 64 ? sm_seq[sh] : S.seq[ring];
+        const uint64_t lo = seq > Su ? seq - Su : 0;
+        const uint64_t q = lo / ps + (uint64_t)pi;
+        const int64_t rec = ring * D.ppr_sched + (int64_t)(q % (uint64_t)D.ppr_sched);
+        const int cnt = q * ps < seq ? S.pr_cnt[rec] : 0;
+        double agg = 0.0;
+        uint64_t oldest = 0;
+        if (cnt > 0) {
+            agg = -(double)((uint64_t)cnt * now - S.pr_sla[rec]);
+            if (C.sched_strategy == PIKV_SCHED_LRU_PLUS)
+                agg = __dadd_rn(agg, __dmul_rn(C.lambda_freq, (double)S.pr_sf[rec]));
+            oldest = S.id[ring * D.S + (int64_t)((q * ps + (uint64_t)S.pr_first[rec]) % Su)];
+        }
+        S.pg_cnt[first_t + i] = cnt;
+        S.pg_agg[first_t + i] = agg;
+        S.pg_oldest[first_t + i] = oldest;
+    }
+    __threadfence_block();
+    __syncthreads();
+    select_body(D, C, S, sg, false);
+}
+
+void launch_sched_lru(const Dims& D, const Cfg& C, const State& S, cudaStream_t st) {
+    launch_pdl(k_sched_lru, dim3(D.B * D.Gl), dim3(kSelThreads), 0, st, D, C, S);
+}
+
 void launch_sched_fused(const Dims& D, const Cfg& C, const State& S, cudaStream_t st) {
     launch_pdl(k_sched_fused, dim3(D.B * D.Gl), dim3(kSelThreads), 0, st, D, C, S);
 }

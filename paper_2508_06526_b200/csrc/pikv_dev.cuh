@@ -138,6 +138,7 @@ struct State {
     int32_t* pr_first;
     uint64_t* pr_sla;       // sum of last_access over live members
     uint64_t* pr_sf;        // sum of freq over live members
+    int32_t* pages_live;    // [B*Gl] scheduler pages with >= 1 live member (EvictionReport.pages_before)
     double* pg_agg;         // [B*R][ppr_sched]
     uint64_t* pg_oldest;
     int32_t* pg_cnt;
@@ -325,6 +326,7 @@ void launch_insert(const Dims& D, const Cfg& C, const State& S, const void* q, c
 void launch_sched_pages(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);
 void launch_sched_select(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);
 void launch_sched_fused(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);
+void launch_sched_lru(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);
 void launch_retr_count(const Dims& D, const State& S, cudaStream_t st);
 void launch_retr_scan(const Dims& D, const State& S, cudaStream_t st);
 void launch_retr_write(const Dims& D, const State& S, cudaStream_t st);
