@@ -745,16 +745,11 @@ static int enqueue_local(pikv_engine* eng, const void* q, const void* k, const v
     launch_insert(D, eng->C, S, q, k, v, sal, st), ++n;
     mark(eng, 2);
     const bool sched = D.Gl > 0 && !eng->C.unbounded_budget;
-    // (k_sched_fused -- keys + select in one CTA per device -- measured slower
-    // than the wide page-key kernel + select: 34.7 vs 28.5 us on c2)
-    if (sched && eng->C.record_agg) {
-        launch_sched_lru(D, eng->C, S, st), ++n;  // live-page counter; keys only where P > K
-        mark(eng, 3);
-    } else {
-        if (sched) launch_sched_pages(D, eng->C, S, st), ++n;
-        mark(eng, 3);
-        if (sched) launch_sched_select(D, eng->C, S, st), ++n;
-    }
+    // LRU/LRU+: both kernels exit at once for devices whose live-page counter
+    // is within budget (single-CTA key computation measured slower: 32 vs 27 us)
+    if (sched) launch_sched_pages(D, eng->C, S, st), ++n;
+    mark(eng, 3);
+    if (sched) launch_sched_select(D, eng->C, S, st), ++n;
     mark(eng, 4);
     launch_retr_count(D, S, st), ++n;
     mark(eng, 5);

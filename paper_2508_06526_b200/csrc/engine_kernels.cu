@@ -788,11 +788,15 @@ __global__ void k_sched_pages(Dims D, Cfg C, State S, int lanes) {
     const uint64_t lo = seq > Su ? seq - Su : 0;
     const uint64_t q = lo / ps + (uint64_t)pi;
     const int64_t rec = ring * D.ppr_sched + (int64_t)(q % (uint64_t)D.ppr_sched);
+    if (C.record_agg) {  // lanes == 1
+        // devices within budget evict nothing: select decides from the
+        // live-page counter and never reads their keys
+        if (!in || S.pages_live[ring / D.SPD] <= C.budget_pages) return;
+    }
     const int cnt = (in && q * ps < seq) ? S.pr_cnt[rec] : 0;
     const bool live_page = cnt > 0 && !S.err[s];
     const uint64_t now = in ? S.now[s] : 0;
-    if (C.record_agg) {  // lanes == 1
-        if (!in) return;
+    if (C.record_agg) {
         double agg = 0.0;
         uint64_t oldest = 0;
         if (live_page) {
@@ -869,6 +873,15 @@ __device__ __forceinline__ void select_body(const Dims& D, const Cfg& C, const S
     __shared__ uint64_t sm_bo;
     __shared__ int sm_bi;
     if (S.err[s]) return;
+    if (C.record_agg && S.pages_live[sg] <= C.budget_pages) {  // P <= K: nothing to evict
+        if (tid == 0) {
+            const int P = S.pages_live[sg];
+            S.pages_before[sg] = P;
+            S.pages_after[sg] = P;
+            S.n_ev[sg] = 0;
+        }
+        return;
+    }
     // ---- fast path (the common steady state evicts 0 or 1 page): one pass
     // over the page keys computes P, the below-theta count T and the argmin;
     // one two-level reduction; a single victim is erased directly.
@@ -1220,46 +1233,6 @@ __global__ void __launch_bounds__(kSelThreads) k_sched_select(Dims D, Cfg C, Sta
     select_body(D, C, S, blockIdx.x, stage != 0);
 }
 
-// LRU / LRU+ with exact sums: one CTA per (stream, local device) computes the
-// keys of all its candidate pages from the page records, then selects and
-// erases in place (evict, scheduler.cpp:262-330) -- one launch, no slot scan.
-__global__ void __launch_bounds__(kSelThreads) k_sched_fused(Dims D, Cfg C, State S) {
-    griddep_enter();
-    const int sg = blockIdx.x;
-    const int s = sg / D.Gl;
-    const int tid = threadIdx.x;
-    __shared__ uint64_t sm_seq[64];
-    if (S.err[s]) return;
-    for (int sh = tid; sh < D.SPD && sh < 64; sh += kSelThreads) sm_seq[sh] = S.seq[(int64_t)sg * D.SPD + sh];
-    __syncthreads();
-    const uint64_t now = S.now[s];
-    const uint64_t Su = (uint64_t)D.S, ps = (uint64_t)D.page_size;
-    const int64_t first_t = (int64_t)sg * D.SPD * D.ppr_sched;
-    const int npg = D.SPD * D.ppr_sched;
-#pragma unroll 4
-    for (int i = tid; i < npg; i += kSelThreads) {
-        const int sh = i / D.ppr_sched, pi = i % D.ppr_sched;
-        const int64_t ring = (int64_t)sg * D.SPD + sh;
-        const uint64_t seq = sh < 64 ? sm_seq[sh] : S.seq[ring];
-        const uint64_t lo = seq > Su ? seq - Su : 0;
-        const uint64_t q = lo / ps + (uint64_t)pi;
-        const int64_t rec = ring * D.ppr_sched + (int64_t)(q % (uint64_t)D.ppr_sched);
-        const int cnt = q * ps < seq ? S.pr_cnt[rec] : 0;
-        double agg = 0.0;
-        uint64_t oldest = 0;
-        if (cnt > 0) {
-            agg = -(double)((uint64_t)cnt * now - S.pr_sla[rec]);
-            if (C.sched_strategy == PIKV_SCHED_LRU_PLUS)
-                agg = __dadd_rn(agg, __dmul_rn(C.lambda_freq, (double)S.pr_sf[rec]));
-            oldest = S.id[ring * D.S + (int64_t)((q * ps + (uint64_t)S.pr_first[rec]) % Su)];
-        }
-        S.pg_cnt[first_t + i] = cnt;
-        S.pg_agg[first_t + i] = agg;
-        S.pg_oldest[first_t + i] = oldest;
-    }
-    __syncthreads();
-    select_body(D, C, S, sg, false);
-}
 
 void launch_sched_pages(const Dims& D, const Cfg& C, const State& S, cudaStream_t st) {
     int lanes = 1;
@@ -1267,64 +1240,7 @@ void launch_sched_pages(const Dims& D, const Cfg& C, const State& S, cudaStream_
     const int64_t threads = (int64_t)D.B * D.R * D.ppr_sched * lanes;
     launch_pdl(k_sched_pages, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0, st, D, C, S, lanes);
 }
-// LRU / LRU+ (record aggregates): the live-page counter decides whether this
-// device evicts at all (P <= K: nothing to do, one load); only evicting
-// devices compute their page keys from the records and select (fast path for
-// one victim).  Bit-identical to the full scan: the keys are the same.
-__global__ void __launch_bounds__(kSelThreads) k_sched_lru(Dims D, Cfg C, State S) {
-    griddep_enter();
-    const int sg = blockIdx.x;
-    const int s = sg / D.Gl;
-    const int tid = threadIdx.x;
-    if (S.err[s]) return;
-    const int P = S.pages_live[sg];
-    if (P <= C.budget_pages) {
-        if (tid == 0) {
-            S.pages_before[sg] = P;
-            S.pages_after[sg] = P;
-            S.n_ev[sg] = 0;
-        }
-        return;
-    }
-    __shared__ uint64_t sm_seq[64];
-    for (int sh = tid; sh < D.SPD && sh < 64; sh += kSelThreads) sm_seq[sh] = S.seq[(int64_t)sg * D.SPD + sh];
-    __syncthreads();
-    const uint64_t now = S.now[s];
-    const uint64_t Su = (uint64_t)D.S, ps = (uint64_t)D.page_size;
-    const int64_t first_t = (int64_t)sg * D.SPD * D.ppr_sched;
-    const int npg = D.SPD * D.ppr_sched;
-    for (int i = tid; i < npg; i += kSelThreads) {
-        const int sh = i / D.ppr_sched, pi = i % D.ppr_sched;
-        const int64_t ring = (int64_t)sg * D.SPD + sh;
-        const uint64_t seq = sh < 64 ? sm_seq[sh] : S.seq[ring];
-        const uint64_t lo = seq > Su ? seq - Su : 0;
-        const uint64_t q = lo / ps + (uint64_t)pi;
-        const int64_t rec = ring * D.ppr_sched + (int64_t)(q % (uint64_t)D.ppr_sched);
-        const int cnt = q * ps < seq ? S.pr_cnt[rec] : 0;
-        double agg = 0.0;
-        uint64_t oldest = 0;
-        if (cnt > 0) {
-            agg = -(double)((uint64_t)cnt * now - S.pr_sla[rec]);
-            if (C.sched_strategy == PIKV_SCHED_LRU_PLUS)
-                agg = __dadd_rn(agg, __dmul_rn(C.lambda_freq, (double)S.pr_sf[rec]));
-            oldest = S.id[ring * D.S + (int64_t)((q * ps + (uint64_t)S.pr_first[rec]) % Su)];
-        }
-        S.pg_cnt[first_t + i] = cnt;
-        S.pg_agg[first_t + i] = agg;
-        S.pg_oldest[first_t + i] = oldest;
-    }
-    __threadfence_block();
-    __syncthreads();
-    select_body(D, C, S, sg, false);
-}
 
-void launch_sched_lru(const Dims& D, const Cfg& C, const State& S, cudaStream_t st) {
-    launch_pdl(k_sched_lru, dim3(D.B * D.Gl), dim3(kSelThreads), 0, st, D, C, S);
-}
-
-void launch_sched_fused(const Dims& D, const Cfg& C, const State& S, cudaStream_t st) {
-    launch_pdl(k_sched_fused, dim3(D.B * D.Gl), dim3(kSelThreads), 0, st, D, C, S);
-}
 void launch_sched_select(const Dims& D, const Cfg& C, const State& S, cudaStream_t st) {
     const size_t keys = (size_t)D.SPD * D.ppr_sched * (8 + 8 + 4);
     const int stage = keys <= 200 * 1024 ? 1 : 0;

@@ -325,8 +325,7 @@ void launch_insert(const Dims& D, const Cfg& C, const State& S, const void* q, c
                    const void* v, const double* saliency, cudaStream_t st);
 void launch_sched_pages(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);
 void launch_sched_select(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);
-void launch_sched_fused(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);
-void launch_sched_lru(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);
+
 void launch_retr_count(const Dims& D, const State& S, cudaStream_t st);
 void launch_retr_scan(const Dims& D, const State& S, cudaStream_t st);
 void launch_retr_write(const Dims& D, const State& S, cudaStream_t st);
