@@ -71,6 +71,48 @@ __global__ void k(int variant, double* out, long long* cyc) {
 #pragma unroll
             for (int u = 0; u < 16; ++u) acc = __dadd_rn(acc, rb[u]);
         }
+    } else if (variant == 6) {
+        // precomputed products (smem), batches of 32 in registers; the next
+        // batch's LDS.128 interleaved between the current batch's DADDs
+        double cur[32], nxt[32];
+#pragma unroll
+        for (int u = 0; u < 32; u += 2) {
+            double2 v = *(const double2*)(p + u);
+            cur[u] = v.x; cur[u + 1] = v.y;
+        }
+        for (int i0 = 0; i0 < D; i0 += 32) {
+            const int nb = (i0 + 32) & (DR - 1);
+#pragma unroll
+            for (int u = 0; u < 32; u += 2) {
+                acc = __dadd_rn(acc, cur[u]);
+                double2 v = *(const double2*)(p + nb + u);
+                acc = __dadd_rn(acc, cur[u + 1]);
+                nxt[u] = v.x; nxt[u + 1] = v.y;
+            }
+#pragma unroll
+            for (int u = 0; u < 32; ++u) cur[u] = nxt[u];
+        }
+    } else if (variant == 7) {
+        // LDS + DMUL of the next batch interleaved between the current DADDs
+        double cur[32], nxt[32];
+#pragma unroll
+        for (int u = 0; u < 32; u += 2) {
+            double2 a = *(const double2*)(w + u), b = *(const double2*)(q + u);
+            cur[u] = __dmul_rn(a.x, b.x); cur[u + 1] = __dmul_rn(a.y, b.y);
+        }
+        for (int i0 = 0; i0 < D; i0 += 32) {
+            const int nb = (i0 + 32) & (DR - 1);
+#pragma unroll
+            for (int u = 0; u < 32; u += 2) {
+                double2 a = *(const double2*)(w + nb + u), b = *(const double2*)(q + nb + u);
+                acc = __dadd_rn(acc, cur[u]);
+                nxt[u] = __dmul_rn(a.x, b.x);
+                acc = __dadd_rn(acc, cur[u + 1]);
+                nxt[u + 1] = __dmul_rn(a.y, b.y);
+            }
+#pragma unroll
+            for (int u = 0; u < 32; ++u) cur[u] = nxt[u];
+        }
     }
     long long t1 = clock64();
     out[e] = acc;
@@ -81,7 +123,7 @@ int main() {
     cudaMalloc(&d_out, 8 * E); cudaMalloc(&d_c, 8 * 8);
     size_t smem = sizeof(double) * (2 * E * LD + DR);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    for (int v = 1; v <= 5; ++v) {
+    for (int v = 1; v <= 7; ++v) {
         k<<<1, 32, smem>>>(v, d_out, d_c);
         k<<<1, 32, smem>>>(v, d_out, d_c);
         long long c[8];
