@@ -364,7 +364,7 @@ static int validate(const pikv_config& c) {
         c.router_strategy > PIKV_ROUTER_HIERARCHICAL)
         return fail(PIKV_ERR_INVALID_CONFIG, "unknown strategy");
     // engine limits
-    if (c.E > kMaxE) return fail(PIKV_ERR_INVALID_CONFIG, "E must be <= 256");
+    if (c.E > 96) return fail(PIKV_ERR_INVALID_CONFIG, "E must be <= 96 (router summer warps)");
     if (c.k > kMaxK) return fail(PIKV_ERR_INVALID_CONFIG, "k must be <= 64");
     if (c.n_heads < 1 || c.d % c.n_heads)
         return fail(PIKV_ERR_INVALID_CONFIG, "n_heads must divide d");

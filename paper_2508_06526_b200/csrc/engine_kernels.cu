@@ -58,9 +58,10 @@ __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin, in
     const int s = blockIdx.x;
     const int tid = threadIdx.x;
     const int nsum_warps = (D.E + 31) / 32;  // warps 0..: one lane per expert chain
-    // warps nsum_warps.. are fillers (other SM sub-partitions: their DMULs do
-    // not contend with the chains' DADDs for the FP64 pipe)
-    const int nfill_warps = ((int)blockDim.x >> 5) - nsum_warps;
+    // filler warps sit on other SM sub-partitions (warp % 4) than the summer
+    // warps, so their DMULs do not contend with the chains' DADDs for FP64
+    int nfill_warps = 0;
+    for (int w2 = nsum_warps; w2 < (int)(blockDim.x >> 5); ++w2) nfill_warps += (w2 & 3) >= nsum_warps;
     // per-step scratch counters of this stream (replaces memset nodes)
     if (tid == 0) S.n_ow[s] = 0;
     for (int g = tid; g < D.Gl; g += blockDim.x) {
@@ -135,36 +136,42 @@ __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin, in
         const int E = D.E, CH = kRouteCH;
         const int nchunk = (D.d + CH - 1) / CH;
         const int warp = tid >> 5, lane = tid & 31;
-        if (warp >= nsum_warps) {
-            // fillers: p[e][i] = W[e][c0+i] * q[c0+i] (correctly rounded
-            // DMUL, as each product of router.cpp:231) for chunk c
-            const int ft = tid - nsum_warps * 32, nft = nfill_warps * 32;
+        // fillers: warps >= nsum_warps on SM sub-partitions (warp % 4) that
+        // host no summer warp
+        const bool filler = warp >= nsum_warps && (warp & 3) >= nsum_warps;
+        if (filler) {
+            // p[e][i] = W[e][c0+i] * q[c0+i] (correctly rounded DMUL, each
+            // product of router.cpp:231); a thread owns whole columns
+            int fidx = 0, nfill = 0;  // rank among filler warps
+            for (int w2 = 0; w2 < (int)(blockDim.x >> 5); ++w2) {
+                const bool f2 = w2 >= nsum_warps && (w2 & 3) >= nsum_warps;
+                if (f2 && w2 < warp) ++fidx;
+                nfill += f2;
+            }
+            const int ft = fidx * 32 + lane, nft = nfill * 32;
             int stage = 0;
             uint32_t phase = 0;
             for (int c = 0; c < nchunk; ++c) {
                 const int c0 = c * CH, w = min(CH, D.d - c0);
                 mbar_wait(&empty[stage], phase ^ 1);
                 double* dst = ring + (size_t)stage * E * ldp;
-                for (int t0 = ft; t0 < E * CH; t0 += 8 * nft) {
+                for (int i = ft; i < w; i += nft) {
+                    const double qi = sm_q[c0 + i];
+                    const double* wc = S.W + c0 + i;
                     double wv[8];
+                    for (int e0 = 0; e0 < E; e0 += 8) {
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const int t = t0 + u * nft;
-                        const int e = t / CH, i = t % CH;
-                        wv[u] = (t < E * CH && i < w) ? __ldg(S.W + (int64_t)e * D.d + c0 + i) : 0.0;
-                    }
+                        for (int u = 0; u < 8; ++u) wv[u] = e0 + u < E ? __ldg(wc + (int64_t)(e0 + u) * D.d) : 0.0;
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const int t = t0 + u * nft;
-                        const int e = t / CH, i = t % CH;
-                        if (t < E * CH && i < w) dst[e * ldp + i] = __dmul_rn(wv[u], sm_q[c0 + i]);
+                        for (int u = 0; u < 8; ++u)
+                            if (e0 + u < E) dst[(e0 + u) * ldp + i] = __dmul_rn(wv[u], qi);
                     }
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&full[stage]);
                 if (++stage == kRouteStages) stage = 0, phase ^= 1;
             }
-        } else {
+        } else if (warp < nsum_warps) {
             // summers: the sequential DADD chain of router.cpp:229-231 in
             // column order.  32-product batches live in registers and the next
             // batch's LDS.128 are interleaved between the current DADDs, so
@@ -400,7 +407,7 @@ void launch_route(const Dims& D, const Cfg& C, const State& S, const void* q, cu
     while (ch > 32 && bytes(ch) > 200 * 1024) ch -= 32;
     const size_t smem = bytes(ch);
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_route, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const int threads = ((D.E + 31) / 32) * 32 + 4 * 32;  // summer warps + 4 filler warps
+    const int threads = 256;  // summer warps (E/32) + filler warps on the other sub-partitions
     launch_pdl(k_route, dim3(D.B), dim3(threads), smem, st, D, C, S, q, ch);
 }
 
