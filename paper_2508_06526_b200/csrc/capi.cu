@@ -364,7 +364,7 @@ static int validate(const pikv_config& c) {
         c.router_strategy > PIKV_ROUTER_HIERARCHICAL)
         return fail(PIKV_ERR_INVALID_CONFIG, "unknown strategy");
     // engine limits
-    if (c.E > 96) return fail(PIKV_ERR_INVALID_CONFIG, "E must be <= 96 (router summer warps)");
+    if (c.E > kMaxE) return fail(PIKV_ERR_INVALID_CONFIG, "E must be <= 256");
     if (c.k > kMaxK) return fail(PIKV_ERR_INVALID_CONFIG, "k must be <= 64");
     if (c.n_heads < 1 || c.d % c.n_heads)
         return fail(PIKV_ERR_INVALID_CONFIG, "n_heads must divide d");
@@ -380,7 +380,7 @@ static int validate(const pikv_config& c) {
         return fail(PIKV_ERR_INVALID_CONFIG, "codec rank must be in [1, head_dim]");
     if (c.n_layers < 0) return fail(PIKV_ERR_INVALID_CONFIG, "n_layers must be >= 0");
     if (c.d > 16384) return fail(PIKV_ERR_INVALID_CONFIG, "d must be <= 16384 (router stages q in smem)");
-    if (128 + 8.0 * c.d + 3.0 * c.E * (32 + 2) * 8 > 200 * 1024)
+    if (128 + 8.0 * c.d + 5.0 * c.E * (32 * 8 + 16) > 200 * 1024)
         return fail(PIKV_ERR_INVALID_CONFIG, "router: E x d too large for the shared-memory W ring");
     return PIKV_OK;
 }

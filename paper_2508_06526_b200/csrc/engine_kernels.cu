@@ -39,7 +39,7 @@ __device__ __forceinline__ void route_select(const Dims& D, const Cfg& C, const 
                                              const double* bias, int* sel);
 
 constexpr int kRouteCHMax = 256;  // columns per stage (reduced so E rows x stages fit)
-constexpr int kRouteStages = 3;
+constexpr int kRouteStages = 5;
 
 __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin, int kRouteCH) {
     griddep_enter();
@@ -47,8 +47,8 @@ __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin, in
     uint64_t* full = (uint64_t*)sm_raw;
     uint64_t* empty = full + kRouteStages;
     double* sm_q = (double*)(sm_raw + 128);
-    const int ldp = kRouteCH + 2;  // padded product row (16 B): 2-way LDS.128 conflicts at worst
-    double* ring = sm_q + D.d;     // [kRouteStages][E][ldp] exact products
+    const int rowb = kRouteCH * 8 + 16;  // padded row: 2-way bank conflicts at worst (CH % 32 == 0)
+    uint8_t* ring = (uint8_t*)(sm_q + D.d);
     __shared__ double sm_logit[kMaxE];
     __shared__ bool sm_flag[kMaxE];
     __shared__ int sm_pool[kMaxE];
@@ -57,11 +57,8 @@ __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin, in
     __shared__ int sm_sel[kMaxK];
     const int s = blockIdx.x;
     const int tid = threadIdx.x;
-    const int nsum_warps = (D.E + 31) / 32;  // warps 0..: one lane per expert chain
-    // filler warps sit on other SM sub-partitions (warp % 4) than the summer
-    // warps, so their DMULs do not contend with the chains' DADDs for FP64
-    int nfill_warps = 0;
-    for (int w2 = nsum_warps; w2 < (int)(blockDim.x >> 5); ++w2) nfill_warps += (w2 & 3) >= nsum_warps;
+    const int nsum_warps = (D.E + 31) / 32;
+    const int prod_warp = nsum_warps;  // last warp
     // per-step scratch counters of this stream (replaces memset nodes)
     if (tid == 0) S.n_ow[s] = 0;
     for (int g = tid; g < D.Gl; g += blockDim.x) {
@@ -83,7 +80,7 @@ __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin, in
     if (dbg) S.dbg[0] = clock64();
     if (tid == 0) {
         for (int i = 0; i < kRouteStages; ++i) {
-            mbar_init(&full[i], nfill_warps);
+            mbar_init(&full[i], 1);
             mbar_init(&empty[i], nsum_warps);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -136,77 +133,54 @@ __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin, in
         const int E = D.E, CH = kRouteCH;
         const int nchunk = (D.d + CH - 1) / CH;
         const int warp = tid >> 5, lane = tid & 31;
-        // fillers: warps >= nsum_warps on SM sub-partitions (warp % 4) that
-        // host no summer warp
-        const bool filler = warp >= nsum_warps && (warp & 3) >= nsum_warps;
-        if (filler) {
-            // p[e][i] = W[e][c0+i] * q[c0+i] (correctly rounded DMUL, each
-            // product of router.cpp:231); a thread owns whole columns
-            int fidx = 0, nfill = 0;  // rank among filler warps
-            for (int w2 = 0; w2 < (int)(blockDim.x >> 5); ++w2) {
-                const bool f2 = w2 >= nsum_warps && (w2 & 3) >= nsum_warps;
-                if (f2 && w2 < warp) ++fidx;
-                nfill += f2;
-            }
-            const int ft = fidx * 32 + lane, nft = nfill * 32;
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int c = 0; c < nchunk; ++c) {
-                const int c0 = c * CH, w = min(CH, D.d - c0);
-                mbar_wait(&empty[stage], phase ^ 1);
-                double* dst = ring + (size_t)stage * E * ldp;
-                for (int i = ft; i < w; i += nft) {
-                    const double qi = sm_q[c0 + i];
-                    const double* wc = S.W + c0 + i;
-                    double wv[8];
-                    for (int e0 = 0; e0 < E; e0 += 8) {
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) wv[u] = e0 + u < E ? __ldg(wc + (int64_t)(e0 + u) * D.d) : 0.0;
-#pragma unroll
-                        for (int u = 0; u < 8; ++u)
-                            if (e0 + u < E) dst[(e0 + u) * ldp + i] = __dmul_rn(wv[u], qi);
-                    }
+        if (warp == prod_warp) {
+            if (lane == 0) {
+                int stage = 0;
+                uint32_t phase = 0;
+                for (int c = 0; c < nchunk; ++c) {
+                    const int c0 = c * CH, w = min(CH, D.d - c0);
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_expect_tx(&full[stage], (uint32_t)(E * w * 8));
+                    uint8_t* dst = ring + (size_t)stage * E * rowb;
+                    for (int e = 0; e < E; ++e)
+                        bulk_g2s_plain(dst + (size_t)e * rowb, S.W + (int64_t)e * D.d + c0,
+                                       (uint32_t)(w * 8), &full[stage]);
+                    if (++stage == kRouteStages) stage = 0, phase ^= 1;
                 }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&full[stage]);
-                if (++stage == kRouteStages) stage = 0, phase ^= 1;
             }
         } else if (warp < nsum_warps) {
-            // summers: the sequential DADD chain of router.cpp:229-231 in
-            // column order.  32-product batches live in registers and the next
-            // batch's LDS.128 are interleaved between the current DADDs, so
-            // the chain runs at the DADD latency (8.1 cycles/column measured,
-            // profiles/microbench/chain_variants.cu variant 6)
             double acc = 0.0;
             int stage = 0;
             uint32_t phase = 0;
             const int e = tid;
+            long long t_wait = 0;
             for (int c = 0; c < nchunk; ++c) {
                 const int c0 = c * CH, w = min(CH, D.d - c0);
+                const long long tw0 = clock64();
                 mbar_wait(&full[stage], phase);
+                t_wait += clock64() - tw0;
                 if (e < E) {
-                    const double* row = ring + (size_t)stage * E * ldp + (size_t)e * ldp;
+                    // 32 products into registers (LDS.128 pairs, independent
+                    // DMULs), then the 32-long DADD chain: measured 10.5
+                    // cycles/column on B200 vs 17.6 for a fused load-mul-add
+                    // loop (profiles/microbench/chain_variants.cu)
+                    const double* row = (const double*)(ring + (size_t)stage * E * rowb + (size_t)e * rowb);
+                    const double* qq = sm_q + c0;
                     if (w == CH) {
-                        double cur[32], nxt[32];
-#pragma unroll
-                        for (int u = 0; u < 32; u += 2) {
-                            const double2 v2 = *(const double2*)(row + u);
-                            cur[u] = v2.x, cur[u + 1] = v2.y;
-                        }
                         for (int i0 = 0; i0 < CH; i0 += 32) {
-                            const int nb = i0 + 32 < CH ? i0 + 32 : i0;  // last batch: harmless reload
+                            double r[32];
 #pragma unroll
                             for (int u = 0; u < 32; u += 2) {
-                                acc = __dadd_rn(acc, cur[u]);
-                                const double2 v2 = *(const double2*)(row + nb + u);
-                                acc = __dadd_rn(acc, cur[u + 1]);
-                                nxt[u] = v2.x, nxt[u + 1] = v2.y;
+                                const double2 a2 = *(const double2*)(row + i0 + u);
+                                const double2 b2 = *(const double2*)(qq + i0 + u);
+                                r[u] = __dmul_rn(a2.x, b2.x);
+                                r[u + 1] = __dmul_rn(a2.y, b2.y);
                             }
 #pragma unroll
-                            for (int u = 0; u < 32; ++u) cur[u] = nxt[u];
+                            for (int u = 0; u < 32; ++u) acc = __dadd_rn(acc, r[u]);
                         }
                     } else {
-                        for (int i = 0; i < w; ++i) acc = __dadd_rn(acc, row[i]);
+                        for (int i = 0; i < w; ++i) acc = __dadd_rn(acc, __dmul_rn(row[i], qq[i]));
                     }
                 }
                 __syncwarp();
@@ -214,6 +188,7 @@ __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin, in
                 if (++stage == kRouteStages) stage = 0, phase ^= 1;
             }
             if (e < E) sm_logit[e] = acc;
+            if (dbg) S.dbg[5] = t_wait;
         }
         __syncthreads();
     }
@@ -402,12 +377,12 @@ __device__ __forceinline__ void route_select(const Dims& D, const Cfg& C, const 
 void launch_route(const Dims& D, const Cfg& C, const State& S, const void* q, cudaStream_t st) {
     int ch = kRouteCHMax;
     auto bytes = [&](int c) {
-        return 128 + sizeof(double) * ((size_t)D.d + (size_t)kRouteStages * D.E * (c + 2));
+        return 128 + sizeof(double) * (size_t)D.d + (size_t)kRouteStages * D.E * ((size_t)c * 8 + 16);
     };
     while (ch > 32 && bytes(ch) > 200 * 1024) ch -= 32;
     const size_t smem = bytes(ch);
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_route, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const int threads = 256;  // summer warps (E/32) + filler warps on the other sub-partitions
+    const int threads = ((D.E + 31) / 32) * 32 + 32;
     launch_pdl(k_route, dim3(D.B), dim3(threads), smem, st, D, C, S, q, ch);
 }
 
