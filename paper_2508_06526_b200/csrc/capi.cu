@@ -603,9 +603,10 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
     chk(S.dbg = eng->alloc<long long>(64));
     chk(S.done_ctr = eng->alloc<unsigned>(1));
     const size_t in_elem = c.kv_dtype == PIKV_DTYPE_BF16 ? 2 : 4;
-    chk(eng->in_q = eng->alloc<uint8_t>((size_t)B * D.d * in_elem));
-    chk(eng->in_k = eng->alloc<uint8_t>((size_t)B * D.d * in_elem));
-    chk(eng->in_v = eng->alloc<uint8_t>((size_t)B * D.d * in_elem));
+    // q, k, v staging: one allocation, packed back to back
+    chk(eng->in_q = eng->alloc<uint8_t>((size_t)3 * B * D.d * in_elem));
+    eng->in_k = (uint8_t*)eng->in_q + (size_t)B * D.d * in_elem;
+    eng->in_v = (uint8_t*)eng->in_k + (size_t)B * D.d * in_elem;
     chk(eng->in_sal = eng->alloc<double>((size_t)B * std::max(D.n_layers, 1)));
     chk(eng->out_y = eng->alloc<float>((size_t)B * D.dp));
     if (!ok) {
@@ -834,9 +835,16 @@ int pikv_step_host(pikv_engine* eng, const void* q, const void* k, const void* v
     const Dims& D = eng->D;
     const size_t n = (size_t)D.B * D.d * (D.kv_dtype == PIKV_DTYPE_BF16 ? 2 : 4);
     cudaStream_t st = eng->stream;
-    CUDA_TRY(cudaMemcpyAsync(eng->in_q, q, n, cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaMemcpyAsync(eng->in_k, k, n, cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaMemcpyAsync(eng->in_v, v, n, cudaMemcpyHostToDevice, st));
+    const uint8_t* hq = (const uint8_t*)q;
+    if ((const uint8_t*)k == hq + n && (const uint8_t*)v == hq + 2 * n) {
+        // q, k, v packed back to back on the host: one transfer into the
+        // (equally packed) staging buffers
+        CUDA_TRY(cudaMemcpyAsync(eng->in_q, q, 3 * n, cudaMemcpyHostToDevice, st));
+    } else {
+        CUDA_TRY(cudaMemcpyAsync(eng->in_q, q, n, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaMemcpyAsync(eng->in_k, k, n, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaMemcpyAsync(eng->in_v, v, n, cudaMemcpyHostToDevice, st));
+    }
     const double* sal = nullptr;
     if (saliency && D.n_layers > 0) {
         CUDA_TRY(cudaMemcpyAsync(eng->in_sal, saliency, sizeof(double) * D.B * D.n_layers,
