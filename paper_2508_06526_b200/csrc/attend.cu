@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
         uint32_t phase = 0;
         for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
             const int s = S.item_stream[w];
-            const int64_t pos0 = S.att_base[s] + S.item_begin[w];
+            const int64_t pos0 = (int64_t)s * D.att_stride + S.item_begin[w];
             const int cnt = S.item_end[w] - S.item_begin[w];
             for (int b = 0; b < cnt; b += P.EPS) {
                 const int n = min(P.EPS, cnt - b);
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
     uint32_t phase = 0;
     for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
         const int s = S.item_stream[w];
-        const int64_t pos0 = S.att_base[s] + S.item_begin[w];
+        const int64_t pos0 = (int64_t)s * D.att_stride + S.item_begin[w];
         const int cnt = S.item_end[w] - S.item_begin[w];
         f2 q[CPT][NP], o[CPT][NP];
         float m = -INFINITY, l = 0.f;

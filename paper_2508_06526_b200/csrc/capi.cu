@@ -66,6 +66,21 @@ constexpr uint64_t kRouterSalt = 0x2545f4914f6cdd1dULL;  // pipeline.cpp:16
 
 // RouterState::init (router.cpp:54-67): W_r = Rng(seed).normal_vector(E*d,
 // 1/sqrt(d)), with pikv::Rng's transforms over std::mt19937_64 (rng.hpp).
+// W_r [E][d] (row-major, router.cpp:54-67) -> the device layout: chunks of
+// route_ch columns, each [E][route_ch + 2] with zero padding (State::W).
+static size_t router_w_elems(const Dims& D) {
+    const size_t nch = (size_t)(D.d + D.route_ch - 1) / D.route_ch;
+    return nch * D.E * (D.route_ch + 2);
+}
+static std::vector<double> pack_router_w(const Dims& D, const double* w) {
+    std::vector<double> out(router_w_elems(D), 0.0);
+    const int ch = D.route_ch, rs = ch + 2;
+    for (int e = 0; e < D.E; ++e)
+        for (int i = 0; i < D.d; ++i)
+            out[((size_t)(i / ch) * D.E + e) * rs + i % ch] = w[(size_t)e * D.d + i];
+    return out;
+}
+
 std::vector<double> router_matrix(int E, int d, uint64_t seed) {
     std::mt19937_64 gen(seed);
     auto uniform = [&]() { return static_cast<double>(gen() >> 11) * 0x1.0p-53; };
@@ -115,6 +130,7 @@ struct pikv_engine {
     bool warmed = false;
     int64_t launches = 0;
     int kernels_per_step = 0;
+    bool fused_control = false;  // k_control replaces route..retr_write (PIKV_CONTROL=0 disables)
     // profiling: per step kPhases+1 events on the engine stream
     bool profiling = false;
     std::vector<cudaEvent_t> ev;
@@ -451,6 +467,8 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
     {
         const char* v = std::getenv("PIKV_ITEMS");
         D.items_per_cta = v ? std::max(1, std::atoi(v)) : 4;
+        const char* dc = std::getenv("PIKV_DEBUG_CTL");
+        D.dbg_ctl = dc && dc[0] == '1';
     }
     D.item_cap = (int64_t)D.items_per_cta * D.attend_ctas + D.B + 16;
     const int64_t total_slots = (int64_t)D.B * D.R * D.S;
@@ -467,7 +485,8 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
     }
     D.pool_pages = (pool_entries + D.spg - 1) / D.spg;
     D.pool_entries = D.pool_pages * D.spg;
-    D.att_cap = std::min<int64_t>(D.pool_entries, total_slots) + 1;
+    D.att_stride = std::min<int64_t>((int64_t)D.max_cand * c.S, D.pool_entries);
+    D.att_cap = (int64_t)D.B * D.att_stride + 1;
     if (const char* msg = attend_check(D)) {
         delete eng;
         return fail(PIKV_ERR_INVALID_CONFIG, std::string("attention layout: ") + msg);
@@ -508,6 +527,10 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
         C.record_agg = C.exact_sum && (c.sched_strategy == PIKV_SCHED_LRU ||
                                        c.sched_strategy == PIKV_SCHED_LRU_PLUS) ? 1 : 0;
     }
+    {
+        const char* v = std::getenv("PIKV_CONTROL");
+        eng->fused_control = control_supported(D, C) && !(v && v[0] == '0');
+    }
 
     // exchange record layout
     ExchangeLayout& X = eng->X;
@@ -524,7 +547,8 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
     const int64_t rings = (int64_t)B * D.R;
     bool ok = true;
     auto chk = [&](void* p) { ok = ok && p != nullptr; };
-    double* W = eng->alloc<double>((size_t)E * D.d);
+    D.route_ch = pick_route_chunk(D);
+    double* W = eng->alloc<double>(router_w_elems(D));
     chk(W);
     S.W = W;
     chk(S.load = eng->alloc<double>((size_t)B * E));
@@ -584,7 +608,7 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
     chk(S.chunk_cnt = eng->alloc<int32_t>(nchunk));
     chk(S.chunk_off = eng->alloc<int32_t>(nchunk));
     chk(S.found = eng->alloc<int32_t>((size_t)B * k));
-    chk(S.att_base = eng->alloc<int64_t>(B + 1));
+    chk(S.att_cnt = eng->alloc<int32_t>(B));
     chk(S.att_slot = eng->alloc<int32_t>(D.att_cap));
     chk(S.att_entry = eng->alloc<int32_t>(D.att_cap));
     chk(S.scores = eng->alloc<float>((size_t)D.att_cap * D.H));
@@ -600,8 +624,9 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
     chk(S.gM = eng->alloc<float>((size_t)B * D.H));
     chk(S.gL = eng->alloc<float>((size_t)B * D.H));
     chk(S.summary = eng->alloc<pikv_step_summary>(B));
-    chk(S.dbg = eng->alloc<long long>(64));
+    chk(S.dbg = eng->alloc<long long>(64 + 8 * (size_t)B));
     chk(S.done_ctr = eng->alloc<unsigned>(1));
+    chk(S.ctl_ctr = eng->alloc<unsigned>(1));
     const size_t in_elem = c.kv_dtype == PIKV_DTYPE_BF16 ? 2 : 4;
     // q, k, v staging: one allocation, packed back to back
     chk(eng->in_q = eng->alloc<uint8_t>((size_t)3 * B * D.d * in_elem));
@@ -615,8 +640,10 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
     }
     // initial state
     cudaStream_t st = eng->stream;
-    auto w = router_matrix(E, D.d, c.seed ^ kRouterSalt);
-    CUDA_TRY(cudaMemcpyAsync(W, w.data(), sizeof(double) * w.size(), cudaMemcpyHostToDevice, st));
+    {
+        const auto w = pack_router_w(D, router_matrix(E, D.d, c.seed ^ kRouterSalt).data());
+        CUDA_TRY(cudaMemcpy(W, w.data(), sizeof(double) * w.size(), cudaMemcpyHostToDevice));
+    }
     std::vector<double> theta(B, c.theta0);  // SchedulerState::init, scheduler.cpp:73-80
     CUDA_TRY(cudaMemcpyAsync(S.theta, theta.data(), sizeof(double) * B, cudaMemcpyHostToDevice, st));
     std::vector<uint64_t> ones(B, 1);  // kvstore.hpp:157 next_id_ = 1
@@ -651,8 +678,9 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
     CUDA_TRY(cudaMemsetAsync(S.summary, 0, sizeof(pikv_step_summary) * B, st));
     CUDA_TRY(cudaMemsetAsync(S.n_items, 0, sizeof(int32_t), st));
     CUDA_TRY(cudaMemsetAsync(S.item_first, 0, sizeof(int32_t) * (B + 1), st));
-    CUDA_TRY(cudaMemsetAsync(S.att_base, 0, sizeof(int64_t) * (B + 1), st));
+    CUDA_TRY(cudaMemsetAsync(S.att_cnt, 0, sizeof(int32_t) * B, st));
     CUDA_TRY(cudaMemsetAsync(S.done_ctr, 0, sizeof(unsigned), st));
+    CUDA_TRY(cudaMemsetAsync(S.ctl_ctr, 0, sizeof(unsigned), st));
     std::vector<int32_t> stack(D.pool_pages);
     for (int64_t i = 0; i < D.pool_pages; ++i) stack[i] = (int32_t)(D.pool_pages - 1 - i);
     CUDA_TRY(cudaMemcpyAsync(S.free_stack, stack.data(), sizeof(int32_t) * D.pool_pages,
@@ -681,9 +709,9 @@ int pikv_engine_destroy(pikv_engine* eng) {
 void* pikv_engine_stream(pikv_engine* eng) { return (void*)eng->stream; }
 
 int pikv_set_router_matrix_host(pikv_engine* eng, const double* w_r) {
-    CUDA_TRY(cudaMemcpyAsync((void*)eng->S.W, w_r, sizeof(double) * eng->D.E * eng->D.d,
-                             cudaMemcpyHostToDevice, eng->stream));
+    const auto w = pack_router_w(eng->D, w_r);
     CUDA_TRY(cudaStreamSynchronize(eng->stream));
+    CUDA_TRY(cudaMemcpy((void*)eng->S.W, w.data(), sizeof(double) * w.size(), cudaMemcpyHostToDevice));
     return PIKV_OK;
 }
 
@@ -737,12 +765,18 @@ static int enqueue_local(pikv_engine* eng, const void* q, const void* k, const v
     eng->cur = -1;
     if (eng->profiling && eng->prof_steps < kProfSteps) eng->cur = eng->prof_steps++ * (kPhases + 1);
     mark(eng, 0);
+    const bool proj = D.codec == PIKV_CODEC_LOWRANK || D.codec == PIKV_CODEC_LORAPLUS;
+    if (eng->fused_control) {
+        // one CTA per stream runs route -> insert -> evict -> retrieve
+        if (proj) launch_project(D, S, q, k, v, st), ++n;
+        launch_control(D, eng->C, S, q, k, v, sal, st), ++n;
+        for (int p = 1; p <= 7; ++p) mark(eng, p);
+    } else {
     launch_route(D, eng->C, S, q, st), ++n;
     mark(eng, 1);
     // a rank that owns no device still issues entry ids (k_insert) and joins
     // the merge with an empty record
-    if (D.codec == PIKV_CODEC_LOWRANK || D.codec == PIKV_CODEC_LORAPLUS)
-        launch_project(D, S, q, k, v, st), ++n;  // q, k, v of all streams in one pass
+    if (proj) launch_project(D, S, q, k, v, st), ++n;  // q, k, v of all streams in one pass
     launch_insert(D, eng->C, S, q, k, v, sal, st), ++n;
     mark(eng, 2);
     const bool sched = D.Gl > 0 && !eng->C.unbounded_budget;
@@ -758,6 +792,7 @@ static int enqueue_local(pikv_engine* eng, const void* q, const void* k, const v
     mark(eng, 6);
     launch_retr_write(D, S, st), ++n;
     mark(eng, 7);
+    }
     if (attend && D.Gl > 0) launch_attend(D, S, st), ++n;
     mark(eng, 8);
     const int direct = D.world == 1;  // single rank: combine writes y and the global (m, l)
@@ -970,9 +1005,10 @@ int pikv_read_attended_host(pikv_engine* eng, int32_t stream, int64_t* token, in
     const Dims& D = eng->D;
     if (stream < 0 || stream >= D.B) return fail(PIKV_ERR_INVALID_ARGUMENT, "stream out of range");
     CUDA_TRY(cudaStreamSynchronize(eng->stream));
-    int64_t base[2];
-    CUDA_TRY(cudaMemcpy(base, eng->S.att_base + stream, sizeof(int64_t) * 2, cudaMemcpyDeviceToHost));
-    const int n = (int)(base[1] - base[0]);
+    int32_t cnt = 0;
+    CUDA_TRY(cudaMemcpy(&cnt, eng->S.att_cnt + stream, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    const int64_t base[1] = {(int64_t)stream * D.att_stride};
+    const int n = cnt;
     *n_out = n;
     const int m = std::min(n, cap);
     if (m <= 0) return PIKV_OK;
@@ -1094,7 +1130,7 @@ int64_t pikv_entry_bytes(pikv_engine* eng) { return eng->D.entry_bytes; }
 // Not part of the public header: debug timestamps written by kernels.
 int pikv_debug_read(pikv_engine* eng, long long* out, int n) {
     CUDA_TRY(cudaStreamSynchronize(eng->stream));
-    CUDA_TRY(cudaMemcpy(out, eng->S.dbg, sizeof(long long) * std::min(n, 64), cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(out, eng->S.dbg, sizeof(long long) * std::min(n, 64 + 8 * eng->D.B), cudaMemcpyDeviceToHost));
     return PIKV_OK;
 }
 int64_t pikv_kernel_launches(pikv_engine* eng) { return eng->launches; }

@@ -18,9 +18,19 @@
 // FMAs, and every reduction keeps the reference's sequential order.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include <cooperative_groups.h>
+
 #include "pikv_dev.cuh"
 
+namespace cg = cooperative_groups;
+
 namespace pikv_dev {
+
+constexpr int kMaxCluster = 8;  // k_control CTAs per stream
 
 // ===========================================================================
 // route
@@ -41,9 +51,11 @@ __device__ __forceinline__ void route_select(const Dims& D, const Cfg& C, const 
 constexpr int kRouteCHMax = 256;  // columns per stage (reduced so E rows x stages fit)
 constexpr int kRouteStages = 5;
 
-__global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin, int kRouteCH) {
-    griddep_enter();
-    extern __shared__ __align__(128) uint8_t sm_raw[];
+// Route stream s with the calling CTA (k_route, k_control); sm_raw = the
+// dynamic shared memory (route_smem_bytes(CH)).
+__device__ __forceinline__ const int* route_body(const Dims& D, const Cfg& C, const State& S, const int s,
+                                           const void* __restrict__ qin, const int kRouteCH,
+                                           uint8_t* sm_raw) {
     uint64_t* full = (uint64_t*)sm_raw;
     uint64_t* empty = full + kRouteStages;
     double* sm_q = (double*)(sm_raw + 128);
@@ -55,7 +67,6 @@ __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin, in
     __shared__ double sm_load[kMaxE], sm_bias[kMaxE];
     __shared__ uint64_t sm_usage[kMaxE], sm_miss[kMaxE];
     __shared__ int sm_sel[kMaxK];
-    const int s = blockIdx.x;
     const int tid = threadIdx.x;
     const int nsum_warps = (D.E + 31) / 32;
     const int prod_warp = nsum_warps;  // last warp
@@ -67,7 +78,7 @@ __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin, in
         S.pages_after[s * D.Gl + g] = 0;
     }
     for (int j = tid; j < D.k; j += blockDim.x) S.found[(int64_t)s * D.k + j] = 0;
-    if (S.err[s]) return;
+    if (S.err[s]) return nullptr;
     // router state of this stream -> smem (thread 0's serial part reads it
     // without dependent global round trips)
     for (int e = tid; e < D.E; e += blockDim.x) {
@@ -137,14 +148,14 @@ __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin, in
             if (lane == 0) {
                 int stage = 0;
                 uint32_t phase = 0;
+                // W is stored chunk-major with padded rows (State::W), so a
+                // stage is one contiguous bulk copy of E padded rows
+                const uint32_t bytes = (uint32_t)(E * rowb);
                 for (int c = 0; c < nchunk; ++c) {
-                    const int c0 = c * CH, w = min(CH, D.d - c0);
                     mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_expect_tx(&full[stage], (uint32_t)(E * w * 8));
-                    uint8_t* dst = ring + (size_t)stage * E * rowb;
-                    for (int e = 0; e < E; ++e)
-                        bulk_g2s_plain(dst + (size_t)e * rowb, S.W + (int64_t)e * D.d + c0,
-                                       (uint32_t)(w * 8), &full[stage]);
+                    mbar_expect_tx(&full[stage], bytes);
+                    bulk_g2s_plain(ring + (size_t)stage * E * rowb, (const uint8_t*)S.W + (size_t)c * bytes, bytes,
+                                   &full[stage]);
                     if (++stage == kRouteStages) stage = 0, phase ^= 1;
                 }
             }
@@ -197,13 +208,20 @@ __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin, in
     if (tid < 32) route_select(D, C, S, s, sm_logit, sm_flag, sm_pool, sm_load, sm_usage, sm_miss,
                                sm_bias, sm_sel);
     __syncthreads();
-    if (S.err[s]) return;
+    if (S.err[s]) return nullptr;
     for (int e = tid; e < D.E; e += blockDim.x) S.load[(int64_t)s * D.E + e] = sm_load[e];
     for (int j = tid; j < D.k; j += blockDim.x) {
         S.usage[(int64_t)s * D.E + sm_sel[j]] = sm_usage[sm_sel[j]];
         S.experts[(int64_t)s * D.k + j] = sm_sel[j];
     }
     if (dbg) S.dbg[4] = clock64();
+    return sm_sel;  // the selected experts, in this CTA's shared memory
+}
+
+__global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin) {
+    griddep_enter();
+    extern __shared__ __align__(128) uint8_t sm_raw[];
+    route_body(D, C, S, blockIdx.x, qin, D.route_ch, sm_raw);
 }
 
 // Warp 0 of k_route: penalties, selection, gates, note_selection and the
@@ -374,16 +392,24 @@ __device__ __forceinline__ void route_select(const Dims& D, const Cfg& C, const 
     if (lane == 0) S.ncand[s] = min(nc, D.max_cand);
 }
 
-void launch_route(const Dims& D, const Cfg& C, const State& S, const void* q, cudaStream_t st) {
+static size_t route_smem_bytes(const Dims& D, int ch) {
+    return 128 + sizeof(double) * (size_t)D.d + (size_t)kRouteStages * D.E * ((size_t)ch * 8 + 16);
+}
+// Router columns per W ring stage, fixed per engine (the W layout depends on
+// it): the largest multiple of 32 <= 256 whose ring fits 200 KB.  Long
+// stages matter: each stage boundary costs the chain a refill bubble
+// (measured: CH 64 -> 38 us, CH 256 -> 31 us at d 4096, E 16).
+int pick_route_chunk(const Dims& D) {
     int ch = kRouteCHMax;
-    auto bytes = [&](int c) {
-        return 128 + sizeof(double) * (size_t)D.d + (size_t)kRouteStages * D.E * ((size_t)c * 8 + 16);
-    };
-    while (ch > 32 && bytes(ch) > 200 * 1024) ch -= 32;
-    const size_t smem = bytes(ch);
+    while (ch > 32 && route_smem_bytes(D, ch) > 200 * 1024) ch -= 32;
+    return ch;
+}
+
+void launch_route(const Dims& D, const Cfg& C, const State& S, const void* q, cudaStream_t st) {
+    const size_t smem = route_smem_bytes(D, D.route_ch);
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_route, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int threads = ((D.E + 31) / 32) * 32 + 32;
-    launch_pdl(k_route, dim3(D.B), dim3(threads), smem, st, D, C, S, q, ch);
+    launch_pdl(k_route, dim3(D.B), dim3(threads), smem, st, D, C, S, q);
 }
 
 // page-record maintenance (see State::pr_*)
@@ -544,204 +570,314 @@ __device__ __forceinline__ void encode_row(const Dims& D, const State& S, const 
     }
 }
 
-__global__ void k_insert(Dims D, Cfg C, State S, const void* __restrict__ qin,
-                         const void* __restrict__ kin, const void* __restrict__ vin,
-                         const double* __restrict__ saliency) {
-    griddep_enter();
-    extern __shared__ __align__(16) uint8_t sm_entry[];  // [entry_bytes] + tmp floats [d]
+// KVStore::insert of stream s's k entries by the calling CTA (k_insert,
+// k_control); sm_entry = dynamic smem of insert_smem_bytes().  `sel` = the
+// step's experts in shared memory when the caller has them (k_control),
+// else they are read from S.experts.
+//
+// Bookkeeping runs on warp 0 only (lane j = selected expert j) while the
+// other warps stage the K/V row (identity codec) and the fp32 query.  When
+// the k entries hit k distinct rings (the common case) the lanes do their
+// KVStore::insert concurrently, loading everything first (ring head/seq,
+// then the head slot and both page records), so the chain is a few
+// independent load rounds; otherwise lane 0 runs them in order.
+// Entry ids are issued in selection order on every rank (kvstore.cpp:114).
+__device__ __forceinline__ void insert_book_seq(const Dims& D, const State& S, const int s, const int* sel,
+                                                const double* __restrict__ saliency, int64_t* sm_dst, int* sm_n) {
+    const uint64_t now = S.now[s];
+    const int64_t token = (int64_t)now;
+    int n = 0;
+    for (int j = 0; j < D.k; ++j) {
+        const int e = sel ? sel[j] : S.experts[(int64_t)s * D.k + j];
+        const int raw = shard_raw(token, e, D.n_tok, D.n_exp, D.additive);
+        const int dev = raw % D.G, sh = raw / D.G;
+        const uint64_t id = S.next_id[s]++;  // every rank issues every id
+        if (dev % D.world != D.rank) continue;
+        const int gl = dev / D.world;
+        const int64_t ring = ((int64_t)s * D.Gl + gl) * D.SPD + sh;
+        const int slot = S.head[ring];
+        const int64_t gi = ring * D.S + slot;
+        const int64_t pidx = ring * D.ppr + slot / D.spg;
+        int32_t page = S.page_table[pidx];
+        if (S.id[gi] != 0) {  // displaced (kvstore.cpp:41-43; pipeline.cpp:200-208)
+            rec_drop_front(D, S, ring, S.shard_seq[gi], S.last_access[gi], S.freq[gi]);
+            const int no = S.n_ow[s]++;
+            EvictRec& r = S.rec_ow[(int64_t)s * D.k + no];
+            r.step = now;
+            r.entry_id = S.id[gi];
+            r.token_id = S.token[gi];
+            r.expert_id = S.expert[gi];
+            r.device = dev;
+            r.score = 0.0;
+            r.reason = PIKV_EVICT_OVERWRITE;
+            r.stream = s;
+            S.st_overwrites[s] += 1;
+        } else {
+            S.live[ring] += 1;
+            if (page < 0) {
+                const int top = atomicSub(S.free_top, 1) - 1;
+                if (top < 0) {
+                    atomicAdd(S.free_top, 1);
+                    S.err[s] = PIKV_ERR_OUT_OF_MEMORY;
+                    break;
+                }
+                page = S.free_stack[top];
+                S.page_table[pidx] = page;
+                S.page_live[page] = 0;
+            }
+            S.page_live[page] += 1;
+        }
+        S.id[gi] = id;
+        rec_append(D, S, ring, S.seq[ring], now);
+        S.shard_seq[gi] = S.seq[ring]++;
+        S.token[gi] = token;
+        S.expert[gi] = e;
+        S.insert_step[gi] = now;
+        S.last_access[gi] = now;
+        S.freq[gi] = 0;
+        S.attn_mass[gi] = 0.0;
+        for (int l = 0; l < D.n_layers; ++l)
+            S.per_layer[gi * D.n_layers + l] = saliency ? saliency[(int64_t)s * D.n_layers + l] : 0.0;
+        S.head[ring] = (slot + 1) % D.S;
+        S.st_inserts[s] += 1;
+        sm_dst[n] = (int64_t)page * D.spg + slot % D.spg;
+        ++n;
+    }
+    *sm_n = n;
+}
+
+// Warp 0: the k inserts of stream s (see above).  Writes the pool entry
+// index of each stored entry (in id order) to sm_dst and their number to
+// *sm_n.
+__device__ __forceinline__ void insert_book(const Dims& D, const State& S, const int s, const int* sel,
+                                            const double* __restrict__ saliency, int64_t* sm_dst, int* sm_n) {
+    const int j = threadIdx.x & 31;
+    const uint64_t now = S.now[s];
+    const int64_t token = (int64_t)now;
+    // round A: expert -> ring (local rings only)
+    bool act = false;
+    int e = 0, dev = 0;
+    int64_t ring = -1 - j;
+    if (j < D.k) {
+        e = sel ? sel[j] : S.experts[(int64_t)s * D.k + j];
+        const int raw = shard_raw(token, e, D.n_tok, D.n_exp, D.additive);
+        dev = raw % D.G;
+        if (dev % D.world == D.rank) {
+            act = true;
+            ring = (int64_t)s * D.R + (dev / D.world) * D.SPD + raw / D.G;
+        }
+    }
+    bool distinct = D.k <= 32;
+    if (distinct) {
+        const unsigned m = __match_any_sync(0xffffffffu, ring);
+        distinct = __all_sync(0xffffffffu, !act || m == (1u << j));
+    }
+    if (!distinct) {
+        if (j == 0) insert_book_seq(D, S, s, sel, saliency, sm_dst, sm_n);
+        __syncwarp();
+        return;
+    }
+    // round B: ring state
+    int slot = 0;
+    uint64_t seq = 0, nid = 0;
+    if (act) {
+        slot = S.head[ring];
+        seq = S.seq[ring];
+    }
+    nid = S.next_id[s];
+    // round C: head slot (possibly displaced) and the append page record
+    const int64_t gi = ring * D.S + slot;
+    const int64_t pidx = ring * D.ppr + slot / D.spg;
+    const int64_t arec = act ? page_rec(D, ring, seq) : 0;
+    int32_t page = -1;
+    uint64_t old = 0, osq = 0, ola = 0, ofr = 0;
+    int64_t otok = 0;
+    int oex = 0, acnt = 0, afirst = 0;
+    uint64_t asla = 0, asf = 0;
+    if (act) {
+        page = S.page_table[pidx];
+        old = S.id[gi];
+        osq = S.shard_seq[gi];
+        ola = S.last_access[gi];
+        ofr = S.freq[gi];
+        otok = S.token[gi];
+        oex = S.expert[gi];
+        acnt = S.pr_cnt[arec];
+        afirst = S.pr_first[arec];
+        asla = S.pr_sla[arec];
+        asf = S.pr_sf[arec];
+    }
+    const bool disp = act && old != 0;
+    // round D: the displaced entry's page record (rec_drop_front)
+    int64_t drec = -1;
+    int dcnt = 0, dfirst = 0;
+    uint64_t dsla = 0, dsf = 0;
+    int pl_delta = 0;  // pages_live change of the ring's device
+    if (disp) {
+        drec = page_rec(D, ring, osq);
+        if (drec == arec) {
+            dcnt = acnt, dfirst = afirst, dsla = asla, dsf = asf;
+        } else {
+            dcnt = S.pr_cnt[drec];
+            dfirst = S.pr_first[drec];
+            dsla = S.pr_sla[drec];
+            dsf = S.pr_sf[drec];
+        }
+        if (--dcnt == 0) --pl_delta;  // last member displaced
+        dfirst += 1;
+        dsla -= ola;
+        dsf -= ofr;
+        if (drec == arec) acnt = dcnt, afirst = dfirst, asla = dsla, asf = dsf;
+    }
+    // page allocation for a fresh slot (pool free stack)
+    bool oom = false, fresh_page = false;
+    if (act && !disp && page < 0) {
+        const int top = atomicSub(S.free_top, 1) - 1;
+        if (top < 0) {
+            atomicAdd(S.free_top, 1);
+            oom = true;
+        } else {
+            page = S.free_stack[top];
+            fresh_page = true;
+        }
+    }
+    const bool ins = act && !oom;
+    // rec_append
+    if (ins) {
+        if (acnt == 0) {
+            ++pl_delta;  // a page comes to life
+            acnt = 1;
+            afirst = (int)(seq % (uint64_t)D.page_size);
+            asla = now;
+            asf = 0;
+        } else {
+            acnt += 1;
+            asla += now;
+        }
+    }
+    // stores
+    if (disp && drec != arec) {
+        S.pr_cnt[drec] = dcnt;
+        S.pr_first[drec] = dfirst;
+        S.pr_sla[drec] = dsla;
+        S.pr_sf[drec] = dsf;
+    }
+    if (ins || (disp && drec == arec)) {
+        S.pr_cnt[arec] = acnt;
+        S.pr_first[arec] = afirst;
+        S.pr_sla[arec] = asla;
+        S.pr_sf[arec] = asf;
+    }
+    if (pl_delta) atomicAdd(&S.pages_live[ring / D.SPD], pl_delta);
+    if (ins) {
+        if (!disp) {
+            atomicAdd(&S.live[ring], 1);
+            if (fresh_page) {
+                S.page_table[pidx] = page;
+                S.page_live[page] = 1;
+            } else {
+                atomicAdd(&S.page_live[page], 1);
+            }
+        }
+        S.id[gi] = nid + (uint64_t)j;
+        S.shard_seq[gi] = seq;
+        S.seq[ring] = seq + 1;
+        S.token[gi] = token;
+        S.expert[gi] = e;
+        S.insert_step[gi] = now;
+        S.last_access[gi] = now;
+        S.freq[gi] = 0;
+        S.attn_mass[gi] = 0.0;
+        for (int l = 0; l < D.n_layers; ++l)
+            S.per_layer[gi * D.n_layers + l] = saliency ? saliency[(int64_t)s * D.n_layers + l] : 0.0;
+        S.head[ring] = (slot + 1) % D.S;
+    }
+    const unsigned dm = __ballot_sync(0xffffffffu, disp);
+    const unsigned am = __ballot_sync(0xffffffffu, ins);
+    if (disp) {  // displaced (kvstore.cpp:41-43; pipeline.cpp:200-208)
+        EvictRec rec;
+        rec.step = now;
+        rec.entry_id = old;
+        rec.token_id = otok;
+        rec.expert_id = oex;
+        rec.device = dev;
+        rec.score = 0.0;
+        rec.reason = PIKV_EVICT_OVERWRITE;
+        rec.stream = s;
+        S.rec_ow[(int64_t)s * D.k + __popc(dm & ((1u << j) - 1u))] = rec;
+    }
+    if (ins) sm_dst[__popc(am & ((1u << j) - 1u))] = (int64_t)page * D.spg + slot % D.spg;
+    if (__any_sync(0xffffffffu, oom) && j == 0) S.err[s] = PIKV_ERR_OUT_OF_MEMORY;
+    if (j == 0) {
+        S.n_ow[s] = __popc(dm);
+        S.st_overwrites[s] += (uint64_t)__popc(dm);
+        S.st_inserts[s] += (uint64_t)__popc(am);
+        S.next_id[s] = nid + (uint64_t)D.k;
+        *sm_n = __popc(am);
+    }
+    __syncwarp();
+}
+
+__device__ __forceinline__ void insert_body(const Dims& D, const Cfg& C, const State& S, const int s,
+                                            const void* __restrict__ qin, const void* __restrict__ kin,
+                                            const void* __restrict__ vin,
+                                            const double* __restrict__ saliency, uint8_t* sm_entry,
+                                            const int* sel = nullptr) {
     __shared__ int64_t sm_dst[kMaxK];
-    __shared__ int64_t sm_slot[kMaxK];
     __shared__ int sm_n;
-    const int s = blockIdx.x, tid = threadIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5;
     if (S.err[s]) return;
     float* tmp = (float*)(sm_entry + ((D.entry_bytes + 15) & ~15));
     const int pay = D.payload_bytes;
-    float* ksc = (float*)(sm_entry + 2 * pay);
-    float* vsc = ksc + D.H;
-    encode_row(D, S, kin, s, sm_entry, ksc, tmp, 0);
-    encode_row(D, S, vin, s, sm_entry + pay, vsc, tmp, 1);
+    const int esz = D.kv_dtype == PIKV_DTYPE_BF16 ? 2 : 4;
+    const bool proj = D.codec == PIKV_CODEC_LOWRANK || D.codec == PIKV_CODEC_LORAPLUS ||
+                      D.codec == PIKV_CODEC_FASTV || D.codec == PIKV_CODEC_PRUNE;
     // the query in the stored (compressed) space, fp32 (pipeline.cpp:295-297)
-    {
+    auto query = [&](int t0, int nt) {
         const int hd = D.d / D.H, r = D.dph;
         const int64_t base = (int64_t)s * D.d;
         float* qa = S.q_attn + (int64_t)s * D.dp;
-        const bool proj = D.codec == PIKV_CODEC_LOWRANK || D.codec == PIKV_CODEC_LORAPLUS ||
-                          D.codec == PIKV_CODEC_FASTV || D.codec == PIKV_CODEC_PRUNE;
         if (!proj && D.kv_dtype == PIKV_DTYPE_BF16 && D.d % 8 == 0) {
             const uint4* src = (const uint4*)((const uint16_t*)qin + base);
-            for (int v = tid; v < D.d / 8; v += blockDim.x) {
+            for (int v = t0; v < D.d / 8; v += nt) {
                 const uint4 w = src[v];
                 float4* dq = (float4*)(qa + v * 8);
                 dq[0] = make_float4(bf16_lo(w.x), bf16_hi(w.x), bf16_lo(w.y), bf16_hi(w.y));
                 dq[1] = make_float4(bf16_lo(w.z), bf16_hi(w.z), bf16_lo(w.w), bf16_hi(w.w));
             }
         } else if (!proj) {
-            for (int o = tid; o < D.d; o += blockDim.x) qa[o] = load_in(qin, D.kv_dtype, base + o);
+            for (int o = t0; o < D.d; o += nt) qa[o] = load_in(qin, D.kv_dtype, base + o);
         } else if (D.codec == PIKV_CODEC_FASTV || D.codec == PIKV_CODEC_PRUNE) {
-            for (int o = tid; o < D.dp; o += blockDim.x) {
+            for (int o = t0; o < D.dp; o += nt) {
                 const int h = o / r, j = o % r;
                 const int i = D.codec == PIKV_CODEC_FASTV ? j : S.kept[h * r + j];
                 qa[o] = load_in(qin, D.kv_dtype, base + h * hd + i);
             }
         }  // LowRank / LoRAPlus: q_attn written by k_project
-    }
-    // Bookkeeping.  Entry ids are issued in selection order on every rank
-    // (kvstore.cpp:114).  When the k entries hit k distinct rings (the common
-    // case) lanes j < k do their KVStore::insert concurrently; otherwise
-    // thread 0 runs them in order.
-    __shared__ int sm_ring[kMaxK];
-    __shared__ int sm_distinct;
-    const uint64_t now = S.now[s];
-    const int64_t token = (int64_t)now;
-    if (tid < D.k) {
-        const int e = S.experts[(int64_t)s * D.k + tid];
-        const int raw = shard_raw(token, e, D.n_tok, D.n_exp, D.additive);
-        const int dev = raw % D.G;
-        sm_ring[tid] = dev % D.world == D.rank ? (dev / D.world) * D.SPD + raw / D.G : -1 - tid;
-    }
-    if (tid == 0) sm_distinct = 1;
-    __syncthreads();
-    if (tid < D.k)
-        for (int j2 = 0; j2 < tid; ++j2)
-            if (sm_ring[j2] == sm_ring[tid]) sm_distinct = 0;
-    __syncthreads();
-    if (sm_distinct && D.k <= 32) {
-        if (tid < 32) {
-            const int j = tid;
-            const bool act = j < D.k && sm_ring[j] >= 0;
-            bool disp = false;
-            int64_t gi = 0;
-            int32_t page = -1;
-            EvictRec rec{};
-            bool oom = false;
-            if (act) {
-                const int e = S.experts[(int64_t)s * D.k + j];
-                const int raw = shard_raw(token, e, D.n_tok, D.n_exp, D.additive);
-                const int dev = raw % D.G;
-                const int64_t ring = (int64_t)s * D.R + sm_ring[j];
-                const int slot = S.head[ring];
-                gi = ring * D.S + slot;
-                const int64_t pidx = ring * D.ppr + slot / D.spg;
-                page = S.page_table[pidx];
-                const uint64_t old = S.id[gi];
-                if (old != 0) {  // displaced (kvstore.cpp:41-43; pipeline.cpp:200-208)
-                    disp = true;
-                    rec_drop_front(D, S, ring, S.shard_seq[gi], S.last_access[gi], S.freq[gi]);
-                    rec.step = now;
-                    rec.entry_id = old;
-                    rec.token_id = S.token[gi];
-                    rec.expert_id = S.expert[gi];
-                    rec.device = dev;
-                    rec.score = 0.0;
-                    rec.reason = PIKV_EVICT_OVERWRITE;
-                    rec.stream = s;
-                } else {
-                    S.live[ring] += 1;
-                    if (page < 0) {
-                        const int top = atomicSub(S.free_top, 1) - 1;
-                        if (top < 0) {
-                            atomicAdd(S.free_top, 1);
-                            oom = true;
-                        } else {
-                            page = S.free_stack[top];
-                            S.page_table[pidx] = page;
-                            S.page_live[page] = 0;
-                        }
-                    }
-                    if (!oom) S.page_live[page] += 1;
-                }
-                if (!oom) {
-                    S.id[gi] = S.next_id[s] + (uint64_t)j;
-                    rec_append(D, S, ring, S.seq[ring], now);
-                    S.shard_seq[gi] = S.seq[ring]++;
-                    S.token[gi] = token;
-                    S.expert[gi] = e;
-                    S.insert_step[gi] = now;
-                    S.last_access[gi] = now;
-                    S.freq[gi] = 0;
-                    S.attn_mass[gi] = 0.0;
-                    for (int l = 0; l < D.n_layers; ++l)
-                        S.per_layer[gi * D.n_layers + l] = saliency ? saliency[(int64_t)s * D.n_layers + l] : 0.0;
-                    S.head[ring] = (slot + 1) % D.S;
-                }
+    };
+    const bool overlap = D.codec == PIKV_CODEC_IDENTITY && (D.d * esz) % 16 == 0 && blockDim.x >= 64;
+    if (overlap) {
+        // warp 0: bookkeeping; warps 1..: K/V rows -> smem entry, query
+        if (warp == 0) {
+            insert_book(D, S, s, sel, saliency, sm_dst, &sm_n);
+        } else {
+            const int t0 = tid - 32, nt = blockDim.x - 32;
+            const int nv = D.d * esz / 16;
+            const uint4* ks = (const uint4*)((const uint8_t*)kin + (int64_t)s * D.d * esz);
+            const uint4* vs = (const uint4*)((const uint8_t*)vin + (int64_t)s * D.d * esz);
+            for (int i = t0; i < nv; i += nt) {
+                ((uint4*)sm_entry)[i] = ks[i];
+                ((uint4*)(sm_entry + pay))[i] = vs[i];
             }
-            const unsigned dm = __ballot_sync(0xffffffffu, disp);
-            const unsigned am = __ballot_sync(0xffffffffu, act && !oom);
-            if (__any_sync(0xffffffffu, oom) && j == 0) S.err[s] = PIKV_ERR_OUT_OF_MEMORY;
-            if (disp) S.rec_ow[(int64_t)s * D.k + __popc(dm & ((1u << j) - 1u))] = rec;
-            if (act && !oom) {
-                const int pos = __popc(am & ((1u << j) - 1u));
-                sm_dst[pos] = (int64_t)page * D.spg + (gi % D.S) % D.spg;
-                sm_slot[pos] = gi;
-            }
-            if (j == 0) {
-                S.n_ow[s] = __popc(dm);
-                S.st_overwrites[s] += (uint64_t)__popc(dm);
-                S.st_inserts[s] += (uint64_t)__popc(am);
-                S.next_id[s] += (uint64_t)D.k;
-                sm_n = __popc(am);
-            }
+            query(t0, nt);
         }
-    } else     if (tid == 0) {
-        int n = 0;
-        for (int j = 0; j < D.k; ++j) {
-            const int e = S.experts[(int64_t)s * D.k + j];
-            const int raw = shard_raw(token, e, D.n_tok, D.n_exp, D.additive);
-            const int dev = raw % D.G, sh = raw / D.G;
-            const uint64_t id = S.next_id[s]++;  // every rank issues every id
-            if (dev % D.world != D.rank) continue;
-            const int gl = dev / D.world;
-            const int64_t ring = ((int64_t)s * D.Gl + gl) * D.SPD + sh;
-            const int slot = S.head[ring];
-            const int64_t gi = ring * D.S + slot;
-            const int64_t pidx = ring * D.ppr + slot / D.spg;
-            int32_t page = S.page_table[pidx];
-            if (S.id[gi] != 0) {  // displaced (kvstore.cpp:41-43; pipeline.cpp:200-208)
-                rec_drop_front(D, S, ring, S.shard_seq[gi], S.last_access[gi], S.freq[gi]);
-                const int no = S.n_ow[s]++;
-                EvictRec& r = S.rec_ow[(int64_t)s * D.k + no];
-                r.step = now;
-                r.entry_id = S.id[gi];
-                r.token_id = S.token[gi];
-                r.expert_id = S.expert[gi];
-                r.device = dev;
-                r.score = 0.0;
-                r.reason = PIKV_EVICT_OVERWRITE;
-                r.stream = s;
-                S.st_overwrites[s] += 1;
-            } else {
-                S.live[ring] += 1;
-                if (page < 0) {
-                    const int top = atomicSub(S.free_top, 1) - 1;
-                    if (top < 0) {
-                        atomicAdd(S.free_top, 1);
-                        S.err[s] = PIKV_ERR_OUT_OF_MEMORY;
-                        break;
-                    }
-                    page = S.free_stack[top];
-                    S.page_table[pidx] = page;
-                    S.page_live[page] = 0;
-                }
-                S.page_live[page] += 1;
-            }
-            S.id[gi] = id;
-            rec_append(D, S, ring, S.seq[ring], now);
-            S.shard_seq[gi] = S.seq[ring]++;
-            S.token[gi] = token;
-            S.expert[gi] = e;
-            S.insert_step[gi] = now;
-            S.last_access[gi] = now;
-            S.freq[gi] = 0;
-            S.attn_mass[gi] = 0.0;
-            for (int l = 0; l < D.n_layers; ++l)
-                S.per_layer[gi * D.n_layers + l] = saliency ? saliency[(int64_t)s * D.n_layers + l] : 0.0;
-            S.head[ring] = (slot + 1) % D.S;
-            S.st_inserts[s] += 1;
-            sm_dst[n] = (int64_t)page * D.spg + slot % D.spg;
-            sm_slot[n] = gi;
-            ++n;
-        }
-        sm_n = n;
+    } else {
+        float* ksc = (float*)(sm_entry + 2 * pay);
+        float* vsc = ksc + D.H;
+        encode_row(D, S, kin, s, sm_entry, ksc, tmp, 0);
+        encode_row(D, S, vin, s, sm_entry + pay, vsc, tmp, 1);
+        query(tid, blockDim.x);
+        if (warp == 0) insert_book(D, S, s, sel, saliency, sm_dst, &sm_n);
     }
     __syncthreads();
     const int n = sm_n;
@@ -753,9 +889,21 @@ __global__ void k_insert(Dims D, Cfg C, State S, const void* __restrict__ qin,
     }
 }
 
+__global__ void k_insert(Dims D, Cfg C, State S, const void* __restrict__ qin,
+                         const void* __restrict__ kin, const void* __restrict__ vin,
+                         const double* __restrict__ saliency) {
+    griddep_enter();
+    extern __shared__ __align__(16) uint8_t sm_entry[];  // [entry_bytes] + tmp floats [d]
+    insert_body(D, C, S, blockIdx.x, qin, kin, vin, saliency, sm_entry);
+}
+
+static size_t insert_smem_bytes(const Dims& D) {
+    return (size_t)((D.entry_bytes + 15) & ~15) + sizeof(float) * (size_t)D.d;
+}
+
 void launch_insert(const Dims& D, const Cfg& C, const State& S, const void* q, const void* k,
                    const void* v, const double* saliency, cudaStream_t st) {
-    size_t smem = (size_t)((D.entry_bytes + 15) & ~15) + sizeof(float) * (size_t)D.d;
+    size_t smem = insert_smem_bytes(D);
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_insert, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     launch_pdl(k_insert, dim3(D.B), dim3(256), smem, st, D, C, S, q, k, v, saliency);
 }
@@ -771,6 +919,29 @@ void launch_insert(const Dims& D, const Cfg& C, const State& S, const void* q, c
 //     dyadic below 2^53).  Other strategies score the live member range: lane u
 //     takes the u-th member in slot order (scheduler.cpp:276-289), lane 0 sums
 //     in that order (or a tree sum when exact in any order).
+// Key of candidate page pi of `ring` from its page record (record_agg
+// strategies): live count, exact aggregate, oldest (= first member's) id.
+__device__ __forceinline__ int page_key_rec(const Dims& D, const Cfg& C, const State& S, const int64_t ring,
+                                            const int pi, const uint64_t now, double& agg, uint64_t& oldest) {
+    const uint64_t seq = S.seq[ring];
+    const uint64_t Su = (uint64_t)D.S, ps = (uint64_t)D.page_size;
+    const uint64_t lo = seq > Su ? seq - Su : 0;
+    const uint64_t q = lo / ps + (uint64_t)pi;
+    const int64_t rec = ring * D.ppr_sched + (int64_t)(q % (uint64_t)D.ppr_sched);
+    const int cnt = q * ps < seq ? S.pr_cnt[rec] : 0;
+    agg = 0.0;
+    oldest = 0;
+    if (cnt > 0) {
+        const int first = S.pr_first[rec];
+        const uint64_t sla = S.pr_sla[rec];
+        agg = -(double)((uint64_t)cnt * now - sla);
+        if (C.sched_strategy == PIKV_SCHED_LRU_PLUS)
+            agg = __dadd_rn(agg, __dmul_rn(C.lambda_freq, (double)S.pr_sf[rec]));
+        oldest = S.id[ring * D.S + (int64_t)((q * ps + (uint64_t)first) % Su)];
+    }
+    return cnt;
+}
+
 __global__ void k_sched_pages(Dims D, Cfg C, State S, int lanes) {
     griddep_enter();
     const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -792,26 +963,17 @@ __global__ void k_sched_pages(Dims D, Cfg C, State S, int lanes) {
         // devices within budget evict nothing: select decides from the
         // live-page counter and never reads their keys
         if (!in || S.pages_live[ring / D.SPD] <= C.budget_pages) return;
-    }
-    const int cnt = (in && q * ps < seq) ? S.pr_cnt[rec] : 0;
-    const bool live_page = cnt > 0 && !S.err[s];
-    const uint64_t now = in ? S.now[s] : 0;
-    if (C.record_agg) {
         double agg = 0.0;
         uint64_t oldest = 0;
-        if (live_page) {
-            const int first = S.pr_first[rec];
-            const uint64_t sla = S.pr_sla[rec];
-            agg = -(double)((uint64_t)cnt * now - sla);
-            if (C.sched_strategy == PIKV_SCHED_LRU_PLUS)
-                agg = __dadd_rn(agg, __dmul_rn(C.lambda_freq, (double)S.pr_sf[rec]));
-            oldest = S.id[ring * D.S + (int64_t)((q * ps + (uint64_t)first) % Su)];
-        }
-        S.pg_cnt[t] = live_page ? cnt : 0;
+        const int c2 = S.err[s] ? 0 : page_key_rec(D, C, S, ring, pi, S.now[s], agg, oldest);
+        S.pg_cnt[t] = c2;
         S.pg_agg[t] = agg;
         S.pg_oldest[t] = oldest;
         return;
     }
+    const int cnt = (in && q * ps < seq) ? S.pr_cnt[rec] : 0;
+    const bool live_page = cnt > 0 && !S.err[s];
+    const uint64_t now = in ? S.now[s] : 0;
     const int first = live_page ? S.pr_first[rec] : 0;
     const uint64_t s0 = (q * ps) % Su;
     const int w = (s0 + ps > Su) ? (int)(Su - s0) : 0;  // offsets wrapping to slot 0 come first
@@ -862,148 +1024,156 @@ __device__ __forceinline__ bool page_less(double a, uint64_t oa, double b, uint6
 }
 
 // (b) one CTA per (stream, local device): select_evictions + erase.
+// Block-size generic (k_sched_select: 1024 threads, k_control: 512).
 constexpr int kSelThreads = 1024;
-__device__ __forceinline__ void select_body(const Dims& D, const Cfg& C, const State& S, const int sg,
-                                            const bool stage) {
-    const int s = sg / D.Gl, gl = sg % D.Gl;
-    const int tid = threadIdx.x;
+
+// Erase scheduler page `pidx` of device sg (scheduler.cpp:305-326) with one
+// warp: lanes over its members in id (= shard_seq) order, records from
+// rec + o.  Returns the member count (lane 0's value is authoritative).
+__device__ __forceinline__ int erase_page_warp(const Dims& D, const Cfg& C, const State& S, const int sg,
+                                               const int pidx, const int reason, int o) {
+    const int s = sg / D.Gl, gl = sg % D.Gl, lane = threadIdx.x & 31;
+    const int64_t ring = (int64_t)sg * D.SPD + pidx / D.ppr_sched;
+    const uint64_t seq = S.seq[ring];
+    const uint64_t Su = (uint64_t)D.S, ps = (uint64_t)D.page_size;
+    const uint64_t lo = seq > Su ? seq - Su : 0;
+    const uint64_t q = lo / ps + (uint64_t)(pidx % D.ppr_sched);
+    const uint64_t sstep = S.sstep[s], now = S.now[s];
+    const int dev = gl * D.world + D.rank;
+    EvictRec* rec = S.rec_ev + (int64_t)sg * D.SPD * D.S;
+    const int o0 = o;
+    for (uint64_t b0 = 0; b0 < ps; b0 += 32) {
+        const uint64_t sq = q * ps + b0 + lane;
+        bool mem = false;
+        int64_t gi = 0;
+        if (b0 + lane < ps) {
+            gi = ring * D.S + (int64_t)(sq % Su);
+            mem = S.id[gi] != 0 && S.shard_seq[gi] == sq;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, mem);
+        if (mem) {
+            EvictRec& r = rec[o + __popc(bal & ((1u << lane) - 1u))];
+            r.step = sstep;
+            r.entry_id = S.id[gi];
+            r.token_id = S.token[gi];
+            r.expert_id = S.expert[gi];
+            r.device = dev;
+            r.score = score_entry(C, S, gi, now, D.n_layers);
+            r.reason = reason;
+            r.stream = s;
+            // KVStore::erase (kvstore.cpp:180-185) + page reclamation
+            S.id[gi] = 0;
+            atomicSub(&S.live[ring], 1);
+            const int slot = (int)(sq % Su);
+            const int64_t pt_i = ring * D.ppr + slot / D.spg;
+            const int32_t page = S.page_table[pt_i];
+            if (atomicSub(&S.page_live[page], 1) == 1) {
+                S.page_table[pt_i] = -1;
+                const int top = atomicAdd(S.free_top, 1);
+                S.free_stack[top] = page;
+            }
+        }
+        o += __popc(bal);
+    }
+    if (lane == 0) {  // the page is gone: reset its record
+        const int64_t r = ring * D.ppr_sched + (int64_t)(q % (uint64_t)D.ppr_sched);
+        if (S.pr_cnt[r] > 0) atomicSub(&S.pages_live[sg], 1);
+        S.pr_cnt[r] = 0;
+        S.pr_first[r] = 0;
+        S.pr_sla[r] = 0;
+        S.pr_sf[r] = 0;
+    }
+    return o - o0;
+}
+
+// Page count P, below-theta count T and the (aggregate, oldest) argmin over
+// the pages i = first + tid + j * step (< np) of one device; the block's
+// result lands in *out (shared memory), visible to all threads on return.
+struct PageBest {
+    int P, T, I;
+    double A;
+    uint64_t O;
+};
+__device__ __forceinline__ void merge_best(PageBest& a, const PageBest& b) {
+    a.P += b.P;
+    a.T += b.T;
+    if (b.I >= 0 && (a.I < 0 || page_less(b.A, b.O, a.A, a.O))) a.A = b.A, a.O = b.O, a.I = b.I;
+}
+template <class KeyFn>
+__device__ __forceinline__ void block_page_scan(const int np, const int first, const int step, KeyFn key,
+                                                const double th, const bool ut, PageBest* out) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NW = blockDim.x >> 5;
+    PageBest b{0, 0, -1, 0.0, 0};
+#pragma unroll 4
+    for (int i = first + tid; i < np; i += step) {
+        double a2;
+        uint64_t o2;
+        if (key(i, a2, o2) <= 0) continue;
+        ++b.P;
+        if (ut && a2 < th) ++b.T;
+        if (b.I < 0 || page_less(a2, o2, b.A, b.O)) b.A = a2, b.O = o2, b.I = i;
+    }
+    __shared__ PageBest wb[32];
+    for (int off = 16; off; off >>= 1) {
+        PageBest o;
+        o.P = __shfl_xor_sync(0xffffffffu, b.P, off);
+        o.T = __shfl_xor_sync(0xffffffffu, b.T, off);
+        o.A = __shfl_xor_sync(0xffffffffu, b.A, off);
+        o.O = __shfl_xor_sync(0xffffffffu, b.O, off);
+        o.I = __shfl_xor_sync(0xffffffffu, b.I, off);
+        merge_best(b, o);
+    }
+    if (lane == 0) wb[warp] = b;
+    __syncthreads();
+    if (tid == 0) {
+        PageBest r = wb[0];
+        for (int w = 1; w < NW; ++w) merge_best(r, wb[w]);
+        *out = r;
+    }
+    __syncthreads();
+}
+
+// select_evictions' count (scheduler.cpp:246-259) from the device's totals;
+// records pages_before/after.  One thread.
+__device__ __forceinline__ int decide_victims(const Cfg& C, const State& S, const int sg, const PageBest& b) {
+    const int V0 = max(b.T, max(b.P - C.budget_pages, 0));
+    S.pages_before[sg] = b.P;
+    S.pages_after[sg] = b.P - V0;
+    S.n_ev[sg] = 0;
+    return V0;
+}
+
+// Fast path (the common steady state evicts 0 or 1 page): one pass over the
+// page keys (key(i, agg, oldest) -> live count) computes P, T and the argmin;
+// a single victim is erased directly.  Returns V (uniform); V > 1 is left to
+// select_general.
+template <class KeyFn>
+__device__ __forceinline__ int select_fast(const Dims& D, const Cfg& C, const State& S, const int sg,
+                                           KeyFn key) {
+    const int s = sg / D.Gl;
+    __shared__ PageBest sb;
+    __shared__ int sV;
+    block_page_scan(D.SPD * D.ppr_sched, 0, blockDim.x, key, S.theta[s],
+                    C.sched_strategy == PIKV_SCHED_ADAKV, &sb);
+    if (threadIdx.x == 0) sV = decide_victims(C, S, sg, sb);
+    __syncthreads();
+    const int V0 = sV;
+    if (V0 == 1 && threadIdx.x < 32) {
+        const int n = erase_page_warp(D, C, S, sg, sb.I, sb.T >= 1 ? PIKV_EVICT_THRESHOLD : PIKV_EVICT_BUDGET, 0);
+        if (threadIdx.x == 0) S.n_ev[sg] = n;
+    }
+    return V0;
+}
+
+// General path (V > 1): recount from the materialised page keys (pg_*),
+// select V victims (argmin rounds for V <= 32, bitonic sort otherwise) and
+// erase them in order, a warp per victim page.
+__device__ __forceinline__ void select_general(const Dims& D, const Cfg& C, const State& S, const int sg,
+                                               const bool stage) {
+    const int s = sg / D.Gl;
+    const int tid = threadIdx.x, NT = blockDim.x, NW = NT / 32;
     __shared__ int sm_red[32];
     __shared__ int sm_P, sm_thr, sm_V;
-    __shared__ double sm_ba;
-    __shared__ uint64_t sm_bo;
-    __shared__ int sm_bi;
-    if (S.err[s]) return;
-    if (C.record_agg && S.pages_live[sg] <= C.budget_pages) {  // P <= K: nothing to evict
-        if (tid == 0) {
-            const int P = S.pages_live[sg];
-            S.pages_before[sg] = P;
-            S.pages_after[sg] = P;
-            S.n_ev[sg] = 0;
-        }
-        return;
-    }
-    // ---- fast path (the common steady state evicts 0 or 1 page): one pass
-    // over the page keys computes P, the below-theta count T and the argmin;
-    // one two-level reduction; a single victim is erased directly.
-    {
-        const int64_t f0 = (int64_t)sg * D.SPD * D.ppr_sched;
-        const int np = D.SPD * D.ppr_sched;
-        const double th = S.theta[s];
-        const bool ut = C.sched_strategy == PIKV_SCHED_ADAKV;
-        int P = 0, T = 0, bi = -1;
-        double ba = 0.0;
-        uint64_t bo = 0;
-#pragma unroll 4
-        for (int i = tid; i < np; i += kSelThreads) {
-            const int c = S.pg_cnt[f0 + i];
-            if (c <= 0) continue;
-            const double a2 = S.pg_agg[f0 + i];
-            const uint64_t o2 = S.pg_oldest[f0 + i];
-            ++P;
-            if (ut && a2 < th) ++T;
-            if (bi < 0 || page_less(a2, o2, ba, bo)) ba = a2, bo = o2, bi = i;
-        }
-        __shared__ int fP[32], fT[32], fI[32];
-        __shared__ double fA[32];
-        __shared__ uint64_t fO[32];
-        __shared__ int fV, fBest, fThr, fPall;
-        const int lane = tid & 31, warp = tid >> 5;
-        for (int off = 16; off; off >>= 1) {
-            P += __shfl_xor_sync(0xffffffffu, P, off);
-            T += __shfl_xor_sync(0xffffffffu, T, off);
-            const double a3 = __shfl_xor_sync(0xffffffffu, ba, off);
-            const uint64_t o3 = __shfl_xor_sync(0xffffffffu, bo, off);
-            const int i3 = __shfl_xor_sync(0xffffffffu, bi, off);
-            if (i3 >= 0 && (bi < 0 || page_less(a3, o3, ba, bo))) ba = a3, bo = o3, bi = i3;
-        }
-        if (lane == 0) fP[warp] = P, fT[warp] = T, fA[warp] = ba, fO[warp] = bo, fI[warp] = bi;
-        __syncthreads();
-        if (warp == 0) {
-            const int nw = kSelThreads / 32;
-            P = lane < nw ? fP[lane] : 0;
-            T = lane < nw ? fT[lane] : 0;
-            ba = lane < nw ? fA[lane] : 0.0;
-            bo = lane < nw ? fO[lane] : 0;
-            bi = lane < nw ? fI[lane] : -1;
-            for (int off = 16; off; off >>= 1) {
-                P += __shfl_xor_sync(0xffffffffu, P, off);
-                T += __shfl_xor_sync(0xffffffffu, T, off);
-                const double a3 = __shfl_xor_sync(0xffffffffu, ba, off);
-                const uint64_t o3 = __shfl_xor_sync(0xffffffffu, bo, off);
-                const int i3 = __shfl_xor_sync(0xffffffffu, bi, off);
-                if (i3 >= 0 && (bi < 0 || page_less(a3, o3, ba, bo))) ba = a3, bo = o3, bi = i3;
-            }
-            if (lane == 0) {
-                const int V0 = max(T, max(P - C.budget_pages, 0));  // scheduler.cpp:246-259
-                fV = V0, fBest = bi, fThr = T, fPall = P;
-                S.pages_before[sg] = P;
-                S.pages_after[sg] = P - V0;
-                S.n_ev[sg] = 0;
-            }
-        }
-        __syncthreads();
-        const int V0 = fV;
-        if (V0 == 0) return;
-        if (V0 == 1) {
-            if (warp == 0) {
-                const int pidx = fBest;
-                const int reason = fThr >= 1 ? PIKV_EVICT_THRESHOLD : PIKV_EVICT_BUDGET;
-                const int64_t ring = (int64_t)sg * D.SPD + pidx / D.ppr_sched;
-                const uint64_t seq = S.seq[ring];
-                const uint64_t Su = (uint64_t)D.S, ps = (uint64_t)D.page_size;
-                const uint64_t lo = seq > Su ? seq - Su : 0;
-                const uint64_t q = lo / ps + (uint64_t)(pidx % D.ppr_sched);
-                const uint64_t sstep = S.sstep[s], now = S.now[s];
-                const int dev = gl * D.world + D.rank;
-                EvictRec* rec = S.rec_ev + (int64_t)sg * D.SPD * D.S;
-                int o = 0;
-                for (uint64_t b0 = 0; b0 < ps; b0 += 32) {
-                    const uint64_t sq = q * ps + b0 + lane;
-                    bool mem = false;
-                    int64_t gi = 0;
-                    if (b0 + lane < ps) {
-                        gi = ring * D.S + (int64_t)(sq % Su);
-                        mem = S.id[gi] != 0 && S.shard_seq[gi] == sq;
-                    }
-                    const unsigned bal = __ballot_sync(0xffffffffu, mem);
-                    if (mem) {
-                        EvictRec& r = rec[o + __popc(bal & ((1u << lane) - 1u))];
-                        r.step = sstep;
-                        r.entry_id = S.id[gi];
-                        r.token_id = S.token[gi];
-                        r.expert_id = S.expert[gi];
-                        r.device = dev;
-                        r.score = score_entry(C, S, gi, now, D.n_layers);
-                        r.reason = reason;
-                        r.stream = s;
-                        S.id[gi] = 0;  // KVStore::erase, kvstore.cpp:180-185
-                        atomicSub(&S.live[ring], 1);
-                        const int slot = (int)(sq % Su);
-                        const int64_t pt_i = ring * D.ppr + slot / D.spg;
-                        const int32_t page = S.page_table[pt_i];
-                        if (atomicSub(&S.page_live[page], 1) == 1) {
-                            S.page_table[pt_i] = -1;
-                            const int top = atomicAdd(S.free_top, 1);
-                            S.free_stack[top] = page;
-                        }
-                    }
-                    o += __popc(bal);
-                }
-                if (lane == 0) {
-                    const int64_t r = ring * D.ppr_sched + (int64_t)(q % (uint64_t)D.ppr_sched);
-                    if (S.pr_cnt[r] > 0) atomicSub(&S.pages_live[sg], 1);
-                    S.pr_cnt[r] = 0;
-                    S.pr_first[r] = 0;
-                    S.pr_sla[r] = 0;
-                    S.pr_sf[r] = 0;
-                    S.n_ev[sg] = o;
-                }
-            }
-            return;
-        }
-        (void)fPall;
-        __syncthreads();  // V > 1: general path below recomputes from the keys
-    }
     const int64_t first0 = (int64_t)sg * D.SPD * D.ppr_sched;  // pages of this device
     const int npg = D.SPD * D.ppr_sched;
     // page keys of this device: staged in shared memory when they fit (every
@@ -1017,7 +1187,7 @@ __device__ __forceinline__ void select_body(const Dims& D, const Cfg& C, const S
         uint64_t* o2 = (uint64_t*)(a2 + npg);
         int32_t* c2 = (int32_t*)(o2 + npg);
 #pragma unroll 4
-        for (int i = tid; i < npg; i += kSelThreads) {
+        for (int i = tid; i < npg; i += NT) {
             a2[i] = KA[i];
             o2[i] = KO[i];
             c2[i] = KC[i];
@@ -1025,28 +1195,27 @@ __device__ __forceinline__ void select_body(const Dims& D, const Cfg& C, const S
         __syncthreads();
         KA = a2, KO = o2, KC = c2;
     }
-    const int64_t first = 0;
     int32_t* list = S.sel_idx + (int64_t)sg * D.sel_stride;
     const double theta = S.theta[s];
     const bool use_theta = C.sched_strategy == PIKV_SCHED_ADAKV;
     // count pages and below-theta pages
     int P = 0, T = 0;
 #pragma unroll 4
-    for (int i = tid; i < npg; i += kSelThreads) {
-        if (KC[first + i] > 0) {
+    for (int i = tid; i < npg; i += NT) {
+        if (KC[i] > 0) {
             ++P;
-            if (use_theta && KA[first + i] < theta) ++T;
+            if (use_theta && KA[i] < theta) ++T;
         }
     }
     for (int off = 16; off; off >>= 1) {
         P += __shfl_xor_sync(0xffffffffu, P, off);
         T += __shfl_xor_sync(0xffffffffu, T, off);
     }
-    if ((tid & 31) == 0) sm_red[tid >> 5] = P | 0;
+    if ((tid & 31) == 0) sm_red[tid >> 5] = P;
     __syncthreads();
     if (tid == 0) {
         int p = 0;
-        for (int w = 0; w < kSelThreads / 32; ++w) p += sm_red[w];
+        for (int w = 0; w < NW; ++w) p += sm_red[w];
         sm_P = p;
     }
     __syncthreads();
@@ -1054,7 +1223,7 @@ __device__ __forceinline__ void select_body(const Dims& D, const Cfg& C, const S
     __syncthreads();
     if (tid == 0) {
         int t = 0;
-        for (int w = 0; w < kSelThreads / 32; ++w) t += sm_red[w];
+        for (int w = 0; w < NW; ++w) t += sm_red[w];
         sm_thr = t;
         const int over = sm_P - C.budget_pages;
         sm_V = max(t, max(over, 0));  // select_evictions, scheduler.cpp:246-259
@@ -1072,10 +1241,10 @@ __device__ __forceinline__ void select_body(const Dims& D, const Cfg& C, const S
             uint64_t bo = 0;
             int bi = -1;
 #pragma unroll 4
-            for (int i = tid; i < npg; i += kSelThreads) {
-                if (KC[first + i] <= 0) continue;
-                const double a = KA[first + i];
-                const uint64_t o = KO[first + i];
+            for (int i = tid; i < npg; i += NT) {
+                if (KC[i] <= 0) continue;
+                const double a = KA[i];
+                const uint64_t o = KO[i];
                 if (bi < 0 || page_less(a, o, ba, bo)) ba = a, bo = o, bi = i;
             }
             for (int off = 16; off; off >>= 1) {
@@ -1093,11 +1262,11 @@ __device__ __forceinline__ void select_body(const Dims& D, const Cfg& C, const S
                 int b = -1;
                 double a = 0.0;
                 uint64_t o = 0;
-                for (int w = 0; w < kSelThreads / 32; ++w) {
+                for (int w = 0; w < NW; ++w) {
                     if (wi[w] >= 0 && (b < 0 || page_less(wa[w], wo[w], a, o))) a = wa[w], o = wo[w], b = wi[w];
                 }
                 list[v] = b;
-                KC[first + b] = -KC[first + b];  // mark taken (negative count)
+                KC[b] = -KC[b];  // mark taken (negative count)
             }
             __syncthreads();
         }
@@ -1106,18 +1275,16 @@ __device__ __forceinline__ void select_body(const Dims& D, const Cfg& C, const S
         // scratch list (power-of-two capacity D.sel_stride; -1 sorts last),
         // then take the first V.
         const int n2 = D.sel_stride;
-        for (int i = tid; i < n2; i += kSelThreads)
-            list[i] = (i < npg && KC[first + i] > 0) ? i : -1;
+        for (int i = tid; i < n2; i += NT) list[i] = (i < npg && KC[i] > 0) ? i : -1;
         __syncthreads();
         auto key_less = [&](int a, int b) {
             if (a < 0) return false;
             if (b < 0) return true;
-            return page_less(KA[first + a], KO[first + a], KA[first + b],
-                             KO[first + b]);
+            return page_less(KA[a], KO[a], KA[b], KO[b]);
         };
         for (int kk = 2; kk <= n2; kk <<= 1) {
             for (int j = kk >> 1; j > 0; j >>= 1) {
-                for (int i = tid; i < n2; i += kSelThreads) {
+                for (int i = tid; i < n2; i += NT) {
                     const int ixj = i ^ j;
                     if (ixj > i) {
                         const int a = list[i], b = list[ixj];
@@ -1131,25 +1298,20 @@ __device__ __forceinline__ void select_body(const Dims& D, const Cfg& C, const S
                 __syncthreads();
             }
         }
-        for (int v = tid; v < V; v += kSelThreads) KC[first + list[v]] = -KC[first + list[v]];
+        for (int v = tid; v < V; v += NT) KC[list[v]] = -KC[list[v]];
         __syncthreads();
     }
-    // erase victims in order (scheduler.cpp:305-326): a warp per victim page,
-    // lanes over its members in id (= shard_seq) order; record offsets are the
-    // exclusive prefix of member counts over victims (block scan) plus the
-    // ballot rank inside the page.
+    // erase victims in order (scheduler.cpp:305-326): a warp per victim page;
+    // record offsets are the exclusive prefix of member counts over victims
+    // (block scan) plus the ballot rank inside the page.
     __shared__ int sm_off;
     __shared__ int vcnt_off[kSelThreads];
     if (tid == 0) sm_off = 0;
     __syncthreads();
-    const uint64_t sstep = S.sstep[s];
-    const uint64_t now = S.now[s];
-    const int dev = gl * D.world + D.rank;
-    EvictRec* rec = S.rec_ev + (int64_t)sg * D.SPD * D.S;
     const int lane = tid & 31, warp = tid >> 5;
-    for (int v0 = 0; v0 < V; v0 += kSelThreads) {
+    for (int v0 = 0; v0 < V; v0 += NT) {
         const int v = v0 + tid;
-        const int cnt = v < V ? -KC[first + list[v]] : 0;
+        const int cnt = v < V ? -KC[list[v]] : 0;
         int x = cnt;
         for (int off = 1; off < 32; off <<= 1) {
             int y = __shfl_up_sync(0xffffffffu, x, off);
@@ -1159,7 +1321,7 @@ __device__ __forceinline__ void select_body(const Dims& D, const Cfg& C, const S
         if (lane == 31) wsum[warp] = x;
         __syncthreads();
         if (tid < 32) {
-            int w = wsum[tid];
+            int w = tid < NW ? wsum[tid] : 0;
             for (int off = 1; off < 32; off <<= 1) {
                 int y = __shfl_up_sync(0xffffffffu, w, off);
                 if (tid >= off) w += y;
@@ -1169,63 +1331,92 @@ __device__ __forceinline__ void select_body(const Dims& D, const Cfg& C, const S
         __syncthreads();
         vcnt_off[tid] = x - cnt + (warp ? wsum[warp - 1] : 0) + sm_off;
         __syncthreads();
-        const int nv = min(kSelThreads, V - v0);
-        for (int vv = warp; vv < nv; vv += kSelThreads / 32) {
-            const int pidx = list[v0 + vv];
+        const int nv = min(NT, V - v0);
+        for (int vv = warp; vv < nv; vv += NW) {
             const int reason = (v0 + vv) < sm_thr ? PIKV_EVICT_THRESHOLD : PIKV_EVICT_BUDGET;
-            const int64_t ring = (int64_t)sg * D.SPD + pidx / D.ppr_sched;
-            const uint64_t seq = S.seq[ring];
-            const uint64_t Su = (uint64_t)D.S, ps = (uint64_t)D.page_size;
-            const uint64_t lo = seq > Su ? seq - Su : 0;
-            const uint64_t q = lo / ps + (uint64_t)(pidx % D.ppr_sched);
-            int o = vcnt_off[vv];
-            for (uint64_t b = 0; b < ps; b += 32) {
-                const uint64_t sq = q * ps + b + lane;
-                bool mem = false;
-                int64_t gi = 0;
-                if (b + lane < ps) {
-                    gi = ring * D.S + (int64_t)(sq % Su);
-                    mem = S.id[gi] != 0 && S.shard_seq[gi] == sq;
-                }
-                const unsigned bal = __ballot_sync(0xffffffffu, mem);
-                if (mem) {
-                    EvictRec& r = rec[o + __popc(bal & ((1u << lane) - 1u))];
-                    r.step = sstep;
-                    r.entry_id = S.id[gi];
-                    r.token_id = S.token[gi];
-                    r.expert_id = S.expert[gi];
-                    r.device = dev;
-                    r.score = score_entry(C, S, gi, now, D.n_layers);
-                    r.reason = reason;
-                    r.stream = s;
-                    // KVStore::erase (kvstore.cpp:180-185) + page reclamation
-                    S.id[gi] = 0;
-                    atomicSub(&S.live[ring], 1);
-                    const int slot = (int)(sq % Su);
-                    const int64_t pt_i = ring * D.ppr + slot / D.spg;
-                    const int32_t page = S.page_table[pt_i];
-                    if (atomicSub(&S.page_live[page], 1) == 1) {
-                        S.page_table[pt_i] = -1;
-                        const int top = atomicAdd(S.free_top, 1);
-                        S.free_stack[top] = page;
-                    }
-                }
-                o += __popc(bal);
-            }
-            if (lane == 0) {  // the page is gone: reset its record
-                const int64_t r = ring * D.ppr_sched + (int64_t)(q % (uint64_t)D.ppr_sched);
-                if (S.pr_cnt[r] > 0) atomicSub(&S.pages_live[sg], 1);
-                S.pr_cnt[r] = 0;
-                S.pr_first[r] = 0;
-                S.pr_sla[r] = 0;
-                S.pr_sf[r] = 0;
-            }
+            erase_page_warp(D, C, S, sg, list[v0 + vv], reason, vcnt_off[vv]);
         }
         __syncthreads();
-        if (tid == kSelThreads - 1) sm_off = vcnt_off[tid] + cnt;
+        if (tid == NT - 1) sm_off = vcnt_off[tid] + cnt;
         __syncthreads();
     }
     if (tid == 0) S.n_ev[sg] = sm_off;
+}
+
+__device__ __forceinline__ bool within_budget(const Dims& D, const Cfg& C, const State& S, const int sg,
+                                              const bool writer = true) {
+    if (!(C.record_agg && S.pages_live[sg] <= C.budget_pages)) return false;
+    if (writer && threadIdx.x == 0) {  // P <= K: nothing to evict
+        const int P = S.pages_live[sg];
+        S.pages_before[sg] = P;
+        S.pages_after[sg] = P;
+        S.n_ev[sg] = 0;
+    }
+    return true;
+}
+
+__device__ __forceinline__ void select_body(const Dims& D, const Cfg& C, const State& S, const int sg,
+                                            const bool stage) {
+    const int s = sg / D.Gl;
+    if (S.err[s]) return;
+    if (within_budget(D, C, S, sg)) return;
+    const int64_t f0 = (int64_t)sg * D.SPD * D.ppr_sched;
+    const int V = select_fast(D, C, S, sg, [&](int i, double& a, uint64_t& o) {
+        const int c = S.pg_cnt[f0 + i];
+        if (c > 0) a = S.pg_agg[f0 + i], o = S.pg_oldest[f0 + i];
+        return c;
+    });
+    if (V <= 1) return;
+    __syncthreads();
+    select_general(D, C, S, sg, stage);
+}
+
+// Evict for device sg inside k_control (record_agg strategies), by the
+// stream's cluster: the page pass is split over the cluster's CTAs, partial
+// (P, T, argmin) meet in rank 0's shared memory (DSMEM); rank 0 decides and
+// erases.  V > 1 materialises the keys (split) and rank 0 runs select_general.
+__device__ __forceinline__ void sched_device_cl(const Dims& D, const Cfg& C, const State& S, const int sg,
+                                                cg::cluster_group& cl) {
+    const int r = (int)cl.block_rank(), CL = (int)cl.num_blocks();
+    if (within_budget(D, C, S, sg, r == 0)) return;  // uniform over the cluster
+    const int s = sg / D.Gl, tid = threadIdx.x, NT = blockDim.x;
+    const uint64_t now = S.now[s];
+    const int64_t ring0 = (int64_t)sg * D.SPD;
+    const int ppr = D.ppr_sched, np = D.SPD * ppr;
+    auto rec_key = [&](int i, double& a, uint64_t& o) {
+        return page_key_rec(D, C, S, ring0 + i / ppr, i % ppr, now, a, o);
+    };
+    __shared__ PageBest sb, parts[kMaxCluster];
+    __shared__ int sV;
+    block_page_scan(np, r * NT, CL * NT, rec_key, S.theta[s], C.sched_strategy == PIKV_SCHED_ADAKV, &sb);
+    if (tid == 0) *cl.map_shared_rank(&parts[r], 0) = sb;
+    cl.sync();
+    if (r == 0 && tid == 0) {
+        PageBest b = parts[0];
+        for (int i = 1; i < CL; ++i) merge_best(b, parts[i]);
+        sb = b;
+        sV = decide_victims(C, S, sg, b);
+    }
+    cl.sync();
+    const int V0 = *cl.map_shared_rank(&sV, 0);
+    if (V0 == 1) {
+        if (r == 0 && tid < 32) {
+            const int n = erase_page_warp(D, C, S, sg, sb.I, sb.T >= 1 ? PIKV_EVICT_THRESHOLD : PIKV_EVICT_BUDGET, 0);
+            if (tid == 0) S.n_ev[sg] = n;
+        }
+    } else if (V0 > 1) {
+        const int64_t f0 = (int64_t)sg * np;
+        for (int i = r * NT + tid; i < np; i += CL * NT) {
+            double a = 0.0;
+            uint64_t o = 0;
+            S.pg_cnt[f0 + i] = rec_key(i, a, o);
+            S.pg_agg[f0 + i] = a;
+            S.pg_oldest[f0 + i] = o;
+        }
+        cl.sync();
+        if (r == 0) select_general(D, C, S, sg, false);
+    }
+    cl.sync();
 }
 
 __global__ void __launch_bounds__(kSelThreads) k_sched_select(Dims D, Cfg C, State S, int stage) {
@@ -1325,10 +1516,53 @@ __device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t* wsum, int
     return excl;
 }
 
+// Attention work items from the per-stream attended counts (att_cnt): a
+// stream's list is cut into items of C entries, C sized so the persistent
+// attention grid gets ~items_per_cta items per CTA.  One CTA, any block size.
+__device__ __forceinline__ void build_items(const Dims& D, const State& S) {
+    __shared__ int64_t wsum[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nt = blockDim.x, nw = nt >> 5;
+    int64_t N = 0;
+    for (int s0 = 0; s0 < D.B; s0 += nt) {
+        int64_t tot;
+        block_excl_scan(s0 + tid < D.B ? (int64_t)S.att_cnt[s0 + tid] : 0, wsum, &tot);
+        N += tot;
+    }
+    const int64_t ipc = D.items_per_cta;  // work items per attention CTA
+    int64_t C = (N + ipc * D.attend_ctas - 1) / (ipc * D.attend_ctas);
+    if (C < 16) C = 16;
+    int64_t carry = 0;
+    for (int s0 = 0; s0 < D.B; s0 += nt) {
+        const int s = s0 + tid;
+        const int64_t n = s < D.B ? S.att_cnt[s] : 0;
+        int64_t tot;
+        const int64_t first = block_excl_scan((n + C - 1) / C, wsum, &tot) + carry;
+        if (s < D.B) {
+            S.item_first[s] = (int32_t)first;
+            S.summary[s].n_attended = (int32_t)n;
+        }
+        carry += tot;
+    }
+    if (tid == 0) {
+        S.item_first[D.B] = (int32_t)carry;
+        S.n_items[0] = (int32_t)carry;
+    }
+    __syncthreads();
+    for (int s = warp; s < D.B; s += nw) {
+        const int64_t ns = S.att_cnt[s];
+        const int64_t f = S.item_first[s];
+        for (int64_t j = lane; j * C < ns; j += 32) {
+            S.item_stream[f + j] = s;
+            S.item_begin[f + j] = (int32_t)(j * C);
+            S.item_end[f + j] = (int32_t)min(ns, (j + 1) * C);
+        }
+    }
+}
+
+// (b) single CTA: in-stream chunk offsets (warp per stream), per-stream
+//     counts, then the attention work items.
 __global__ void __launch_bounds__(1024) k_retr_scan(Dims D, State S) {
     griddep_enter();
-    __shared__ int64_t sm_n[1024];
-    __shared__ int64_t wsum[32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
     const int per = D.max_cand * D.nch;
     for (int s = warp; s < D.B; s += nw) {
@@ -1344,38 +1578,10 @@ __global__ void __launch_bounds__(1024) k_retr_scan(Dims D, State S) {
             if (b0 + lane < per) S.chunk_off[ci] = (int32_t)(run + x - c);
             run += __shfl_sync(0xffffffffu, x, 31);
         }
-        if (lane == 0) sm_n[s] = run;
+        if (lane == 0) S.att_cnt[s] = (int32_t)run;
     }
     __syncthreads();
-    const int64_t n = tid < D.B ? sm_n[tid] : 0;
-    int64_t N;
-    const int64_t base = block_excl_scan(n, wsum, &N);
-    const int64_t ipc = D.items_per_cta;  // work items per attention CTA
-    int64_t C = (N + ipc * D.attend_ctas - 1) / (ipc * D.attend_ctas);
-    if (C < 16) C = 16;
-    const int64_t items = (n + C - 1) / C;
-    int64_t W;
-    const int64_t first = block_excl_scan(items, wsum, &W);
-    if (tid < D.B) {
-        S.summary[tid].n_attended = (int32_t)n;
-        S.att_base[tid] = base;
-        S.item_first[tid] = (int32_t)first;
-    }
-    if (tid == 0) {
-        S.att_base[D.B] = N;
-        S.item_first[D.B] = (int32_t)W;
-        S.n_items[0] = (int32_t)W;
-    }
-    __syncthreads();
-    for (int s = warp; s < D.B; s += nw) {
-        const int64_t ns = sm_n[s];
-        const int64_t f = S.item_first[s];
-        for (int64_t j = lane; j * C < ns; j += 32) {
-            S.item_stream[f + j] = s;
-            S.item_begin[f + j] = (int32_t)(j * C);
-            S.item_end[f + j] = (int32_t)min(ns, (j + 1) * C);
-        }
-    }
+    build_items(D, S);
 }
 
 // (c) write the compacted (slot, entry) lists; bump freq / last_access.
@@ -1420,7 +1626,7 @@ __global__ void k_retr_write(Dims D, State S) {
     __syncthreads();
     if (m) {
         const int excl = x - 1 + ((tid >> 5) ? ws[(tid >> 5) - 1] : 0);
-        const int64_t pos = S.att_base[s] + S.chunk_off[ci] + excl;
+        const int64_t pos = (int64_t)s * D.att_stride + S.chunk_off[ci] + excl;
         S.att_slot[pos] = (int32_t)gi;
         const int32_t page = S.page_table[ring * D.ppr + slot / D.spg];
         S.att_entry[pos] = page * D.spg + slot % D.spg;
@@ -1430,6 +1636,317 @@ __global__ void k_retr_write(Dims D, State S) {
         S.freq[gi] += 1;  // kvstore.cpp:165-168
         S.last_access[gi] = now;
     }
+}
+
+// Retrieval for stream s by its cluster (k_control).  The stream's
+// candidate rings (ascending) concatenated in slot order form one list of
+// slots; rank r takes the r-th contiguous 1/CL of it.  Pass 1 counts the
+// matches of each rank (and the per-expert hits); the counts meet in rank
+// 0's shared memory and give each rank its output base; pass 2 writes the
+// (slot, pool entry) lists in (ring, slot) order and bumps freq /
+// last_access (kvstore.cpp:136-168) - the filter of k_retr_count/k_retr_write.
+// Tiles of kRetrU x blockDim slots (thread t takes slots t, t + NT, ...).
+constexpr int kRetrU = 4;
+
+template <bool kWrite>
+__device__ __forceinline__ int retrieve_tiles(const Dims& D, const State& S, const int s, const int64_t ring,
+                                              const int a, const int b, const uint64_t now, const int* sm_ex,
+                                              int* sm_found, int* sm_off, int* sm_tile, int64_t out) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NT = blockDim.x, NW = NT >> 5;
+    int mine = 0;
+    for (int t0 = a; t0 < b; t0 += kRetrU * NT) {
+        uint64_t id[kRetrU];
+        int64_t tok[kRetrU] = {};
+        int ex[kRetrU] = {};
+#pragma unroll
+        for (int u = 0; u < kRetrU; ++u) {
+            const int slot = t0 + u * NT + tid;
+            id[u] = 0;
+            if (slot < b) {
+                const int64_t gi = ring * D.S + slot;
+                id[u] = S.id[gi];
+                tok[u] = S.token[gi];
+                ex[u] = S.expert[gi];
+            }
+        }
+        int jh[kRetrU];
+#pragma unroll
+        for (int u = 0; u < kRetrU; ++u) {
+            jh[u] = -1;
+            if (id[u] != 0 && tok[u] < (int64_t)now)
+                for (int j = 0; j < D.k; ++j)
+                    if (sm_ex[j] == ex[u]) {
+                        jh[u] = j;
+                        break;
+                    }
+        }
+        if constexpr (!kWrite) {
+#pragma unroll
+            for (int u = 0; u < kRetrU; ++u)
+                if (jh[u] >= 0) ++mine, atomicAdd(&sm_found[jh[u]], 1);
+            continue;
+        }
+        unsigned bal[kRetrU];
+#pragma unroll
+        for (int u = 0; u < kRetrU; ++u) {
+            bal[u] = __ballot_sync(0xffffffffu, jh[u] >= 0);
+            if (lane == 0) sm_off[u * NW + warp] = __popc(bal[u]);
+        }
+        __syncthreads();
+        if (warp == 0) {  // exclusive scan over (u, warp) = slot order
+            const int n = kRetrU * NW, per = (n + 31) / 32;
+            int loc[kRetrU];  // per <= kRetrU (NW <= 32)
+            int sum = 0;
+            for (int i = 0; i < per; ++i) {
+                const int idx = lane * per + i;
+                loc[i] = idx < n ? sm_off[idx] : 0;
+                sum += loc[i];
+            }
+            int x = sum;
+            for (int off = 1; off < 32; off <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x, off);
+                if (lane >= off) x += y;
+            }
+            int e = x - sum;
+            for (int i = 0; i < per; ++i) {
+                const int idx = lane * per + i;
+                if (idx < n) sm_off[idx] = e;
+                e += loc[i];
+            }
+            if (lane == 31) *sm_tile = x;
+        }
+        __syncthreads();
+        // every load of the tile first (all in flight), then the stores:
+        // interleaving them would serialise the tile on may-alias ordering
+        int32_t page[kRetrU];
+        uint64_t sq[kRetrU], la[kRetrU], fr[kRetrU];
+#pragma unroll
+        for (int u = 0; u < kRetrU; ++u) {
+            if (jh[u] < 0) continue;
+            const int slot = t0 + u * NT + tid;
+            const int64_t gi = ring * D.S + slot;
+            page[u] = S.page_table[ring * D.ppr + slot / D.spg];
+            sq[u] = S.shard_seq[gi];
+            la[u] = S.last_access[gi];
+            fr[u] = S.freq[gi];
+        }
+#pragma unroll
+        for (int u = 0; u < kRetrU; ++u) {
+            if (jh[u] < 0) continue;
+            const int slot = t0 + u * NT + tid;
+            const int64_t gi = ring * D.S + slot;
+            const int64_t pos = out + sm_off[u * NW + warp] + __popc(bal[u] & ((1u << lane) - 1u));
+            S.att_slot[pos] = (int32_t)gi;
+            S.att_entry[pos] = page[u] * D.spg + slot % D.spg;
+            const int64_t prec = page_rec(D, ring, sq[u]);
+            atomicAdd((unsigned long long*)&S.pr_sla[prec], (unsigned long long)(now - la[u]));
+            atomicAdd((unsigned long long*)&S.pr_sf[prec], 1ull);
+            S.freq[gi] = fr[u] + 1;  // kvstore.cpp:165-168
+            S.last_access[gi] = now;
+        }
+        out += *sm_tile;
+        mine += *sm_tile;
+        __syncthreads();  // sm_off / sm_tile reused by the next tile
+    }
+    return mine;  // kWrite: block total; else this thread's count
+}
+
+__device__ __forceinline__ void gstamp(long long* p) {
+    if (p && threadIdx.x == 0) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        *p = (long long)t;
+    }
+}
+
+__device__ __forceinline__ void retrieve_cl(const Dims& D, const State& S, const int s, cg::cluster_group& cl,
+                                            long long* dbg) {
+    const int r = (int)cl.block_rank(), CL = (int)cl.num_blocks();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NT = blockDim.x;
+    __shared__ int sm_ex[kMaxK], sm_found[kMaxK];
+    __shared__ int sm_off[kRetrU * 32];
+    __shared__ int sm_tile, sm_red[32];
+    __shared__ int sm_cnt[kMaxCluster];
+    for (int j = tid; j < D.k; j += NT) {
+        sm_ex[j] = S.experts[(int64_t)s * D.k + j];
+        sm_found[j] = 0;
+    }
+    __syncthreads();
+    const uint64_t now = S.now[s];
+    const int nc = S.ncand[s];
+    int64_t total = 0;
+    for (int c = 0; c < nc; ++c) {
+        const uint64_t seq = S.seq[(int64_t)s * D.R + S.cand[(int64_t)s * D.max_cand + c]];
+        total += seq < (uint64_t)D.S ? (int64_t)seq : D.S;
+    }
+    const int64_t lo = total * r / CL, hi = total * (r + 1) / CL;
+    // pass 1: count
+    int mine = 0;
+    {
+        int64_t off = 0;
+        for (int c = 0; c < nc; ++c) {
+            const int64_t ring = (int64_t)s * D.R + S.cand[(int64_t)s * D.max_cand + c];
+            const uint64_t seq = S.seq[ring];
+            const int fill = seq < (uint64_t)D.S ? (int)seq : D.S;
+            const int a = (int)(max(lo, off) - off), b = (int)(min(hi, off + fill) - off);
+            if (a < b) mine += retrieve_tiles<false>(D, S, s, ring, a, b, now, sm_ex, sm_found, sm_off, &sm_tile, 0);
+            off += fill;
+        }
+    }
+    for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    if (lane == 0) sm_red[warp] = mine;
+    __syncthreads();
+    if (tid == 0) {
+        int t = 0;
+        for (int w = 0; w < (NT >> 5); ++w) t += sm_red[w];
+        *cl.map_shared_rank(&sm_cnt[r], 0) = t;
+    }
+    for (int j = tid; j < D.k; j += NT)
+        if (sm_found[j]) atomicAdd(&S.found[(int64_t)s * D.k + j], sm_found[j]);
+    gstamp(dbg);
+    cl.sync();
+    gstamp(dbg ? dbg + 1 : nullptr);
+    int base = 0, all = 0;
+    {
+        const int* c0 = cl.map_shared_rank(sm_cnt, 0);
+        for (int i = 0; i < CL; ++i) {
+            const int x = c0[i];
+            if (i < r) base += x;
+            all += x;
+        }
+    }
+    if (r == 0 && tid == 0) S.att_cnt[s] = all;
+    // pass 2: write
+    int64_t out = (int64_t)s * D.att_stride + base;
+    int64_t off = 0;
+    for (int c = 0; c < nc; ++c) {
+        const int64_t ring = (int64_t)s * D.R + S.cand[(int64_t)s * D.max_cand + c];
+        const uint64_t seq = S.seq[ring];
+        const int fill = seq < (uint64_t)D.S ? (int)seq : D.S;
+        const int a = (int)(max(lo, off) - off), b = (int)(min(hi, off + fill) - off);
+        if (a < b) out += retrieve_tiles<true>(D, S, s, ring, a, b, now, sm_ex, sm_found, sm_off, &sm_tile, out);
+        off += fill;
+    }
+    cl.sync();  // rank 0's sm_cnt stays readable until every rank has read it
+}
+
+// ===========================================================================
+// control: the whole pre-attention part of the step, one cluster per stream
+// ===========================================================================
+// route -> insert (rank 0) -> evict (each local device) -> retrieve (whole
+// cluster), with cluster barriers between phases: streams are independent
+// until attention, so no stream waits for the slowest stream's phase (the
+// multi-kernel path's grid barriers) and the memory-parallel phases still
+// get CL SMs per stream.  The last CTA builds the attention work items.
+// Used for record_agg strategies (LRU/LRU+) and unbounded budgets, whose
+// eviction keys come from the page records; other strategies run the
+// multi-kernel path (their keys need the wide member scan).
+constexpr int kCtlThreads = 512;
+__global__ void __launch_bounds__(kCtlThreads, 1)
+    k_control(Dims D, Cfg C, State S, const void* __restrict__ qin, const void* __restrict__ kin,
+              const void* __restrict__ vin, const double* __restrict__ saliency, int route_ch) {
+    griddep_enter();
+    extern __shared__ __align__(128) uint8_t sm_dyn[];
+    cg::cluster_group cl = cg::this_cluster();
+    const int r = (int)cl.block_rank();
+    const int s = blockIdx.x / (int)cl.num_blocks(), tid = threadIdx.x;
+    auto stamp = [&](int p) {
+        if (D.dbg_ctl && tid == 0 && r == 0) {
+            uint64_t t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            S.dbg[64 + 8 * s + p] = (long long)t;
+        }
+    };
+    stamp(0);
+    if (r == 0) {
+        if (tid == 0) S.att_cnt[s] = 0;
+        const int* sel = route_body(D, C, S, s, qin, route_ch, sm_dyn);
+        __syncthreads();
+        stamp(1);
+        if (!S.err[s]) insert_body(D, C, S, s, qin, kin, vin, saliency, sm_dyn, sel);
+    }
+    cl.sync();
+    stamp(2);
+    const bool ok = !S.err[s];
+    if (ok && !C.unbounded_budget)
+        for (int gl = 0; gl < D.Gl; ++gl) sched_device_cl(D, C, S, s * D.Gl + gl, cl);
+    stamp(3);
+    if (ok) retrieve_cl(D, S, s, cl, D.dbg_ctl && r == 0 ? S.dbg + 64 + 8 * s + 6 : nullptr);
+    stamp(4);
+    // last CTA of the grid: attention work items over all streams
+    __shared__ bool sm_last;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) sm_last = atomicAdd(S.ctl_ctr, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!sm_last) return;
+    __threadfence();
+    build_items(D, S);
+    if (tid == 0) *S.ctl_ctr = 0;
+    if (D.dbg_ctl && tid == 0) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        S.dbg[64 + 8 * s + 5] = (long long)t;
+    }
+}
+
+bool control_supported(const Dims& D, const Cfg& C) {
+    return (C.record_agg || C.unbounded_budget) && D.E + 32 <= kCtlThreads;
+}
+
+// Launch geometry of k_control, fixed per engine: the route's W ring is
+// sized so two CTAs fit per SM (only rank 0 uses it, but every CTA of a
+// launch gets the same shared memory), and the cluster size is the largest
+// power of two <= 8 whose B clusters are all co-resident
+// (cudaOccupancyMaxActiveClusters): a cluster that waits for a second wave
+// delays its whole stream.
+struct CtlGeom {
+    int ch = 0, cl = 1;
+    size_t smem = 0;
+};
+static CtlGeom control_geom(const Dims& D) {
+    CtlGeom g;
+    g.ch = D.route_ch;
+    g.smem = std::max(route_smem_bytes(D, g.ch), insert_smem_bytes(D));
+    if (g.smem > 48 * 1024)
+        cudaFuncSetAttribute(k_control, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
+    g.cl = 1;
+    for (int cl = kMaxCluster; cl > 1; --cl) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(D.B * cl);
+        cfg.blockDim = dim3(kCtlThreads);
+        cfg.dynamicSmemBytes = g.smem;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)cl;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int active = 0;
+        const cudaError_t e = cudaOccupancyMaxActiveClusters(&active, k_control, &cfg);
+        if (D.dbg_ctl) fprintf(stderr, "[k_control] cluster %d: max active %d (B %d, smem %zu, ch %d)\n", cl, active, D.B, g.smem, g.ch);
+        if (e == cudaSuccess && active >= D.B) {
+            g.cl = cl;
+            break;
+        }
+        cudaGetLastError();
+    }
+    if (const char* v = std::getenv("PIKV_CTL_CLUSTER")) g.cl = std::max(1, std::min(kMaxCluster, std::atoi(v)));
+    return g;
+}
+
+void launch_control(const Dims& D, const Cfg& C, const State& S, const void* q, const void* k, const void* v,
+                    const double* saliency, cudaStream_t st) {
+    static CtlGeom g;
+    static Dims gd{};
+    if (g.ch == 0 || gd.B != D.B || gd.d != D.d || gd.E != D.E || gd.entry_bytes != D.entry_bytes ||
+        gd.route_ch != D.route_ch) {
+        g = control_geom(D);
+        gd = D;
+    }
+    launch_cluster(k_control, dim3(D.B * g.cl), dim3(kCtlThreads), g.smem, st, g.cl, D, C, S, q, k, v, saliency,
+                   g.ch);
 }
 
 void launch_retr_count(const Dims& D, const State& S, cudaStream_t st) {
@@ -1643,28 +2160,22 @@ __device__ __forceinline__ void feedback_stream(const Dims& D, const Cfg& C, con
 // the global (M, 1/L) of every (stream, head) are staged in shared memory.
 __global__ void k_foldback(Dims D, Cfg C, State S) {
     griddep_enter();
-    extern __shared__ float sm_ml[];  // [B*H] M, then [B*H] 1/L (0 when empty)
-    __shared__ int64_t sm_base[1025];
-    const int nb = D.B + 1;
+    extern __shared__ float sm_ml[];  // [B*H] M, then [B*H] 1/L (0 when empty), then [B] counts
     const int BH = D.B * D.H;
-    for (int i = threadIdx.x; i < nb; i += blockDim.x) sm_base[i] = S.att_base[i];
+    int* sm_cnt = (int*)(sm_ml + 2 * BH);
     for (int i = threadIdx.x; i < BH; i += blockDim.x) {
         sm_ml[i] = S.gM[i];
         const float L = S.gL[i];
         sm_ml[BH + i] = L > 0.f ? 1.f / L : 0.f;
     }
+    for (int i = threadIdx.x; i < D.B; i += blockDim.x) sm_cnt[i] = S.err[i] ? 0 : S.att_cnt[i];
     __syncthreads();
-    const int64_t N = sm_base[D.B];
+    const int64_t N = (int64_t)D.B * D.att_stride;  // per-stream regions, counts in sm_cnt
     const bool vec = (D.H % 4) == 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N;
          i += (int64_t)gridDim.x * blockDim.x) {
-        int lo = 0, hi = D.B;  // stream: last s with base[s] <= i
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (sm_base[mid] <= i) lo = mid; else hi = mid;
-        }
-        const int s = lo;
-        if (S.err[s]) continue;
+        const int s = (int)(i / D.att_stride);
+        if (i - (int64_t)s * D.att_stride >= sm_cnt[s]) continue;
         const float* M = sm_ml + s * D.H;
         const float* iL = sm_ml + BH + s * D.H;
         const float* sc = S.scores + i * D.H;
@@ -1709,7 +2220,7 @@ void launch_finish_merge(const Dims& D, const Cfg& C, const State& S, const Exch
     launch_pdl(k_finish_merge, dim3(D.B), dim3(256), 0, st, D, C, S, X, gathered, y, granks);
 }
 void launch_foldback(const Dims& D, const Cfg& C, const State& S, cudaStream_t st) {
-    const size_t smem = sizeof(float) * 2 * (size_t)D.B * D.H;
+    const size_t smem = sizeof(float) * 2 * (size_t)D.B * D.H + sizeof(int) * (size_t)D.B;
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_foldback, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     launch_pdl(k_foldback, dim3(D.attend_ctas * 2), dim3(256), smem, st, D, C, S);
 }

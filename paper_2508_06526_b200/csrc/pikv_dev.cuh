@@ -57,8 +57,11 @@ struct Dims {
     int max_cand, nch, chunk_slots;  // retrieval grid
     int sel_stride;                  // pow2 >= SPD * ppr_sched
     int64_t pool_entries, pool_pages, att_cap, item_cap;
+    int64_t att_stride;  // attended-list region per stream: min(max_cand * S, pool_entries)
     int attend_ctas;
     int items_per_cta;  // split-K work items per attention CTA (PIKV_ITEMS, default 4)
+    int route_ch;       // router columns per W ring stage (pick_route_chunk)
+    int dbg_ctl;        // k_control phase timestamps into dbg[64 + 8 s + p] (PIKV_DEBUG_CTL=1)
 };
 
 struct Cfg {  // scalar config needed on device (copied by value into kernels)
@@ -75,7 +78,8 @@ struct Cfg {  // scalar config needed on device (copied by value into kernels)
 
 struct State {
     // router (router.hpp:41-56), per stream
-    const double* W;  // E x d, shared by all streams (same seed)
+    const double* W;  // W_r, shared by all streams (same seed), chunk-major:
+                      // [ceil(d / route_ch)][E][route_ch + 2] (zero-padded rows)
     double* load;
     uint64_t* usage;
     uint64_t* total_usage;
@@ -146,10 +150,10 @@ struct State {
     int32_t* chunk_cnt;     // [B][max_cand][nch]
     int32_t* chunk_off;     // same, exclusive within stream
     int32_t* found;         // [B][k]
-    int64_t* att_base;      // [B+1]
-    int32_t* att_slot;      // [att_cap] global slot index (ring*S+slot)
-    int32_t* att_entry;     // [att_cap] pool entry index
-    float* scores;          // [att_cap][H]  (base-2 logits)
+    int32_t* att_cnt;       // [B] attended entries of each stream (this rank)
+    int32_t* att_slot;      // [B][att_stride] global slot index (ring*S+slot)
+    int32_t* att_entry;     // [B][att_stride] pool entry index
+    float* scores;          // [B][att_stride][H]  (base-2 logits)
     int32_t* item_stream;   // [item_cap]
     int32_t* item_begin;
     int32_t* item_end;
@@ -164,6 +168,7 @@ struct State {
     pikv_step_summary* summary;  // [B]
     long long* dbg;              // [64] debug timestamps (k_route, stream 0)
     unsigned* done_ctr;          // last-block counter (k_foldback)
+    unsigned* ctl_ctr;           // last-block counter (k_control)
 };
 
 // ---- helpers -------------------------------------------------------------
@@ -317,6 +322,27 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
     return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
+// Launch with thread-block clusters of `cl` CTAs along x (grid.x % cl == 0).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_cluster(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                  cudaStream_t st, int cl, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)cl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // ---- launch wrappers (defined in the .cu files) ----------------------------
 void launch_route(const Dims& D, const Cfg& C, const State& S, const void* q, cudaStream_t st);
 void launch_project(const Dims& D, const State& S, const void* q, const void* k, const void* v,
@@ -326,6 +352,10 @@ void launch_insert(const Dims& D, const Cfg& C, const State& S, const void* q, c
 void launch_sched_pages(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);
 void launch_sched_select(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);
 
+bool control_supported(const Dims& D, const Cfg& C);
+int pick_route_chunk(const Dims& D);
+void launch_control(const Dims& D, const Cfg& C, const State& S, const void* q, const void* k, const void* v,
+                    const double* saliency, cudaStream_t st);  // route+insert+evict+retrieve per stream
 void launch_retr_count(const Dims& D, const State& S, cudaStream_t st);
 void launch_retr_scan(const Dims& D, const State& S, cudaStream_t st);
 void launch_retr_write(const Dims& D, const State& S, cudaStream_t st);

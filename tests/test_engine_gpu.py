@@ -280,3 +280,21 @@ def test_engine_c5_shape_parity():
                         n_exp=64, S=32, ps=8, budget=40, batch=3, dtype="bf16", n_layers=0)
     cfg.model.head_width = 128
     run_parity(cfg, 80, 23, inject=False)
+
+
+@pytest.mark.parametrize("sched,kw", [
+    ("LRU", dict()),
+    ("LRU", dict(S=10, ps=4, budget=3)),
+    ("LRUPlus", dict(budget=1, ps=1)),
+    (None, dict()),                                                # unbounded
+])
+def test_engine_multikernel_path(monkeypatch, sched, kw):
+    """LRU/LRU+/unbounded steps normally run the per-stream control kernel
+    (k_control); PIKV_CONTROL=0 selects the multi-kernel path (route, insert,
+    sched, retrieval kernels), which must be bit-identical as well."""
+    monkeypatch.setenv("PIKV_CONTROL", "0")
+    if sched is None:
+        cfg = engine_config(router="Adaptive", unbounded=True, S=128, batch=3)
+    else:
+        cfg = engine_config(router="Adaptive", sched=sched, batch=2, **kw)
+    run_parity(cfg, 60, 31)
