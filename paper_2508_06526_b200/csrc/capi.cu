@@ -788,15 +788,15 @@ static int enqueue_local(pikv_engine* eng, const void* q, const void* k, const v
     mark(eng, 4);
     launch_retr_count(D, S, st), ++n;
     mark(eng, 5);
-    launch_retr_scan(D, S, st), ++n;
+    launch_retr_scan(D, eng->C, S, st), ++n;
     mark(eng, 6);
     launch_retr_write(D, S, st), ++n;
     mark(eng, 7);
     }
     if (attend && D.Gl > 0) launch_attend(D, S, st), ++n;
     mark(eng, 8);
-    const int direct = D.world == 1;  // single rank: combine writes y and the global (m, l)
-    launch_combine(D, eng->C, S, eng->X, y, direct, st), ++n;
+    const int direct = D.world == 1;  // single rank: combine writes y
+    if (attend || !direct) launch_combine(D, eng->C, S, eng->X, y, direct, attend, st), ++n;
     mark(eng, 9);
     CUDA_TRY(cudaGetLastError());
     eng->kernels_per_step = n;

@@ -1519,7 +1519,7 @@ __device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t* wsum, int
 // Attention work items from the per-stream attended counts (att_cnt): a
 // stream's list is cut into items of C entries, C sized so the persistent
 // attention grid gets ~items_per_cta items per CTA.  One CTA, any block size.
-__device__ __forceinline__ void build_items(const Dims& D, const State& S) {
+__device__ __forceinline__ void build_items(const Dims& D, const Cfg& C, const State& S) {
     __shared__ int64_t wsum[32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nt = blockDim.x, nw = nt >> 5;
     int64_t N = 0;
@@ -1529,17 +1529,37 @@ __device__ __forceinline__ void build_items(const Dims& D, const State& S) {
         N += tot;
     }
     const int64_t ipc = D.items_per_cta;  // work items per attention CTA
-    int64_t C = (N + ipc * D.attend_ctas - 1) / (ipc * D.attend_ctas);
-    if (C < 16) C = 16;
+    int64_t cs = (N + ipc * D.attend_ctas - 1) / (ipc * D.attend_ctas);  // entries per item
+    if (cs < 16) cs = 16;
     int64_t carry = 0;
     for (int s0 = 0; s0 < D.B; s0 += nt) {
         const int s = s0 + tid;
         const int64_t n = s < D.B ? S.att_cnt[s] : 0;
         int64_t tot;
-        const int64_t first = block_excl_scan((n + C - 1) / C, wsum, &tot) + carry;
+        const int64_t first = block_excl_scan((n + cs - 1) / cs, wsum, &tot) + carry;
         if (s < D.B) {
             S.item_first[s] = (int32_t)first;
-            S.summary[s].n_attended = (int32_t)n;
+            // the step's summary (StepResult counters) is complete before
+            // attention: this rank's view, made global by k_finish_merge
+            int nev = S.n_ow[s], pb = 0, pa = 0, hits = 0;
+            for (int gl = 0; gl < D.Gl; ++gl) {
+                nev += S.n_ev[s * D.Gl + gl];
+                pb += S.pages_before[s * D.Gl + gl];
+                pa += S.pages_after[s * D.Gl + gl];
+            }
+            for (int j = 0; j < D.k; ++j) hits += S.found[(int64_t)s * D.k + j] > 0;
+            pikv_step_summary& sm = S.summary[s];
+            sm.step = S.now[s];
+            sm.inserts = D.k;
+            sm.lookups = D.k;
+            sm.hits = hits;
+            sm.n_attended = (int32_t)n;
+            const int hw = C.head_width < D.dp ? C.head_width : D.dp;  // pipeline.cpp:22-26, 262-264
+            sm.fetch_elements = (int64_t)n * (int64_t)(2 * hw + D.dp);
+            sm.n_evictions = nev;
+            sm.pages_before = pb;
+            sm.pages_after = pa;
+            sm.error = S.err[s];
         }
         carry += tot;
     }
@@ -1551,17 +1571,17 @@ __device__ __forceinline__ void build_items(const Dims& D, const State& S) {
     for (int s = warp; s < D.B; s += nw) {
         const int64_t ns = S.att_cnt[s];
         const int64_t f = S.item_first[s];
-        for (int64_t j = lane; j * C < ns; j += 32) {
+        for (int64_t j = lane; j * cs < ns; j += 32) {
             S.item_stream[f + j] = s;
-            S.item_begin[f + j] = (int32_t)(j * C);
-            S.item_end[f + j] = (int32_t)min(ns, (j + 1) * C);
+            S.item_begin[f + j] = (int32_t)(j * cs);
+            S.item_end[f + j] = (int32_t)min(ns, (j + 1) * cs);
         }
     }
 }
 
 // (b) single CTA: in-stream chunk offsets (warp per stream), per-stream
 //     counts, then the attention work items.
-__global__ void __launch_bounds__(1024) k_retr_scan(Dims D, State S) {
+__global__ void __launch_bounds__(1024) k_retr_scan(Dims D, Cfg C, State S) {
     griddep_enter();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
     const int per = D.max_cand * D.nch;
@@ -1581,7 +1601,7 @@ __global__ void __launch_bounds__(1024) k_retr_scan(Dims D, State S) {
         if (lane == 0) S.att_cnt[s] = (int32_t)run;
     }
     __syncthreads();
-    build_items(D, S);
+    build_items(D, C, S);
 }
 
 // (c) write the compacted (slot, entry) lists; bump freq / last_access.
@@ -1881,7 +1901,7 @@ __global__ void __launch_bounds__(kCtlThreads, 1)
     __syncthreads();
     if (!sm_last) return;
     __threadfence();
-    build_items(D, S);
+    build_items(D, C, S);
     if (tid == 0) *S.ctl_ctr = 0;
     if (D.dbg_ctl && tid == 0) {
         uint64_t t;
@@ -1952,8 +1972,8 @@ void launch_control(const Dims& D, const Cfg& C, const State& S, const void* q, 
 void launch_retr_count(const Dims& D, const State& S, cudaStream_t st) {
     launch_pdl(k_retr_count, dim3(D.B, D.max_cand, D.nch), dim3(D.chunk_slots), 0, st, D, S);
 }
-void launch_retr_scan(const Dims& D, const State& S, cudaStream_t st) {
-    launch_pdl(k_retr_scan, dim3(1), dim3(1024), 0, st, D, S);
+void launch_retr_scan(const Dims& D, const Cfg& C, const State& S, cudaStream_t st) {
+    launch_pdl(k_retr_scan, dim3(1), dim3(1024), 0, st, D, C, S);
 }
 void launch_retr_write(const Dims& D, const State& S, cudaStream_t st) {
     launch_pdl(k_retr_write, dim3(D.B, D.max_cand, D.nch), dim3(D.chunk_slots), 0, st, D, S);
@@ -1962,18 +1982,19 @@ void launch_retr_write(const Dims& D, const State& S, cudaStream_t st) {
 // ===========================================================================
 // combine: per-stream merge of work-item partials into the exchange record
 // ===========================================================================
-__global__ void k_combine(Dims D, Cfg C, State S, ExchangeLayout X, float* __restrict__ y, int direct) {
+// LSE merge of one (stream, head) over its work items: y and the global
+// (M, L) (single rank), or the exchange record's (o, m, l) plus its found /
+// stats part for the cross-rank merge.
+__global__ void k_combine(Dims D, Cfg C, State S, ExchangeLayout X, float* __restrict__ y, int direct,
+                          int attended) {
     griddep_enter();
     const int s = blockIdx.x, h = blockIdx.y;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
     extern __shared__ float sm_f[];  // [n_items of stream s] scale factors
     __shared__ float red[32];
     uint8_t* rec = S.exchange + (int64_t)s * X.bytes_per_stream;
-    float* xo = (float*)(rec + X.o_off);
-    float* xm = (float*)(rec + X.m_off);
-    float* xl = (float*)(rec + X.l_off);
-    const int w0 = S.item_first[s], w1 = S.item_first[s + 1];
-    const int nw = w1 - w0;
+    const int w0 = S.item_first[s];
+    const int nw = attended ? S.item_first[s + 1] - w0 : 0;
     const bool ok = !S.err[s];
     float M = -INFINITY;
     for (int i = tid; i < nw; i += blockDim.x) M = fmaxf(M, S.part_m[(int64_t)(w0 + i) * D.H + h]);
@@ -2003,57 +2024,34 @@ __global__ void k_combine(Dims D, Cfg C, State S, ExchangeLayout X, float* __res
         if (direct) {
             if (y && ok) y[(int64_t)s * D.dp + h * D.dph + o] = L > 0.f ? acc / L : 0.f;
         } else {
-            xo[h * D.dph + o] = ok ? acc : 0.f;
+            ((float*)(rec + X.o_off))[h * D.dph + o] = ok ? acc : 0.f;
         }
     }
-    if (tid == 0) {
-        if (direct) {
-            S.gM[s * D.H + h] = M;
-            S.gL[s * D.H + h] = L;
-        } else {
-            xm[h] = ok ? M : -INFINITY;
-            xl[h] = ok ? L : 0.f;
-        }
+    if (tid != 0) return;
+    if (direct) {  // single rank: the global (M, L) for the fold-back
+        S.gM[s * D.H + h] = M;
+        S.gL[s * D.H + h] = L;
+        return;
     }
-    if (h == 0 && tid == 0) {
-        int nev = S.n_ow[s], pb = 0, pa = 0;
-        for (int gl = 0; gl < D.Gl; ++gl) {
-            nev += S.n_ev[s * D.Gl + gl];
-            pb += S.pages_before[s * D.Gl + gl];
-            pa += S.pages_after[s * D.Gl + gl];
-        }
-        const int n_att = S.summary[s].n_attended;
-        if (direct) {  // world == 1: this rank's counts are the global ones
-            int hits = 0;
-            for (int j = 0; j < D.k; ++j) hits += S.found[(int64_t)s * D.k + j] > 0;
-            pikv_step_summary& sm = S.summary[s];
-            sm.step = S.now[s];
-            sm.inserts = D.k;
-            sm.lookups = D.k;
-            sm.hits = hits;
-            const int hw = C.head_width < D.dp ? C.head_width : D.dp;  // pipeline.cpp:22-26
-            sm.fetch_elements = (int64_t)n_att * (int64_t)(2 * hw + D.dp);
-            sm.n_evictions = nev;
-            sm.pages_before = pb;
-            sm.pages_after = pa;
-            sm.error = S.err[s];
-        } else {
-            int32_t* xf = (int32_t*)(rec + X.found_off);
-            int32_t* xs = (int32_t*)(rec + X.stats_off);
-            for (int j = 0; j < D.k; ++j) xf[j] = S.found[(int64_t)s * D.k + j];
-            xs[0] = n_att;
-            xs[1] = nev;
-            xs[2] = pb;
-            xs[3] = pa;
-        }
+    ((float*)(rec + X.m_off))[h] = ok ? M : -INFINITY;
+    ((float*)(rec + X.l_off))[h] = ok ? L : 0.f;
+    if (h == 0) {
+        const pikv_step_summary& sm = S.summary[s];  // this rank's counts (build_items)
+        int32_t* xf = (int32_t*)(rec + X.found_off);
+        int32_t* xs = (int32_t*)(rec + X.stats_off);
+        for (int j = 0; j < D.k; ++j) xf[j] = S.found[(int64_t)s * D.k + j];
+        xs[0] = sm.n_attended;
+        xs[1] = sm.n_evictions;
+        xs[2] = sm.pages_before;
+        xs[3] = sm.pages_after;
     }
 }
 
 void launch_combine(const Dims& D, const Cfg& C, const State& S, const ExchangeLayout& X, float* y,
-                    int direct, cudaStream_t st) {
+                    int direct, int attended, cudaStream_t st) {
     const int threads = D.dph >= 128 ? 128 : (D.dph >= 64 ? 64 : 32);
     launch_pdl(k_combine, dim3(D.B, D.H), dim3(threads), sizeof(float) * (size_t)D.item_cap, st, D, C, S, X, y,
-               direct);
+               direct, attended);
 }
 
 // ===========================================================================

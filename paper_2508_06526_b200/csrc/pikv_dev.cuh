@@ -163,7 +163,7 @@ struct State {
     float* part_l;
     float* part_o;          // [item_cap][H][dph]
     uint8_t* exchange;      // [B][bytes_per_stream]
-    float* gM;              // [B][H] global max (base 2)
+    float* gM;              // [B][H] global max (base 2): k_combine (one rank) / k_finish_merge
     float* gL;              // [B][H]
     pikv_step_summary* summary;  // [B]
     long long* dbg;              // [64] debug timestamps (k_route, stream 0)
@@ -357,11 +357,11 @@ int pick_route_chunk(const Dims& D);
 void launch_control(const Dims& D, const Cfg& C, const State& S, const void* q, const void* k, const void* v,
                     const double* saliency, cudaStream_t st);  // route+insert+evict+retrieve per stream
 void launch_retr_count(const Dims& D, const State& S, cudaStream_t st);
-void launch_retr_scan(const Dims& D, const State& S, cudaStream_t st);
+void launch_retr_scan(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);
 void launch_retr_write(const Dims& D, const State& S, cudaStream_t st);
 void launch_attend(const Dims& D, const State& S, cudaStream_t st);
 void launch_combine(const Dims& D, const Cfg& C, const State& S, const ExchangeLayout& X, float* y,
-                    int direct, cudaStream_t st);
+                    int direct, int attended, cudaStream_t st);
 void launch_finish_merge(const Dims& D, const Cfg& C, const State& S, const ExchangeLayout& X,
                          const uint8_t* gathered, float* y, int granks, cudaStream_t st);
 void launch_foldback(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);  // + feedback
