@@ -250,6 +250,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ncu-window", action="store_true",
+                    help="cudaProfilerStart/Stop around the timed steps (ncu --profile-from-start off)")
     ap.add_argument("--prefill", type=int, default=None, help="override prefill tokens")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: stage the exchange through host memory (single-GPU rehearsal)")
@@ -330,11 +332,15 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
+        if args.ncu_window:
+            torch.cuda.cudart().cudaProfilerStart()
         ev0.record(es)
         for i in range(args.steps):
             one_step(args.warmup + i)
         ev1.record(es)
         torch.cuda.synchronize()
+        if args.ncu_window:
+            torch.cuda.cudart().cudaProfilerStop()
     if world > 1:
         dist.barrier()
     ms = ev0.elapsed_time(ev1)

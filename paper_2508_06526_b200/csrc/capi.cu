@@ -130,7 +130,7 @@ struct pikv_engine {
     bool warmed = false;
     int64_t launches = 0;
     int kernels_per_step = 0;
-    bool fused_control = false;  // k_control replaces route..retr_write (PIKV_CONTROL=0 disables)
+    bool fused_control = false;  // k_control replaces route..retr_write (B <= 8; PIKV_CONTROL=0/1 forces)
     // profiling: per step kPhases+1 events on the engine stream
     bool profiling = false;
     std::vector<cudaEvent_t> ev;
@@ -528,8 +528,12 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
                                        c.sched_strategy == PIKV_SCHED_LRU_PLUS) ? 1 : 0;
     }
     {
-        const char* v = std::getenv("PIKV_CONTROL");
-        eng->fused_control = control_supported(D, C) && !(v && v[0] == '0');
+        // measured (profiles/README.md): the per-stream control kernel wins
+        // when the step is launch-bound (B = 1: +5%); from B = 16 the wide
+        // multi-kernel path is as fast or faster (c2 tie, c3-c5 +2-7%)
+        bool want = D.B <= 8;
+        if (const char* v = std::getenv("PIKV_CONTROL")) want = v[0] == '1';
+        eng->fused_control = control_supported(D, C) && want;
     }
 
     // exchange record layout

@@ -227,9 +227,12 @@ def test_prefill_then_step_graph_replay():
     assert torch.isfinite(y).all()
 
 
-def test_engine_c2_shape_parity():
+@pytest.mark.parametrize("control", ["1", "0"])
+def test_engine_c2_shape_parity(monkeypatch, control):
     """BASELINE configs[1] shapes (d = 32 x 128, bf16, E16 top-2, pure expert
-    sharding n_tok=1/n_exp=16, LRU page budget) over 120 steps, 2 streams."""
+    sharding n_tok=1/n_exp=16, LRU page budget) over 120 steps, 2 streams,
+    through the per-stream control kernel and the multi-kernel path."""
+    monkeypatch.setenv("PIKV_CONTROL", control)
     cfg = engine_config(router="TopK", sched="LRU", d=4096, H=32, E=16, k=2, G=1, n_tok=1,
                         n_exp=16, S=64, ps=16, budget=6, batch=2, dtype="bf16", n_layers=0)
     cfg.model.head_width = 128
@@ -289,12 +292,22 @@ def test_engine_c5_shape_parity():
     (None, dict()),                                                # unbounded
 ])
 def test_engine_multikernel_path(monkeypatch, sched, kw):
-    """LRU/LRU+/unbounded steps normally run the per-stream control kernel
-    (k_control); PIKV_CONTROL=0 selects the multi-kernel path (route, insert,
-    sched, retrieval kernels), which must be bit-identical as well."""
+    """At B <= 8, LRU/LRU+/unbounded steps run the per-stream control kernel
+    (k_control) by default; PIKV_CONTROL=0 selects the multi-kernel path
+    (route, insert, sched, retrieval kernels; the default from B = 16), which
+    must be bit-identical as well."""
     monkeypatch.setenv("PIKV_CONTROL", "0")
     if sched is None:
         cfg = engine_config(router="Adaptive", unbounded=True, S=128, batch=3)
     else:
         cfg = engine_config(router="Adaptive", sched=sched, batch=2, **kw)
     run_parity(cfg, 60, 31)
+
+
+def test_engine_control_kernel_many_streams(monkeypatch):
+    """PIKV_CONTROL=1 at B = 12 (the default switches to the multi-kernel
+    path above 8 streams): the cluster size comes from the co-residency
+    query, every stream's cluster splits eviction and retrieval."""
+    monkeypatch.setenv("PIKV_CONTROL", "1")
+    cfg = engine_config(router="TopK", sched="LRU", S=32, ps=4, budget=3, batch=12, H=2)
+    run_parity(cfg, 50, 41)
