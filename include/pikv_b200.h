@@ -138,6 +138,17 @@ typedef struct pikv_evict_record {
     int32_t stream;
 } pikv_evict_record;
 
+/* One live entry of the store, KVStore::snapshot (kvstore.hpp:89-96). */
+typedef struct pikv_snapshot_record {
+    int32_t device;
+    int32_t shard;      /* shard index within the device */
+    int64_t token_id;
+    int32_t expert_id;
+    int32_t reserved;
+    uint64_t age;       /* now - insert_step (0 when negative), types.hpp:19-21 */
+    uint64_t freq;
+} pikv_snapshot_record;
+
 /* Per-stream summary of the last step (StepResult, pipeline.hpp:68-80). */
 typedef struct pikv_step_summary {
     uint64_t step;
@@ -257,6 +268,12 @@ int pikv_read_evictions_host(pikv_engine* eng, pikv_evict_record* out, int32_t c
 int pikv_read_attended_host(pikv_engine* eng, int32_t stream, int64_t* token,
                             int32_t* expert, double* alpha, int32_t cap,
                             int32_t* n_out);
+/* KVStore::snapshot(now) (kvstore.cpp:206-221) of `stream`: its live entries
+ * on this rank's devices, sorted by (device, shard, token, expert), computed
+ * on the GPU.  now < 0 takes the stream's current step.  *n_out = number of
+ * live entries; at most cap records are written. */
+int pikv_snapshot_host(pikv_engine* eng, int32_t stream, int64_t now, pikv_snapshot_record* out,
+                       int64_t cap, int64_t* n_out);
 /* Slot metadata of `stream` for its owned devices:
  * [G_local][SPD][S] arrays; id 0 marks an empty slot.  Any pointer may be NULL. */
 int64_t pikv_slot_count(pikv_engine* eng);

@@ -21,6 +21,8 @@
 #pragma once
 
 #include <algorithm>
+#include <charconv>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <stdexcept>
@@ -229,6 +231,13 @@ struct StepResult {  // pipeline.hpp:68-80
     std::vector<AttendedEntry> attended;    // (token, expert) order (kvstore.cpp:144-163)
 };
 
+struct SnapshotRecord {  // kvstore.hpp:89-96
+    int device = 0, shard = 0;
+    std::int64_t token_id = 0;
+    int expert_id = 0;
+    std::uint64_t age = 0, freq = 0;
+};
+
 struct StoreStats { std::uint64_t live = 0, memory_bytes = 0, inserts = 0, overwrites = 0; };
 struct RouterStateView { std::vector<double> load, bandit_bias; std::vector<std::uint64_t> usage_counts,
                          miss_counts; std::uint64_t total_usage = 0, step = 0; };
@@ -327,6 +336,19 @@ class Engine {
         return out;
     }
 
+    // KVStore::snapshot(now) (kvstore.cpp:206-221), computed on the GPU;
+    // now < 0: the stream's current step.
+    std::vector<SnapshotRecord> snapshot(int stream = 0, std::int64_t now = -1) const {
+        std::int64_t n = 0;
+        check(pikv_snapshot_host(h_, stream, now, nullptr, 0, &n));
+        std::vector<pikv_snapshot_record> raw(static_cast<std::size_t>(n));
+        if (n) check(pikv_snapshot_host(h_, stream, now, raw.data(), n, &n));
+        std::vector<SnapshotRecord> out;
+        out.reserve(raw.size());
+        for (const auto& r : raw) out.push_back({r.device, r.shard, r.token_id, r.expert_id, r.age, r.freq});
+        return out;
+    }
+
     StoreStats store_stats(int stream = 0) const {
         StoreStats st;
         check(pikv_store_stats_host(h_, stream, &st.live, &st.memory_bytes, &st.inserts, &st.overwrites));
@@ -370,5 +392,55 @@ class Engine {
     EngineConfig cfg_;
     pikv_engine* h_ = nullptr;
 };
+
+// ---- wire formats of the reference's run output (runner.cpp) --------------
+// nlohmann::json dump(): keys sorted, compact, doubles as shortest digits in
+// nlohmann's layout (fixed for decimal exponents -4 < n <= 15); see
+// paper_2508_06526_b200/wire.py for the grisu2 note.
+namespace wire {
+
+inline std::string json_double(double x) {
+    if (x != x || x - x != 0.0) return "null";  // NaN, inf
+    if (x == 0.0) return std::signbit(x) ? "-0.0" : "0.0";
+    char buf[64];
+    auto res = std::to_chars(buf, buf + sizeof(buf), x < 0 ? -x : x, std::chars_format::scientific);
+    std::string sci(buf, res.ptr);  // d[.ddd]e(+|-)XX, shortest round-trip digits
+    const auto epos = sci.find('e');
+    std::string ds = sci.substr(0, epos);
+    ds.erase(std::remove(ds.begin(), ds.end(), '.'), ds.end());
+    while (ds.size() > 1 && ds.back() == '0') ds.pop_back();
+    const int k = static_cast<int>(ds.size());
+    const int n = std::stoi(sci.substr(epos + 1)) + 1;  // value = 0.d1..dk * 10^n
+    std::string out = x < 0 ? "-" : "";
+    if (k <= n && n <= 15) return out + ds + std::string(n - k, '0') + ".0";
+    if (0 < n && n <= 15) return out + ds.substr(0, n) + "." + ds.substr(n);
+    if (-4 < n && n <= 0) return out + "0." + std::string(-n, '0') + ds;
+    const int e = n - 1;
+    std::string es = std::to_string(e < 0 ? -e : e);
+    if (es.size() < 2) es = "0" + es;
+    out += ds.substr(0, 1);
+    if (k > 1) out += "." + ds.substr(1);
+    return out + "e" + (e < 0 ? "-" : "+") + es;
+}
+
+inline const char* reason_name(EvictReason r) {  // scheduler.cpp:40-46
+    return r == EvictReason::Budget ? "budget" : r == EvictReason::Threshold ? "threshold" : "overwrite";
+}
+
+// runner.cpp:215-222 (store dump line)
+inline std::string store_dump_line(const SnapshotRecord& r) {
+    return "{\"age\":" + std::to_string(r.age) + ",\"device\":" + std::to_string(r.device) +
+           ",\"expert\":" + std::to_string(r.expert_id) + ",\"freq\":" + std::to_string(r.freq) +
+           ",\"shard\":" + std::to_string(r.shard) + ",\"token\":" + std::to_string(r.token_id) + "}";
+}
+
+// runner.cpp:58-65 (eviction_json)
+inline std::string eviction_line(const EvictionRecord& r) {
+    return "{\"device\":" + std::to_string(r.device) + ",\"expert\":" + std::to_string(r.expert_id) +
+           ",\"id\":" + std::to_string(r.entry_id) + ",\"reason\":\"" + reason_name(r.reason) +
+           "\",\"score\":" + json_double(r.score) + ",\"token\":" + std::to_string(r.token_id) + "}";
+}
+
+}  // namespace wire
 
 }  // namespace pikv::b200

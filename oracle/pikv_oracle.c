@@ -650,6 +650,48 @@ int po_engine_dump_slots(const po_engine* e, uint64_t* id, uint64_t* shard_seq, 
     return PIKV_OK;
 }
 
+/* KVStore::snapshot, kvstore.cpp:206-221: every live entry as (device, shard,
+ * token, expert, age = EntryMeta::age(now) (types.hpp:19-21), freq), visited
+ * device-major in for_each_live (slot) order, then sorted by (device, shard,
+ * token, expert). */
+static int snap_cmp(const void* a, const void* b) {
+    const pikv_snapshot_record* x = (const pikv_snapshot_record*)a;
+    const pikv_snapshot_record* y = (const pikv_snapshot_record*)b;
+    if (x->device != y->device) return x->device < y->device ? -1 : 1;
+    if (x->shard != y->shard) return x->shard < y->shard ? -1 : 1;
+    if (x->token_id != y->token_id) return x->token_id < y->token_id ? -1 : 1;
+    if (x->expert_id != y->expert_id) return x->expert_id < y->expert_id ? -1 : 1;
+    return 0;
+}
+
+int po_engine_snapshot(const po_engine* e, uint64_t now, pikv_snapshot_record* out, int64_t cap,
+                       int64_t* n_out) {
+    const int64_t n_slots = po_engine_slot_count(e);
+    const int spd = e->spd, S = e->c.S;
+    int64_t n = 0;
+    for (int64_t i = 0; i < n_slots; ++i) n += e->slots[i].id != 0;
+    pikv_snapshot_record* all = (pikv_snapshot_record*)calloc((size_t)(n ? n : 1), sizeof(*all));
+    if (!all) return PIKV_ERR_OUT_OF_MEMORY;
+    int64_t m = 0;
+    for (int64_t i = 0; i < n_slots; ++i) {
+        const po_slot* sl = &e->slots[i];
+        if (!sl->id) continue;
+        const int64_t ring = i / S;
+        pikv_snapshot_record* r = &all[m++];
+        r->device = (int32_t)(ring / spd);
+        r->shard = (int32_t)(ring % spd);
+        r->token_id = sl->token;
+        r->expert_id = sl->expert;
+        r->age = now >= sl->insert_step ? now - sl->insert_step : 0;
+        r->freq = sl->freq;
+    }
+    qsort(all, (size_t)n, sizeof(*all), snap_cmp);
+    if (out) memcpy(out, all, (size_t)(n < cap ? n : cap) * sizeof(*all));
+    free(all);
+    if (n_out) *n_out = n;
+    return PIKV_OK;
+}
+
 int po_engine_set_attn_mass(po_engine* e, const double* attn_mass, const double* per_layer) {
     int64_t n = po_engine_slot_count(e);
     for (int64_t i = 0; i < n; ++i)

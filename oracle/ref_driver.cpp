@@ -307,6 +307,23 @@ int ref_dump_slots(ref_engine* e, uint64_t* id, uint64_t* shard_seq, int64_t* to
     return 0;
 }
 
+// The reference's own KVStore::snapshot (kvstore.cpp:206-221).
+int ref_snapshot(ref_engine* e, uint64_t now, pikv_snapshot_record* out, int64_t cap, int64_t* n_out) {
+    const auto recs = e->store.snapshot(now);
+    const int64_t n = static_cast<int64_t>(recs.size());
+    for (int64_t i = 0; i < n && i < cap; ++i) {
+        out[i].device = recs[i].device;
+        out[i].shard = recs[i].shard;
+        out[i].token_id = recs[i].token_id;
+        out[i].expert_id = recs[i].expert_id;
+        out[i].reserved = 0;
+        out[i].age = recs[i].age;
+        out[i].freq = recs[i].freq;
+    }
+    *n_out = n;
+    return 0;
+}
+
 void ref_router_state(ref_engine* e, double* load, uint64_t* usage, uint64_t* miss, double* bias,
                       uint64_t* step, uint64_t* total_usage) {
     const auto& s = e->rs;

@@ -1004,6 +1004,49 @@ int pikv_read_evictions_host(pikv_engine* eng, pikv_evict_record* out, int32_t c
     return PIKV_OK;
 }
 
+int pikv_snapshot_host(pikv_engine* eng, int32_t stream, int64_t now, pikv_snapshot_record* out,
+                       int64_t cap, int64_t* n_out) {
+    const Dims& D = eng->D;
+    if (stream < 0 || stream >= D.B) return fail(PIKV_ERR_INVALID_ARGUMENT, "stream out of range");
+    if (!n_out) return fail(PIKV_ERR_INVALID_ARGUMENT, "n_out is NULL");
+    cudaSetDevice(eng->device);
+    CUDA_TRY(cudaStreamSynchronize(eng->stream));
+    std::vector<int32_t> live(D.R > 0 ? D.R : 1);
+    if (D.R > 0)
+        CUDA_TRY(cudaMemcpy(live.data(), eng->S.live + (int64_t)stream * D.R, sizeof(int32_t) * D.R,
+                            cudaMemcpyDeviceToHost));
+    std::vector<int64_t> off(D.R + 1, 0);
+    for (int r = 0; r < D.R; ++r) off[r + 1] = off[r] + live[r];
+    const int64_t n = off[D.R];
+    *n_out = n;
+    if (!out || cap <= 0 || n == 0) return PIKV_OK;
+    uint64_t t = 0;
+    if (now < 0) {
+        CUDA_TRY(cudaMemcpy(&t, eng->S.now + stream, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    } else {
+        t = (uint64_t)now;
+    }
+    int64_t* d_off = nullptr;
+    pikv_snapshot_record* d_rec = nullptr;
+    CUDA_TRY(cudaMalloc(&d_off, sizeof(int64_t) * (D.R + 1)));
+    cudaError_t e = cudaMalloc(&d_rec, sizeof(pikv_snapshot_record) * n);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(d_off, off.data(), sizeof(int64_t) * (D.R + 1), cudaMemcpyHostToDevice,
+                            eng->stream);
+    if (e == cudaSuccess) {
+        launch_snapshot(D, eng->S, stream, t, d_off, d_rec, n, eng->stream);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(out, d_rec, sizeof(pikv_snapshot_record) * std::min(n, cap),
+                            cudaMemcpyDeviceToHost, eng->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(eng->stream);
+    cudaFree(d_off);
+    cudaFree(d_rec);
+    if (e != cudaSuccess) return fail(PIKV_ERR_CUDA, std::string("snapshot: ") + cudaGetErrorString(e));
+    return PIKV_OK;
+}
+
 int pikv_read_attended_host(pikv_engine* eng, int32_t stream, int64_t* token, int32_t* expert,
                             double* alpha, int32_t cap, int32_t* n_out) {
     const Dims& D = eng->D;

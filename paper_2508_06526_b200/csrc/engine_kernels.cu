@@ -2227,6 +2227,84 @@ void launch_feedback(const Dims& D, const Cfg& C, const State& S, cudaStream_t s
 }
 
 // ===========================================================================
+// snapshot: KVStore::snapshot (kvstore.cpp:206-221) of one stream
+// ===========================================================================
+// (a) one CTA per local ring: its live entries in shard_seq order (= token
+//     order: a ring's entries are inserted in step order) compacted at the
+//     ring's offset (exclusive scan of the live counts); rings are already
+//     in (device, shard) order.
+__global__ void k_snapshot(Dims D, State S, int s, uint64_t now, const int64_t* __restrict__ ring_off,
+                           pikv_snapshot_record* __restrict__ out) {
+    const int rl = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t ring = (int64_t)s * D.R + rl;
+    const uint64_t seq = S.seq[ring];
+    const int fill = seq < (uint64_t)D.S ? (int)seq : D.S;
+    const uint64_t lo = seq - (uint64_t)fill;
+    __shared__ int wsum[32];
+    __shared__ int sm_total;
+    int64_t o = ring_off[rl];
+    for (int c0 = 0; c0 < fill; c0 += blockDim.x) {
+        const int i = c0 + tid;
+        const uint64_t sq = lo + (uint64_t)i;
+        const int64_t gi = ring * D.S + (int64_t)(sq % (uint64_t)D.S);
+        const bool live = i < fill && S.id[gi] != 0 && S.shard_seq[gi] == sq;
+        const unsigned bal = __ballot_sync(0xffffffffu, live);
+        if (lane == 0) wsum[warp] = __popc(bal);
+        __syncthreads();
+        if (tid == 0) {
+            int t = 0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+                const int c = wsum[w];
+                wsum[w] = t;
+                t += c;
+            }
+            sm_total = t;
+        }
+        __syncthreads();
+        if (live) {
+            pikv_snapshot_record r;
+            r.device = (rl / D.SPD) * D.world + D.rank;
+            r.shard = rl % D.SPD;
+            r.token_id = S.token[gi];
+            r.expert_id = S.expert[gi];
+            r.reserved = 0;
+            const uint64_t ins = S.insert_step[gi];
+            r.age = now >= ins ? now - ins : 0;  // EntryMeta::age, types.hpp:19-21
+            r.freq = S.freq[gi];
+            out[o + wsum[warp] + __popc(bal & ((1u << lane) - 1u))] = r;
+        }
+        o += sm_total;
+        __syncthreads();
+    }
+}
+
+// (b) a step's entries of one shard are consecutive with equal tokens, in
+//     selection order: sort each such run by expert (runs are <= k long).
+__global__ void k_snapshot_ties(pikv_snapshot_record* __restrict__ out, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    auto same = [&](int64_t a, int64_t b) {
+        return out[a].device == out[b].device && out[a].shard == out[b].shard &&
+               out[a].token_id == out[b].token_id;
+    };
+    if (i > 0 && same(i - 1, i)) return;  // not the first of its run
+    int64_t j = i + 1;
+    while (j < n && same(i, j)) ++j;
+    for (int64_t a = i + 1; a < j; ++a) {
+        const pikv_snapshot_record x = out[a];
+        int64_t b = a - 1;
+        while (b >= i && out[b].expert_id > x.expert_id) out[b + 1] = out[b], --b;
+        out[b + 1] = x;
+    }
+}
+
+void launch_snapshot(const Dims& D, const State& S, int s, uint64_t now, const int64_t* ring_off,
+                     pikv_snapshot_record* out, int64_t n, cudaStream_t st) {
+    if (D.R > 0) k_snapshot<<<D.R, 256, 0, st>>>(D, S, s, now, ring_off, out);
+    if (n > 0) k_snapshot_ties<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(out, n);
+}
+
+// ===========================================================================
 // synthetic inputs: N(0,1) from a counter hash, rounded to kv_dtype
 // ===========================================================================
 __host__ __device__ __forceinline__ uint64_t splitmix(uint64_t x) {

@@ -366,6 +366,8 @@ void launch_finish_merge(const Dims& D, const Cfg& C, const State& S, const Exch
                          const uint8_t* gathered, float* y, int granks, cudaStream_t st);
 void launch_foldback(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);  // + feedback
 void launch_feedback(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);
+void launch_snapshot(const Dims& D, const State& S, int s, uint64_t now, const int64_t* ring_off,
+                     pikv_snapshot_record* out, int64_t n, cudaStream_t st);
 void launch_synth(const Dims& D, void* q, void* k, void* v, uint64_t seed, uint64_t step,
                   cudaStream_t st);
 int attend_max_smem();

@@ -262,6 +262,21 @@ class Engine:
                                             _np_ptr(al), m, ctypes.byref(n)))
         return tok[:m], ex[:m], al[:m]
 
+    def snapshot(self, stream: int, now: int = -1):
+        """KVStore::snapshot(now) (kvstore.cpp:206-221) of `stream`, computed on
+        the GPU: live entries of this rank's devices as a wire.SNAPSHOT_DTYPE
+        array sorted by (device, shard, token, expert); now < 0 = the
+        stream's current step.  wire.store_dump_lines() gives runner.cpp's
+        JSONL."""
+        from .wire import SNAPSHOT_DTYPE
+        n = ctypes.c_int64(0)
+        check(lib().pikv_snapshot_host(self.h, stream, now, None, 0, ctypes.byref(n)))
+        out = np.zeros(n.value, dtype=SNAPSHOT_DTYPE)
+        if n.value:
+            check(lib().pikv_snapshot_host(self.h, stream, now, out.ctypes.data, n.value,
+                                           ctypes.byref(n)))
+        return out
+
     def slots(self, stream: int):
         n = lib().pikv_slot_count(self.h)
         cols = {"id": np.uint64, "shard_seq": np.uint64, "token": np.int64, "expert": np.int32,

@@ -19,6 +19,7 @@ sys.path.insert(0, ROOT)
 
 from oracle import build as obuild  # noqa: E402
 from paper_2508_06526_b200.config import EngineConfig, PikvConfigC  # noqa: E402
+from paper_2508_06526_b200.wire import SNAPSHOT_DTYPE  # noqa: E402
 
 c_double_p = ctypes.POINTER(ctypes.c_double)
 c_u64_p = ctypes.POINTER(ctypes.c_uint64)
@@ -70,6 +71,8 @@ def oracle_lib():
         lib.po_engine_dump_slots.argtypes = [ctypes.c_void_p, c_u64_p, c_u64_p, c_i64_p, c_i32_p,
                                              c_u64_p, c_u64_p, c_u64_p, c_double_p, c_double_p]
         lib.po_engine_set_attn_mass.argtypes = [ctypes.c_void_p, c_double_p, c_double_p]
+        lib.po_engine_snapshot.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p,
+                                           ctypes.c_int64, c_i64_p]
         lib.po_engine_router.restype = ctypes.c_void_p
         lib.po_engine_router.argtypes = [ctypes.c_void_p]
         lib.po_router_state.argtypes = [ctypes.c_void_p, c_double_p, c_u64_p, c_u64_p,
@@ -128,6 +131,8 @@ def ref_lib():
         lib.ref_step_noattend.argtypes = lib.ref_step.argtypes
         lib.ref_dump_slots.argtypes = [ctypes.c_void_p, c_u64_p, c_u64_p, c_i64_p, c_i32_p,
                                        c_u64_p, c_u64_p, c_u64_p, c_double_p]
+        lib.ref_snapshot.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p,
+                                     ctypes.c_int64, c_i64_p]
         lib.ref_router_state.argtypes = [ctypes.c_void_p, c_double_p, c_u64_p, c_u64_p,
                                          c_double_p, c_u64_p, c_u64_p]
         lib.ref_sched_state.argtypes = [ctypes.c_void_p, c_double_p, c_double_p, c_u64_p]
@@ -264,6 +269,14 @@ class OracleEngine(_StepMixin):
             _ptr(out["per_layer"], c_double_p))
         return out
 
+    def snapshot(self, now):
+        """KVStore::snapshot(now) restated (po_engine_snapshot)."""
+        n = ctypes.c_int64(0)
+        self.lib.po_engine_snapshot(self.h, now, None, 0, ctypes.byref(n))
+        out = np.zeros(n.value, dtype=SNAPSHOT_DTYPE)
+        self.lib.po_engine_snapshot(self.h, now, out.ctypes.data, n.value, ctypes.byref(n))
+        return out
+
     def set_attn_mass(self, attn_mass, per_layer=None):
         a = np.ascontiguousarray(attn_mass, dtype=np.float64)
         p = None if per_layer is None else np.ascontiguousarray(per_layer, dtype=np.float64)
@@ -328,6 +341,14 @@ class RefEngine(_StepMixin):
         if rc:
             raise RuntimeError("ref step error %d" % rc)
         return self._collect(self.out)
+
+    def snapshot(self, now):
+        """The reference's own KVStore::snapshot(now)."""
+        n = ctypes.c_int64(0)
+        self.lib.ref_snapshot(self.h, now, None, 0, ctypes.byref(n))
+        out = np.zeros(n.value, dtype=SNAPSHOT_DTYPE)
+        self.lib.ref_snapshot(self.h, now, out.ctypes.data, n.value, ctypes.byref(n))
+        return out
 
     def slots(self, n_slots):
         cols = {"id": np.uint64, "shard_seq": np.uint64, "token": np.int64, "expert": np.int32,

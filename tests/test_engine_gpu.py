@@ -28,6 +28,7 @@ if not torch.cuda.is_available():  # pragma: no cover
     pytest.skip("no CUDA device", allow_module_level=True)
 
 from paper_2508_06526_b200.engine import Engine  # noqa: E402
+from paper_2508_06526_b200.wire import store_dump_lines  # noqa: E402
 
 Y_TOL = 2e-5
 
@@ -114,6 +115,12 @@ def run_parity(cfg, T, seed, inject=True, basis=None, bias=None, kept=None, chec
             assert sa["running_hit"] == sb["running_hit"] and sa["theta"] == sb["theta"]
             st_a, st_b = eng.store_stats(s), orc[s].store_stats()
             assert st_a == st_b
+            # KVStore::snapshot on the GPU and its JSONL lines
+            for now in (-1, T + 7):
+                sa = eng.snapshot(s, now)
+                sb = orc[s].snapshot(T if now < 0 else now)
+                assert np.array_equal(sa, sb), (s, now)
+            assert store_dump_lines(sa) == store_dump_lines(sb)
     return eng, orc
 
 
