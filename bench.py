@@ -77,6 +77,45 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
+def cost_model_block(cfg, w, summ, ms_step, peak_gbs):
+    """The reference's analytic model (costmodel.cpp, restated bit-exactly in
+    paper_2508_06526_b200/costmodel.py) evaluated for this workload on the
+    measured B200 peaks, beside the measured counterparts (runner.cpp:199-205:
+    I/O measured vs modelled at the measured mean attended prefix)."""
+    from paper_2508_06526_b200.costmodel import (b200_profile, io_and_roofline, latency_step,
+                                                 optimal_shard_size)
+    bf16 = 1672.3
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            bf16 = float(json.load(f).get("bf16_tflops", bf16))
+    except Exception:
+        pass
+    m, B, k = cfg.model, w["B"], w["k"]
+    hw = b200_profile(peak_gbs, bf16)
+    lat = latency_step(m, hw, float(B))
+    roof = io_and_roofline(m, hw, float(B))
+    shard = optimal_shard_size(m)
+    dp = cfg.stored_width
+    head = min(m.head_width, dp)
+    fetch = sum(s["fetch_elements"] for s in summ)            # pipeline.cpp:262-264
+    retrieved = sum(s["n_attended"] for s in summ)
+    hits, lookups = sum(s["hits"] for s in summ), sum(s["lookups"] for s in summ)
+    mean_prefix = retrieved / k if lookups else 0.0          # per expert, this step
+    io_model = (2.0 * head + dp) * mean_prefix * k
+    return {"source": "costmodel.cpp:8-133 (bit-exact restatement, tests/test_costmodel.py)",
+            "hw": {"beta_gbs": peak_gbs, "gamma_gbs": peak_gbs, "peak_bf16_tflops": bf16},
+            "t_step_model_s": lat.step, "t_step_measured_s": ms_step * 1e-3,
+            "io_sparse_model_elements": roof.io_sparse, "io_dense_model_elements": roof.io_dense,
+            "io_measured_elements": fetch, "io_model_at_measured_prefix": io_model,
+            "io_measured_over_model": fetch / io_model if io_model else 1.0,
+            "hit_rate_model": roof.hit_rate,
+            "hit_rate_measured": hits / lookups if lookups else 0.0,
+            "arith_intensity": roof.arith_intensity, "compute_bound": roof.compute_bound,
+            "throughput_scaling_model": roof.throughput_scaling,
+            "shard_size_opt": shard.exact, "shard_size_opt_integer": shard.best_integer,
+            "shard_size_used": m.S}
+
+
 def make_config(w, world=1, rank=0, G=None):
     from paper_2508_06526_b200.config import (CompressorConfig, EngineConfig, ModelConfig,
                                               RouterConfig, SchedulerConfig, StoreConfig)
@@ -424,6 +463,7 @@ def main():
                      "peak_kind": peak_kind, "avg_launch_ms": attend_avg_ms,
                      "algorithmic_bytes_per_launch": alg_bytes / max(n_launch, 1)},
         "phase_ms": phase_avg,
+        "cost_model": cost_model_block(cfg, w, summ, ms / args.steps, peak),
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "e2e": e2e,

@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "pikv/errors.hpp"
+#include "pikv/costmodel.hpp"
 #include "pikv/kvstore.hpp"
 #include "pikv/pipeline.hpp"
 #include "pikv/rng.hpp"
@@ -305,6 +306,41 @@ int ref_dump_slots(ref_engine* e, uint64_t* id, uint64_t* shard_seq, int64_t* to
         }
     }
     return 0;
+}
+
+// The reference's own cost_report (costmodel.cpp:123-135), flattened:
+// out[0..2] memory, [3..5] memory_bytes, [6..10] shard (exact, floor, ceil,
+// best_integer, best_cost), [11..13] latency, [14..21] roofline (io_dense,
+// io_sparse, rd_dense, rd_sparse, hit_rate, arith_intensity,
+// throughput_scaling, compute_bound), [22..24] utilization (eta, threshold,
+// pass), [25] mem_total_optimal, [26] speedup(1, rho).  hw = beta, gamma,
+// eta, peak_compute, peak_mem_bw.
+int ref_cost_report(const pikv_config* c, const double* hw, double batch, int active, double thr,
+                    double* out) {
+    try {
+        const ModelConfig m = model_of(*c);
+        HardwareProfile h;
+        h.hbm_bandwidth = hw[0];
+        h.core_throughput = hw[1];
+        h.decode_factor = hw[2];
+        h.peak_compute = hw[3];
+        h.peak_mem_bw = hw[4];
+        const CostReport r = cost_report(m, h, batch, active, thr);
+        const double v[] = {r.memory.token, r.memory.page, r.memory.total,
+                            r.memory_bytes.token, r.memory_bytes.page, r.memory_bytes.total,
+                            r.shard.exact, (double)r.shard.floor_candidate, (double)r.shard.ceil_candidate,
+                            (double)r.shard.best_integer, r.shard.best_cost,
+                            r.latency.read, r.latency.decode, r.latency.step,
+                            r.roofline.io_dense, r.roofline.io_sparse, r.roofline.rd_dense,
+                            r.roofline.rd_sparse, r.roofline.hit_rate, r.roofline.arith_intensity,
+                            r.roofline.throughput_scaling, r.roofline.compute_bound ? 1.0 : 0.0,
+                            r.utilization.eta_util, r.utilization.threshold, r.utilization.pass ? 1.0 : 0.0,
+                            mem_total_optimal(m), speedup(1.0, m.rho)};
+        std::memcpy(out, v, sizeof(v));
+        return 0;
+    } catch (const std::exception& ex) {
+        return code_of(ex);
+    }
 }
 
 // The reference's own KVStore::snapshot (kvstore.cpp:206-221).
