@@ -238,6 +238,18 @@ int pikv_step(pikv_engine* eng, const void* q, const void* k, const void* v,
  * runs the step and copies y back, synchronising before returning. */
 int pikv_step_host(pikv_engine* eng, const void* q, const void* k, const void* v,
                    const double* saliency, float* y_out);
+/* Engine::step(TokenInput) from the tokens' embeddings, pipeline.cpp:213-351
+ * including the encode at :222: the QueryEncoder (pipeline.cpp:29-57; seeded
+ * like the reference, cfg.seed ^ 0x71c9de52ae0aef, unless replaced by
+ * pikv_set_encoder_host) runs on the GPU in fp64 with the reference's
+ * summation order, so routing is bit-exact; K/V are stored in cfg.kv_dtype.
+ * emb: device [B][d] fp64 (pikv_step_embed) or host (pikv_step_embed_host). */
+int pikv_step_embed(pikv_engine* eng, const double* emb, const double* saliency, float* y_out);
+int pikv_step_embed_host(pikv_engine* eng, const double* emb, const double* saliency,
+                         float* y_out);
+/* Replace the QueryEncoder's matrices (each [d][d] row-major fp64, host). */
+int pikv_set_encoder_host(pikv_engine* eng, const double* w_query, const double* w_key,
+                          const double* w_value);
 /* Multi-rank step: run the rank-local part, exchange the merge records with
  * an all-gather (caller-provided, e.g. NCCL), then finish.  The exchange
  * buffer is device memory of pikv_exchange_bytes() per rank. */

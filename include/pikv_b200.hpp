@@ -201,8 +201,13 @@ struct EngineConfig {  // pipeline.hpp:87-98 (+ B200 runtime fields)
 
 // ---- step I/O (pipeline.hpp:59-85) ----------------------------------------
 struct TokenInput {
-    std::vector<double> query, key, value;  // width d, rounded to kv_dtype by the engine
+    // The reference's TokenInput (pipeline.hpp:59-62): the token's embedding
+    // (width d); the step runs the QueryEncoder on the GPU (pipeline.cpp:222).
+    std::vector<double> embedding;
     std::vector<double> layer_saliency;     // n_layers (Duo)
+    // Alternatively the already-encoded q/k/v (width d, rounded to kv_dtype
+    // by the engine): used when `embedding` is empty.
+    std::vector<double> query, key, value;
 };
 
 struct EvictionRecord {  // scheduler.hpp:90-98
@@ -267,11 +272,22 @@ class Engine {
         const int B = cfg_.batch, d = cfg_.model.d, k = cfg_.router.k, E = cfg_.model.E;
         if (static_cast<int>(tokens.size()) != B) throw InvalidArgument("Engine::step: one token per stream");
         const bool bf16 = cfg_.kv_dtype == DType::BF16;
+        const bool embed = !tokens.empty() && !tokens[0].embedding.empty();
         std::vector<std::uint16_t> qb, kb, vb;
         std::vector<float> qf, kf, vf;
+        std::vector<double> emb;
         std::vector<double> sal(static_cast<std::size_t>(B) * (cfg_.n_layers > 0 ? cfg_.n_layers : 1));
         for (int s = 0; s < B; ++s) {
             const TokenInput& t = tokens[s];
+            for (int l = 0; l < cfg_.n_layers; ++l)
+                sal[static_cast<std::size_t>(s) * cfg_.n_layers + l] =
+                    l < static_cast<int>(t.layer_saliency.size()) ? t.layer_saliency[l] : 0.0;
+            if (embed) {
+                if (static_cast<int>(t.embedding.size()) != d)
+                    throw InvalidArgument("Engine::step: embedding width mismatch");  // pipeline.cpp:214-216
+                emb.insert(emb.end(), t.embedding.begin(), t.embedding.end());
+                continue;
+            }
             if (static_cast<int>(t.query.size()) != d || static_cast<int>(t.key.size()) != d ||
                 static_cast<int>(t.value.size()) != d)
                 throw InvalidArgument("Engine::step: embedding width mismatch");  // pipeline.cpp:214-216
@@ -284,16 +300,17 @@ class Engine {
                     vf.push_back(static_cast<float>(t.value[i]));
                 }
             }
-            for (int l = 0; l < cfg_.n_layers; ++l)
-                sal[static_cast<std::size_t>(s) * cfg_.n_layers + l] =
-                    l < static_cast<int>(t.layer_saliency.size()) ? t.layer_saliency[l] : 0.0;
         }
         const int dp = stored_width();
         std::vector<float> y(static_cast<std::size_t>(B) * dp);
-        const void* q = bf16 ? static_cast<const void*>(qb.data()) : qf.data();
-        const void* kk = bf16 ? static_cast<const void*>(kb.data()) : kf.data();
-        const void* v = bf16 ? static_cast<const void*>(vb.data()) : vf.data();
-        check(pikv_step_host(h_, q, kk, v, cfg_.n_layers > 0 ? sal.data() : nullptr, y.data()));
+        if (embed) {
+            check(pikv_step_embed_host(h_, emb.data(), cfg_.n_layers > 0 ? sal.data() : nullptr, y.data()));
+        } else {
+            const void* q = bf16 ? static_cast<const void*>(qb.data()) : qf.data();
+            const void* kk = bf16 ? static_cast<const void*>(kb.data()) : kf.data();
+            const void* v = bf16 ? static_cast<const void*>(vb.data()) : vf.data();
+            check(pikv_step_host(h_, q, kk, v, cfg_.n_layers > 0 ? sal.data() : nullptr, y.data()));
+        }
         check(pikv_sync(h_));
         std::vector<std::int32_t> ex(static_cast<std::size_t>(B) * k);
         std::vector<double> gates(static_cast<std::size_t>(B) * k);

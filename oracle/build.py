@@ -6,7 +6,8 @@
 * ``build_ref()`` compiles the REFERENCE's own code from /root/reference
   (present only in the build container) into ``oracle/_ref/libpikv_ref.so``:
     - mathops.cpp, kvstore.cpp, router.cpp: compiled unchanged, in place;
-    - scheduler.cpp lines 49-80 and 162-350 and pipeline.cpp lines 59-85:
+    - scheduler.cpp lines 49-80 and 162-350 and pipeline.cpp lines 29-57
+      (QueryEncoder) and 59-85 (attention):
       line-extracted (sha256-verified) into oracle/_ref/ because the rest of
       those files needs Eigen (absent) and scheduler.cpp:352-377 does not
       compile (SURVEY §0.5).  The extracted lines are byte-identical;
@@ -33,6 +34,8 @@ EXTRACTS = [
      "30cdc95c732fad259c0eb492ffc0422286c3f75f7833e1c7581609580d9900f7"),
     ("src/pipeline.cpp", 59, 85,
      "0b7a58bb7cf2a88e9dc9a5104abcacda680d760ba71f6d5b5c4e2ddb930bc5f2"),
+    ("src/pipeline.cpp", 29, 57,  # QueryEncoder (the step's encode, pipeline.cpp:222)
+     "94bea718658aadb9356db62905d46ab4460b919e090f97e3d4d0d2f1a581388a"),
 ]
 
 
@@ -87,8 +90,8 @@ def build_ref(force: bool = False) -> str | None:
              "namespace pikv {\n"
              + _extract(*EXTRACTS[0]) + _extract(*EXTRACTS[1]) + "}  // namespace pikv\n")
     pipe = ('#include "pikv/pipeline.hpp"\n#include <cmath>\n#include "pikv/errors.hpp"\n'
-            '#include "pikv/mathops.hpp"\nnamespace pikv {\n'
-            + _extract(*EXTRACTS[2]) + "}  // namespace pikv\n")
+            '#include "pikv/mathops.hpp"\n#include "pikv/rng.hpp"\nnamespace pikv {\n'
+            + _extract(*EXTRACTS[3]) + _extract(*EXTRACTS[2]) + "}  // namespace pikv\n")
     gen = {"scheduler_extract.cpp": sched, "pipeline_extract.cpp": pipe}
     for name, text in gen.items():
         with open(os.path.join(REF_OUT, name), "w") as f:

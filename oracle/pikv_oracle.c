@@ -495,6 +495,8 @@ struct po_engine {
     double* basis; /* [H][r][hd] */
     double* bias;  /* [d] */
     int32_t* kept; /* [H][r] */
+    /* QueryEncoder (pipeline.cpp:29-57), generated on first embedding step */
+    double* enc_w;  /* [3][d][d]: w_query, w_key, w_value row-major */
     /* scratch */
     double* stage_k;
     double* stage_v;
@@ -602,7 +604,7 @@ void po_engine_destroy(po_engine* e) {
     if (!e) return;
     free(e->slots), free(e->payload), free(e->layers), free(e->head), free(e->live);
     free(e->seq), free(e->basis), free(e->bias), free(e->kept);
-    free(e->stage_k), free(e->stage_v);
+    free(e->stage_k), free(e->stage_v), free(e->enc_w);
     po_router_destroy(e->router);
     free(e);
 }
@@ -1060,6 +1062,57 @@ static int engine_step_impl(po_engine* e, const double* q, const double* k, cons
         e->theta += c->adakv_step * (c->target_hit - e->running_hit); /* :340-342 */
     e->now += 1;
     return PIKV_OK;
+}
+
+/* QueryEncoder(width, seed), pipeline.cpp:29-36: w_query, w_key, w_value
+ * drawn in that order from one Rng, each normal_vector(width^2, 1/sqrt(width)). */
+void po_encoder_weights(int width, uint64_t seed, double* w3) {
+    po_rng r;
+    po_rng_init(&r, seed);
+    const double scale = 1.0 / sqrt((double)width);
+    const int64_t n = (int64_t)width * width;
+    for (int64_t i = 0; i < 3 * n; ++i) w3[i] = scale * po_rng_normal(&r);
+}
+
+/* QueryEncoder::apply / encode, pipeline.cpp:38-57: out[i] = sum_j W[i][j] x[j]
+ * in j order, for W = w_query, w_key, w_value. */
+void po_encode(const double* w3, int width, const double* x, double* q, double* k, double* v) {
+    double* outs[3] = {q, k, v};
+    for (int m = 0; m < 3; ++m) {
+        const double* W = w3 + (size_t)m * width * width;
+        for (int i = 0; i < width; ++i) {
+            const double* row = W + (size_t)i * width;
+            double s = 0.0;
+            for (int j = 0; j < width; ++j) s += row[j] * x[j];
+            outs[m][i] = s;
+        }
+    }
+}
+
+#define PO_ENCODER_SALT 0x71c9de52ae0aefULL /* pipeline.cpp:15 kEncoderSalt */
+
+/* Engine::step from the token's embedding (pipeline.cpp:213-351 incl. the
+ * encode at :222).  q stays fp64 (routing is bit-exact); k and v are rounded
+ * to the storage dtype, as the engine stores them. */
+int po_engine_step_embed(po_engine* e, const double* emb, const double* saliency, po_step_out* out,
+                         int attend) {
+    const int d = e->c.d;
+    if (!e->enc_w) {
+        e->enc_w = (double*)malloc(sizeof(double) * 3 * (size_t)d * d);
+        if (!e->enc_w) return PIKV_ERR_OUT_OF_MEMORY;
+        po_encoder_weights(d, e->c.seed ^ PO_ENCODER_SALT, e->enc_w);
+    }
+    double* q = (double*)malloc(sizeof(double) * 3 * (size_t)d);
+    double* k = q + d;
+    double* v = k + d;
+    po_encode(e->enc_w, d, emb, q, k, v);
+    for (int i = 0; i < d; ++i) {
+        k[i] = round_to_dtype(k[i], e->c.kv_dtype);
+        v[i] = round_to_dtype(v[i], e->c.kv_dtype);
+    }
+    const int rc = engine_step_impl(e, q, k, v, saliency, out, attend);
+    free(q);
+    return rc;
 }
 
 int po_engine_step(po_engine* e, const double* q, const double* k, const double* v,

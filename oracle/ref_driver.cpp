@@ -343,6 +343,21 @@ int ref_cost_report(const pikv_config* c, const double* hw, double batch, int ac
     }
 }
 
+// The reference's own QueryEncoder (pipeline.cpp:29-57): construct from the
+// seed and encode one embedding.
+int ref_encode(int width, uint64_t seed, const double* x, double* q, double* k, double* v) {
+    try {
+        QueryEncoder enc(width, seed);
+        const auto r = enc.encode(std::span<const double>(x, static_cast<std::size_t>(width)));
+        std::memcpy(q, r.query.data(), sizeof(double) * width);
+        std::memcpy(k, r.key.data(), sizeof(double) * width);
+        std::memcpy(v, r.value.data(), sizeof(double) * width);
+        return 0;
+    } catch (const std::exception& ex) {
+        return code_of(ex);
+    }
+}
+
 // The reference's own KVStore::snapshot (kvstore.cpp:206-221).
 int ref_snapshot(ref_engine* e, uint64_t now, pikv_snapshot_record* out, int64_t cap, int64_t* n_out) {
     const auto recs = e->store.snapshot(now);

@@ -64,8 +64,6 @@ bool is_pow2(int n) { return n >= 1 && (n & (n - 1)) == 0; }
 
 constexpr uint64_t kRouterSalt = 0x2545f4914f6cdd1dULL;  // pipeline.cpp:16
 
-// RouterState::init (router.cpp:54-67): W_r = Rng(seed).normal_vector(E*d,
-// 1/sqrt(d)), with pikv::Rng's transforms over std::mt19937_64 (rng.hpp).
 // W_r [E][d] (row-major, router.cpp:54-67) -> the device layout: chunks of
 // route_ch columns, each [E][route_ch + 2] with zero padding (State::W).
 static size_t router_w_elems(const Dims& D) {
@@ -81,7 +79,11 @@ static std::vector<double> pack_router_w(const Dims& D, const double* w) {
     return out;
 }
 
-std::vector<double> router_matrix(int E, int d, uint64_t seed) {
+// n draws of Rng(seed).normal() * 1/sqrt(width): pikv::Rng's transforms
+// over std::mt19937_64 (rng.hpp).  RouterState::init (router.cpp:54-67):
+// W_r = normal_vector(E*d, 1/sqrt(d)); QueryEncoder (pipeline.cpp:29-36):
+// w_query, w_key, w_value = three consecutive normal_vector(d*d, 1/sqrt(d)).
+std::vector<double> reference_normals(size_t n, int width, uint64_t seed) {
     std::mt19937_64 gen(seed);
     auto uniform = [&]() { return static_cast<double>(gen() >> 11) * 0x1.0p-53; };
     bool has_spare = false;
@@ -100,11 +102,17 @@ std::vector<double> router_matrix(int E, int d, uint64_t seed) {
         has_spare = true;
         return radius * std::cos(angle);
     };
-    const double scale = 1.0 / std::sqrt(static_cast<double>(d));
-    std::vector<double> w(static_cast<size_t>(E) * d);
+    const double scale = 1.0 / std::sqrt(static_cast<double>(width));
+    std::vector<double> w(n);
     for (auto& x : w) x = scale * normal();
     return w;
 }
+
+std::vector<double> router_matrix(int E, int d, uint64_t seed) {
+    return reference_normals(static_cast<size_t>(E) * d, d, seed);
+}
+
+constexpr uint64_t kEncoderSalt = 0x71c9de52ae0aefULL;  // pipeline.cpp:15
 
 }  // namespace
 
@@ -122,6 +130,11 @@ struct pikv_engine {
     void* in_k = nullptr;
     void* in_v = nullptr;
     double* in_sal = nullptr;
+    // QueryEncoder (pipeline.cpp:29-57) for the embedding step, allocated on
+    // first use: W^T [3][d][d] fp64, the step's fp64 q, host-path staging
+    double* enc_wt = nullptr;
+    double* q64 = nullptr;
+    double* in_emb = nullptr;
     float* out_y = nullptr;
     // graph cache keyed by (q, k, v, saliency, y, attend)
     std::map<std::tuple<const void*, const void*, const void*, const void*, void*, int>,
@@ -761,8 +774,9 @@ static void mark(pikv_engine* eng, int phase) {
 
 // The step's launch sequence (pipeline.cpp:213-351 ordering).
 static int enqueue_local(pikv_engine* eng, const void* q, const void* k, const void* v,
-                         const double* sal, bool attend, float* y) {
-    const Dims& D = eng->D;
+                         const double* sal, bool attend, float* y, bool q_f64 = false) {
+    Dims D = eng->D;
+    D.q_f64 = q_f64 ? 1 : 0;
     const State& S = eng->S;
     cudaStream_t st = eng->stream;
     int n = 0;
@@ -824,8 +838,23 @@ static int enqueue_finish(pikv_engine* eng, const uint8_t* gathered, float* y, b
     return PIKV_OK;
 }
 
+// emb != nullptr: the step starts from the tokens' embeddings (Engine::step,
+// pipeline.cpp:222): the QueryEncoder kernel writes q (fp64) and the stored
+// K/V, then the step proceeds on them.
+static int enqueue_step(pikv_engine* eng, const double* emb, const void* q, const void* k, const void* v,
+                        const double* sal, float* y, bool attend) {
+    if (emb) {
+        launch_encode(eng->D, eng->enc_wt, emb, eng->q64, eng->in_k, eng->in_v, eng->stream);
+        q = eng->q64, k = eng->in_k, v = eng->in_v;
+    }
+    int rc = enqueue_local(eng, q, k, v, sal, attend, y, emb != nullptr);
+    if (!rc) rc = enqueue_finish(eng, eng->S.exchange, y, attend, 1);
+    if (emb) eng->kernels_per_step += (eng->D.B + 63) / 64;
+    return rc;
+}
+
 static int run_step(pikv_engine* eng, const void* q, const void* k, const void* v,
-                    const double* sal, float* y, bool attend) {
+                    const double* sal, float* y, bool attend, const double* emb = nullptr) {
     int rc = codec_ready(eng);
     if (rc) return rc;
     if (eng->D.world != 1)
@@ -833,20 +862,19 @@ static int run_step(pikv_engine* eng, const void* q, const void* k, const void* 
     cudaSetDevice(eng->device);
     const bool use_graph = eng->warmed && !eng->profiling;
     if (!use_graph) {
-        rc = enqueue_local(eng, q, k, v, sal, attend, y);
-        if (!rc) rc = enqueue_finish(eng, eng->S.exchange, y, attend, 1);
+        rc = enqueue_step(eng, emb, q, k, v, sal, y, attend);
         if (rc) return rc;
         eng->warmed = true;  // first eager pass sets kernel attributes
         eng->launches += eng->kernels_per_step;
         return PIKV_OK;
     }
-    auto key = std::make_tuple(q, k, v, (const void*)sal, (void*)y, attend ? 1 : 0);
+    auto key = std::make_tuple(emb ? (const void*)emb : q, k, v, (const void*)sal, (void*)y,
+                               (attend ? 1 : 0) + (emb ? 2 : 0));
     auto it = eng->graphs.find(key);
     if (it == eng->graphs.end()) {
         cudaGraph_t g;
         CUDA_TRY(cudaStreamBeginCapture(eng->stream, cudaStreamCaptureModeThreadLocal));
-        rc = enqueue_local(eng, q, k, v, sal, attend, y);
-        if (!rc) rc = enqueue_finish(eng, eng->S.exchange, y, attend, 1);
+        rc = enqueue_step(eng, emb, q, k, v, sal, y, attend);
         cudaError_t ce = cudaStreamEndCapture(eng->stream, &g);
         if (rc) return rc;
         if (ce != cudaSuccess) return fail(PIKV_ERR_CUDA, std::string("capture: ") + cudaGetErrorString(ce));
@@ -867,6 +895,74 @@ static int run_step(pikv_engine* eng, const void* q, const void* k, const void* 
 int pikv_step(pikv_engine* eng, const void* q, const void* k, const void* v, const double* saliency,
               float* y_out) {
     return run_step(eng, q, k, v, saliency, y_out, true);
+}
+
+// QueryEncoder weights on the device as W^T [3][d][d] (k_encode layout).
+static int upload_encoder(pikv_engine* eng, const double* wq, const double* wk, const double* wv) {
+    const int d = eng->D.d;
+    const size_t dd = (size_t)d * d;
+    if (!eng->enc_wt) {
+        eng->enc_wt = eng->alloc<double>(3 * dd);
+        eng->q64 = eng->alloc<double>((size_t)eng->D.B * d);
+        eng->in_emb = eng->alloc<double>((size_t)eng->D.B * d);
+        if (!eng->enc_wt || !eng->q64 || !eng->in_emb)
+            return fail(PIKV_ERR_OUT_OF_MEMORY, "cudaMalloc failed (QueryEncoder weights)");
+    }
+    std::vector<double> t(dd);
+    const double* w3[3] = {wq, wk, wv};
+    for (int m = 0; m < 3; ++m) {
+        for (int i = 0; i < d; ++i)
+            for (int j = 0; j < d; ++j) t[(size_t)j * d + i] = w3[m][(size_t)i * d + j];
+        CUDA_TRY(cudaMemcpy(eng->enc_wt + (size_t)m * dd, t.data(), sizeof(double) * dd, cudaMemcpyHostToDevice));
+    }
+    return PIKV_OK;
+}
+
+static int encoder_ready(pikv_engine* eng) {
+    if (eng->enc_wt) return PIKV_OK;
+    const int d = eng->D.d;
+    const size_t dd = (size_t)d * d;
+    // QueryEncoder(d, seed ^ kEncoderSalt), pipeline.cpp:29-36, 89
+    const auto w = reference_normals(3 * dd, d, eng->cfg.seed ^ kEncoderSalt);
+    return upload_encoder(eng, w.data(), w.data() + dd, w.data() + 2 * dd);
+}
+
+int pikv_set_encoder_host(pikv_engine* eng, const double* w_query, const double* w_key,
+                          const double* w_value) {
+    if (!w_query || !w_key || !w_value) return fail(PIKV_ERR_INVALID_ARGUMENT, "encoder matrix is NULL");
+    cudaSetDevice(eng->device);
+    CUDA_TRY(cudaStreamSynchronize(eng->stream));
+    return upload_encoder(eng, w_query, w_key, w_value);
+}
+
+int pikv_step_embed(pikv_engine* eng, const double* emb, const double* saliency, float* y_out) {
+    if (!emb) return fail(PIKV_ERR_INVALID_ARGUMENT, "embedding is NULL");
+    cudaSetDevice(eng->device);
+    int rc = encoder_ready(eng);
+    if (rc) return rc;
+    return run_step(eng, nullptr, nullptr, nullptr, saliency, y_out, true, emb);
+}
+
+int pikv_step_embed_host(pikv_engine* eng, const double* emb, const double* saliency, float* y_out) {
+    if (!emb) return fail(PIKV_ERR_INVALID_ARGUMENT, "embedding is NULL");
+    const Dims& D = eng->D;
+    cudaSetDevice(eng->device);
+    int rc = encoder_ready(eng);
+    if (rc) return rc;
+    cudaStream_t st = eng->stream;
+    CUDA_TRY(cudaMemcpyAsync(eng->in_emb, emb, sizeof(double) * D.B * D.d, cudaMemcpyHostToDevice, st));
+    const double* sal = nullptr;
+    if (saliency && D.n_layers > 0) {
+        CUDA_TRY(cudaMemcpyAsync(eng->in_sal, saliency, sizeof(double) * D.B * D.n_layers,
+                                 cudaMemcpyHostToDevice, st));
+        sal = eng->in_sal;
+    }
+    rc = run_step(eng, nullptr, nullptr, nullptr, sal, eng->out_y, true, eng->in_emb);
+    if (rc) return rc;
+    if (y_out)
+        CUDA_TRY(cudaMemcpyAsync(y_out, eng->out_y, sizeof(float) * D.B * D.dp, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return PIKV_OK;
 }
 
 int pikv_step_host(pikv_engine* eng, const void* q, const void* k, const void* v,

@@ -96,8 +96,15 @@ __device__ __forceinline__ const int* route_body(const Dims& D, const Cfg& C, co
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    // query in fp64 (exact upcast of bf16/f32); 16-byte loads, all in flight
-    {
+    // query in fp64 (exact upcast of bf16/f32, or the encoder's fp64 q);
+    // 16-byte loads, all in flight
+    if (D.q_f64) {
+        const double2* qd = (const double2*)((const double*)qin + (int64_t)s * D.d);
+        if (D.d % 2 == 0)
+            for (int v = tid; v < D.d / 2; v += blockDim.x) ((double2*)sm_q)[v] = qd[v];
+        else
+            for (int i = tid; i < D.d; i += blockDim.x) sm_q[i] = ((const double*)qin)[(int64_t)s * D.d + i];
+    } else {
         const int esz = D.kv_dtype == PIKV_DTYPE_BF16 ? 2 : 4;
         const int nvec = (D.d * esz) / 16;
         const uint8_t* qb = (const uint8_t*)qin + (int64_t)s * D.d * esz;
@@ -462,7 +469,8 @@ __global__ void k_project(Dims D, State S, const void* __restrict__ qin, const v
     for (int t = tid; t < r * hd; t += nt) bs[t] = S.basis[(int64_t)h * r * hd + t];
     for (int t = tid; t < D.B * hd; t += nt) {
         const int b = t / hd, i = t % hd;
-        float xi = load_in(x, D.kv_dtype, (int64_t)b * D.d + h * hd + i);
+        float xi = (row == 0 && D.q_f64) ? (float)((const double*)x)[(int64_t)b * D.d + h * hd + i]
+                                          : load_in(x, D.kv_dtype, (int64_t)b * D.d + h * hd + i);
         if (D.codec == PIKV_CODEC_LORAPLUS) xi -= S.cbias[h * hd + i];
         xs[t] = xi;
     }
@@ -837,7 +845,18 @@ __device__ __forceinline__ void insert_body(const Dims& D, const Cfg& C, const S
         const int hd = D.d / D.H, r = D.dph;
         const int64_t base = (int64_t)s * D.d;
         float* qa = S.q_attn + (int64_t)s * D.dp;
-        if (!proj && D.kv_dtype == PIKV_DTYPE_BF16 && D.d % 8 == 0) {
+        if (D.q_f64) {  // encoder output: fp64 -> fp32 (projections use the same input)
+            const double* q64 = (const double*)qin + base;
+            if (!proj) {
+                for (int o = t0; o < D.d; o += nt) qa[o] = (float)q64[o];
+            } else if (D.codec == PIKV_CODEC_FASTV || D.codec == PIKV_CODEC_PRUNE) {
+                for (int o = t0; o < D.dp; o += nt) {
+                    const int h = o / r, j = o % r;
+                    const int i = D.codec == PIKV_CODEC_FASTV ? j : S.kept[h * r + j];
+                    qa[o] = (float)q64[h * hd + i];
+                }
+            }
+        } else if (!proj && D.kv_dtype == PIKV_DTYPE_BF16 && D.d % 8 == 0) {
             const uint4* src = (const uint4*)((const uint16_t*)qin + base);
             for (int v = t0; v < D.d / 8; v += nt) {
                 const uint4 w = src[v];
@@ -2224,6 +2243,94 @@ void launch_foldback(const Dims& D, const Cfg& C, const State& S, cudaStream_t s
 }
 void launch_feedback(const Dims& D, const Cfg& C, const State& S, cudaStream_t st) {
     launch_pdl(k_feedback, dim3((D.B + 127) / 128), dim3(128), 0, st, D, C, S);
+}
+
+// ===========================================================================
+// encode: QueryEncoder::encode (pipeline.cpp:38-57) of every stream's token
+// ===========================================================================
+// q, k, v = W_{q,k,v} x in fp64 with the reference's sequential order
+// (s = ((0 + W[i][0] x0) + W[i][1] x1) + ..., __dmul_rn/__dadd_rn: no FMA),
+// so routing on q is bit-exact.  wt = [3][d][d] transposed (wt[m][j][i] =
+// W_m[i][j]): lane = output row i, so every column step is one coalesced
+// 256-byte row segment per warp; warp w owns NB streams (NB chains per
+// thread, interleaved); the streams' embedding columns are staged through
+// shared memory in chunks.  One launch covers <= 4 * NB streams.
+constexpr int kEncWarps = 4;
+template <int NB>
+__global__ void __launch_bounds__(kEncWarps * 32)
+    k_encode(Dims D, const double* __restrict__ wt, const double* __restrict__ emb, int b0, int chunk,
+             double* __restrict__ q64, void* __restrict__ kout, void* __restrict__ vout) {
+    griddep_enter();
+    extern __shared__ double xs[];  // [kEncWarps * NB][chunk]
+    const int d = D.d, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int row = blockIdx.x * 32 + lane;  // in [0, 3d)
+    const bool on = row < 3 * d;
+    const int m = on ? row / d : 0, r = on ? row % d : 0;
+    const double* w = wt + (size_t)m * d * d + r;
+    const int nsb = kEncWarps * NB;
+    double acc[NB];
+#pragma unroll
+    for (int u = 0; u < NB; ++u) acc[u] = 0.0;
+    for (int c0 = 0; c0 < d; c0 += chunk) {
+        const int wn = min(chunk, d - c0);
+        __syncthreads();
+        for (int t = tid; t < nsb * chunk; t += blockDim.x) {
+            const int sb = t / chunk, jj = t % chunk, b = b0 + sb;
+            xs[t] = (b < D.B && jj < wn) ? emb[(int64_t)b * d + c0 + jj] : 0.0;
+        }
+        __syncthreads();
+        if (on) {
+            const double* wc = w + (size_t)c0 * d;
+            const double* xw = xs + warp * NB * chunk;
+#pragma unroll 4
+            for (int jj = 0; jj < wn; ++jj) {
+                const double wv = wc[(size_t)jj * d];
+#pragma unroll
+                for (int u = 0; u < NB; ++u) acc[u] = __dadd_rn(acc[u], __dmul_rn(wv, xw[u * chunk + jj]));
+            }
+        }
+    }
+    if (!on) return;
+#pragma unroll
+    for (int u = 0; u < NB; ++u) {
+        const int b = b0 + warp * NB + u;
+        if (b >= D.B) continue;
+        const int64_t o = (int64_t)b * d + r;
+        if (m == 0) {
+            q64[o] = acc[u];
+        } else {
+            void* dst = m == 1 ? kout : vout;
+            const float f = (float)acc[u];  // stored K/V: fp64 -> fp32 (-> bf16 RNE)
+            if (D.kv_dtype == PIKV_DTYPE_BF16) ((uint16_t*)dst)[o] = f32_to_bf16_rne(f);
+            else ((float*)dst)[o] = f;
+        }
+    }
+}
+
+int encode_chunk(const Dims& D, int nb) {
+    int c = (40 * 1024) / (8 * kEncWarps * nb);
+    c = c >= 32 ? c & ~31 : c;
+    return std::max(1, std::min(c, D.d));
+}
+
+void launch_encode(const Dims& D, const double* wt, const double* emb, double* q64, void* kout, void* vout,
+                   cudaStream_t st) {
+    // chains per thread: enough warps x NB to cover B in as few launches as
+    // possible, NB <= 16
+    int nb = 1;
+    while (nb < 16 && kEncWarps * nb < D.B) nb *= 2;
+    const int chunk = encode_chunk(D, nb);
+    const size_t smem = sizeof(double) * kEncWarps * nb * chunk;
+    const dim3 grid((unsigned)((3 * D.d + 31) / 32));
+    for (int b0 = 0; b0 < D.B; b0 += kEncWarps * nb) {
+        switch (nb) {
+            case 1: launch_pdl(k_encode<1>, grid, dim3(kEncWarps * 32), smem, st, D, wt, emb, b0, chunk, q64, kout, vout); break;
+            case 2: launch_pdl(k_encode<2>, grid, dim3(kEncWarps * 32), smem, st, D, wt, emb, b0, chunk, q64, kout, vout); break;
+            case 4: launch_pdl(k_encode<4>, grid, dim3(kEncWarps * 32), smem, st, D, wt, emb, b0, chunk, q64, kout, vout); break;
+            case 8: launch_pdl(k_encode<8>, grid, dim3(kEncWarps * 32), smem, st, D, wt, emb, b0, chunk, q64, kout, vout); break;
+            default: launch_pdl(k_encode<16>, grid, dim3(kEncWarps * 32), smem, st, D, wt, emb, b0, chunk, q64, kout, vout); break;
+        }
+    }
 }
 
 // ===========================================================================

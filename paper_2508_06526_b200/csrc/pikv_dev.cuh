@@ -61,6 +61,7 @@ struct Dims {
     int attend_ctas;
     int items_per_cta;  // split-K work items per attention CTA (PIKV_ITEMS, default 4)
     int route_ch;       // router columns per W ring stage (pick_route_chunk)
+    int q_f64;          // the step's q is fp64 (QueryEncoder output), not kv_dtype
     int dbg_ctl;        // k_control phase timestamps into dbg[64 + 8 s + p] (PIKV_DEBUG_CTL=1)
 };
 
@@ -366,6 +367,9 @@ void launch_finish_merge(const Dims& D, const Cfg& C, const State& S, const Exch
                          const uint8_t* gathered, float* y, int granks, cudaStream_t st);
 void launch_foldback(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);  // + feedback
 void launch_feedback(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);
+int encode_chunk(const Dims& D, int nb);
+void launch_encode(const Dims& D, const double* wt, const double* emb, double* q64, void* kout, void* vout,
+                   cudaStream_t st);  // QueryEncoder (pipeline.cpp:29-57) for all streams
 void launch_snapshot(const Dims& D, const State& S, int s, uint64_t now, const int64_t* ring_off,
                      pikv_snapshot_record* out, int64_t n, cudaStream_t st);
 void launch_synth(const Dims& D, void* q, void* k, void* v, uint64_t seed, uint64_t step,

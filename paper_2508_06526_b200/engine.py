@@ -223,6 +223,31 @@ class Engine:
                                    _np_ptr(y)))
         return y
 
+    def step_embed(self, emb, saliency=None, y=None):
+        """Engine::step(TokenInput{embedding}) for all streams: device fp64
+        tensor [B][d]; the QueryEncoder runs on the GPU (pipeline.cpp:222)."""
+        if y is None:
+            y = torch.empty(self.B, self.dp, dtype=torch.float32, device="cuda")
+        es = self.external_stream()
+        es.wait_stream(torch.cuda.current_stream())
+        check(lib().pikv_step_embed(self.h, _ptr(emb), _ptr(saliency), _ptr(y)))
+        torch.cuda.current_stream().wait_stream(es)
+        return y
+
+    def step_embed_host(self, emb, saliency=None):
+        """Engine::step(TokenInput{embedding}) through host buffers (numpy
+        fp64 [B][d]); returns y [B][d'] fp32."""
+        x = np.ascontiguousarray(emb, dtype=np.float64)
+        sal = None if saliency is None else np.ascontiguousarray(saliency, dtype=np.float64)
+        y = np.empty((self.B, self.dp), dtype=np.float32)
+        check(lib().pikv_step_embed_host(self.h, _np_ptr(x), _np_ptr(sal), _np_ptr(y)))
+        return y
+
+    def set_encoder(self, w_query, w_key, w_value):
+        """Replace the seeded QueryEncoder's [d][d] matrices."""
+        ws = [np.ascontiguousarray(w, dtype=np.float64) for w in (w_query, w_key, w_value)]
+        check(lib().pikv_set_encoder_host(self.h, *[_np_ptr(w) for w in ws]))
+
     def prefill_synthetic(self, tokens: int, seed: int = 1):
         check(lib().pikv_prefill_synthetic(self.h, int(tokens), int(seed)))
 

@@ -6,6 +6,8 @@
 #include <cstdio>
 #include <random>
 
+#include <tuple>
+
 #include "pikv_b200.hpp"
 
 using namespace pikv::b200;
@@ -130,6 +132,35 @@ int main() {
                 CHECK(std::fabs(total - 1.0) < 1e-5);
             }
         }
+    }
+    // the reference's TokenInput{embedding}: the QueryEncoder runs on the GPU
+    // (pipeline.cpp:222); width check before any state change (:214-216)
+    {
+        auto cfg = engine_config(RouterStrategy::Adaptive);
+        Engine a(cfg), b(cfg);
+        std::mt19937_64 g(17);
+        std::normal_distribution<double> n(0.0, 1.0);
+        for (int t = 0; t < 30; ++t) {
+            TokenInput tok;
+            tok.embedding.resize(16);
+            for (auto& x : tok.embedding) x = n(g);
+            auto ra = a.step({tok})[0];
+            auto rb = b.step({tok})[0];
+            CHECK(ra.experts == rb.experts && ra.attn.output == rb.attn.output);
+            CHECK(ra.step == static_cast<std::uint64_t>(t));
+        }
+        TokenInput bad;
+        bad.embedding.assign(15, 0.0);
+        const auto live = a.store_stats().live;
+        CHECK_THROWS_AS(a.step({bad}), InvalidArgument);
+        CHECK(a.store_stats().live == live);
+        // KVStore::snapshot (kvstore.cpp:206-221): one record per live entry, sorted
+        const auto snap = a.snapshot();
+        CHECK(snap.size() == live);
+        for (std::size_t i = 1; i < snap.size(); ++i)
+            CHECK(std::tie(snap[i - 1].device, snap[i - 1].shard, snap[i - 1].token_id, snap[i - 1].expert_id) <
+                  std::tie(snap[i].device, snap[i].shard, snap[i].token_id, snap[i].expert_id));
+        CHECK(!snap.empty() && wire::store_dump_line(snap[0]).find("\"age\":") == 1);
     }
     // QUEST needs a fitted scorer (test_scheduler.cpp:142-153)
     {

@@ -71,6 +71,11 @@ def oracle_lib():
         lib.po_engine_dump_slots.argtypes = [ctypes.c_void_p, c_u64_p, c_u64_p, c_i64_p, c_i32_p,
                                              c_u64_p, c_u64_p, c_u64_p, c_double_p, c_double_p]
         lib.po_engine_set_attn_mass.argtypes = [ctypes.c_void_p, c_double_p, c_double_p]
+        lib.po_engine_step_embed.argtypes = [ctypes.c_void_p, c_double_p, c_double_p,
+                                             ctypes.POINTER(PoStepOut), ctypes.c_int]
+        lib.po_encoder_weights.argtypes = [ctypes.c_int, ctypes.c_uint64, c_double_p]
+        lib.po_encode.argtypes = [c_double_p, ctypes.c_int, c_double_p, c_double_p, c_double_p,
+                                  c_double_p]
         lib.po_engine_snapshot.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p,
                                            ctypes.c_int64, c_i64_p]
         lib.po_engine_router.restype = ctypes.c_void_p
@@ -269,6 +274,16 @@ class OracleEngine(_StepMixin):
             _ptr(out["per_layer"], c_double_p))
         return out
 
+    def step_embed(self, emb, saliency=None, attend=True):
+        """Engine::step(TokenInput{embedding}) incl. the QueryEncoder."""
+        x = np.ascontiguousarray(emb, dtype=np.float64)
+        sal = None if saliency is None else np.ascontiguousarray(saliency, dtype=np.float64)
+        rc = self.lib.po_engine_step_embed(self.h, _ptr(x, c_double_p), _ptr(sal, c_double_p),
+                                           ctypes.byref(self.out), 1 if attend else 0)
+        if rc:
+            raise RuntimeError("oracle step error %d" % rc)
+        return self._collect(self.out)
+
     def snapshot(self, now):
         """KVStore::snapshot(now) restated (po_engine_snapshot)."""
         n = ctypes.c_int64(0)
@@ -391,3 +406,15 @@ def make_stream(T: int, d: int, seed: int, dtype: str = "f32", n_layers: int = 0
     v = round_to(raw[:, 2 * d:3 * d], dtype)
     sal = np.abs(raw[:, 3 * d:]) * 0.1 if n_layers else None
     return q, k, v, sal
+
+
+def oracle_encode(width: int, seed: int, x):
+    """QueryEncoder restated (po_encoder_weights + po_encode)."""
+    lib = oracle_lib()
+    w = np.zeros(3 * width * width)
+    lib.po_encoder_weights(width, seed, _ptr(w, c_double_p))
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    q, k, v = (np.zeros(width) for _ in range(3))
+    lib.po_encode(_ptr(w, c_double_p), width, _ptr(x, c_double_p), _ptr(q, c_double_p),
+                  _ptr(k, c_double_p), _ptr(v, c_double_p))
+    return q, k, v

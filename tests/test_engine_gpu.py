@@ -46,7 +46,7 @@ def rel_l2(a, b):
 
 
 def run_parity(cfg, T, seed, inject=True, basis=None, bias=None, kept=None, check_slots=True,
-               mutate=None):
+               mutate=None, embed=False):
     B = cfg.batch
     eng = Engine(cfg)
     if basis is not None or bias is not None or kept is not None:
@@ -67,12 +67,18 @@ def run_parity(cfg, T, seed, inject=True, basis=None, bias=None, kept=None, chec
         v = np.stack([streams[s][2][t] for s in range(B)])
         sal = None if cfg.n_layers == 0 else np.stack([streams[s][3][t] for s in range(B)])
         before = [eng.slots(s) for s in range(B)] if inject else None
-        y = eng.step_host(to_kv(q, cfg.kv_dtype), to_kv(k, cfg.kv_dtype), to_kv(v, cfg.kv_dtype),
-                          sal)
+        if embed:  # Engine::step(TokenInput{embedding}): the encoder runs on the GPU
+            y = eng.step_embed_host(q, sal)
+        else:
+            y = eng.step_host(to_kv(q, cfg.kv_dtype), to_kv(k, cfg.kv_dtype),
+                              to_kv(v, cfg.kv_dtype), sal)
         experts, gates, logits, summ = eng.read_step()
         evs = eng.read_evictions()
         for s in range(B):
-            r = orc[s].step(q[s], k[s], v[s], None if sal is None else sal[s])
+            if embed:
+                r = orc[s].step_embed(q[s], None if sal is None else sal[s])
+            else:
+                r = orc[s].step(q[s], k[s], v[s], None if sal is None else sal[s])
             ctx = (t, s)
             assert summ[s]["error"] == 0, ctx
             assert experts[s].tolist() == r["experts"], ctx
@@ -318,3 +324,21 @@ def test_engine_control_kernel_many_streams(monkeypatch):
     monkeypatch.setenv("PIKV_CONTROL", "1")
     cfg = engine_config(router="TopK", sched="LRU", S=32, ps=4, budget=3, batch=12, H=2)
     run_parity(cfg, 50, 41)
+
+
+@pytest.mark.parametrize("router,sched,kw", [
+    ("TopK", "LRU", dict()),
+    ("Adaptive", None, dict(S=128)),
+    ("LoadBalanced", "H2O", dict(H=2, dtype="bf16")),
+    ("Hierarchical", "AdaKV", dict(E=16, k=4, G=4, n_tok=4, n_exp=8)),
+])
+def test_engine_embedding_step(router, sched, kw):
+    """Engine::step(TokenInput{embedding}) (pipeline.cpp:213-351 from the
+    encode at :222): the QueryEncoder (pipeline.cpp:29-57, seeded like the
+    reference) runs on the GPU in fp64 -> routing, evictions, retrieval stay
+    bit-exact vs the oracle's encode + step; y in the stated tolerance."""
+    if sched is None:
+        cfg = engine_config(router=router, unbounded=True, batch=3, **kw)
+    else:
+        cfg = engine_config(router=router, sched=sched, batch=3, **kw)
+    run_parity(cfg, 50, 53, embed=True)
