@@ -280,6 +280,13 @@ int pikv_read_evictions_host(pikv_engine* eng, pikv_evict_record* out, int32_t c
 int pikv_read_attended_host(pikv_engine* eng, int32_t stream, int64_t* token,
                             int32_t* expert, double* alpha, int32_t cap,
                             int32_t* n_out);
+/* generate_trace (trace.cpp:54-82) with TraceSpec{steps, width, vocab,
+ * zipf_skew, seed, layers} (trace.hpp:12-21; errors per TraceSpec::validate):
+ * the vocabulary [vocab][width] fp64, each step's embedding id [steps] and
+ * per-layer saliency [steps][layers].  Any output pointer may be NULL. */
+int pikv_generate_trace(uint64_t steps, int32_t width, int32_t vocab, double zipf_skew,
+                        uint64_t seed, int32_t layers, double* vocab_out, uint32_t* embed_ids,
+                        float* saliency);
 /* KVStore::snapshot(now) (kvstore.cpp:206-221) of `stream`: its live entries
  * on this rank's devices, sorted by (device, shard, token, expert), computed
  * on the GPU.  now < 0 takes the stream's current step.  *n_out = number of

@@ -97,7 +97,7 @@ def build_ref(force: bool = False) -> str | None:
         with open(os.path.join(REF_OUT, name), "w") as f:
             f.write(text)
     srcs = [os.path.join(REF, "src", s)
-            for s in ("mathops.cpp", "kvstore.cpp", "router.cpp", "costmodel.cpp")]
+            for s in ("mathops.cpp", "kvstore.cpp", "router.cpp", "costmodel.cpp", "trace.cpp")]
     srcs += [os.path.join(REF_OUT, n) for n in gen] + [drv]
     flags = ["g++", "-std=c++20", "-O2", "-fPIC", "-include", "unordered_map", "-I", inc,
              "-I", HERE, "-I", os.path.join(HERE, "..", "include")]

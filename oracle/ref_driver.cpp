@@ -24,6 +24,7 @@
 #include "pikv/errors.hpp"
 #include "pikv/costmodel.hpp"
 #include "pikv/kvstore.hpp"
+#include "pikv/trace.hpp"
 #include "pikv/pipeline.hpp"
 #include "pikv/rng.hpp"
 #include "pikv/router.hpp"
@@ -352,6 +353,28 @@ int ref_encode(int width, uint64_t seed, const double* x, double* q, double* k, 
         std::memcpy(q, r.query.data(), sizeof(double) * width);
         std::memcpy(k, r.key.data(), sizeof(double) * width);
         std::memcpy(v, r.value.data(), sizeof(double) * width);
+        return 0;
+    } catch (const std::exception& ex) {
+        return code_of(ex);
+    }
+}
+
+// The reference's own generate_trace (trace.cpp:54-82) and trace file I/O
+// (save_trace / load_trace, trace.cpp:84-134).
+int ref_generate_trace(uint64_t steps, int width, int vocab, double skew, uint64_t seed, int layers,
+                       double* vocab_out, uint32_t* embed_ids, float* saliency, const char* save_path) {
+    try {
+        TraceSpec spec;
+        spec.steps = steps, spec.width = width, spec.vocab = vocab, spec.zipf_skew = skew;
+        spec.seed = seed, spec.layers = layers;
+        Trace tr = generate_trace(spec);
+        for (int v = 0; v < vocab; ++v)
+            std::memcpy(vocab_out + (size_t)v * width, tr.vocabulary[v].data(), sizeof(double) * width);
+        for (uint64_t t = 0; t < steps; ++t) {
+            embed_ids[t] = tr.events[t].embed_id;
+            for (int l = 0; l < layers; ++l) saliency[t * layers + l] = tr.events[t].layer_saliency[l];
+        }
+        if (save_path) save_trace(tr, save_path);
         return 0;
     } catch (const std::exception& ex) {
         return code_of(ex);

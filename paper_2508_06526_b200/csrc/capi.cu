@@ -83,12 +83,10 @@ static std::vector<double> pack_router_w(const Dims& D, const double* w) {
 // over std::mt19937_64 (rng.hpp).  RouterState::init (router.cpp:54-67):
 // W_r = normal_vector(E*d, 1/sqrt(d)); QueryEncoder (pipeline.cpp:29-36):
 // w_query, w_key, w_value = three consecutive normal_vector(d*d, 1/sqrt(d)).
-std::vector<double> reference_normals(size_t n, int width, uint64_t seed) {
-    std::mt19937_64 gen(seed);
-    auto uniform = [&]() { return static_cast<double>(gen() >> 11) * 0x1.0p-53; };
-    bool has_spare = false;
-    double spare = 0.0;
-    auto normal = [&]() {
+struct RefRng {  // pikv::Rng (rng.hpp:15-70): std::mt19937_64 + its double transforms
+    explicit RefRng(uint64_t seed) : gen(seed) {}
+    double uniform() { return static_cast<double>(gen() >> 11) * 0x1.0p-53; }
+    double normal() {
         if (has_spare) {
             has_spare = false;
             return spare;
@@ -101,10 +99,17 @@ std::vector<double> reference_normals(size_t n, int width, uint64_t seed) {
         spare = radius * std::sin(angle);
         has_spare = true;
         return radius * std::cos(angle);
-    };
+    }
+    std::mt19937_64 gen;
+    bool has_spare = false;
+    double spare = 0.0;
+};
+
+std::vector<double> reference_normals(size_t n, int width, uint64_t seed) {
+    RefRng rng(seed);
     const double scale = 1.0 / std::sqrt(static_cast<double>(width));
     std::vector<double> w(n);
-    for (auto& x : w) x = scale * normal();
+    for (auto& x : w) x = scale * rng.normal();
     return w;
 }
 
@@ -1097,6 +1102,41 @@ int pikv_read_evictions_host(pikv_engine* eng, pikv_evict_record* out, int32_t c
         }
     }
     *n_out = n;
+    return PIKV_OK;
+}
+
+// generate_trace (trace.cpp:54-82): vocabulary = Rng(seed).normal_vector(width)
+// per word; embed ids by inverse-CDF sampling of p_i ~ (i+1)^-skew with
+// Rng(seed ^ 0x7ace5eed); per-layer saliency float(|normal| * 0.1).
+int pikv_generate_trace(uint64_t steps, int32_t width, int32_t vocab, double zipf_skew, uint64_t seed,
+                        int32_t layers, double* vocab_out, uint32_t* embed_ids, float* saliency) {
+    // TraceSpec::validate, trace.cpp:39-44
+    if (width < 1) return fail(PIKV_ERR_INVALID_CONFIG, "TraceSpec: width must be >= 1");
+    if (vocab < 1) return fail(PIKV_ERR_INVALID_CONFIG, "TraceSpec: vocab must be >= 1");
+    if (zipf_skew < 0) return fail(PIKV_ERR_INVALID_CONFIG, "TraceSpec: skew must be >= 0");
+    if (layers < 1) return fail(PIKV_ERR_INVALID_CONFIG, "TraceSpec: layers must be >= 1");
+    if (vocab_out) {
+        RefRng rng(seed);
+        for (size_t i = 0; i < (size_t)vocab * width; ++i) vocab_out[i] = rng.normal();
+    }
+    std::vector<double> cdf(vocab);
+    double total = 0.0;
+    for (int i = 0; i < vocab; ++i) {
+        total += std::pow(static_cast<double>(i + 1), -zipf_skew);
+        cdf[i] = total;
+    }
+    for (auto& c : cdf) c /= total;
+    RefRng rng(seed ^ 0x7ace5eedULL);
+    for (uint64_t t = 0; t < steps; ++t) {
+        const double u = rng.uniform();
+        const auto it = std::lower_bound(cdf.begin(), cdf.end(), u);
+        const uint32_t id = static_cast<uint32_t>(std::min<std::ptrdiff_t>(it - cdf.begin(), vocab - 1));
+        if (embed_ids) embed_ids[t] = id;
+        for (int l = 0; l < layers; ++l) {
+            const float sv = static_cast<float>(std::abs(rng.normal()) * 0.1);
+            if (saliency) saliency[t * layers + l] = sv;
+        }
+    }
     return PIKV_OK;
 }
 
