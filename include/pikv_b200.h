@@ -280,6 +280,21 @@ int pikv_read_evictions_host(pikv_engine* eng, pikv_evict_record* out, int32_t c
 int pikv_read_attended_host(pikv_engine* eng, int32_t stream, int64_t* token,
                             int32_t* expert, double* alpha, int32_t cap,
                             int32_t* n_out);
+/* The store build of a prefill: T tokens of `stream` with
+ * their experts given (experts [T][k], selection order) -- token t is step
+ * now + t -- are encoded with the engine's codec and inserted exactly as T
+ * Engine::step inserts would (pipeline.cpp:148-211, kvstore.cpp:107-120:
+ * ids in order, ring overwrite, metadata insert_step = last_access = step),
+ * without routing, eviction or retrieval; now advances by T.  Runs as bulk
+ * kernels: entries placed straight at their final ring slots, pages built
+ * once, LowRank/LoRAPlus projections as one GEMM over all T rows (tcgen05 on
+ * sm_100a).  k, v: [T][d] in kv_dtype; saliency [T][n_layers] fp64 or NULL;
+ * *n_displaced = KVStore::insert displacements.  Device buffers
+ * (pikv_insert_bulk) or host buffers (pikv_insert_bulk_host). */
+int pikv_insert_bulk(pikv_engine* eng, int32_t stream, int64_t T, const void* k, const void* v,
+                     const int32_t* experts, const double* saliency, int64_t* n_displaced);
+int pikv_insert_bulk_host(pikv_engine* eng, int32_t stream, int64_t T, const void* k, const void* v,
+                          const int32_t* experts, const double* saliency, int64_t* n_displaced);
 /* generate_trace (trace.cpp:54-82) with TraceSpec{steps, width, vocab,
  * zipf_skew, seed, layers} (trace.hpp:12-21; errors per TraceSpec::validate):
  * the vocabulary [vocab][width] fp64, each step's embedding id [steps] and

@@ -1115,6 +1115,30 @@ int po_engine_step_embed(po_engine* e, const double* emb, const double* saliency
     return rc;
 }
 
+/* The store build of a prefill: for t = 0..T-1 (steps now+t)
+ * the token's k entries (experts[t][0..k-1], selection order) are encoded
+ * and inserted as Engine::step inserts them (pipeline.cpp:148-211,
+ * kvstore.cpp:107-120) -- no routing, eviction or retrieval -- then now
+ * advances by T.  k/v rows are [T][d]; saliency [T][n_layers] or NULL. */
+int po_engine_insert_bulk(po_engine* e, int64_t T, const double* k, const double* v,
+                          const int32_t* experts, const double* saliency, int64_t* n_displaced) {
+    const pikv_config* c = &e->c;
+    int64_t nd = 0;
+    for (int64_t t = 0; t < T; ++t) {
+        encode_row(e, k + (size_t)t * c->d, e->stage_k, 0);
+        encode_row(e, v + (size_t)t * c->d, e->stage_v, 0);
+        for (int j = 0; j < c->k; ++j) {
+            po_slot disp;
+            int ddev = 0;
+            nd += store_insert(e, (int64_t)e->now, experts[t * c->k + j], e->stage_k, e->stage_v,
+                               saliency ? saliency + (size_t)t * c->n_layers : NULL, &disp, &ddev);
+        }
+        e->now += 1;
+    }
+    if (n_displaced) *n_displaced = nd;
+    return PIKV_OK;
+}
+
 int po_engine_step(po_engine* e, const double* q, const double* k, const double* v,
                    const double* saliency, po_step_out* out) {
     return engine_step_impl(e, q, k, v, saliency, out, 1);

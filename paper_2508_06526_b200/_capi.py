@@ -75,6 +75,8 @@ SIGNATURES = {
     "pikv_step_embed": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "pikv_step_embed_host": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "pikv_set_encoder_host": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
+    "pikv_insert_bulk": (ctypes.c_int, [c_vp, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp, P(c_i64)]),
+    "pikv_insert_bulk_host": (ctypes.c_int, [c_vp, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp, P(c_i64)]),
     "pikv_generate_trace": (ctypes.c_int, [c_u64, c_i32, c_i32, c_f64, c_u64, c_i32, c_vp, c_vp,
                                            c_vp]),
     "pikv_snapshot_host": (ctypes.c_int, [c_vp, c_i32, ctypes.c_int64, c_vp, ctypes.c_int64,

@@ -1105,6 +1105,70 @@ int pikv_read_evictions_host(pikv_engine* eng, pikv_evict_record* out, int32_t c
     return PIKV_OK;
 }
 
+// The store build of a prefill, see pikv_b200.h.
+int pikv_insert_bulk(pikv_engine* eng, int32_t stream, int64_t T, const void* k, const void* v,
+                     const int32_t* experts, const double* saliency, int64_t* n_displaced) {
+    const Dims& D = eng->D;
+    if (stream < 0 || stream >= D.B) return fail(PIKV_ERR_INVALID_ARGUMENT, "stream out of range");
+    if (T < 0 || (T > 0 && (!k || !v || !experts)))
+        return fail(PIKV_ERR_INVALID_ARGUMENT, "insert_bulk: null input");
+    int rc = codec_ready(eng);
+    if (rc) return rc;
+    cudaSetDevice(eng->device);
+    cudaStream_t st = eng->stream;
+    const bool proj = D.codec == PIKV_CODEC_LOWRANK || D.codec == PIKV_CODEC_LORAPLUS;
+    int64_t* dst = nullptr;
+    float* pr = nullptr;
+    unsigned long long* ctr = nullptr;
+    CUDA_TRY(cudaMallocAsync(&dst, sizeof(int64_t) * (size_t)std::max<int64_t>(1, T * D.k), st));
+    cudaError_t e = cudaMallocAsync(&ctr, sizeof(unsigned long long) * (2 + D.Gl), st);
+    if (e == cudaSuccess && proj)
+        e = cudaMallocAsync(&pr, sizeof(float) * 2 * (size_t)std::max<int64_t>(1, T) * D.dp, st);
+    if (e == cudaSuccess) {
+        const char* tc = std::getenv("PIKV_BULK_TC");
+        e = (cudaError_t)bulk_insert(D, eng->S, stream, T, k, v, experts, saliency, dst, pr, ctr,
+                                     tc ? std::atoi(tc) : 1, st);
+    }
+    unsigned long long host_ctr[2] = {0, 0};
+    if (e == cudaSuccess) e = cudaMemcpyAsync(host_ctr, ctr, sizeof(host_ctr), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFreeAsync(dst, st);
+    if (ctr) cudaFreeAsync(ctr, st);
+    if (pr) cudaFreeAsync(pr, st);
+    if (e != cudaSuccess) return fail(PIKV_ERR_CUDA, std::string("insert_bulk: ") + cudaGetErrorString(e));
+    int32_t err = 0;
+    CUDA_TRY(cudaMemcpy(&err, eng->S.err + stream, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    if (err) return fail(err, "insert_bulk: KV page pool exhausted");
+    if (n_displaced) *n_displaced = (int64_t)host_ctr[1];
+    return PIKV_OK;
+}
+
+int pikv_insert_bulk_host(pikv_engine* eng, int32_t stream, int64_t T, const void* k, const void* v,
+                          const int32_t* experts, const double* saliency, int64_t* n_displaced) {
+    const Dims& D = eng->D;
+    if (T <= 0) return pikv_insert_bulk(eng, stream, T, k, v, experts, saliency, n_displaced);
+    const size_t row = (size_t)D.d * (D.kv_dtype == PIKV_DTYPE_BF16 ? 2 : 4);
+    cudaSetDevice(eng->device);
+    cudaStream_t st = eng->stream;
+    uint8_t* buf = nullptr;
+    const size_t nk = row * T, ne = sizeof(int32_t) * (size_t)T * D.k;
+    const size_t ns = saliency && D.n_layers > 0 ? sizeof(double) * (size_t)T * D.n_layers : 0;
+    CUDA_TRY(cudaMallocAsync(&buf, 2 * nk + ne + ns + 64, st));
+    uint8_t* dk = buf;
+    uint8_t* dv = buf + nk;
+    int32_t* de = (int32_t*)(buf + 2 * nk);
+    double* ds = ns ? (double*)(((uintptr_t)(buf + 2 * nk + ne) + 15) & ~(uintptr_t)15) : nullptr;
+    cudaError_t e = cudaMemcpyAsync(dk, k, nk, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dv, v, nk, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(de, experts, ne, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess && ns) e = cudaMemcpyAsync(ds, saliency, ns, cudaMemcpyHostToDevice, st);
+    int rc = e == cudaSuccess ? pikv_insert_bulk(eng, stream, T, dk, dv, de, ds, n_displaced)
+                              : fail(PIKV_ERR_CUDA, std::string("insert_bulk_host: ") + cudaGetErrorString(e));
+    cudaFreeAsync(buf, st);
+    cudaStreamSynchronize(st);
+    return rc;
+}
+
 // generate_trace (trace.cpp:54-82): vocabulary = Rng(seed).normal_vector(width)
 // per word; embed ids by inverse-CDF sampling of p_i ~ (i+1)^-skew with
 // Rng(seed ^ 0x7ace5eed); per-layer saliency float(|normal| * 0.1).

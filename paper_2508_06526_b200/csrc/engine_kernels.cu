@@ -2334,6 +2334,277 @@ void launch_encode(const Dims& D, const double* wt, const double* emb, double* q
 }
 
 // ===========================================================================
+// bulk insert: the store build of a prefill
+// ===========================================================================
+// T tokens of stream s with given experts: entry e = t*k + j is the j-th
+// selected expert of token t (step now + t); ids now_id + e in order.  The
+// result equals T*k sequential KVStore::insert calls (kvstore.cpp:36-53,
+// 107-120) with Engine::step's metadata (pipeline.cpp:191-193).
+//
+// (a) one CTA per local ring: count the ring's entries c; the j-th of them
+//     goes to slot (head + j) mod S and only the last min(c, S) survive
+//     (earlier ones are overwritten inside the bulk); displacements = bulk
+//     overwrites + previously live slots among the first min(c, S) writes.
+//     Survivors get their metadata and a pool entry (pages allocated on
+//     first use); then the ring's live count, storage-page counts and
+//     scheduler page records are rebuilt from the final slots.
+__device__ __forceinline__ int bulk_ring_of(const Dims& D, int64_t token, int e) {
+    const int raw = shard_raw(token, e, D.n_tok, D.n_exp, D.additive);
+    const int dev = raw % D.G;
+    if (dev % D.world != D.rank) return -1;
+    return (dev / D.world) * D.SPD + raw / D.G;
+}
+
+__global__ void __launch_bounds__(512) k_bulk_ring(Dims D, State S, int s, int64_t T,
+                                                   const int32_t* __restrict__ experts,
+                                                   const double* __restrict__ saliency,
+                                                   int64_t* __restrict__ dst, unsigned long long* counters) {
+    const int rl = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NT = blockDim.x;
+    const int NW = NT >> 5;
+    const int64_t ring = (int64_t)s * D.R + rl;
+    const uint64_t now0 = S.now[s], id0 = S.next_id[s];
+    const int head = S.head[ring];
+    const uint64_t seq0 = S.seq[ring];
+    const int64_t n = T * D.k;
+    __shared__ int64_t wsum[32];
+    __shared__ int64_t sm_c, sm_run;
+    __shared__ unsigned long long sm_disp;
+    // count
+    int64_t mine = 0;
+    for (int64_t e = tid; e < n; e += NT)
+        mine += bulk_ring_of(D, (int64_t)(now0 + (uint64_t)(e / D.k)), experts[e]) == rl;
+    int64_t tot;
+    block_excl_scan(mine, wsum, &tot);
+    if (tid == 0) sm_c = tot, sm_run = 0, sm_disp = 0;
+    __syncthreads();
+    const int64_t c = sm_c;  // c == 0: nothing placed, the ring still counts its live pages
+    const int64_t first_surv = c > D.S ? c - D.S : 0;  // ring rank of the first survivor
+    // displaced previously-live entries: the first min(c, S) writes
+    unsigned long long dl = 0;
+    for (int64_t j = tid; j < (c < D.S ? c : D.S); j += NT)
+        dl += S.id[ring * D.S + (head + j) % D.S] != 0;
+    for (int o = 16; o; o >>= 1) dl += __shfl_xor_sync(0xffffffffu, dl, o);
+    if (lane == 0) atomicAdd(&sm_disp, dl);
+    // storage pages of the survivor slots: allocate before any write
+    const int64_t nsurv = c - first_surv;
+    const int64_t s0 = (head + first_surv) % D.S;  // survivor slots: cyclic [s0, s0 + nsurv)
+    for (int p = tid; p < D.ppr; p += NT) {
+        bool touched = false;
+        for (int q = 0; q < D.spg && !touched; ++q) {
+            const int64_t slot = (int64_t)p * D.spg + q;
+            touched = ((slot - s0 + D.S) % D.S) < nsurv;
+        }
+        if (touched && S.page_table[ring * D.ppr + p] < 0) {
+            const int top = atomicSub(S.free_top, 1) - 1;
+            if (top < 0) {
+                atomicAdd(S.free_top, 1);
+                S.err[s] = PIKV_ERR_OUT_OF_MEMORY;
+            } else {
+                const int32_t page = S.free_stack[top];
+                S.page_table[ring * D.ppr + p] = page;
+            }
+        }
+    }
+    __shared__ int sm_err;
+    __syncthreads();
+    if (tid == 0) sm_err = S.err[s];
+    __syncthreads();
+    if (sm_err) return;  // pool exhausted: the bulk insert fails (PIKV_ERR_OUT_OF_MEMORY)
+    // place: entries in order, rank within the ring by block scans
+    for (int64_t e0 = 0; c > 0 && e0 < n; e0 += NT) {
+        const int64_t e = e0 + tid;
+        const int64_t t = e / D.k;
+        const bool in = e < n && bulk_ring_of(D, (int64_t)(now0 + (uint64_t)t), e < n ? experts[e] : 0) == rl;
+        const unsigned bal = __ballot_sync(0xffffffffu, in);
+        if (lane == 0) wsum[warp] = __popc(bal);
+        __syncthreads();
+        if (tid == 0) {
+            int64_t acc = 0;
+            for (int w = 0; w < NW; ++w) {
+                const int64_t x = wsum[w];
+                wsum[w] = acc;
+                acc += x;
+            }
+            wsum[31] = acc;  // chunk total (NW <= 16)
+        }
+        __syncthreads();
+        if (in) {
+            const int64_t j = sm_run + wsum[warp] + __popc(bal & ((1u << lane) - 1u));
+            if (j >= first_surv) {
+                const int slot = (int)((head + j) % D.S);
+                const int64_t gi = ring * D.S + slot;
+                const uint64_t step = now0 + (uint64_t)t;
+                S.id[gi] = id0 + (uint64_t)e;
+                S.shard_seq[gi] = seq0 + (uint64_t)j;
+                S.token[gi] = (int64_t)step;
+                S.expert[gi] = experts[e];
+                S.insert_step[gi] = step;
+                S.last_access[gi] = step;
+                S.freq[gi] = 0;
+                S.attn_mass[gi] = 0.0;
+                for (int l = 0; l < D.n_layers; ++l)
+                    S.per_layer[gi * D.n_layers + l] = saliency ? saliency[t * D.n_layers + l] : 0.0;
+                const int32_t page = S.page_table[ring * D.ppr + slot / D.spg];
+                dst[e] = (int64_t)page * D.spg + slot % D.spg;
+            } else {
+                dst[e] = -1;  // overwritten later in the bulk
+            }
+        }
+        __syncthreads();
+        if (tid == 0) sm_run += wsum[31];
+        __syncthreads();
+    }
+    if (tid == 0) {
+        S.head[ring] = (int)((head + c) % D.S);
+        S.seq[ring] = seq0 + (uint64_t)c;
+        atomicAdd(&counters[0], (unsigned long long)c);                                  // inserts
+        atomicAdd(&counters[1], sm_disp + (unsigned long long)(c > D.S ? c - D.S : 0));  // displaced
+    }
+    __threadfence_block();
+    __syncthreads();
+    // rebuild the ring's counters and page records from its final slots
+    for (int64_t r = tid; r < D.ppr_sched; r += NT) {
+        const int64_t ri = ring * D.ppr_sched + r;
+        S.pr_cnt[ri] = 0, S.pr_first[ri] = 0x7fffffff, S.pr_sla[ri] = 0, S.pr_sf[ri] = 0;
+    }
+    for (int p = tid; p < D.ppr; p += NT) {
+        const int32_t page = S.page_table[ring * D.ppr + p];
+        if (page >= 0) S.page_live[page] = 0;
+    }
+    __syncthreads();
+    int lv = 0;
+    for (int slot = tid; slot < D.S; slot += NT) {
+        const int64_t gi = ring * D.S + slot;
+        if (S.id[gi] == 0) continue;
+        ++lv;
+        const uint64_t sq = S.shard_seq[gi];
+        const int64_t ri = page_rec(D, ring, sq);
+        atomicAdd(&S.pr_cnt[ri], 1);
+        atomicMin(&S.pr_first[ri], (int)(sq % (uint64_t)D.page_size));
+        atomicAdd((unsigned long long*)&S.pr_sla[ri], (unsigned long long)S.last_access[gi]);
+        atomicAdd((unsigned long long*)&S.pr_sf[ri], (unsigned long long)S.freq[gi]);
+        atomicAdd(&S.page_live[S.page_table[ring * D.ppr + slot / D.spg]], 1);
+    }
+    for (int o = 16; o; o >>= 1) lv += __shfl_xor_sync(0xffffffffu, lv, o);
+    __shared__ int sm_lv, sm_pages;
+    if (tid == 0) sm_lv = 0, sm_pages = 0;
+    __syncthreads();
+    if (lane == 0) atomicAdd(&sm_lv, lv);
+    __syncthreads();
+    int pg = 0;
+    for (int64_t r = tid; r < D.ppr_sched; r += NT) {
+        const int64_t ri = ring * D.ppr_sched + r;
+        if (S.pr_cnt[ri] > 0) ++pg;
+        else S.pr_first[ri] = 0;
+    }
+    for (int o = 16; o; o >>= 1) pg += __shfl_xor_sync(0xffffffffu, pg, o);
+    if (lane == 0) atomicAdd(&sm_pages, pg);
+    __syncthreads();
+    if (tid == 0) {
+        S.live[ring] = sm_lv;
+        atomicAdd(&counters[2 + rl / D.SPD], (unsigned long long)sm_pages);  // live pages per device
+    }
+}
+
+// (b) one CTA per token: encode its K and V once (codec of the engine; the
+//     low-rank projections come precomputed in proj [2][T][dp]) and copy the
+//     entry to every surviving destination of the token.
+__global__ void k_bulk_payload(Dims D, State S, int64_t T, const void* __restrict__ k, const void* __restrict__ v,
+                               const float* __restrict__ proj, const int64_t* __restrict__ dst) {
+    extern __shared__ __align__(16) uint8_t sm_entry[];  // [entry_bytes] + tmp floats [d]
+    const int64_t t = blockIdx.x;
+    const int tid = threadIdx.x;
+    bool any = false;
+    for (int j = 0; j < D.k; ++j) any |= dst[t * D.k + j] >= 0;
+    if (!any) return;
+    float* tmp = (float*)(sm_entry + ((D.entry_bytes + 15) & ~15));
+    const int pay = D.payload_bytes;
+    float* ksc = (float*)(sm_entry + 2 * pay);
+    float* vsc = ksc + D.H;
+    if (D.codec == PIKV_CODEC_LOWRANK || D.codec == PIKV_CODEC_LORAPLUS) {
+        for (int row = 0; row < 2; ++row) {
+            const float* pr = proj + ((int64_t)row * T + t) * D.dp;
+            uint8_t* out = sm_entry + row * pay;
+            for (int o = tid; o < D.dp; o += blockDim.x) {
+                if (D.kv_dtype == PIKV_DTYPE_BF16) ((uint16_t*)out)[o] = f32_to_bf16_rne(pr[o]);
+                else ((float*)out)[o] = pr[o];
+            }
+        }
+    } else {
+        // encode_row reads row `s` of a [.][d] input: pass the token's row
+        const int esz = D.kv_dtype == PIKV_DTYPE_BF16 ? 2 : 4;
+        encode_row(D, S, (const uint8_t*)k + t * D.d * esz, 0, sm_entry, ksc, tmp, 0);
+        encode_row(D, S, (const uint8_t*)v + t * D.d * esz, 0, sm_entry + pay, vsc, tmp, 1);
+    }
+    __syncthreads();
+    const int nvec = D.entry_bytes / 16;
+    for (int j = 0; j < D.k; ++j) {
+        const int64_t de = dst[t * D.k + j];
+        if (de < 0) continue;
+        uint4* o = (uint4*)(S.pool + de * (int64_t)D.entry_bytes);
+        for (int i = tid; i < nvec; i += blockDim.x) o[i] = ((const uint4*)sm_entry)[i];
+    }
+}
+
+// (c) stream counters: ids, steps, store totals, live pages per device.
+__global__ void k_bulk_finish(Dims D, State S, int s, int64_t T, const unsigned long long* counters) {
+    if (threadIdx.x != 0) return;
+    S.next_id[s] += (uint64_t)(T * D.k);
+    S.now[s] += (uint64_t)T;
+    S.st_inserts[s] += counters[0];
+    S.st_overwrites[s] += counters[1];
+    for (int gl = 0; gl < D.Gl; ++gl) S.pages_live[s * D.Gl + gl] = (int32_t)counters[2 + gl];
+}
+
+// Codec::encode_vector of LowRank / LoRAPlus for T rows on CUDA cores (fp32,
+// i ascending like k_project): proj[row][t][h*r + j] = sum_i B[h][j][i] x_i.
+__global__ void k_bulk_project_fma(Dims D, State S, int64_t T, const void* __restrict__ kin,
+                                   const void* __restrict__ vin, float* __restrict__ proj) {
+    const int h = blockIdx.y, row = blockIdx.z;
+    const int hd = D.d / D.H, r = D.dph;
+    const void* x = row == 0 ? kin : vin;
+    extern __shared__ float sm_b[];  // basis [r][hd]
+    for (int i = threadIdx.x; i < r * hd; i += blockDim.x) sm_b[i] = S.basis[(int64_t)h * r * hd + i];
+    __syncthreads();
+    for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < T * r;
+         o += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = o / r;
+        const int j = (int)(o % r);
+        const float* col = sm_b + (size_t)j * hd;
+        float acc = 0.f;
+        for (int i = 0; i < hd; ++i) {
+            float xi = load_in(x, D.kv_dtype, t * D.d + h * hd + i);
+            if (D.codec == PIKV_CODEC_LORAPLUS) xi -= S.cbias[h * hd + i];
+            acc = fmaf(col[i], xi, acc);
+        }
+        proj[((int64_t)row * T + t) * D.dp + h * r + j] = acc;
+    }
+}
+
+int bulk_insert(const Dims& D, const State& S, int s, int64_t T, const void* k, const void* v,
+                const int32_t* experts, const double* saliency, int64_t* dst, float* proj,
+                unsigned long long* counters, int use_tc, cudaStream_t st) {
+    cudaMemsetAsync(counters, 0, sizeof(unsigned long long) * (2 + D.Gl), st);
+    cudaMemsetAsync(dst, 0xff, sizeof(int64_t) * (size_t)(T * D.k), st);  // -1: not stored here
+    if ((D.codec == PIKV_CODEC_LOWRANK || D.codec == PIKV_CODEC_LORAPLUS) && T > 0) {
+        if (!(use_tc && launch_bulk_project_tc(D, S, T, k, v, proj, st) == 0)) {
+            const int hd = D.d / D.H;
+            const size_t smem = sizeof(float) * (size_t)D.dph * hd;
+            if (smem > 48 * 1024)
+                cudaFuncSetAttribute(k_bulk_project_fma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            k_bulk_project_fma<<<dim3(64, D.H, 2), 256, smem, st>>>(D, S, T, k, v, proj);
+        }
+    }
+    if (D.R > 0) k_bulk_ring<<<D.R, 512, 0, st>>>(D, S, s, T, experts, saliency, dst, counters);
+    const size_t psmem = (size_t)((D.entry_bytes + 15) & ~15) + sizeof(float) * (size_t)D.d;
+    if (psmem > 48 * 1024)
+        cudaFuncSetAttribute(k_bulk_payload, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
+    if (T > 0) k_bulk_payload<<<(unsigned)T, 256, psmem, st>>>(D, S, T, k, v, proj, dst);
+    k_bulk_finish<<<1, 32, 0, st>>>(D, S, s, T, counters);
+    return (int)cudaGetLastError();
+}
+
+// ===========================================================================
 // snapshot: KVStore::snapshot (kvstore.cpp:206-221) of one stream
 // ===========================================================================
 // (a) one CTA per local ring: its live entries in shard_seq order (= token

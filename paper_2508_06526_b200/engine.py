@@ -243,6 +243,20 @@ class Engine:
         check(lib().pikv_step_embed_host(self.h, _np_ptr(x), _np_ptr(sal), _np_ptr(y)))
         return y
 
+    def insert_bulk_host(self, stream: int, k, v, experts, saliency=None) -> int:
+        """The store build of a prefill (pikv_insert_bulk_host): T tokens with
+        given experts [T][k]; k/v [T][d] numpy in the engine's kv dtype
+        (uint16 bf16 bits or float32).  Returns the displacement count."""
+        dt = np.float32 if self.cfg.kv_dtype == "f32" else np.uint16
+        k, v = (np.ascontiguousarray(a).view(dt) if a.dtype != dt else np.ascontiguousarray(a)
+                for a in (k, v))
+        ex = np.ascontiguousarray(experts, dtype=np.int32)
+        sal = None if saliency is None else np.ascontiguousarray(saliency, dtype=np.float64)
+        nd = ctypes.c_int64(0)
+        check(lib().pikv_insert_bulk_host(self.h, stream, int(ex.shape[0]), _np_ptr(k), _np_ptr(v),
+                                          _np_ptr(ex), _np_ptr(sal), ctypes.byref(nd)))
+        return nd.value
+
     def set_encoder(self, w_query, w_key, w_value):
         """Replace the seeded QueryEncoder's [d][d] matrices."""
         ws = [np.ascontiguousarray(w, dtype=np.float64) for w in (w_query, w_key, w_value)]

@@ -76,6 +76,8 @@ def oracle_lib():
         lib.po_encoder_weights.argtypes = [ctypes.c_int, ctypes.c_uint64, c_double_p]
         lib.po_encode.argtypes = [c_double_p, ctypes.c_int, c_double_p, c_double_p, c_double_p,
                                   c_double_p]
+        lib.po_engine_insert_bulk.argtypes = [ctypes.c_void_p, ctypes.c_int64, c_double_p,
+                                              c_double_p, c_i32_p, c_double_p, c_i64_p]
         lib.po_engine_snapshot.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p,
                                            ctypes.c_int64, c_i64_p]
         lib.po_engine_router.restype = ctypes.c_void_p
@@ -283,6 +285,19 @@ class OracleEngine(_StepMixin):
         if rc:
             raise RuntimeError("oracle step error %d" % rc)
         return self._collect(self.out)
+
+    def insert_bulk(self, k, v, experts, saliency=None) -> int:
+        """The store build of a prefill restated (po_engine_insert_bulk)."""
+        k, v = (np.ascontiguousarray(a, dtype=np.float64) for a in (k, v))
+        ex = np.ascontiguousarray(experts, dtype=np.int32)
+        sal = None if saliency is None else np.ascontiguousarray(saliency, dtype=np.float64)
+        nd = ctypes.c_int64(0)
+        rc = self.lib.po_engine_insert_bulk(self.h, ex.shape[0], _ptr(k, c_double_p),
+                                            _ptr(v, c_double_p), _ptr(ex, c_i32_p),
+                                            _ptr(sal, c_double_p), ctypes.byref(nd))
+        if rc:
+            raise RuntimeError("oracle insert_bulk error %d" % rc)
+        return nd.value
 
     def snapshot(self, now):
         """KVStore::snapshot(now) restated (po_engine_snapshot)."""
