@@ -113,3 +113,37 @@ def test_insert_bulk_empty_and_errors():
     with pytest.raises(PikvError):
         eng.insert_bulk_host(5, np.zeros((1, 16), np.float32), np.zeros((1, 16), np.float32),
                              np.zeros((1, 2), np.int32))
+
+
+@pytest.mark.parametrize("codec,dtype,d,H,rank", [
+    ("LowRank", "bf16", 128, 2, 32),
+    ("LoRAPlus", "f32", 64, 2, 8),
+    ("LowRank", "f32", 256, 2, 64),
+])
+def test_bulk_projection_tensor_cores_match_cuda_cores(monkeypatch, codec, dtype, d, H, rank):
+    """The bulk projection GEMM on tcgen05 (PIKV_BULK_TC=2: tensor cores
+    required, fails loudly otherwise) vs the CUDA-core fp32 projection
+    (PIKV_BULK_TC=0): identical store metadata, and the decode outputs over
+    the bulk-built entries agree to fp32 level (bf16 hi+lo operand split)."""
+    rng = np.random.default_rng(5)
+    outs = []
+    for tc in ("2", "0"):
+        monkeypatch.setenv("PIKV_BULK_TC", tc)
+        cfg = engine_config(router="TopK", sched="LRU", unbounded=True, d=d, H=H, S=256, batch=1,
+                            codec=codec, rank=rank, dtype=dtype)
+        basis, bias, _ = codec_params(codec, d, H, rank, np.random.default_rng(9))
+        eng = Engine(cfg)
+        eng.set_codec(basis, None if bias is None else bias.astype(np.float32), None)
+        T = 300
+        st = make_stream(T + 4, d, 21, dtype, 0)
+        ex = np.stack([np.random.default_rng(t).choice(cfg.model.E, cfg.router.k, replace=False)
+                       for t in range(T)]).astype(np.int32)
+        eng.insert_bulk_host(0, to_kv(st[1][:T], dtype), to_kv(st[2][:T], dtype), ex)
+        ys = [eng.step_host(to_kv(st[0][T + i:T + i + 1], dtype), to_kv(st[1][T + i:T + i + 1], dtype),
+                            to_kv(st[2][T + i:T + i + 1], dtype)) for i in range(4)]
+        outs.append((eng.slots(0), np.concatenate(ys)))
+        eng.close()
+    (sa, ya), (sb, yb) = outs
+    assert np.array_equal(sa["id"], sb["id"]) and np.array_equal(sa["token"], sb["token"])
+    tol = 2e-3 if dtype == "bf16" else 1e-5
+    assert rel_l2(ya.astype(np.float64), yb.astype(np.float64)) <= tol
