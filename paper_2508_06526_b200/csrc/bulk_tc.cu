@@ -220,19 +220,19 @@ int launch_np(const Dims& D, const State& S, int64_t T, const void* k, const voi
 }  // namespace
 
 int launch_bulk_project_tc(const Dims& D, const State& S, int64_t T, const void* k, const void* v, float* proj,
-                           cudaStream_t st) {
+                           float* bias_scratch, cudaStream_t st) {
     const int hd = D.d / D.H, r = D.dph;
     if (hd % 16 != 0 || r < 1 || r > 64 || T <= 0) return 1;
+    // LoRAPlus: bias B^T [H][r] in the caller's scratch
     float* bias_proj = nullptr;
     if (D.codec == PIKV_CODEC_LORAPLUS) {
-        if (cudaMallocAsync(&bias_proj, sizeof(float) * D.H * r, st) != cudaSuccess) return 1;
+        bias_proj = bias_scratch;
         k_bias_proj<<<1, 256, 0, st>>>(D, S, bias_proj);
     }
     int rc;
     if (r <= 16) rc = launch_np<16>(D, S, T, k, v, proj, bias_proj, st);
     else if (r <= 32) rc = launch_np<32>(D, S, T, k, v, proj, bias_proj, st);
     else rc = launch_np<64>(D, S, T, k, v, proj, bias_proj, st);
-    if (bias_proj) cudaFreeAsync(bias_proj, st);
     return rc;
 }
 

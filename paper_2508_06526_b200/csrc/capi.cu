@@ -137,6 +137,13 @@ struct pikv_engine {
     double* in_sal = nullptr;
     // QueryEncoder (pipeline.cpp:29-57) for the embedding step, allocated on
     // first use: W^T [3][d][d] fp64, the step's fp64 q, host-path staging
+    // grow-only scratch of the bulk store build (device) and its host-path
+    // staging; freed at destroy (not through the async pool: no per-call
+    // map/unmap)
+    void* bulk_buf = nullptr;
+    size_t bulk_cap = 0;
+    void* bulk_stage = nullptr;
+    size_t stage_cap = 0;
     double* enc_wt = nullptr;
     double* q64 = nullptr;
     double* in_emb = nullptr;
@@ -723,6 +730,8 @@ int pikv_engine_destroy(pikv_engine* eng) {
     for (auto& kv : eng->graphs) cudaGraphExecDestroy(kv.second);
     for (auto e : eng->ev) cudaEventDestroy(e);
     for (void* p : eng->allocs) cudaFree(p);
+    if (eng->bulk_buf) cudaFree(eng->bulk_buf);
+    if (eng->bulk_stage) cudaFree(eng->bulk_stage);
     if (eng->stream) cudaStreamDestroy(eng->stream);
     delete eng;
     return PIKV_OK;
@@ -1117,14 +1126,22 @@ int pikv_insert_bulk(pikv_engine* eng, int32_t stream, int64_t T, const void* k,
     cudaSetDevice(eng->device);
     cudaStream_t st = eng->stream;
     const bool proj = D.codec == PIKV_CODEC_LOWRANK || D.codec == PIKV_CODEC_LORAPLUS;
-    int64_t* dst = nullptr;
-    float* pr = nullptr;
-    unsigned long long* ctr = nullptr;
-    CUDA_TRY(cudaMallocAsync(&dst, sizeof(int64_t) * (size_t)std::max<int64_t>(1, T * D.k), st));
-    cudaError_t e = cudaMallocAsync(&ctr, sizeof(unsigned long long) * (2 + D.Gl), st);
-    if (e == cudaSuccess && proj)
-        e = cudaMallocAsync(&pr, sizeof(float) * 2 * (size_t)std::max<int64_t>(1, T) * D.dp, st);
-    if (e == cudaSuccess) {
+    const size_t n_dst = sizeof(int64_t) * (size_t)std::max<int64_t>(1, T * D.k);
+    const size_t n_ctr = sizeof(unsigned long long) * (2 + D.Gl);
+    const size_t n_pr = proj ? sizeof(float) * (2 * (size_t)std::max<int64_t>(1, T) * D.dp + (size_t)D.dp) : 0;
+    const size_t need = ((n_dst + 255) & ~(size_t)255) + ((n_ctr + 255) & ~(size_t)255) + n_pr;
+    if (need > eng->bulk_cap) {
+        CUDA_TRY(cudaStreamSynchronize(st));
+        if (eng->bulk_buf) cudaFree(eng->bulk_buf);
+        eng->bulk_buf = nullptr, eng->bulk_cap = 0;
+        CUDA_TRY(cudaMalloc(&eng->bulk_buf, need));
+        eng->bulk_cap = need;
+    }
+    int64_t* dst = (int64_t*)eng->bulk_buf;
+    unsigned long long* ctr = (unsigned long long*)((uint8_t*)eng->bulk_buf + ((n_dst + 255) & ~(size_t)255));
+    float* pr = proj ? (float*)((uint8_t*)ctr + ((n_ctr + 255) & ~(size_t)255)) : nullptr;
+    cudaError_t e = cudaSuccess;
+    {
         const char* tc = std::getenv("PIKV_BULK_TC");
         e = (cudaError_t)bulk_insert(D, eng->S, stream, T, k, v, experts, saliency, dst, pr, ctr,
                                      tc ? std::atoi(tc) : 1, st);
@@ -1132,9 +1149,6 @@ int pikv_insert_bulk(pikv_engine* eng, int32_t stream, int64_t T, const void* k,
     unsigned long long host_ctr[2] = {0, 0};
     if (e == cudaSuccess) e = cudaMemcpyAsync(host_ctr, ctr, sizeof(host_ctr), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    cudaFreeAsync(dst, st);
-    if (ctr) cudaFreeAsync(ctr, st);
-    if (pr) cudaFreeAsync(pr, st);
     if (e != cudaSuccess) return fail(PIKV_ERR_CUDA, std::string("insert_bulk: ") + cudaGetErrorString(e));
     int32_t err = 0;
     CUDA_TRY(cudaMemcpy(&err, eng->S.err + stream, sizeof(int32_t), cudaMemcpyDeviceToHost));
@@ -1150,10 +1164,16 @@ int pikv_insert_bulk_host(pikv_engine* eng, int32_t stream, int64_t T, const voi
     const size_t row = (size_t)D.d * (D.kv_dtype == PIKV_DTYPE_BF16 ? 2 : 4);
     cudaSetDevice(eng->device);
     cudaStream_t st = eng->stream;
-    uint8_t* buf = nullptr;
     const size_t nk = row * T, ne = sizeof(int32_t) * (size_t)T * D.k;
     const size_t ns = saliency && D.n_layers > 0 ? sizeof(double) * (size_t)T * D.n_layers : 0;
-    CUDA_TRY(cudaMallocAsync(&buf, 2 * nk + ne + ns + 64, st));
+    if (2 * nk + ne + ns + 64 > eng->stage_cap) {
+        CUDA_TRY(cudaStreamSynchronize(st));
+        if (eng->bulk_stage) cudaFree(eng->bulk_stage);
+        eng->bulk_stage = nullptr, eng->stage_cap = 0;
+        CUDA_TRY(cudaMalloc(&eng->bulk_stage, 2 * nk + ne + ns + 64));
+        eng->stage_cap = 2 * nk + ne + ns + 64;
+    }
+    uint8_t* buf = (uint8_t*)eng->bulk_stage;
     uint8_t* dk = buf;
     uint8_t* dv = buf + nk;
     int32_t* de = (int32_t*)(buf + 2 * nk);
@@ -1164,7 +1184,6 @@ int pikv_insert_bulk_host(pikv_engine* eng, int32_t stream, int64_t T, const voi
     if (e == cudaSuccess && ns) e = cudaMemcpyAsync(ds, saliency, ns, cudaMemcpyHostToDevice, st);
     int rc = e == cudaSuccess ? pikv_insert_bulk(eng, stream, T, dk, dv, de, ds, n_displaced)
                               : fail(PIKV_ERR_CUDA, std::string("insert_bulk_host: ") + cudaGetErrorString(e));
-    cudaFreeAsync(buf, st);
     cudaStreamSynchronize(st);
     return rc;
 }

@@ -2587,7 +2587,7 @@ int bulk_insert(const Dims& D, const State& S, int s, int64_t T, const void* k, 
     cudaMemsetAsync(counters, 0, sizeof(unsigned long long) * (2 + D.Gl), st);
     cudaMemsetAsync(dst, 0xff, sizeof(int64_t) * (size_t)(T * D.k), st);  // -1: not stored here
     if ((D.codec == PIKV_CODEC_LOWRANK || D.codec == PIKV_CODEC_LORAPLUS) && T > 0) {
-        const bool tc_ok = use_tc && launch_bulk_project_tc(D, S, T, k, v, proj, st) == 0;
+        const bool tc_ok = use_tc && launch_bulk_project_tc(D, S, T, k, v, proj, proj + 2 * T * D.dp, st) == 0;
         if (!tc_ok && use_tc == 2) return (int)cudaErrorNotSupported;  // tensor cores required
         if (!tc_ok) {
             const int hd = D.d / D.H;

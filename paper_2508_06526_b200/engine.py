@@ -177,9 +177,12 @@ class Engine:
         self.d = cfg.model.d
 
     def close(self):
-        if getattr(self, "h", None):
-            lib().pikv_engine_destroy(self.h)
-            self.h = None
+        h, self.h = getattr(self, "h", None), None
+        if h:
+            try:
+                lib().pikv_engine_destroy(h)
+            except (AttributeError, TypeError):  # interpreter shutdown: modules torn down
+                pass
 
     __del__ = close
 
