@@ -2282,9 +2282,31 @@ __global__ void __launch_bounds__(kEncWarps * 32)
         if (on) {
             const double* wc = w + (size_t)c0 * d;
             const double* xw = xs + warp * NB * chunk;
-#pragma unroll 4
-            for (int jj = 0; jj < wn; ++jj) {
-                const double wv = wc[(size_t)jj * d];
+            // 16 columns of W in flight before the chains consume them: the
+            // loads are independent of the DADD chains, so they must not sit
+            // on their critical path
+            // software-pipelined: the next 16 columns load while these 16 compute
+            int jj = 0;
+            double wv[16], wn16[16];
+            if (wn >= 16) {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) wv[q] = __ldg(wc + (size_t)q * d);
+            }
+            for (; jj + 16 <= wn; jj += 16) {
+                const bool more = jj + 32 <= wn;
+#pragma unroll
+                for (int q = 0; q < 16; ++q)
+                    wn16[q] = more ? __ldg(wc + (size_t)(jj + 16 + q) * d) : 0.0;
+#pragma unroll
+                for (int q = 0; q < 16; ++q)
+#pragma unroll
+                    for (int u = 0; u < NB; ++u)
+                        acc[u] = __dadd_rn(acc[u], __dmul_rn(wv[q], xw[u * chunk + jj + q]));
+#pragma unroll
+                for (int q = 0; q < 16; ++q) wv[q] = wn16[q];
+            }
+            for (; jj < wn; ++jj) {
+                const double wv = __ldg(wc + (size_t)jj * d);
 #pragma unroll
                 for (int u = 0; u < NB; ++u) acc[u] = __dadd_rn(acc[u], __dmul_rn(wv, xw[u * chunk + jj]));
             }
