@@ -87,7 +87,7 @@ __device__ __forceinline__ const int* route_body(const Dims& D, const Cfg& C, co
         sm_miss[e] = S.miss[(int64_t)s * D.E + e];
         sm_bias[e] = S.bias[(int64_t)s * D.E + e];
     }
-    const bool dbg = s == 0 && tid == 0 && S.dbg;
+    const bool dbg = D.dbg_ctl && s == 0 && tid == 0 && S.dbg;  // PIKV_DEBUG_CTL timestamps
     if (dbg) S.dbg[0] = clock64();
     if (tid == 0) {
         for (int i = 0; i < kRouteStages; ++i) {
@@ -172,11 +172,12 @@ __device__ __forceinline__ const int* route_body(const Dims& D, const Cfg& C, co
             uint32_t phase = 0;
             const int e = tid;
             long long t_wait = 0;
+            const bool timing = D.dbg_ctl != 0;
             for (int c = 0; c < nchunk; ++c) {
                 const int c0 = c * CH, w = min(CH, D.d - c0);
-                const long long tw0 = clock64();
+                const long long tw0 = timing ? clock64() : 0;
                 mbar_wait(&full[stage], phase);
-                t_wait += clock64() - tw0;
+                if (timing) t_wait += clock64() - tw0;
                 if (e < E) {
                     // 32 products into registers (LDS.128 pairs, independent
                     // DMULs), then the 32-long DADD chain: measured 10.5
@@ -1723,8 +1724,7 @@ __device__ __forceinline__ int retrieve_tiles(const Dims& D, const State& S, con
 #pragma unroll
             for (int u = 0; u < kRetrU; ++u)
                 if (jh[u] >= 0) ++mine, atomicAdd(&sm_found[jh[u]], 1);
-            continue;
-        }
+        } else {
         unsigned bal[kRetrU];
 #pragma unroll
         for (int u = 0; u < kRetrU; ++u) {
@@ -1786,6 +1786,7 @@ __device__ __forceinline__ int retrieve_tiles(const Dims& D, const State& S, con
         out += *sm_tile;
         mine += *sm_tile;
         __syncthreads();  // sm_off / sm_tile reused by the next tile
+        }
     }
     return mine;  // kWrite: block total; else this thread's count
 }

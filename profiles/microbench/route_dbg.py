@@ -1,3 +1,4 @@
+import os; os.environ["PIKV_DEBUG_CTL"] = "1"  # route timestamps (dbg slots 0-5)
 import ctypes, sys, numpy as np, torch
 sys.path.insert(0,'.')
 from bench import make_config, WORKLOADS
