@@ -22,9 +22,18 @@
 //    the tensor-core ridge, so CUDA cores are the right unit.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include <algorithm>
 
 #include "pikv_dev.cuh"
+
+#ifndef PIKV_ATTEND_NOHINT
+#define PIKV_ATTEND_NOHINT 0  // experiment builds only: TMA without the L2 evict-first hint
+#endif
+#ifndef PIKV_ATTEND_NOMATH
+#define PIKV_ATTEND_NOMATH 0  // experiment builds only: consumers skip the math
+#endif
 
 namespace pikv_dev {
 
@@ -162,21 +171,52 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
         const uint64_t pol = evict_first_policy();
         int stage = 0;
         uint32_t phase = 0;
+        // The pool indices of the item's entries are read a 32-entry window
+        // ahead (one coalesced load per window, lane i holds entry win + i),
+        // so refilling a stage never waits on a global load.
+        // next item's (position, count) and first index window are loaded
+        // during the current item: no metadata round trips between items
+        auto item_of = [&](int w, int64_t& pos, int& cnt) {
+            if (w < n_items) {
+                pos = (int64_t)S.item_stream[w] * D.att_stride + S.item_begin[w];
+                cnt = S.item_end[w] - S.item_begin[w];
+            } else {
+                pos = 0, cnt = 0;
+            }
+        };
+        int64_t npos;
+        int ncnt;
+        item_of(blockIdx.x, npos, ncnt);
+        int32_t nwin = lane < ncnt ? S.att_entry[npos + lane] : 0;
         for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
-            const int s = S.item_stream[w];
-            const int64_t pos0 = (int64_t)s * D.att_stride + S.item_begin[w];
-            const int cnt = S.item_end[w] - S.item_begin[w];
+            const int64_t pos0 = npos;
+            const int cnt = ncnt;
+            auto win_load = [&](int w0) { return w0 + lane < cnt ? S.att_entry[pos0 + w0 + lane] : 0; };
+            int win = 0;
+            int32_t cur = nwin, nxt = win_load(32);
+            item_of(w + gridDim.x, npos, ncnt);
+            nwin = lane < ncnt ? S.att_entry[npos + lane] : 0;
             for (int b = 0; b < cnt; b += P.EPS) {
                 const int n = min(P.EPS, cnt - b);
+                while (b >= win + 32) win += 32, cur = nxt, nxt = win_load(win + 32);
+                // entry b + lane: from the current window, or the next one when
+                // the stage straddles the boundary (EPS <= 32)
+                const int o = b - win + lane;
+                const int32_t e_cur = __shfl_sync(0xffffffffu, cur, o & 31);
+                const int32_t e_nxt = __shfl_sync(0xffffffffu, nxt, o & 31);
+                const int64_t ent = o < 32 ? e_cur : e_nxt;
                 if (lane == 0) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_expect_tx(&full[stage], (uint32_t)(n * eb));
                 }
                 __syncwarp();
                 if (lane < n) {
-                    const int64_t ent = S.att_entry[pos0 + b + lane];
-                    bulk_g2s(stages + (size_t)stage * P.stage_bytes + (size_t)lane * eb,
-                             S.pool + ent * (int64_t)eb, (uint32_t)eb, &full[stage], pol);
+                    if (PIKV_ATTEND_NOHINT)
+                        bulk_g2s_plain(stages + (size_t)stage * P.stage_bytes + (size_t)lane * eb,
+                                       S.pool + ent * (int64_t)eb, (uint32_t)eb, &full[stage]);
+                    else
+                        bulk_g2s(stages + (size_t)stage * P.stage_bytes + (size_t)lane * eb,
+                                 S.pool + ent * (int64_t)eb, (uint32_t)eb, &full[stage], pol);
                 }
                 if (++stage == P.NST) stage = 0, phase ^= 1;
             }
@@ -214,7 +254,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
             mbar_wait(&full[stage], phase);
             const uint8_t* sb = stages + (size_t)stage * P.stage_bytes;
             // warp-uniform trip count (sub-groups of a warp see different entries)
-            for (int e0 = 0; e0 < n; e0 += P.EP * NB) {
+            for (int e0 = 0; e0 < (PIKV_ATTEND_NOMATH ? 0 : n); e0 += P.EP * NB) {
                 float sc[NB];
 #pragma unroll
                 for (int bb = 0; bb < NB; ++bb) {
@@ -389,6 +429,8 @@ Plan make_plan(const Dims& D) {
     pl.P.NST = nst > 8 ? 8 : nst;
     pl.P.quant = D.codec == PIKV_CODEC_INT8 || D.codec == PIKV_CODEC_INT4;
     pl.P.scale2 = 1.4426950408889634f / sqrtf((float)D.dph);
+
+
     pl.smem = 256 + (size_t)pl.P.NST * pl.P.stage_bytes + redb;
     return pl;
 }

@@ -1,0 +1,87 @@
+// HBM read bandwidth for the attention's access pattern: 4 GB read as
+// blocks of `blk` bytes in a random permutation (pool pages land anywhere),
+// each block streamed by one CTA with TMA bulk copies into a 3 x 32 KB
+// shared-memory ring (2 CTAs/SM, like k_attend) vs plain loads.
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include <algorithm>
+#include <random>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned c) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(c));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned tx) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(tx));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned ph) {
+    asm volatile("{\n .reg .pred p;\n W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W;\n}" ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(ph));
+}
+__device__ __forceinline__ void bulk(void* dst, const void* src, unsigned n, uint64_t* b) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src), "r"(n), "r"((unsigned)__cvta_generic_to_shared(b)) : "memory");
+}
+
+// one warp: producer lane 0 keeps 3 stages of 32 KB in flight; all threads "consume" (checksum 1 word / 16 B)
+__global__ void __launch_bounds__(288, 2) k_tma(const uint8_t* base, const int* perm, int nblk, size_t blk, unsigned* out,
+                                                int pieces) {
+    extern __shared__ __align__(128) uint8_t sm[];
+    uint64_t* full = (uint64_t*)sm;
+    uint8_t* st = sm + 128;
+    const int tid = threadIdx.x;
+    if (tid == 0) { for (int i = 0; i < 3; ++i) mbar_init(&full[i], 1); asm volatile("fence.mbarrier_init.release.cluster;"); }
+    __syncthreads();
+    const size_t per = 32768;
+    unsigned acc = 0;
+    // flattened list of 32 KB pieces of this CTA's blocks
+    const long long npieces = (long long)((nblk + gridDim.x - 1 - blockIdx.x) / gridDim.x) * (blk / per);
+    auto src_of = [&](long long p) {
+        const long long bi = blockIdx.x + (p / (long long)(blk / per)) * gridDim.x;
+        return base + (size_t)perm[bi] * blk + (size_t)(p % (long long)(blk / per)) * per;
+    };
+    auto issue = [&](int s, long long p) {
+        mbar_expect_tx(&full[s], per);
+        for (int q = 0; q < pieces; ++q)
+            bulk(st + s * per + q * (per / pieces), src_of(p) + q * (per / pieces), per / pieces, &full[s]);
+    };
+    if (tid == 0) for (int s = 0; s < 3 && s < npieces; ++s) issue(s, s);
+    for (long long p = 0; p < npieces; ++p) {
+        const int s = p % 3; const unsigned ph = (p / 3) & 1;
+        mbar_wait(&full[s], ph);
+        for (int i = tid; i < (int)(per / 16); i += blockDim.x) acc ^= ((const unsigned*)(st + s * per))[i * 4];
+        __syncthreads();
+        if (tid == 0 && p + 3 < npieces) issue(s, p + 3);
+    }
+    if (acc == 0x12345678u) *out = acc;
+}
+
+int main(int argc, char** argv) {
+    // read 2 GB as random 32 KB blocks drawn from a buffer of `span` GB
+    cudaFuncSetAttribute(k_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 + 3 * 32768);
+    cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+    unsigned* o; cudaMalloc(&o, 4);
+    for (size_t span_gb : {4ul, 12ul, 24ul, 48ul}) {
+        const size_t bytes = span_gb << 30;
+        uint8_t* p;
+        if (cudaMalloc(&p, bytes) != cudaSuccess) { printf("{\"span_gb\": %zu, \"err\": \"oom\"}\n", span_gb); break; }
+        cudaMemset(p, 1, bytes);
+        const size_t blk = 32768;
+        const int nblk_all = (int)(bytes / blk), nblk = (int)((2ull << 30) / blk);
+        std::vector<int> perm(nblk_all);
+        for (int i = 0; i < nblk_all; ++i) perm[i] = i;
+        std::shuffle(perm.begin(), perm.end(), std::mt19937(1));
+        int* dperm; cudaMalloc(&dperm, sizeof(int) * nblk);
+        cudaMemcpy(dperm, perm.data(), sizeof(int) * nblk, cudaMemcpyHostToDevice);
+        float best = 1e9f;
+        for (int r = 0; r < 8; ++r) {
+            cudaEventRecord(a);
+            k_tma<<<296, 288, 128 + 3 * 32768>>>(p, dperm, nblk, blk, o, 2);
+            cudaEventRecord(b); cudaEventSynchronize(b);
+            float ms; cudaEventElapsedTime(&ms, a, b); if (ms < best) best = ms;
+        }
+        printf("{\"span_gb\": %zu, \"read_2gb_random_32k_gbs\": %.1f}\n", span_gb, (2ull << 30) / (best * 1e-3) / 1e9);
+        cudaFree(dperm); cudaFree(p);
+    }
+    return 0;
+}
