@@ -164,6 +164,8 @@ struct pikv_engine {
     bool warmed = false;
     int64_t launches = 0;
     int kernels_per_step = 0;
+    bool fused_retrieval = false;  // PIKV_RETR_FUSED=1: single-pass k_retr_fused (measured: not faster
+                                   // in graph replay, profiles/README.md)
     bool fused_control = false;  // k_control replaces route..retr_write (B <= 8; PIKV_CONTROL=0/1 forces)
     // profiling: per step kPhases+1 events on the engine stream
     bool profiling = false;
@@ -568,6 +570,7 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
         bool want = D.B <= 8;
         if (const char* v = std::getenv("PIKV_CONTROL")) want = v[0] == '1';
         eng->fused_control = control_supported(D, C) && want;
+        if (const char* v = std::getenv("PIKV_RETR_FUSED")) eng->fused_retrieval = v[0] == '1';
     }
 
     // exchange record layout
@@ -644,7 +647,7 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
     chk(S.sel_idx = eng->alloc<int32_t>((size_t)B * std::max(D.Gl, 1) * D.sel_stride));
     const size_t nchunk = (size_t)B * D.max_cand * D.nch;
     chk(S.chunk_cnt = eng->alloc<int32_t>(nchunk));
-    chk(S.chunk_off = eng->alloc<int32_t>(nchunk));
+    chk(S.chunk_off = eng->alloc<int32_t>(2 * nchunk));  // int32 offsets / 64-bit look-back words
     chk(S.found = eng->alloc<int32_t>((size_t)B * k));
     chk(S.att_cnt = eng->alloc<int32_t>(B));
     chk(S.att_slot = eng->alloc<int32_t>(D.att_cap));
@@ -664,7 +667,7 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
     chk(S.summary = eng->alloc<pikv_step_summary>(B));
     chk(S.dbg = eng->alloc<long long>(64 + 8 * (size_t)B));
     chk(S.done_ctr = eng->alloc<unsigned>(1));
-    chk(S.ctl_ctr = eng->alloc<unsigned>(1));
+    chk(S.ctl_ctr = eng->alloc<unsigned>(4));
     const size_t in_elem = c.kv_dtype == PIKV_DTYPE_BF16 ? 2 : 4;
     // q, k, v staging: one allocation, packed back to back
     chk(eng->in_q = eng->alloc<uint8_t>((size_t)3 * B * D.d * in_elem));
@@ -718,7 +721,8 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
     CUDA_TRY(cudaMemsetAsync(S.item_first, 0, sizeof(int32_t) * (B + 1), st));
     CUDA_TRY(cudaMemsetAsync(S.att_cnt, 0, sizeof(int32_t) * B, st));
     CUDA_TRY(cudaMemsetAsync(S.done_ctr, 0, sizeof(unsigned), st));
-    CUDA_TRY(cudaMemsetAsync(S.ctl_ctr, 0, sizeof(unsigned), st));
+    CUDA_TRY(cudaMemsetAsync(S.ctl_ctr, 0, 4 * sizeof(unsigned), st));
+    CUDA_TRY(cudaMemsetAsync(S.chunk_off, 0, 2 * sizeof(int32_t) * nchunk, st));
     std::vector<int32_t> stack(D.pool_pages);
     for (int64_t i = 0; i < D.pool_pages; ++i) stack[i] = (int32_t)(D.pool_pages - 1 - i);
     CUDA_TRY(cudaMemcpyAsync(S.free_stack, stack.data(), sizeof(int32_t) * D.pool_pages,
@@ -838,11 +842,16 @@ static int enqueue_local(pikv_engine* eng, const void* q, const void* k, const v
     mark(eng, 3);
     if (sched) launch_sched_select(D, eng->C, S, st), ++n;
     mark(eng, 4);
-    launch_retr_count(D, S, st), ++n;
-    mark(eng, 5);
-    launch_retr_scan(D, eng->C, S, st), ++n;
-    mark(eng, 6);
-    launch_retr_write(D, S, st), ++n;
+    if (eng->fused_retrieval) {
+        launch_retr_fused(D, eng->C, S, st), ++n;
+        mark(eng, 5), mark(eng, 6);
+    } else {
+        launch_retr_count(D, S, st), ++n;
+        mark(eng, 5);
+        launch_retr_scan(D, eng->C, S, st), ++n;
+        mark(eng, 6);
+        launch_retr_write(D, S, st), ++n;
+    }
     mark(eng, 7);
     }
     if (attend && D.Gl > 0) launch_attend(D, S, st), ++n;

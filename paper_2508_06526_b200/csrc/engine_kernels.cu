@@ -1989,6 +1989,132 @@ void launch_control(const Dims& D, const Cfg& C, const State& S, const void* q, 
                    g.ch);
 }
 
+// Single-pass retrieval (replaces count / scan / write): chunk tiles are
+// taken in (stream, candidate ring, chunk) order through a ticket (so every
+// tile's predecessors are already running: no deadlock however few CTAs are
+// resident); a tile counts its matches, publishes its aggregate, looks back
+// for its predecessors' inclusive prefix (decoupled look-back) and writes
+// its entries in (ring, slot) order.  The last tile builds the work items.
+// S.chunk_off holds the look-back words: bit 63 = inclusive, bit 62 =
+// aggregate only, low 32 bits the value.
+__global__ void __launch_bounds__(1024) k_retr_fused(Dims D, Cfg C, State S) {
+    griddep_enter();
+    __shared__ int sm_tile, sm_off, ws[32];
+    __shared__ int red[32][kMaxK + 1];
+    __shared__ bool sm_last;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = (int)(blockDim.x >> 5);
+    unsigned long long* look = (unsigned long long*)S.chunk_off;  // [B * max_cand * nch]
+    const int per = D.max_cand * D.nch;
+    if (tid == 0) sm_tile = (int)atomicAdd(S.ctl_ctr + 1, 1u);
+    __syncthreads();
+    const int tile = sm_tile;
+    const int s = tile / per, L = tile % per, c = L / D.nch, ch = L % D.nch;
+    const bool active = !S.err[s] && c < S.ncand[s];
+    int j_hit = -1;
+    int64_t ring = 0, gi = 0;
+    const int slot = ch * D.chunk_slots + tid;
+    const uint64_t now = S.now[s];
+    if (active) {
+        ring = (int64_t)s * D.R + S.cand[(int64_t)s * D.max_cand + c];
+        const uint64_t seq = S.seq[ring];
+        const int fill = seq < (uint64_t)D.S ? (int)seq : D.S;
+        if (slot < fill && tid < D.chunk_slots) {
+            gi = ring * D.S + slot;
+            if (S.id[gi] != 0 && S.token[gi] < (int64_t)now) {
+                const int e = S.expert[gi];
+                for (int j = 0; j < D.k; ++j)
+                    if (S.experts[(int64_t)s * D.k + j] == e) {
+                        j_hit = j;
+                        break;
+                    }
+            }
+        }
+    }
+    // block scan of the match flags (slot order) + per-expert hit counts
+    const int m = j_hit >= 0;
+    int x = m;
+    for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, off);
+        if (lane >= off) x += y;
+    }
+    if (lane == 31) ws[warp] = x;
+    for (int j = 0; j < D.k; ++j) {
+        const int cj = __popc(__ballot_sync(0xffffffffu, j_hit == j));
+        if (lane == 0) red[warp][j] = cj;
+    }
+    __syncthreads();
+    if (tid < 32) {
+        int w = tid < nw ? ws[tid] : 0;
+        for (int off = 1; off < 32; off <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, w, off);
+            if (tid >= off) w += y;
+        }
+        ws[tid] = w;
+    }
+    if (active && tid < D.k) {
+        int f = 0;
+        for (int w2 = 0; w2 < nw; ++w2) f += red[w2][tid];
+        if (f) atomicAdd(&S.found[(int64_t)s * D.k + tid], f);
+    }
+    __syncthreads();
+    const int agg = ws[nw - 1];
+    // publish, then look back over this stream's earlier tiles with warp 0:
+    // 32 predecessors per pass, summing aggregates back to the nearest
+    // inclusive prefix (every tile publishes its aggregate right after
+    // counting, so this rarely waits)
+    if (warp == 0) {
+        unsigned long long* base = look + (int64_t)s * per;
+        if (lane == 0) atomicExch(base + L, (L == 0 ? (1ull << 63) : (1ull << 62)) | (unsigned)agg);
+        int acc = 0;
+        for (int p0 = L - 1; p0 >= 0; p0 -= 32) {
+            const int p = p0 - lane;
+            unsigned long long v = 0;
+            if (p >= 0) do {
+                    v = atomicAdd(base + p, 0ull);
+                } while ((v >> 62) == 0);
+            const unsigned incl = __ballot_sync(0xffffffffu, p >= 0 && (v >> 63));
+            const int stop = incl ? __ffs(incl) - 1 : 32;  // nearest inclusive predecessor
+            int part = (p >= 0 && lane <= stop) ? (int)(v & 0xffffffffu) : 0;
+            for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+            acc += part;
+            if (incl) break;
+        }
+        if (lane == 0) {
+            if (L > 0) atomicExch(base + L, (1ull << 63) | (unsigned)(acc + agg));
+            sm_off = acc;
+            __threadfence();
+        }
+    }
+    __syncthreads();
+    if (m) {
+        const int excl = x - 1 + (warp ? ws[warp - 1] : 0);
+        const int64_t pos = (int64_t)s * D.att_stride + sm_off + excl;
+        S.att_slot[pos] = (int32_t)gi;
+        const int32_t page = S.page_table[ring * D.ppr + slot / D.spg];
+        S.att_entry[pos] = page * D.spg + slot % D.spg;
+        const int64_t prec = page_rec(D, ring, S.shard_seq[gi]);
+        atomicAdd((unsigned long long*)&S.pr_sla[prec], (unsigned long long)(now - S.last_access[gi]));
+        atomicAdd((unsigned long long*)&S.pr_sf[prec], 1ull);
+        S.freq[gi] += 1;  // kvstore.cpp:165-168
+        S.last_access[gi] = now;
+    }
+    if (tid == 0 && L == per - 1) S.att_cnt[s] = sm_off + agg;  // the stream's total
+    // last tile: work items over all streams, then reset the look-back words
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) sm_last = atomicAdd(S.ctl_ctr + 2, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!sm_last) return;
+    __threadfence();
+    build_items(D, C, S);
+    for (int i = tid; i < D.B * per; i += blockDim.x) look[i] = 0;
+    if (tid == 0) S.ctl_ctr[1] = 0, S.ctl_ctr[2] = 0;
+}
+
+void launch_retr_fused(const Dims& D, const Cfg& C, const State& S, cudaStream_t st) {
+    launch_pdl(k_retr_fused, dim3(D.B * D.max_cand * D.nch), dim3(D.chunk_slots), 0, st, D, C, S);
+}
+
 void launch_retr_count(const Dims& D, const State& S, cudaStream_t st) {
     launch_pdl(k_retr_count, dim3(D.B, D.max_cand, D.nch), dim3(D.chunk_slots), 0, st, D, S);
 }

@@ -169,7 +169,7 @@ struct State {
     pikv_step_summary* summary;  // [B]
     long long* dbg;              // [64] debug timestamps (k_route, stream 0)
     unsigned* done_ctr;          // last-block counter (k_foldback)
-    unsigned* ctl_ctr;           // last-block counter (k_control)
+    unsigned* ctl_ctr;           // [4] last-block counter (k_control); [1] ticket, [2] done (k_retr_fused)
 };
 
 // ---- helpers -------------------------------------------------------------
@@ -357,6 +357,7 @@ bool control_supported(const Dims& D, const Cfg& C);
 int pick_route_chunk(const Dims& D);
 void launch_control(const Dims& D, const Cfg& C, const State& S, const void* q, const void* k, const void* v,
                     const double* saliency, cudaStream_t st);  // route+insert+evict+retrieve per stream
+void launch_retr_fused(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);  // count+scan+write
 void launch_retr_count(const Dims& D, const State& S, cudaStream_t st);
 void launch_retr_scan(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);
 void launch_retr_write(const Dims& D, const State& S, cudaStream_t st);

@@ -368,3 +368,13 @@ def test_step_host_graph_path_matches_device_path():
                                      host[t, 2].data_ptr(), None, hy.data_ptr()))
         assert torch.equal(ya, hy), t
         assert np.array_equal(a.read_step()[0], b.read_step()[0]), t
+
+
+@pytest.mark.parametrize("sched,kw", [("LRU", dict(S=16, ps=4, budget=3)), ("H2O", dict(H=2))])
+def test_engine_single_pass_retrieval(monkeypatch, sched, kw):
+    """PIKV_RETR_FUSED=1: retrieval as one decoupled-look-back kernel
+    (k_retr_fused) instead of count / scan / write -- same parity bar."""
+    monkeypatch.setenv("PIKV_RETR_FUSED", "1")
+    monkeypatch.setenv("PIKV_CONTROL", "0")
+    cfg = engine_config(router="TopK", sched=sched, batch=3, **kw)
+    run_parity(cfg, 50, 61)
