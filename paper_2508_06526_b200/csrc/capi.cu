@@ -589,6 +589,7 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
     bool ok = true;
     auto chk = [&](void* p) { ok = ok && p != nullptr; };
     D.route_ch = pick_route_chunk(D);
+    if (eng->fused_control) control_geometry(D);  // needs route_ch
     double* W = eng->alloc<double>(router_w_elems(D));
     chk(W);
     S.W = W;

@@ -1940,22 +1940,21 @@ bool control_supported(const Dims& D, const Cfg& C) {
 // power of two <= 8 whose B clusters are all co-resident
 // (cudaOccupancyMaxActiveClusters): a cluster that waits for a second wave
 // delays its whole stream.
-struct CtlGeom {
-    int ch = 0, cl = 1;
-    size_t smem = 0;
-};
-static CtlGeom control_geom(const Dims& D) {
-    CtlGeom g;
-    g.ch = D.route_ch;
-    g.smem = std::max(route_smem_bytes(D, g.ch), insert_smem_bytes(D));
-    if (g.smem > 48 * 1024)
-        cudaFuncSetAttribute(k_control, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
-    g.cl = 1;
+// k_control launch geometry, fixed per engine (Dims::ctl_cl / ctl_smem, set
+// at creation): shared memory for the route ring or the insert staging,
+// and the largest cluster size <= 8 whose B clusters are co-resident
+// (cudaOccupancyMaxActiveClusters) -- a cluster waiting for a second wave
+// delays its whole stream.
+void control_geometry(Dims& D) {
+    size_t smem = std::max(route_smem_bytes(D, D.route_ch), insert_smem_bytes(D));
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(k_control, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int best = 1;
     for (int cl = kMaxCluster; cl > 1; --cl) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(D.B * cl);
         cfg.blockDim = dim3(kCtlThreads);
-        cfg.dynamicSmemBytes = g.smem;
+        cfg.dynamicSmemBytes = smem;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
         attr[0].val.clusterDim.x = (unsigned)cl;
@@ -1965,28 +1964,24 @@ static CtlGeom control_geom(const Dims& D) {
         cfg.numAttrs = 1;
         int active = 0;
         const cudaError_t e = cudaOccupancyMaxActiveClusters(&active, k_control, &cfg);
-        if (D.dbg_ctl) fprintf(stderr, "[k_control] cluster %d: max active %d (B %d, smem %zu, ch %d)\n", cl, active, D.B, g.smem, g.ch);
+        if (D.dbg_ctl)
+            fprintf(stderr, "[k_control] cluster %d: max active %d (B %d, smem %zu, ch %d)\n", cl, active, D.B, smem,
+                    D.route_ch);
         if (e == cudaSuccess && active >= D.B) {
-            g.cl = cl;
+            best = cl;
             break;
         }
         cudaGetLastError();
     }
-    if (const char* v = std::getenv("PIKV_CTL_CLUSTER")) g.cl = std::max(1, std::min(kMaxCluster, std::atoi(v)));
-    return g;
+    if (const char* v = std::getenv("PIKV_CTL_CLUSTER")) best = std::max(1, std::min(kMaxCluster, std::atoi(v)));
+    D.ctl_cl = best;
+    D.ctl_smem = (int)smem;
 }
 
 void launch_control(const Dims& D, const Cfg& C, const State& S, const void* q, const void* k, const void* v,
                     const double* saliency, cudaStream_t st) {
-    static CtlGeom g;
-    static Dims gd{};
-    if (g.ch == 0 || gd.B != D.B || gd.d != D.d || gd.E != D.E || gd.entry_bytes != D.entry_bytes ||
-        gd.route_ch != D.route_ch) {
-        g = control_geom(D);
-        gd = D;
-    }
-    launch_cluster(k_control, dim3(D.B * g.cl), dim3(kCtlThreads), g.smem, st, g.cl, D, C, S, q, k, v, saliency,
-                   g.ch);
+    launch_cluster(k_control, dim3(D.B * D.ctl_cl), dim3(kCtlThreads), (size_t)D.ctl_smem, st, D.ctl_cl, D, C, S,
+                   q, k, v, saliency, D.route_ch);
 }
 
 // Single-pass retrieval (replaces count / scan / write): chunk tiles are

@@ -62,6 +62,7 @@ struct Dims {
     int items_per_cta;  // split-K work items per attention CTA (PIKV_ITEMS, default 4)
     int route_ch;       // router columns per W ring stage (pick_route_chunk)
     int q_f64;          // the step's q is fp64 (QueryEncoder output), not kv_dtype
+    int ctl_cl, ctl_smem;  // k_control cluster size and dynamic smem (control_geometry)
     int dbg_ctl;        // k_control phase timestamps into dbg[64 + 8 s + p] (PIKV_DEBUG_CTL=1)
 };
 
@@ -354,6 +355,7 @@ void launch_sched_pages(const Dims& D, const Cfg& C, const State& S, cudaStream_
 void launch_sched_select(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);
 
 bool control_supported(const Dims& D, const Cfg& C);
+void control_geometry(Dims& D);
 int pick_route_chunk(const Dims& D);
 void launch_control(const Dims& D, const Cfg& C, const State& S, const void* q, const void* k, const void* v,
                     const double* saliency, cudaStream_t st);  // route+insert+evict+retrieve per stream
