@@ -87,6 +87,23 @@ __device__ __forceinline__ void tmem_ld_rows(uint32_t taddr, float* out) {
     for (int j = 0; j < NP; ++j) out[j] = __uint_as_float(r[j]);
 }
 
+// One accumulator row (r <= NP values) to global memory: 16-byte stores when
+// the row is 16-byte aligned (r % 4 == 0), minus the LoRAPlus bias term.
+template <int NP>
+__device__ __forceinline__ void store_row(float* out, const float (&v)[NP], int r, const float* bias) {
+    if ((r & 3) == 0 && (((uintptr_t)out) & 15) == 0) {
+#pragma unroll
+        for (int j = 0; j < NP; j += 4) {
+            if (j >= r) break;
+            float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+            if (bias) o.x -= bias[j], o.y -= bias[j + 1], o.z -= bias[j + 2], o.w -= bias[j + 3];
+            *(float4*)(out + j) = o;
+        }
+    } else {
+        for (int j = 0; j < r; ++j) out[j] = v[j] - (bias ? bias[j] : 0.f);
+    }
+}
+
 template <int NP>
 __global__ void __launch_bounds__(128) k_bulk_project_tc(Dims D, State S, int64_t T, const void* __restrict__ kin,
                                                          const void* __restrict__ vin, float* __restrict__ proj,
@@ -184,7 +201,7 @@ __global__ void __launch_bounds__(128) k_bulk_project_tc(Dims D, State S, int64_
     const int64_t t = t0 + warp * 32 + lane;
     if (t < T) {
         float* out = proj + ((int64_t)row * T + t) * D.dp + h * r;
-        for (int j = 0; j < r; ++j) out[j] = accv[j] - (bias_proj ? bias_proj[h * r + j] : 0.f);
+        store_row(out, accv, r, bias_proj ? bias_proj + h * r : nullptr);
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -203,11 +220,182 @@ __global__ void k_bias_proj(Dims D, State S, float* __restrict__ out) {
     }
 }
 
+// ---- pipelined variant -------------------------------------------------
+// The basis of every head split once into bf16 hi / lo, already in the
+// core-matrix layout: bhl[h][2][NP x hd].
+template <int NP>
+__global__ void k_basis_split(Dims D, State S, uint16_t* __restrict__ bhl) {
+    const int hd = D.d / D.H, r = D.dph, kc = hd / 8;
+    const int64_t per = (int64_t)NP * hd;
+    for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < (int64_t)D.H * per;
+         o += (int64_t)gridDim.x * blockDim.x) {
+        const int h = (int)(o / per), rem = (int)(o % per), j = rem / hd, i = rem % hd;
+        const float f = j < r ? S.basis[((int64_t)h * r + j) * hd + i] : 0.f;
+        const uint16_t hi = bf16_rne(f), lo = bf16_rne(f - bf16_val(hi));
+        const uint32_t off = core_off(j, i, kc) / 2;
+        bhl[(int64_t)h * 2 * per + off] = hi;
+        bhl[(int64_t)h * 2 * per + per + off] = lo;
+    }
+}
+
+// Persistent CTA per (head, K|V) slice of the M tiles: B (hi, lo) staged
+// once; A tiles double-buffered in shared memory with the next tile's
+// global loads in flight (registers) while thread 0 issues this tile's MMAs
+// into one of two TMEM accumulators and the warps drain the previous tile's
+// accumulator (tcgen05.ld) to global memory.  bf16 inputs only (fp32 K/V
+// keep the single-tile kernel).
+template <int NP, int KC>
+__global__ void __launch_bounds__(128) k_bulk_project_tc2(Dims D, int64_t T, const void* __restrict__ kin,
+                                                          const void* __restrict__ vin,
+                                                          const uint16_t* __restrict__ bhl,
+                                                          float* __restrict__ proj,
+                                                          const float* __restrict__ bias_proj) {
+    extern __shared__ __align__(128) uint8_t sm[];
+    constexpr int HD = KC * 8;
+    constexpr uint32_t A_BYTES = (uint32_t)kTcM * HD * 2, B_BYTES = (uint32_t)NP * HD * 2;
+    constexpr int NACC = NP < 32 ? 32 : NP;  // TMEM columns per accumulator
+    const int r = D.dph;
+    const int h = blockIdx.y, row = blockIdx.z, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    uint8_t* a_st[2] = {sm, sm + A_BYTES};
+    uint8_t* b_hl = sm + 2 * A_BYTES;  // hi then lo
+    uint64_t* mbar = (uint64_t*)(b_hl + 2 * B_BYTES);  // [2]
+    uint32_t* tmem_slot = (uint32_t*)(mbar + 2);
+    const uint16_t* x = (const uint16_t*)(row == 0 ? kin : vin);
+    const int64_t ntiles = (T + kTcM - 1) / kTcM;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                     "n"(2 * NACC));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    if (tid == 0) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    {  // B: contiguous copy of the pre-split basis
+        const uint4* src = (const uint4*)(bhl + (int64_t)h * 2 * NP * HD);
+        for (int i = tid; i < (int)(2 * B_BYTES / 16); i += blockDim.x) ((uint4*)b_hl)[i] = src[i];
+    }
+    // A tile t -> registers: thread handles rows rr = tid / KC ... (KC chunks of 16 B per row)
+    constexpr int PER = kTcM * KC / 128;  // 16-byte chunks per thread
+    uint4 regs[PER];
+    auto load_tile = [&](int64_t t) {
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            const int i = tid + u * 128, rr = i / KC, c = i % KC;
+            const int64_t g = t * kTcM + rr;
+            regs[u] = g < T ? *(const uint4*)(x + g * D.d + h * HD + c * 8) : make_uint4(0, 0, 0, 0);
+        }
+    };
+    auto store_tile = [&](uint8_t* dst) {
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            const int i = tid + u * 128, rr = i / KC, c = i % KC;
+            *(uint4*)(dst + core_off(rr, c * 8, KC)) = regs[u];
+        }
+    };
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t idesc = umma_idesc_bf16(NP);
+    // epilogue: the warp's 32 accumulator rows -> smem (transpose) -> one
+    // coalesced row per store instruction (lanes over the row's r values)
+    float* tr = (float*)(tmem_slot + 4) + warp * 32 * (NP + 1);
+    auto drain = [&](int pb, int64_t tile) {
+        float accv[NP];
+        tmem_ld_rows<NP>(tmem + (uint32_t)(pb * NACC) + ((uint32_t)(warp * 32) << 16), accv);
+#pragma unroll
+        for (int j = 0; j < NP; ++j) tr[lane * (NP + 1) + j] = accv[j];
+        __syncwarp();
+        const float bj = (bias_proj && lane < r) ? bias_proj[h * r + lane] : 0.f;
+        for (int rr = 0; rr < 32; ++rr) {
+            const int64_t g = tile * kTcM + warp * 32 + rr;
+            if (g < T && lane < r)
+                proj[((int64_t)row * T + g) * D.dp + h * r + lane] = tr[rr * (NP + 1) + lane] - bj;
+        }
+        if (NP > 32)  // r > 32: second half of the row
+            for (int rr = 0; rr < 32; ++rr) {
+                const int64_t g = tile * kTcM + warp * 32 + rr;
+                const int c = 32 + lane;
+                if (g < T && c < r)
+                    proj[((int64_t)row * T + g) * D.dp + h * r + c] =
+                        tr[rr * (NP + 1) + c] - (bias_proj ? bias_proj[h * r + c] : 0.f);
+            }
+        __syncwarp();
+    };
+    int64_t t = blockIdx.x;
+    if (t < ntiles) load_tile(t);
+    int it = 0;
+    int64_t prev = -1;
+    for (; t < ntiles; t += gridDim.x, ++it) {
+        const int buf = it & 1;
+        store_tile(a_st[buf]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (tid == 0) {
+            const uint32_t A = smem_u32(a_st[buf]), Bh = smem_u32(b_hl), Bl = Bh + B_BYTES;
+            const uint32_t acc = tmem + (uint32_t)(buf * NACC);
+            const uint32_t sbo = KC * 128;
+#pragma unroll
+            for (int ks = 0; ks < KC / 2; ++ks)
+                umma_bf16(acc, umma_desc(A + ks * 256, 128, sbo), umma_desc(Bh + ks * 256, 128, sbo), idesc, ks > 0);
+#pragma unroll
+            for (int ks = 0; ks < KC / 2; ++ks)
+                umma_bf16(acc, umma_desc(A + ks * 256, 128, sbo), umma_desc(Bl + ks * 256, 128, sbo), idesc, 1);
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.b64 [%0];\n" ::"l"(
+                             (uint64_t)__cvta_generic_to_shared(&mbar[buf]))
+                         : "memory");
+        }
+        // next tile's global loads fly while the MMAs run and the previous
+        // accumulator drains
+        if (t + gridDim.x < ntiles) load_tile(t + gridDim.x);
+        if (prev >= 0) {
+            const int pb = buf ^ 1;
+            mbar_wait(&mbar[pb], (uint32_t)(((it - 1) >> 1) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            drain(pb, prev);
+        }
+        prev = t;
+    }
+    if (prev >= 0) {  // drain the last tile
+        const int pb = (it - 1) & 1;
+        mbar_wait(&mbar[pb], (uint32_t)(((it - 1) >> 1) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        drain(pb, prev);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(2 * NACC));
+}
+
 template <int NP>
 int launch_np(const Dims& D, const State& S, int64_t T, const void* k, const void* v, float* proj,
-              const float* bias_proj, cudaStream_t st) {
+              const float* bias_proj, float* scratch_b, cudaStream_t st) {
     const int hd = D.d / D.H;
     const bool f32in = D.kv_dtype != PIKV_DTYPE_BF16;
+    if (!f32in && hd == 128 && scratch_b) {  // pipelined persistent kernel
+        uint16_t* bhl = (uint16_t*)scratch_b;
+        k_basis_split<NP><<<64, 256, 0, st>>>(D, S, bhl);
+        constexpr int KC = 16;
+        const size_t smem = 2 * (size_t)kTcM * 128 * 2 + 2 * (size_t)NP * 128 * 2 + 64 +
+                            sizeof(float) * 4 * 32 * (NP + 1);  // + epilogue transpose
+        cudaFuncSetAttribute(k_bulk_project_tc2<NP, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const int64_t ntiles = (T + kTcM - 1) / kTcM;
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+        // ~2 CTAs per SM over all (head, K|V) pairs
+        int64_t per = (2LL * sms + 2LL * D.H - 1) / (2LL * D.H);
+        if (per > ntiles) per = ntiles;
+        if (per < 1) per = 1;
+        k_bulk_project_tc2<NP, KC><<<dim3((unsigned)per, D.H, 2), 128, smem, st>>>(D, T, k, v, bhl, proj,
+                                                                                    bias_proj);
+        return cudaGetLastError() == cudaSuccess ? 0 : 1;
+    }
     const size_t smem = (size_t)kTcM * hd * 2 * (f32in ? 2 : 1) + (size_t)NP * hd * 2 * 2 + 16 + 16;
     if (smem > 200 * 1024) return 1;
     if (smem > 48 * 1024)
@@ -223,16 +411,17 @@ int launch_bulk_project_tc(const Dims& D, const State& S, int64_t T, const void*
                            float* bias_scratch, cudaStream_t st) {
     const int hd = D.d / D.H, r = D.dph;
     if (hd % 16 != 0 || r < 1 || r > 64 || T <= 0) return 1;
-    // LoRAPlus: bias B^T [H][r] in the caller's scratch
+    // scratch: [H][r] bias B^T, then the pre-split basis (H x 2 x NP x hd bf16)
     float* bias_proj = nullptr;
     if (D.codec == PIKV_CODEC_LORAPLUS) {
         bias_proj = bias_scratch;
         k_bias_proj<<<1, 256, 0, st>>>(D, S, bias_proj);
     }
+    float* bsplit = bias_scratch + ((D.H * r + 63) & ~63);
     int rc;
-    if (r <= 16) rc = launch_np<16>(D, S, T, k, v, proj, bias_proj, st);
-    else if (r <= 32) rc = launch_np<32>(D, S, T, k, v, proj, bias_proj, st);
-    else rc = launch_np<64>(D, S, T, k, v, proj, bias_proj, st);
+    if (r <= 16) rc = launch_np<16>(D, S, T, k, v, proj, bias_proj, bsplit, st);
+    else if (r <= 32) rc = launch_np<32>(D, S, T, k, v, proj, bias_proj, bsplit, st);
+    else rc = launch_np<64>(D, S, T, k, v, proj, bias_proj, bsplit, st);
     return rc;
 }
 

@@ -1237,7 +1237,12 @@ int pikv_insert_bulk(pikv_engine* eng, int32_t stream, int64_t T, const void* k,
     const bool proj = D.codec == PIKV_CODEC_LOWRANK || D.codec == PIKV_CODEC_LORAPLUS;
     const size_t n_dst = sizeof(int64_t) * (size_t)std::max<int64_t>(1, T * D.k);
     const size_t n_ctr = sizeof(unsigned long long) * (2 + D.Gl);
-    const size_t n_pr = proj ? sizeof(float) * (2 * (size_t)std::max<int64_t>(1, T) * D.dp + (size_t)D.dp) : 0;
+    // projections [2][T][dp], then the tcgen05 path's bias B^T [H][r] and
+    // pre-split basis [H][2][64][hd] bf16
+    const size_t n_pr = proj ? sizeof(float) * (2 * (size_t)std::max<int64_t>(1, T) * D.dp +
+                                                (((size_t)D.dp + 63) & ~(size_t)63) +
+                                                (size_t)D.H * 64 * (D.d / D.H) + 64)
+                             : 0;
     const size_t need = ((n_dst + 255) & ~(size_t)255) + ((n_ctr + 255) & ~(size_t)255) + n_pr;
     if (need > eng->bulk_cap) {
         CUDA_TRY(cudaStreamSynchronize(st));

@@ -116,6 +116,8 @@ def test_insert_bulk_empty_and_errors():
 
 
 @pytest.mark.parametrize("codec,dtype,d,H,rank", [
+    ("LowRank", "bf16", 256, 2, 32),    # head width 128, bf16: the pipelined persistent kernel
+    ("LoRAPlus", "bf16", 256, 2, 16),
     ("LowRank", "bf16", 128, 2, 32),
     ("LoRAPlus", "f32", 64, 2, 8),
     ("LowRank", "f32", 256, 2, 64),
