@@ -439,6 +439,36 @@ def main():
                "h2d_bytes_per_step": 3 * B * d * elem, "d2h_bytes_per_step": B * dp * 4,
                "ms_per_step": e2e_ms / args.steps}
         del npdt
+    else:
+        # N ranks: every rank copies its step inputs in from pinned host memory,
+        # runs the sharded step (step_local -> all-gather -> step_finish, the
+        # public multi-rank API) and reads y back; max over ranks
+        elem = 2 if cfg.kv_dtype == "bf16" else 4
+        hq = torch.empty(args.steps, 3, B, d, dtype=tdt).pin_memory()
+        hq.copy_(bank[args.warmup:].cpu())
+        hy = torch.empty(B, dp, dtype=torch.float32).pin_memory()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(es)
+        for i in range(args.steps):
+            with torch.cuda.stream(es):
+                q.copy_(hq[i, 0], non_blocking=True)
+                k.copy_(hq[i, 1], non_blocking=True)
+                v.copy_(hq[i, 2], non_blocking=True)
+            stepper.step(q, k, v, y)
+            with torch.cuda.stream(es):
+                hy.copy_(y, non_blocking=True)
+            es.synchronize()
+        e1.record(es)
+        torch.cuda.synchronize()
+        t_e2e = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t_e2e.item())
+        e2e = {"value": B * args.steps / (e2e_ms * 1e-3), "unit": "tokens/s",
+               "h2d_bytes_per_step": 3 * B * d * elem, "d2h_bytes_per_step": B * dp * 4,
+               "ms_per_step": e2e_ms / args.steps, "per_rank": True}
 
     tokens = B * args.steps
     kv_bytes_step = att_last * entry_bytes  # last step's attended KV (global)
@@ -482,9 +512,18 @@ def main():
             line["cpu_baseline"] = {"value": None, "error": str(ex)}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    eng.close()
     if world > 1:
+        # explicit teardown: every rank done, group gone, engine freed -- then
+        # leave without interpreter teardown (torch/NCCL/gloo destructors
+        # racing the CUDA context aborted the rehearsal run after the result)
+        torch.cuda.synchronize()
+        dist.barrier()
         dist.destroy_process_group()
+        eng.close()
+        sys.stdout.flush()
+        sys.stderr.flush()
+        os._exit(0)
+    eng.close()
 
 
 if __name__ == "__main__":
