@@ -477,6 +477,10 @@ const char* attend_check(const Dims& D) {
 
 int attend_max_smem() { return kSmemBudget; }
 
+// entries per ring stage of the attention plan (work items are sized in
+// multiples of it so no item ends in a partly filled stage)
+int attend_entries_per_stage(const Dims& D) { return make_plan(D).P.EPS; }
+
 void launch_attend(const Dims& D, const State& S, cudaStream_t st) {
     Plan pl = make_plan(D);
     switch (D.codec) {

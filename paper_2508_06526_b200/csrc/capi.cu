@@ -42,6 +42,7 @@ __global__ void k_lr_encode(const float*, const float*, const float*, int32_t, i
 __global__ void k_lr_decode(const float*, const float*, const float*, int32_t, int32_t, int32_t,
                             int32_t, float*);
 const char* attend_check(const Dims& D);
+int attend_entries_per_stage(const Dims& D);
 }  // namespace pikv_dev
 
 namespace {
@@ -523,6 +524,7 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
     D.pool_entries = D.pool_pages * D.spg;
     D.att_stride = std::min<int64_t>((int64_t)D.max_cand * c.S, D.pool_entries);
     D.att_cap = (int64_t)D.B * D.att_stride + 1;
+    D.att_eps = std::max(1, attend_entries_per_stage(D));
     if (const char* msg = attend_check(D)) {
         delete eng;
         return fail(PIKV_ERR_INVALID_CONFIG, std::string("attention layout: ") + msg);

@@ -1564,16 +1564,18 @@ __device__ __forceinline__ void build_items(const Dims& D, const Cfg& C, const S
         }
         return all;
     };
-    int64_t cs = (N + K - 1) / K;
-    if (cs < 16) cs = 16;
+    const int64_t eps = D.att_eps > 0 ? D.att_eps : 1;  // whole ring stages per item
+    auto round_up = [&](int64_t c) { return (c + eps - 1) / eps * eps; };
+    int64_t cs = round_up((N + K - 1) / K);
+    if (cs < 16) cs = round_up(16);
     for (int it = 0; it < 3; ++it) {
         const int64_t t = total_items(cs);
         if (t <= K) break;
-        const int64_t next = (cs * t + K - 1) / K;
-        cs = next > cs ? next : cs + 1;
+        const int64_t next = round_up((cs * t + K - 1) / K);
+        cs = next > cs ? next : cs + eps;
     }
     if (K > D.B) {  // guarantee: sum ceil(n_s / cs) <= N / cs + B <= K
-        const int64_t safe = (N + (K - D.B) - 1) / (K - D.B);
+        const int64_t safe = round_up((N + (K - D.B) - 1) / (K - D.B));
         if (total_items(cs) > K && safe > cs) cs = safe;
     }
     int64_t carry = 0;

@@ -63,6 +63,7 @@ struct Dims {
     int route_ch;       // router columns per W ring stage (pick_route_chunk)
     int q_f64;          // the step's q is fp64 (QueryEncoder output), not kv_dtype
     int ctl_cl, ctl_smem;  // k_control cluster size and dynamic smem (control_geometry)
+    int att_eps;           // k_attend entries per ring stage (item sizes are multiples)
     int dbg_ctl;        // k_control phase timestamps into dbg[64 + 8 s + p] (PIKV_DEBUG_CTL=1)
 };
 
