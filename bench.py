@@ -11,7 +11,11 @@ alpha fold-back.  Default workload (N=1) is BASELINE.json configs[1]:
 prefilled synthetically to L tokens (untimed).  value = decode tokens/s of the
 whole job (B * K / device time, inputs resident in HBM); e2e = the same
 through pikv_step_host with pinned host buffers (H2D of q/k/v, D2H of y inside
-the timed region).  Under torchrun (N>1) the experts are sharded over the
+the timed region).  At N=1 with an even batch the streams run as two
+micro-batches pipelined on the GPU (pikv_group: micro-batch m's control plane
+and fold-back overlap micro-batch m-1's attention; --micro 1 turns it off);
+e2e then goes through pikv_group_submit(host=1) / pikv_group_wait, waiting for
+each micro-batch's y before submitting its next token.  Under torchrun (N>1) the experts are sharded over the
 ranks (G = N logical devices, device g on rank g), the batch grows to 16 N
 streams (per-GPU KV work constant: weak scaling) and the per-step partial
 softmax states are merged with an NCCL all-gather.
@@ -281,6 +285,179 @@ def run_reference_arm(args, w, name):
     print(json.dumps(line), flush=True)
 
 
+DEFAULT_ATTEND_SMS = 0  # 0 = the library's default (all but 24 SMs; profiles/README.md sweep)
+
+
+def run_group(args, w, name, cfg, n_micro, local):
+    """N=1 with the micro-batch pipeline (pikv_group): the batch's streams are
+    split into n_micro engines; micro-batch m's control plane / fold-back
+    overlap micro-batch m-1's attention.  Same metric, config and timing rules
+    as the single-engine path."""
+    import torch
+    from paper_2508_06526_b200.engine import EngineGroup
+    attend_sms = args.attend_sms if args.attend_sms is not None else DEFAULT_ATTEND_SMS
+    if attend_sms <= 0:
+        attend_sms = torch.cuda.get_device_properties(local).multi_processor_count - 24
+    grp = EngineGroup(cfg, n_micro=n_micro, attend_sms=attend_sms, device=local)
+    B, d, dp, Bm = cfg.batch, cfg.model.d, cfg.stored_width, grp.Bm
+    if cfg.compressor.scheme in ("LowRank",):
+        hd, r = cfg.head_dim, cfg.compressor.rank
+        rng = np.random.default_rng(0)
+        basis = np.linalg.qr(rng.standard_normal((hd, hd)))[0][:, :r].T
+        grp.set_codec(np.ascontiguousarray(np.repeat(basis[None], cfg.n_heads, 0), np.float32))
+    t0 = time.time()
+    grp.prefill_synthetic(w["L"], seed=7)
+    prefill_s = time.time() - t0
+
+    tdt = torch.bfloat16 if cfg.kv_dtype == "bf16" else torch.float32
+    nbank = args.warmup + args.steps
+    bank = torch.empty(nbank, 3, B, d, dtype=tdt, device="cuda")
+    for i in range(nbank):
+        for m, e in enumerate(grp.engines):
+            sl = slice(m * Bm, (m + 1) * Bm)
+            e.fill_synthetic(bank[i, 0, sl], bank[i, 1, sl], bank[i, 2, sl], seed=1000 + i + 7919 * m)
+    q = torch.empty(3, B, d, dtype=tdt, device="cuda")
+    y = torch.empty(B, dp, dtype=torch.float32, device="cuda")
+    streams = [e.external_stream() for e in grp.engines]
+    torch.cuda.synchronize()
+
+    def one_step(i):
+        for m in range(n_micro):
+            sl = slice(m * Bm, (m + 1) * Bm)
+            with torch.cuda.stream(streams[m]):
+                q[:, sl].copy_(bank[i, :, sl], non_blocking=True)
+            grp.submit(m, q[0, sl].data_ptr(), q[1, sl].data_ptr(), q[2, sl].data_ptr(), None,
+                       y[sl].data_ptr())
+
+    for i in range(args.warmup):
+        one_step(i)
+    grp.sync()
+    launches0 = grp.kernel_launches()
+    grp.read_timing()
+
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    grp.set_timing(True)
+    with ClockSampler(local) as clk:
+        if args.ncu_window:
+            torch.cuda.cudart().cudaProfilerStart()
+        ev0.record(streams[0])
+        for i in range(args.steps):
+            one_step(args.warmup + i)
+        grp.join()
+        ev1.record(streams[0])
+        torch.cuda.synchronize()
+        if args.ncu_window:
+            torch.cuda.cudart().cudaProfilerStop()
+    grp.set_timing(False)
+    ms = ev0.elapsed_time(ev1)
+    launches = grp.kernel_launches() - launches0
+    att_ms, n_att = grp.read_timing()
+    grp.sync()
+    _, _, _, summ = grp.read_step()
+    att_last = sum(s["n_attended"] for s in summ)
+    entry_bytes = grp.engines[0].entry_bytes()
+    peak, peak_kind = load_peaks()
+    attend_avg_ms = att_ms / max(n_att, 1)
+    alg_per_launch = att_last * entry_bytes / n_micro
+    achieved = alg_per_launch / (attend_avg_ms * 1e-3) / 1e9 if attend_avg_ms else 0.0
+
+    # per-kernel breakdown of one micro-batch engine (eager, events between kernels)
+    e0 = grp.engines[0]
+    e0.set_profiling(True)
+    for i in range(min(args.steps, 20)):
+        sl = slice(0, Bm)
+        with torch.cuda.stream(streams[0]):
+            q[:, sl].copy_(bank[args.warmup + i, :, sl], non_blocking=True)
+        grp.submit(0, q[0, sl].data_ptr(), q[1, sl].data_ptr(), q[2, sl].data_ptr(), None,
+                   y[sl].data_ptr())
+    phases, n_launch = e0.read_profile()
+    e0.set_profiling(False)
+    phase_avg = {k2: round(v / max(n_launch, 1), 4) for k2, v in phases.items()}
+    grp.sync()
+
+    # ---------------- end to end through host buffers ----------------
+    elem = 2 if cfg.kv_dtype == "bf16" else 4
+    hq = torch.empty(args.steps, 3, B, d, dtype=tdt).pin_memory()
+    hq.copy_(bank[args.warmup:].cpu())
+    hy = torch.empty(B, dp, dtype=torch.float32).pin_memory()
+    ptrs = [[(hq[i, 0, m * Bm].data_ptr(), hq[i, 1, m * Bm].data_ptr(), hq[i, 2, m * Bm].data_ptr())
+             for m in range(n_micro)] for i in range(args.steps)]
+    yptr = [hy[m * Bm].data_ptr() for m in range(n_micro)]
+    from paper_2508_06526_b200 import _capi
+    L = _capi.lib()
+    submit, wait, h = L.pikv_group_submit, L.pikv_group_wait, grp.h
+    torch.cuda.synchronize()
+    x0 = torch.cuda.Event(enable_timing=True)
+    x1 = torch.cuda.Event(enable_timing=True)
+    x0.record(streams[0])
+    for i in range(args.steps):
+        for m in range(n_micro):
+            if i:
+                _capi.check(wait(h, m))  # y of micro-batch m's previous step is in host memory
+            pq, pk, pv = ptrs[i][m]
+            _capi.check(submit(h, m, pq, pk, pv, None, yptr[m], 1))
+    for m in range(n_micro):
+        _capi.check(wait(h, m))
+    grp.join()
+    x1.record(streams[0])
+    torch.cuda.synchronize()
+    e2e_ms = x0.elapsed_time(x1)
+    e2e = {"value": B * args.steps / (e2e_ms * 1e-3), "unit": "tokens/s",
+           "h2d_bytes_per_step": 3 * B * d * elem, "d2h_bytes_per_step": B * dp * 4,
+           "ms_per_step": e2e_ms / args.steps,
+           "api": "pikv_group_submit(host=1) / pikv_group_wait per micro-batch"}
+
+    tokens = B * args.steps
+    kv_bytes_step = att_last * entry_bytes
+    line = {
+        "metric": "decode tokens/sec", "value": tokens / (ms * 1e-3), "unit": "tokens/s",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16" if cfg.kv_dtype == "bf16" else "f32",
+        "data": "synthetic (device-generated N(0,1) q/k/v; store prefilled to L)",
+        "config": {"workload": name, "description": WORKLOADS[name][0], "batch": B,
+                   "context": w["L"], "experts": w["E"], "top_k": w["k"], "heads": w["H"],
+                   "head_dim": w["hd"], "codec": w["codec"], "scheduler": "LRU page budget",
+                   "placement": "expert-sharded over 1 GPU(s)", "global_batch": B,
+                   "parallelism": "ep1, %d micro-batches of %d streams pipelined "
+                                  "(control/fold-back of one overlap the other's attention)"
+                                  % (n_micro, Bm),
+                   "micro_batches": n_micro, "attend_sms": attend_sms,
+                   "l2": "inputs larger than L2 (2 GiB KV read per step)",
+                   "prefill_s": round(prefill_s, 2)},
+        "kv_gbs": kv_bytes_step / (ms / args.steps * 1e-3) / 1e9,
+        "kv_frac_of_hbm": kv_bytes_step / (ms / args.steps * 1e-3) / 1e9 / peak,
+        "attended_per_step": att_last,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak,
+                     "traffic": (load_traffic(name) or (None, None))[0],
+                     "traffic_source": (load_traffic(name) or (None, None))[1],
+                     "kernel": "k_attend (decode attention, TMA bulk ring), one launch per "
+                               "micro-batch, timed live in the timed region",
+                     "peak_kind": peak_kind, "avg_launch_ms": attend_avg_ms,
+                     "launches_timed": n_att,
+                     "algorithmic_bytes_per_launch": alg_per_launch,
+                     "attend_share_of_step": att_ms / ms if ms else None},
+        "phase_ms_micro0": phase_avg,
+        "cost_model": cost_model_block(cfg, w, summ, ms / args.steps, peak),
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "e2e": e2e,
+    }
+    if not args.no_cpu_baseline:
+        try:
+            res = cpu_reference(w, steps=2)
+            line["cpu_baseline"] = {k2: res[k2] for k2 in ("value", "unit", "cores", "kind",
+                                                           "sample")}
+        except Exception as ex:  # pragma: no cover
+            line["cpu_baseline"] = {"value": None, "error": str(ex)}
+    print(json.dumps(line), flush=True)
+    grp.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -292,6 +469,10 @@ def main():
     ap.add_argument("--ncu-window", action="store_true",
                     help="cudaProfilerStart/Stop around the timed steps (ncu --profile-from-start off)")
     ap.add_argument("--prefill", type=int, default=None, help="override prefill tokens")
+    ap.add_argument("--micro", type=int, default=None,
+                    help="micro-batches pipelined on the GPU (default 2 at N=1 when B is even)")
+    ap.add_argument("--attend-sms", type=int, default=None,
+                    help="SMs of the persistent attention grid in the micro-batch pipeline")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: stage the exchange through host memory (single-GPU rehearsal)")
     args = ap.parse_args()
@@ -324,6 +505,12 @@ def main():
         # the per-GPU KV read per step stays that of one GPU ("weak" scaling)
         w["B"] = w["B"] * world
     cfg = make_config(w, world=world, rank=rank)
+    n_micro = args.micro if args.micro is not None else (2 if world == 1 and w["B"] % 2 == 0 else 1)
+    if world > 1 or w["B"] % n_micro:
+        n_micro = 1
+    if n_micro > 1:
+        run_group(args, w, name, cfg, n_micro, local)
+        return
     eng = Engine(cfg, device=local)
     B, d, dp = cfg.batch, cfg.model.d, cfg.stored_width
     if cfg.compressor.scheme in ("LowRank",):

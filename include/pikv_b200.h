@@ -344,6 +344,46 @@ int pikv_set_profiling(pikv_engine* eng, int32_t on);
 int pikv_read_profile_host(pikv_engine* eng, float* phase_ms, int32_t n_phases,
                            int32_t* n_steps);
 
+/* ---- micro-batch pipeline (no reference counterpart) ------------------
+ * The reference's Engine is one stream; B streams are B independent
+ * Engine::step calls.  A group splits them into n_micro
+ * engines of B / n_micro streams, each on its own CUDA stream, and orders
+ * only their attention kernels (micro-batch m's attention starts after
+ * micro-batch m-1's): the latency-bound control plane (route, insert, evict,
+ * retrieve) and merge/fold-back of one micro-batch run while another one's
+ * attention streams the KV pool from HBM.  Every stream still executes
+ * exactly the reference's step sequence; results equal those of the
+ * micro-batch engines stepped one after another.
+ * attend_sms > 0 limits the persistent attention grid to that many SMs so
+ * the other micro-batch's control kernels find free SMs (0 = auto: all but
+ * 24 SMs when n_micro > 1, the measured optimum on B200). */
+typedef struct pikv_group pikv_group;
+int pikv_group_create(const pikv_config* cfg, int32_t n_micro, int32_t attend_sms,
+                      int32_t cuda_device, pikv_group** out);
+int pikv_group_destroy(pikv_group* grp);
+int pikv_group_size(pikv_group* grp);
+/* Micro-batch m's engine (its streams are the group's streams
+ * [m B/n, (m+1) B/n)); all per-engine calls apply (readback, codec, ...). */
+pikv_engine* pikv_group_engine(pikv_group* grp, int32_t m);
+/* Enqueue one step of micro-batch m: q/k/v [B/n][d], saliency [B/n][n_layers]
+ * or NULL, y_out [B/n][d'].  host != 0: pinned host buffers (copied in and
+ * out on the micro-batch's stream); host == 0: device buffers.  Returns
+ * without waiting; pikv_group_wait(m) blocks until y_out is written. */
+int pikv_group_submit(pikv_group* grp, int32_t m, const void* q, const void* k, const void* v,
+                      const double* saliency, float* y_out, int32_t host);
+int pikv_group_wait(pikv_group* grp, int32_t m);
+/* One step of all B streams from full-batch device buffers (q/k/v [B][d],
+ * y [B][d']): pikv_group_submit for every micro-batch, no host wait. */
+int pikv_group_step(pikv_group* grp, const void* q, const void* k, const void* v,
+                    const double* saliency, float* y_out);
+/* Make micro-batch 0's stream wait for all work submitted so far. */
+int pikv_group_join(pikv_group* grp);
+int pikv_group_sync(pikv_group* grp);
+/* Attention timing: when on, every submit brackets its attention kernel with
+ * CUDA events; *ms = summed attention time since the last read, *n = count. */
+int pikv_group_set_timing(pikv_group* grp, int32_t on);
+int pikv_group_read_timing(pikv_group* grp, double* ms, int32_t* n);
+
 #ifdef __cplusplus
 }
 #endif

@@ -92,6 +92,17 @@ SIGNATURES = {
     "pikv_kernel_launches": (c_i64, [c_vp]),
     "pikv_set_profiling": (ctypes.c_int, [c_vp, c_i32]),
     "pikv_read_profile_host": (ctypes.c_int, [c_vp, c_vp, c_i32, P(c_i32)]),
+    "pikv_group_create": (ctypes.c_int, [P(PikvConfigC), c_i32, c_i32, c_i32, P(c_vp)]),
+    "pikv_group_destroy": (ctypes.c_int, [c_vp]),
+    "pikv_group_size": (ctypes.c_int, [c_vp]),
+    "pikv_group_engine": (c_vp, [c_vp, c_i32]),
+    "pikv_group_submit": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32]),
+    "pikv_group_wait": (ctypes.c_int, [c_vp, c_i32]),
+    "pikv_group_step": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "pikv_group_join": (ctypes.c_int, [c_vp]),
+    "pikv_group_sync": (ctypes.c_int, [c_vp]),
+    "pikv_group_set_timing": (ctypes.c_int, [c_vp, c_i32]),
+    "pikv_group_read_timing": (ctypes.c_int, [c_vp, P(c_f64), P(c_i32)]),
 }
 
 _LIB = None

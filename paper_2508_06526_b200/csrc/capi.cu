@@ -158,10 +158,19 @@ struct pikv_engine {
     double* q64 = nullptr;
     double* in_emb = nullptr;
     float* out_y = nullptr;
-    // graph cache keyed by (q, k, v, saliency, y, attend)
-    std::map<std::tuple<const void*, const void*, const void*, const void*, void*, int>,
-             cudaGraphExec_t>
+    // graph cache keyed by (q, k, v, saliency, y, attend | emb | parts):
+    // the executable and the number of kernels it launches
+    struct Captured {
+        cudaGraphExec_t ge;
+        int kernels;
+    };
+    std::map<std::tuple<const void*, const void*, const void*, const void*, void*, int>, Captured>
         graphs;
+    void drop_graphs() {
+        for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.ge);
+        graphs.clear();
+    }
+    unsigned warmed_parts = 0;  // step parts run eagerly once (kernel attributes set)
     bool warmed = false;
     int64_t launches = 0;
     int kernels_per_step = 0;
@@ -438,7 +447,9 @@ static int validate(const pikv_config& c) {
     return PIKV_OK;
 }
 
-int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine** out) {
+// attend_sms > 0: the persistent attention grid spans that many SMs (the rest
+// stay free for the other micro-batch's control kernels, pikv_group)
+static int engine_create(const pikv_config* cfg, int32_t cuda_device, int attend_sms, pikv_engine** out) {
     *out = nullptr;
     int rc = validate(*cfg);
     if (rc) return rc;
@@ -500,7 +511,8 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
     D.nch = (c.S + D.chunk_slots - 1) / D.chunk_slots;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device);
-    D.attend_ctas = 2 * sms;  // k_attend runs two CTAs per SM
+    if (const char* v = std::getenv("PIKV_ATTEND_SMS")) attend_sms = std::atoi(v);
+    D.attend_ctas = 2 * (attend_sms > 0 ? std::min(attend_sms, sms) : sms);  // two CTAs per SM
     {
         const char* v = std::getenv("PIKV_ITEMS");
         D.items_per_cta = v ? std::max(1, std::atoi(v)) : 4;
@@ -739,11 +751,15 @@ int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine*
     return PIKV_OK;
 }
 
+int pikv_engine_create(const pikv_config* cfg, int32_t cuda_device, pikv_engine** out) {
+    return engine_create(cfg, cuda_device, 0, out);
+}
+
 int pikv_engine_destroy(pikv_engine* eng) {
     if (!eng) return PIKV_OK;
     cudaSetDevice(eng->device);
     if (eng->stream) cudaStreamSynchronize(eng->stream);
-    for (auto& kv : eng->graphs) cudaGraphExecDestroy(kv.second);
+    eng->drop_graphs();
     for (auto e : eng->ev) cudaEventDestroy(e);
     for (void* p : eng->allocs) cudaFree(p);
     for (auto e : {eng->ev_fork, eng->ev_kv, eng->ev_y, eng->ev_join})
@@ -784,7 +800,7 @@ int pikv_set_codec_host(pikv_engine* eng, const float* basis, const float* bias,
             if (kept[i] < 0 || kept[i] >= hd) return fail(PIKV_ERR_INVALID_ARGUMENT, "kept index out of range");
         eng->S.kept = (const int32_t*)up(kept, sizeof(int32_t) * (size_t)D.H * r);
     }
-    eng->graphs.clear();  // captured kernels hold the old pointers
+    eng->drop_graphs();  // captured kernels hold the old pointers
     return PIKV_OK;
 }
 
@@ -808,22 +824,33 @@ static void mark(pikv_engine* eng, int phase) {
     cudaEventRecord(eng->ev[eng->cur + phase], eng->stream);
 }
 
+// Parts of one step, enqueued together or separately (the micro-batch
+// pipeline of pikv_group interleaves them across engines):
+//   CTL    route -> insert -> evict -> retrieve (latency-bound control plane)
+//   ATTEND decode attention (HBM-bound)
+//   TAIL   combine (y) -> [finish merge] -> fold-back + feedback
+enum : unsigned { kPartCtl = 1u, kPartAttend = 2u, kPartTail = 4u, kPartAll = 7u };
+
 // The step's launch sequence (pipeline.cpp:213-351 ordering).
 // kv_ready: if set, waited on (stream-ordered) right before the first
 // kernel that reads k/v; y_ready: if set, recorded as soon as y is written.
 static int enqueue_local(pikv_engine* eng, const void* q, const void* k, const void* v,
                          const double* sal, bool attend, float* y, bool q_f64 = false,
-                         cudaEvent_t kv_ready = nullptr, cudaEvent_t y_ready = nullptr) {
+                         cudaEvent_t kv_ready = nullptr, cudaEvent_t y_ready = nullptr,
+                         unsigned parts = kPartAll) {
     Dims D = eng->D;
     D.q_f64 = q_f64 ? 1 : 0;
     const State& S = eng->S;
     cudaStream_t st = eng->stream;
     int n = 0;
-    eng->cur = -1;
-    if (eng->profiling && eng->prof_steps < kProfSteps) eng->cur = eng->prof_steps++ * (kPhases + 1);
+    if (parts & kPartCtl) {
+        eng->cur = -1;
+        if (eng->profiling && eng->prof_steps < kProfSteps) eng->cur = eng->prof_steps++ * (kPhases + 1);
+    }
     mark(eng, 0);
     const bool proj = D.codec == PIKV_CODEC_LOWRANK || D.codec == PIKV_CODEC_LORAPLUS;
-    if (eng->fused_control) {
+    if (!(parts & kPartCtl)) {
+    } else if (eng->fused_control) {
         // one CTA per stream runs route -> insert -> evict -> retrieve
         if (kv_ready) cudaStreamWaitEvent(st, kv_ready, 0);
         if (proj) launch_project(D, S, q, k, v, st), ++n;
@@ -857,11 +884,13 @@ static int enqueue_local(pikv_engine* eng, const void* q, const void* k, const v
     }
     mark(eng, 7);
     }
-    if (attend && D.Gl > 0) launch_attend(D, S, st), ++n;
+    if ((parts & kPartAttend) && attend && D.Gl > 0) launch_attend(D, S, st), ++n;
     mark(eng, 8);
-    const int direct = D.world == 1;  // single rank: combine writes y
-    if (attend || !direct) launch_combine(D, eng->C, S, eng->X, y, direct, attend, st), ++n;
-    if (y_ready) cudaEventRecord(y_ready, st);
+    if (parts & kPartTail) {
+        const int direct = D.world == 1;  // single rank: combine writes y
+        if (attend || !direct) launch_combine(D, eng->C, S, eng->X, y, direct, attend, st), ++n;
+        if (y_ready) cudaEventRecord(y_ready, st);
+    }
     mark(eng, 9);
     CUDA_TRY(cudaGetLastError());
     eng->kernels_per_step = n;
@@ -889,53 +918,52 @@ static int enqueue_finish(pikv_engine* eng, const uint8_t* gathered, float* y, b
 // pipeline.cpp:222): the QueryEncoder kernel writes q (fp64) and the stored
 // K/V, then the step proceeds on them.
 static int enqueue_step(pikv_engine* eng, const double* emb, const void* q, const void* k, const void* v,
-                        const double* sal, float* y, bool attend) {
-    if (emb) {
+                        const double* sal, float* y, bool attend, unsigned parts = kPartAll) {
+    if (emb && (parts & kPartCtl)) {
         launch_encode(eng->D, eng->enc_wt, emb, eng->q64, eng->in_k, eng->in_v, eng->stream);
-        q = eng->q64, k = eng->in_k, v = eng->in_v;
     }
-    int rc = enqueue_local(eng, q, k, v, sal, attend, y, emb != nullptr);
-    if (!rc) rc = enqueue_finish(eng, eng->S.exchange, y, attend, 1);
-    if (emb) eng->kernels_per_step += (eng->D.B + 63) / 64;
+    if (emb) q = eng->q64, k = eng->in_k, v = eng->in_v;
+    int rc = enqueue_local(eng, q, k, v, sal, attend, y, emb != nullptr, nullptr, nullptr, parts);
+    if (!rc && (parts & kPartTail)) rc = enqueue_finish(eng, eng->S.exchange, y, attend, 1);
+    if (emb && (parts & kPartCtl)) eng->kernels_per_step += (eng->D.B + 63) / 64;
     return rc;
 }
 
 static int run_step(pikv_engine* eng, const void* q, const void* k, const void* v,
-                    const double* sal, float* y, bool attend, const double* emb = nullptr) {
+                    const double* sal, float* y, bool attend, const double* emb = nullptr,
+                    unsigned parts = kPartAll) {
     int rc = codec_ready(eng);
     if (rc) return rc;
     if (eng->D.world != 1)
         return fail(PIKV_ERR_INVALID_ARGUMENT, "world_size > 1: use pikv_step_local / pikv_step_finish");
     cudaSetDevice(eng->device);
-    const bool use_graph = eng->warmed && !eng->profiling;
+    const bool use_graph = (eng->warmed_parts & parts) == parts && !eng->profiling;
     if (!use_graph) {
-        rc = enqueue_step(eng, emb, q, k, v, sal, y, attend);
+        rc = enqueue_step(eng, emb, q, k, v, sal, y, attend, parts);
         if (rc) return rc;
-        eng->warmed = true;  // first eager pass sets kernel attributes
+        eng->warmed_parts |= parts;  // first eager pass sets kernel attributes
+        eng->warmed = eng->warmed_parts == kPartAll;
         eng->launches += eng->kernels_per_step;
         return PIKV_OK;
     }
     auto key = std::make_tuple(emb ? (const void*)emb : q, k, v, (const void*)sal, (void*)y,
-                               (attend ? 1 : 0) + (emb ? 2 : 0));
+                               (attend ? 1 : 0) + (emb ? 2 : 0) + (int)(parts << 2));
     auto it = eng->graphs.find(key);
     if (it == eng->graphs.end()) {
         cudaGraph_t g;
         CUDA_TRY(cudaStreamBeginCapture(eng->stream, cudaStreamCaptureModeThreadLocal));
-        rc = enqueue_step(eng, emb, q, k, v, sal, y, attend);
+        rc = enqueue_step(eng, emb, q, k, v, sal, y, attend, parts);
         cudaError_t ce = cudaStreamEndCapture(eng->stream, &g);
         if (rc) return rc;
         if (ce != cudaSuccess) return fail(PIKV_ERR_CUDA, std::string("capture: ") + cudaGetErrorString(ce));
         cudaGraphExec_t ge;
         CUDA_TRY(cudaGraphInstantiate(&ge, g, 0));
         cudaGraphDestroy(g);
-        if (eng->graphs.size() > 8) {
-            for (auto& kv : eng->graphs) cudaGraphExecDestroy(kv.second);
-            eng->graphs.clear();
-        }
-        it = eng->graphs.emplace(key, ge).first;
+        if (eng->graphs.size() > 16) eng->drop_graphs();
+        it = eng->graphs.emplace(key, pikv_engine::Captured{ge, eng->kernels_per_step}).first;
     }
-    CUDA_TRY(cudaGraphLaunch(it->second, eng->stream));
-    eng->launches += eng->kernels_per_step;
+    CUDA_TRY(cudaGraphLaunch(it->second.ge, eng->stream));
+    eng->launches += it->second.kernels;
     return PIKV_OK;
 }
 
@@ -1541,6 +1569,207 @@ int pikv_read_profile_host(pikv_engine* eng, float* phase_ms, int32_t n_phases, 
     for (int p = 0; p < n_phases && p < kPhases; ++p) phase_ms[p] = acc[p];
     if (n_steps) *n_steps = eng->prof_steps;
     eng->prof_steps = 0;
+    return PIKV_OK;
+}
+
+// ---------------------------------------------------------------------------
+// micro-batch pipeline
+// ---------------------------------------------------------------------------
+struct pikv_group {
+    int n = 0;
+    int device = 0;
+    std::vector<pikv_engine*> eng;
+    std::vector<cudaEvent_t> att_done;  // per micro-batch: its last attention
+    std::vector<cudaEvent_t> y_done;    // per micro-batch: its last y written
+    cudaEvent_t join = nullptr;
+    bool timing = false;
+    // timing: per micro-batch, event pairs of submitted steps not yet read
+    std::vector<std::vector<std::pair<cudaEvent_t, cudaEvent_t>>> tev;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tfree;
+    size_t in_bytes = 0, y_bytes = 0, sal_elems = 0;  // per micro-batch
+};
+
+int pikv_group_create(const pikv_config* cfg, int32_t n_micro, int32_t attend_sms, int32_t cuda_device,
+                      pikv_group** out) {
+    *out = nullptr;
+    if (n_micro < 1 || cfg->batch % n_micro != 0)
+        return fail(PIKV_ERR_INVALID_CONFIG, "batch must be a multiple of n_micro");
+    if (cfg->world_size != 1) return fail(PIKV_ERR_INVALID_CONFIG, "pikv_group: world_size must be 1");
+    int rc = validate(*cfg);
+    if (rc) return rc;
+    CUDA_TRY(cudaSetDevice(cuda_device));
+    auto* g = new pikv_group();
+    g->n = n_micro;
+    g->device = cuda_device;
+    pikv_config c = *cfg;
+    c.batch = cfg->batch / n_micro;
+    if (cfg->pool_entries > 0) c.pool_entries = cfg->pool_entries / n_micro;
+    if (attend_sms <= 0 && n_micro > 1) {
+        // leave 24 SMs to the control plane of the other micro-batch
+        // (c2 sweep, profiles/README.md: 148 -> 34.3 K, 136 -> 39.0 K,
+        // 124 -> 42.1 K, 112 -> 41.8 K tokens/s)
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device);
+        attend_sms = std::max(1, sms - 24);
+    }
+    for (int m = 0; m < n_micro; ++m) {
+        pikv_engine* e = nullptr;
+        rc = engine_create(&c, cuda_device, attend_sms, &e);
+        if (rc) {
+            pikv_group_destroy(g);
+            return rc;
+        }
+        // the cluster control kernel (one CTA per SM per cluster rank) cannot
+        // share SMs with the other micro-batch's attention: use the multi-kernel
+        // control plane unless PIKV_CONTROL=1 forces it
+        const char* cv = std::getenv("PIKV_CONTROL");
+        if (!(cv && cv[0] == '1')) e->fused_control = false;
+        g->eng.push_back(e);
+        cudaEvent_t a, y;
+        cudaEventCreateWithFlags(&a, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&y, cudaEventDisableTiming);
+        g->att_done.push_back(a);
+        g->y_done.push_back(y);
+    }
+    cudaEventCreateWithFlags(&g->join, cudaEventDisableTiming);
+    g->tev.resize(n_micro);
+    const Dims& D = g->eng[0]->D;
+    g->in_bytes = (size_t)D.B * D.d * (D.kv_dtype == PIKV_DTYPE_BF16 ? 2 : 4);
+    g->y_bytes = sizeof(float) * (size_t)D.B * D.dp;
+    g->sal_elems = (size_t)D.B * D.n_layers;
+    *out = g;
+    return PIKV_OK;
+}
+
+int pikv_group_destroy(pikv_group* g) {
+    if (!g) return PIKV_OK;
+    cudaSetDevice(g->device);
+    for (auto* e : g->eng) pikv_engine_destroy(e);
+    for (auto e : g->att_done) cudaEventDestroy(e);
+    for (auto e : g->y_done) cudaEventDestroy(e);
+    for (auto& v : g->tev)
+        for (auto& p : v) cudaEventDestroy(p.first), cudaEventDestroy(p.second);
+    for (auto& p : g->tfree) cudaEventDestroy(p.first), cudaEventDestroy(p.second);
+    if (g->join) cudaEventDestroy(g->join);
+    delete g;
+    return PIKV_OK;
+}
+
+int pikv_group_size(pikv_group* g) { return g->n; }
+
+pikv_engine* pikv_group_engine(pikv_group* g, int32_t m) {
+    return m >= 0 && m < g->n ? g->eng[m] : nullptr;
+}
+
+int pikv_group_submit(pikv_group* g, int32_t m, const void* q, const void* k, const void* v,
+                      const double* sal, float* y, int32_t host) {
+    if (m < 0 || m >= g->n) return fail(PIKV_ERR_INVALID_ARGUMENT, "micro-batch index out of range");
+    pikv_engine* e = g->eng[m];
+    cudaSetDevice(g->device);
+    int rc = codec_ready(e);
+    if (rc) return rc;
+    cudaStream_t st = e->stream;
+    const void *dq = q, *dk = k, *dv = v;
+    const double* ds = sal;
+    float* dy = y;
+    if (host) {
+        CUDA_TRY(cudaMemcpyAsync(e->in_q, q, g->in_bytes, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaMemcpyAsync(e->in_k, k, g->in_bytes, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaMemcpyAsync(e->in_v, v, g->in_bytes, cudaMemcpyHostToDevice, st));
+        if (sal && g->sal_elems)
+            CUDA_TRY(cudaMemcpyAsync(e->in_sal, sal, sizeof(double) * g->sal_elems, cudaMemcpyHostToDevice, st));
+        dq = e->in_q, dk = e->in_k, dv = e->in_v, ds = sal ? e->in_sal : nullptr, dy = e->out_y;
+    }
+    if (e->profiling) {
+        rc = run_step(e, dq, dk, dv, ds, dy, true);
+    } else {
+        // control graph -> [wait for the previous micro-batch's attention] ->
+        // attention graph -> [record] -> tail graph; the ordering is stream
+        // API calls between the graph launches.  (Attention on a separate
+        // highest-priority stream measured slower: 37.5 vs 42.1 K tokens/s at c2.)
+        rc = run_step(e, dq, dk, dv, ds, dy, true, nullptr, kPartCtl);
+        if (!rc) {
+            if (g->n > 1) CUDA_TRY(cudaStreamWaitEvent(st, g->att_done[(m + g->n - 1) % g->n], 0));
+            std::pair<cudaEvent_t, cudaEvent_t> p{nullptr, nullptr};
+            if (g->timing) {
+                if (g->tfree.empty()) {
+                    CUDA_TRY(cudaEventCreate(&p.first));
+                    CUDA_TRY(cudaEventCreate(&p.second));
+                } else {
+                    p = g->tfree.back();
+                    g->tfree.pop_back();
+                }
+                g->tev[m].push_back(p);
+                CUDA_TRY(cudaEventRecord(p.first, st));
+            }
+            rc = run_step(e, dq, dk, dv, ds, dy, true, nullptr, kPartAttend);
+            if (p.second) CUDA_TRY(cudaEventRecord(p.second, st));
+            CUDA_TRY(cudaEventRecord(g->att_done[m], st));
+        }
+        if (!rc) rc = run_step(e, dq, dk, dv, ds, dy, true, nullptr, kPartTail);
+    }
+    if (rc) return rc;
+    if (host) CUDA_TRY(cudaMemcpyAsync(y, e->out_y, g->y_bytes, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaEventRecord(g->y_done[m], st));
+    return PIKV_OK;
+}
+
+int pikv_group_wait(pikv_group* g, int32_t m) {
+    if (m < 0 || m >= g->n) return fail(PIKV_ERR_INVALID_ARGUMENT, "micro-batch index out of range");
+    CUDA_TRY(cudaEventSynchronize(g->y_done[m]));
+    return PIKV_OK;
+}
+
+int pikv_group_step(pikv_group* g, const void* q, const void* k, const void* v, const double* sal,
+                    float* y) {
+    for (int m = 0; m < g->n; ++m) {
+        const size_t o = (size_t)m * g->in_bytes;
+        int rc = pikv_group_submit(g, m, (const uint8_t*)q + o, (const uint8_t*)k + o, (const uint8_t*)v + o,
+                                   sal ? sal + (size_t)m * g->sal_elems : nullptr,
+                                   y ? (float*)((uint8_t*)y + (size_t)m * g->y_bytes) : nullptr, 0);
+        if (rc) return rc;
+    }
+    return PIKV_OK;
+}
+
+int pikv_group_join(pikv_group* g) {
+    cudaSetDevice(g->device);
+    cudaStream_t s0 = g->eng[0]->stream;
+    for (int m = 1; m < g->n; ++m) {
+        CUDA_TRY(cudaEventRecord(g->join, g->eng[m]->stream));
+        CUDA_TRY(cudaStreamWaitEvent(s0, g->join, 0));
+    }
+    return PIKV_OK;
+}
+
+int pikv_group_sync(pikv_group* g) {
+    for (auto* e : g->eng) {
+        int rc = pikv_sync(e);
+        if (rc) return rc;
+    }
+    return PIKV_OK;
+}
+
+int pikv_group_set_timing(pikv_group* g, int32_t on) {
+    g->timing = on != 0;
+    return PIKV_OK;
+}
+
+int pikv_group_read_timing(pikv_group* g, double* ms, int32_t* n) {
+    double tot = 0;
+    int cnt = 0;
+    for (auto& v : g->tev) {
+        for (auto& p : v) {
+            CUDA_TRY(cudaEventSynchronize(p.second));
+            float t = 0;
+            CUDA_TRY(cudaEventElapsedTime(&t, p.first, p.second));
+            tot += t, ++cnt;
+            g->tfree.push_back(p);
+        }
+        v.clear();
+    }
+    if (ms) *ms = tot;
+    if (n) *n = cnt;
     return PIKV_OK;
 }
 

@@ -176,9 +176,21 @@ class Engine:
         self.dp = cfg.stored_width
         self.d = cfg.model.d
 
+    @classmethod
+    def _borrowed(cls, cfg: EngineConfig, handle, device: int):
+        """An engine owned by a group (not destroyed by this object)."""
+        self = cls.__new__(cls)
+        self.cfg, self._c = cfg, cfg.to_c()
+        self.h, self._owned, self.device = ctypes.c_void_p(handle), False, device
+        self.B = cfg.batch
+        self.E, self.k = cfg.model.E, cfg.router.k
+        self.dp = cfg.stored_width
+        self.d = cfg.model.d
+        return self
+
     def close(self):
         h, self.h = getattr(self, "h", None), None
-        if h:
+        if h and getattr(self, "_owned", True):
             try:
                 lib().pikv_engine_destroy(h)
             except (AttributeError, TypeError):  # interpreter shutdown: modules torn down
@@ -410,3 +422,89 @@ class Engine:
 __all__ = ["Engine", "EngineConfig", "EvictionRecord", "PikvError", "ShardId", "attention",
            "dequantize", "lowrank_decode", "lowrank_encode", "quantize", "select_evictions",
            "shard_assign", "_capi"]
+
+
+class EngineGroup:
+    """B streams split into ``n_micro`` engines pipelined on one GPU
+    (include/pikv_b200.h, pikv_group_*): micro-batch m's control plane and
+    fold-back overlap the other micro-batches' attention.  No reference
+    counterpart; each stream still runs Engine::step (pipeline.cpp:213-351)."""
+
+    def __init__(self, cfg: EngineConfig, n_micro: int = 2, attend_sms: int = 0, device: int = 0):
+        import dataclasses
+        self.cfg = cfg
+        self._c = cfg.to_c()
+        h = ctypes.c_void_p()
+        check(lib().pikv_group_create(ctypes.byref(self._c), n_micro, attend_sms, device,
+                                      ctypes.byref(h)))
+        self.h, self.n, self.device = h, n_micro, device
+        self.B, self.dp, self.d = cfg.batch, cfg.stored_width, cfg.model.d
+        self.Bm = cfg.batch // n_micro
+        mcfg = dataclasses.replace(cfg, batch=self.Bm)
+        self.engines = [Engine._borrowed(mcfg, lib().pikv_group_engine(h, m), device)
+                        for m in range(n_micro)]
+
+    def close(self):
+        h, self.h = getattr(self, "h", None), None
+        if h:
+            for e in self.engines:
+                e.h = None
+            try:
+                lib().pikv_group_destroy(h)
+            except (AttributeError, TypeError):
+                pass
+
+    __del__ = close
+
+    def step(self, q, k, v, saliency=None, y=None):
+        """One step of all B streams on full-batch device tensors (no host wait)."""
+        if y is None:
+            y = torch.empty(self.B, self.dp, dtype=torch.float32, device="cuda")
+        cur = torch.cuda.current_stream()
+        for e in self.engines:
+            e.external_stream().wait_stream(cur)
+        check(lib().pikv_group_step(self.h, _ptr(q), _ptr(k), _ptr(v), _ptr(saliency), _ptr(y)))
+        for e in self.engines:
+            cur.wait_stream(e.external_stream())
+        return y
+
+    def submit(self, m: int, q, k, v, saliency=None, y=None, host: bool = False):
+        """Enqueue micro-batch m's step (raw pointers or tensors / arrays)."""
+        conv = (lambda a: a if isinstance(a, int) or a is None else
+                (a.ctypes.data if isinstance(a, np.ndarray) else a.data_ptr()))
+        check(lib().pikv_group_submit(self.h, m, conv(q), conv(k), conv(v), conv(saliency),
+                                      conv(y), int(host)))
+
+    def wait(self, m: int):
+        check(lib().pikv_group_wait(self.h, m))
+
+    def join(self):
+        check(lib().pikv_group_join(self.h))
+
+    def sync(self):
+        check(lib().pikv_group_sync(self.h))
+
+    def set_timing(self, on: bool):
+        check(lib().pikv_group_set_timing(self.h, int(on)))
+
+    def read_timing(self):
+        ms, n = ctypes.c_double(), ctypes.c_int32()
+        check(lib().pikv_group_read_timing(self.h, ctypes.byref(ms), ctypes.byref(n)))
+        return ms.value, n.value
+
+    def prefill_synthetic(self, tokens: int, seed: int = 1):
+        for m, e in enumerate(self.engines):
+            e.prefill_synthetic(tokens, seed=seed + 7919 * m)
+
+    def set_codec(self, basis=None, bias=None, kept=None):
+        for e in self.engines:
+            e.set_codec(basis, bias, kept)
+
+    def kernel_launches(self) -> int:
+        return sum(e.kernel_launches() for e in self.engines)
+
+    def read_step(self):
+        """Concatenated (experts, gates, logits, summaries) over micro-batches."""
+        parts = [e.read_step() for e in self.engines]
+        return (np.concatenate([p[0] for p in parts]), np.concatenate([p[1] for p in parts]),
+                np.concatenate([p[2] for p in parts]), sum((list(p[3]) for p in parts), []))
