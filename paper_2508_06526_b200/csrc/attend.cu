@@ -138,6 +138,7 @@ struct AttParams {
     int stage_bytes;
     int quant;        // INT8/INT4: per-(entry, head) scales after the payloads
     float scale2;     // log2(e) / sqrt(dph)
+    int dyn;          // work items from the global ticket (1) or strided by CTA (0)
 };
 
 // Thread (sub, head, j) owns chunks j + i*LPH (i < CPT) of one head: the
@@ -148,8 +149,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
     griddep_enter();
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr int N = Dec::N, NP = N / 2;
-    uint64_t* full = (uint64_t*)smem;
+    uint64_t* full = (uint64_t*)smem;  // [0, 8): stage ring (NST <= 8)
     uint64_t* empty = full + 16;
+    // work-item queue, producer -> consumers: item index in iq, handed over
+    // with ifull / iempty (the producer fetches the next item while the
+    // consumers still work on the current one)
+    uint64_t* ifull = full + 8;
+    uint64_t* iempty = empty + 8;
+    int* iq = (int*)(full + 12);
+    constexpr int NQ = 4;
     uint8_t* stages = smem + 256;
     float* red = (float*)(stages + (size_t)P.NST * P.stage_bytes);  // EP merge scratch
     const int tid = threadIdx.x;
@@ -158,6 +166,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
         for (int i = 0; i < P.NST; ++i) {
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], kConsumers / 32);
+        }
+        for (int i = 0; i < NQ; ++i) {
+            mbar_init(&ifull[i], 1);
+            mbar_init(&iempty[i], kConsumers / 32);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -184,17 +196,40 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
                 pos = 0, cnt = 0;
             }
         };
+        // Items are taken from a global ticket (n_items[1], reset by the
+        // kernel that builds them) so CTAs that start late -- their SM still
+        // busy with the previous micro-batch's tail kernels -- simply run
+        // fewer items; P.dyn = 0 strides them statically (blockIdx + i*grid).
+        auto next_item = [&](int prev) -> int {
+            if (!P.dyn) return prev < 0 ? (int)blockIdx.x : prev + (int)gridDim.x;
+            int w = 0;
+            if (lane == 0) w = atomicAdd(&S.n_items[1], 1);
+            return __shfl_sync(0xffffffffu, w, 0);
+        };
+        int kq = 0;
+        auto publish = [&](int w) {
+            if (lane == 0) {
+                mbar_wait(&iempty[kq % NQ], ((kq / NQ) & 1) ^ 1);
+                *(volatile int*)&iq[kq % NQ] = w;
+                mbar_arrive(&ifull[kq % NQ]);
+            }
+            ++kq;
+        };
         int64_t npos;
         int ncnt;
-        item_of(blockIdx.x, npos, ncnt);
+        int w = next_item(-1);
+        item_of(w, npos, ncnt);
         int32_t nwin = lane < ncnt ? S.att_entry[npos + lane] : 0;
-        for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+        for (;;) {
+            publish(w);
+            if (w >= n_items) break;
             const int64_t pos0 = npos;
             const int cnt = ncnt;
             auto win_load = [&](int w0) { return w0 + lane < cnt ? S.att_entry[pos0 + w0 + lane] : 0; };
             int win = 0;
             int32_t cur = nwin, nxt = win_load(32);
-            item_of(w + gridDim.x, npos, ncnt);
+            const int wn = next_item(w);
+            item_of(wn, npos, ncnt);
             nwin = lane < ncnt ? S.att_entry[npos + lane] : 0;
             for (int b = 0; b < cnt; b += P.EPS) {
                 const int n = min(P.EPS, cnt - b);
@@ -220,6 +255,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
                 }
                 if (++stage == P.NST) stage = 0, phase ^= 1;
             }
+            w = wn;
         }
         return;
     }
@@ -234,7 +270,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
     for (int i = 0; i < CPT; ++i) coff[i] = (head * P.CPH + j + i * P.LPH) * 16;
     int stage = 0;
     uint32_t phase = 0;
-    for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+    for (int kq = 0;; ++kq) {
+        mbar_wait(&ifull[kq % NQ], (kq / NQ) & 1);
+        const int w = *(volatile int*)&iq[kq % NQ];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&iempty[kq % NQ]);
+        if (w >= n_items) break;
         const int s = S.item_stream[w];
         const int64_t pos0 = (int64_t)s * D.att_stride + S.item_begin[w];
         const int cnt = S.item_end[w] - S.item_begin[w];
@@ -429,6 +470,10 @@ Plan make_plan(const Dims& D) {
     pl.P.NST = nst > 8 ? 8 : nst;
     pl.P.quant = D.codec == PIKV_CODEC_INT8 || D.codec == PIKV_CODEC_INT4;
     pl.P.scale2 = 1.4426950408889634f / sqrtf((float)D.dph);
+    {
+        const char* st = std::getenv("PIKV_ATT_STATIC");  // A/B experiments only
+        pl.P.dyn = st && st[0] == '1' ? 0 : 1;
+    }
 
 
     pl.smem = 256 + (size_t)pl.P.NST * pl.P.stage_bytes + redb;

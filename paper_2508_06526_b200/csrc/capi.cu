@@ -671,7 +671,7 @@ static int engine_create(const pikv_config* cfg, int32_t cuda_device, int attend
     chk(S.item_stream = eng->alloc<int32_t>(D.item_cap));
     chk(S.item_begin = eng->alloc<int32_t>(D.item_cap));
     chk(S.item_end = eng->alloc<int32_t>(D.item_cap));
-    chk(S.n_items = eng->alloc<int32_t>(1));
+    chk(S.n_items = eng->alloc<int32_t>(2));  // [count, attention's dynamic item ticket]
     chk(S.item_first = eng->alloc<int32_t>(B + 1));
     chk(S.part_m = eng->alloc<float>((size_t)D.item_cap * D.H));
     chk(S.part_l = eng->alloc<float>((size_t)D.item_cap * D.H));
@@ -732,7 +732,7 @@ static int engine_create(const pikv_config* cfg, int32_t cuda_device, int attend
     CUDA_TRY(cudaMemsetAsync(S.pages_before, 0, sizeof(int32_t) * B * std::max(D.Gl, 1), st));
     CUDA_TRY(cudaMemsetAsync(S.pages_after, 0, sizeof(int32_t) * B * std::max(D.Gl, 1), st));
     CUDA_TRY(cudaMemsetAsync(S.summary, 0, sizeof(pikv_step_summary) * B, st));
-    CUDA_TRY(cudaMemsetAsync(S.n_items, 0, sizeof(int32_t), st));
+    CUDA_TRY(cudaMemsetAsync(S.n_items, 0, 2 * sizeof(int32_t), st));
     CUDA_TRY(cudaMemsetAsync(S.item_first, 0, sizeof(int32_t) * (B + 1), st));
     CUDA_TRY(cudaMemsetAsync(S.att_cnt, 0, sizeof(int32_t) * B, st));
     CUDA_TRY(cudaMemsetAsync(S.done_ctr, 0, sizeof(unsigned), st));

@@ -1613,6 +1613,7 @@ __device__ __forceinline__ void build_items(const Dims& D, const Cfg& C, const S
     if (tid == 0) {
         S.item_first[D.B] = (int32_t)carry;
         S.n_items[0] = (int32_t)carry;
+        S.n_items[1] = 0;  // k_attend's item ticket
     }
     __syncthreads();
     for (int s = warp; s < D.B; s += nw) {

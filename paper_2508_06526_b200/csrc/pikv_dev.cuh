@@ -160,7 +160,7 @@ struct State {
     int32_t* item_stream;   // [item_cap]
     int32_t* item_begin;
     int32_t* item_end;
-    int32_t* n_items;       // [1]
+    int32_t* n_items;       // [2]: item count, k_attend's dynamic item ticket
     int32_t* item_first;    // [B+1] first work item of each stream
     float* part_m;          // [item_cap][H]
     float* part_l;
