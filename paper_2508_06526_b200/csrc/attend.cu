@@ -128,6 +128,10 @@ struct DecI4 {
     }
 };
 
+template <class Dec> struct IsQuant { static constexpr bool v = false; };
+template <> struct IsQuant<DecI8> { static constexpr bool v = true; };
+template <> struct IsQuant<DecI4> { static constexpr bool v = true; };
+
 struct AttParams {
     int CPH;          // 16-byte chunks per head (K payload)
     int LPH;          // lanes per head = CPH / CPT
@@ -136,7 +140,6 @@ struct AttParams {
     int EPS;          // entries per stage
     int NST;          // stages
     int stage_bytes;
-    int quant;        // INT8/INT4: per-(entry, head) scales after the payloads
     float scale2;     // log2(e) / sqrt(dph)
     int dyn;          // work items from the global ticket (1) or strided by CTA (0)
 };
@@ -144,7 +147,14 @@ struct AttParams {
 // Thread (sub, head, j) owns chunks j + i*LPH (i < CPT) of one head: the
 // q.k partial is reduced over the head's LPH lanes (xor shuffles), so every
 // lane of the group holds the head's score and its own slice of o.
-template <class Dec, int CPT, int NB>
+__device__ __forceinline__ float ex2(float x) {  // 2^x, x <= 0 (flushes to 0 below 2^-126)
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// LPHC: lanes per head as a compile-time constant (0 = P.LPH at run time)
+template <class Dec, int CPT, int NB, int LPHC>
 __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttParams P) {
     griddep_enter();
     extern __shared__ __align__(128) uint8_t smem[];
@@ -209,7 +219,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
         int kq = 0;
         auto publish = [&](int w) {
             if (lane == 0) {
-                mbar_wait(&iempty[kq % NQ], ((kq / NQ) & 1) ^ 1);
+                mbar_wait_sleep(&iempty[kq % NQ], ((kq / NQ) & 1) ^ 1);
                 *(volatile int*)&iq[kq % NQ] = w;
                 mbar_arrive(&ifull[kq % NQ]);
             }
@@ -241,7 +251,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
                 const int32_t e_nxt = __shfl_sync(0xffffffffu, nxt, o & 31);
                 const int64_t ent = o < 32 ? e_cur : e_nxt;
                 if (lane == 0) {
-                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_wait_sleep(&empty[stage], phase ^ 1);
                     mbar_expect_tx(&full[stage], (uint32_t)(n * eb));
                 }
                 __syncwarp();
@@ -263,15 +273,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
     // ================= consumer warps =================
     const int sub = tid / P.TPE;
     const int r = tid % P.TPE;
-    const int head = r / P.LPH, j = r % P.LPH;
+    const int LPH = LPHC ? LPHC : P.LPH;
+    constexpr bool QUANT = IsQuant<Dec>::v;
+    const int head = r / LPH, j = r % LPH;
     const bool active_sub = sub < P.EP;
     int coff[CPT];  // byte offset of chunk i inside the K (or V) payload
 #pragma unroll
-    for (int i = 0; i < CPT; ++i) coff[i] = (head * P.CPH + j + i * P.LPH) * 16;
+    for (int i = 0; i < CPT; ++i) coff[i] = (head * P.CPH + j + i * LPH) * 16;
     int stage = 0;
     uint32_t phase = 0;
     for (int kq = 0;; ++kq) {
-        mbar_wait(&ifull[kq % NQ], (kq / NQ) & 1);
+        mbar_wait_sleep(&ifull[kq % NQ], (kq / NQ) & 1);
         const int w = *(volatile int*)&iq[kq % NQ];
         __syncwarp();
         if (lane == 0) mbar_arrive(&iempty[kq % NQ]);
@@ -283,7 +295,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
         float m = -INFINITY, l = 0.f;
 #pragma unroll
         for (int i = 0; i < CPT; ++i) {
-            const float* qs = S.q_attn + (int64_t)s * D.dp + head * dph + (j + i * P.LPH) * N;
+            const float* qs = S.q_attn + (int64_t)s * D.dp + head * dph + (j + i * LPH) * N;
 #pragma unroll
             for (int t = 0; t < NP; ++t) {
                 q[i][t] = {qs[2 * t], qs[2 * t + 1]};
@@ -292,8 +304,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
         }
         for (int b = 0; b < cnt; b += P.EPS) {
             const int n = min(P.EPS, cnt - b);
-            mbar_wait(&full[stage], phase);
+            mbar_wait_sleep(&full[stage], phase);
             const uint8_t* sb = stages + (size_t)stage * P.stage_bytes;
+            float* scp = S.scores + (pos0 + b) * H + head;  // this stage's logits, entry e at scp[e * H]
             // warp-uniform trip count (sub-groups of a warp see different entries)
             for (int e0 = 0; e0 < (PIKV_ATTEND_NOMATH ? 0 : n); e0 += P.EP * NB) {
                 float sc[NB];
@@ -313,7 +326,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
                 }
 #pragma unroll
                 for (int off = 16; off; off >>= 1) {
-                    if (off < P.LPH) {
+                    if (off < LPH) {
 #pragma unroll
                         for (int bb = 0; bb < NB; ++bb) sc[bb] += __shfl_xor_sync(0xffffffffu, sc[bb], off);
                     }
@@ -325,13 +338,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
                     const bool valid = active_sub && e < n;
                     const uint8_t* ent = sb + (size_t)(valid ? e : 0) * eb;
                     float x = sc[bb] * P.scale2;
-                    if (P.quant) x *= ((const float*)(ent + 2 * pay))[head];
+                    if (QUANT) x *= ((const float*)(ent + 2 * pay))[head];
                     sc[bb] = valid ? x : -INFINITY;
-                    if (valid && j == 0) S.scores[(pos0 + b + e) * H + head] = x;
+                    if (valid && j == 0) scp[e * H] = x;
                     mx = fmaxf(mx, sc[bb]);
                 }
                 if (mx > m) {  // lazy rescale: only when the running max moves
-                    const float corr = exp2f(m - mx);  // m = -inf -> 0
+                    const float corr = ex2(m - mx);  // m = -inf -> 0
                     l *= corr;
                     const f2 c2 = {corr, corr};
 #pragma unroll
@@ -345,9 +358,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
                     const int e = e0 + sub + bb * P.EP;
                     if (active_sub && e < n) {
                         const uint8_t* ent = sb + (size_t)e * eb;
-                        float pp = exp2f(sc[bb] - m);
+                        float pp = ex2(sc[bb] - m);
                         l += pp;
-                        if (P.quant) pp *= ((const float*)(ent + 2 * pay))[H + head];
+                        if (QUANT) pp *= ((const float*)(ent + 2 * pay))[H + head];
                         const f2 p2 = {pp, pp};
 #pragma unroll
                         for (int i = 0; i < CPT; ++i) {
@@ -367,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
         if (P.EP == 1) {
 #pragma unroll
             for (int i = 0; i < CPT; ++i) {
-                float* po = S.part_o + ((int64_t)w * H + head) * dph + (j + i * P.LPH) * N;
+                float* po = S.part_o + ((int64_t)w * H + head) * dph + (j + i * LPH) * N;
 #pragma unroll
                 for (int t = 0; t < NP; ++t) po[2 * t] = o[i][t].x, po[2 * t + 1] = o[i][t].y;
             }
@@ -383,7 +396,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
             if (active_sub) {
 #pragma unroll
                 for (int i = 0; i < CPT; ++i) {
-                    float* dst = ro + (size_t)sub * H * dph + head * dph + (j + i * P.LPH) * N;
+                    float* dst = ro + (size_t)sub * H * dph + head * dph + (j + i * LPH) * N;
 #pragma unroll
                     for (int t = 0; t < NP; ++t) dst[2 * t] = o[i][t].x, dst[2 * t + 1] = o[i][t].y;
                 }
@@ -408,7 +421,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
                     L += rl[g * H + head] * f;
 #pragma unroll
                     for (int i = 0; i < CPT; ++i) {
-                        const float* src = ro + (size_t)g * H * dph + head * dph + (j + i * P.LPH) * N;
+                        const float* src = ro + (size_t)g * H * dph + head * dph + (j + i * LPH) * N;
 #pragma unroll
                         for (int t = 0; t < NP; ++t) {
                             acc[i][t].x += src[2 * t] * f;
@@ -418,7 +431,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
                 }
 #pragma unroll
                 for (int i = 0; i < CPT; ++i) {
-                    float* po = S.part_o + ((int64_t)w * H + head) * dph + (j + i * P.LPH) * N;
+                    float* po = S.part_o + ((int64_t)w * H + head) * dph + (j + i * LPH) * N;
 #pragma unroll
                     for (int t = 0; t < NP; ++t) po[2 * t] = acc[i][t].x, po[2 * t + 1] = acc[i][t].y;
                 }
@@ -452,6 +465,10 @@ Plan make_plan(const Dims& D) {
     // the 256 consumer threads
     int cpt = pl.P.CPH >= 8 ? pl.P.CPH / 8 : 1;
     while (cpt < 8 && cpt < pl.P.CPH && D.H * (pl.P.CPH / cpt) > kConsumers) cpt *= 2;
+    if (const char* v = std::getenv("PIKV_ATT_CPT")) {  // A/B experiments only
+        const int want = std::atoi(v);
+        if (want >= cpt && want <= 8 && want <= pl.P.CPH && (want & (want - 1)) == 0) cpt = want;
+    }
     pl.cpt = cpt;
     pl.P.LPH = pl.P.CPH / cpt;
     pl.P.TPE = D.H * pl.P.LPH;
@@ -460,15 +477,19 @@ Plan make_plan(const Dims& D) {
     // and small enough that the ring keeps >= 3 stages in flight
     const size_t redb = pl.P.EP > 1 ? sizeof(float) * (size_t)pl.P.EP * D.H * (D.dph + 2) : 0;
     const int ring_max = (int)((kSmemBudget - 256 - redb) / D.entry_bytes);  // entries that fit
+    // a stage holds whole consumer batches (EP sub-groups x NB entries): a
+    // partly filled batch still decodes and dots its K chunks
+    const int nb = D.codec == PIKV_CODEC_INT8 ? 4 : 2;  // BatchOf<Dec>::NB
+    const int batch = std::max(1, pl.P.EP * nb);
     int eps = (32 * 1024) / D.entry_bytes;
-    eps = std::max(eps, std::min(2 * pl.P.EP, 32));
+    eps = std::max(eps, std::min(batch, 32));
+    if (eps % batch && (eps / batch + 1) * batch <= std::max(1, ring_max / 3)) eps = (eps / batch + 1) * batch;
     eps = std::min(eps, std::max(1, ring_max / 3));
     eps = eps < 1 ? 1 : (eps > 32 ? 32 : eps);
     pl.P.EPS = eps;
     pl.P.stage_bytes = eps * D.entry_bytes;
     int nst = (int)((kSmemBudget - 256 - redb) / pl.P.stage_bytes);
     pl.P.NST = nst > 8 ? 8 : nst;
-    pl.P.quant = D.codec == PIKV_CODEC_INT8 || D.codec == PIKV_CODEC_INT4;
     pl.P.scale2 = 1.4426950408889634f / sqrtf((float)D.dph);
     {
         const char* st = std::getenv("PIKV_ATT_STATIC");  // A/B experiments only
@@ -482,22 +503,31 @@ Plan make_plan(const Dims& D) {
 
 template <class Dec> struct BatchOf { static constexpr int NB = 2; };
 template <> struct BatchOf<DecI8> { static constexpr int NB = 4; };  // half/quarter-size entries:
-template <> struct BatchOf<DecI4> { static constexpr int NB = 4; };  // amortize per-entry work
+template <> struct BatchOf<DecI4> { static constexpr int NB = 2; };  // amortize per-entry work (NB 4 spills)
 
-template <class Dec, int CPT>
+template <class Dec, int CPT, int LPHC>
 void launch_t(const Dims& D, const State& S, const Plan& pl, cudaStream_t st) {
-    auto kern = k_attend<Dec, CPT, BatchOf<Dec>::NB>;
+    auto kern = k_attend<Dec, CPT, BatchOf<Dec>::NB, LPHC>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
     launch_pdl(kern, dim3(D.attend_ctas), dim3(kThreads), pl.smem, st, D, S, pl.P);
+}
+
+// lanes per head fixed at compile time for the common layouts (4 or 8 lanes:
+// 128-dim bf16/int8/int4 heads, rank-32 projections), run-time otherwise
+template <class Dec, int CPT>
+void launch_lph(const Dims& D, const State& S, const Plan& pl, cudaStream_t st) {
+    if (pl.P.LPH == 8) launch_t<Dec, CPT, 8>(D, S, pl, st);
+    else if (pl.P.LPH == 4) launch_t<Dec, CPT, 4>(D, S, pl, st);
+    else launch_t<Dec, CPT, 0>(D, S, pl, st);
 }
 
 template <class Dec>
 void launch_dec(const Dims& D, const State& S, const Plan& pl, cudaStream_t st) {
     switch (pl.cpt) {
-        case 1: launch_t<Dec, 1>(D, S, pl, st); break;
-        case 2: launch_t<Dec, 2>(D, S, pl, st); break;
-        case 4: launch_t<Dec, 4>(D, S, pl, st); break;
-        case 8: launch_t<Dec, 8>(D, S, pl, st); break;
+        case 1: launch_lph<Dec, 1>(D, S, pl, st); break;
+        case 2: launch_lph<Dec, 2>(D, S, pl, st); break;
+        case 4: launch_t<Dec, 4, 0>(D, S, pl, st); break;
+        case 8: launch_t<Dec, 8, 0>(D, S, pl, st); break;
         default: break;
     }
 }

@@ -273,6 +273,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
             : "memory");
     }
 }
+// Same wait with a suspend-time hint: the warp sleeps in hardware until the
+// phase completes (or the hint expires) instead of re-issuing try_wait --
+// spinning producer / consumer warps otherwise take issue slots from the
+// warps doing the math on the same SM sub-partition.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity, uint32_t hint_ns = 20000) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(b)), "r"(parity), "r"(hint_ns)
+            : "memory");
+    }
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
                                          uint64_t policy) {
     asm volatile(
