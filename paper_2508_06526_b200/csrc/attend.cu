@@ -314,15 +314,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
                 for (int bb = 0; bb < NB; ++bb) {
                     const int e = e0 + sub + bb * P.EP;
                     const uint8_t* ent = sb + (size_t)((active_sub && e < n) ? e : 0) * eb;
-                    f2 acc = {0.f, 0.f};
+                    // two accumulators: halves the dependent FFMA2 chain (ILP)
+                    f2 acc[2] = {{0.f, 0.f}, {0.f, 0.f}};
 #pragma unroll
                     for (int i = 0; i < CPT; ++i) {
                         f2 kx[NP];
                         Dec::dec(*(const uint4*)(ent + coff[i]), kx);
 #pragma unroll
-                        for (int t = 0; t < NP; ++t) acc = fma2(q[i][t], kx[t], acc);
+                        for (int t = 0; t < NP; ++t) acc[t & 1] = fma2(q[i][t], kx[t], acc[t & 1]);
                     }
-                    sc[bb] = acc.x + acc.y;
+                    const f2 a = add2(acc[0], acc[1]);
+                    sc[bb] = a.x + a.y;
                 }
 #pragma unroll
                 for (int off = 16; off; off >>= 1) {
