@@ -296,8 +296,9 @@ def run_group(args, w, name, cfg, n_micro, local):
     import torch
     from paper_2508_06526_b200.engine import EngineGroup
     attend_sms = args.attend_sms if args.attend_sms is not None else DEFAULT_ATTEND_SMS
-    if attend_sms <= 0:
-        attend_sms = torch.cuda.get_device_properties(local).multi_processor_count - 24
+    if attend_sms <= 0:  # the library default (pikv_group_create, attend_sms = 0)
+        nsm = torch.cuda.get_device_properties(local).multi_processor_count
+        attend_sms = nsm if w["codec"] in ("Int8", "Int4") else nsm - 36
     grp = EngineGroup(cfg, n_micro=n_micro, attend_sms=attend_sms, device=local)
     B, d, dp, Bm = cfg.batch, cfg.model.d, cfg.stored_width, grp.Bm
     if cfg.compressor.scheme in ("LowRank",):
@@ -379,35 +380,42 @@ def run_group(args, w, name, cfg, n_micro, local):
 
     # ---------------- end to end through host buffers ----------------
     elem = 2 if cfg.kv_dtype == "bf16" else 4
-    hq = torch.empty(args.steps, 3, B, d, dtype=tdt).pin_memory()
-    hq.copy_(bank[args.warmup:].cpu())
+    # the caller's pinned inputs, per step and micro-batch q/k/v packed back to back
+    hq = torch.empty(args.steps, n_micro, 3, Bm, d, dtype=tdt).pin_memory()
+    hq.copy_(bank[args.warmup:].view(args.steps, 3, n_micro, Bm, d).transpose(1, 2).cpu())
     hy = torch.empty(B, dp, dtype=torch.float32).pin_memory()
-    ptrs = [[(hq[i, 0, m * Bm].data_ptr(), hq[i, 1, m * Bm].data_ptr(), hq[i, 2, m * Bm].data_ptr())
+    ptrs = [[(hq[i, m, 0].data_ptr(), hq[i, m, 1].data_ptr(), hq[i, m, 2].data_ptr())
              for m in range(n_micro)] for i in range(args.steps)]
     yptr = [hy[m * Bm].data_ptr() for m in range(n_micro)]
     from paper_2508_06526_b200 import _capi
     L = _capi.lib()
     submit, wait, h = L.pikv_group_submit, L.pikv_group_wait, grp.h
-    torch.cuda.synchronize()
-    x0 = torch.cuda.Event(enable_timing=True)
-    x1 = torch.cuda.Event(enable_timing=True)
-    x0.record(streams[0])
-    for i in range(args.steps):
+    def e2e_run():
+        torch.cuda.synchronize()
+        x0 = torch.cuda.Event(enable_timing=True)
+        x1 = torch.cuda.Event(enable_timing=True)
+        x0.record(streams[0])
+        for i in range(args.steps):
+            for m in range(n_micro):
+                if i:
+                    _capi.check(wait(h, m))  # y of micro-batch m's previous step is in host memory
+                pq, pk, pv = ptrs[i][m]
+                _capi.check(submit(h, m, pq, pk, pv, None, yptr[m], 1))
         for m in range(n_micro):
-            if i:
-                _capi.check(wait(h, m))  # y of micro-batch m's previous step is in host memory
-            pq, pk, pv = ptrs[i][m]
-            _capi.check(submit(h, m, pq, pk, pv, None, yptr[m], 1))
-    for m in range(n_micro):
-        _capi.check(wait(h, m))
-    grp.join()
-    x1.record(streams[0])
-    torch.cuda.synchronize()
-    e2e_ms = x0.elapsed_time(x1)
+            _capi.check(wait(h, m))
+        grp.join()
+        x1.record(streams[0])
+        torch.cuda.synchronize()
+        return x0.elapsed_time(x1)
+
+    # the host loop is exposed to host scheduling jitter: median of 3 runs
+    e2e_runs = [e2e_run() for _ in range(3)]
+    e2e_ms = float(np.median(e2e_runs))
     e2e = {"value": B * args.steps / (e2e_ms * 1e-3), "unit": "tokens/s",
            "h2d_bytes_per_step": 3 * B * d * elem, "d2h_bytes_per_step": B * dp * 4,
            "ms_per_step": e2e_ms / args.steps,
-           "api": "pikv_group_submit(host=1) / pikv_group_wait per micro-batch"}
+           "api": "pikv_group_submit(host=1) / pikv_group_wait per micro-batch",
+           "runs_ms": [round(x, 3) for x in e2e_runs], "statistic": "median of 3 runs"}
 
     tokens = B * args.steps
     kv_bytes_step = att_last * entry_bytes
@@ -613,18 +621,25 @@ def main():
         ptrs = [(hq_np[i, 0].ctypes.data, hq_np[i, 1].ctypes.data, hq_np[i, 2].ctypes.data)
                 for i in range(args.steps)]
         fn, h, yp = L.pikv_step_host, eng.h, hy.data_ptr()
-        torch.cuda.synchronize()
-        e0.record(es)
-        for pq, pk, pv in ptrs:
-            rc = fn(h, pq, pk, pv, None, yp)
-            if rc:
-                _capi.check(rc)
-        e1.record(es)
-        torch.cuda.synchronize()
-        e2e_ms = e0.elapsed_time(e1)
+
+        def e2e_run():
+            torch.cuda.synchronize()
+            e0.record(es)
+            for pq, pk, pv in ptrs:
+                rc = fn(h, pq, pk, pv, None, yp)
+                if rc:
+                    _capi.check(rc)
+            e1.record(es)
+            torch.cuda.synchronize()
+            return e0.elapsed_time(e1)
+
+        # a synchronous host loop is exposed to host scheduling jitter: median of 3 runs
+        e2e_runs = [e2e_run() for _ in range(3)]
+        e2e_ms = float(np.median(e2e_runs))
         e2e = {"value": B * args.steps / (e2e_ms * 1e-3), "unit": "tokens/s",
                "h2d_bytes_per_step": 3 * B * d * elem, "d2h_bytes_per_step": B * dp * 4,
-               "ms_per_step": e2e_ms / args.steps}
+               "ms_per_step": e2e_ms / args.steps, "api": "pikv_step_host",
+               "runs_ms": [round(x, 3) for x in e2e_runs], "statistic": "median of 3 runs"}
         del npdt
     else:
         # N ranks: every rank copies its step inputs in from pinned host memory,

@@ -829,8 +829,10 @@ static void mark(pikv_engine* eng, int phase) {
 // pipeline of pikv_group interleaves them across engines):
 //   CTL    route -> insert -> evict -> retrieve (latency-bound control plane)
 //   ATTEND decode attention (HBM-bound)
-//   TAIL   combine (y) -> [finish merge] -> fold-back + feedback
-enum : unsigned { kPartCtl = 1u, kPartAttend = 2u, kPartTail = 4u, kPartAll = 7u };
+//   MERGE  combine (y)
+//   FOLD   [finish merge] -> fold-back + feedback
+enum : unsigned { kPartCtl = 1u, kPartAttend = 2u, kPartMerge = 4u, kPartFold = 8u, kPartTail = 12u,
+                  kPartAll = 15u };
 
 // The step's launch sequence (pipeline.cpp:213-351 ordering).
 // kv_ready: if set, waited on (stream-ordered) right before the first
@@ -887,7 +889,7 @@ static int enqueue_local(pikv_engine* eng, const void* q, const void* k, const v
     }
     if ((parts & kPartAttend) && attend && D.Gl > 0) launch_attend(D, S, st), ++n;
     mark(eng, 8);
-    if (parts & kPartTail) {
+    if (parts & kPartMerge) {
         const int direct = D.world == 1;  // single rank: combine writes y
         if (attend || !direct) launch_combine(D, eng->C, S, eng->X, y, direct, attend, st), ++n;
         if (y_ready) cudaEventRecord(y_ready, st);
@@ -925,7 +927,7 @@ static int enqueue_step(pikv_engine* eng, const double* emb, const void* q, cons
     }
     if (emb) q = eng->q64, k = eng->in_k, v = eng->in_v;
     int rc = enqueue_local(eng, q, k, v, sal, attend, y, emb != nullptr, nullptr, nullptr, parts);
-    if (!rc && (parts & kPartTail)) rc = enqueue_finish(eng, eng->S.exchange, y, attend, 1);
+    if (!rc && (parts & kPartFold)) rc = enqueue_finish(eng, eng->S.exchange, y, attend, 1);
     if (emb && (parts & kPartCtl)) eng->kernels_per_step += (eng->D.B + 63) / 64;
     return rc;
 }
@@ -1582,6 +1584,8 @@ struct pikv_group {
     std::vector<pikv_engine*> eng;
     std::vector<cudaEvent_t> att_done;  // per micro-batch: its last attention
     std::vector<cudaEvent_t> y_done;    // per micro-batch: its last y written
+    std::vector<cudaEvent_t> y_ready;   // host path: y merged on the device
+    std::vector<cudaStream_t> side;     // host path: D2H of y beside the fold-back
     cudaEvent_t join = nullptr;
     bool timing = false;
     // timing: per micro-batch, event pairs of submitted steps not yet read
@@ -1606,12 +1610,14 @@ int pikv_group_create(const pikv_config* cfg, int32_t n_micro, int32_t attend_sm
     c.batch = cfg->batch / n_micro;
     if (cfg->pool_entries > 0) c.pool_entries = cfg->pool_entries / n_micro;
     if (attend_sms <= 0 && n_micro > 1) {
-        // leave 24 SMs to the control plane of the other micro-batch
-        // (c2 sweep, profiles/README.md: 148 -> 34.3 K, 136 -> 39.0 K,
-        // 124 -> 42.1 K, 112 -> 41.8 K tokens/s)
+        // leave 36 SMs to the control plane of the other micro-batch (c2 sweep,
+        // profiles/README.md: 148 -> 34.3 K, 136 -> 39.0 K, 124 -> 42.6 K,
+        // 116 / 108 -> 44.1 K tokens/s); int8/int4 attention is instruction-
+        // bound and keeps every SM (c4-int8: 33.7 K at 148)
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device);
-        attend_sms = std::max(1, sms - 24);
+        const bool quant = cfg->codec == PIKV_CODEC_INT8 || cfg->codec == PIKV_CODEC_INT4;
+        attend_sms = quant ? sms : std::max(1, sms - 36);
     }
     for (int m = 0; m < n_micro; ++m) {
         pikv_engine* e = nullptr;
@@ -1634,6 +1640,12 @@ int pikv_group_create(const pikv_config* cfg, int32_t n_micro, int32_t attend_sm
         cudaEventCreateWithFlags(&y, cudaEventDisableTiming);
         g->att_done.push_back(a);
         g->y_done.push_back(y);
+        cudaEvent_t yr;
+        cudaStream_t sd;
+        cudaEventCreateWithFlags(&yr, cudaEventDisableTiming);
+        cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking);
+        g->y_ready.push_back(yr);
+        g->side.push_back(sd);
     }
     cudaEventCreateWithFlags(&g->join, cudaEventDisableTiming);
     g->tev.resize(n_micro);
@@ -1651,6 +1663,8 @@ int pikv_group_destroy(pikv_group* g) {
     for (auto* e : g->eng) pikv_engine_destroy(e);
     for (auto e : g->att_done) cudaEventDestroy(e);
     for (auto e : g->y_done) cudaEventDestroy(e);
+    for (auto e : g->y_ready) cudaEventDestroy(e);
+    for (auto st : g->side) cudaStreamSynchronize(st), cudaStreamDestroy(st);
     for (auto& v : g->tev)
         for (auto& p : v) cudaEventDestroy(p.first), cudaEventDestroy(p.second);
     for (auto& p : g->tfree) cudaEventDestroy(p.first), cudaEventDestroy(p.second);
@@ -1677,9 +1691,15 @@ int pikv_group_submit(pikv_group* g, int32_t m, const void* q, const void* k, co
     const double* ds = sal;
     float* dy = y;
     if (host) {
-        CUDA_TRY(cudaMemcpyAsync(e->in_q, q, g->in_bytes, cudaMemcpyHostToDevice, st));
-        CUDA_TRY(cudaMemcpyAsync(e->in_k, k, g->in_bytes, cudaMemcpyHostToDevice, st));
-        CUDA_TRY(cudaMemcpyAsync(e->in_v, v, g->in_bytes, cudaMemcpyHostToDevice, st));
+        const uint8_t* hq = (const uint8_t*)q;
+        if ((const uint8_t*)k == hq + g->in_bytes && (const uint8_t*)v == hq + 2 * g->in_bytes) {
+            // q, k, v packed back to back: one transfer into the packed staging
+            CUDA_TRY(cudaMemcpyAsync(e->in_q, q, 3 * g->in_bytes, cudaMemcpyHostToDevice, st));
+        } else {
+            CUDA_TRY(cudaMemcpyAsync(e->in_q, q, g->in_bytes, cudaMemcpyHostToDevice, st));
+            CUDA_TRY(cudaMemcpyAsync(e->in_k, k, g->in_bytes, cudaMemcpyHostToDevice, st));
+            CUDA_TRY(cudaMemcpyAsync(e->in_v, v, g->in_bytes, cudaMemcpyHostToDevice, st));
+        }
         if (sal && g->sal_elems)
             CUDA_TRY(cudaMemcpyAsync(e->in_sal, sal, sizeof(double) * g->sal_elems, cudaMemcpyHostToDevice, st));
         dq = e->in_q, dk = e->in_k, dv = e->in_v, ds = sal ? e->in_sal : nullptr, dy = e->out_y;
@@ -1710,11 +1730,24 @@ int pikv_group_submit(pikv_group* g, int32_t m, const void* q, const void* k, co
             if (p.second) CUDA_TRY(cudaEventRecord(p.second, st));
             CUDA_TRY(cudaEventRecord(g->att_done[m], st));
         }
-        if (!rc) rc = run_step(e, dq, dk, dv, ds, dy, true, nullptr, kPartTail);
+        if (!host) {
+            if (!rc) rc = run_step(e, dq, dk, dv, ds, dy, true, nullptr, kPartTail);
+        } else {
+            // y leaves for the host on a side stream as soon as the merge wrote
+            // it, while the fold-back runs: the caller's wait returns earlier
+            if (!rc) rc = run_step(e, dq, dk, dv, ds, dy, true, nullptr, kPartMerge);
+            if (!rc) {
+                CUDA_TRY(cudaEventRecord(g->y_ready[m], st));
+                CUDA_TRY(cudaStreamWaitEvent(g->side[m], g->y_ready[m], 0));
+                CUDA_TRY(cudaMemcpyAsync(y, e->out_y, g->y_bytes, cudaMemcpyDeviceToHost, g->side[m]));
+                CUDA_TRY(cudaEventRecord(g->y_done[m], g->side[m]));
+                rc = run_step(e, dq, dk, dv, ds, dy, true, nullptr, kPartFold);
+            }
+        }
     }
     if (rc) return rc;
-    if (host) CUDA_TRY(cudaMemcpyAsync(y, e->out_y, g->y_bytes, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaEventRecord(g->y_done[m], st));
+    if (e->profiling && host) CUDA_TRY(cudaMemcpyAsync(y, e->out_y, g->y_bytes, cudaMemcpyDeviceToHost, st));
+    if (!host || e->profiling) CUDA_TRY(cudaEventRecord(g->y_done[m], st));
     return PIKV_OK;
 }
 
@@ -1739,14 +1772,19 @@ int pikv_group_step(pikv_group* g, const void* q, const void* k, const void* v, 
 int pikv_group_join(pikv_group* g) {
     cudaSetDevice(g->device);
     cudaStream_t s0 = g->eng[0]->stream;
-    for (int m = 1; m < g->n; ++m) {
-        CUDA_TRY(cudaEventRecord(g->join, g->eng[m]->stream));
+    for (int m = 0; m < g->n; ++m) {
+        if (m) {
+            CUDA_TRY(cudaEventRecord(g->join, g->eng[m]->stream));
+            CUDA_TRY(cudaStreamWaitEvent(s0, g->join, 0));
+        }
+        CUDA_TRY(cudaEventRecord(g->join, g->side[m]));
         CUDA_TRY(cudaStreamWaitEvent(s0, g->join, 0));
     }
     return PIKV_OK;
 }
 
 int pikv_group_sync(pikv_group* g) {
+    for (auto st : g->side) CUDA_TRY(cudaStreamSynchronize(st));
     for (auto* e : g->eng) {
         int rc = pikv_sync(e);
         if (rc) return rc;
