@@ -31,6 +31,9 @@
 #ifndef PIKV_ATTEND_NOHINT
 #define PIKV_ATTEND_NOHINT 0  // experiment builds only: TMA without the L2 evict-first hint
 #endif
+#ifndef PIKV_ATTEND_I8DOT
+#define PIKV_ATTEND_I8DOT 1  // int8 q.k as IDP4A digit planes (0: decode + FFMA2, A/B builds)
+#endif
 #ifndef PIKV_ATTEND_NOMATH
 #define PIKV_ATTEND_NOMATH 0  // experiment builds only: consumers skip the math
 #endif
@@ -275,6 +278,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
     const int r = tid % P.TPE;
     const int LPH = LPHC ? LPHC : P.LPH;
     constexpr bool QUANT = IsQuant<Dec>::v;
+    constexpr bool I8DOT = QUANT && Dec::N == 16 && PIKV_ATTEND_I8DOT;  // int8: integer q.k
     const int head = r / LPH, j = r % LPH;
     const bool active_sub = sub < P.EP;
     int coff[CPT];  // byte offset of chunk i inside the K (or V) payload
@@ -302,6 +306,46 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
                 o[i][t] = {0.f, 0.f};
             }
         }
+        // int8 K: q as three signed base-256 digit planes of a 23-bit fixed-point
+        // q (scale 2^(22 - e), e = exponent of the head's max |q|), so q.k is
+        // three exact integer dot products (IDP4A on the raw codes, no decode):
+        // q.k = (S0 + 256 S1 + 65536 S2) * 2^(e - 22) up to the rounding of q to
+        // 23 bits relative to the head's max (~1e-7 relative on the logit)
+        int qd[I8DOT ? CPT : 1][4][3];
+        float qinv = 1.f;
+        if constexpr (I8DOT) {
+            float mx = 0.f;
+#pragma unroll
+            for (int i = 0; i < CPT; ++i)
+#pragma unroll
+                for (int t = 0; t < NP; ++t) mx = fmaxf(mx, fmaxf(fabsf(q[i][t].x), fabsf(q[i][t].y)));
+#pragma unroll
+            for (int off = 16; off; off >>= 1)
+                if (off < LPH) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+            int ex = 0;
+            if (mx > 0.f) frexpf(mx, &ex);
+            const float qs_ = ldexpf(1.f, 22 - ex);
+            qinv = ldexpf(1.f, ex - 22);
+#pragma unroll
+            for (int i = 0; i < CPT; ++i)
+#pragma unroll
+                for (int wd = 0; wd < 4; ++wd) {
+                    uint32_t pk[3] = {0u, 0u, 0u};
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        const f2 qq = q[i][2 * wd + (b >> 1)];
+                        const int v = __float2int_rn((b & 1 ? qq.y : qq.x) * qs_);
+                        const int d0 = ((v + 128) & 255) - 128;
+                        const int r1 = (v - d0) >> 8;
+                        const int d1 = ((r1 + 128) & 255) - 128;
+                        const int d2 = (r1 - d1) >> 8;
+                        pk[0] |= (uint32_t)(d0 & 255) << (8 * b);
+                        pk[1] |= (uint32_t)(d1 & 255) << (8 * b);
+                        pk[2] |= (uint32_t)(d2 & 255) << (8 * b);
+                    }
+                    qd[i][wd][0] = (int)pk[0], qd[i][wd][1] = (int)pk[1], qd[i][wd][2] = (int)pk[2];
+                }
+        }
         for (int b = 0; b < cnt; b += P.EPS) {
             const int n = min(P.EPS, cnt - b);
             mbar_wait_sleep(&full[stage], phase);
@@ -314,17 +358,33 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
                 for (int bb = 0; bb < NB; ++bb) {
                     const int e = e0 + sub + bb * P.EP;
                     const uint8_t* ent = sb + (size_t)((active_sub && e < n) ? e : 0) * eb;
-                    // two accumulators: halves the dependent FFMA2 chain (ILP)
-                    f2 acc[2] = {{0.f, 0.f}, {0.f, 0.f}};
+                    if constexpr (I8DOT) {
+                        int d0 = 0, d1 = 0, d2 = 0;
 #pragma unroll
-                    for (int i = 0; i < CPT; ++i) {
-                        f2 kx[NP];
-                        Dec::dec(*(const uint4*)(ent + coff[i]), kx);
+                        for (int i = 0; i < CPT; ++i) {
+                            const uint4 kw = *(const uint4*)(ent + coff[i]);
+                            const int kk[4] = {(int)kw.x, (int)kw.y, (int)kw.z, (int)kw.w};
 #pragma unroll
-                        for (int t = 0; t < NP; ++t) acc[t & 1] = fma2(q[i][t], kx[t], acc[t & 1]);
+                            for (int wd = 0; wd < 4; ++wd) {
+                                d0 = __dp4a(kk[wd], qd[i][wd][0], d0);
+                                d1 = __dp4a(kk[wd], qd[i][wd][1], d1);
+                                d2 = __dp4a(kk[wd], qd[i][wd][2], d2);
+                            }
+                        }
+                        sc[bb] = fmaf((float)d2, 65536.f, fmaf((float)d1, 256.f, (float)d0)) * qinv;
+                    } else {
+                        // two accumulators: halves the dependent FFMA2 chain (ILP)
+                        f2 acc[2] = {{0.f, 0.f}, {0.f, 0.f}};
+#pragma unroll
+                        for (int i = 0; i < CPT; ++i) {
+                            f2 kx[NP];
+                            Dec::dec(*(const uint4*)(ent + coff[i]), kx);
+#pragma unroll
+                            for (int t = 0; t < NP; ++t) acc[t & 1] = fma2(q[i][t], kx[t], acc[t & 1]);
+                        }
+                        const f2 a = add2(acc[0], acc[1]);
+                        sc[bb] = a.x + a.y;
                     }
-                    const f2 a = add2(acc[0], acc[1]);
-                    sc[bb] = a.x + a.y;
                 }
 #pragma unroll
                 for (int off = 16; off; off >>= 1) {

@@ -252,6 +252,18 @@ def test_engine_c2_shape_parity(monkeypatch, control):
     run_parity(cfg, 120, 17, inject=False)
 
 
+@pytest.mark.parametrize("codec", ["Int8", "Int4"])
+def test_engine_c4_quant_shape_parity(codec):
+    """BASELINE configs[3] head shape for int8/int4 KV (32 heads x 128, bf16
+    inputs, E16 top-2, pure expert sharding): the int8 q.k runs as IDP4A digit
+    planes, int4 through the nibble decoder; codes bit-exact, y within 2e-5."""
+    cfg = engine_config(router="TopK", sched="LRU", d=4096, H=32, E=16, k=2, G=1, n_tok=1,
+                        n_exp=16, S=64, ps=16, budget=6, batch=2, dtype="bf16", n_layers=0,
+                        codec=codec)
+    cfg.model.head_width = 128
+    run_parity(cfg, 60, 23, inject=False)
+
+
 def test_engine_full_context_invariants():
     """c2 at full context (32K-token synthetic prefill, B = 4): no device
     error, live entries follow the page budget, every stream attends exactly
