@@ -279,6 +279,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
     const int LPH = LPHC ? LPHC : P.LPH;
     constexpr bool QUANT = IsQuant<Dec>::v;
     constexpr bool I8DOT = QUANT && Dec::N == 16 && PIKV_ATTEND_I8DOT;  // int8: integer q.k
+    constexpr bool I4DOT = QUANT && Dec::N == 32 && PIKV_ATTEND_I8DOT;  // int4: integer q.k
     const int head = r / LPH, j = r % LPH;
     const bool active_sub = sub < P.EP;
     int coff[CPT];  // byte offset of chunk i inside the K (or V) payload
@@ -313,6 +314,48 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
         // 23 bits relative to the head's max (~1e-7 relative on the logit)
         int qd[I8DOT ? CPT : 1][4][3];
         float qinv = 1.f;
+        // int4 K: the same digit planes, split into even / odd elements (the
+        // two nibbles of a code byte); codes are biased to 0..15 (xor 8) so a
+        // byte is a non-negative int8, and 8 * sum(digits) is subtracted
+        int qe[I4DOT ? CPT : 1][4][2][3];
+        int corr[3] = {0, 0, 0};
+        if constexpr (I4DOT) {
+            float mx = 0.f;
+#pragma unroll
+            for (int i = 0; i < CPT; ++i)
+#pragma unroll
+                for (int t = 0; t < NP; ++t) mx = fmaxf(mx, fmaxf(fabsf(q[i][t].x), fabsf(q[i][t].y)));
+#pragma unroll
+            for (int off = 16; off; off >>= 1)
+                if (off < LPH) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+            int ex = 0;
+            if (mx > 0.f) frexpf(mx, &ex);
+            const float qs_ = ldexpf(1.f, 22 - ex);
+            qinv = ldexpf(1.f, ex - 22);
+#pragma unroll
+            for (int i = 0; i < CPT; ++i)
+#pragma unroll
+                for (int wd = 0; wd < 4; ++wd)
+#pragma unroll
+                    for (int h2 = 0; h2 < 2; ++h2) {
+                        uint32_t pk[3] = {0u, 0u, 0u};
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) {
+                            const f2 qq = q[i][4 * wd + b];
+                            const int v = __float2int_rn((h2 ? qq.y : qq.x) * qs_);
+                            const int d0 = ((v + 128) & 255) - 128;
+                            const int r1 = (v - d0) >> 8;
+                            const int d1 = ((r1 + 128) & 255) - 128;
+                            const int d2 = (r1 - d1) >> 8;
+                            corr[0] += d0, corr[1] += d1, corr[2] += d2;
+                            pk[0] |= (uint32_t)(d0 & 255) << (8 * b);
+                            pk[1] |= (uint32_t)(d1 & 255) << (8 * b);
+                            pk[2] |= (uint32_t)(d2 & 255) << (8 * b);
+                        }
+                        qe[i][wd][h2][0] = (int)pk[0], qe[i][wd][h2][1] = (int)pk[1], qe[i][wd][h2][2] = (int)pk[2];
+                    }
+            corr[0] *= -8, corr[1] *= -8, corr[2] *= -8;
+        }
         if constexpr (I8DOT) {
             float mx = 0.f;
 #pragma unroll
@@ -369,6 +412,25 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
                                 d0 = __dp4a(kk[wd], qd[i][wd][0], d0);
                                 d1 = __dp4a(kk[wd], qd[i][wd][1], d1);
                                 d2 = __dp4a(kk[wd], qd[i][wd][2], d2);
+                            }
+                        }
+                        sc[bb] = fmaf((float)d2, 65536.f, fmaf((float)d1, 256.f, (float)d0)) * qinv;
+                    } else if constexpr (I4DOT) {
+                        int d0 = corr[0], d1 = corr[1], d2 = corr[2];
+#pragma unroll
+                        for (int i = 0; i < CPT; ++i) {
+                            const uint4 kw = *(const uint4*)(ent + coff[i]);
+                            const uint32_t kk[4] = {kw.x ^ 0x88888888u, kw.y ^ 0x88888888u, kw.z ^ 0x88888888u,
+                                                    kw.w ^ 0x88888888u};
+#pragma unroll
+                            for (int wd = 0; wd < 4; ++wd) {
+                                const int lo = (int)(kk[wd] & 0x0F0F0F0Fu), hi = (int)((kk[wd] >> 4) & 0x0F0F0F0Fu);
+                                d0 = __dp4a(lo, qe[i][wd][0][0], d0);
+                                d1 = __dp4a(lo, qe[i][wd][0][1], d1);
+                                d2 = __dp4a(lo, qe[i][wd][0][2], d2);
+                                d0 = __dp4a(hi, qe[i][wd][1][0], d0);
+                                d1 = __dp4a(hi, qe[i][wd][1][1], d1);
+                                d2 = __dp4a(hi, qe[i][wd][1][2], d2);
                             }
                         }
                         sc[bb] = fmaf((float)d2, 65536.f, fmaf((float)d1, 256.f, (float)d0)) * qinv;
@@ -541,7 +603,7 @@ Plan make_plan(const Dims& D) {
     const int ring_max = (int)((kSmemBudget - 256 - redb) / D.entry_bytes);  // entries that fit
     // a stage holds whole consumer batches (EP sub-groups x NB entries): a
     // partly filled batch still decodes and dots its K chunks
-    const int nb = D.codec == PIKV_CODEC_INT8 ? 4 : 2;  // BatchOf<Dec>::NB
+    const int nb = (D.codec == PIKV_CODEC_INT8 || D.codec == PIKV_CODEC_INT4) ? 4 : 2;  // BatchOf<Dec>::NB
     const int batch = std::max(1, pl.P.EP * nb);
     int eps = (32 * 1024) / D.entry_bytes;
     eps = std::max(eps, std::min(batch, 32));
@@ -565,7 +627,7 @@ Plan make_plan(const Dims& D) {
 
 template <class Dec> struct BatchOf { static constexpr int NB = 2; };
 template <> struct BatchOf<DecI8> { static constexpr int NB = 4; };  // half/quarter-size entries:
-template <> struct BatchOf<DecI4> { static constexpr int NB = 2; };  // amortize per-entry work (NB 4 spills)
+template <> struct BatchOf<DecI4> { static constexpr int NB = 4; };  // amortize per-entry work
 
 template <class Dec, int CPT, int LPHC>
 void launch_t(const Dims& D, const State& S, const Plan& pl, cudaStream_t st) {
