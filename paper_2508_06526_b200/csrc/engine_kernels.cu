@@ -461,13 +461,15 @@ __device__ __forceinline__ float load_in(const void* p, int dtype, int64_t i) {
 __global__ void k_project(Dims D, State S, const void* __restrict__ qin, const void* __restrict__ kin,
                           const void* __restrict__ vin) {
     griddep_enter();
-    extern __shared__ float sm_p[];  // basis [r][hd] then x [B][hd]
+    extern __shared__ float sm_p[];  // basis [r][hd + 1] then x [B][hd]
     const int h = blockIdx.x, row = blockIdx.y;
     const int hd = D.d / D.H, r = D.dph, tid = threadIdx.x, nt = blockDim.x;
+    const int hdp = hd + 1;  // padded basis rows: lanes j = 0..31 read column i of 32 rows
+                             // from 32 different banks (unpadded: one bank, 32-way conflict)
     const void* x = row == 0 ? qin : (row == 1 ? kin : vin);
     float* bs = sm_p;
-    float* xs = sm_p + (size_t)r * hd;
-    for (int t = tid; t < r * hd; t += nt) bs[t] = S.basis[(int64_t)h * r * hd + t];
+    float* xs = sm_p + (size_t)r * hdp;
+    for (int t = tid; t < r * hd; t += nt) bs[(t / hd) * hdp + t % hd] = S.basis[(int64_t)h * r * hd + t];
     for (int t = tid; t < D.B * hd; t += nt) {
         const int b = t / hd, i = t % hd;
         float xi = (row == 0 && D.q_f64) ? (float)((const double*)x)[(int64_t)b * D.d + h * hd + i]
@@ -478,7 +480,7 @@ __global__ void k_project(Dims D, State S, const void* __restrict__ qin, const v
     __syncthreads();
     for (int t = tid; t < D.B * r; t += nt) {
         const int b = t / r, j = t % r;
-        const float* col = bs + (size_t)j * hd;
+        const float* col = bs + (size_t)j * hdp;
         const float* xb = xs + (size_t)b * hd;
         float acc = 0.f;
 #pragma unroll 8
@@ -491,7 +493,7 @@ __global__ void k_project(Dims D, State S, const void* __restrict__ qin, const v
 void launch_project(const Dims& D, const State& S, const void* q, const void* k, const void* v,
                     cudaStream_t st) {
     const int hd = D.d / D.H;
-    const size_t smem = sizeof(float) * ((size_t)D.dph * hd + (size_t)D.B * hd);
+    const size_t smem = sizeof(float) * ((size_t)D.dph * (hd + 1) + (size_t)D.B * hd);
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_project, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     launch_pdl(k_project, dim3(D.H, 3), dim3(256), smem, st, D, S, q, k, v);
 }

@@ -65,3 +65,28 @@ def test_shard_assign_host_validation_without_gpu():
     rc = L.pikv_shard_assign_host(ctypes.byref(t), ctypes.byref(e), 1, 3, 4, 2, 0,
                                   ctypes.byref(d), None, None)
     assert rc == 2  # kvstore.cpp:17-19
+
+
+def group_rc(cfg, n_micro):
+    c = cfg.to_c()
+    h = ctypes.c_void_p()
+    rc = L.pikv_group_create(ctypes.byref(c), n_micro, 0, 0, ctypes.byref(h))
+    if rc == 0:
+        L.pikv_group_destroy(h)
+    return rc
+
+
+@pytest.mark.parametrize("batch,n_micro,world", [(3, 2, 1), (4, 0, 1), (4, 3, 1), (4, 2, 2)])
+def test_group_rejects_bad_split_before_cuda(batch, n_micro, world):
+    """pikv_group_create: the batch must split evenly into n_micro >= 1
+    micro-batches of a single-rank engine -> InvalidConfig, checked before
+    any CUDA call (include/pikv_b200.h, micro-batch pipeline)."""
+    cfg = engine_config(batch=batch)
+    cfg.world_size = world
+    assert _capi.ERRORS[group_rc(cfg, n_micro)] == "InvalidConfig"
+
+
+def test_group_rejects_invalid_engine_config():
+    cfg = mutate(model__d=0)
+    cfg.batch = 2
+    assert _capi.ERRORS[group_rc(cfg, 2)] == "InvalidConfig"
