@@ -18,9 +18,12 @@
 // with tcgen05.ld.  fp32 operands are split into bf16 hi + lo, and the
 // products hi*hi + hi*lo (+ lo*hi for fp32 inputs) keep ~2^-16 relative
 // accuracy, i.e. fp32-level agreement with the CUDA-core projection.
+#include <cuda.h>  // CUtensorMap (encoded through the runtime's driver entry point; no -lcuda)
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+
+#include <algorithm>
 
 #include "pikv_dev.cuh"
 
@@ -373,11 +376,198 @@ __global__ void __launch_bounds__(128) k_bulk_project_tc2(Dims D, int64_t T, con
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(2 * NACC));
 }
 
+// ---- TMA-fed variant ----------------------------------------------------
+// A tiles arrive by TMA (cp.async.bulk.tensor.2d, one elected thread) into a
+// 2-stage ring in the SWIZZLE_128B K-major layout the UMMA descriptor reads
+// directly (two 128-row x 64-column boxes per 128 x 128 tile, rows beyond T
+// zero-filled by the TMA unit), so no thread touches the A bytes; B (basis
+// hi / lo) stays in the SWIZZLE_NONE canonical layout (k_basis_split).  The
+// MMA of tile i+1 and the TMA of tile i+2 run while the warps drain tile i's
+// accumulator.  Persistent CTA per (head, K|V) slice of the tiles.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t start) {
+    // start >> 4, LBO (unused for swizzled K-major) = 1, SBO = 1024 B (8 rows
+    // x 128 B), version 1, layout SWIZZLE_128B (2) at bits [61, 64)
+    return (uint64_t)((start >> 4) & 0x3FFF) | (1ull << 16) | ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) |
+           (2ull << 61);
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+            smem_u32(dst)),
+        "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <int NP>
+__global__ void __launch_bounds__(128) k_bulk_project_tc3(const __grid_constant__ CUtensorMap map_k,
+                                                          const __grid_constant__ CUtensorMap map_v, Dims D,
+                                                          int64_t T, const uint16_t* __restrict__ bhl,
+                                                          float* __restrict__ proj,
+                                                          const float* __restrict__ bias_proj) {
+    extern __shared__ __align__(1024) uint8_t sm3[];
+    constexpr int HD = 128, KC = 16;
+    constexpr uint32_t A_BYTES = (uint32_t)kTcM * HD * 2, B_BYTES = (uint32_t)NP * HD * 2;
+    constexpr int NACC = NP < 32 ? 32 : NP;
+    const int r = D.dph;
+    const int h = blockIdx.y, row = blockIdx.z, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // 1024-byte aligned stages (SWIZZLE_128B atoms)
+    uint8_t* base = (uint8_t*)(((uintptr_t)sm3 + 1023) & ~(uintptr_t)1023);
+    uint8_t* a_st[2] = {base, base + A_BYTES};
+    uint8_t* b_hl = base + 2 * A_BYTES;
+    uint64_t* full = (uint64_t*)(b_hl + 2 * B_BYTES);  // [2] TMA landed
+    uint64_t* done = full + 2;                         // [2] MMAs of the stage finished
+    uint32_t* tmem_slot = (uint32_t*)(done + 2);
+    float* tr = (float*)(tmem_slot + 4) + warp * 32 * (NP + 1);
+    const CUtensorMap* map = row == 0 ? &map_k : &map_v;
+    const int64_t ntiles = (T + kTcM - 1) / kTcM;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                     "n"(2 * NACC));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    if (tid == 0) {
+        for (int i = 0; i < 2; ++i) mbar_init(&full[i], 1), mbar_init(&done[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)map) : "memory");
+    }
+    {
+        const uint4* src = (const uint4*)(bhl + (int64_t)h * 2 * NP * HD);
+        for (int i = tid; i < (int)(2 * B_BYTES / 16); i += blockDim.x) ((uint4*)b_hl)[i] = src[i];
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t idesc = umma_idesc_bf16(NP);
+    auto issue_load = [&](int stg, int64_t tile) {  // thread 0
+        mbar_expect_tx(&full[stg], A_BYTES);
+        tma_load_2d(a_st[stg], map, h * HD, (int)(tile * kTcM), &full[stg]);
+        tma_load_2d(a_st[stg] + A_BYTES / 2, map, h * HD + 64, (int)(tile * kTcM), &full[stg]);
+    };
+    auto drain = [&](int pb, int64_t tile) {
+        float accv[NP];
+        tmem_ld_rows<NP>(tmem + (uint32_t)(pb * NACC) + ((uint32_t)(warp * 32) << 16), accv);
+#pragma unroll
+        for (int j = 0; j < NP; ++j) tr[lane * (NP + 1) + j] = accv[j];
+        __syncwarp();
+        for (int c = lane; c < r; c += 32) {
+            const float bj = bias_proj ? bias_proj[h * r + c] : 0.f;
+            for (int rr = 0; rr < 32; ++rr) {
+                const int64_t g = tile * kTcM + warp * 32 + rr;
+                if (g < T) proj[((int64_t)row * T + g) * D.dp + h * r + c] = tr[rr * (NP + 1) + c] - bj;
+            }
+        }
+        __syncwarp();
+    };
+    const int64_t t0 = blockIdx.x, step = gridDim.x;
+    if (tid == 0) {
+        if (t0 < ntiles) issue_load(0, t0);
+        if (t0 + step < ntiles) issue_load(1, t0 + step);
+    }
+    int it = 0;
+    int64_t prev = -1;
+    for (int64_t t = t0; t < ntiles; t += step, ++it) {
+        const int stg = it & 1;
+        if (tid == 0) {
+            mbar_wait(&full[stg], (uint32_t)((it >> 1) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t A = smem_u32(a_st[stg]), Bh = smem_u32(b_hl), Bl = Bh + B_BYTES;
+            const uint32_t acc = tmem + (uint32_t)(stg * NACC);
+            // K = 128 = two 64-column swizzle atoms (A + kb * 16 KB), 4 MMAs of
+            // K = 16 (32 B) each; B canonical: 256 B per K = 16 step
+#pragma unroll
+            for (int hl = 0; hl < 2; ++hl)
+#pragma unroll
+                for (int ks = 0; ks < KC / 2; ++ks) {
+                    const uint32_t a_addr = A + (uint32_t)(ks >> 2) * (A_BYTES / 2) + (uint32_t)(ks & 3) * 32;
+                    umma_bf16(acc, umma_desc_sw128(a_addr), umma_desc((hl ? Bl : Bh) + ks * 256, 128, KC * 128),
+                              idesc, (hl | ks) != 0);
+                }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.b64 [%0];\n" ::"l"(
+                             (uint64_t)__cvta_generic_to_shared(&done[stg]))
+                         : "memory");
+        }
+        if (prev >= 0) {
+            const int pb = stg ^ 1;
+            mbar_wait(&done[pb], (uint32_t)(((it - 1) >> 1) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            // stage pb is free (its MMAs finished): refill it with tile t + step
+            if (tid == 0 && t + step < ntiles) issue_load(pb, t + step);
+            drain(pb, prev);
+        }
+        prev = t;
+    }
+    if (prev >= 0) {
+        const int pb = (it - 1) & 1;
+        mbar_wait(&done[pb], (uint32_t)(((it - 1) >> 1) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        drain(pb, prev);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(2 * NACC));
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled_fn() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return (EncodeTiledFn)p;
+    }();
+    return fn;
+}
+
+// [T][d] bf16 rows, boxes of 128 rows x 64 columns (128 B), SWIZZLE_128B
+bool make_kv_map(CUtensorMap* m, const void* x, int64_t T, int d) {
+    EncodeTiledFn fn = encode_tiled_fn();
+    if (!fn || ((uintptr_t)x & 15) || (d * 2) % 16) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)T};
+    const cuuint64_t strides[1] = {(cuuint64_t)d * 2};
+    const cuuint32_t box[2] = {64, (cuuint32_t)kTcM};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int NP>
 int launch_np(const Dims& D, const State& S, int64_t T, const void* k, const void* v, float* proj,
               const float* bias_proj, float* scratch_b, cudaStream_t st) {
     const int hd = D.d / D.H;
     const bool f32in = D.kv_dtype != PIKV_DTYPE_BF16;
+    const char* tv = std::getenv("PIKV_BULK_TMA");  // A/B: 0 = register-staged tc2
+    CUtensorMap mk, mv;
+    if (!f32in && hd == 128 && scratch_b && !(tv && tv[0] == '0') && make_kv_map(&mk, k, T, D.d) &&
+        make_kv_map(&mv, v, T, D.d)) {
+        uint16_t* bhl = (uint16_t*)scratch_b;
+        k_basis_split<NP><<<64, 256, 0, st>>>(D, S, bhl);
+        const size_t smem = 1024 + 2 * (size_t)kTcM * 128 * 2 + 2 * (size_t)NP * 128 * 2 + 64 +
+                            sizeof(float) * 4 * 32 * (NP + 1);
+        cudaFuncSetAttribute(k_bulk_project_tc3<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const int64_t ntiles = (T + kTcM - 1) / kTcM;
+        int sms = 148, smem_sm = 228 * 1024;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+        cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, 0);
+        const int occ = std::max(1, std::min(4, smem_sm / (int)(smem + 1024)));  // CTAs per SM by shared memory
+        // one wave: (head, K|V) pairs x slices <= resident CTAs
+        int64_t per = (int64_t)occ * sms / (2LL * D.H);
+        if (per > ntiles) per = ntiles;
+        if (per < 1) per = 1;
+        k_bulk_project_tc3<NP><<<dim3((unsigned)per, D.H, 2), 128, smem, st>>>(mk, mv, D, T, bhl, proj, bias_proj);
+        return cudaGetLastError() == cudaSuccess ? 0 : 1;
+    }
     if (!f32in && hd == 128 && scratch_b) {  // pipelined persistent kernel
         uint16_t* bhl = (uint16_t*)scratch_b;
         k_basis_split<NP><<<64, 256, 0, st>>>(D, S, bhl);

@@ -149,3 +149,31 @@ def test_bulk_projection_tensor_cores_match_cuda_cores(monkeypatch, codec, dtype
     assert np.array_equal(sa["id"], sb["id"]) and np.array_equal(sa["token"], sb["token"])
     tol = 2e-3 if dtype == "bf16" else 1e-5
     assert rel_l2(ya.astype(np.float64), yb.astype(np.float64)) <= tol
+
+
+@pytest.mark.parametrize("d,H,rank,T", [(256, 2, 32, 300), (4096, 32, 32, 2000), (4096, 32, 16, 700)])
+def test_bulk_projection_tma_matches_register_staged(monkeypatch, d, H, rank, T):
+    """The TMA-fed tcgen05 projection (A tiles by cp.async.bulk.tensor into
+    SWIZZLE_128B stages) issues the same MMAs in the same order as the
+    register-staged kernel (PIKV_BULK_TMA=0), so decode over the bulk-built
+    store is bit-identical; d = 32 x 128 gives every CTA several tiles (the
+    persistent loop, both ring stages) and a partial last tile."""
+    rng = np.random.default_rng(11)
+    outs = []
+    for tma in ("1", "0"):
+        monkeypatch.setenv("PIKV_BULK_TC", "2")
+        monkeypatch.setenv("PIKV_BULK_TMA", tma)
+        cfg = engine_config(router="TopK", sched="LRU", unbounded=True, d=d, H=H, S=4096, batch=1,
+                            codec="LowRank", rank=rank, dtype="bf16", n_layers=0)
+        basis, _, _ = codec_params("LowRank", d, H, rank, np.random.default_rng(3))
+        eng = Engine(cfg)
+        eng.set_codec(basis, None, None)
+        st = make_stream(T + 3, d, 31, "bf16", 0)
+        ex = np.stack([rng.choice(cfg.model.E, cfg.router.k, replace=False) for _ in range(T)]).astype(np.int32)
+        eng.insert_bulk_host(0, to_kv(st[1][:T], "bf16"), to_kv(st[2][:T], "bf16"), ex)
+        ys = [eng.step_host(to_kv(st[0][T + i:T + i + 1], "bf16"), to_kv(st[1][T + i:T + i + 1], "bf16"),
+                            to_kv(st[2][T + i:T + i + 1], "bf16")) for i in range(3)]
+        outs.append(np.concatenate(ys))
+        eng.close()
+        rng = np.random.default_rng(11)
+    assert np.array_equal(outs[0], outs[1])
