@@ -31,15 +31,25 @@ def bf16_bits(x):
     return (f.view(np.uint32) >> 16).astype(np.uint16)
 
 
-@pytest.mark.parametrize("n_micro,sched", [(2, "LRU"), (2, "H2O"), (4, "LRUPlus")])
-def test_group_matches_standalone_engines(monkeypatch, n_micro, sched):
+@pytest.mark.parametrize("n_micro,sched,codec", [(2, "LRU", "Identity"), (2, "H2O", "Identity"),
+                                                 (4, "LRUPlus", "Identity"), (2, "LRU", "Int8"),
+                                                 (2, "H2O", "Int4"), (2, "LRU", "LowRank")])
+def test_group_matches_standalone_engines(monkeypatch, n_micro, sched, codec):
     monkeypatch.setenv("PIKV_ATTEND_SMS", "12")  # same attention grid for both sides
     B, T = 8, 48
     cfg = engine_config(router="TopK", sched=sched, d=256, H=4, E=8, k=2, S=64, G=2, n_tok=1,
-                        n_exp=8, budget=6, ps=4, n_layers=0, dtype="bf16", batch=B)
+                        n_exp=8, budget=6, ps=4, n_layers=0, dtype="bf16", batch=B, codec=codec,
+                        rank=16)
     Bm = B // n_micro
     grp = EngineGroup(cfg, n_micro=n_micro, attend_sms=12)
     refs = [Engine(dataclasses.replace(cfg, batch=Bm)) for _ in range(n_micro)]
+    if codec == "LowRank":
+        hd = cfg.model.d // cfg.n_heads
+        basis = np.linalg.qr(np.random.default_rng(1).standard_normal((hd, hd)))[0][:, :16].T
+        basis = np.ascontiguousarray(np.repeat(basis[None], cfg.n_heads, 0), np.float32)
+        grp.set_codec(basis)
+        for r in refs:
+            r.set_codec(basis)
     rng = np.random.default_rng(5)
     x = bf16_bits(rng.standard_normal((T, 3, B, cfg.model.d)))
     dev = torch.from_numpy(x.view(np.int16)).cuda()
