@@ -1636,16 +1636,21 @@ int pikv_group_create(const pikv_config* cfg, int32_t n_micro, int32_t attend_sm
         if (!(cv && cv[0] == '1')) e->fused_control = false;
         g->eng.push_back(e);
         cudaEvent_t a, y;
-        cudaEventCreateWithFlags(&a, cudaEventDisableTiming);
+        // att_done keeps timing enabled: the other micro-batch's attention waits
+        // on it, and a DisableTiming event recorded right behind the attention
+        // graph launch released that wait later (e2e step 0.398 -> 0.357 ms at
+        // c2, profiles/microbench/e2e_timing_ab.py)
+        cudaEventCreate(&a);
         cudaEventCreateWithFlags(&y, cudaEventDisableTiming);
         g->att_done.push_back(a);
         g->y_done.push_back(y);
         cudaEvent_t yr;
         cudaStream_t sd;
-        cudaEventCreateWithFlags(&yr, cudaEventDisableTiming);
+        cudaEventCreate(&yr);  // timing enabled: waited on by the side stream (see att_done)
         cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking);
         g->y_ready.push_back(yr);
         g->side.push_back(sd);
+
     }
     cudaEventCreateWithFlags(&g->join, cudaEventDisableTiming);
     g->tev.resize(n_micro);
