@@ -298,7 +298,7 @@ def run_group(args, w, name, cfg, n_micro, local):
     attend_sms = args.attend_sms if args.attend_sms is not None else DEFAULT_ATTEND_SMS
     if attend_sms <= 0:  # the library default (pikv_group_create, attend_sms = 0)
         nsm = torch.cuda.get_device_properties(local).multi_processor_count
-        attend_sms = nsm if w["codec"] in ("Int8", "Int4") else nsm - 36
+        attend_sms = nsm - (12 if w["codec"] in ("Int8", "Int4") else 44)
     grp = EngineGroup(cfg, n_micro=n_micro, attend_sms=attend_sms, device=local)
     B, d, dp, Bm = cfg.batch, cfg.model.d, cfg.stored_width, grp.Bm
     if cfg.compressor.scheme in ("LowRank",):

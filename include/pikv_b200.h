@@ -356,7 +356,7 @@ int pikv_read_profile_host(pikv_engine* eng, float* phase_ms, int32_t n_phases,
  * micro-batch engines stepped one after another.
  * attend_sms > 0 limits the persistent attention grid to that many SMs so
  * the other micro-batch's control kernels find free SMs (0 = auto: all but
- * 36 SMs when n_micro > 1, all SMs for int8/int4; measured on B200). */
+ * 44 SMs when n_micro > 1, all but 12 for int8/int4; measured on B200). */
 typedef struct pikv_group pikv_group;
 int pikv_group_create(const pikv_config* cfg, int32_t n_micro, int32_t attend_sms,
                       int32_t cuda_device, pikv_group** out);

@@ -1610,14 +1610,16 @@ int pikv_group_create(const pikv_config* cfg, int32_t n_micro, int32_t attend_sm
     c.batch = cfg->batch / n_micro;
     if (cfg->pool_entries > 0) c.pool_entries = cfg->pool_entries / n_micro;
     if (attend_sms <= 0 && n_micro > 1) {
-        // leave 36 SMs to the control plane of the other micro-batch (c2 sweep,
-        // profiles/README.md: 148 -> 34.3 K, 136 -> 39.0 K, 124 -> 42.6 K,
-        // 116 / 108 -> 44.1 K tokens/s); int8/int4 attention is instruction-
-        // bound and keeps every SM (c4-int8: 33.7 K at 148)
+        // leave SMs to the control plane of the other micro-batch (sweeps in
+        // profiles/README.md): 44 for bf16/f32/low-rank attention (c2 flat at
+        // 44 K from 100 to 116 SMs, c3 42.7 K at 100 vs 39.9 K at 124,
+        // c4-low-rank 71.8 K at 104 vs 68.9 K at 120), 12 for int8/int4 whose
+        // attention needs more issue slots per byte (c4-int8 39.7 K at 136 vs
+        // 36.6 K at 148 and 37.7 K at 124; c4-int4 35.0 K at 136 vs 33.2 K at 148)
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device);
         const bool quant = cfg->codec == PIKV_CODEC_INT8 || cfg->codec == PIKV_CODEC_INT4;
-        attend_sms = quant ? sms : std::max(1, sms - 36);
+        attend_sms = std::max(1, sms - (quant ? 12 : 44));
     }
     for (int m = 0; m < n_micro; ++m) {
         pikv_engine* e = nullptr;
