@@ -410,6 +410,42 @@ class Engine {
     pikv_engine* h_ = nullptr;
 };
 
+// Micro-batch pipeline (include/pikv_b200.h, pikv_group_*; no reference
+// counterpart): the B streams split into n_micro engines whose control plane
+// overlaps each other's attention.  Serving loop per micro-batch m:
+// wait(m) -> the caller's next-token inputs -> submit(m, ...).  Host buffers
+// (pinned for asynchronous copies): q/k/v [B/n][d] in the kv dtype (uint16
+// bf16 bits or float), y [B/n][d'] fp32, valid after the next wait(m).
+class EngineGroup {
+  public:
+    explicit EngineGroup(const EngineConfig& cfg, int n_micro = 2, int attend_sms = 0) : cfg_(cfg) {
+        pikv_config c = cfg.to_c();
+        check(pikv_group_create(&c, n_micro, attend_sms, cfg.cuda_device, &g_));
+    }
+    ~EngineGroup() { if (g_) pikv_group_destroy(g_); }
+    EngineGroup(const EngineGroup&) = delete;
+    EngineGroup& operator=(const EngineGroup&) = delete;
+
+    int size() const { return pikv_group_size(g_); }
+    int streams_per_micro() const { return cfg_.batch / size(); }
+    void set_codec(const std::vector<float>& basis, const std::vector<float>& bias = {},
+                   const std::vector<std::int32_t>& kept = {}) {
+        for (int m = 0; m < size(); ++m)
+            check(pikv_set_codec_host(pikv_group_engine(g_, m), basis.empty() ? nullptr : basis.data(),
+                                      bias.empty() ? nullptr : bias.data(), kept.empty() ? nullptr : kept.data()));
+    }
+    void submit(int m, const void* q, const void* k, const void* v, float* y) {
+        check(pikv_group_submit(g_, m, q, k, v, nullptr, y, 1));
+    }
+    void wait(int m) { check(pikv_group_wait(g_, m)); }
+    void sync() { check(pikv_group_sync(g_)); }
+    pikv_engine* engine(int m) { return pikv_group_engine(g_, m); }
+
+  private:
+    EngineConfig cfg_;
+    pikv_group* g_ = nullptr;
+};
+
 // ---- wire formats of the reference's run output (runner.cpp) --------------
 // nlohmann::json dump(): keys sorted, compact, doubles as shortest digits in
 // nlohmann's layout (fixed for decimal exponents -4 < n <= 15); see

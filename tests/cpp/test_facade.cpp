@@ -4,6 +4,7 @@
 // cites the reference test it mirrors.  Exit code = number of failures.
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <random>
 
 #include <tuple>
@@ -161,6 +162,65 @@ int main() {
             CHECK(std::tie(snap[i - 1].device, snap[i - 1].shard, snap[i - 1].token_id, snap[i - 1].expert_id) <
                   std::tie(snap[i].device, snap[i].shard, snap[i].token_id, snap[i].expert_id));
         CHECK(!snap.empty() && wire::store_dump_line(snap[0]).find("\"age\":") == 1);
+    }
+    // micro-batch pipeline (pikv_group_*): a group of 2 x 2 streams submitted
+    // without waiting between micro-batches equals two engines stepped one
+    // call at a time (experts exactly; y to fp32 rounding: the attention grids
+    // differ, so the split-K partials merge in another order)
+    {
+        auto cfg = engine_config(RouterStrategy::TopK);
+        cfg.batch = 4;
+        EngineGroup grp(cfg, 2);
+        CHECK(grp.size() == 2 && grp.streams_per_micro() == 2);
+        auto one = cfg;
+        one.batch = 2;
+        Engine e0(one), e1(one);
+        Engine* ref[2] = {&e0, &e1};
+        std::mt19937_64 g(23);
+        std::normal_distribution<double> n(0.0, 1.0);
+        const int d = cfg.model.d, T = 20;
+        std::vector<float> in(static_cast<std::size_t>(T) * 4 * 3 * d), y(static_cast<std::size_t>(T) * 4 * d);
+        for (auto& x : in) x = static_cast<float>(n(g));
+        auto at = [&](int t, int s, int which) { return &in[((static_cast<std::size_t>(t) * 4 + s) * 3 + which) * d]; };
+        // packed per micro-batch: [q of its 2 streams][k][v]
+        std::vector<float> packed(static_cast<std::size_t>(T) * 2 * 3 * 2 * d);
+        for (int t = 0; t < T; ++t)
+            for (int m = 0; m < 2; ++m)
+                for (int w = 0; w < 3; ++w)
+                    for (int s = 0; s < 2; ++s)
+                        std::memcpy(&packed[((((static_cast<std::size_t>(t) * 2 + m) * 3 + w) * 2 + s) * d)],
+                                    at(t, 2 * m + s, w), sizeof(float) * d);
+        for (int t = 0; t < T; ++t)
+            for (int m = 0; m < 2; ++m) {
+                if (t) grp.wait(m);
+                const float* b = &packed[((static_cast<std::size_t>(t) * 2 + m) * 3) * 2 * d];
+                grp.submit(m, b, b + 2 * d, b + 4 * d, &y[(static_cast<std::size_t>(t) * 4 + 2 * m) * d]);
+            }
+        grp.sync();
+        double err = 0.0, nrm = 0.0;
+        for (int t = 0; t < T; ++t)
+            for (int m = 0; m < 2; ++m) {
+                std::vector<TokenInput> toks(2);
+                for (int s = 0; s < 2; ++s) {
+                    toks[s].query.assign(at(t, 2 * m + s, 0), at(t, 2 * m + s, 0) + d);
+                    toks[s].key.assign(at(t, 2 * m + s, 1), at(t, 2 * m + s, 1) + d);
+                    toks[s].value.assign(at(t, 2 * m + s, 2), at(t, 2 * m + s, 2) + d);
+                }
+                auto r = ref[m]->step(toks);
+                for (int s = 0; s < 2; ++s)
+                    for (int i = 0; i < d; ++i) {
+                        const double a = y[(static_cast<std::size_t>(t) * 4 + 2 * m + s) * d + i];
+                        const double b = r[s].attn.output[i];
+                        err += (a - b) * (a - b), nrm += b * b;
+                    }
+            }
+        CHECK(std::sqrt(err / (nrm > 0 ? nrm : 1.0)) <= 2e-5);
+        for (int m = 0; m < 2; ++m) {  // last step's routing, both streams of the micro-batch
+            std::vector<std::int32_t> ea(4), eb(4);
+            CHECK(pikv_read_step_host(grp.engine(m), ea.data(), nullptr, nullptr, nullptr) == 0);
+            CHECK(pikv_read_step_host(ref[m]->handle(), eb.data(), nullptr, nullptr, nullptr) == 0);
+            CHECK(ea == eb);
+        }
     }
     // QUEST needs a fitted scorer (test_scheduler.cpp:142-153)
     {
