@@ -603,7 +603,7 @@ Plan make_plan(const Dims& D) {
     const int ring_max = (int)((kSmemBudget - 256 - redb) / D.entry_bytes);  // entries that fit
     // a stage holds whole consumer batches (EP sub-groups x NB entries): a
     // partly filled batch still decodes and dots its K chunks
-    const int nb = (D.codec == PIKV_CODEC_INT8 || D.codec == PIKV_CODEC_INT4) ? 4 : 2;  // BatchOf<Dec>::NB
+    const int nb = (D.codec == PIKV_CODEC_INT8 || D.codec == PIKV_CODEC_INT4 || cpt == 1) ? 4 : 2;  // BatchOf::NB
     const int batch = std::max(1, pl.P.EP * nb);
     int eps = (32 * 1024) / D.entry_bytes;
     eps = std::max(eps, std::min(batch, 32));
@@ -625,13 +625,16 @@ Plan make_plan(const Dims& D) {
     return pl;
 }
 
-template <class Dec> struct BatchOf { static constexpr int NB = 2; };
-template <> struct BatchOf<DecI8> { static constexpr int NB = 4; };  // half/quarter-size entries:
-template <> struct BatchOf<DecI4> { static constexpr int NB = 4; };  // amortize per-entry work
+// entries per consumer batch: 4 where a thread's share of an entry is small
+// (int8 / int4 codes; one 16-byte chunk of a bf16/f32 head, e.g. rank-32
+// projections) to amortize the per-entry softmax work, else 2 (registers)
+template <class Dec, int CPT> struct BatchOf { static constexpr int NB = CPT == 1 ? 4 : 2; };
+template <int CPT> struct BatchOf<DecI8, CPT> { static constexpr int NB = 4; };
+template <int CPT> struct BatchOf<DecI4, CPT> { static constexpr int NB = 4; };
 
 template <class Dec, int CPT, int LPHC>
 void launch_t(const Dims& D, const State& S, const Plan& pl, cudaStream_t st) {
-    auto kern = k_attend<Dec, CPT, BatchOf<Dec>::NB, LPHC>;
+    auto kern = k_attend<Dec, CPT, BatchOf<Dec, CPT>::NB, LPHC>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
     launch_pdl(kern, dim3(D.attend_ctas), dim3(kThreads), pl.smem, st, D, S, pl.P);
 }
