@@ -399,9 +399,20 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
-template <int NP>
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];\n" ::"l"((uint64_t)map),
+        "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+
+// TST: the epilogue stores through TMA (r == NP, a multiple of 32: each warp's
+// 32 accumulator rows go to a SWIZZLE_128B smem box per 32 columns, one
+// cp.async.bulk.tensor store each; rows beyond T are clipped by the unit)
+template <int NP, bool TST>
 __global__ void __launch_bounds__(128) k_bulk_project_tc3(const __grid_constant__ CUtensorMap map_k,
-                                                          const __grid_constant__ CUtensorMap map_v, Dims D,
+                                                          const __grid_constant__ CUtensorMap map_v,
+                                                          const __grid_constant__ CUtensorMap map_o, Dims D,
                                                           int64_t T, const uint16_t* __restrict__ bhl,
                                                           float* __restrict__ proj,
                                                           const float* __restrict__ bias_proj) {
@@ -409,13 +420,15 @@ __global__ void __launch_bounds__(128) k_bulk_project_tc3(const __grid_constant_
     constexpr int HD = 128, KC = 16;
     constexpr uint32_t A_BYTES = (uint32_t)kTcM * HD * 2, B_BYTES = (uint32_t)NP * HD * 2;
     constexpr int NACC = NP < 32 ? 32 : NP;
+    constexpr int NBOX = TST ? NP / 32 : 0;  // 32-column output boxes per warp
     const int r = D.dph;
     const int h = blockIdx.y, row = blockIdx.z, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     // 1024-byte aligned stages (SWIZZLE_128B atoms)
     uint8_t* base = (uint8_t*)(((uintptr_t)sm3 + 1023) & ~(uintptr_t)1023);
     uint8_t* a_st[2] = {base, base + A_BYTES};
     uint8_t* b_hl = base + 2 * A_BYTES;
-    uint64_t* full = (uint64_t*)(b_hl + 2 * B_BYTES);  // [2] TMA landed
+    uint8_t* obuf = b_hl + 2 * B_BYTES + (size_t)warp * NBOX * 4096;  // TST: this warp's boxes
+    uint64_t* full = (uint64_t*)(b_hl + 2 * B_BYTES + 4 * NBOX * 4096);  // [2] TMA landed
     uint64_t* done = full + 2;                         // [2] MMAs of the stage finished
     uint32_t* tmem_slot = (uint32_t*)(done + 2);
     float* tr = (float*)(tmem_slot + 4) + warp * 32 * (NP + 1);
@@ -450,17 +463,42 @@ __global__ void __launch_bounds__(128) k_bulk_project_tc3(const __grid_constant_
     auto drain = [&](int pb, int64_t tile) {
         float accv[NP];
         tmem_ld_rows<NP>(tmem + (uint32_t)(pb * NACC) + ((uint32_t)(warp * 32) << 16), accv);
+        if constexpr (TST) {
+            if (bias_proj) {
 #pragma unroll
-        for (int j = 0; j < NP; ++j) tr[lane * (NP + 1) + j] = accv[j];
-        __syncwarp();
-        for (int c = lane; c < r; c += 32) {
-            const float bj = bias_proj ? bias_proj[h * r + c] : 0.f;
-            for (int rr = 0; rr < 32; ++rr) {
-                const int64_t g = tile * kTcM + warp * 32 + rr;
-                if (g < T) proj[((int64_t)row * T + g) * D.dp + h * r + c] = tr[rr * (NP + 1) + c] - bj;
+                for (int j = 0; j < NP; ++j) accv[j] -= bias_proj[h * NP + j];
             }
+            // the previous tile's store must have read the boxes
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            __syncwarp();
+#pragma unroll
+            for (int bx = 0; bx < NBOX; ++bx)
+#pragma unroll
+                for (int c = 0; c < 8; ++c)  // row = lane: 16-byte chunk c at c ^ (row & 7)
+                    *(float4*)(obuf + bx * 4096 + lane * 128 + ((c ^ (lane & 7)) << 4)) =
+                        make_float4(accv[bx * 32 + 4 * c], accv[bx * 32 + 4 * c + 1], accv[bx * 32 + 4 * c + 2],
+                                    accv[bx * 32 + 4 * c + 3]);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+#pragma unroll
+                for (int bx = 0; bx < NBOX; ++bx)
+                    tma_store_3d(&map_o, obuf + bx * 4096, h * NP + bx * 32, (int)(tile * kTcM) + warp * 32, row);
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < NP; ++j) tr[lane * (NP + 1) + j] = accv[j];
+            __syncwarp();
+            for (int c = lane; c < r; c += 32) {
+                const float bj = bias_proj ? bias_proj[h * r + c] : 0.f;
+                for (int rr = 0; rr < 32; ++rr) {
+                    const int64_t g = tile * kTcM + warp * 32 + rr;
+                    if (g < T) proj[((int64_t)row * T + g) * D.dp + h * r + c] = tr[rr * (NP + 1) + c] - bj;
+                }
+            }
+            __syncwarp();
         }
-        __syncwarp();
     };
     const int64_t t0 = blockIdx.x, step = gridDim.x;
     if (tid == 0) {
@@ -506,6 +544,7 @@ __global__ void __launch_bounds__(128) k_bulk_project_tc3(const __grid_constant_
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         drain(pb, prev);
     }
+    if (TST && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 0)
@@ -542,6 +581,40 @@ bool make_kv_map(CUtensorMap* m, const void* x, int64_t T, int d) {
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// proj [2][T][dp] fp32 as a 3-D map, boxes of 32 columns (128 B) x 32 rows x 1,
+// SWIZZLE_128B (the epilogue's conflict-free box layout)
+bool make_out_map(CUtensorMap* m, float* proj, int64_t T, int dp) {
+    EncodeTiledFn fn = encode_tiled_fn();
+    if (!fn || ((uintptr_t)proj & 15) || (dp * 4) % 16) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)dp, (cuuint64_t)T, 2};
+    const cuuint64_t strides[2] = {(cuuint64_t)dp * 4, (cuuint64_t)T * dp * 4};
+    const cuuint32_t box[3] = {32, 32, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, proj, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int NP, bool TST>
+int launch_tc3(const Dims& D, int64_t T, const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mo,
+               const uint16_t* bhl, float* proj, const float* bias_proj, cudaStream_t st) {
+    const size_t smem = 1024 + 2 * (size_t)kTcM * 128 * 2 + 2 * (size_t)NP * 128 * 2 + 64 +
+                        (TST ? (size_t)4 * (NP / 32) * 4096 : sizeof(float) * 4 * 32 * (NP + 1));
+    cudaFuncSetAttribute(k_bulk_project_tc3<NP, TST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int64_t ntiles = (T + kTcM - 1) / kTcM;
+    int sms = 148, smem_sm = 228 * 1024;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, 0);
+    const int occ = std::max(1, std::min(4, smem_sm / (int)(smem + 1024)));  // CTAs per SM by shared memory
+    // one wave: (head, K|V) pairs x slices <= resident CTAs
+    int64_t per = (int64_t)occ * sms / (2LL * D.H);
+    if (per > ntiles) per = ntiles;
+    if (per < 1) per = 1;
+    k_bulk_project_tc3<NP, TST><<<dim3((unsigned)per, D.H, 2), 128, smem, st>>>(mk, mv, mo, D, T, bhl, proj,
+                                                                                bias_proj);
+    return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
 template <int NP>
 int launch_np(const Dims& D, const State& S, int64_t T, const void* k, const void* v, float* proj,
               const float* bias_proj, float* scratch_b, cudaStream_t st) {
@@ -553,20 +626,13 @@ int launch_np(const Dims& D, const State& S, int64_t T, const void* k, const voi
         make_kv_map(&mv, v, T, D.d)) {
         uint16_t* bhl = (uint16_t*)scratch_b;
         k_basis_split<NP><<<64, 256, 0, st>>>(D, S, bhl);
-        const size_t smem = 1024 + 2 * (size_t)kTcM * 128 * 2 + 2 * (size_t)NP * 128 * 2 + 64 +
-                            sizeof(float) * 4 * 32 * (NP + 1);
-        cudaFuncSetAttribute(k_bulk_project_tc3<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        const int64_t ntiles = (T + kTcM - 1) / kTcM;
-        int sms = 148, smem_sm = 228 * 1024;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-        cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, 0);
-        const int occ = std::max(1, std::min(4, smem_sm / (int)(smem + 1024)));  // CTAs per SM by shared memory
-        // one wave: (head, K|V) pairs x slices <= resident CTAs
-        int64_t per = (int64_t)occ * sms / (2LL * D.H);
-        if (per > ntiles) per = ntiles;
-        if (per < 1) per = 1;
-        k_bulk_project_tc3<NP><<<dim3((unsigned)per, D.H, 2), 128, smem, st>>>(mk, mv, D, T, bhl, proj, bias_proj);
-        return cudaGetLastError() == cudaSuccess ? 0 : 1;
+        const char* ts = std::getenv("PIKV_BULK_TSTORE");  // A/B: 0 = thread stores
+        CUtensorMap mo;
+        if constexpr (NP % 32 == 0) {
+            if (D.dph == NP && !(ts && ts[0] == '0') && make_out_map(&mo, proj, T, D.dp))
+                return launch_tc3<NP, true>(D, T, mk, mv, mo, bhl, proj, bias_proj, st);
+        }
+        return launch_tc3<NP, false>(D, T, mk, mv, mk, bhl, proj, bias_proj, st);
     }
     if (!f32in && hd == 128 && scratch_b) {  // pipelined persistent kernel
         uint16_t* bhl = (uint16_t*)scratch_b;

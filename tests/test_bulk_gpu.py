@@ -151,10 +151,13 @@ def test_bulk_projection_tensor_cores_match_cuda_cores(monkeypatch, codec, dtype
     assert rel_l2(ya.astype(np.float64), yb.astype(np.float64)) <= tol
 
 
-@pytest.mark.parametrize("d,H,rank,T", [(256, 2, 32, 300), (4096, 32, 32, 2000), (4096, 32, 16, 700)])
-def test_bulk_projection_tma_matches_register_staged(monkeypatch, d, H, rank, T):
+@pytest.mark.parametrize("codec,d,H,rank,T", [("LowRank", 256, 2, 32, 300), ("LowRank", 4096, 32, 32, 2000),
+                                               ("LowRank", 4096, 32, 16, 700), ("LoRAPlus", 256, 2, 32, 300),
+                                               ("LowRank", 256, 2, 64, 260)])
+def test_bulk_projection_tma_matches_register_staged(monkeypatch, codec, d, H, rank, T):
     """The TMA-fed tcgen05 projection (A tiles by cp.async.bulk.tensor into
-    SWIZZLE_128B stages) issues the same MMAs in the same order as the
+    SWIZZLE_128B stages; ranks 32 / 64 also store through TMA, LoRAPlus bias
+    subtracted before the store) issues the same MMAs in the same order as the
     register-staged kernel (PIKV_BULK_TMA=0), so decode over the bulk-built
     store is bit-identical; d = 32 x 128 gives every CTA several tiles (the
     persistent loop, both ring stages) and a partial last tile."""
@@ -164,10 +167,10 @@ def test_bulk_projection_tma_matches_register_staged(monkeypatch, d, H, rank, T)
         monkeypatch.setenv("PIKV_BULK_TC", "2")
         monkeypatch.setenv("PIKV_BULK_TMA", tma)
         cfg = engine_config(router="TopK", sched="LRU", unbounded=True, d=d, H=H, S=4096, batch=1,
-                            codec="LowRank", rank=rank, dtype="bf16", n_layers=0)
-        basis, _, _ = codec_params("LowRank", d, H, rank, np.random.default_rng(3))
+                            codec=codec, rank=rank, dtype="bf16", n_layers=0)
+        basis, bias, _ = codec_params(codec, d, H, rank, np.random.default_rng(3))
         eng = Engine(cfg)
-        eng.set_codec(basis, None, None)
+        eng.set_codec(basis, None if bias is None else bias.astype(np.float32), None)
         st = make_stream(T + 3, d, 31, "bf16", 0)
         ex = np.stack([rng.choice(cfg.model.E, cfg.router.k, replace=False) for _ in range(T)]).astype(np.int32)
         eng.insert_bulk_host(0, to_kv(st[1][:T], "bf16"), to_kv(st[2][:T], "bf16"), ex)
