@@ -2545,8 +2545,11 @@ __global__ void __launch_bounds__(512) k_bulk_ring(Dims D, State S, int s, int64
     __shared__ unsigned long long sm_disp;
     // count
     int64_t mine = 0;
+    // token of entry e: 32-bit division when the bulk fits (always, in practice)
+    const bool small = n < (1LL << 31);
+    auto tok_of = [&](int64_t e) -> int64_t { return small ? (int64_t)((uint32_t)e / (uint32_t)D.k) : e / D.k; };
     for (int64_t e = tid; e < n; e += NT)
-        mine += bulk_ring_of(D, (int64_t)(now0 + (uint64_t)(e / D.k)), experts[e]) == rl;
+        mine += bulk_ring_of(D, (int64_t)(now0 + (uint64_t)tok_of(e)), experts[e]) == rl;
     int64_t tot;
     block_excl_scan(mine, wsum, &tot);
     if (tid == 0) sm_c = tot, sm_run = 0, sm_disp = 0;
@@ -2595,7 +2598,7 @@ __global__ void __launch_bounds__(512) k_bulk_ring(Dims D, State S, int s, int64
 #pragma unroll
         for (int u = 0; u < PER; ++u) {
             const int64_t e = eb + u;
-            const bool in = e < n && bulk_ring_of(D, (int64_t)(now0 + (uint64_t)(e / D.k)), experts[e]) == rl;
+            const bool in = e < n && bulk_ring_of(D, (int64_t)(now0 + (uint64_t)tok_of(e)), experts[e]) == rl;
             mask |= (uint32_t)in << u;
         }
         int64_t chunk;
@@ -2603,7 +2606,7 @@ __global__ void __launch_bounds__(512) k_bulk_ring(Dims D, State S, int s, int64
         for (; mask; mask &= mask - 1, ++j) {
             const int u = __ffs(mask) - 1;
             const int64_t e = eb + u;
-            const int64_t t = e / D.k;
+            const int64_t t = tok_of(e);
             if (j >= first_surv) {
                 const int slot = (int)((head + j) % D.S);
                 const int64_t gi = ring * D.S + slot;

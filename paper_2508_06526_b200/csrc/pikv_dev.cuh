@@ -175,9 +175,11 @@ struct State {
 };
 
 // ---- helpers -------------------------------------------------------------
+// t, e >= 0 and n_tok, n_exp powers of two (validated on the host,
+// kvstore.cpp:17-22), so the moduli are masks (no 64-bit division)
 __device__ __forceinline__ int shard_raw(int64_t t, int e, int n_tok, int n_exp, int additive) {
-    int lhs = (int)(t % n_tok);
-    int rhs = e % n_exp;
+    int lhs = (int)(t & (int64_t)(n_tok - 1));
+    int rhs = e & (n_exp - 1);
     return additive ? lhs + rhs : (lhs ^ rhs);
 }
 
