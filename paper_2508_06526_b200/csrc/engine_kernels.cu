@@ -2532,7 +2532,8 @@ __device__ __forceinline__ int bulk_ring_of(const Dims& D, int64_t token, int e)
 __global__ void __launch_bounds__(512) k_bulk_ring(Dims D, State S, int s, int64_t T,
                                                    const int32_t* __restrict__ experts,
                                                    const double* __restrict__ saliency,
-                                                   int64_t* __restrict__ dst, unsigned long long* counters) {
+                                                   int64_t* __restrict__ dst, unsigned long long* counters,
+                                                   int use_smem) {
     const int rl = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NT = blockDim.x;
     const int NW = NT >> 5;
     const int64_t ring = (int64_t)s * D.R + rl;
@@ -2637,14 +2638,25 @@ __global__ void __launch_bounds__(512) k_bulk_ring(Dims D, State S, int s, int64
     }
     __threadfence_block();
     __syncthreads();
-    // rebuild the ring's counters and page records from its final slots
-    for (int64_t r = tid; r < D.ppr_sched; r += NT) {
-        const int64_t ri = ring * D.ppr_sched + r;
-        S.pr_cnt[ri] = 0, S.pr_first[ri] = 0x7fffffff, S.pr_sla[ri] = 0, S.pr_sf[ri] = 0;
-    }
+    // rebuild the ring's counters and page records from its final slots:
+    // accumulated in shared memory (16 consecutive slots share a record, so
+    // global atomics serialized 16-deep per warp), written once
+    // (rings too large for shared memory accumulate in the global records)
+    extern __shared__ __align__(16) uint8_t sm_rec[];
+    const int64_t base_r = use_smem ? 0 : ring * D.ppr_sched;
+    unsigned long long* r_sla = use_smem ? (unsigned long long*)sm_rec : (unsigned long long*)S.pr_sla + base_r;
+    unsigned long long* r_sf = use_smem ? r_sla + D.ppr_sched : (unsigned long long*)S.pr_sf + base_r;
+    int* r_cnt = use_smem ? (int*)(r_sf + D.ppr_sched) : S.pr_cnt + base_r;
+    int* r_first = use_smem ? r_cnt + D.ppr_sched : S.pr_first + base_r;
+    int* p_live = use_smem ? r_first + D.ppr_sched : nullptr;
+    for (int r = tid; r < D.ppr_sched; r += NT) r_sla[r] = 0, r_sf[r] = 0, r_cnt[r] = 0, r_first[r] = 0x7fffffff;
     for (int p = tid; p < D.ppr; p += NT) {
-        const int32_t page = S.page_table[ring * D.ppr + p];
-        if (page >= 0) S.page_live[page] = 0;
+        if (use_smem) {
+            p_live[p] = 0;
+        } else {
+            const int32_t page = S.page_table[ring * D.ppr + p];
+            if (page >= 0) S.page_live[page] = 0;
+        }
     }
     __syncthreads();
     int lv = 0;
@@ -2653,12 +2665,18 @@ __global__ void __launch_bounds__(512) k_bulk_ring(Dims D, State S, int s, int64
         if (S.id[gi] == 0) continue;
         ++lv;
         const uint64_t sq = S.shard_seq[gi];
-        const int64_t ri = page_rec(D, ring, sq);
-        atomicAdd(&S.pr_cnt[ri], 1);
-        atomicMin(&S.pr_first[ri], (int)(sq % (uint64_t)D.page_size));
-        atomicAdd((unsigned long long*)&S.pr_sla[ri], (unsigned long long)S.last_access[gi]);
-        atomicAdd((unsigned long long*)&S.pr_sf[ri], (unsigned long long)S.freq[gi]);
-        atomicAdd(&S.page_live[S.page_table[ring * D.ppr + slot / D.spg]], 1);
+        const int r = (int)(page_rec(D, ring, sq) - ring * D.ppr_sched);
+        atomicAdd(&r_cnt[r], 1);
+        atomicMin(&r_first[r], (int)(sq % (uint64_t)D.page_size));
+        atomicAdd(&r_sla[r], (unsigned long long)S.last_access[gi]);
+        atomicAdd(&r_sf[r], (unsigned long long)S.freq[gi]);
+        if (use_smem) atomicAdd(&p_live[slot / D.spg], 1);
+        else atomicAdd(&S.page_live[S.page_table[ring * D.ppr + slot / D.spg]], 1);
+    }
+    __syncthreads();
+    for (int p = tid; use_smem && p < D.ppr; p += NT) {
+        const int32_t page = S.page_table[ring * D.ppr + p];
+        if (page >= 0) S.page_live[page] = p_live[p];
     }
     for (int o = 16; o; o >>= 1) lv += __shfl_xor_sync(0xffffffffu, lv, o);
     __shared__ int sm_lv, sm_pages;
@@ -2667,10 +2685,16 @@ __global__ void __launch_bounds__(512) k_bulk_ring(Dims D, State S, int s, int64
     if (lane == 0) atomicAdd(&sm_lv, lv);
     __syncthreads();
     int pg = 0;
-    for (int64_t r = tid; r < D.ppr_sched; r += NT) {
+    for (int r = tid; r < D.ppr_sched; r += NT) {
         const int64_t ri = ring * D.ppr_sched + r;
-        if (S.pr_cnt[ri] > 0) ++pg;
-        else S.pr_first[ri] = 0;
+        const int cnt = r_cnt[r];
+        const int first = cnt > 0 ? r_first[r] : 0;
+        const unsigned long long sla = r_sla[r], sf = r_sf[r];
+        S.pr_cnt[ri] = cnt;
+        S.pr_first[ri] = first;
+        S.pr_sla[ri] = sla;
+        S.pr_sf[ri] = sf;
+        pg += cnt > 0;
     }
     for (int o = 16; o; o >>= 1) pg += __shfl_xor_sync(0xffffffffu, pg, o);
     if (lane == 0) atomicAdd(&sm_pages, pg);
@@ -2781,7 +2805,13 @@ int bulk_insert(const Dims& D, const State& S, int s, int64_t T, const void* k, 
             k_bulk_project_fma<<<dim3(64, D.H, 2), 256, smem, st>>>(D, S, T, k, v, proj);
         }
     }
-    if (D.R > 0) k_bulk_ring<<<D.R, 512, 0, st>>>(D, S, s, T, experts, saliency, dst, counters);
+    if (D.R > 0) {
+        size_t rsm = (size_t)D.ppr_sched * 24 + (size_t)D.ppr * 4;  // page-record accumulators
+        const int use_smem = rsm <= 160 * 1024;
+        if (!use_smem) rsm = 0;
+        if (rsm > 48 * 1024) cudaFuncSetAttribute(k_bulk_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
+        k_bulk_ring<<<D.R, 512, rsm, st>>>(D, S, s, T, experts, saliency, dst, counters, use_smem);
+    }
     const size_t psmem = (size_t)((D.entry_bytes + 15) & ~15) + sizeof(float) * (size_t)D.d;
     if (psmem > 48 * 1024)
         cudaFuncSetAttribute(k_bulk_payload, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
