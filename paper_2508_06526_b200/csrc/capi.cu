@@ -1276,7 +1276,9 @@ int pikv_insert_bulk(pikv_engine* eng, int32_t stream, int64_t T, const void* k,
                                                 (((size_t)D.dp + 63) & ~(size_t)63) +
                                                 (size_t)D.H * 64 * (D.d / D.H) + 64)
                              : 0;
-    const size_t need = ((n_dst + 255) & ~(size_t)255) + ((n_ctr + 255) & ~(size_t)255) + n_pr;
+    const size_t n_sort = sizeof(int32_t) * bulk_sort_ints(D, T);
+    const size_t need = ((n_dst + 255) & ~(size_t)255) + ((n_ctr + 255) & ~(size_t)255) + ((n_pr + 255) & ~(size_t)255) +
+                        n_sort;
     if (need > eng->bulk_cap) {
         CUDA_TRY(cudaStreamSynchronize(st));
         if (eng->bulk_buf) cudaFree(eng->bulk_buf);
@@ -1287,11 +1289,13 @@ int pikv_insert_bulk(pikv_engine* eng, int32_t stream, int64_t T, const void* k,
     int64_t* dst = (int64_t*)eng->bulk_buf;
     unsigned long long* ctr = (unsigned long long*)((uint8_t*)eng->bulk_buf + ((n_dst + 255) & ~(size_t)255));
     float* pr = proj ? (float*)((uint8_t*)ctr + ((n_ctr + 255) & ~(size_t)255)) : nullptr;
+    int32_t* sort_buf = (int32_t*)((uint8_t*)ctr + ((n_ctr + 255) & ~(size_t)255) + ((n_pr + 255) & ~(size_t)255));
     cudaError_t e = cudaSuccess;
     {
         const char* tc = std::getenv("PIKV_BULK_TC");
+        const char* so = std::getenv("PIKV_BULK_SORT");  // A/B: 0 = per-ring scans
         e = (cudaError_t)bulk_insert(D, eng->S, stream, T, k, v, experts, saliency, dst, pr, ctr,
-                                     tc ? std::atoi(tc) : 1, st);
+                                     tc ? std::atoi(tc) : 1, st, (so && so[0] == '0') ? nullptr : sort_buf);
     }
     unsigned long long host_ctr[2] = {0, 0};
     if (e == cudaSuccess) e = cudaMemcpyAsync(host_ctr, ctr, sizeof(host_ctr), cudaMemcpyDeviceToHost, st);

@@ -2529,11 +2529,92 @@ __device__ __forceinline__ int bulk_ring_of(const Dims& D, int64_t token, int e)
     return (dev / D.world) * D.SPD + raw / D.G;
 }
 
+// ---- grid-wide stable counting sort of the bulk's (token, expert) pairs by
+// local ring (replaces each ring CTA scanning every pair twice) ------------
+constexpr int kSortChunk = 4096;  // pairs per block (512 threads x 8)
+constexpr int kSortMaxR = 256;    // rings per stream handled by the sort path
+
+// ring of every pair (-1: another rank's device) and per-chunk ring counts
+__global__ void __launch_bounds__(512) k_bulk_hist(Dims D, State S, int s, int64_t n,
+                                                   const int32_t* __restrict__ experts,
+                                                   int32_t* __restrict__ ringof, int32_t* __restrict__ hist) {
+    __shared__ int hs[kSortMaxR];
+    const int tid = threadIdx.x;
+    for (int r = tid; r < D.R; r += blockDim.x) hs[r] = 0;
+    __syncthreads();
+    const uint64_t now0 = S.now[s];
+    const int64_t c0 = (int64_t)blockIdx.x * kSortChunk;
+    for (int i = tid; i < kSortChunk; i += blockDim.x) {
+        const int64_t e = c0 + i;
+        if (e >= n) break;
+        const int64_t t = n < (1LL << 31) ? (int64_t)((uint32_t)e / (uint32_t)D.k) : e / D.k;
+        const int r = bulk_ring_of(D, (int64_t)(now0 + (uint64_t)t), experts[e]);
+        ringof[e] = r;
+        if (r >= 0) atomicAdd(&hs[r], 1);
+    }
+    __syncthreads();
+    for (int r = tid; r < D.R; r += blockDim.x) hist[(int64_t)blockIdx.x * D.R + r] = hs[r];
+}
+
+// per ring: exclusive scan over chunks (in place), ring totals and bases
+__global__ void k_bulk_offsets(Dims D, int nchunk, int32_t* __restrict__ hist, int32_t* __restrict__ ring_c,
+                               int32_t* __restrict__ ring_base) {
+    __shared__ int64_t wsum[32];
+    const int r = threadIdx.x;
+    int run = 0;
+    if (r < D.R)
+        for (int c = 0; c < nchunk; ++c) {
+            const int x = hist[(int64_t)c * D.R + r];
+            hist[(int64_t)c * D.R + r] = run;
+            run += x;
+        }
+    int64_t tot;
+    const int64_t b = block_excl_scan(r < D.R ? (int64_t)run : 0, wsum, &tot);
+    if (r < D.R) ring_c[r] = run, ring_base[r] = (int32_t)b;
+}
+
+// stable ranks: pairs of a chunk in rounds of 512 (warp match + per-warp
+// counts scanned in warp order); list[ring_base[r] + rank] = pair index
+__global__ void __launch_bounds__(512) k_bulk_rank(Dims D, int64_t n, const int32_t* __restrict__ ringof,
+                                                   const int32_t* __restrict__ off,
+                                                   const int32_t* __restrict__ ring_base,
+                                                   int32_t* __restrict__ list) {
+    __shared__ int cnt[16][kSortMaxR];
+    __shared__ int run[kSortMaxR];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int r = tid; r < D.R; r += blockDim.x) run[r] = off[(int64_t)blockIdx.x * D.R + r];
+    const int64_t c0 = (int64_t)blockIdx.x * kSortChunk;
+    for (int i0 = 0; i0 < kSortChunk; i0 += 512) {
+        for (int x = tid; x < 16 * D.R; x += blockDim.x) cnt[x / D.R][x % D.R] = 0;
+        __syncthreads();
+        const int64_t e = c0 + i0 + tid;
+        const int r = e < n ? ringof[e] : -1;
+        const unsigned peers = __match_any_sync(0xffffffffu, r);
+        const int rk = __popc(peers & ((1u << lane) - 1u));
+        if (r >= 0 && rk == 0) cnt[warp][r] = __popc(peers);
+        __syncthreads();
+        if (r >= 0) {
+            int before = run[r];
+            for (int w = 0; w < warp; ++w) before += cnt[w][r];
+            list[ring_base[r] + before + rk] = (int32_t)e;
+        }
+        __syncthreads();
+        for (int x = tid; x < D.R; x += blockDim.x) {
+            int t = 0;
+            for (int w = 0; w < 16; ++w) t += cnt[w][x];
+            run[x] += t;
+        }
+        __syncthreads();
+    }
+}
+
 __global__ void __launch_bounds__(512) k_bulk_ring(Dims D, State S, int s, int64_t T,
                                                    const int32_t* __restrict__ experts,
                                                    const double* __restrict__ saliency,
                                                    int64_t* __restrict__ dst, unsigned long long* counters,
-                                                   int use_smem) {
+                                                   int use_smem, const int32_t* __restrict__ list,
+                                                   const int32_t* __restrict__ ring_c,
+                                                   const int32_t* __restrict__ ring_base) {
     const int rl = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NT = blockDim.x;
     const int NW = NT >> 5;
     const int64_t ring = (int64_t)s * D.R + rl;
@@ -2549,10 +2630,12 @@ __global__ void __launch_bounds__(512) k_bulk_ring(Dims D, State S, int s, int64
     // token of entry e: 32-bit division when the bulk fits (always, in practice)
     const bool small = n < (1LL << 31);
     auto tok_of = [&](int64_t e) -> int64_t { return small ? (int64_t)((uint32_t)e / (uint32_t)D.k) : e / D.k; };
-    for (int64_t e = tid; e < n; e += NT)
-        mine += bulk_ring_of(D, (int64_t)(now0 + (uint64_t)tok_of(e)), experts[e]) == rl;
+    if (!list)
+        for (int64_t e = tid; e < n; e += NT)
+            mine += bulk_ring_of(D, (int64_t)(now0 + (uint64_t)tok_of(e)), experts[e]) == rl;
     int64_t tot;
     block_excl_scan(mine, wsum, &tot);
+    if (list) tot = ring_c[rl];  // counted by the sort
     if (tid == 0) sm_c = tot, sm_run = 0, sm_disp = 0;
     __syncthreads();
     const int64_t c = sm_c;  // c == 0: nothing placed, the ring still counts its live pages
@@ -2593,7 +2676,27 @@ __global__ void __launch_bounds__(512) k_bulk_ring(Dims D, State S, int s, int64
     // entries with a serial warp prefix: 365 -> ~60 us at 32K tokens)
     constexpr int PER = 16;
     int64_t run = 0;
-    for (int64_t e0 = 0; c > 0 && e0 < n; e0 += (int64_t)NT * PER) {
+    // sorted path: the ring's pairs in order at list[ring_base + j]
+    for (int64_t j = first_surv + tid; list && j < c; j += NT) {
+        const int64_t e = list[ring_base[rl] + j];
+        const int64_t t = tok_of(e);
+        const int slot = (int)((head + j) % D.S);
+        const int64_t gi = ring * D.S + slot;
+        const uint64_t step = now0 + (uint64_t)t;
+        S.id[gi] = id0 + (uint64_t)e;
+        S.shard_seq[gi] = seq0 + (uint64_t)j;
+        S.token[gi] = (int64_t)step;
+        S.expert[gi] = experts[e];
+        S.insert_step[gi] = step;
+        S.last_access[gi] = step;
+        S.freq[gi] = 0;
+        S.attn_mass[gi] = 0.0;
+        for (int l = 0; l < D.n_layers; ++l)
+            S.per_layer[gi * D.n_layers + l] = saliency ? saliency[t * D.n_layers + l] : 0.0;
+        const int32_t page = S.page_table[ring * D.ppr + slot / D.spg];
+        dst[e] = (int64_t)page * D.spg + slot % D.spg;
+    }
+    for (int64_t e0 = 0; !list && c > 0 && e0 < n; e0 += (int64_t)NT * PER) {
         const int64_t eb = e0 + (int64_t)tid * PER;
         uint32_t mask = 0;
 #pragma unroll
@@ -2789,9 +2892,14 @@ __global__ void k_bulk_project_fma(Dims D, State S, int64_t T, const void* __res
     }
 }
 
+size_t bulk_sort_ints(const Dims& D, int64_t T) {  // scratch of the counting sort (int32 count)
+    const int64_t n = T * D.k, nchunk = (n + kSortChunk - 1) / kSortChunk;
+    return (size_t)(2 * n + nchunk * D.R + 2 * D.R + 64);
+}
+
 int bulk_insert(const Dims& D, const State& S, int s, int64_t T, const void* k, const void* v,
                 const int32_t* experts, const double* saliency, int64_t* dst, float* proj,
-                unsigned long long* counters, int use_tc, cudaStream_t st) {
+                unsigned long long* counters, int use_tc, cudaStream_t st, int32_t* sort_buf) {
     cudaMemsetAsync(counters, 0, sizeof(unsigned long long) * (2 + D.Gl), st);
     cudaMemsetAsync(dst, 0xff, sizeof(int64_t) * (size_t)(T * D.k), st);  // -1: not stored here
     if ((D.codec == PIKV_CODEC_LOWRANK || D.codec == PIKV_CODEC_LORAPLUS) && T > 0) {
@@ -2810,7 +2918,20 @@ int bulk_insert(const Dims& D, const State& S, int s, int64_t T, const void* k, 
         const int use_smem = rsm <= 160 * 1024;
         if (!use_smem) rsm = 0;
         if (rsm > 48 * 1024) cudaFuncSetAttribute(k_bulk_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
-        k_bulk_ring<<<D.R, 512, rsm, st>>>(D, S, s, T, experts, saliency, dst, counters, use_smem);
+        const int64_t n = T * D.k, nchunk = (n + kSortChunk - 1) / kSortChunk;
+        int32_t *list = nullptr, *ring_c = nullptr, *ring_base = nullptr;
+        if (sort_buf && D.R <= kSortMaxR && n > 0 && n < (1LL << 31)) {
+            int32_t* ringof = sort_buf;
+            list = ringof + n;
+            int32_t* hist = list + n;
+            ring_c = hist + nchunk * D.R;
+            ring_base = ring_c + D.R;
+            k_bulk_hist<<<(unsigned)nchunk, 512, 0, st>>>(D, S, s, n, experts, ringof, hist);
+            k_bulk_offsets<<<1, 256, 0, st>>>(D, (int)nchunk, hist, ring_c, ring_base);
+            k_bulk_rank<<<(unsigned)nchunk, 512, 0, st>>>(D, n, ringof, hist, ring_base, list);
+        }
+        k_bulk_ring<<<D.R, 512, rsm, st>>>(D, S, s, T, experts, saliency, dst, counters, use_smem, list, ring_c,
+                                           ring_base);
     }
     const size_t psmem = (size_t)((D.entry_bytes + 15) & ~15) + sizeof(float) * (size_t)D.d;
     if (psmem > 48 * 1024)

@@ -390,10 +390,12 @@ void launch_finish_merge(const Dims& D, const Cfg& C, const State& S, const Exch
 void launch_foldback(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);  // + feedback
 void launch_feedback(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);
 // bulk store build of a prefill (engine_kernels.cu); dst [T*k] int64 scratch,
-// proj [2][T][dp] + [H][r] fp32 (LowRank/LoRAPlus), counters [2 + Gl]
+// proj [2][T][dp] + [H][r] fp32 (LowRank/LoRAPlus), counters [2 + Gl],
+// sort_buf bulk_sort_ints(D, T) int32 for the ring counting sort (or null)
+size_t bulk_sort_ints(const Dims& D, int64_t T);
 int bulk_insert(const Dims& D, const State& S, int s, int64_t T, const void* k, const void* v,
                 const int32_t* experts, const double* saliency, int64_t* dst, float* proj,
-                unsigned long long* counters, int use_tc, cudaStream_t st);
+                unsigned long long* counters, int use_tc, cudaStream_t st, int32_t* sort_buf);
 // tcgen05 projection GEMM (bulk_tc.cu); nonzero when the shape is unsupported
 int launch_bulk_project_tc(const Dims& D, const State& S, int64_t T, const void* k, const void* v, float* proj,
                            float* bias_scratch, cudaStream_t st);
