@@ -2819,6 +2819,37 @@ __global__ void k_bulk_payload(Dims D, State S, int64_t T, const void* __restric
     bool any = false;
     for (int j = 0; j < D.k; ++j) any |= dst[t * D.k + j] >= 0;
     if (!any) return;
+    // direct paths (no shared-memory staging): identity rows and bf16 low-rank
+    // projections are written straight to every destination entry
+    const int esz = D.kv_dtype == PIKV_DTYPE_BF16 ? 2 : 4;
+    if (D.codec == PIKV_CODEC_IDENTITY && (D.d * esz) % 16 == 0 && D.payload_bytes == D.d * esz) {
+        const int nv = D.d * esz / 16;
+        const uint4* ks = (const uint4*)((const uint8_t*)k + t * D.d * esz);
+        const uint4* vs = (const uint4*)((const uint8_t*)v + t * D.d * esz);
+        for (int i = tid; i < 2 * nv; i += blockDim.x) {
+            const uint4 w = i < nv ? ks[i] : vs[i - nv];
+            for (int j = 0; j < D.k; ++j) {
+                const int64_t de = dst[t * D.k + j];
+                if (de >= 0) ((uint4*)(S.pool + de * (int64_t)D.entry_bytes))[i] = w;
+            }
+        }
+        return;
+    }
+    if ((D.codec == PIKV_CODEC_LOWRANK || D.codec == PIKV_CODEC_LORAPLUS) && D.kv_dtype == PIKV_DTYPE_BF16 &&
+        D.dp % 4 == 0 && D.payload_bytes == D.dp * 2) {
+        const int n4 = D.dp / 4;
+        for (int i = tid; i < 2 * n4; i += blockDim.x) {
+            const int row = i / n4, o4 = i % n4;
+            const float4 f = ((const float4*)(proj + ((int64_t)row * T + t) * D.dp))[o4];
+            const uint2 b = make_uint2((uint32_t)f32_to_bf16_rne(f.x) | ((uint32_t)f32_to_bf16_rne(f.y) << 16),
+                                       (uint32_t)f32_to_bf16_rne(f.z) | ((uint32_t)f32_to_bf16_rne(f.w) << 16));
+            for (int j = 0; j < D.k; ++j) {
+                const int64_t de = dst[t * D.k + j];
+                if (de >= 0) ((uint2*)(S.pool + de * (int64_t)D.entry_bytes + (int64_t)row * D.payload_bytes))[o4] = b;
+            }
+        }
+        return;
+    }
     float* tmp = (float*)(sm_entry + ((D.entry_bytes + 15) & ~15));
     const int pay = D.payload_bytes;
     float* ksc = (float*)(sm_entry + 2 * pay);
@@ -2843,7 +2874,6 @@ __global__ void k_bulk_payload(Dims D, State S, int64_t T, const void* __restric
         }
     } else {
         // encode_row reads row `s` of a [.][d] input: pass the token's row
-        const int esz = D.kv_dtype == PIKV_DTYPE_BF16 ? 2 : 4;
         encode_row(D, S, (const uint8_t*)k + t * D.d * esz, 0, sm_entry, ksc, tmp, 0);
         encode_row(D, S, (const uint8_t*)v + t * D.d * esz, 0, sm_entry + pay, vsc, tmp, 1);
     }

@@ -1,0 +1,4 @@
+set -x
+timeout 900 python -m pytest tests/test_bulk_gpu.py tests/test_replay_gpu.py -x -q > gpurun_out/bulk_tests.log 2>&1; echo BT $?
+timeout 300 python profiles/microbench/bulk_bench.py 32768 > gpurun_out/bulk_pl.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv -k regex:"k_bulk|k_basis" -c 8 --log-file gpurun_out/bulk_ll6.csv python profiles/microbench/bulk_bench.py 32768 > gpurun_out/bulk_ll6.log 2>&1
