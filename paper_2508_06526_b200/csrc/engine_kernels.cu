@@ -46,7 +46,7 @@ constexpr int kMaxCluster = 8;  // k_control CTAs per stream
 __device__ __forceinline__ void route_select(const Dims& D, const Cfg& C, const State& S, int s,
                                              double* sm_logit, bool* sm_flag, int* sm_pool,
                                              double* load, uint64_t* usage, const uint64_t* miss,
-                                             const double* bias, int* sel);
+                                             const double* bias, int* sel, const uint64_t* pre, int* errf);
 
 constexpr int kRouteCHMax = 256;  // columns per stage (reduced so E rows x stages fit)
 constexpr int kRouteStages = 5;
@@ -87,6 +87,10 @@ __device__ __forceinline__ const int* route_body(const Dims& D, const Cfg& C, co
         sm_miss[e] = S.miss[(int64_t)s * D.E + e];
         sm_bias[e] = S.bias[(int64_t)s * D.E + e];
     }
+    // the selection's scalar state, fetched while the logit chains run
+    __shared__ uint64_t sm_pre[2];  // total_usage, rstep
+    __shared__ int sm_errf;         // set by route_select (NaN logits)
+    if (tid == 0) sm_pre[0] = S.total_usage[s], sm_pre[1] = S.rstep[s], sm_errf = 0;
     const bool dbg = D.dbg_ctl && s == 0 && tid == 0 && S.dbg;  // PIKV_DEBUG_CTL timestamps
     if (dbg) S.dbg[0] = clock64();
     if (tid == 0) {
@@ -214,9 +218,9 @@ __device__ __forceinline__ const int* route_body(const Dims& D, const Cfg& C, co
     if (dbg) S.dbg[2] = clock64();
     if (dbg) S.dbg[3] = clock64();
     if (tid < 32) route_select(D, C, S, s, sm_logit, sm_flag, sm_pool, sm_load, sm_usage, sm_miss,
-                               sm_bias, sm_sel);
+                               sm_bias, sm_sel, sm_pre, &sm_errf);
     __syncthreads();
-    if (S.err[s]) return nullptr;
+    if (sm_errf) return nullptr;
     for (int e = tid; e < D.E; e += blockDim.x) S.load[(int64_t)s * D.E + e] = sm_load[e];
     for (int j = tid; j < D.k; j += blockDim.x) {
         S.usage[(int64_t)s * D.E + sm_sel[j]] = sm_usage[sm_sel[j]];
@@ -239,17 +243,16 @@ __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin) {
 __device__ __forceinline__ void route_select(const Dims& D, const Cfg& C, const State& S, int s,
                                              double* sm_logit, bool* sm_flag, int* sm_pool,
                                              double* load, uint64_t* usage, const uint64_t* miss,
-                                             const double* bias, int* sel) {
+                                             const double* bias, int* sel, const uint64_t* pre, int* errf) {
     const int lane = threadIdx.x & 31;
     const int E = D.E, k = D.k;
     double* gates = S.gates + (int64_t)s * k;
     double* lg = S.logits + (int64_t)s * E;
     const bool base = C.router_strategy == PIKV_ROUTER_BASE;
     __shared__ double sm_mean;
-    __shared__ uint64_t sm_tot;
-    if (lane == 0) sm_tot = S.total_usage[s];
+    const uint64_t sm_tot = pre[0];  // S.total_usage[s], prefetched
     if (base) {  // base_round_robin, router.cpp:107-118
-        const int64_t t = (int64_t)S.rstep[s];
+        const int64_t t = (int64_t)pre[1];  // S.rstep[s]
         for (int j = lane; j < k; j += 32) {
             sel[j] = (int)((t * C.stride + j) % E);
             gates[j] = __ddiv_rn(1.0, (double)k);
@@ -259,7 +262,7 @@ __device__ __forceinline__ void route_select(const Dims& D, const Cfg& C, const 
         bool nan_seen = false;
         for (int e = lane; e < E; e += 32) nan_seen |= isnan(sm_logit[e]);
         if (__any_sync(0xffffffffu, nan_seen)) {  // router.cpp:131-133
-            if (lane == 0) S.err[s] = PIKV_ERR_NUMERICAL;
+            if (lane == 0) S.err[s] = PIKV_ERR_NUMERICAL, *errf = 1;
             return;
         }
         if (C.router_strategy == PIKV_ROUTER_LOAD_BALANCED && lane == 0) {
@@ -378,7 +381,7 @@ __device__ __forceinline__ void route_select(const Dims& D, const Cfg& C, const 
     for (int j = lane; j < k; j += 32) usage[sel[j]] += 1;
     if (lane == 0) {
         S.total_usage[s] = sm_tot + (uint64_t)k;
-        S.rstep[s] += 1;
+        S.rstep[s] = pre[1] + 1;
     }
     // candidate local rings for retrieval (ascending ring id)
     int nc = 0;
