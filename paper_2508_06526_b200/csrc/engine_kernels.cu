@@ -359,15 +359,21 @@ __device__ __forceinline__ void route_select(const Dims& D, const Cfg& C, const 
             }
         }
         __syncwarp();
-        if (lane == 0) {  // gates = softmax(selected logits), mathops.cpp:11-30
+        {  // gates = softmax(selected logits), mathops.cpp:11-30: the exps and
+           // divisions on lanes j < k, the sum sequential in j order on lane 0
+            __shared__ double sm_g[kMaxK];
+            __shared__ double sm_gtot;
             double mx = sm_logit[sel[0]];
             for (int j = 0; j < k; ++j) mx = (mx < sm_logit[sel[j]]) ? sm_logit[sel[j]] : mx;
-            double tot2 = 0.0;
-            for (int j = 0; j < k; ++j) {
-                gates[j] = exp(__dsub_rn(sm_logit[sel[j]], mx));
-                tot2 = __dadd_rn(tot2, gates[j]);
+            for (int j = lane; j < k; j += 32) sm_g[j] = exp(__dsub_rn(sm_logit[sel[j]], mx));
+            __syncwarp();
+            if (lane == 0) {
+                double tot2 = 0.0;
+                for (int j = 0; j < k; ++j) tot2 = __dadd_rn(tot2, sm_g[j]);
+                sm_gtot = tot2;
             }
-            for (int j = 0; j < k; ++j) gates[j] = __ddiv_rn(gates[j], tot2);
+            __syncwarp();
+            for (int j = lane; j < k; j += 32) gates[j] = __ddiv_rn(sm_g[j], sm_gtot);
         }
     }
     __syncwarp();
