@@ -406,16 +406,23 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void*
         : "memory");
 }
 
-// TST: the epilogue stores through TMA (r == NP, a multiple of 32: each warp's
-// 32 accumulator rows go to a SWIZZLE_128B smem box per 32 columns, one
-// cp.async.bulk.tensor store each; rows beyond T are clipped by the unit)
-template <int NP, bool TST>
+// MODE 0: the epilogue stores the fp32 projections with thread stores; 1:
+// through TMA (r == NP, a multiple of 32: each warp's 32 accumulator rows go
+// to a SWIZZLE_128B smem box per 32 columns, one cp.async.bulk.tensor store
+// each; rows beyond T are clipped by the unit); 2: fused with the bulk
+// payload -- each row is rounded to bf16 and written straight into the KV
+// pool entries of its token's experts (dst from the ring placement), so the
+// fp32 projections never go to HBM
+template <int NP, int MODE>
 __global__ void __launch_bounds__(128) k_bulk_project_tc3(const __grid_constant__ CUtensorMap map_k,
                                                           const __grid_constant__ CUtensorMap map_v,
                                                           const __grid_constant__ CUtensorMap map_o, Dims D,
                                                           int64_t T, const uint16_t* __restrict__ bhl,
                                                           float* __restrict__ proj,
-                                                          const float* __restrict__ bias_proj) {
+                                                          const float* __restrict__ bias_proj,
+                                                          const int64_t* __restrict__ dst,
+                                                          uint8_t* __restrict__ pool) {
+    constexpr bool TST = MODE == 1;
     extern __shared__ __align__(1024) uint8_t sm3[];
     constexpr int HD = 128, KC = 16;
     constexpr uint32_t A_BYTES = (uint32_t)kTcM * HD * 2, B_BYTES = (uint32_t)NP * HD * 2;
@@ -463,7 +470,32 @@ __global__ void __launch_bounds__(128) k_bulk_project_tc3(const __grid_constant_
     auto drain = [&](int pb, int64_t tile) {
         float accv[NP];
         tmem_ld_rows<NP>(tmem + (uint32_t)(pb * NACC) + ((uint32_t)(warp * 32) << 16), accv);
-        if constexpr (TST) {
+        if constexpr (MODE == 2) {
+            const int64_t g = tile * kTcM + warp * 32 + lane;  // this lane's token row
+            if (g < T) {
+                uint4 pk[NP / 8];
+#pragma unroll
+                for (int q = 0; q < NP / 8; ++q) {
+                    uint32_t w[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int c = q * 8 + 2 * u;
+                        const float a = accv[c] - (bias_proj ? bias_proj[h * NP + c] : 0.f);
+                        const float b = accv[c + 1] - (bias_proj ? bias_proj[h * NP + c + 1] : 0.f);
+                        w[u] = (uint32_t)f32_to_bf16_rne(a) | ((uint32_t)f32_to_bf16_rne(b) << 16);
+                    }
+                    pk[q] = make_uint4(w[0], w[1], w[2], w[3]);
+                }
+                for (int j = 0; j < D.k; ++j) {
+                    const int64_t de = dst[g * D.k + j];
+                    if (de < 0) continue;
+                    uint4* o = (uint4*)(pool + de * (int64_t)D.entry_bytes + (int64_t)row * D.payload_bytes +
+                                        (int64_t)h * NP * 2);
+#pragma unroll
+                    for (int q = 0; q < NP / 8; ++q) o[q] = pk[q];
+                }
+            }
+        } else if constexpr (TST) {
             if (bias_proj) {
 #pragma unroll
                 for (int j = 0; j < NP; ++j) accv[j] -= bias_proj[h * NP + j];
@@ -595,12 +627,14 @@ bool make_out_map(CUtensorMap* m, float* proj, int64_t T, int dp) {
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int NP, bool TST>
+template <int NP, int MODE>
 int launch_tc3(const Dims& D, int64_t T, const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mo,
-               const uint16_t* bhl, float* proj, const float* bias_proj, cudaStream_t st) {
+               const uint16_t* bhl, float* proj, const float* bias_proj, cudaStream_t st,
+               const int64_t* dst = nullptr, uint8_t* pool = nullptr) {
+    constexpr bool TST = MODE == 1;
     const size_t smem = 1024 + 2 * (size_t)kTcM * 128 * 2 + 2 * (size_t)NP * 128 * 2 + 64 +
                         (TST ? (size_t)4 * (NP / 32) * 4096 : sizeof(float) * 4 * 32 * (NP + 1));
-    cudaFuncSetAttribute(k_bulk_project_tc3<NP, TST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_bulk_project_tc3<NP, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int64_t ntiles = (T + kTcM - 1) / kTcM;
     int sms = 148, smem_sm = 228 * 1024;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -610,14 +644,14 @@ int launch_tc3(const Dims& D, int64_t T, const CUtensorMap& mk, const CUtensorMa
     int64_t per = (int64_t)occ * sms / (2LL * D.H);
     if (per > ntiles) per = ntiles;
     if (per < 1) per = 1;
-    k_bulk_project_tc3<NP, TST><<<dim3((unsigned)per, D.H, 2), 128, smem, st>>>(mk, mv, mo, D, T, bhl, proj,
-                                                                                bias_proj);
-    return cudaGetLastError() == cudaSuccess ? 0 : 1;
+    k_bulk_project_tc3<NP, MODE><<<dim3((unsigned)per, D.H, 2), 128, smem, st>>>(mk, mv, mo, D, T, bhl, proj,
+                                                                                 bias_proj, dst, pool);
+    return cudaGetLastError() == cudaSuccess ? (MODE == 2 ? 2 : 0) : 1;
 }
 
 template <int NP>
 int launch_np(const Dims& D, const State& S, int64_t T, const void* k, const void* v, float* proj,
-              const float* bias_proj, float* scratch_b, cudaStream_t st) {
+              const float* bias_proj, float* scratch_b, cudaStream_t st, const int64_t* fuse_dst) {
     const int hd = D.d / D.H;
     const bool f32in = D.kv_dtype != PIKV_DTYPE_BF16;
     const char* tv = std::getenv("PIKV_BULK_TMA");  // A/B: 0 = register-staged tc2
@@ -628,11 +662,13 @@ int launch_np(const Dims& D, const State& S, int64_t T, const void* k, const voi
         k_basis_split<NP><<<64, 256, 0, st>>>(D, S, bhl);
         const char* ts = std::getenv("PIKV_BULK_TSTORE");  // A/B: 0 = thread stores
         CUtensorMap mo;
+        if (fuse_dst && D.dph == NP && D.payload_bytes == D.dp * 2)  // fused payload (returns 2)
+            return launch_tc3<NP, 2>(D, T, mk, mv, mk, bhl, proj, bias_proj, st, fuse_dst, S.pool);
         if constexpr (NP % 32 == 0) {
             if (D.dph == NP && !(ts && ts[0] == '0') && make_out_map(&mo, proj, T, D.dp))
-                return launch_tc3<NP, true>(D, T, mk, mv, mo, bhl, proj, bias_proj, st);
+                return launch_tc3<NP, 1>(D, T, mk, mv, mo, bhl, proj, bias_proj, st);
         }
-        return launch_tc3<NP, false>(D, T, mk, mv, mk, bhl, proj, bias_proj, st);
+        return launch_tc3<NP, 0>(D, T, mk, mv, mk, bhl, proj, bias_proj, st);
     }
     if (!f32in && hd == 128 && scratch_b) {  // pipelined persistent kernel
         uint16_t* bhl = (uint16_t*)scratch_b;
@@ -664,7 +700,7 @@ int launch_np(const Dims& D, const State& S, int64_t T, const void* k, const voi
 }  // namespace
 
 int launch_bulk_project_tc(const Dims& D, const State& S, int64_t T, const void* k, const void* v, float* proj,
-                           float* bias_scratch, cudaStream_t st) {
+                           float* bias_scratch, cudaStream_t st, const int64_t* fuse_dst) {
     const int hd = D.d / D.H, r = D.dph;
     if (hd % 16 != 0 || r < 1 || r > 64 || T <= 0) return 1;
     // scratch: [H][r] bias B^T, then the pre-split basis (H x 2 x NP x hd bf16)
@@ -675,9 +711,9 @@ int launch_bulk_project_tc(const Dims& D, const State& S, int64_t T, const void*
     }
     float* bsplit = bias_scratch + ((D.H * r + 63) & ~63);
     int rc;
-    if (r <= 16) rc = launch_np<16>(D, S, T, k, v, proj, bias_proj, bsplit, st);
-    else if (r <= 32) rc = launch_np<32>(D, S, T, k, v, proj, bias_proj, bsplit, st);
-    else rc = launch_np<64>(D, S, T, k, v, proj, bias_proj, bsplit, st);
+    if (r <= 16) rc = launch_np<16>(D, S, T, k, v, proj, bias_proj, bsplit, st, fuse_dst);
+    else if (r <= 32) rc = launch_np<32>(D, S, T, k, v, proj, bias_proj, bsplit, st, fuse_dst);
+    else rc = launch_np<64>(D, S, T, k, v, proj, bias_proj, bsplit, st, fuse_dst);
     return rc;
 }
 

@@ -2941,17 +2941,8 @@ int bulk_insert(const Dims& D, const State& S, int s, int64_t T, const void* k, 
                 unsigned long long* counters, int use_tc, cudaStream_t st, int32_t* sort_buf) {
     cudaMemsetAsync(counters, 0, sizeof(unsigned long long) * (2 + D.Gl), st);
     cudaMemsetAsync(dst, 0xff, sizeof(int64_t) * (size_t)(T * D.k), st);  // -1: not stored here
-    if ((D.codec == PIKV_CODEC_LOWRANK || D.codec == PIKV_CODEC_LORAPLUS) && T > 0) {
-        const bool tc_ok = use_tc && launch_bulk_project_tc(D, S, T, k, v, proj, proj + 2 * T * D.dp, st) == 0;
-        if (!tc_ok && use_tc == 2) return (int)cudaErrorNotSupported;  // tensor cores required
-        if (!tc_ok) {
-            const int hd = D.d / D.H;
-            const size_t smem = sizeof(float) * (size_t)D.dph * hd;
-            if (smem > 48 * 1024)
-                cudaFuncSetAttribute(k_bulk_project_fma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            k_bulk_project_fma<<<dim3(64, D.H, 2), 256, smem, st>>>(D, S, T, k, v, proj);
-        }
-    }
+    // ring placement first: it fixes every entry's pool slot (dst), so the
+    // tcgen05 projection can write its bf16 rows straight into the entries
     if (D.R > 0) {
         size_t rsm = (size_t)D.ppr_sched * 24 + (size_t)D.ppr * 4;  // page-record accumulators
         const int use_smem = rsm <= 160 * 1024;
@@ -2972,10 +2963,28 @@ int bulk_insert(const Dims& D, const State& S, int s, int64_t T, const void* k, 
         k_bulk_ring<<<D.R, 512, rsm, st>>>(D, S, s, T, experts, saliency, dst, counters, use_smem, list, ring_c,
                                            ring_base);
     }
+    bool fused = false;
+    if ((D.codec == PIKV_CODEC_LOWRANK || D.codec == PIKV_CODEC_LORAPLUS) && T > 0) {
+        const char* fz = std::getenv("PIKV_BULK_FUSE");  // A/B: 0 = fp32 projections + payload kernel
+        const bool want_fuse = !(fz && fz[0] == '0');
+        const int rc = use_tc ? launch_bulk_project_tc(D, S, T, k, v, proj, proj + 2 * T * D.dp, st,
+                                                       want_fuse ? dst : nullptr)
+                              : 1;
+        fused = rc == 2;
+        const bool tc_ok = rc == 0 || rc == 2;
+        if (!tc_ok && use_tc == 2) return (int)cudaErrorNotSupported;  // tensor cores required
+        if (!tc_ok) {
+            const int hd = D.d / D.H;
+            const size_t smem = sizeof(float) * (size_t)D.dph * hd;
+            if (smem > 48 * 1024)
+                cudaFuncSetAttribute(k_bulk_project_fma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            k_bulk_project_fma<<<dim3(64, D.H, 2), 256, smem, st>>>(D, S, T, k, v, proj);
+        }
+    }
     const size_t psmem = (size_t)((D.entry_bytes + 15) & ~15) + sizeof(float) * (size_t)D.d;
     if (psmem > 48 * 1024)
         cudaFuncSetAttribute(k_bulk_payload, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
-    if (T > 0) k_bulk_payload<<<(unsigned)T, 256, psmem, st>>>(D, S, T, k, v, proj, dst);
+    if (T > 0 && !fused) k_bulk_payload<<<(unsigned)T, 256, psmem, st>>>(D, S, T, k, v, proj, dst);
     k_bulk_finish<<<1, 32, 0, st>>>(D, S, s, T, counters);
     return (int)cudaGetLastError();
 }

@@ -397,8 +397,10 @@ int bulk_insert(const Dims& D, const State& S, int s, int64_t T, const void* k, 
                 const int32_t* experts, const double* saliency, int64_t* dst, float* proj,
                 unsigned long long* counters, int use_tc, cudaStream_t st, int32_t* sort_buf);
 // tcgen05 projection GEMM (bulk_tc.cu); nonzero when the shape is unsupported
+// fuse_dst != null: may write the bf16 projections straight into the pool
+// entries dst (returns 2 then; 0 = fp32 projections in proj; 1 = unsupported)
 int launch_bulk_project_tc(const Dims& D, const State& S, int64_t T, const void* k, const void* v, float* proj,
-                           float* bias_scratch, cudaStream_t st);
+                           float* bias_scratch, cudaStream_t st, const int64_t* fuse_dst = nullptr);
 int encode_chunk(const Dims& D, int nb);
 void launch_encode(const Dims& D, const double* wt, const double* emb, double* q64, void* kout, void* vout,
                    cudaStream_t st);  // QueryEncoder (pipeline.cpp:29-57) for all streams

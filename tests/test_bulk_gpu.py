@@ -156,8 +156,9 @@ def test_bulk_projection_tensor_cores_match_cuda_cores(monkeypatch, codec, dtype
                                                ("LowRank", 256, 2, 64, 260)])
 def test_bulk_projection_tma_matches_register_staged(monkeypatch, codec, d, H, rank, T):
     """The TMA-fed tcgen05 projection (A tiles by cp.async.bulk.tensor into
-    SWIZZLE_128B stages; ranks 32 / 64 also store through TMA, LoRAPlus bias
-    subtracted before the store) issues the same MMAs in the same order as the
+    SWIZZLE_128B stages; by default its epilogue rounds each row to bf16 and
+    writes it straight into the token's pool entries, LoRAPlus bias subtracted
+    first) issues the same MMAs in the same order as the
     register-staged kernel (PIKV_BULK_TMA=0), so decode over the bulk-built
     store is bit-identical; d = 32 x 128 gives every CTA several tiles (the
     persistent loop, both ring stages) and a partial last tile."""
