@@ -380,7 +380,8 @@ int pikv_group_step(pikv_group* grp, const void* q, const void* k, const void* v
 int pikv_group_join(pikv_group* grp);
 int pikv_group_sync(pikv_group* grp);
 /* Attention timing: when on, every submit brackets its attention kernel with
- * CUDA events; *ms = summed attention time since the last read, *n = count. */
+ * CUDA events; *ms = summed attention time since the last read, *n = count
+ * (at most 8192 launches per micro-batch are kept between reads). */
 int pikv_group_set_timing(pikv_group* grp, int32_t on);
 int pikv_group_read_timing(pikv_group* grp, double* ms, int32_t* n);
 
