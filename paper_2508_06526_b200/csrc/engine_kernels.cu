@@ -2195,12 +2195,31 @@ __global__ void k_combine(Dims D, Cfg C, State S, ExchangeLayout X, float* __res
     __syncthreads();
     L = 0.f;
     for (int w = 0; w < nwarp; ++w) L += red[w];
-    for (int o = tid; o < D.dph; o += blockDim.x) {
+    // o: G groups of dph threads split the items (group g takes i = g, g+G, ...),
+    // summed in group order through shared memory -- many items per stream
+    // (small batches) no longer serialise on one thread per output
+    const int G = (D.dph > 0 && (int)blockDim.x % D.dph == 0) ? (int)blockDim.x / D.dph : 1;
+    float* red_o = sm_f + D.item_cap;  // [G][dph]
+    if (G > 1) {
+        const int g = tid / D.dph, o = tid % D.dph;
         float acc = 0.f;
         const float* po = S.part_o + ((int64_t)w0 * D.H + h) * D.dph + o;
         const int64_t stride = (int64_t)D.H * D.dph;
+#pragma unroll 4
+        for (int i = g; i < nw; i += G) acc = fmaf(po[i * stride], sm_f[i], acc);
+        red_o[g * D.dph + o] = acc;
+        __syncthreads();
+    }
+    for (int o = tid; o < D.dph; o += blockDim.x) {
+        float acc = 0.f;
+        if (G > 1) {
+            for (int g = 0; g < G; ++g) acc += red_o[g * D.dph + o];
+        } else {
+            const float* po = S.part_o + ((int64_t)w0 * D.H + h) * D.dph + o;
+            const int64_t stride = (int64_t)D.H * D.dph;
 #pragma unroll 8
-        for (int i = 0; i < nw; ++i) acc = fmaf(po[i * stride], sm_f[i], acc);
+            for (int i = 0; i < nw; ++i) acc = fmaf(po[i * stride], sm_f[i], acc);
+        }
         if (direct) {
             if (y && ok) y[(int64_t)s * D.dp + h * D.dph + o] = L > 0.f ? acc / L : 0.f;
         } else {
@@ -2229,9 +2248,11 @@ __global__ void k_combine(Dims D, Cfg C, State S, ExchangeLayout X, float* __res
 
 void launch_combine(const Dims& D, const Cfg& C, const State& S, const ExchangeLayout& X, float* y,
                     int direct, int attended, cudaStream_t st) {
-    const int threads = D.dph >= 128 ? 128 : (D.dph >= 64 ? 64 : 32);
-    launch_pdl(k_combine, dim3(D.B, D.H), dim3(threads), sizeof(float) * (size_t)D.item_cap, st, D, C, S, X, y,
-               direct, attended);
+    // dph threads per item group, up to 4 groups (512 threads)
+    int threads = D.dph >= 128 ? 128 : (D.dph >= 64 ? 64 : 32);
+    if (D.dph <= 128 && 128 % D.dph == 0) threads = std::max(32, std::min(512, 4 * D.dph));
+    const size_t smem = sizeof(float) * ((size_t)D.item_cap + (size_t)threads);
+    launch_pdl(k_combine, dim3(D.B, D.H), dim3(threads), smem, st, D, C, S, X, y, direct, attended);
 }
 
 // ===========================================================================
