@@ -472,6 +472,10 @@ typedef struct po_slot {
     int32_t expert;
     uint64_t insert_step, last_access, freq;
     double attn_mass;
+    /* per_layer_scores non-empty: the TokenInput carried layer saliency
+     * (pipeline.cpp:307 folds only into non-empty vectors; an empty vector
+     * scores 0 under Duo, scheduler.cpp:222-226) */
+    int32_t has_layers;
 } po_slot;
 
 struct po_engine {
@@ -479,7 +483,13 @@ struct po_engine {
     int H, hd, dp, dph; /* heads, head dim, stored width d', stored per head */
     int spd, nrings;
     po_slot* slots;     /* [nrings][S] */
-    double* payload;    /* [nrings][S][2][dp]: K then V, as attended (dequantized) */
+    /* K then V of each slot as attended (dequantized), [2][dp] floats per slot
+     * in chunks of PO_CHUNK slots allocated on first write, so host memory
+     * follows the slots ever written, not nrings * S (full-context parity
+     * runs).  float is exact: every stored value is an f32/bf16-rounded input,
+     * a dtype-rounded projection or an f32 dequantized code. */
+    float** payload;
+    size_t n_chunks;
     double* layers;     /* [nrings][S][n_layers] */
     int* head;
     int* live;
@@ -501,6 +511,18 @@ struct po_engine {
     double* stage_k;
     double* stage_v;
 };
+
+#define PO_CHUNK 64
+/* K/V floats of slot gi (allocating its chunk when `write`). */
+static float* slot_payload(po_engine* e, size_t gi, int write) {
+    float** ch = &e->payload[gi / PO_CHUNK];
+    if (!*ch) {
+        if (!write) abort(); /* a live slot was never written */
+        *ch = (float*)calloc((size_t)PO_CHUNK * 2 * (size_t)e->dp, sizeof(float));
+        if (!*ch) abort();
+    }
+    return *ch + (gi % PO_CHUNK) * 2 * (size_t)e->dp;
+}
 
 static int model_validate(const pikv_config* c) { /* config.hpp:42-54 */
     if (c->d < 1) return PIKV_ERR_INVALID_CONFIG;
@@ -570,7 +592,8 @@ po_engine* po_engine_create(const pikv_config* c, const double* w_r, const doubl
     e->nrings = c->G * spd;
     size_t ns = (size_t)e->nrings * (size_t)c->S;
     e->slots = (po_slot*)calloc(ns, sizeof(po_slot));
-    e->payload = (double*)calloc(ns * 2 * (size_t)e->dp, sizeof(double));
+    e->n_chunks = (ns + PO_CHUNK - 1) / PO_CHUNK;
+    e->payload = (float**)calloc(e->n_chunks, sizeof(float*));
     e->layers = (double*)calloc(ns * (size_t)(c->n_layers > 0 ? c->n_layers : 1), sizeof(double));
     e->head = (int*)calloc((size_t)e->nrings, sizeof(int));
     e->live = (int*)calloc((size_t)e->nrings, sizeof(int));
@@ -602,6 +625,8 @@ po_engine* po_engine_create(const pikv_config* c, const double* w_r, const doubl
 
 void po_engine_destroy(po_engine* e) {
     if (!e) return;
+    if (e->payload)
+        for (size_t i = 0; i < e->n_chunks; ++i) free(e->payload[i]);
     free(e->slots), free(e->payload), free(e->layers), free(e->head), free(e->live);
     free(e->seq), free(e->basis), free(e->bias), free(e->kept);
     free(e->stage_k), free(e->stage_v), free(e->enc_w);
@@ -787,8 +812,9 @@ static int store_insert(po_engine* e, int64_t token, int expert, const double* k
     s->last_access = e->now;
     s->freq = 0;
     s->attn_mass = 0.0;
-    memcpy(e->payload + gi * 2 * e->dp, k, sizeof(double) * (size_t)e->dp);
-    memcpy(e->payload + gi * 2 * e->dp + e->dp, v, sizeof(double) * (size_t)e->dp);
+    float* pp = slot_payload(e, gi, 1);
+    for (int i = 0; i < e->dp; ++i) pp[i] = (float)k[i], pp[e->dp + i] = (float)v[i];
+    s->has_layers = c->n_layers > 0 && saliency != NULL;
     if (c->n_layers > 0) {
         double* pl = e->layers + gi * (size_t)c->n_layers;
         for (int l = 0; l < c->n_layers; ++l) pl[l] = saliency ? saliency[l] : 0.0;
@@ -830,6 +856,7 @@ static double score_entry(const po_engine* e, const po_slot* s, size_t gi) {
         }
         case PIKV_SCHED_DUO: {
             double u = 0.0;
+            if (!s->has_layers) return u; /* empty per_layer_scores */
             const double* pl = e->layers + gi * (size_t)c->n_layers;
             for (int l = 0; l < c->n_layers; ++l) u += pl[l];
             return u;
@@ -1026,9 +1053,11 @@ static int engine_step_impl(po_engine* e, const double* q, const double* k, cons
         double* alpha = (double*)calloc((size_t)(nh > 0 ? nh : 1), sizeof(double));
         for (int h = 0; h < H; ++h) {
             for (int i = 0; i < nh; ++i) {
-                const double* p = e->payload + hits[i].gi * 2 * (size_t)e->dp;
-                memcpy(kbuf + (size_t)i * w, p + (size_t)h * w, sizeof(double) * (size_t)w);
-                memcpy(vbuf + (size_t)i * w, p + e->dp + (size_t)h * w, sizeof(double) * (size_t)w);
+                const float* p = slot_payload(e, hits[i].gi, 0);
+                for (int o = 0; o < w; ++o) {
+                    kbuf[(size_t)i * w + o] = (double)p[(size_t)h * w + o];
+                    vbuf[(size_t)i * w + o] = (double)p[e->dp + (size_t)h * w + o];
+                }
             }
             po_attention(qa + (size_t)h * w, kbuf, vbuf, nh, w, out->y + (size_t)h * w, wts);
             for (int i = 0; i < nh; ++i) alpha[i] += wts[i];
@@ -1038,7 +1067,7 @@ static int engine_step_impl(po_engine* e, const double* q, const double* k, cons
             double a = alpha[i] / H;
             po_slot* s = &e->slots[hits[i].gi];
             s->attn_mass += a;
-            if (c->n_layers > 0) e->layers[hits[i].gi * (size_t)c->n_layers + e->now % (uint64_t)c->n_layers] += a;
+            if (s->has_layers) e->layers[hits[i].gi * (size_t)c->n_layers + e->now % (uint64_t)c->n_layers] += a;
             if (i < out->att_cap) {
                 if (out->att_token) out->att_token[i] = s->token;
                 if (out->att_expert) out->att_expert[i] = s->expert;

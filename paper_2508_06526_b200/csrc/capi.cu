@@ -170,6 +170,15 @@ struct pikv_engine {
         for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.ge);
         graphs.clear();
     }
+    // every captured graph: the keyed cache and the pikv_step_host graph
+    // (kernels captured State by value, so new codec buffers need new graphs)
+    void invalidate() {
+        drop_graphs();
+        if (host_ge) cudaGraphExecDestroy(host_ge);
+        if (host_g) cudaGraphDestroy(host_g);
+        host_ge = nullptr, host_g = nullptr;
+        host_h2d = host_h2d_kv = host_d2h = nullptr;
+    }
     unsigned warmed_parts = 0;  // step parts run eagerly once (kernel attributes set)
     bool warmed = false;
     int64_t launches = 0;
@@ -442,6 +451,9 @@ static int validate(const pikv_config& c) {
         return fail(PIKV_ERR_INVALID_CONFIG, "codec rank must be in [1, head_dim]");
     if (c.n_layers < 0) return fail(PIKV_ERR_INVALID_CONFIG, "n_layers must be >= 0");
     if (c.d > 16384) return fail(PIKV_ERR_INVALID_CONFIG, "d must be <= 16384 (router stages q in smem)");
+    // k_foldback stages the per-(stream, head) global (m, l) in shared memory
+    if (8.0 * c.batch * c.n_heads + 4.0 * c.batch > 227.0 * 1024)
+        return fail(PIKV_ERR_INVALID_CONFIG, "batch x n_heads too large (fold-back: 8 B H + 4 B <= 227 KB)");
     if (128 + 8.0 * c.d + 5.0 * c.E * (32 * 8 + 16) > 200 * 1024)
         return fail(PIKV_ERR_INVALID_CONFIG, "router: E x d too large for the shared-memory W ring");
     return PIKV_OK;
@@ -635,6 +647,7 @@ static int engine_create(const pikv_config* cfg, int32_t cuda_device, int attend
     chk(S.freq = eng->alloc<uint64_t>(total_slots));
     chk(S.attn_mass = eng->alloc<double>(total_slots));
     chk(S.per_layer = eng->alloc<double>((size_t)total_slots * std::max(D.n_layers, 1)));
+    chk(S.has_pl = eng->alloc<uint8_t>(total_slots));
     chk(S.pool = eng->alloc<uint8_t>((size_t)D.pool_entries * D.entry_bytes));
     chk(S.page_live = eng->alloc<int32_t>(D.pool_pages));
     chk(S.free_stack = eng->alloc<int32_t>(D.pool_pages));
@@ -723,6 +736,7 @@ static int engine_create(const pikv_config* cfg, int32_t cuda_device, int attend
     CUDA_TRY(cudaMemsetAsync(S.page_table, 0xff, sizeof(int32_t) * rings * D.ppr, st));
     CUDA_TRY(cudaMemsetAsync(S.id, 0, sizeof(uint64_t) * total_slots, st));
     CUDA_TRY(cudaMemsetAsync(S.attn_mass, 0, sizeof(double) * total_slots, st));
+    CUDA_TRY(cudaMemsetAsync(S.has_pl, 0, total_slots, st));
     CUDA_TRY(cudaMemsetAsync(S.pr_cnt, 0, sizeof(int32_t) * rings * D.ppr_sched, st));
     CUDA_TRY(cudaMemsetAsync(S.pages_live, 0, sizeof(int32_t) * B * std::max(D.Gl, 1), st));
     CUDA_TRY(cudaMemsetAsync(S.pr_first, 0, sizeof(int32_t) * rings * D.ppr_sched, st));
@@ -801,7 +815,8 @@ int pikv_set_codec_host(pikv_engine* eng, const float* basis, const float* bias,
             if (kept[i] < 0 || kept[i] >= hd) return fail(PIKV_ERR_INVALID_ARGUMENT, "kept index out of range");
         eng->S.kept = (const int32_t*)up(kept, sizeof(int32_t) * (size_t)D.H * r);
     }
-    eng->drop_graphs();  // captured kernels hold the old pointers
+    cudaStreamSynchronize(eng->stream);
+    eng->invalidate();  // captured kernels hold the old pointers
     return PIKV_OK;
 }
 
@@ -1269,7 +1284,8 @@ int pikv_insert_bulk(pikv_engine* eng, int32_t stream, int64_t T, const void* k,
     cudaStream_t st = eng->stream;
     const bool proj = D.codec == PIKV_CODEC_LOWRANK || D.codec == PIKV_CODEC_LORAPLUS;
     const size_t n_dst = sizeof(int64_t) * (size_t)std::max<int64_t>(1, T * D.k);
-    const size_t n_ctr = sizeof(unsigned long long) * (2 + D.Gl);
+    // counters [2 + Gl], then the ring scratch of the two-phase placement [R][3]
+    const size_t n_ctr = sizeof(unsigned long long) * (2 + D.Gl + 3 * (size_t)std::max(D.R, 1));
     // projections [2][T][dp], then the tcgen05 path's bias B^T [H][r] and
     // pre-split basis [H][2][64][hd] bf16
     const size_t n_pr = proj ? sizeof(float) * (2 * (size_t)std::max<int64_t>(1, T) * D.dp +
@@ -1435,13 +1451,24 @@ int pikv_read_attended_host(pikv_engine* eng, int32_t stream, int64_t* token, in
     CUDA_TRY(cudaMemcpy(sc.data(), eng->S.scores + base[0] * D.H, sizeof(float) * m * D.H, cudaMemcpyDeviceToHost));
     CUDA_TRY(cudaMemcpy(gM.data(), eng->S.gM + stream * D.H, sizeof(float) * D.H, cudaMemcpyDeviceToHost));
     CUDA_TRY(cudaMemcpy(gL.data(), eng->S.gL + stream * D.H, sizeof(float) * D.H, cudaMemcpyDeviceToHost));
+    std::vector<int64_t> ht(m);
+    std::vector<int32_t> he(m);
+    {
+        uint8_t* buf = nullptr;
+        CUDA_TRY(cudaMalloc(&buf, 12 * (size_t)m));
+        launch_gather_slots(eng->S, eng->S.att_slot + base[0], m, (int64_t*)buf, (int32_t*)(buf + 8 * (size_t)m),
+                            eng->stream);
+        cudaError_t e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaMemcpyAsync(ht.data(), buf, 8 * (size_t)m, cudaMemcpyDeviceToHost, eng->stream);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(he.data(), buf + 8 * (size_t)m, 4 * (size_t)m, cudaMemcpyDeviceToHost, eng->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(eng->stream);
+        cudaFree(buf);
+        if (e != cudaSuccess) return fail(PIKV_ERR_CUDA, std::string("read_attended: ") + cudaGetErrorString(e));
+    }
     for (int i = 0; i < m; ++i) {
-        int64_t t;
-        int32_t e;
-        CUDA_TRY(cudaMemcpy(&t, eng->S.token + slot[i], sizeof(int64_t), cudaMemcpyDeviceToHost));
-        CUDA_TRY(cudaMemcpy(&e, eng->S.expert + slot[i], sizeof(int32_t), cudaMemcpyDeviceToHost));
-        if (token) token[i] = t;
-        if (expert) expert[i] = e;
+        if (token) token[i] = ht[i];
+        if (expert) expert[i] = he[i];
         if (alpha) {  // same expression as k_foldback
             double a = 0.0;
             for (int h = 0; h < D.H; ++h)
@@ -1747,6 +1774,9 @@ int pikv_group_submit(pikv_group* g, int32_t m, const void* q, const void* k, co
         } else {
             // y leaves for the host on a side stream as soon as the merge wrote
             // it, while the fold-back runs: the caller's wait returns earlier
+            // the merge rewrites out_y: order it after the previous step's D2H
+            // of out_y on the side stream (a no-op in the steady state)
+            if (!rc) CUDA_TRY(cudaStreamWaitEvent(st, g->y_done[m], 0));
             if (!rc) rc = run_step(e, dq, dk, dv, ds, dy, true, nullptr, kPartMerge);
             if (!rc) {
                 CUDA_TRY(cudaEventRecord(g->y_ready[m], st));

@@ -606,6 +606,40 @@ __device__ __forceinline__ void insert_book_seq(const Dims& D, const State& S, c
                                                 const double* __restrict__ saliency, int64_t* sm_dst, int* sm_n) {
     const uint64_t now = S.now[s];
     const int64_t token = (int64_t)now;
+    // pass 1: the pool pages the k inserts will need (the i-th insert of the
+    // step into a ring lands at head + i), reserved with one atomic before
+    // any store: an exhausted pool fails the insert with no partial state
+    // (pipeline.cpp:153-154)
+    int64_t rng[kMaxK], newp[kMaxK];
+    int nnew = 0;
+    for (int j = 0; j < D.k; ++j) {
+        const int e = sel ? sel[j] : S.experts[(int64_t)s * D.k + j];
+        const int raw = shard_raw(token, e, D.n_tok, D.n_exp, D.additive);
+        const int dev = raw % D.G;
+        rng[j] = -1;
+        if (dev % D.world != D.rank) continue;
+        const int64_t ring = ((int64_t)s * D.Gl + dev / D.world) * D.SPD + raw / D.G;
+        rng[j] = ring;
+        int off = 0;
+        for (int i = 0; i < j; ++i) off += rng[i] == ring;
+        const int slot = (S.head[ring] + off) % D.S;
+        if (off >= D.S || S.id[ring * D.S + slot] != 0) continue;  // displaces: no new page
+        const int64_t pidx = ring * D.ppr + slot / D.spg;
+        if (S.page_table[pidx] >= 0) continue;
+        bool seen = false;
+        for (int i = 0; i < nnew; ++i) seen |= newp[i] == pidx;
+        if (!seen) newp[nnew++] = pidx;
+    }
+    int pbase = 0;
+    if (nnew > 0) {
+        pbase = atomicSub(S.free_top, nnew) - nnew;
+        if (pbase < 0) {
+            atomicAdd(S.free_top, nnew);
+            S.err[s] = PIKV_ERR_OUT_OF_MEMORY;
+            *sm_n = 0;
+            return;
+        }
+    }
     int n = 0;
     for (int j = 0; j < D.k; ++j) {
         const int e = sel ? sel[j] : S.experts[(int64_t)s * D.k + j];
@@ -634,14 +668,8 @@ __device__ __forceinline__ void insert_book_seq(const Dims& D, const State& S, c
             S.st_overwrites[s] += 1;
         } else {
             S.live[ring] += 1;
-            if (page < 0) {
-                const int top = atomicSub(S.free_top, 1) - 1;
-                if (top < 0) {
-                    atomicAdd(S.free_top, 1);
-                    S.err[s] = PIKV_ERR_OUT_OF_MEMORY;
-                    break;
-                }
-                page = S.free_stack[top];
+            if (page < 0) {  // reserved in pass 1
+                page = S.free_stack[pbase++];
                 S.page_table[pidx] = page;
                 S.page_live[page] = 0;
             }
@@ -658,6 +686,7 @@ __device__ __forceinline__ void insert_book_seq(const Dims& D, const State& S, c
         S.attn_mass[gi] = 0.0;
         for (int l = 0; l < D.n_layers; ++l)
             S.per_layer[gi * D.n_layers + l] = saliency ? saliency[(int64_t)s * D.n_layers + l] : 0.0;
+        S.has_pl[gi] = D.n_layers > 0 && saliency != nullptr;
         S.head[ring] = (slot + 1) % D.S;
         S.st_inserts[s] += 1;
         sm_dst[n] = (int64_t)page * D.spg + slot % D.spg;
@@ -749,19 +778,31 @@ __device__ __forceinline__ void insert_book(const Dims& D, const State& S, const
         dsf -= ofr;
         if (drec == arec) acnt = dcnt, afirst = dfirst, asla = dsla, asf = dsf;
     }
-    // page allocation for a fresh slot (pool free stack)
-    bool oom = false, fresh_page = false;
-    if (act && !disp && page < 0) {
-        const int top = atomicSub(S.free_top, 1) - 1;
-        if (top < 0) {
-            atomicAdd(S.free_top, 1);
-            oom = true;
-        } else {
-            page = S.free_stack[top];
+    // page allocation for fresh slots: the step's new pages are reserved
+    // with one atomic, and an exhausted pool fails the whole insert before
+    // any store (no partial state, pipeline.cpp:153-154)
+    bool fresh_page = false;
+    {
+        const bool need = act && !disp && page < 0;
+        const unsigned nm = __ballot_sync(0xffffffffu, need);
+        int base = 0;
+        if (j == 0 && nm) {
+            const int c = __popc(nm);
+            base = atomicSub(S.free_top, c) - c;
+            if (base < 0) atomicAdd(S.free_top, c);
+        }
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (base < 0) {
+            if (j == 0) S.err[s] = PIKV_ERR_OUT_OF_MEMORY, *sm_n = 0;
+            __syncwarp();
+            return;
+        }
+        if (need) {
+            page = S.free_stack[base + __popc(nm & ((1u << j) - 1u))];
             fresh_page = true;
         }
     }
-    const bool ins = act && !oom;
+    const bool ins = act;
     // rec_append
     if (ins) {
         if (acnt == 0) {
@@ -810,6 +851,7 @@ __device__ __forceinline__ void insert_book(const Dims& D, const State& S, const
         S.attn_mass[gi] = 0.0;
         for (int l = 0; l < D.n_layers; ++l)
             S.per_layer[gi * D.n_layers + l] = saliency ? saliency[(int64_t)s * D.n_layers + l] : 0.0;
+        S.has_pl[gi] = D.n_layers > 0 && saliency != nullptr;
         S.head[ring] = (slot + 1) % D.S;
     }
     const unsigned dm = __ballot_sync(0xffffffffu, disp);
@@ -827,7 +869,6 @@ __device__ __forceinline__ void insert_book(const Dims& D, const State& S, const
         S.rec_ow[(int64_t)s * D.k + __popc(dm & ((1u << j) - 1u))] = rec;
     }
     if (ins) sm_dst[__popc(am & ((1u << j) - 1u))] = (int64_t)page * D.spg + slot % D.spg;
-    if (__any_sync(0xffffffffu, oom) && j == 0) S.err[s] = PIKV_ERR_OUT_OF_MEMORY;
     if (j == 0) {
         S.n_ow[s] = __popc(dm);
         S.st_overwrites[s] += (uint64_t)__popc(dm);
@@ -2391,7 +2432,7 @@ __global__ void k_foldback(Dims D, Cfg C, State S) {
         const double al = (double)a / (double)D.H;
         const int64_t gi = S.att_slot[i];
         S.attn_mass[gi] += al;
-        if (D.n_layers > 0) S.per_layer[gi * D.n_layers + (int64_t)(S.now[s] % (uint64_t)D.n_layers)] += al;
+        if (S.has_pl[gi]) S.per_layer[gi * D.n_layers + (int64_t)(S.now[s] % (uint64_t)D.n_layers)] += al;
     }
     // the last CTA to finish runs the per-stream feedback (now++ must follow
     // every fold-back that reads now)
@@ -2644,7 +2685,8 @@ __global__ void __launch_bounds__(512) k_bulk_ring(Dims D, State S, int s, int64
                                                    int64_t* __restrict__ dst, unsigned long long* counters,
                                                    int use_smem, const int32_t* __restrict__ list,
                                                    const int32_t* __restrict__ ring_c,
-                                                   const int32_t* __restrict__ ring_base) {
+                                                   const int32_t* __restrict__ ring_base, int phase,
+                                                   int64_t* __restrict__ ring_scr) {
     const int rl = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NT = blockDim.x;
     const int NW = NT >> 5;
     const int64_t ring = (int64_t)s * D.R + rl;
@@ -2660,47 +2702,61 @@ __global__ void __launch_bounds__(512) k_bulk_ring(Dims D, State S, int s, int64
     // token of entry e: 32-bit division when the bulk fits (always, in practice)
     const bool small = n < (1LL << 31);
     auto tok_of = [&](int64_t e) -> int64_t { return small ? (int64_t)((uint32_t)e / (uint32_t)D.k) : e / D.k; };
-    if (!list)
+    if (!list && phase == 0)
         for (int64_t e = tid; e < n; e += NT)
             mine += bulk_ring_of(D, (int64_t)(now0 + (uint64_t)tok_of(e)), experts[e]) == rl;
     int64_t tot;
     block_excl_scan(mine, wsum, &tot);
     if (list) tot = ring_c[rl];  // counted by the sort
+    if (phase == 1) tot = ring_scr[3 * rl];  // counted in phase 0
     if (tid == 0) sm_c = tot, sm_run = 0, sm_disp = 0;
     __syncthreads();
     const int64_t c = sm_c;  // c == 0: nothing placed, the ring still counts its live pages
     const int64_t first_surv = c > D.S ? c - D.S : 0;  // ring rank of the first survivor
+    const int64_t nsurv = c - first_surv;
+    const int64_t s0 = (head + first_surv) % D.S;  // survivor slots: cyclic [s0, s0 + nsurv)
+    // storage pages of the survivor slots that have no pool page yet, counted
+    // in phase 0 and taken in phase 1 from the range k_bulk_reserve reserved
+    // for this ring (an exhausted pool fails the bulk before any store)
+    auto needs_page = [&](int p) {
+        if (p >= D.ppr) return false;
+        bool touched = false;
+        for (int q = 0; q < D.spg && !touched; ++q) {
+            const int64_t slot = (int64_t)p * D.spg + q;
+            touched = ((slot - s0 + D.S) % D.S) < nsurv;
+        }
+        return touched && S.page_table[ring * D.ppr + p] < 0;
+    };
+    if (phase == 0) {
+        int64_t need = 0;
+        for (int p = tid; p < D.ppr; p += NT) need += needs_page(p);
+        int64_t tn;
+        block_excl_scan(need, wsum, &tn);
+        if (tid == 0) ring_scr[3 * rl] = c, ring_scr[3 * rl + 1] = tn;
+        return;
+    }
     // displaced previously-live entries: the first min(c, S) writes
     unsigned long long dl = 0;
     for (int64_t j = tid; j < (c < D.S ? c : D.S); j += NT)
         dl += S.id[ring * D.S + (head + j) % D.S] != 0;
     for (int o = 16; o; o >>= 1) dl += __shfl_xor_sync(0xffffffffu, dl, o);
     if (lane == 0) atomicAdd(&sm_disp, dl);
-    // storage pages of the survivor slots: allocate before any write
-    const int64_t nsurv = c - first_surv;
-    const int64_t s0 = (head + first_surv) % D.S;  // survivor slots: cyclic [s0, s0 + nsurv)
-    for (int p = tid; p < D.ppr; p += NT) {
-        bool touched = false;
-        for (int q = 0; q < D.spg && !touched; ++q) {
-            const int64_t slot = (int64_t)p * D.spg + q;
-            touched = ((slot - s0 + D.S) % D.S) < nsurv;
-        }
-        if (touched && S.page_table[ring * D.ppr + p] < 0) {
-            const int top = atomicSub(S.free_top, 1) - 1;
-            if (top < 0) {
-                atomicAdd(S.free_top, 1);
-                S.err[s] = PIKV_ERR_OUT_OF_MEMORY;
-            } else {
-                const int32_t page = S.free_stack[top];
-                S.page_table[ring * D.ppr + p] = page;
-            }
-        }
-    }
     __shared__ int sm_err;
-    __syncthreads();
     if (tid == 0) sm_err = S.err[s];
     __syncthreads();
-    if (sm_err) return;  // pool exhausted: the bulk insert fails (PIKV_ERR_OUT_OF_MEMORY)
+    if (sm_err) return;  // pool exhausted (k_bulk_reserve): nothing was stored
+    {
+        const int64_t pbase = ring_scr[3 * rl + 2];
+        int64_t taken = 0;
+        for (int p0 = 0; p0 < D.ppr; p0 += NT) {
+            const bool nd = needs_page(p0 + tid);
+            int64_t tn;
+            const int64_t idx = block_excl_scan(nd ? 1 : 0, wsum, &tn);
+            if (nd) S.page_table[ring * D.ppr + p0 + tid] = S.free_stack[pbase + taken + idx];
+            taken += tn;
+        }
+    }
+    __syncthreads();
     // place: entries in order, rank within the ring by one block scan per
     // chunk of PER consecutive entries per thread (was one scan per 512
     // entries with a serial warp prefix: 365 -> ~60 us at 32K tokens)
@@ -2723,6 +2779,7 @@ __global__ void __launch_bounds__(512) k_bulk_ring(Dims D, State S, int s, int64
         S.attn_mass[gi] = 0.0;
         for (int l = 0; l < D.n_layers; ++l)
             S.per_layer[gi * D.n_layers + l] = saliency ? saliency[t * D.n_layers + l] : 0.0;
+        S.has_pl[gi] = D.n_layers > 0 && saliency != nullptr;
         const int32_t page = S.page_table[ring * D.ppr + slot / D.spg];
         dst[e] = (int64_t)page * D.spg + slot % D.spg;
     }
@@ -2755,6 +2812,7 @@ __global__ void __launch_bounds__(512) k_bulk_ring(Dims D, State S, int s, int64
                 S.attn_mass[gi] = 0.0;
                 for (int l = 0; l < D.n_layers; ++l)
                     S.per_layer[gi * D.n_layers + l] = saliency ? saliency[t * D.n_layers + l] : 0.0;
+                S.has_pl[gi] = D.n_layers > 0 && saliency != nullptr;
                 const int32_t page = S.page_table[ring * D.ppr + slot / D.spg];
                 dst[e] = (int64_t)page * D.spg + slot % D.spg;
             } else {
@@ -2838,6 +2896,32 @@ __global__ void __launch_bounds__(512) k_bulk_ring(Dims D, State S, int s, int64
     }
 }
 
+// Between the two k_bulk_ring phases: reserve every ring's new pool pages
+// at once (ring_scr[3r + 1] needed -> ring_scr[3r + 2] first free-stack
+// index); an exhausted pool sets PIKV_ERR_OUT_OF_MEMORY before any store.
+__global__ void k_bulk_reserve(Dims D, State S, int s, int64_t* __restrict__ ring_scr) {
+    __shared__ int64_t wsum[32];
+    __shared__ int64_t sm_tot;
+    const int tid = threadIdx.x;
+    int64_t run = 0;
+    for (int r0 = 0; r0 < D.R; r0 += blockDim.x) {
+        const int r = r0 + tid;
+        const int64_t need = r < D.R ? ring_scr[3 * r + 1] : 0;
+        int64_t tn;
+        const int64_t ex = block_excl_scan(need, wsum, &tn);
+        if (r < D.R) ring_scr[3 * r + 2] = run + ex;  // offset, rebased below
+        run += tn;
+    }
+    if (tid == 0) sm_tot = run;
+    __syncthreads();
+    const int64_t tot = sm_tot;
+    const int top = *S.free_top;  // no concurrent allocation: the engine stream is serial
+    const bool oom = S.err[s] != 0 || tot > top;
+    if (tid == 0 && !oom) *S.free_top = top - (int)tot;
+    if (tid == 0 && oom && !S.err[s]) S.err[s] = PIKV_ERR_OUT_OF_MEMORY;
+    for (int r = tid; r < D.R && !oom; r += blockDim.x) ring_scr[3 * r + 2] += top - tot;
+}
+
 // (b) one CTA per token: encode its K and V once (codec of the engine; the
 //     low-rank projections come precomputed in proj [2][T][dp]) and copy the
 //     entry to every surviving destination of the token.
@@ -2919,7 +3003,7 @@ __global__ void k_bulk_payload(Dims D, State S, int64_t T, const void* __restric
 
 // (c) stream counters: ids, steps, store totals, live pages per device.
 __global__ void k_bulk_finish(Dims D, State S, int s, int64_t T, const unsigned long long* counters) {
-    if (threadIdx.x != 0) return;
+    if (threadIdx.x != 0 || S.err[s]) return;
     S.next_id[s] += (uint64_t)(T * D.k);
     S.now[s] += (uint64_t)T;
     S.st_inserts[s] += counters[0];
@@ -2981,8 +3065,12 @@ int bulk_insert(const Dims& D, const State& S, int s, int64_t T, const void* k, 
             k_bulk_offsets<<<1, 256, 0, st>>>(D, (int)nchunk, hist, ring_c, ring_base);
             k_bulk_rank<<<(unsigned)nchunk, 512, 0, st>>>(D, n, ringof, hist, ring_base, list);
         }
+        int64_t* ring_scr = (int64_t*)(counters + 2 + D.Gl);
+        k_bulk_ring<<<D.R, 512, 0, st>>>(D, S, s, T, experts, saliency, dst, counters, use_smem, list, ring_c,
+                                         ring_base, 0, ring_scr);
+        k_bulk_reserve<<<1, 256, 0, st>>>(D, S, s, ring_scr);
         k_bulk_ring<<<D.R, 512, rsm, st>>>(D, S, s, T, experts, saliency, dst, counters, use_smem, list, ring_c,
-                                           ring_base);
+                                           ring_base, 1, ring_scr);
     }
     bool fused = false;
     if ((D.codec == PIKV_CODEC_LOWRANK || D.codec == PIKV_CODEC_LORAPLUS) && T > 0) {
@@ -3086,6 +3174,20 @@ void launch_snapshot(const Dims& D, const State& S, int s, uint64_t now, const i
                      pikv_snapshot_record* out, int64_t n, cudaStream_t st) {
     if (D.R > 0) k_snapshot<<<D.R, 256, 0, st>>>(D, S, s, now, ring_off, out);
     if (n > 0) k_snapshot_ties<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(out, n);
+}
+
+// token / expert of a list of slots (pikv_read_attended_host)
+__global__ void k_gather_slots(State S, const int32_t* __restrict__ slot, int n, int64_t* __restrict__ token,
+                               int32_t* __restrict__ expert) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int32_t gi = slot[i];
+        token[i] = S.token[gi];
+        expert[i] = S.expert[gi];
+    }
+}
+void launch_gather_slots(const State& S, const int32_t* slot, int n, int64_t* token, int32_t* expert,
+                         cudaStream_t st) {
+    if (n > 0) k_gather_slots<<<(n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024, 256, 0, st>>>(S, slot, n, token, expert);
 }
 
 // ===========================================================================

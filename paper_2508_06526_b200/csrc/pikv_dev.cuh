@@ -114,6 +114,8 @@ struct State {
     uint64_t* freq;
     double* attn_mass;
     double* per_layer;
+    uint8_t* has_pl;  // per_layer_scores non-empty (the insert carried saliency;
+                      // pipeline.cpp:307, scheduler.cpp:222-226)
     // pool
     uint8_t* pool;
     int32_t* page_live;
@@ -240,6 +242,7 @@ __device__ __forceinline__ double score_entry(const Cfg& c, const State& st, int
         }
         case PIKV_SCHED_DUO: {
             double u = 0.0;
+            if (!st.has_pl[gi]) return u;  // empty per_layer_scores
             const double* pl = st.per_layer + gi * (int64_t)n_layers;
             for (int l = 0; l < n_layers; ++l) u = __dadd_rn(u, pl[l]);
             return u;
@@ -409,5 +412,8 @@ void launch_snapshot(const Dims& D, const State& S, int s, uint64_t now, const i
 void launch_synth(const Dims& D, void* q, void* k, void* v, uint64_t seed, uint64_t step,
                   cudaStream_t st);
 int attend_max_smem();
+// token / expert of n slots (global slot indices) -> out arrays (readback)
+void launch_gather_slots(const State& S, const int32_t* slot, int n, int64_t* token, int32_t* expert,
+                         cudaStream_t st);
 
 }  // namespace pikv_dev

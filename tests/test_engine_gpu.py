@@ -46,7 +46,7 @@ def rel_l2(a, b):
 
 
 def run_parity(cfg, T, seed, inject=True, basis=None, bias=None, kept=None, check_slots=True,
-               mutate=None, embed=False):
+               mutate=None, embed=False, no_saliency=False):
     B = cfg.batch
     eng = Engine(cfg)
     if basis is not None or bias is not None or kept is not None:
@@ -65,7 +65,7 @@ def run_parity(cfg, T, seed, inject=True, basis=None, bias=None, kept=None, chec
         q = np.stack([streams[s][0][t] for s in range(B)])
         k = np.stack([streams[s][1][t] for s in range(B)])
         v = np.stack([streams[s][2][t] for s in range(B)])
-        sal = None if cfg.n_layers == 0 else np.stack([streams[s][3][t] for s in range(B)])
+        sal = None if cfg.n_layers == 0 or no_saliency else np.stack([streams[s][3][t] for s in range(B)])
         before = [eng.slots(s) for s in range(B)] if inject else None
         if embed:  # Engine::step(TokenInput{embedding}): the encoder runs on the GPU
             y = eng.step_embed_host(q, sal)
