@@ -138,6 +138,21 @@ typedef struct pikv_evict_record {
     int32_t stream;
 } pikv_evict_record;
 
+/* One KV entry's identity and metadata: KVEntry (types.hpp:27-34) minus its
+ * key/value vectors, with EntryMeta (types.hpp:11-24) inlined.  id and
+ * shard_seq are assigned by the store on insert (kvstore.cpp:114-115). */
+typedef struct pikv_entry {
+    uint64_t id;
+    uint64_t shard_seq;
+    int64_t token_id;
+    int32_t expert_id;
+    int32_t has_layers;        /* per_layer_scores non-empty (n_layers values) */
+    uint64_t insert_step;
+    uint64_t last_access_step;
+    uint64_t freq;
+    double attn_mass;
+} pikv_entry;
+
 /* One live entry of the store, KVStore::snapshot (kvstore.hpp:89-96). */
 typedef struct pikv_snapshot_record {
     int32_t device;
@@ -272,7 +287,8 @@ int pikv_sync(pikv_engine* eng);
 int pikv_read_step_host(pikv_engine* eng, int32_t* experts, double* gates,
                         double* logits, pikv_step_summary* summary);
 /* Eviction records of the last step for all streams, reference order per
- * stream (overwrites, then per device the scheduled victims). */
+ * stream (overwrites, then per device the scheduled victims): at most cap
+ * written, *n_out = the step's total (cap 0 queries the count). */
 int pikv_read_evictions_host(pikv_engine* eng, pikv_evict_record* out, int32_t cap,
                              int32_t* n_out);
 /* Attended entries of the last step of `stream`: (token, expert, alpha) in
@@ -315,6 +331,12 @@ int pikv_read_slots_host(pikv_engine* eng, int32_t stream, uint64_t* id,
                          uint64_t* shard_seq, int64_t* token, int32_t* expert,
                          uint64_t* insert_step, uint64_t* last_access,
                          uint64_t* freq, double* attn_mass, double* per_layer);
+/* Stored K and V of n slots of `stream` (stream-local slot index, the
+ * pikv_read_slots_host order) decoded to fp32 -- the values attention reads:
+ * KVEntry::key / value (types.hpp:27-34) in the stored width d'.  Empty
+ * slots read as zeros.  key_out / value_out: [n][d'] host. */
+int pikv_read_entries_host(pikv_engine* eng, int32_t stream, const int64_t* slots, int32_t n,
+                           float* key_out, float* value_out);
 /* Overwrite attn_mass (and optionally per_layer) of `stream`'s slots, to
  * inject identical metadata for step-local parity of H2O/AdaKV/Duo. */
 int pikv_write_attn_mass_host(pikv_engine* eng, int32_t stream,
@@ -343,6 +365,96 @@ int64_t pikv_kernel_launches(pikv_engine* eng);
 int pikv_set_profiling(pikv_engine* eng, int32_t on);
 int pikv_read_profile_host(pikv_engine* eng, float* phase_ms, int32_t n_phases,
                            int32_t* n_steps);
+
+/* ---- component API: the reference's free functions and classes ----------
+ * The reference exposes its pieces individually (kvstore.hpp, router.hpp,
+ * scheduler.hpp, compressor.hpp, pipeline.hpp:46-47); these entry points run
+ * them on the GPU against ONE stream of an engine -- the same HBM store,
+ * RouterState and SchedulerState Engine::step uses.  Host buffers,
+ * synchronous, world_size 1.  Vectors in the stored space are fp32 of width
+ * d' (KVEntry::key/value, types.hpp:27-34); slots are stream-local indices
+ * (the pikv_read_slots_host order). */
+
+/* Router / scheduler coefficients and strategies of later calls (route(q,
+ * state, cfg) takes its RouterConfig per call, router.hpp:64-66); structural
+ * fields (d, E, k, G, S, heads, store/codec layout, batch) must be unchanged. */
+int pikv_update_config(pikv_engine* eng, const pikv_config* cfg);
+/* route (router.cpp:216-234): exact fp64 W_r q, penalty, selection, gates,
+ * note_selection.  query [d] fp64 (NULL allowed for Base).  experts [k],
+ * gates [k], logits [E] (RoutingDecision, router.hpp:58-62); any out may be
+ * NULL.  NaN logits -> PIKV_ERR_NUMERICAL with the state unchanged. */
+int pikv_route_host(pikv_engine* eng, int32_t stream, const double* query, int32_t* experts,
+                    double* gates, double* logits);
+/* route_logits (router.cpp:122-214) on caller logits [E]. */
+int pikv_route_logits_host(pikv_engine* eng, int32_t stream, const double* logits_in,
+                           int32_t* experts, double* gates, double* logits);
+int pikv_record_miss(pikv_engine* eng, int32_t stream, int32_t expert);     /* router.cpp:236-241 */
+int pikv_router_adapt(pikv_engine* eng, int32_t stream, const int32_t* experts, int32_t n,
+                      double reward);                                       /* router.cpp:243-255 */
+/* RouterState / SchedulerState overwrite (any pointer NULL = keep). */
+int pikv_write_router_state_host(pikv_engine* eng, int32_t stream, const double* load,
+                                 const uint64_t* usage, const uint64_t* miss, const double* bias,
+                                 const uint64_t* step, const uint64_t* total_usage);
+int pikv_write_sched_state_host(pikv_engine* eng, int32_t stream, const double* theta,
+                                const double* running_hit, const uint64_t* step);
+/* KVStore::insert (kvstore.cpp:107-120) of n entries in order: entries[j]
+ * carries (token, expert, EntryMeta); key/value [n][d'] fp32 in the stored
+ * space (kv_dtype values, or quantized for INT8/INT4); per_layer [n][n_layers]
+ * or NULL.  Displaced entries (full ring, kvstore.cpp:41-43) come back in
+ * displaced[j] / displaced_key/value[j] / displaced_layers[j] with
+ * displaced_flag[j] = 1.  Any output may be NULL. */
+int pikv_store_insert_host(pikv_engine* eng, int32_t stream, int32_t n, const pikv_entry* entries,
+                           const float* key, const float* value, const double* per_layer,
+                           pikv_entry* displaced, float* displaced_key, float* displaced_value,
+                           double* displaced_layers, int32_t* displaced_flag);
+/* KVStore::retrieve (kvstore.cpp:122-178): live entries with expert in the
+ * set and token < since, ordered by (token, expert); freq += 1 and
+ * last_access = now for each; *n_out = count, slots_out = their slots (at
+ * most cap), missed_out = experts with no hit (given order). */
+int pikv_store_retrieve_host(pikv_engine* eng, int32_t stream, const int32_t* experts,
+                             int32_t n_experts, int64_t since, uint64_t now, int64_t* slots_out,
+                             int32_t cap, int32_t* n_out, int32_t* missed_out, int32_t* n_missed);
+/* KVStore::erase (kvstore.cpp:180-185); *erased = 1 when the id was live. */
+int pikv_store_erase_host(pikv_engine* eng, int32_t stream, uint64_t entry_id, int32_t* erased);
+/* StoreStats retrievals / misses (kvstore.hpp:74-79; inserts and overwrites:
+ * pikv_store_stats_host). */
+int pikv_store_counters_host(pikv_engine* eng, int32_t stream, uint64_t* retrievals, uint64_t* misses);
+/* ShardBuffer::live_count of every local (device, shard): live [G_local][SPD]. */
+int pikv_ring_live_host(pikv_engine* eng, int32_t stream, int32_t* live);
+/* score_entry (scheduler.cpp:181-229) of n entries' metadata under cfg's
+ * scheduler strategy at `now`; per_layer [n][cfg->n_layers] or NULL. */
+int pikv_score_entries_host(const pikv_config* cfg, const pikv_entry* entries, const double* per_layer,
+                            int32_t n, uint64_t now, double* out);
+/* evict (scheduler.cpp:262-330) on the stream's store at `now` (also the
+ * stream's clock from here on): page scores, select_evictions per device,
+ * erase in id order, state.step++.  Records as pikv_read_evictions_host
+ * (at most cap); pages summed over the devices (EvictionReport). */
+int pikv_evict_host(pikv_engine* eng, int32_t stream, uint64_t now, pikv_evict_record* out, int32_t cap,
+                    int32_t* n_out, int32_t* pages_before, int32_t* pages_after);
+int pikv_observe_hits(pikv_engine* eng, int32_t stream, uint64_t hits, uint64_t lookups); /* :332-338 */
+int pikv_adakv_update(pikv_engine* eng, int32_t stream);                                 /* :340-342 */
+/* attention (pipeline.cpp:59-85) of a stored-space query [d'] over stored
+ * entries (slots [n]) per head, multi-head convention: y [d'], alpha [n] =
+ * mean over heads of the weights (NULL allowed). */
+int pikv_attend_host(pikv_engine* eng, int32_t stream, const float* query, const int64_t* slots, int32_t n,
+                     float* y_out, float* alpha_out);
+/* Codec::encode_vector / decode_vector (compressor.cpp:364-474) for
+ * IDENTITY / LOWRANK / LORAPLUS / FASTV / PRUNE, per head of width hd ->
+ * r: x [rows][heads*hd] <-> y [rows][heads*r]; basis [heads][r][hd], bias
+ * [heads*hd], kept [heads][r] (sorted).  Device buffers, or host (_host). */
+int pikv_codec_encode(int32_t codec, int32_t rows, int32_t heads, int32_t hd, int32_t r, const float* basis,
+                      const float* bias, const int32_t* kept, const float* x, float* y);
+int pikv_codec_decode(int32_t codec, int32_t rows, int32_t heads, int32_t hd, int32_t r, const float* basis,
+                      const float* bias, const int32_t* kept, const float* y, float* x);
+int pikv_codec_encode_host(int32_t codec, int32_t rows, int32_t heads, int32_t hd, int32_t r,
+                           const float* basis, const float* bias, const int32_t* kept, const float* x,
+                           float* y);
+int pikv_codec_decode_host(int32_t codec, int32_t rows, int32_t heads, int32_t hd, int32_t r,
+                           const float* basis, const float* bias, const int32_t* kept, const float* y,
+                           float* x);
+/* Column variances of n calibration rows [n][d] (Prune's fit statistic,
+ * compressor.cpp:250-255). */
+int pikv_column_variance_host(const double* rows, int32_t n, int32_t d, double* var);
 
 /* ---- micro-batch pipeline (no reference counterpart) ------------------
  * The reference's Engine is one stream; B streams are B independent

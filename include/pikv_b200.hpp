@@ -10,7 +10,14 @@
 //   pikv::shard_assign (kvstore.hpp:25)     pikv::b200::shard_assign
 //   pikv::select_evictions (scheduler.hpp:114) pikv::b200::select_evictions
 //   pikv::attention (pipeline.hpp:46)       pikv::b200::attention
-//   pikv::Engine (pipeline.hpp:101)         pikv::b200::Engine (B streams)
+//   pikv::Engine (pipeline.hpp:101)         pikv::b200::Engine (B streams; step,
+//                                           flush, StepResult.inserted)
+//   pikv::KVStore (kvstore.hpp:100-159)     pikv::b200::KVStore (in HBM)
+//   pikv::RouterState, route, route_logits, record_miss, adapt (router.hpp:41-79)
+//                                           same names (state in HBM)
+//   pikv::score_entry, evict, observe_hits, adakv_update (scheduler.hpp:83-129)
+//                                           score_entry / KVStore::evict / ...
+//   pikv::Codec encode/decode_vector (compressor.hpp:57-80)  pikv::b200::Codec
 //   pikv::Error tree (errors.hpp:9-47)      pikv::b200::Error tree
 //
 // Differences, all from the reference's own scope notes: the engine takes the
@@ -25,6 +32,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -138,7 +146,8 @@ inline AttentionOutput attention(const std::vector<double>& query,
 //      compressor.hpp, pipeline.hpp) -------------------------------------
 enum class RouterStrategy { Base, TopK, LoadBalanced, CacheAware, EntropyLB, Adaptive, Hierarchical };
 enum class SchedStrategy { H2O, SL, QUEST, Flex, LRU, LRUPlus, AdaKV, Duo };
-enum class Codec { Identity, LowRank, LoRAPlus, FastV, Prune, Int8, Int4 };
+// compressor.hpp:14-23 (Scheme; SVD / LoRA are LowRank here), plus this engine's quantizers
+enum class Scheme { Identity, LowRank, LoRAPlus, FastV, Prune, Int8, Int4 };
 enum class DType { F32, BF16 };
 
 struct ModelConfig { int d = 64, head_width = 16, E = 8, k = 2; long long L = 1024; int G = 2, S = 16, K = 4;
@@ -152,7 +161,7 @@ struct SchedulerConfig { SchedStrategy strategy = SchedStrategy::LRU; int budget
                          target_hit = 0.9, gamma_sim = 0.5, theta0 = -1e18, hit_decay = 0.9;
                          std::vector<double> adakv_weights{1.0, 0.5, 0.25};
                          std::vector<double> flex_plan{1.0}; int flex_bucket = 16; };
-struct CompressorConfig { Codec scheme = Codec::Identity; int rank = 8; };
+struct CompressorConfig { Scheme scheme = Scheme::Identity; int rank = 8; };
 
 struct EngineConfig {  // pipeline.hpp:87-98 (+ B200 runtime fields)
     ModelConfig model;
@@ -229,6 +238,7 @@ struct StepResult {  // pipeline.hpp:68-80
     std::vector<int> experts;
     std::vector<double> gates;
     int inserts = 0;
+    std::vector<std::pair<std::int64_t, int>> inserted;  // (token, expert) per stored entry
     std::vector<EvictionRecord> evictions;  // overwrite + scheduled
     std::uint64_t fetch_elements = 0;
     std::uint64_t hits = 0, lookups = 0;
@@ -244,6 +254,7 @@ struct SnapshotRecord {  // kvstore.hpp:89-96
 };
 
 struct StoreStats { std::uint64_t live = 0, memory_bytes = 0, inserts = 0, overwrites = 0; };
+using pikv_store_stats_view = StoreStats;
 struct RouterStateView { std::vector<double> load, bandit_bias; std::vector<std::uint64_t> usage_counts,
                          miss_counts; std::uint64_t total_usage = 0, step = 0; };
 struct SchedulerStateView { double theta = 0.0, running_hit = 0.0; std::uint64_t step = 0; };
@@ -316,9 +327,10 @@ class Engine {
         std::vector<double> gates(static_cast<std::size_t>(B) * k);
         std::vector<pikv_step_summary> sm(B);
         check(pikv_read_step_host(h_, ex.data(), gates.data(), nullptr, sm.data()));
-        std::vector<pikv_evict_record> recs(1u << 16);
         std::int32_t nrec = 0;
-        check(pikv_read_evictions_host(h_, recs.data(), static_cast<std::int32_t>(recs.size()), &nrec));
+        check(pikv_read_evictions_host(h_, nullptr, 0, &nrec));  // count, then the records
+        std::vector<pikv_evict_record> recs(nrec > 0 ? nrec : 1);
+        check(pikv_read_evictions_host(h_, recs.data(), nrec, &nrec));
         std::vector<StepResult> out(B);
         for (int s = 0; s < B; ++s) {
             StepResult& r = out[s];
@@ -326,6 +338,10 @@ class Engine {
             r.experts.assign(ex.begin() + s * k, ex.begin() + (s + 1) * k);
             r.gates.assign(gates.begin() + s * k, gates.begin() + (s + 1) * k);
             r.inserts = sm[s].inserts;
+            // Engine::insert_compressed (pipeline.cpp:197-199): one entry per
+            // selected expert, token = the step, in selection order
+            for (int j = 0; j < r.inserts && j < k; ++j)
+                r.inserted.emplace_back(static_cast<std::int64_t>(r.step), r.experts[j]);
             r.fetch_elements = static_cast<std::uint64_t>(sm[s].fetch_elements);
             r.hits = static_cast<std::uint64_t>(sm[s].hits);
             r.lookups = static_cast<std::uint64_t>(sm[s].lookups);
@@ -352,6 +368,12 @@ class Engine {
         (void)E;
         return out;
     }
+
+    // Engine::flush (pipeline.hpp:108): inserts a Chunk codec's pending
+    // entries.  No codec here buffers entries (Chunk is out of scope), so
+    // nothing is pending: an empty result per stream, as the reference
+    // returns for non-Chunk codecs.
+    std::vector<StepResult> flush() { return std::vector<StepResult>(cfg_.batch); }
 
     // KVStore::snapshot(now) (kvstore.cpp:206-221), computed on the GPU;
     // now < 0: the stream's current step.
@@ -386,8 +408,8 @@ class Engine {
     }
     int stored_width() const {
         const int hd = cfg_.model.d / cfg_.n_heads;
-        const bool proj = cfg_.compressor.scheme == Codec::LowRank || cfg_.compressor.scheme == Codec::LoRAPlus ||
-                          cfg_.compressor.scheme == Codec::FastV || cfg_.compressor.scheme == Codec::Prune;
+        const bool proj = cfg_.compressor.scheme == Scheme::LowRank || cfg_.compressor.scheme == Scheme::LoRAPlus ||
+                          cfg_.compressor.scheme == Scheme::FastV || cfg_.compressor.scheme == Scheme::Prune;
         return (proj ? cfg_.compressor.rank : hd) * cfg_.n_heads;
     }
     pikv_engine* handle() { return h_; }
@@ -408,6 +430,434 @@ class Engine {
     }
     EngineConfig cfg_;
     pikv_engine* h_ = nullptr;
+};
+
+// ---- component classes (kvstore.hpp, router.hpp, scheduler.hpp,
+//      compressor.hpp) over the component C-ABI: one-stream engines whose
+//      HBM state is the store / RouterState / SchedulerState -----------------
+struct EntryMeta {  // types.hpp:11-24
+    std::uint64_t insert_step = 0, last_access_step = 0, freq = 0;
+    double attn_mass = 0.0;
+    std::vector<double> per_layer_scores;
+};
+struct KVEntry {  // types.hpp:27-34
+    std::uint64_t id = 0, shard_seq = 0;
+    std::int64_t token_id = 0;
+    int expert_id = 0;
+    std::vector<double> key, value;
+    EntryMeta meta;
+};
+// kvstore.hpp:81-87; entries are host copies (the store lives in HBM), with
+// their stream-local slots for attention over stored entries
+struct RetrievalResult {
+    std::vector<KVEntry> entries;
+    std::vector<int> missed_experts;
+    std::vector<std::int64_t> slots;
+};
+struct StoreCounters { std::uint64_t inserts = 0, overwrites = 0, retrievals = 0, misses = 0; };
+struct EvictionReport {  // scheduler.hpp:100-104
+    std::vector<EvictionRecord> evicted;
+    int pages_before = 0, pages_after = 0;
+};
+
+namespace detail {
+inline pikv_entry to_c(const KVEntry& e) {
+    pikv_entry c{};
+    c.token_id = e.token_id, c.expert_id = e.expert_id;
+    c.has_layers = e.meta.per_layer_scores.empty() ? 0 : 1;
+    c.insert_step = e.meta.insert_step, c.last_access_step = e.meta.last_access_step;
+    c.freq = e.meta.freq, c.attn_mass = e.meta.attn_mass;
+    return c;
+}
+}  // namespace detail
+
+// KVStore (kvstore.hpp:100-159) in HBM.  The store is built for the
+// scheduler's page size (its page records are maintained on every insert).
+class KVStore {
+  public:
+    KVStore(const ModelConfig& model, const StoreConfig& store, int page_size = 16, int n_layers = 0,
+            DType kv_dtype = DType::F32, int cuda_device = 0)
+        : n_layers_(n_layers) {
+        EngineConfig c;
+        c.model = model;
+        c.model.d = d_prime_of(model);
+        c.model.rho = 1.0;
+        c.model.head_width = std::min(model.head_width, c.model.d);
+        c.store = store;
+        c.router.k = 1;
+        c.scheduler.page_size = page_size;
+        c.n_layers = n_layers, c.kv_dtype = kv_dtype, c.batch = 1, c.cuda_device = cuda_device;
+        cfg_ = c;
+        pikv_config pc = c.to_c();
+        check(pikv_engine_create(&pc, cuda_device, &h_));
+    }
+    ~KVStore() { if (h_) pikv_engine_destroy(h_); }
+    KVStore(const KVStore&) = delete;
+    KVStore& operator=(const KVStore&) = delete;
+
+    ShardId locate(std::int64_t token_id, int expert_id) const {  // kvstore.hpp:105
+        return shard_assign(token_id, expert_id, cfg_.store.n_tok, cfg_.store.n_exp, cfg_.model.G,
+                            cfg_.store.additive);
+    }
+    // KVStore::insert (kvstore.cpp:107-120): the displaced entry, if any
+    std::optional<KVEntry> insert(const KVEntry& e) {
+        const int dp = stored_width();
+        if (static_cast<int>(e.key.size()) != dp || static_cast<int>(e.value.size()) != dp)
+            throw InvalidEntry("KVStore::insert: entry width != d'");  // kvstore.cpp:108-111
+        pikv_entry in = detail::to_c(e), out{};
+        std::vector<float> k(e.key.begin(), e.key.end()), v(e.value.begin(), e.value.end());
+        std::vector<double> layers(n_layers_ > 0 ? n_layers_ : 1, 0.0), dl(layers.size());
+        for (int l = 0; l < n_layers_ && l < static_cast<int>(e.meta.per_layer_scores.size()); ++l)
+            layers[l] = e.meta.per_layer_scores[l];
+        if (n_layers_ == 0) in.has_layers = 0;
+        std::vector<float> dk(dp), dv(dp);
+        std::int32_t flag = 0;
+        check(pikv_store_insert_host(h_, 0, 1, &in, k.data(), v.data(), in.has_layers ? layers.data() : nullptr,
+                                     &out, dk.data(), dv.data(), dl.data(), &flag));
+        if (!flag) return std::nullopt;
+        KVEntry r;
+        r.id = out.id, r.shard_seq = out.shard_seq, r.token_id = out.token_id, r.expert_id = out.expert_id;
+        r.key.assign(dk.begin(), dk.end()), r.value.assign(dv.begin(), dv.end());
+        r.meta = {out.insert_step, out.last_access_step, out.freq, out.attn_mass, {}};
+        if (out.has_layers) r.meta.per_layer_scores.assign(dl.begin(), dl.begin() + n_layers_);
+        return r;
+    }
+    // KVStore::retrieve (kvstore.cpp:122-178)
+    RetrievalResult retrieve(const std::vector<int>& experts, std::int64_t since, std::uint64_t now) {
+        std::vector<std::int32_t> ex(experts.begin(), experts.end()), missed(experts.size() + 1);
+        const std::int64_t cap = pikv_slot_count(h_);
+        std::vector<std::int64_t> slots(cap > 0 ? cap : 1);
+        std::int32_t n = 0, nm = 0;
+        check(pikv_store_retrieve_host(h_, 0, ex.data(), static_cast<std::int32_t>(ex.size()), since, now,
+                                       slots.data(), static_cast<std::int32_t>(cap), &n, missed.data(), &nm));
+        RetrievalResult r;
+        r.slots.assign(slots.begin(), slots.begin() + n);
+        r.entries = entries_at(r.slots);
+        r.missed_experts.assign(missed.begin(), missed.begin() + nm);
+        return r;
+    }
+    bool erase(std::uint64_t entry_id) {  // kvstore.cpp:180-185
+        std::int32_t ok = 0;
+        check(pikv_store_erase_host(h_, 0, entry_id, &ok));
+        return ok != 0;
+    }
+    std::uint64_t memory_bytes() const { return stats_raw().memory_bytes; }
+    std::uint64_t live_entries() const { return stats_raw().live; }
+    StoreCounters stats() const {
+        StoreCounters c;
+        const auto s = stats_raw();
+        c.inserts = s.inserts, c.overwrites = s.overwrites;
+        check(pikv_store_counters_host(h_, 0, &c.retrievals, &c.misses));
+        return c;
+    }
+    int devices() const { return cfg_.model.G; }
+    int shards_per_device() const { return static_cast<int>(pikv_slot_count(h_) / cfg_.model.S / cfg_.model.G); }
+    int stored_width() const { return cfg_.model.d; }
+    int shard_capacity() const { return cfg_.model.S; }
+    // buffer(device, shard).live_count() (kvstore.hpp:41)
+    int live_count(int device, int shard) const {
+        std::vector<std::int32_t> live(static_cast<std::size_t>(devices()) * shards_per_device());
+        check(pikv_ring_live_host(h_, 0, live.data()));
+        return live[static_cast<std::size_t>(device) * shards_per_device() + shard];
+    }
+    // for_each_live (kvstore.hpp:136-144): fn(device, shard, entry) in slot order
+    template <typename Fn>
+    void for_each_live(Fn&& fn) const {
+        const std::int64_t n = pikv_slot_count(h_);
+        std::vector<std::uint64_t> id(n);
+        check(pikv_read_slots_host(h_, 0, id.data(), nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                   nullptr));
+        std::vector<std::int64_t> live;
+        for (std::int64_t i = 0; i < n; ++i)
+            if (id[i]) live.push_back(i);
+        const auto es = entries_at(live);
+        const int S = cfg_.model.S, spd = shards_per_device();
+        for (std::size_t i = 0; i < live.size(); ++i)
+            fn(static_cast<int>(live[i] / S) / spd, static_cast<int>(live[i] / S) % spd, es[i]);
+    }
+    std::vector<SnapshotRecord> snapshot(std::uint64_t now) const {
+        std::int64_t n = 0;
+        check(pikv_snapshot_host(h_, 0, static_cast<std::int64_t>(now), nullptr, 0, &n));
+        std::vector<pikv_snapshot_record> raw(static_cast<std::size_t>(n));
+        if (n) check(pikv_snapshot_host(h_, 0, static_cast<std::int64_t>(now), raw.data(), n, &n));
+        std::vector<SnapshotRecord> out;
+        for (const auto& r : raw) out.push_back({r.device, r.shard, r.token_id, r.expert_id, r.age, r.freq});
+        return out;
+    }
+    // attention (pipeline.cpp:59-85) of a stored-space query over retrieved entries
+    AttentionOutput attention(const std::vector<double>& query, const std::vector<std::int64_t>& slots) {
+        if (static_cast<int>(query.size()) != stored_width())
+            throw InvalidArgument("attention: key/query width mismatch");
+        std::vector<float> q(query.begin(), query.end()), y(stored_width()), a(slots.size() + 1);
+        check(pikv_attend_host(h_, 0, q.data(), slots.data(), static_cast<std::int32_t>(slots.size()), y.data(),
+                               a.data()));
+        AttentionOutput o;
+        o.output.assign(y.begin(), y.end());
+        o.weights.assign(a.begin(), a.begin() + slots.size());
+        o.retrieved = slots.size();
+        return o;
+    }
+    std::vector<KVEntry> entries_at(const std::vector<std::int64_t>& slots) const {
+        std::vector<KVEntry> out;
+        if (slots.empty()) return out;
+        const std::int64_t n = pikv_slot_count(h_);
+        std::vector<std::uint64_t> id(n), sq(n), ins(n), la(n), fr(n);
+        std::vector<std::int64_t> tok(n);
+        std::vector<std::int32_t> ex(n);
+        std::vector<double> mass(n), pl(static_cast<std::size_t>(n) * (n_layers_ > 0 ? n_layers_ : 1));
+        check(pikv_read_slots_host(h_, 0, id.data(), sq.data(), tok.data(), ex.data(), ins.data(), la.data(),
+                                   fr.data(), mass.data(), n_layers_ > 0 ? pl.data() : nullptr));
+        const int dp = stored_width();
+        std::vector<float> k(slots.size() * dp), v(slots.size() * dp);
+        check(pikv_read_entries_host(h_, 0, slots.data(), static_cast<std::int32_t>(slots.size()), k.data(),
+                                     v.data()));
+        for (std::size_t i = 0; i < slots.size(); ++i) {
+            const std::int64_t s = slots[i];
+            KVEntry e;
+            e.id = id[s], e.shard_seq = sq[s], e.token_id = tok[s], e.expert_id = ex[s];
+            e.key.assign(k.begin() + i * dp, k.begin() + (i + 1) * dp);
+            e.value.assign(v.begin() + i * dp, v.begin() + (i + 1) * dp);
+            e.meta = {ins[s], la[s], fr[s], mass[s], {}};
+            if (n_layers_ > 0) e.meta.per_layer_scores.assign(pl.begin() + s * n_layers_, pl.begin() + (s + 1) * n_layers_);
+            out.push_back(std::move(e));
+        }
+        return out;
+    }
+
+    // scheduler on this store (scheduler.hpp:118-129), with its SchedulerState
+    EvictionReport evict(const SchedulerConfig& cfg, std::uint64_t now) {
+        set_scheduler(cfg);
+        const std::int64_t cap = pikv_slot_count(h_);
+        std::vector<pikv_evict_record> recs(cap > 0 ? cap : 1);
+        std::int32_t n = 0, pb = 0, pa = 0;
+        check(pikv_evict_host(h_, 0, now, recs.data(), static_cast<std::int32_t>(cap), &n, &pb, &pa));
+        EvictionReport r;
+        r.pages_before = pb, r.pages_after = pa;
+        for (int i = 0; i < n; ++i)
+            r.evicted.push_back({recs[i].step, recs[i].entry_id, recs[i].token_id, recs[i].expert_id,
+                                 recs[i].device, recs[i].score, static_cast<EvictReason>(recs[i].reason)});
+        return r;
+    }
+    void observe_hits(const SchedulerConfig& cfg, std::uint64_t hits, std::uint64_t lookups) {
+        set_scheduler(cfg);
+        check(pikv_observe_hits(h_, 0, hits, lookups));
+    }
+    void adakv_update(const SchedulerConfig& cfg) {
+        set_scheduler(cfg);
+        check(pikv_adakv_update(h_, 0));
+    }
+    SchedulerStateView scheduler_state() const {
+        SchedulerStateView v;
+        check(pikv_read_sched_state_host(h_, 0, &v.theta, &v.running_hit, &v.step));
+        return v;
+    }
+    void set_scheduler_state(double theta, double running_hit) {
+        check(pikv_write_sched_state_host(h_, 0, &theta, &running_hit, nullptr));
+    }
+    pikv_engine* handle() { return h_; }
+
+  private:
+    static int d_prime_of(const ModelConfig& m) {  // config.hpp:37-40
+        const long long dp = std::llround(m.d / m.rho);
+        return dp < 1 ? 1 : static_cast<int>(dp);
+    }
+    void set_scheduler(const SchedulerConfig& cfg) {
+        if (cfg.page_size != cfg_.scheduler.page_size)
+            throw InvalidConfig("evict: the store was built for another page_size");
+        cfg_.scheduler = cfg;
+        pikv_config pc = cfg_.to_c();
+        check(pikv_update_config(h_, &pc));
+    }
+    pikv_store_stats_view stats_raw() const {
+        pikv_store_stats_view s{};
+        check(pikv_store_stats_host(h_, 0, &s.live, &s.memory_bytes, &s.inserts, &s.overwrites));
+        return s;
+    }
+    EngineConfig cfg_;
+    int n_layers_ = 0;
+    pikv_engine* h_ = nullptr;
+};
+
+// score_entry (scheduler.cpp:181-229) of one entry's metadata, on the GPU.
+inline double score_entry(const KVEntry& e, const SchedulerConfig& cfg, std::uint64_t now) {
+    EngineConfig ec;
+    ec.scheduler = cfg;
+    ec.n_layers = static_cast<int>(e.meta.per_layer_scores.size());
+    pikv_config pc = ec.to_c();
+    pikv_entry in = detail::to_c(e);
+    double out = 0.0;
+    check(pikv_score_entries_host(&pc, &in, e.meta.per_layer_scores.empty() ? nullptr : e.meta.per_layer_scores.data(),
+                                  1, now, &out));
+    return out;
+}
+
+struct RoutingDecision {  // router.hpp:58-62
+    std::vector<int> experts;
+    std::vector<double> gates;
+    std::vector<double> logits;
+};
+
+// RouterState::init(experts, width, seed) (router.cpp:54-67): W_r =
+// Rng(seed) N(0, 1/d) and the load / usage / miss / bias estimators in HBM.
+// Sized for one k at a time; a call with another k moves the state over.
+class RouterState {
+  public:
+    static RouterState init(int experts, int width, std::uint64_t seed) { return RouterState(experts, width, seed); }
+    RouterState(int experts, int width, std::uint64_t seed) : E_(experts), d_(width), seed_(seed) {}
+    ~RouterState() { if (h_) pikv_engine_destroy(h_); }
+    RouterState(RouterState&& o) noexcept { *this = std::move(o); }
+    RouterState& operator=(RouterState&& o) noexcept {
+        std::swap(E_, o.E_), std::swap(d_, o.d_), std::swap(seed_, o.seed_), std::swap(h_, o.h_);
+        std::swap(cfg_, o.cfg_);
+        return *this;
+    }
+    RouterStateView view() const {
+        RouterStateView r;
+        r.load.assign(E_, 0.0), r.bandit_bias.assign(E_, 0.0), r.usage_counts.assign(E_, 0), r.miss_counts.assign(E_, 0);
+        if (h_)
+            check(pikv_read_router_state_host(h_, 0, r.load.data(), r.usage_counts.data(), r.miss_counts.data(),
+                                              r.bandit_bias.data(), &r.step, &r.total_usage));
+        return r;
+    }
+    void set_load(const std::vector<double>& v) { bind(cfg_.router); write(v.data(), nullptr); }
+    void set_bias(const std::vector<double>& v) { bind(cfg_.router); write(nullptr, v.data()); }
+    int experts() const { return E_; }
+    int width() const { return d_; }
+
+    pikv_engine* bind(const RouterConfig& rc) {
+        if (h_ && rc.k == cfg_.router.k) {
+            cfg_.router = rc;
+            pikv_config pc = cfg_.to_c();
+            check(pikv_update_config(h_, &pc));
+            return h_;
+        }
+        const bool carry = h_ != nullptr;
+        const RouterStateView old = view();
+        if (h_) pikv_engine_destroy(h_), h_ = nullptr;
+        cfg_ = EngineConfig{};
+        cfg_.model.d = d_, cfg_.model.head_width = 1, cfg_.model.E = E_, cfg_.model.G = 1, cfg_.model.S = 1;
+        cfg_.store.n_tok = 1, cfg_.store.n_exp = 1;
+        cfg_.router = rc;
+        cfg_.unbounded_budget = true;
+        cfg_.seed = seed_ ^ 0x2545f4914f6cdd1dULL;  // the engine seeds W_r with seed ^ kRouterSalt
+        cfg_.pool_entries = 16;
+        pikv_config pc = cfg_.to_c();
+        check(pikv_engine_create(&pc, 0, &h_));
+        if (carry)
+            check(pikv_write_router_state_host(h_, 0, old.load.data(), old.usage_counts.data(), old.miss_counts.data(),
+                                               old.bandit_bias.data(), &old.step, &old.total_usage));
+        return h_;
+    }
+
+  private:
+    void write(const double* load, const double* bias) {
+        check(pikv_write_router_state_host(h_, 0, load, nullptr, nullptr, bias, nullptr, nullptr));
+    }
+    int E_ = 0, d_ = 0;
+    std::uint64_t seed_ = 0;
+    EngineConfig cfg_;
+    pikv_engine* h_ = nullptr;
+};
+
+namespace detail {
+inline RoutingDecision decision(pikv_engine* h, int k, int E, const double* q, const double* logits) {
+    RoutingDecision d;
+    d.experts.resize(k), d.gates.resize(k), d.logits.resize(E);
+    std::vector<std::int32_t> ex(k);
+    if (logits) check(pikv_route_logits_host(h, 0, logits, ex.data(), d.gates.data(), d.logits.data()));
+    else check(pikv_route_host(h, 0, q, ex.data(), d.gates.data(), d.logits.data()));
+    d.experts.assign(ex.begin(), ex.end());
+    return d;
+}
+}  // namespace detail
+
+// route (router.cpp:216-234): exact fp64 logits W_r q, penalty, selection
+inline RoutingDecision route(const std::vector<double>& query, RouterState& st, const RouterConfig& cfg) {
+    if (cfg.strategy != RouterStrategy::Base && static_cast<int>(query.size()) != st.width())
+        throw InvalidArgument("route: query width != d");
+    return detail::decision(st.bind(cfg), cfg.k, st.experts(), query.data(), nullptr);
+}
+// route_logits (router.cpp:122-214)
+inline RoutingDecision route_logits(const std::vector<double>& logits, RouterState& st, const RouterConfig& cfg) {
+    if (static_cast<int>(logits.size()) != st.experts()) throw InvalidArgument("route_logits: logit width != E");
+    return detail::decision(st.bind(cfg), cfg.k, st.experts(), nullptr, logits.data());
+}
+inline void record_miss(RouterState& st, int expert, const RouterConfig& cfg = {}) {  // router.cpp:236-241
+    check(pikv_record_miss(st.bind(cfg), 0, expert));
+}
+inline void adapt(RouterState& st, const RoutingDecision& d, double reward, const RouterConfig& cfg) {
+    std::vector<std::int32_t> ex(d.experts.begin(), d.experts.end());  // router.cpp:243-255
+    check(pikv_router_adapt(st.bind(cfg), 0, ex.data(), static_cast<std::int32_t>(ex.size()), reward));
+}
+
+// Codec (compressor.hpp:57-80): encode_vector / decode_vector on the GPU for
+// Identity / LowRank (SVD, LoRA) / LoRAPlus / FastV / Prune.  Projection
+// bases come from the caller (fitting is offline); FastV and Prune fit here.
+class Codec {
+  public:
+    static Codec identity(int d) { return Codec(PIKV_CODEC_IDENTITY, d, d); }
+    static Codec lowrank(int d, int r, std::vector<float> basis /* [r][d] */, std::vector<float> bias = {}) {
+        Codec c(bias.empty() ? PIKV_CODEC_LOWRANK : PIKV_CODEC_LORAPLUS, d, r);
+        c.basis_ = std::move(basis), c.bias_ = std::move(bias);
+        return c;
+    }
+    static Codec fastv(int d, int r) { return Codec(PIKV_CODEC_FASTV, d, r); }
+    // Prune fit (compressor.cpp:250-262): keep the d - ceil(frac d) highest-
+    // variance coordinates (ties by index), sorted
+    static Codec fit_prune(const std::vector<std::vector<double>>& rows, double prune_frac) {
+        if (rows.empty()) throw InsufficientCalibration("Prune: no calibration rows");
+        const int d = static_cast<int>(rows[0].size()), n = static_cast<int>(rows.size());
+        std::vector<double> flat, var(d);
+        for (const auto& r : rows) flat.insert(flat.end(), r.begin(), r.end());
+        check(pikv_column_variance_host(flat.data(), n, d, var.data()));
+        int keep = d - static_cast<int>(std::ceil(prune_frac * d));
+        if (keep < 1) keep = 1;
+        std::vector<int> order(d);
+        for (int i = 0; i < d; ++i) order[i] = i;
+        std::sort(order.begin(), order.end(), [&](int a, int b) { return var[a] != var[b] ? var[a] > var[b] : a < b; });
+        Codec c(PIKV_CODEC_PRUNE, d, keep);
+        c.kept_.assign(order.begin(), order.begin() + keep);
+        std::sort(c.kept_.begin(), c.kept_.end());
+        return c;
+    }
+    int stored_width() const { return r_; }
+    std::vector<int> zero_set() const {
+        std::vector<int> z;
+        for (int i = 0; i < d_; ++i)
+            if (codec_ == PIKV_CODEC_PRUNE && !std::binary_search(kept_.begin(), kept_.end(), i)) z.push_back(i);
+        return z;
+    }
+    std::vector<double> encode_vector(const std::vector<double>& x) const {
+        if (static_cast<int>(x.size()) != d_) throw InvalidEntry("encode: width mismatch");
+        return run(false, x, r_);
+    }
+    std::vector<double> decode_vector(const std::vector<double>& y) const {
+        if (static_cast<int>(y.size()) != r_) throw CodecMismatch("decode: payload width mismatch");
+        return run(true, y, d_);
+    }
+    double reconstruction_error(const std::vector<double>& x) const {  // compressor.cpp:551-572
+        const auto xr = decode_vector(encode_vector(x));
+        double num = 0, den = 0;
+        for (std::size_t i = 0; i < x.size(); ++i) num += (x[i] - xr[i]) * (x[i] - xr[i]), den += x[i] * x[i];
+        if (den == 0.0) throw InvalidArgument("reconstruction_error: zero-norm input");
+        return std::sqrt(num / den);
+    }
+
+  private:
+    Codec(int codec, int d, int r) : codec_(codec), d_(d), r_(r) {}
+    std::vector<double> run(bool decode, const std::vector<double>& in, int wout) const {
+        std::vector<float> x(in.begin(), in.end()), y(wout);
+        const int r = codec_ == PIKV_CODEC_IDENTITY ? d_ : r_;
+        const float* b = basis_.empty() ? nullptr : basis_.data();
+        const float* bi = bias_.empty() ? nullptr : bias_.data();
+        const std::int32_t* k = kept_.empty() ? nullptr : kept_.data();
+        check(decode ? pikv_codec_decode_host(codec_, 1, 1, d_, r, b, bi, k, x.data(), y.data())
+                     : pikv_codec_encode_host(codec_, 1, 1, d_, r, b, bi, k, x.data(), y.data()));
+        return std::vector<double>(y.begin(), y.end());
+    }
+    int codec_ = PIKV_CODEC_IDENTITY, d_ = 0, r_ = 0;
+    std::vector<float> basis_, bias_;
+    std::vector<std::int32_t> kept_;
 };
 
 // Micro-batch pipeline (include/pikv_b200.h, pikv_group_*; no reference

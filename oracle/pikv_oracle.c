@@ -719,6 +719,19 @@ int po_engine_snapshot(const po_engine* e, uint64_t now, pikv_snapshot_record* o
     return PIKV_OK;
 }
 
+/* Stored K/V of slot gi as attended (zeros for an empty slot). */
+int po_engine_read_payload(po_engine* e, int64_t gi, float* key, float* value) {
+    if (gi < 0 || gi >= po_engine_slot_count(e)) return PIKV_ERR_INVALID_ARGUMENT;
+    if (!e->slots[gi].id || !e->payload[(size_t)gi / PO_CHUNK]) {
+        memset(key, 0, sizeof(float) * (size_t)e->dp), memset(value, 0, sizeof(float) * (size_t)e->dp);
+        return PIKV_OK;
+    }
+    const float* p = slot_payload(e, (size_t)gi, 0);
+    memcpy(key, p, sizeof(float) * (size_t)e->dp);
+    memcpy(value, p + e->dp, sizeof(float) * (size_t)e->dp);
+    return PIKV_OK;
+}
+
 int po_engine_set_attn_mass(po_engine* e, const double* attn_mass, const double* per_layer) {
     int64_t n = po_engine_slot_count(e);
     for (int64_t i = 0; i < n; ++i)

@@ -30,6 +30,13 @@ class PikvEvictRecord(ctypes.Structure):
                 ("device", c_i32), ("score", c_f64), ("reason", c_i32), ("stream", c_i32)]
 
 
+class PikvEntry(ctypes.Structure):
+    """pikv_entry: KVEntry identity + EntryMeta (types.hpp:11-34)."""
+    _fields_ = [("id", c_u64), ("shard_seq", c_u64), ("token_id", c_i64), ("expert_id", c_i32),
+                ("has_layers", c_i32), ("insert_step", c_u64), ("last_access_step", c_u64),
+                ("freq", c_u64), ("attn_mass", c_f64)]
+
+
 class PikvStepSummary(ctypes.Structure):
     _fields_ = [("step", c_u64), ("inserts", c_i32), ("hits", c_i32), ("lookups", c_i32),
                 ("n_attended", c_i32), ("fetch_elements", c_i64), ("n_evictions", c_i32),
@@ -84,6 +91,7 @@ SIGNATURES = {
     "pikv_slot_count": (c_i64, [c_vp]),
     "pikv_read_slots_host": (ctypes.c_int, [c_vp, c_i32] + [c_vp] * 9),
     "pikv_write_attn_mass_host": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp]),
+    "pikv_read_entries_host": (ctypes.c_int, [c_vp, c_i32, c_vp, c_i32, c_vp, c_vp]),
     "pikv_read_router_state_host": (ctypes.c_int, [c_vp, c_i32] + [c_vp] * 6),
     "pikv_read_sched_state_host": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp, c_vp]),
     "pikv_store_stats_host": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp]),
@@ -103,6 +111,30 @@ SIGNATURES = {
     "pikv_group_sync": (ctypes.c_int, [c_vp]),
     "pikv_group_set_timing": (ctypes.c_int, [c_vp, c_i32]),
     "pikv_group_read_timing": (ctypes.c_int, [c_vp, P(c_f64), P(c_i32)]),
+    # component API
+    "pikv_update_config": (ctypes.c_int, [c_vp, P(PikvConfigC)]),
+    "pikv_route_host": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp]),
+    "pikv_route_logits_host": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp]),
+    "pikv_record_miss": (ctypes.c_int, [c_vp, c_i32, c_i32]),
+    "pikv_router_adapt": (ctypes.c_int, [c_vp, c_i32, c_vp, c_i32, c_f64]),
+    "pikv_write_router_state_host": (ctypes.c_int, [c_vp, c_i32] + [c_vp] * 6),
+    "pikv_write_sched_state_host": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp, c_vp]),
+    "pikv_store_insert_host": (ctypes.c_int, [c_vp, c_i32, c_i32] + [c_vp] * 9),
+    "pikv_store_retrieve_host": (ctypes.c_int, [c_vp, c_i32, c_vp, c_i32, c_i64, c_u64, c_vp, c_i32,
+                                                P(c_i32), c_vp, P(c_i32)]),
+    "pikv_store_erase_host": (ctypes.c_int, [c_vp, c_i32, c_u64, P(c_i32)]),
+    "pikv_store_counters_host": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp]),
+    "pikv_ring_live_host": (ctypes.c_int, [c_vp, c_i32, c_vp]),
+    "pikv_score_entries_host": (ctypes.c_int, [P(PikvConfigC), c_vp, c_vp, c_i32, c_u64, c_vp]),
+    "pikv_evict_host": (ctypes.c_int, [c_vp, c_i32, c_u64, c_vp, c_i32, P(c_i32), P(c_i32), P(c_i32)]),
+    "pikv_observe_hits": (ctypes.c_int, [c_vp, c_i32, c_u64, c_u64]),
+    "pikv_adakv_update": (ctypes.c_int, [c_vp, c_i32]),
+    "pikv_attend_host": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp, c_i32, c_vp, c_vp]),
+    "pikv_codec_encode": (ctypes.c_int, [c_i32] * 5 + [c_vp] * 5),
+    "pikv_codec_decode": (ctypes.c_int, [c_i32] * 5 + [c_vp] * 5),
+    "pikv_codec_encode_host": (ctypes.c_int, [c_i32] * 5 + [c_vp] * 5),
+    "pikv_codec_decode_host": (ctypes.c_int, [c_i32] * 5 + [c_vp] * 5),
+    "pikv_column_variance_host": (ctypes.c_int, [c_vp, c_i32, c_i32, c_vp]),
 }
 
 _LIB = None

@@ -459,6 +459,45 @@ static int validate(const pikv_config& c) {
     return PIKV_OK;
 }
 
+// The device-side scalar config (Cfg) of a pikv_config: router and
+// scheduler coefficients, and whether page aggregates are exact in any order.
+static void fill_cfg(const pikv_config& c, Cfg& C) {
+    C.router_strategy = c.router_strategy, C.groups = c.groups, C.stride = c.stride;
+    C.alpha = c.alpha, C.lambda_miss = c.lambda_miss, C.beta_ent = c.beta_ent;
+    C.bandit_step = c.bandit_step, C.bias_cap = c.bias_cap, C.load_decay = c.load_decay;
+    C.sched_strategy = c.sched_strategy, C.budget_pages = c.budget_pages;
+    C.page_size = c.page_size, C.sink = c.sink, C.flex_bucket = c.flex_bucket;
+    C.n_adakv_weights = c.n_adakv_weights, C.n_flex_plan = c.n_flex_plan;
+    C.tau = c.tau, C.lambda_freq = c.lambda_freq, C.adakv_step = c.adakv_step;
+    C.target_hit = c.target_hit, C.theta0 = c.theta0, C.hit_decay = c.hit_decay;
+    std::memcpy(C.adakv_weights, c.adakv_weights, sizeof(C.adakv_weights));
+    std::memcpy(C.flex_plan, c.flex_plan, sizeof(C.flex_plan));
+    C.unbounded_budget = c.unbounded_budget, C.head_width = c.head_width;
+    // Page aggregates (scheduler.cpp:276-289) are summed in slot order.  When
+    // every score is an integer multiple of 2^-10 and the page sum stays below
+    // 2^42 in magnitude, each partial sum is exact, so any summation order is
+    // bit-identical and the kernel may use a tree reduction.  True for LRU
+    // (-recency) and SL ({0,1,2,3}) always, for LRUPlus when lambda*1024 is an
+    // integer, and for Flex when every plan value is such a multiple.  With
+    // step counters < 2^31: LRU |sum| <= ps 2^31 < 2^53; LRUPlus needs
+    // ps (1 + |lambda|) 2^31 2^10 <= 2^53; Flex |plan| < 2^20 -> ps 2^30 <= 2^53.
+    {
+        auto dyadic = [](double x) { return std::isfinite(x) && std::fabs(x) < 1048576.0 &&
+                                            std::nearbyint(x * 1024.0) == x * 1024.0; };
+        bool ex = false;
+        if (c.sched_strategy == PIKV_SCHED_LRU || c.sched_strategy == PIKV_SCHED_SL) ex = true;
+        if (c.sched_strategy == PIKV_SCHED_LRU_PLUS)
+            ex = dyadic(c.lambda_freq) && (double)c.page_size * (1.0 + std::fabs(c.lambda_freq)) <= 4096.0;
+        if (c.sched_strategy == PIKV_SCHED_FLEX) {
+            ex = true;
+            for (int i = 0; i < c.n_flex_plan; ++i) ex = ex && dyadic(c.flex_plan[i]);
+        }
+        C.exact_sum = ex && c.page_size <= 1024 ? 1 : 0;
+        C.record_agg = C.exact_sum && (c.sched_strategy == PIKV_SCHED_LRU ||
+                                       c.sched_strategy == PIKV_SCHED_LRU_PLUS) ? 1 : 0;
+    }
+}
+
 // attend_sms > 0: the persistent attention grid spans that many SMs (the rest
 // stay free for the other micro-batch's control kernels, pikv_group)
 static int engine_create(const pikv_config* cfg, int32_t cuda_device, int attend_sms, pikv_engine** out,
@@ -532,6 +571,8 @@ static int engine_create(const pikv_config* cfg, int32_t cuda_device, int attend
         const char* dc = std::getenv("PIKV_DEBUG_CTL");
         D.dbg_ctl = dc && dc[0] == '1';
     }
+    D.only_s = -1;  // scheduler kernels: all streams
+    D.holes = 0;    // no arbitrary erase yet: page members are contiguous
     D.item_cap = (int64_t)D.items_per_cta * D.attend_ctas + D.B + 16;
     const int64_t total_slots = (int64_t)D.B * D.R * D.S;
     if (total_slots >= (1LL << 31)) {
@@ -554,49 +595,14 @@ static int engine_create(const pikv_config* cfg, int32_t cuda_device, int attend
         delete eng;
         return fail(PIKV_ERR_INVALID_CONFIG, std::string("attention layout: ") + msg);
     }
-    // scalar config
-    Cfg& C = eng->C;
-    C.router_strategy = c.router_strategy, C.groups = c.groups, C.stride = c.stride;
-    C.alpha = c.alpha, C.lambda_miss = c.lambda_miss, C.beta_ent = c.beta_ent;
-    C.bandit_step = c.bandit_step, C.bias_cap = c.bias_cap, C.load_decay = c.load_decay;
-    C.sched_strategy = c.sched_strategy, C.budget_pages = c.budget_pages;
-    C.page_size = c.page_size, C.sink = c.sink, C.flex_bucket = c.flex_bucket;
-    C.n_adakv_weights = c.n_adakv_weights, C.n_flex_plan = c.n_flex_plan;
-    C.tau = c.tau, C.lambda_freq = c.lambda_freq, C.adakv_step = c.adakv_step;
-    C.target_hit = c.target_hit, C.theta0 = c.theta0, C.hit_decay = c.hit_decay;
-    std::memcpy(C.adakv_weights, c.adakv_weights, sizeof(C.adakv_weights));
-    std::memcpy(C.flex_plan, c.flex_plan, sizeof(C.flex_plan));
-    C.unbounded_budget = c.unbounded_budget, C.head_width = c.head_width;
-    // Page aggregates (scheduler.cpp:276-289) are summed in slot order.  When
-    // every score is an integer multiple of 2^-10 and the page sum stays below
-    // 2^42 in magnitude, each partial sum is exact, so any summation order is
-    // bit-identical and the kernel may use a tree reduction.  True for LRU
-    // (-recency) and SL ({0,1,2,3}) always, for LRUPlus when lambda*1024 is an
-    // integer, and for Flex when every plan value is such a multiple.  With
-    // step counters < 2^31: LRU |sum| <= ps 2^31 < 2^53; LRUPlus needs
-    // ps (1 + |lambda|) 2^31 2^10 <= 2^53; Flex |plan| < 2^20 -> ps 2^30 <= 2^53.
-    {
-        auto dyadic = [](double x) { return std::isfinite(x) && std::fabs(x) < 1048576.0 &&
-                                            std::nearbyint(x * 1024.0) == x * 1024.0; };
-        bool ex = false;
-        if (c.sched_strategy == PIKV_SCHED_LRU || c.sched_strategy == PIKV_SCHED_SL) ex = true;
-        if (c.sched_strategy == PIKV_SCHED_LRU_PLUS)
-            ex = dyadic(c.lambda_freq) && (double)c.page_size * (1.0 + std::fabs(c.lambda_freq)) <= 4096.0;
-        if (c.sched_strategy == PIKV_SCHED_FLEX) {
-            ex = true;
-            for (int i = 0; i < c.n_flex_plan; ++i) ex = ex && dyadic(c.flex_plan[i]);
-        }
-        C.exact_sum = ex && c.page_size <= 1024 ? 1 : 0;
-        C.record_agg = C.exact_sum && (c.sched_strategy == PIKV_SCHED_LRU ||
-                                       c.sched_strategy == PIKV_SCHED_LRU_PLUS) ? 1 : 0;
-    }
+    fill_cfg(*cfg, eng->C);
     {
         // measured (profiles/README.md): the per-stream control kernel wins
         // when the step is launch-bound (B = 1: +5%); from B = 16 the wide
         // multi-kernel path is as fast or faster (c2 tie, c3-c5 +2-7%)
         bool want = D.B <= 8;
         if (const char* v = std::getenv("PIKV_CONTROL")) want = v[0] == '1';
-        eng->fused_control = control_supported(D, C) && want;
+        eng->fused_control = control_supported(D, eng->C) && want;
         if (const char* v = std::getenv("PIKV_RETR_FUSED")) eng->fused_retrieval = v[0] == '1';
     }
 
@@ -634,6 +640,8 @@ static int engine_create(const pikv_config* cfg, int32_t cuda_device, int attend
     chk(S.err = eng->alloc<int32_t>(B));
     chk(S.st_inserts = eng->alloc<uint64_t>(B));
     chk(S.st_overwrites = eng->alloc<uint64_t>(B));
+    chk(S.st_retrievals = eng->alloc<uint64_t>(B));
+    chk(S.st_misses = eng->alloc<uint64_t>(B));
     chk(S.head = eng->alloc<int32_t>(rings));
     chk(S.live = eng->alloc<int32_t>(rings));
     chk(S.seq = eng->alloc<uint64_t>(rings));
@@ -730,6 +738,8 @@ static int engine_create(const pikv_config* cfg, int32_t cuda_device, int attend
     CUDA_TRY(cudaMemsetAsync(S.err, 0, sizeof(int32_t) * B, st));
     CUDA_TRY(cudaMemsetAsync(S.st_inserts, 0, sizeof(uint64_t) * B, st));
     CUDA_TRY(cudaMemsetAsync(S.st_overwrites, 0, sizeof(uint64_t) * B, st));
+    CUDA_TRY(cudaMemsetAsync(S.st_retrievals, 0, sizeof(uint64_t) * B, st));
+    CUDA_TRY(cudaMemsetAsync(S.st_misses, 0, sizeof(uint64_t) * B, st));
     CUDA_TRY(cudaMemsetAsync(S.head, 0, sizeof(int32_t) * rings, st));
     CUDA_TRY(cudaMemsetAsync(S.live, 0, sizeof(int32_t) * rings, st));
     CUDA_TRY(cudaMemsetAsync(S.seq, 0, sizeof(uint64_t) * rings, st));
@@ -1252,22 +1262,22 @@ int pikv_read_evictions_host(pikv_engine* eng, pikv_evict_record* out, int32_t c
     std::vector<int32_t> now(D.B), nev((size_t)D.B * Gl);
     CUDA_TRY(cudaMemcpy(now.data(), eng->S.n_ow, sizeof(int32_t) * D.B, cudaMemcpyDeviceToHost));
     CUDA_TRY(cudaMemcpy(nev.data(), eng->S.n_ev, sizeof(int32_t) * D.B * Gl, cudaMemcpyDeviceToHost));
-    int32_t n = 0;
+    int32_t n = 0, tot = 0;  // records written (<= cap), records of the step
     for (int s = 0; s < D.B; ++s) {
         const int no = std::min(now[s], std::max(0, cap - n));
         if (no > 0)
             CUDA_TRY(cudaMemcpy(out + n, eng->S.rec_ow + (size_t)s * D.k, sizeof(pikv_evict_record) * no,
                                 cudaMemcpyDeviceToHost));
-        n += no;
+        n += no, tot += now[s];
         for (int gl = 0; gl < D.Gl; ++gl) {
             const int ne = std::min(nev[(size_t)s * Gl + gl], std::max(0, cap - n));
             if (ne > 0)
                 CUDA_TRY(cudaMemcpy(out + n, eng->S.rec_ev + ((size_t)s * Gl + gl) * D.SPD * D.S,
                                     sizeof(pikv_evict_record) * ne, cudaMemcpyDeviceToHost));
-            n += ne;
+            n += ne, tot += nev[(size_t)s * Gl + gl];
         }
     }
-    *n_out = n;
+    *n_out = tot;
     return PIKV_OK;
 }
 
@@ -1479,6 +1489,33 @@ int pikv_read_attended_host(pikv_engine* eng, int32_t stream, int64_t* token, in
     return PIKV_OK;
 }
 
+int pikv_read_entries_host(pikv_engine* eng, int32_t stream, const int64_t* slots, int32_t n, float* key_out,
+                           float* value_out) {
+    const Dims& D = eng->D;
+    if (stream < 0 || stream >= D.B) return fail(PIKV_ERR_INVALID_ARGUMENT, "stream out of range");
+    if (n <= 0) return PIKV_OK;
+    if (!slots || !key_out || !value_out) return fail(PIKV_ERR_INVALID_ARGUMENT, "read_entries: null buffer");
+    const int64_t ns = (int64_t)D.R * D.S;
+    for (int i = 0; i < n; ++i)
+        if (slots[i] < 0 || slots[i] >= ns) return fail(PIKV_ERR_INVALID_ARGUMENT, "read_entries: slot out of range");
+    cudaSetDevice(eng->device);
+    const size_t nb = 8 * (size_t)n, kb = sizeof(float) * (size_t)n * D.dp;
+    uint8_t* buf = nullptr;
+    CUDA_TRY(cudaMalloc(&buf, nb + 2 * kb));
+    cudaStream_t st = eng->stream;
+    cudaError_t e = cudaMemcpyAsync(buf, slots, nb, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) {
+        launch_read_entries(D, eng->S, stream, (const int64_t*)buf, n, (float*)(buf + nb), (float*)(buf + nb + kb), st);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(key_out, buf + nb, kb, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(value_out, buf + nb + kb, kb, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(buf);
+    if (e != cudaSuccess) return fail(PIKV_ERR_CUDA, std::string("read_entries: ") + cudaGetErrorString(e));
+    return PIKV_OK;
+}
+
 int64_t pikv_slot_count(pikv_engine* eng) { return (int64_t)eng->D.R * eng->D.S; }
 
 int pikv_read_slots_host(pikv_engine* eng, int32_t stream, uint64_t* id, uint64_t* shard_seq,
@@ -1603,6 +1640,492 @@ int pikv_read_profile_host(pikv_engine* eng, float* phase_ms, int32_t n_phases, 
     for (int p = 0; p < n_phases && p < kPhases; ++p) phase_ms[p] = acc[p];
     if (n_steps) *n_steps = eng->prof_steps;
     eng->prof_steps = 0;
+    return PIKV_OK;
+}
+
+// ---------------------------------------------------------------------------
+// component API: the reference's free functions and classes on one stream
+// (include/pikv_b200.h "component API"); kernels in components.cu
+// ---------------------------------------------------------------------------
+namespace {
+// device scratch of one component call, freed on scope exit
+struct Scratch {
+    void* p = nullptr;
+    cudaError_t e = cudaSuccess;
+    explicit Scratch(size_t n) { e = cudaMalloc(&p, n ? n : 1); }
+    ~Scratch() { if (p) cudaFree(p); }
+    uint8_t* at(size_t off) const { return (uint8_t*)p + off; }
+};
+size_t al256(size_t n) { return (n + 255) & ~(size_t)255; }
+
+int component_check(pikv_engine* eng, int32_t stream) {
+    if (!eng) return fail(PIKV_ERR_INVALID_ARGUMENT, "engine is NULL");
+    if (stream < 0 || stream >= eng->D.B) return fail(PIKV_ERR_INVALID_ARGUMENT, "stream out of range");
+    if (eng->D.world != 1) return fail(PIKV_ERR_INVALID_ARGUMENT, "component API: world_size must be 1");
+    cudaSetDevice(eng->device);
+    return PIKV_OK;
+}
+}  // namespace
+
+int pikv_update_config(pikv_engine* eng, const pikv_config* cfg) {
+    if (!eng || !cfg) return fail(PIKV_ERR_INVALID_ARGUMENT, "NULL argument");
+    const pikv_config& o = eng->cfg;
+    // structural fields fix the HBM layout: they must not change
+    if (cfg->d != o.d || cfg->E != o.E || cfg->k != o.k || cfg->G != o.G || cfg->S != o.S ||
+        cfg->n_heads != o.n_heads || cfg->n_tok != o.n_tok || cfg->n_exp != o.n_exp ||
+        cfg->additive != o.additive || cfg->page_size != o.page_size || cfg->codec != o.codec ||
+        cfg->rank != o.rank || cfg->n_layers != o.n_layers || cfg->batch != o.batch ||
+        cfg->kv_dtype != o.kv_dtype || cfg->world_size != o.world_size)
+        return fail(PIKV_ERR_INVALID_CONFIG, "update_config: only router / scheduler coefficients may change");
+    int rc = validate(*cfg);
+    if (rc) return rc;
+    CUDA_TRY(cudaStreamSynchronize(eng->stream));
+    eng->cfg = *cfg;
+    fill_cfg(*cfg, eng->C);
+    eng->invalidate();  // captured kernels hold the old Cfg
+    return PIKV_OK;
+}
+
+static int route_common(pikv_engine* eng, int32_t stream, const double* query, const double* logits_in,
+                        int32_t* experts, double* gates, double* logits) {
+    int rc = component_check(eng, stream);
+    if (rc) return rc;
+    const Dims& D = eng->D;
+    cudaStream_t st = eng->stream;
+    const size_t nq = query ? sizeof(double) * (size_t)D.B * D.d : 0;
+    Scratch buf(al256(nq) + sizeof(double) * (size_t)D.E);
+    if (buf.e != cudaSuccess) return fail(PIKV_ERR_CUDA, "route: cudaMalloc");
+    double* dq = (double*)buf.at(0);
+    double* dl = (double*)buf.at(al256(nq));
+    if (query) CUDA_TRY(cudaMemcpyAsync(dq + (size_t)stream * D.d, query, sizeof(double) * D.d,
+                                        cudaMemcpyHostToDevice, st));
+    if (logits_in) CUDA_TRY(cudaMemcpyAsync(dl, logits_in, sizeof(double) * D.E, cudaMemcpyHostToDevice, st));
+    launch_route_one(D, eng->C, eng->S, stream, query ? dq : nullptr, logits_in ? dl : nullptr, st);
+    CUDA_TRY(cudaGetLastError());
+    int32_t err = 0;
+    CUDA_TRY(cudaMemcpyAsync(&err, eng->S.err + stream, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (err == PIKV_ERR_NUMERICAL) {  // router.cpp:131-133: throws before any state change
+        CUDA_TRY(cudaMemset(eng->S.err + stream, 0, sizeof(int32_t)));
+        return fail(PIKV_ERR_NUMERICAL, "route_logits: NaN logit");
+    }
+    if (err) return fail(err, "route: stream is in an error state");
+    const size_t k = (size_t)D.k, E = (size_t)D.E;
+    if (experts) CUDA_TRY(cudaMemcpy(experts, eng->S.experts + stream * k, 4 * k, cudaMemcpyDeviceToHost));
+    if (gates) CUDA_TRY(cudaMemcpy(gates, eng->S.gates + stream * k, 8 * k, cudaMemcpyDeviceToHost));
+    if (logits) CUDA_TRY(cudaMemcpy(logits, eng->S.logits + stream * E, 8 * E, cudaMemcpyDeviceToHost));
+    return PIKV_OK;
+}
+
+int pikv_route_host(pikv_engine* eng, int32_t stream, const double* query, int32_t* experts, double* gates,
+                    double* logits) {
+    if (!query && eng && eng->C.router_strategy != PIKV_ROUTER_BASE)
+        return fail(PIKV_ERR_INVALID_ARGUMENT, "route: query is NULL");
+    if (!query) {  // Base ignores the query (router.cpp:219-221)
+        static const double zero = 0.0;
+        return route_common(eng, stream, nullptr, &zero, experts, gates, logits);
+    }
+    return route_common(eng, stream, query, nullptr, experts, gates, logits);
+}
+
+int pikv_route_logits_host(pikv_engine* eng, int32_t stream, const double* logits_in, int32_t* experts,
+                           double* gates, double* logits) {
+    if (!logits_in) return fail(PIKV_ERR_INVALID_ARGUMENT, "route_logits: logits are NULL");
+    return route_common(eng, stream, nullptr, logits_in, experts, gates, logits);
+}
+
+static int state_op(pikv_engine* eng, int32_t stream, int op, uint64_t a, uint64_t b, const int32_t* experts,
+                    int n, double reward) {
+    int rc = component_check(eng, stream);
+    if (rc) return rc;
+    Scratch buf(4 * (size_t)(n > 0 ? n : 1));
+    if (buf.e != cudaSuccess) return fail(PIKV_ERR_CUDA, "cudaMalloc");
+    if (n > 0) CUDA_TRY(cudaMemcpyAsync(buf.p, experts, 4 * (size_t)n, cudaMemcpyHostToDevice, eng->stream));
+    launch_state_op(eng->D, eng->C, eng->S, stream, op, a, b, (const int32_t*)buf.p, n, reward, eng->stream);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(eng->stream));
+    return PIKV_OK;
+}
+
+int pikv_record_miss(pikv_engine* eng, int32_t stream, int32_t expert) {
+    if (eng && (expert < 0 || expert >= eng->D.E))  // router.cpp:237-239
+        return fail(PIKV_ERR_INVALID_ARGUMENT, "record_miss: expert out of range");
+    return state_op(eng, stream, 3, (uint64_t)expert, 0, nullptr, 0, 0.0);
+}
+
+int pikv_router_adapt(pikv_engine* eng, int32_t stream, const int32_t* experts, int32_t n, double reward) {
+    if (!(reward >= 0.0 && reward <= 1.0))  // router.cpp:245-247
+        return fail(PIKV_ERR_INVALID_ARGUMENT, "adapt: reward must be in [0, 1]");
+    for (int j = 0; j < n; ++j)
+        if (eng && (experts[j] < 0 || experts[j] >= eng->D.E))
+            return fail(PIKV_ERR_INVALID_ARGUMENT, "adapt: expert out of range");
+    return state_op(eng, stream, 4, 0, 0, experts, n, reward);
+}
+
+int pikv_observe_hits(pikv_engine* eng, int32_t stream, uint64_t hits, uint64_t lookups) {
+    return state_op(eng, stream, 0, hits, lookups, nullptr, 0, 0.0);
+}
+
+int pikv_adakv_update(pikv_engine* eng, int32_t stream) { return state_op(eng, stream, 1, 0, 0, nullptr, 0, 0.0); }
+
+int pikv_write_router_state_host(pikv_engine* eng, int32_t stream, const double* load, const uint64_t* usage,
+                                 const uint64_t* miss, const double* bias, const uint64_t* step,
+                                 const uint64_t* total_usage) {
+    int rc = component_check(eng, stream);
+    if (rc) return rc;
+    CUDA_TRY(cudaStreamSynchronize(eng->stream));
+    const size_t E = eng->D.E, o = (size_t)stream * E;
+    if (load) CUDA_TRY(cudaMemcpy(eng->S.load + o, load, 8 * E, cudaMemcpyHostToDevice));
+    if (usage) CUDA_TRY(cudaMemcpy(eng->S.usage + o, usage, 8 * E, cudaMemcpyHostToDevice));
+    if (miss) CUDA_TRY(cudaMemcpy(eng->S.miss + o, miss, 8 * E, cudaMemcpyHostToDevice));
+    if (bias) CUDA_TRY(cudaMemcpy(eng->S.bias + o, bias, 8 * E, cudaMemcpyHostToDevice));
+    if (step) CUDA_TRY(cudaMemcpy(eng->S.rstep + stream, step, 8, cudaMemcpyHostToDevice));
+    if (total_usage) CUDA_TRY(cudaMemcpy(eng->S.total_usage + stream, total_usage, 8, cudaMemcpyHostToDevice));
+    return PIKV_OK;
+}
+
+int pikv_write_sched_state_host(pikv_engine* eng, int32_t stream, const double* theta, const double* running_hit,
+                                const uint64_t* step) {
+    int rc = component_check(eng, stream);
+    if (rc) return rc;
+    CUDA_TRY(cudaStreamSynchronize(eng->stream));
+    if (theta) CUDA_TRY(cudaMemcpy(eng->S.theta + stream, theta, 8, cudaMemcpyHostToDevice));
+    if (running_hit) CUDA_TRY(cudaMemcpy(eng->S.running_hit + stream, running_hit, 8, cudaMemcpyHostToDevice));
+    if (step) CUDA_TRY(cudaMemcpy(eng->S.sstep + stream, step, 8, cudaMemcpyHostToDevice));
+    return PIKV_OK;
+}
+
+int pikv_store_insert_host(pikv_engine* eng, int32_t stream, int32_t n, const pikv_entry* entries,
+                           const float* key, const float* value, const double* per_layer, pikv_entry* displaced,
+                           float* displaced_key, float* displaced_value, double* displaced_layers,
+                           int32_t* displaced_flag) {
+    int rc = component_check(eng, stream);
+    if (rc) return rc;
+    if (n <= 0) return PIKV_OK;
+    if (!entries || !key || !value) return fail(PIKV_ERR_INVALID_ARGUMENT, "store_insert: NULL input");
+    const Dims& D = eng->D;
+    for (int j = 0; j < n; ++j)  // kvstore.cpp:17-22 (shard_assign of the entry)
+        if (entries[j].token_id < 0 || entries[j].expert_id < 0)
+            return fail(PIKV_ERR_INVALID_ARGUMENT, "shard_assign: negative token or expert index");
+    const size_t dp = (size_t)D.dp, nl = (size_t)std::max(D.n_layers, 0);
+    std::vector<float> kv(2 * dp * n);
+    for (int j = 0; j < n; ++j) {
+        std::memcpy(&kv[(2 * (size_t)j) * dp], key + (size_t)j * dp, 4 * dp);
+        std::memcpy(&kv[(2 * (size_t)j + 1) * dp], value + (size_t)j * dp, 4 * dp);
+    }
+    const size_t o_in = 0, o_kv = al256(sizeof(pikv_entry) * n), o_ly = o_kv + al256(4 * kv.size());
+    const size_t o_dsp = o_ly + al256(8 * nl * n), o_dkv = o_dsp + al256(sizeof(pikv_entry) * n);
+    const size_t o_dly = o_dkv + al256(4 * kv.size()), o_flag = o_dly + al256(8 * nl * n);
+    const size_t o_st = o_flag + al256(4 * (size_t)n);
+    Scratch buf(o_st + 16);
+    if (buf.e != cudaSuccess) return fail(PIKV_ERR_CUDA, "store_insert: cudaMalloc");
+    cudaStream_t st = eng->stream;
+    CUDA_TRY(cudaMemcpyAsync(buf.at(o_in), entries, sizeof(pikv_entry) * n, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(buf.at(o_kv), kv.data(), 4 * kv.size(), cudaMemcpyHostToDevice, st));
+    if (per_layer && nl) CUDA_TRY(cudaMemcpyAsync(buf.at(o_ly), per_layer, 8 * nl * n, cudaMemcpyHostToDevice, st));
+    launch_store_insert(D, eng->S, stream, n, (const pikv_entry*)buf.at(o_in), (const float*)buf.at(o_kv),
+                        per_layer && nl ? (const double*)buf.at(o_ly) : nullptr, (pikv_entry*)buf.at(o_dsp),
+                        (float*)buf.at(o_dkv), nl ? (double*)buf.at(o_dly) : nullptr, (int32_t*)buf.at(o_flag),
+                        (int32_t*)buf.at(o_st), st);
+    CUDA_TRY(cudaGetLastError());
+    int32_t status = 0;
+    std::vector<int32_t> flag(n);
+    std::vector<float> dkv(kv.size());
+    CUDA_TRY(cudaMemcpyAsync(&status, buf.at(o_st), 4, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(flag.data(), buf.at(o_flag), 4 * (size_t)n, cudaMemcpyDeviceToHost, st));
+    if (displaced) CUDA_TRY(cudaMemcpyAsync(displaced, buf.at(o_dsp), sizeof(pikv_entry) * n, cudaMemcpyDeviceToHost, st));
+    if (displaced_key || displaced_value)
+        CUDA_TRY(cudaMemcpyAsync(dkv.data(), buf.at(o_dkv), 4 * dkv.size(), cudaMemcpyDeviceToHost, st));
+    if (displaced_layers && nl)
+        CUDA_TRY(cudaMemcpyAsync(displaced_layers, buf.at(o_dly), 8 * nl * n, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    for (int j = 0; j < n; ++j) {
+        if (displaced_flag) displaced_flag[j] = flag[j];
+        if (!flag[j]) continue;
+        if (displaced_key) std::memcpy(displaced_key + (size_t)j * dp, &dkv[2 * (size_t)j * dp], 4 * dp);
+        if (displaced_value) std::memcpy(displaced_value + (size_t)j * dp, &dkv[(2 * (size_t)j + 1) * dp], 4 * dp);
+    }
+    if (status) return fail(status, "store_insert: KV page pool exhausted");
+    return PIKV_OK;
+}
+
+int pikv_store_retrieve_host(pikv_engine* eng, int32_t stream, const int32_t* experts, int32_t n_experts,
+                             int64_t since, uint64_t now, int64_t* slots_out, int32_t cap, int32_t* n_out,
+                             int32_t* missed_out, int32_t* n_missed) {
+    int rc = component_check(eng, stream);
+    if (rc) return rc;
+    if (n_experts <= 0 || !experts)  // kvstore.cpp:124-126
+        return fail(PIKV_ERR_INVALID_ARGUMENT, "KVStore::retrieve: empty expert set");
+    for (int j = 0; j < n_experts; ++j)
+        if (experts[j] < 0) return fail(PIKV_ERR_INVALID_ARGUMENT, "KVStore::retrieve: negative expert");
+    const Dims& D = eng->D;
+    uint32_t want[8] = {0};
+    for (int j = 0; j < n_experts; ++j)
+        if (experts[j] < 256) want[experts[j] >> 5] |= 1u << (experts[j] & 31);
+    cudaStream_t st = eng->stream;
+    Scratch buf(retrieve_scratch_bytes(D) + 256);
+    if (buf.e != cudaSuccess) return fail(PIKV_ERR_CUDA, "retrieve: cudaMalloc");
+    uint32_t* dwant = (uint32_t*)buf.at(0);
+    CUDA_TRY(cudaMemcpyAsync(dwant, want, sizeof(want), cudaMemcpyHostToDevice, st));
+    int32_t *sorted = nullptr, *cnt = nullptr;
+    uint32_t* found = nullptr;
+    const int e = launch_retrieve(D, eng->S, stream, since, now, dwant, buf.at(256), &sorted, &cnt, &found, st);
+    if (e) return fail(PIKV_ERR_CUDA, std::string("retrieve: ") + cudaGetErrorString((cudaError_t)e));
+    int32_t n = 0;
+    uint32_t hfound[256];
+    CUDA_TRY(cudaMemcpyAsync(&n, cnt, 4, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(hfound, found, sizeof(hfound), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (n_out) *n_out = n;
+    const int m = std::min(n, cap);
+    if (slots_out && m > 0) {
+        std::vector<int32_t> sl(m);
+        CUDA_TRY(cudaMemcpy(sl.data(), sorted, 4 * (size_t)m, cudaMemcpyDeviceToHost));
+        for (int i = 0; i < m; ++i) slots_out[i] = sl[i];
+    }
+    int nm = 0;  // missed experts in the order given (kvstore.cpp:169-174)
+    for (int j = 0; j < n_experts; ++j)
+        if (experts[j] >= 256 || hfound[experts[j]] == 0) {
+            if (missed_out) missed_out[nm] = experts[j];
+            ++nm;
+        }
+    if (n_missed) *n_missed = nm;
+    // StoreStats: retrievals += 1, misses += |missed| (kvstore.cpp:169-176)
+    std::vector<uint64_t> cs(2);
+    CUDA_TRY(cudaMemcpy(&cs[0], eng->S.st_retrievals + stream, 8, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(&cs[1], eng->S.st_misses + stream, 8, cudaMemcpyDeviceToHost));
+    cs[0] += 1, cs[1] += (uint64_t)nm;
+    CUDA_TRY(cudaMemcpy(eng->S.st_retrievals + stream, &cs[0], 8, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(eng->S.st_misses + stream, &cs[1], 8, cudaMemcpyHostToDevice));
+    return PIKV_OK;
+}
+
+int pikv_store_erase_host(pikv_engine* eng, int32_t stream, uint64_t entry_id, int32_t* erased) {
+    int rc = component_check(eng, stream);
+    if (rc) return rc;
+    if (erased) *erased = 0;
+    if (entry_id == 0) return PIKV_OK;  // ids start at 1 (kvstore.hpp:157)
+    if (!eng->D.holes) {  // page members may have holes from now on
+        CUDA_TRY(cudaStreamSynchronize(eng->stream));
+        eng->D.holes = 1;
+        eng->invalidate();
+    }
+    Scratch buf(16);
+    if (buf.e != cudaSuccess) return fail(PIKV_ERR_CUDA, "erase: cudaMalloc");
+    launch_store_erase(eng->D, eng->S, stream, entry_id, (int32_t*)buf.p, eng->stream);
+    CUDA_TRY(cudaGetLastError());
+    int32_t st = 0;
+    CUDA_TRY(cudaMemcpyAsync(&st, buf.p, 4, cudaMemcpyDeviceToHost, eng->stream));
+    CUDA_TRY(cudaStreamSynchronize(eng->stream));
+    if (erased) *erased = st;
+    return PIKV_OK;
+}
+
+int pikv_store_counters_host(pikv_engine* eng, int32_t stream, uint64_t* retrievals, uint64_t* misses) {
+    int rc = component_check(eng, stream);
+    if (rc) return rc;
+    CUDA_TRY(cudaStreamSynchronize(eng->stream));
+    if (retrievals) CUDA_TRY(cudaMemcpy(retrievals, eng->S.st_retrievals + stream, 8, cudaMemcpyDeviceToHost));
+    if (misses) CUDA_TRY(cudaMemcpy(misses, eng->S.st_misses + stream, 8, cudaMemcpyDeviceToHost));
+    return PIKV_OK;
+}
+
+int pikv_ring_live_host(pikv_engine* eng, int32_t stream, int32_t* live) {
+    int rc = component_check(eng, stream);
+    if (rc) return rc;
+    CUDA_TRY(cudaStreamSynchronize(eng->stream));
+    CUDA_TRY(cudaMemcpy(live, eng->S.live + (size_t)stream * eng->D.R, 4 * (size_t)eng->D.R, cudaMemcpyDeviceToHost));
+    return PIKV_OK;
+}
+
+int pikv_score_entries_host(const pikv_config* cfg, const pikv_entry* entries, const double* per_layer, int32_t n,
+                            uint64_t now, double* out) {
+    if (!cfg || (n > 0 && (!entries || !out))) return fail(PIKV_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (cfg->sched_strategy == PIKV_SCHED_QUEST)  // scheduler.cpp:199-203
+        return fail(PIKV_ERR_NOT_FITTED, "score: QUEST scorer not fitted");
+    if (n <= 0) return PIKV_OK;
+    Cfg C{};
+    fill_cfg(*cfg, C);
+    const size_t nl = (size_t)std::max(cfg->n_layers, 0);
+    Scratch buf(al256(sizeof(pikv_entry) * n) + al256(8 * nl * n) + 8 * (size_t)n);
+    if (buf.e != cudaSuccess) return fail(PIKV_ERR_CUDA, "score: cudaMalloc");
+    const size_t o_ly = al256(sizeof(pikv_entry) * n), o_out = o_ly + al256(8 * nl * n);
+    CUDA_TRY(cudaMemcpy(buf.at(0), entries, sizeof(pikv_entry) * n, cudaMemcpyHostToDevice));
+    if (per_layer && nl) CUDA_TRY(cudaMemcpy(buf.at(o_ly), per_layer, 8 * nl * n, cudaMemcpyHostToDevice));
+    launch_score_meta(C, (const pikv_entry*)buf.at(0), per_layer && nl ? (const double*)buf.at(o_ly) : nullptr,
+                      (int)nl, n, now, (double*)buf.at(o_out), 0);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpy(out, buf.at(o_out), 8 * (size_t)n, cudaMemcpyDeviceToHost));
+    return PIKV_OK;
+}
+
+int pikv_evict_host(pikv_engine* eng, int32_t stream, uint64_t now, pikv_evict_record* out, int32_t cap,
+                    int32_t* n_out, int32_t* pages_before, int32_t* pages_after) {
+    int rc = component_check(eng, stream);
+    if (rc) return rc;
+    const Dims& D = eng->D;
+    cudaStream_t st = eng->stream;
+    const int Gl = std::max(D.Gl, 1);
+    const size_t o = (size_t)stream * Gl;
+    CUDA_TRY(cudaMemcpyAsync(eng->S.now + stream, &now, 8, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemsetAsync(eng->S.n_ev + o, 0, 4 * (size_t)Gl, st));
+    CUDA_TRY(cudaMemsetAsync(eng->S.pages_before + o, 0, 4 * (size_t)Gl, st));
+    CUDA_TRY(cudaMemsetAsync(eng->S.pages_after + o, 0, 4 * (size_t)Gl, st));
+    Dims d1 = D;
+    d1.only_s = stream;  // scheduler kernels for this stream only
+    if (D.Gl > 0) {
+        launch_sched_pages(d1, eng->C, eng->S, st);
+        launch_sched_select(d1, eng->C, eng->S, st);
+    }
+    launch_state_op(D, eng->C, eng->S, stream, 2, 0, 0, nullptr, 0, 0.0, st);  // state.step++ (scheduler.cpp:328)
+    CUDA_TRY(cudaGetLastError());
+    std::vector<int32_t> nev(Gl), pb(Gl), pa(Gl);
+    CUDA_TRY(cudaMemcpyAsync(nev.data(), eng->S.n_ev + o, 4 * (size_t)Gl, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(pb.data(), eng->S.pages_before + o, 4 * (size_t)Gl, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(pa.data(), eng->S.pages_after + o, 4 * (size_t)Gl, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    int32_t n = 0, sb = 0, sa = 0;
+    for (int gl = 0; gl < D.Gl; ++gl) {
+        sb += pb[gl], sa += pa[gl];
+        const int ne = std::min(nev[gl], std::max(0, cap - n));
+        if (out && ne > 0)
+            CUDA_TRY(cudaMemcpy(out + n, eng->S.rec_ev + (o + gl) * D.SPD * D.S, sizeof(pikv_evict_record) * ne,
+                                cudaMemcpyDeviceToHost));
+        n += nev[gl];
+    }
+    if (n_out) *n_out = n;
+    if (pages_before) *pages_before = sb;
+    if (pages_after) *pages_after = sa;
+    return PIKV_OK;
+}
+
+int pikv_attend_host(pikv_engine* eng, int32_t stream, const float* query, const int64_t* slots, int32_t n,
+                     float* y_out, float* alpha_out) {
+    int rc = component_check(eng, stream);
+    if (rc) return rc;
+    const Dims& D = eng->D;
+    if (!query || !y_out || (n > 0 && !slots)) return fail(PIKV_ERR_INVALID_ARGUMENT, "attend: NULL argument");
+    if (n == 0) {  // pipeline.cpp:63-66: zero vector, no weights
+        std::memset(y_out, 0, sizeof(float) * D.dp);
+        return PIKV_OK;
+    }
+    const int64_t ns = (int64_t)D.R * D.S;
+    for (int i = 0; i < n; ++i)
+        if (slots[i] < 0 || slots[i] >= ns) return fail(PIKV_ERR_INVALID_ARGUMENT, "attend: slot out of range");
+    if ((size_t)n * 4 > 200 * 1024) return fail(PIKV_ERR_INVALID_ARGUMENT, "attend: too many entries for one call");
+    const size_t kvb = 4 * (size_t)D.H * n * D.dph;
+    const size_t o_sl = 0, o_q = al256(8 * (size_t)n), o_k = o_q + al256(4 * (size_t)D.dp), o_v = o_k + al256(kvb);
+    const size_t o_y = o_v + al256(kvb), o_w = o_y + al256(4 * (size_t)D.dp), o_a = o_w + al256(4 * (size_t)D.H * n);
+    Scratch buf(o_a + 4 * (size_t)n);
+    if (buf.e != cudaSuccess) return fail(PIKV_ERR_CUDA, "attend: cudaMalloc");
+    cudaStream_t st = eng->stream;
+    CUDA_TRY(cudaMemcpyAsync(buf.at(o_sl), slots, 8 * (size_t)n, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(buf.at(o_q), query, 4 * (size_t)D.dp, cudaMemcpyHostToDevice, st));
+    launch_read_heads(D, eng->S, stream, (const int64_t*)buf.at(o_sl), n, (float*)buf.at(o_k), (float*)buf.at(o_v), st);
+    const size_t smem = sizeof(float) * (size_t)n;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_attention, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_attention<<<D.H, 256, smem, st>>>((const float*)buf.at(o_q), (const float*)buf.at(o_k), (const float*)buf.at(o_v),
+                                        n, D.dph, (float*)buf.at(o_y), (float*)buf.at(o_w));
+    launch_head_mean((const float*)buf.at(o_w), D.H, n, (float*)buf.at(o_a), st);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(y_out, buf.at(o_y), 4 * (size_t)D.dp, cudaMemcpyDeviceToHost, st));
+    if (alpha_out) CUDA_TRY(cudaMemcpyAsync(alpha_out, buf.at(o_a), 4 * (size_t)n, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return PIKV_OK;
+}
+
+int pikv_codec_encode(int32_t codec, int32_t rows, int32_t heads, int32_t hd, int32_t r, const float* basis,
+                      const float* bias, const int32_t* kept, const float* x, float* y) {
+    if (rows < 0 || heads < 1 || hd < 1) return fail(PIKV_ERR_INVALID_ARGUMENT, "codec: bad shape");
+    switch (codec) {
+        case PIKV_CODEC_IDENTITY:
+            CUDA_TRY(cudaMemcpy(y, x, 4 * (size_t)rows * heads * hd, cudaMemcpyDeviceToDevice));
+            return PIKV_OK;
+        case PIKV_CODEC_LOWRANK:
+        case PIKV_CODEC_LORAPLUS:
+            if (!basis || (codec == PIKV_CODEC_LORAPLUS && !bias)) return fail(PIKV_ERR_NOT_FITTED, "codec: basis/bias");
+            return pikv_lowrank_encode(x, basis, codec == PIKV_CODEC_LORAPLUS ? bias : nullptr, rows, heads, hd, r, y);
+        case PIKV_CODEC_FASTV:
+        case PIKV_CODEC_PRUNE:
+            if (r < 1 || r > hd || (codec == PIKV_CODEC_PRUNE && !kept))
+                return fail(PIKV_ERR_NOT_FITTED, "codec: rank / kept set");
+            launch_codec_select(0, codec, rows, heads, hd, r, kept, x, y, 0);
+            CUDA_TRY(cudaGetLastError());
+            CUDA_TRY(cudaDeviceSynchronize());
+            return PIKV_OK;
+    }
+    return fail(PIKV_ERR_CODEC_MISMATCH, "codec_encode: int8/int4 use pikv_quantize");
+}
+
+int pikv_codec_decode(int32_t codec, int32_t rows, int32_t heads, int32_t hd, int32_t r, const float* basis,
+                      const float* bias, const int32_t* kept, const float* y, float* x) {
+    if (rows < 0 || heads < 1 || hd < 1) return fail(PIKV_ERR_INVALID_ARGUMENT, "codec: bad shape");
+    switch (codec) {
+        case PIKV_CODEC_IDENTITY:
+            CUDA_TRY(cudaMemcpy(x, y, 4 * (size_t)rows * heads * hd, cudaMemcpyDeviceToDevice));
+            return PIKV_OK;
+        case PIKV_CODEC_LOWRANK:
+        case PIKV_CODEC_LORAPLUS:
+            if (!basis || (codec == PIKV_CODEC_LORAPLUS && !bias)) return fail(PIKV_ERR_NOT_FITTED, "codec: basis/bias");
+            return pikv_lowrank_decode(y, basis, codec == PIKV_CODEC_LORAPLUS ? bias : nullptr, rows, heads, hd, r, x);
+        case PIKV_CODEC_FASTV:
+        case PIKV_CODEC_PRUNE:
+            if (r < 1 || r > hd || (codec == PIKV_CODEC_PRUNE && !kept))
+                return fail(PIKV_ERR_NOT_FITTED, "codec: rank / kept set");
+            launch_codec_select(1, codec, rows, heads, hd, r, kept, y, x, 0);
+            CUDA_TRY(cudaGetLastError());
+            CUDA_TRY(cudaDeviceSynchronize());
+            return PIKV_OK;
+    }
+    return fail(PIKV_ERR_CODEC_MISMATCH, "codec_decode: int8/int4 use pikv_dequantize");
+}
+
+static int codec_host(bool decode, int32_t codec, int32_t rows, int32_t heads, int32_t hd, int32_t r,
+                      const float* basis, const float* bias, const int32_t* kept, const float* in, float* out) {
+    const int wi = decode ? (codec == PIKV_CODEC_IDENTITY ? hd : r) : hd;
+    const int wo = decode ? hd : (codec == PIKV_CODEC_IDENTITY ? hd : r);
+    const size_t nin = 4 * (size_t)rows * heads * wi, nout = 4 * (size_t)rows * heads * wo;
+    const size_t nb = basis ? 4 * (size_t)heads * r * hd : 0, nbias = bias ? 4 * (size_t)heads * hd : 0;
+    const size_t nk = kept ? 4 * (size_t)heads * r : 0;
+    const size_t o_in = 0, o_out = al256(nin), o_b = o_out + al256(nout), o_bias = o_b + al256(nb);
+    const size_t o_k = o_bias + al256(nbias);
+    Scratch buf(o_k + nk + 16);
+    if (buf.e != cudaSuccess) return fail(PIKV_ERR_CUDA, "codec: cudaMalloc");
+    CUDA_TRY(cudaMemcpy(buf.at(o_in), in, nin, cudaMemcpyHostToDevice));
+    if (nb) CUDA_TRY(cudaMemcpy(buf.at(o_b), basis, nb, cudaMemcpyHostToDevice));
+    if (nbias) CUDA_TRY(cudaMemcpy(buf.at(o_bias), bias, nbias, cudaMemcpyHostToDevice));
+    if (nk) CUDA_TRY(cudaMemcpy(buf.at(o_k), kept, nk, cudaMemcpyHostToDevice));
+    auto* fb = nb ? (const float*)buf.at(o_b) : nullptr;
+    auto* fbias = nbias ? (const float*)buf.at(o_bias) : nullptr;
+    auto* fk = nk ? (const int32_t*)buf.at(o_k) : nullptr;
+    int rc = decode ? pikv_codec_decode(codec, rows, heads, hd, r, fb, fbias, fk, (const float*)buf.at(o_in),
+                                        (float*)buf.at(o_out))
+                    : pikv_codec_encode(codec, rows, heads, hd, r, fb, fbias, fk, (const float*)buf.at(o_in),
+                                        (float*)buf.at(o_out));
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpy(out, buf.at(o_out), nout, cudaMemcpyDeviceToHost));
+    return PIKV_OK;
+}
+
+int pikv_codec_encode_host(int32_t codec, int32_t rows, int32_t heads, int32_t hd, int32_t r, const float* basis,
+                           const float* bias, const int32_t* kept, const float* x, float* y) {
+    return codec_host(false, codec, rows, heads, hd, r, basis, bias, kept, x, y);
+}
+
+int pikv_codec_decode_host(int32_t codec, int32_t rows, int32_t heads, int32_t hd, int32_t r, const float* basis,
+                           const float* bias, const int32_t* kept, const float* y, float* x) {
+    return codec_host(true, codec, rows, heads, hd, r, basis, bias, kept, y, x);
+}
+
+int pikv_column_variance_host(const double* rows, int32_t n, int32_t d, double* var) {
+    if (n < 1 || d < 1 || !rows || !var) return fail(PIKV_ERR_INSUFFICIENT_CALIBRATION, "column variance: no rows");
+    const size_t nx = 8 * (size_t)n * d;
+    Scratch buf(al256(nx) + 8 * (size_t)d);
+    if (buf.e != cudaSuccess) return fail(PIKV_ERR_CUDA, "variance: cudaMalloc");
+    CUDA_TRY(cudaMemcpy(buf.at(0), rows, nx, cudaMemcpyHostToDevice));
+    launch_col_var((const double*)buf.at(0), n, d, (double*)buf.at(al256(nx)), 0);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpy(var, buf.at(al256(nx)), 8 * (size_t)d, cudaMemcpyDeviceToHost));
     return PIKV_OK;
 }
 

@@ -55,7 +55,7 @@ constexpr int kRouteStages = 5;
 // dynamic shared memory (route_smem_bytes(CH)).
 __device__ __forceinline__ const int* route_body(const Dims& D, const Cfg& C, const State& S, const int s,
                                            const void* __restrict__ qin, const int kRouteCH,
-                                           uint8_t* sm_raw) {
+                                           uint8_t* sm_raw, const double* logits_in = nullptr) {
     uint64_t* full = (uint64_t*)sm_raw;
     uint64_t* empty = full + kRouteStages;
     double* sm_q = (double*)(sm_raw + 128);
@@ -101,8 +101,9 @@ __device__ __forceinline__ const int* route_body(const Dims& D, const Cfg& C, co
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     // query in fp64 (exact upcast of bf16/f32, or the encoder's fp64 q);
-    // 16-byte loads, all in flight
-    if (D.q_f64) {
+    // 16-byte loads, all in flight.  route_logits (logits_in): no query
+    if (logits_in) {
+    } else if (D.q_f64) {
         const double2* qd = (const double2*)((const double*)qin + (int64_t)s * D.d);
         if (D.d % 2 == 0)
             for (int v = tid; v < D.d / 2; v += blockDim.x) ((double2*)sm_q)[v] = qd[v];
@@ -151,7 +152,11 @@ __device__ __forceinline__ const int* route_body(const Dims& D, const Cfg& C, co
     __syncthreads();
     if (dbg) S.dbg[1] = clock64();
     const bool base = C.router_strategy == PIKV_ROUTER_BASE;
-    if (!base) {
+    if (logits_in && !base) {  // route_logits, router.cpp:122-214: the given logits
+        for (int e = tid; e < D.E; e += blockDim.x) sm_logit[e] = logits_in[e];
+        __syncthreads();
+    }
+    if (!base && !logits_in) {
         const int E = D.E, CH = kRouteCH;
         const int nchunk = (D.d + CH - 1) / CH;
         const int warp = tid >> 5, lane = tid & 31;
@@ -234,6 +239,24 @@ __global__ void k_route(Dims D, Cfg C, State S, const void* __restrict__ qin) {
     griddep_enter();
     extern __shared__ __align__(128) uint8_t sm_raw[];
     route_body(D, C, S, blockIdx.x, qin, D.route_ch, sm_raw);
+}
+
+// route / route_logits of one stream (component API, pikv_route_host):
+// q [B][d] fp64 staging with the query in row s, or logits [E].
+__global__ void k_route_one(Dims D, Cfg C, State S, int s, const double* __restrict__ q,
+                            const double* __restrict__ logits) {
+    extern __shared__ __align__(128) uint8_t sm_raw[];
+    route_body(D, C, S, s, q, D.route_ch, sm_raw, logits);
+}
+static size_t route_smem_bytes(const Dims& D, int ch);
+void launch_route_one(const Dims& D, const Cfg& C, const State& S, int s, const double* q, const double* logits,
+                      cudaStream_t st) {
+    Dims d1 = D;
+    d1.q_f64 = 1;
+    const size_t smem = route_smem_bytes(d1, d1.route_ch);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_route_one, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int threads = ((D.E + 31) / 32) * 32 + 32;
+    k_route_one<<<1, threads, smem, st>>>(d1, C, S, s, q, logits);
 }
 
 // Warp 0 of k_route: penalties, selection, gates, note_selection and the
@@ -427,38 +450,6 @@ void launch_route(const Dims& D, const Cfg& C, const State& S, const void* q, cu
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_route, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int threads = ((D.E + 31) / 32) * 32 + 32;
     launch_pdl(k_route, dim3(D.B), dim3(threads), smem, st, D, C, S, q);
-}
-
-// page-record maintenance (see State::pr_*)
-__device__ __forceinline__ int64_t page_rec(const Dims& D, int64_t ring, uint64_t shard_seq) {
-    return ring * D.ppr_sched + (int64_t)((shard_seq / (uint64_t)D.page_size) % (uint64_t)D.ppr_sched);
-}
-__device__ __forceinline__ void rec_append(const Dims& D, const State& S, int64_t ring, uint64_t sq,
-                                           uint64_t now) {
-    const int64_t r = page_rec(D, ring, sq);
-    if (S.pr_cnt[r] == 0) {
-        atomicAdd(&S.pages_live[ring / D.SPD], 1);  // a page comes to life
-        S.pr_cnt[r] = 1;
-        S.pr_first[r] = (int)(sq % (uint64_t)D.page_size);
-        S.pr_sla[r] = now;
-        S.pr_sf[r] = 0;
-    } else {
-        S.pr_cnt[r] += 1;
-        S.pr_sla[r] += now;
-    }
-}
-__device__ __forceinline__ void rec_drop_front(const Dims& D, const State& S, int64_t ring, uint64_t sq,
-                                               uint64_t la, uint64_t fr) {
-    const int64_t r = page_rec(D, ring, sq);
-    if (--S.pr_cnt[r] == 0) atomicSub(&S.pages_live[ring / D.SPD], 1);  // last member displaced
-    S.pr_first[r] += 1;
-    S.pr_sla[r] -= la;
-    S.pr_sf[r] -= fr;
-}
-
-__device__ __forceinline__ float load_in(const void* p, int dtype, int64_t i) {
-    if (dtype == PIKV_DTYPE_BF16) return __uint_as_float(((uint32_t)((const uint16_t*)p)[i]) << 16);
-    return ((const float*)p)[i];
 }
 
 // ===========================================================================
@@ -774,6 +765,7 @@ __device__ __forceinline__ void insert_book(const Dims& D, const State& S, const
         }
         if (--dcnt == 0) --pl_delta;  // last member displaced
         dfirst += 1;
+        if (D.holes && dcnt > 0) dfirst = next_member(D, S, ring, osq / (uint64_t)D.page_size, dfirst);
         dsla -= ola;
         dsf -= ofr;
         if (drec == arec) acnt = dcnt, afirst = dfirst, asla = dsla, asf = dsf;
@@ -1026,7 +1018,8 @@ __global__ void k_sched_pages(Dims D, Cfg C, State S, int lanes) {
     const int64_t ring = in ? t / D.ppr_sched : 0;
     const int pi = in ? (int)(t % D.ppr_sched) : 0;
     const int s = (int)(ring / D.R);
-    const uint64_t seq = in ? S.seq[ring] : 0;
+    const bool skip = D.only_s >= 0 && s != D.only_s;  // pikv_evict_host: one stream
+    const uint64_t seq = in && !skip ? S.seq[ring] : 0;
     const uint64_t Su = (uint64_t)D.S, ps = (uint64_t)D.page_size;
     const uint64_t lo = seq > Su ? seq - Su : 0;
     const uint64_t q = lo / ps + (uint64_t)pi;
@@ -1034,7 +1027,7 @@ __global__ void k_sched_pages(Dims D, Cfg C, State S, int lanes) {
     if (C.record_agg) {  // lanes == 1
         // devices within budget evict nothing: select decides from the
         // live-page counter and never reads their keys
-        if (!in || S.pages_live[ring / D.SPD] <= C.budget_pages) return;
+        if (!in || skip || S.pages_live[ring / D.SPD] <= C.budget_pages) return;
         double agg = 0.0;
         uint64_t oldest = 0;
         const int c2 = S.err[s] ? 0 : page_key_rec(D, C, S, ring, pi, S.now[s], agg, oldest);
@@ -1043,7 +1036,7 @@ __global__ void k_sched_pages(Dims D, Cfg C, State S, int lanes) {
         S.pg_oldest[t] = oldest;
         return;
     }
-    const int cnt = (in && q * ps < seq) ? S.pr_cnt[rec] : 0;
+    const int cnt = (in && !skip && q * ps < seq) ? S.pr_cnt[rec] : 0;
     const bool live_page = cnt > 0 && !S.err[s];
     const uint64_t now = in ? S.now[s] : 0;
     const int first = live_page ? S.pr_first[rec] : 0;
@@ -1058,7 +1051,7 @@ __global__ void k_sched_pages(Dims D, Cfg C, State S, int lanes) {
         uint64_t id = 0;
         if (live_page && u < (int)ps) {
             const int i = (w + u) % (int)ps;  // member offset in slot order
-            if (i >= first && i < first + cnt) {
+            if (D.holes ? page_member(D, S, ring, q, i) : (i >= first && i < first + cnt)) {
                 const int64_t gi = ring * D.S + (int64_t)((q * ps + (uint64_t)i) % Su);
                 id = S.id[gi];
                 sc = score_entry(C, S, gi, now, D.n_layers);
@@ -1084,7 +1077,7 @@ __global__ void k_sched_pages(Dims D, Cfg C, State S, int lanes) {
         const uint64_t o2 = __shfl_xor_sync(0xffffffffu, oldest, off);
         oldest = o2 < oldest ? o2 : oldest;
     }
-    if (in && u0 == 0) {
+    if (in && !skip && u0 == 0) {
         S.pg_cnt[t] = live_page ? cnt : 0;
         S.pg_agg[t] = agg;
         S.pg_oldest[t] = live_page ? oldest : 0;
@@ -1430,6 +1423,7 @@ __device__ __forceinline__ bool within_budget(const Dims& D, const Cfg& C, const
 __device__ __forceinline__ void select_body(const Dims& D, const Cfg& C, const State& S, const int sg,
                                             const bool stage) {
     const int s = sg / D.Gl;
+    if (D.only_s >= 0 && s != D.only_s) return;  // pikv_evict_host: one stream
     if (S.err[s]) return;
     if (within_budget(D, C, S, sg)) return;
     const int64_t f0 = (int64_t)sg * D.SPD * D.ppr_sched;
@@ -2374,6 +2368,8 @@ __device__ __forceinline__ void feedback_stream(const Dims& D, const Cfg& C, con
         if (S.found[(int64_t)s * k + j] > 0) ++hits;
         else S.miss[(int64_t)s * E + S.experts[(int64_t)s * k + j]] += 1;
     }
+    S.st_retrievals[s] += 1;  // KVStore::retrieve stats (kvstore.cpp:169-176)
+    S.st_misses[s] += (uint64_t)(k - hits);
     const double reward = __ddiv_rn((double)hits, (double)k);
     if (C.router_strategy == PIKV_ROUTER_ADAPTIVE) {  // adapt, router.cpp:243-255
         double* bias = S.bias + (int64_t)s * E;
@@ -3174,6 +3170,51 @@ void launch_snapshot(const Dims& D, const State& S, int s, uint64_t now, const i
                      pikv_snapshot_record* out, int64_t n, cudaStream_t st) {
     if (D.R > 0) k_snapshot<<<D.R, 256, 0, st>>>(D, S, s, now, ring_off, out);
     if (n > 0) k_snapshot_ties<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(out, n);
+}
+
+// Stored K/V of n slots of stream s decoded to fp32 (the values the
+// attention reads): KVEntry::key / value of the reference (types.hpp:27-34)
+// for the store facade and the full-context parity checks.  slot = the
+// stream-local index ring_local * S + slot; empty slots decode to zeros.
+__global__ void k_read_entries(Dims D, State S, int s, const int64_t* __restrict__ slots, int n,
+                               float* __restrict__ kout, float* __restrict__ vout) {
+    const int i = blockIdx.x;
+    if (i >= n) return;
+    const int64_t ls = slots[i];
+    const int64_t ring = (int64_t)s * D.R + ls / D.S;
+    const int slot = (int)(ls % D.S);
+    const int64_t gi = ring * D.S + slot;
+    const int32_t page = S.page_table[ring * D.ppr + slot / D.spg];
+    const bool live = S.id[gi] != 0 && page >= 0;
+    const uint8_t* ent = live ? S.pool + ((int64_t)page * D.spg + slot % D.spg) * D.entry_bytes : nullptr;
+    const int pay = D.payload_bytes, hw = D.dph;
+    for (int o = threadIdx.x; o < 2 * D.dp; o += blockDim.x) {
+        const int row = o / D.dp, c = o % D.dp;
+        float x = 0.f;
+        if (live) {
+            const uint8_t* p = ent + row * pay;
+            if (D.codec == PIKV_CODEC_INT8 || D.codec == PIKV_CODEC_INT4) {
+                const float sc = ((const float*)(ent + 2 * pay))[row * D.H + c / hw];
+                int code;
+                if (D.codec == PIKV_CODEC_INT8) {
+                    code = (int)((const int8_t*)p)[c];
+                } else {
+                    const int nib = (p[c >> 1] >> ((c & 1) * 4)) & 0xF;
+                    code = nib >= 8 ? nib - 16 : nib;
+                }
+                x = __fmul_rn((float)code, sc);
+            } else if (D.kv_dtype == PIKV_DTYPE_BF16) {
+                x = __uint_as_float(((uint32_t)((const uint16_t*)p)[c]) << 16);
+            } else {
+                x = ((const float*)p)[c];
+            }
+        }
+        (row ? vout : kout)[(int64_t)i * D.dp + c] = x;
+    }
+}
+void launch_read_entries(const Dims& D, const State& S, int s, const int64_t* slots, int n, float* k, float* v,
+                         cudaStream_t st) {
+    if (n > 0) k_read_entries<<<n, 256, 0, st>>>(D, S, s, slots, n, k, v);
 }
 
 // token / expert of a list of slots (pikv_read_attended_host)

@@ -65,6 +65,9 @@ struct Dims {
     int ctl_cl, ctl_smem;  // k_control cluster size and dynamic smem (control_geometry)
     int att_eps;           // k_attend entries per ring stage (item sizes are multiples)
     int dbg_ctl;        // k_control phase timestamps into dbg[64 + 8 s + p] (PIKV_DEBUG_CTL=1)
+    int only_s;         // >= 0: the scheduler kernels evict this stream only (pikv_evict_host)
+    int holes;          // an arbitrary KVStore::erase happened: page members are not a
+                        // contiguous range, membership is checked per slot
 };
 
 struct Cfg {  // scalar config needed on device (copied by value into kernels)
@@ -99,6 +102,8 @@ struct State {
     int32_t* err;       // per stream
     uint64_t* st_inserts;
     uint64_t* st_overwrites;
+    uint64_t* st_retrievals;  // StoreStats (kvstore.hpp:74-79): retrieve calls
+    uint64_t* st_misses;      // and missed experts
     // rings
     int32_t* head;
     int32_t* live;
@@ -208,31 +213,37 @@ __device__ __forceinline__ uint64_t dkey(double x) {
     return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
 }
 
-// score_entry, scheduler.cpp:181-229 (QUEST rejected at create).
-__device__ __forceinline__ double score_entry(const Cfg& c, const State& st, int64_t gi,
-                                              uint64_t now, int n_layers) {
-    uint64_t ins = st.insert_step[gi], la = st.last_access[gi];
-    uint64_t age = now >= ins ? now - ins : 0;
-    uint64_t rec = now >= la ? now - la : 0;
+// score_entry, scheduler.cpp:181-229 (QUEST rejected at create).  `m`
+// reads one entry's EntryMeta fields (types.hpp:11-24) lazily: each
+// strategy loads only what it scores.
+template <class Meta>
+__device__ __forceinline__ double score_impl(const Cfg& c, const Meta& m, int n_layers, uint64_t now) {
     switch (c.sched_strategy) {
         case PIKV_SCHED_H2O:
-            return st.attn_mass[gi];
+            return m.mass();
         case PIKV_SCHED_SL: {
+            const uint64_t ins = m.ins(), age = now >= ins ? now - ins : 0;
             double u = (double)age <= c.tau ? 1.0 : 0.0;
-            if (st.token[gi] < c.sink) u = __dadd_rn(u, 2.0);
+            if (m.token() < c.sink) u = __dadd_rn(u, 2.0);
             return u;
         }
         case PIKV_SCHED_FLEX: {
+            const uint64_t ins = m.ins(), age = now >= ins ? now - ins : 0;
             uint64_t bucket = age / (uint64_t)c.flex_bucket;
             if (bucket >= (uint64_t)c.n_flex_plan) bucket = (uint64_t)c.n_flex_plan - 1;
             return c.flex_plan[bucket];
         }
-        case PIKV_SCHED_LRU:
-            return -(double)rec;
-        case PIKV_SCHED_LRU_PLUS:
-            return __dadd_rn(-(double)rec, __dmul_rn(c.lambda_freq, (double)st.freq[gi]));
+        case PIKV_SCHED_LRU: {
+            const uint64_t la = m.la();
+            return -(double)(now >= la ? now - la : 0);
+        }
+        case PIKV_SCHED_LRU_PLUS: {
+            const uint64_t la = m.la();
+            return __dadd_rn(-(double)(now >= la ? now - la : 0), __dmul_rn(c.lambda_freq, (double)m.freq()));
+        }
         case PIKV_SCHED_ADAKV: {
-            double phi0 = st.attn_mass[gi], phi1 = (double)st.freq[gi];
+            const uint64_t ins = m.ins(), age = now >= ins ? now - ins : 0;
+            double phi0 = m.mass(), phi1 = (double)m.freq();
             double phi2 = __ddiv_rn(1.0, __dadd_rn(1.0, (double)age));
             double u = 0.0;
             if (c.n_adakv_weights > 0) u = __dadd_rn(u, __dmul_rn(c.adakv_weights[0], phi0));
@@ -242,13 +253,78 @@ __device__ __forceinline__ double score_entry(const Cfg& c, const State& st, int
         }
         case PIKV_SCHED_DUO: {
             double u = 0.0;
-            if (!st.has_pl[gi]) return u;  // empty per_layer_scores
-            const double* pl = st.per_layer + gi * (int64_t)n_layers;
+            if (!m.has_pl()) return u;  // empty per_layer_scores
+            const double* pl = m.pl();
             for (int l = 0; l < n_layers; ++l) u = __dadd_rn(u, pl[l]);
             return u;
         }
     }
     return 0.0;
+}
+
+struct SlotMeta {  // stored slot gi
+    const State& st;
+    int64_t gi;
+    int n_layers;
+    __device__ uint64_t ins() const { return st.insert_step[gi]; }
+    __device__ uint64_t la() const { return st.last_access[gi]; }
+    __device__ uint64_t freq() const { return st.freq[gi]; }
+    __device__ double mass() const { return st.attn_mass[gi]; }
+    __device__ int64_t token() const { return st.token[gi]; }
+    __device__ bool has_pl() const { return st.has_pl[gi] != 0; }
+    __device__ const double* pl() const { return st.per_layer + gi * (int64_t)n_layers; }
+};
+
+__device__ __forceinline__ double score_entry(const Cfg& c, const State& st, int64_t gi,
+                                              uint64_t now, int n_layers) {
+    return score_impl(c, SlotMeta{st, gi, n_layers}, n_layers, now);
+}
+
+// page-record maintenance (see State::pr_*)
+__device__ __forceinline__ int64_t page_rec(const Dims& D, int64_t ring, uint64_t shard_seq) {
+    return ring * D.ppr_sched + (int64_t)((shard_seq / (uint64_t)D.page_size) % (uint64_t)D.ppr_sched);
+}
+__device__ __forceinline__ void rec_append(const Dims& D, const State& S, int64_t ring, uint64_t sq,
+                                           uint64_t now) {
+    const int64_t r = page_rec(D, ring, sq);
+    if (S.pr_cnt[r] == 0) {
+        atomicAdd(&S.pages_live[ring / D.SPD], 1);  // a page comes to life
+        S.pr_cnt[r] = 1;
+        S.pr_first[r] = (int)(sq % (uint64_t)D.page_size);
+        S.pr_sla[r] = now;
+        S.pr_sf[r] = 0;
+    } else {
+        S.pr_cnt[r] += 1;
+        S.pr_sla[r] += now;
+    }
+}
+// Is offset i of scheduler page q of `ring` a live member (slot holds that shard_seq)?
+__device__ __forceinline__ bool page_member(const Dims& D, const State& S, int64_t ring, uint64_t q, int i) {
+    const uint64_t sq = q * (uint64_t)D.page_size + (uint64_t)i;
+    const int64_t gi = ring * D.S + (int64_t)(sq % (uint64_t)D.S);
+    return S.id[gi] != 0 && S.shard_seq[gi] == sq;
+}
+// First live member offset >= `from` of page q (after the previous first
+// left): from itself unless arbitrary erases left holes (D.holes).
+__device__ __forceinline__ int next_member(const Dims& D, const State& S, int64_t ring, uint64_t q, int from) {
+    if (!D.holes) return from;
+    while (from < D.page_size && !page_member(D, S, ring, q, from)) ++from;
+    return from;
+}
+__device__ __forceinline__ void rec_drop_front(const Dims& D, const State& S, int64_t ring, uint64_t sq,
+                                               uint64_t la, uint64_t fr) {
+    const int64_t r = page_rec(D, ring, sq);
+    if (--S.pr_cnt[r] == 0) atomicSub(&S.pages_live[ring / D.SPD], 1);  // last member displaced
+    S.pr_first[r] += 1;
+    if (D.holes && S.pr_cnt[r] > 0)
+        S.pr_first[r] = next_member(D, S, ring, sq / (uint64_t)D.page_size, S.pr_first[r]);
+    S.pr_sla[r] -= la;
+    S.pr_sf[r] -= fr;
+}
+
+__device__ __forceinline__ float load_in(const void* p, int dtype, int64_t i) {
+    if (dtype == PIKV_DTYPE_BF16) return __uint_as_float(((uint32_t)((const uint16_t*)p)[i]) << 16);
+    return ((const float*)p)[i];
 }
 
 // ---- mbarrier / TMA bulk-copy helpers (sm_90+ PTX; SASS SYNCS.* / UBLKCP) ----
@@ -412,6 +488,29 @@ void launch_snapshot(const Dims& D, const State& S, int s, uint64_t now, const i
 void launch_synth(const Dims& D, void* q, void* k, void* v, uint64_t seed, uint64_t step,
                   cudaStream_t st);
 int attend_max_smem();
+// ---- component API (components.cu; pikv_route_host / pikv_store_* / ...) ----
+void launch_route_one(const Dims& D, const Cfg& C, const State& S, int s, const double* q, const double* logits,
+                      cudaStream_t st);
+void launch_store_insert(const Dims& D, const State& S, int s, int n, const pikv_entry* in, const float* kv,
+                         const double* layers, pikv_entry* disp, float* disp_kv, double* disp_layers,
+                         int32_t* disp_flag, int32_t* status, cudaStream_t st);
+void launch_store_erase(const Dims& D, const State& S, int s, uint64_t id, int32_t* status, cudaStream_t st);
+size_t retrieve_scratch_bytes(const Dims& D);
+int launch_retrieve(const Dims& D, const State& S, int s, int64_t since, uint64_t now, const uint32_t* want,
+                    void* scratch, int32_t** sorted_out, int32_t** cnt_out, uint32_t** found_out, cudaStream_t st);
+void launch_score_meta(const Cfg& C, const pikv_entry* m, const double* layers, int n_layers, int n, uint64_t now,
+                       double* out, cudaStream_t st);
+void launch_state_op(const Dims& D, const Cfg& C, const State& S, int s, int op, uint64_t a, uint64_t b,
+                     const int32_t* experts, int n, double reward, cudaStream_t st);
+void launch_read_heads(const Dims& D, const State& S, int s, const int64_t* slots, int n, float* kh, float* vh,
+                       cudaStream_t st);
+void launch_head_mean(const float* w, int H, int n, float* out, cudaStream_t st);
+void launch_codec_select(int decode, int codec, int64_t rows, int heads, int hd, int r, const int32_t* kept,
+                         const float* x, float* y, cudaStream_t st);
+void launch_col_var(const double* x, int n, int d, double* var, cudaStream_t st);
+// stored K/V of n stream-local slots decoded to fp32 (readback)
+void launch_read_entries(const Dims& D, const State& S, int s, const int64_t* slots, int n, float* k, float* v,
+                         cudaStream_t st);
 // token / expert of n slots (global slot indices) -> out arrays (readback)
 void launch_gather_slots(const State& S, const int32_t* slot, int n, int64_t* token, int32_t* expert,
                          cudaStream_t st);

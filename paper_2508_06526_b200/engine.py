@@ -299,8 +299,10 @@ class Engine:
         return experts, gates, logits, summary
 
     def read_evictions(self, cap: int = 1 << 20) -> List[EvictionRecord]:
-        buf = (PikvEvictRecord * cap)()
         n = ctypes.c_int32(0)
+        check(lib().pikv_read_evictions_host(self.h, None, 0, ctypes.byref(n)))  # count
+        cap = min(cap, n.value)
+        buf = (PikvEvictRecord * max(cap, 1))()
         check(lib().pikv_read_evictions_host(self.h, ctypes.addressof(buf), cap, ctypes.byref(n)))
         return [EvictionRecord(r.step, r.entry_id, r.token_id, r.expert_id, r.device, r.score,
                                REASON[r.reason], r.stream) for r in buf[:min(n.value, cap)]]
@@ -342,6 +344,14 @@ class Engine:
         check(lib().pikv_read_slots_host(self.h, stream, *[_np_ptr(out[c]) for c in cols],
                                          _np_ptr(out["per_layer"]) if nl > 0 else None))
         return out
+
+    def read_entries(self, stream: int, slots):
+        """Stored K, V of stream-local slots decoded to fp32 ([n][d'] each)."""
+        sl = np.ascontiguousarray(slots, dtype=np.int64)
+        k = np.zeros((len(sl), self.dp), dtype=np.float32)
+        v = np.zeros((len(sl), self.dp), dtype=np.float32)
+        check(lib().pikv_read_entries_host(self.h, stream, _np_ptr(sl), len(sl), _np_ptr(k), _np_ptr(v)))
+        return k, v
 
     def set_attn_mass(self, stream: int, attn_mass, per_layer=None):
         a = np.ascontiguousarray(attn_mass, dtype=np.float64)

@@ -228,6 +228,157 @@ int main() {
         cfg.scheduler.strategy = SchedStrategy::QUEST;
         CHECK_THROWS_AS(Engine{cfg}, NotFitted);
     }
+    // ---- component classes (kvstore / router / scheduler / compressor) ----
+    {  // test_kvstore.cpp:72-88: ring fill then FIFO overwrite (one shard)
+        ModelConfig m;
+        m.d = 2, m.head_width = 1, m.E = 8, m.k = 1, m.S = 4, m.G = 1;
+        KVStore st(m, StoreConfig{1, 1, false, 0});
+        auto mk = [](std::int64_t t) { KVEntry e; e.token_id = t; e.key.assign(2, 1.0); e.value.assign(2, 1.0); return e; };
+        CHECK(!st.insert(mk(0)).has_value());
+        CHECK(st.live_count(0, 0) == 1);
+        for (int t = 1; t < 4; ++t) st.insert(mk(t));
+        auto fifth = st.insert(mk(4));
+        CHECK(fifth.has_value() && fifth->token_id == 0);
+        for (int t = 5; t < 7; ++t) st.insert(mk(t));
+        auto eighth = st.insert(mk(7));
+        CHECK(eighth.has_value() && eighth->token_id == 3);
+        CHECK(st.live_count(0, 0) == 4);
+        KVEntry bad = mk(9);
+        bad.key.assign(3, 1.0);
+        CHECK_THROWS_AS(st.insert(bad), InvalidEntry);  // test_kvstore.cpp:109-112
+    }
+    {  // test_kvstore.cpp:114-160, 220-230
+        ModelConfig m;
+        m.d = 4, m.head_width = 1, m.E = 8, m.k = 1, m.S = 16, m.G = 1;
+        KVStore st(m, StoreConfig{8, 8, false, 0});
+        auto r0 = st.retrieve({2}, 100, 100);
+        CHECK(r0.entries.empty() && r0.missed_experts == std::vector<int>{2} && st.stats().misses == 1);
+        for (std::int64_t t = 0; t < 12; ++t) {
+            KVEntry e;
+            e.token_id = t, e.expert_id = static_cast<int>(t % 3);
+            e.key.assign(4, 1.0), e.value.assign(4, 1.0);
+            st.insert(e);
+        }
+        auto r = st.retrieve({0, 2}, 12, 12);
+        std::vector<std::int64_t> got, want;
+        for (const auto& e : r.entries) got.push_back(e.token_id);
+        for (std::int64_t t = 0; t < 12; ++t)
+            if (t % 3 != 1) want.push_back(t);
+        CHECK(got == want);
+        CHECK(r.entries[0].meta.freq == 1 && r.entries[0].meta.last_access_step == 12);
+        const auto id = r.entries[0].id;
+        CHECK(st.erase(id));
+        CHECK(!st.erase(id));
+        CHECK(st.live_entries() == 11);
+        auto snap = st.snapshot(12);
+        CHECK(snap.size() == 11);
+    }
+    {  // test_kvstore.cpp:178-205: memory accounting
+        ModelConfig m;
+        m.d = 16, m.head_width = 1, m.E = 8, m.k = 1, m.S = 8, m.G = 1, m.elem_bytes = 2;
+        KVStore st(m, StoreConfig{2, 1, false, 0});
+        auto mk = [](std::int64_t t) { KVEntry e; e.token_id = t; e.key.assign(16, 1.0); e.value.assign(16, 1.0); return e; };
+        for (std::int64_t t : {0, 2, 4}) st.insert(mk(t));
+        for (std::int64_t t : {1, 3, 5, 7, 9}) st.insert(mk(t));
+        CHECK(st.live_count(0, 0) == 3 && st.live_count(0, 1) == 5 && st.memory_bytes() == 512);
+    }
+    {  // test_router.cpp:34-117, 281-291
+        RouterState base = RouterState::init(4, 8, 1);
+        RouterConfig rb;
+        rb.strategy = RouterStrategy::Base, rb.k = 1;
+        for (int t = 0; t < 4; ++t) {
+            auto d = route(std::vector<double>(8, 0.0), base, rb);
+            CHECK(d.experts.size() == 1 && d.experts[0] == t && std::fabs(d.gates[0] - 1.0) < 1e-12);
+        }
+        RouterState st = RouterState::init(4, 4, 1);
+        RouterConfig top;
+        top.strategy = RouterStrategy::TopK, top.k = 2;
+        auto d = route_logits({2, 1, 0, -1}, st, top);
+        CHECK((d.experts == std::vector<int>{0, 1}));
+        CHECK(std::fabs(d.gates[0] - 0.7310585786300049) <= 1e-12 && std::fabs(d.gates[1] - 0.2689414213699951) <= 1e-12);
+        RouterState lb = RouterState::init(4, 4, 1);
+        RouterConfig lbc;
+        lbc.strategy = RouterStrategy::LoadBalanced, lbc.k = 1, lbc.alpha = 0.5;
+        lb.bind(lbc);
+        lb.set_load({10, 0, 0, 0});
+        CHECK(route_logits({1, 1, 1, 1}, lb, lbc).experts[0] == 1);
+        record_miss(st, 2, top);
+        record_miss(st, 2, top);
+        CHECK(st.view().miss_counts[2] == 2);
+        CHECK_THROWS_AS(record_miss(st, 4, top), InvalidArgument);
+        RouterConfig ad;
+        ad.strategy = RouterStrategy::Adaptive, ad.k = 2, ad.bandit_step = 0.1;
+        RouterState sa = RouterState::init(4, 4, 1);
+        RoutingDecision dec;
+        dec.experts = {0, 2};
+        adapt(sa, dec, 1.0, ad);
+        auto v = sa.view();
+        CHECK(std::fabs(v.bandit_bias[0] - 0.1) < 1e-12 && std::fabs(v.bandit_bias[2] - 0.1) < 1e-12 && v.bandit_bias[1] == 0.0);
+        CHECK_THROWS_AS(adapt(sa, dec, 1.5, ad), InvalidArgument);
+        CHECK_THROWS_AS(route_logits({0.0, std::nan(""), 1.0, 2.0}, st, top), NumericalError);
+    }
+    {  // test_scheduler.cpp:75-104, 236-259, 277-292
+        KVEntry e;
+        e.meta.attn_mass = 0.37;
+        SchedulerConfig h2o;
+        h2o.strategy = SchedStrategy::H2O;
+        CHECK(std::fabs(score_entry(e, h2o, 5) - 0.37) < 1e-15);
+        KVEntry l;
+        l.meta.last_access_step = 3, l.meta.freq = 3;
+        SchedulerConfig lp;
+        lp.strategy = SchedStrategy::LRUPlus, lp.lambda_freq = 0.5;
+        CHECK(score_entry(l, lp, 5) == -0.5);
+        ModelConfig m;
+        m.d = 2, m.head_width = 1, m.E = 4, m.k = 1, m.S = 16, m.G = 1;
+        KVStore st(m, StoreConfig{1, 1, false, 0}, /*page_size=*/1);
+        const double attn[4] = {5.0, 1.0, 3.0, 2.0};
+        for (int t = 0; t < 4; ++t) {
+            KVEntry x;
+            x.token_id = t, x.key.assign(2, 1.0), x.value.assign(2, 1.0), x.meta.attn_mass = attn[t];
+            st.insert(x);
+        }
+        SchedulerConfig c;
+        c.strategy = SchedStrategy::H2O, c.page_size = 1, c.budget_pages = 2;
+        auto rep = st.evict(c, 4);
+        CHECK(rep.pages_before == 4 && rep.pages_after == 2 && rep.evicted.size() == 2);
+        CHECK(rep.evicted.size() == 2 && rep.evicted[0].token_id == 1 && rep.evicted[1].token_id == 3);
+        CHECK(st.live_entries() == 2 && st.evict(c, 5).evicted.empty());
+        SchedulerConfig ak;
+        ak.strategy = SchedStrategy::AdaKV, ak.adakv_step = 0.1, ak.target_hit = 0.9, ak.theta0 = 0.5, ak.hit_decay = 0.0;
+        ak.page_size = 1;
+        st.set_scheduler_state(0.5, 0.0);
+        st.observe_hits(ak, 7, 10);
+        st.adakv_update(ak);
+        CHECK(std::fabs(st.scheduler_state().theta - 0.52) < 1e-12);
+    }
+    {  // test_compressor.cpp:130-161; test_pipeline.cpp:80-119 on stored entries
+        Codec fv = Codec::fastv(2, 1);
+        CHECK(fv.encode_vector({3, 4}) == std::vector<double>{3});
+        CHECK((fv.decode_vector(fv.encode_vector({3, 4})) == std::vector<double>{3, 0}));
+        CHECK(std::fabs(fv.reconstruction_error({3, 4}) - 0.8) < 1e-6);
+        Codec pr = Codec::fit_prune({{1, 7}, {-3, 7}, {2, 7}, {-1, 7}}, 0.5);
+        CHECK(pr.zero_set() == std::vector<int>{1});
+        CHECK((pr.decode_vector(pr.encode_vector({3, 4})) == std::vector<double>{3, 0}));
+        ModelConfig m;
+        m.d = 2, m.head_width = 1, m.E = 4, m.k = 1, m.S = 8, m.G = 1;
+        KVStore st(m, StoreConfig{1, 1, false, 0});
+        CHECK(st.attention({1.0, 0.0}, {}).output == (std::vector<double>{0.0, 0.0}));
+        for (int t = 0; t < 2; ++t) {
+            KVEntry x;
+            x.token_id = t, x.key = {1.0, 0.0}, x.value = {3.0 + 2 * t, 4.0 + 2 * t};
+            st.insert(x);
+        }
+        auto a = st.attention({1.0, 0.0}, {0, 1});  // identical keys: 0.5 / 0.5
+        CHECK(std::fabs(a.weights[0] - 0.5) < 1e-6 && std::fabs(a.output[0] - 4.0) < 1e-5);
+    }
+    {  // Engine::flush / StepResult.inserted (pipeline.hpp:79, 108)
+        EngineConfig cfg = engine_config(RouterStrategy::TopK, 64);
+        Engine eng(cfg);
+        auto toks = make_stream(2, cfg.model.d, 5);
+        auto r = eng.step({toks[0]});
+        CHECK(r[0].inserted.size() == 2 && r[0].inserted[0].first == 0 && r[0].inserted[0].second == r[0].experts[0]);
+        CHECK(eng.flush().size() == 1 && eng.flush()[0].inserted.empty());
+    }
     std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "ok", failures);
     return failures;
 }

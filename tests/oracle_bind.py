@@ -71,6 +71,9 @@ def oracle_lib():
         lib.po_engine_dump_slots.argtypes = [ctypes.c_void_p, c_u64_p, c_u64_p, c_i64_p, c_i32_p,
                                              c_u64_p, c_u64_p, c_u64_p, c_double_p, c_double_p]
         lib.po_engine_set_attn_mass.argtypes = [ctypes.c_void_p, c_double_p, c_double_p]
+        lib.po_engine_read_payload.argtypes = [ctypes.c_void_p, ctypes.c_int64,
+                                               ctypes.POINTER(ctypes.c_float),
+                                               ctypes.POINTER(ctypes.c_float)]
         lib.po_engine_step_embed.argtypes = [ctypes.c_void_p, c_double_p, c_double_p,
                                              ctypes.POINTER(PoStepOut), ctypes.c_int]
         lib.po_encoder_weights.argtypes = [ctypes.c_int, ctypes.c_uint64, c_double_p]
@@ -227,7 +230,8 @@ class _StepMixin:
 class OracleEngine(_StepMixin):
     """One decode stream of the C restatement (pikv_oracle.c)."""
 
-    def __init__(self, cfg: EngineConfig, w_r=None, basis=None, bias=None, kept=None):
+    def __init__(self, cfg: EngineConfig, w_r=None, basis=None, bias=None, kept=None,
+                 evict_cap=4096, att_cap=1 << 16):
         self.lib = oracle_lib()
         self.cfg = cfg
         self.E, self.k, self.dp = cfg.model.E, cfg.router.k, cfg.stored_width
@@ -243,7 +247,7 @@ class OracleEngine(_StepMixin):
         if not self.h:
             raise RuntimeError("po_engine_create failed: %d" % err.value)
         self.error = err.value
-        self.out = self._new_out()
+        self.out = self._new_out(evict_cap, att_cap)
 
     def __del__(self):
         if getattr(self, "h", None):
@@ -306,6 +310,16 @@ class OracleEngine(_StepMixin):
         out = np.zeros(n.value, dtype=SNAPSHOT_DTYPE)
         self.lib.po_engine_snapshot(self.h, now, out.ctypes.data, n.value, ctypes.byref(n))
         return out
+
+    def read_payload(self, slots):
+        """Stored K, V (as attended) of the given slots, [n][d'] float32."""
+        fp = ctypes.POINTER(ctypes.c_float)
+        k = np.zeros((len(slots), self.dp), dtype=np.float32)
+        v = np.zeros((len(slots), self.dp), dtype=np.float32)
+        for i, gi in enumerate(slots):
+            self.lib.po_engine_read_payload(self.h, int(gi), k[i].ctypes.data_as(fp),
+                                            v[i].ctypes.data_as(fp))
+        return k, v
 
     def set_attn_mass(self, attn_mass, per_layer=None):
         a = np.ascontiguousarray(attn_mass, dtype=np.float64)
