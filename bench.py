@@ -144,7 +144,15 @@ def make_config(w, world=1, rank=0, G=None):
         S *= 2
     c.model = ModelConfig(d=d, head_width=hd, E=E, k=k, L=L, G=G, S=S, K=4, rho=1.0,
                           elem_bytes=2)
-    c.store = StoreConfig(n_tok=1, n_exp=E)          # pure expert partitioning
+    # pure expert partitioning (n_tok = 1: expert e on device e % G), or
+    # token-interleaved (n_tok = G: every expert's entries spread over all
+    # devices by token), both the reference's shard_assign (kvstore.cpp:14-30)
+    n_tok = 1
+    if w.get("placement", "expert") == "token" and G > 1:
+        n_tok = 1
+        while n_tok < G:
+            n_tok *= 2
+    c.store = StoreConfig(n_tok=n_tok, n_exp=E)
     c.router = RouterConfig(strategy="TopK", k=k)
     # LRU page budget per device: keep ~retain * k * L entries in steady state
     budget = max(1, int(retain * k * L / ps / G))
@@ -501,6 +509,8 @@ def main():
                     help="micro-batches pipelined on the GPU (default 2 at N=1 when B is even)")
     ap.add_argument("--attend-sms", type=int, default=None,
                     help="SMs of the persistent attention grid in the micro-batch pipeline")
+    ap.add_argument("--placement", default="expert", choices=["expert", "token"],
+                    help="shard_assign placement: expert (n_tok=1) or token-interleaved (n_tok=G)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: stage the exchange through host memory (single-GPU rehearsal)")
     args = ap.parse_args()
@@ -512,6 +522,7 @@ def main():
         w["B"] = args.batch
     if args.retain is not None:
         w["retain"] = args.retain
+    w["placement"] = args.placement
     if args.impl == "reference":
         run_reference_arm(args, w, name)
         return
@@ -550,7 +561,21 @@ def main():
         rng = np.random.default_rng(0)
         basis = np.linalg.qr(rng.standard_normal((hd, hd)))[0][:, :r].T
         eng.set_codec(np.ascontiguousarray(np.repeat(basis[None], cfg.n_heads, 0), np.float32))
-    stepper = ShardedStepper(eng) if world > 1 else None
+    stepper = None
+    exchange = "none (one rank)"
+    if world > 1:
+        # the all-gather of the LSE records inside the library (NCCL on the
+        # engine stream, captured in the step graph); torch.distributed as the
+        # transport only if the library's communicator cannot be created
+        try:
+            if args.dist_backend != "nccl":
+                raise RuntimeError("gloo rehearsal")
+            from paper_2508_06526_b200.parallel import attach_nccl
+            attach_nccl(eng)
+            exchange = "ncclAllGather inside libpikv_b200 (engine stream, step graph)"
+        except Exception as ex:  # pragma: no cover
+            stepper = ShardedStepper(eng)
+            exchange = "torch.distributed all_gather via pikv_step_local/finish (%s)" % str(ex)[:80]
 
     t0 = time.time()
     eng.prefill_synthetic(w["L"], seed=7)
@@ -616,13 +641,19 @@ def main():
     nprof = min(args.steps, 20)
     for i in range(nprof):
         one_step(args.warmup + (i % args.steps))
-        _, _, _, sm = eng.read_step()
-        att_total += sum(s["n_attended"] for s in sm)
+        att_total += eng.local_attended()  # this rank's attended entries (its own shards)
     phases, n_launch = eng.read_profile()
     eng.set_profiling(False)
     entry_bytes = eng.entry_bytes()
-    # KV bytes this rank's attention kernel must read (global count / ranks)
-    alg_bytes = att_total * entry_bytes / max(world, 1)
+    # KV bytes this rank's attention kernel read (its own count, not global / ranks)
+    alg_bytes = att_total * entry_bytes
+    rank_bytes = None
+    if world > 1:  # per-rank KV bytes per step: max and min over ranks (balance)
+        t_b = torch.tensor([alg_bytes / max(nprof, 1)], dtype=torch.float64, device="cuda")
+        mx, mn = t_b.clone(), t_b.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(mn, op=dist.ReduceOp.MIN)
+        rank_bytes = {"max": float(mx.item()), "min": float(mn.item()), "this_rank": float(t_b.item())}
     attend_avg_ms = phases["attend"] / max(n_launch, 1)
     peak, peak_kind = load_peaks()
     achieved = alg_bytes / max(n_launch, 1) / (attend_avg_ms * 1e-3) / 1e9 if attend_avg_ms else 0.0
@@ -630,7 +661,7 @@ def main():
 
     # ---------------- end to end through host buffers ----------------
     e2e = None
-    if world == 1:
+    if stepper is None:
         elem = 2 if cfg.kv_dtype == "bf16" else 4
         npdt = np.uint16 if elem == 2 else np.float32
         hq = torch.empty(args.steps, 3, B, d, dtype=tdt).pin_memory()
@@ -658,12 +689,19 @@ def main():
             return e0.elapsed_time(e1)
 
         # a synchronous host loop is exposed to host scheduling jitter: median of 3 runs
+        if world > 1:
+            dist.barrier()
         e2e_runs = [e2e_run() for _ in range(3)]
         e2e_ms = float(np.median(e2e_runs))
+        if world > 1:  # max over ranks
+            t_e2e = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t_e2e.item())
         e2e = {"value": B * args.steps / (e2e_ms * 1e-3), "unit": "tokens/s",
                "h2d_bytes_per_step": 3 * B * d * elem, "d2h_bytes_per_step": B * dp * 4,
                "ms_per_step": e2e_ms / args.steps, "api": "pikv_step_host",
-               "runs_ms": [round(x, 3) for x in e2e_runs], "statistic": "median of 3 runs"}
+               "runs_ms": [round(x, 3) for x in e2e_runs], "statistic": "median of 3 runs" +
+               (", max over ranks" if world > 1 else "")}
         del npdt
     else:
         # N ranks: every rank copies its step inputs in from pinned host memory,
@@ -708,14 +746,17 @@ def main():
         "config": {"workload": name, "description": WORKLOADS[name][0], "batch": B,
                    "context": w["L"], "experts": w["E"], "top_k": w["k"], "heads": w["H"],
                    "head_dim": w["hd"], "codec": w["codec"], "scheduler": "LRU page budget",
-                   "placement": "expert-sharded over %d GPU(s)" % world,
+                   "placement": "%s-sharded over %d GPU(s) (n_tok=%d, n_exp=%d)" % (
+                       args.placement, world, cfg.store.n_tok, cfg.store.n_exp),
                    "global_batch": B,
                    "parallelism": "ep%d (experts over GPUs, LSE merge all-gather)" % world,
+                   "exchange": exchange,
                    "l2": l2_note(att_last * entry_bytes),
                    "prefill_s": round(prefill_s, 2)},
         "kv_gbs": kv_bytes_step / (ms / args.steps * 1e-3) / 1e9,
         "kv_frac_of_hbm": kv_bytes_step / (ms / args.steps * 1e-3) / 1e9 / (peak * world),
         "attended_per_step": att_last,
+        "kv_bytes_per_rank_step": rank_bytes,
         "stream_errors": sum(1 for x in summ if x["error"]),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak,

@@ -265,9 +265,27 @@ int pikv_step_embed_host(pikv_engine* eng, const double* emb, const double* sali
 /* Replace the QueryEncoder's matrices (each [d][d] row-major fp64, host). */
 int pikv_set_encoder_host(pikv_engine* eng, const double* w_query, const double* w_key,
                           const double* w_value);
-/* Multi-rank step: run the rank-local part, exchange the merge records with
- * an all-gather (caller-provided, e.g. NCCL), then finish.  The exchange
- * buffer is device memory of pikv_exchange_bytes() per rank. */
+/* ---- multi-GPU (expert-sharded store, SURVEY 8 e) ---------------------
+ * Rank r of world_size owns the logical devices g with g % world == r.
+ * With NCCL attached, pikv_step / pikv_step_host / pikv_prefill_synthetic /
+ * the group run the whole sharded step, the all-gather of the per-stream LSE
+ * records (B x pikv_exchange_bytes()/B bytes) enqueued on the engine stream
+ * inside the captured step graph, then the cross-rank merge on every rank.
+ * pikv_nccl_unique_id: rank 0 creates the id, the caller broadcasts its
+ * PIKV_NCCL_ID_BYTES bytes; pikv_engine_attach_nccl is collective over the
+ * ranks (ncclCommInitRank with world_size / rank_id of the config).
+ * pikv_engine_set_nccl_comm takes a caller-owned ncclComm_t instead (NULL
+ * detaches).  A one-rank communicator runs the same exchange path. */
+#define PIKV_NCCL_ID_BYTES 128
+int pikv_nccl_unique_id(uint8_t* id_out);
+int pikv_engine_attach_nccl(pikv_engine* eng, const uint8_t* id);
+int pikv_engine_set_nccl_comm(pikv_engine* eng, void* nccl_comm);
+/* Attended entries of this rank's last step, summed over streams (the KV this
+ * rank's attention kernel read; the summaries carry the global counts). */
+int64_t pikv_local_attended(pikv_engine* eng);
+/* Without NCCL: the rank-local part, an all-gather the caller provides (any
+ * transport) into [world][exchange] device memory, then the finish.  The
+ * exchange buffer is device memory of pikv_exchange_bytes() per rank. */
 int64_t pikv_exchange_bytes(pikv_engine* eng);
 int pikv_step_local(pikv_engine* eng, const void* q, const void* k, const void* v,
                     const double* saliency, void** exchange_out);
@@ -484,6 +502,10 @@ pikv_engine* pikv_group_engine(pikv_group* grp, int32_t m);
 int pikv_group_submit(pikv_group* grp, int32_t m, const void* q, const void* k, const void* v,
                       const double* saliency, float* y_out, int32_t host);
 int pikv_group_wait(pikv_group* grp, int32_t m);
+/* world_size > 1: one NCCL communicator per micro-batch (ids
+ * [n_micro][PIKV_NCCL_ID_BYTES], each from pikv_nccl_unique_id on rank 0);
+ * micro-batch m's all-gather overlaps micro-batch m+1's attention. */
+int pikv_group_attach_nccl(pikv_group* grp, const uint8_t* ids);
 /* One step of all B streams from full-batch device buffers (q/k/v [B][d],
  * y [B][d']): pikv_group_submit for every micro-batch, no host wait. */
 int pikv_group_step(pikv_group* grp, const void* q, const void* k, const void* v,

@@ -111,6 +111,11 @@ SIGNATURES = {
     "pikv_group_sync": (ctypes.c_int, [c_vp]),
     "pikv_group_set_timing": (ctypes.c_int, [c_vp, c_i32]),
     "pikv_group_read_timing": (ctypes.c_int, [c_vp, P(c_f64), P(c_i32)]),
+    "pikv_nccl_unique_id": (ctypes.c_int, [c_vp]),
+    "pikv_engine_attach_nccl": (ctypes.c_int, [c_vp, c_vp]),
+    "pikv_engine_set_nccl_comm": (ctypes.c_int, [c_vp, c_vp]),
+    "pikv_local_attended": (c_i64, [c_vp]),
+    "pikv_group_attach_nccl": (ctypes.c_int, [c_vp, c_vp]),
     # component API
     "pikv_update_config": (ctypes.c_int, [c_vp, P(PikvConfigC)]),
     "pikv_route_host": (ctypes.c_int, [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp]),

@@ -4,6 +4,7 @@
 // HBM allocation, the per-step launch sequence (captured once into a CUDA
 // graph and replayed), result readback and the pure-function entry points.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -154,6 +155,18 @@ struct pikv_engine {
     size_t bulk_cap = 0;
     void* bulk_stage = nullptr;
     size_t stage_cap = 0;
+    // multi-GPU exchange (pikv_engine_attach_nccl / pikv_engine_set_nccl_comm):
+    // the step all-gathers every rank's exchange records into `gathered` on
+    // the engine stream (inside the captured step graph) and finishes the
+    // LSE merge on every rank
+    ncclComm_t comm = nullptr;
+    bool own_comm = false;
+    uint8_t* gathered = nullptr;
+    // grow-only readback scratch (pikv_read_attended_host)
+    void* rb_buf = nullptr;
+    size_t rb_cap = 0;
+    bool exchange_path() const { return D.world > 1 || comm != nullptr; }
+    std::string attend_err;  // non-empty: the decode step cannot run this layout
     double* enc_wt = nullptr;
     double* q64 = nullptr;
     double* in_emb = nullptr;
@@ -591,10 +604,10 @@ static int engine_create(const pikv_config* cfg, int32_t cuda_device, int attend
     D.att_stride = std::min<int64_t>((int64_t)D.max_cand * c.S, D.pool_entries);
     D.att_cap = (int64_t)D.B * D.att_stride + 1;
     D.att_eps = std::max(1, attend_entries_per_stage(D));
-    if (const char* msg = attend_check(D)) {
-        delete eng;
-        return fail(PIKV_ERR_INVALID_CONFIG, std::string("attention layout: ") + msg);
-    }
+    // a layout the decode-attention kernel cannot run is an error of the step
+    // (run_step), not of the engine: the component API (store, router,
+    // scheduler, attention over stored entries) works at any width
+    if (const char* msg = attend_check(D)) eng->attend_err = std::string("attention layout: ") + msg;
     fill_cfg(*cfg, eng->C);
     {
         // measured (profiles/README.md): the per-stream control kernel wins
@@ -794,6 +807,9 @@ int pikv_engine_destroy(pikv_engine* eng) {
     if (eng->host_g) cudaGraphDestroy(eng->host_g);
     if (eng->host_ph) cudaFreeHost(eng->host_ph);
     if (eng->bulk_buf) cudaFree(eng->bulk_buf);
+    if (eng->rb_buf) cudaFree(eng->rb_buf);
+    if (eng->gathered) cudaFree(eng->gathered);
+    if (eng->comm && eng->own_comm) ncclCommDestroy(eng->comm);
     if (eng->bulk_stage) cudaFree(eng->bulk_stage);
     if (eng->stream) cudaStreamDestroy(eng->stream);
     delete eng;
@@ -831,6 +847,7 @@ int pikv_set_codec_host(pikv_engine* eng, const float* basis, const float* bias,
 }
 
 static int codec_ready(pikv_engine* eng) {
+    if (!eng->attend_err.empty()) return fail(PIKV_ERR_INVALID_CONFIG, eng->attend_err);
     const int c = eng->D.codec;
     if ((c == PIKV_CODEC_LOWRANK || c == PIKV_CODEC_LORAPLUS) && !eng->S.basis)
         return fail(PIKV_ERR_NOT_FITTED, "codec basis not set (pikv_set_codec_host)");
@@ -915,7 +932,7 @@ static int enqueue_local(pikv_engine* eng, const void* q, const void* k, const v
     if ((parts & kPartAttend) && attend && D.Gl > 0) launch_attend(D, S, st), ++n;
     mark(eng, 8);
     if (parts & kPartMerge) {
-        const int direct = D.world == 1;  // single rank: combine writes y
+        const int direct = !eng->exchange_path();  // single rank: combine writes y
         if (attend || !direct) launch_combine(D, eng->C, S, eng->X, y, direct, attend, st), ++n;
         if (y_ready) cudaEventRecord(y_ready, st);
     }
@@ -927,8 +944,8 @@ static int enqueue_local(pikv_engine* eng, const void* q, const void* k, const v
 
 static int enqueue_finish(pikv_engine* eng, const uint8_t* gathered, float* y, bool attend,
                           int granks) {
-    if (eng->D.world > 1)
-        launch_finish_merge(eng->D, eng->C, eng->S, eng->X, gathered, y, granks, eng->stream);
+    const bool xp = eng->exchange_path();
+    if (xp) launch_finish_merge(eng->D, eng->C, eng->S, eng->X, gathered, y, granks, eng->stream);
     mark(eng, 10);
     // fold-back + feedback in one launch (last CTA runs the feedback); the
     // prefill (no attention) launches the feedback alone
@@ -937,7 +954,7 @@ static int enqueue_finish(pikv_engine* eng, const uint8_t* gathered, float* y, b
     if (!attend) launch_feedback(eng->D, eng->C, eng->S, eng->stream);
     mark(eng, 12);
     eng->cur = -1;
-    eng->kernels_per_step += 1 + (eng->D.world > 1 ? 1 : 0);
+    eng->kernels_per_step += 1 + (xp ? 1 : 0);
     CUDA_TRY(cudaGetLastError());
     return PIKV_OK;
 }
@@ -952,7 +969,16 @@ static int enqueue_step(pikv_engine* eng, const double* emb, const void* q, cons
     }
     if (emb) q = eng->q64, k = eng->in_k, v = eng->in_v;
     int rc = enqueue_local(eng, q, k, v, sal, attend, y, emb != nullptr, nullptr, nullptr, parts);
-    if (!rc && (parts & kPartFold)) rc = enqueue_finish(eng, eng->S.exchange, y, attend, 1);
+    if (!rc && (parts & kPartFold)) {
+        if (eng->comm) {  // the one exchange of the path: all-gather of the LSE records
+            const size_t nb = (size_t)eng->D.B * eng->X.bytes_per_stream;
+            const ncclResult_t r = ncclAllGather(eng->S.exchange, eng->gathered, nb, ncclUint8, eng->comm, eng->stream);
+            if (r != ncclSuccess) return fail(PIKV_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(r));
+            rc = enqueue_finish(eng, eng->gathered, y, attend, eng->D.world);
+        } else {
+            rc = enqueue_finish(eng, eng->S.exchange, y, attend, 1);
+        }
+    }
     if (emb && (parts & kPartCtl)) eng->kernels_per_step += (eng->D.B + 63) / 64;
     return rc;
 }
@@ -962,8 +988,9 @@ static int run_step(pikv_engine* eng, const void* q, const void* k, const void* 
                     unsigned parts = kPartAll) {
     int rc = codec_ready(eng);
     if (rc) return rc;
-    if (eng->D.world != 1)
-        return fail(PIKV_ERR_INVALID_ARGUMENT, "world_size > 1: use pikv_step_local / pikv_step_finish");
+    if (eng->D.world != 1 && !eng->comm)
+        return fail(PIKV_ERR_INVALID_ARGUMENT,
+                    "world_size > 1: attach NCCL (pikv_engine_attach_nccl) or use pikv_step_local / pikv_step_finish");
     cudaSetDevice(eng->device);
     const bool use_graph = (eng->warmed_parts & parts) == parts && !eng->profiling;
     if (!use_graph) {
@@ -1147,7 +1174,7 @@ int pikv_step_host(pikv_engine* eng, const void* q, const void* k, const void* v
     cudaStream_t st = eng->stream;
     const uint8_t* hq = (const uint8_t*)q;
     const bool packed = (const uint8_t*)k == hq + n && (const uint8_t*)v == hq + 2 * n;
-    if (packed && y_out && !(saliency && D.n_layers > 0) && D.world == 1 && eng->warmed && !eng->profiling &&
+    if (packed && y_out && !(saliency && D.n_layers > 0) && !eng->exchange_path() && eng->warmed && !eng->profiling &&
         codec_ready(eng) == PIKV_OK && is_pinned(q) && is_pinned(y_out)) {
         cudaSetDevice(eng->device);
         return step_host_graph(eng, q, y_out, n, sizeof(float) * D.B * D.dp);
@@ -1173,6 +1200,64 @@ int pikv_step_host(pikv_engine* eng, const void* q, const void* k, const void* v
         CUDA_TRY(cudaMemcpyAsync(y_out, eng->out_y, sizeof(float) * D.B * D.dp, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     return PIKV_OK;
+}
+
+// ---- multi-GPU: NCCL inside the library ------------------------------------
+int pikv_nccl_unique_id(uint8_t* id_out) {
+    if (!id_out) return fail(PIKV_ERR_INVALID_ARGUMENT, "id_out is NULL");
+    ncclUniqueId id;
+    const ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) return fail(PIKV_ERR_NCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    static_assert(sizeof(ncclUniqueId) == PIKV_NCCL_ID_BYTES, "ncclUniqueId size");
+    std::memcpy(id_out, &id, sizeof(id));
+    return PIKV_OK;
+}
+
+static int use_comm(pikv_engine* eng, ncclComm_t comm, bool own) {
+    int n = 0, r = 0;
+    if (comm) {
+        ncclResult_t e = ncclCommCount(comm, &n);
+        if (e == ncclSuccess) e = ncclCommUserRank(comm, &r);
+        if (e != ncclSuccess) return fail(PIKV_ERR_NCCL, std::string("nccl comm: ") + ncclGetErrorString(e));
+        if (n != eng->D.world || r != eng->D.rank)
+            return fail(PIKV_ERR_INVALID_CONFIG, "NCCL communicator size / rank != world_size / rank_id");
+    }
+    CUDA_TRY(cudaStreamSynchronize(eng->stream));
+    if (eng->comm && eng->own_comm) ncclCommDestroy(eng->comm);
+    eng->comm = comm, eng->own_comm = own && comm;
+    if (comm && !eng->gathered) {
+        CUDA_TRY(cudaMalloc(&eng->gathered, (size_t)eng->D.world * eng->D.B * eng->X.bytes_per_stream));
+    }
+    eng->invalidate();  // the captured steps change shape (exchange, all-gather, finish)
+    eng->warmed_parts = 0, eng->warmed = false;
+    return PIKV_OK;
+}
+
+int pikv_engine_attach_nccl(pikv_engine* eng, const uint8_t* id) {
+    if (!eng || !id) return fail(PIKV_ERR_INVALID_ARGUMENT, "NULL argument");
+    cudaSetDevice(eng->device);
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    ncclComm_t comm = nullptr;
+    const ncclResult_t r = ncclCommInitRank(&comm, eng->D.world, uid, eng->D.rank);
+    if (r != ncclSuccess) return fail(PIKV_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    return use_comm(eng, comm, true);
+}
+
+int pikv_engine_set_nccl_comm(pikv_engine* eng, void* nccl_comm) {
+    if (!eng) return fail(PIKV_ERR_INVALID_ARGUMENT, "engine is NULL");
+    cudaSetDevice(eng->device);
+    return use_comm(eng, (ncclComm_t)nccl_comm, false);
+}
+
+int64_t pikv_local_attended(pikv_engine* eng) {
+    cudaStreamSynchronize(eng->stream);
+    std::vector<int32_t> cnt(eng->D.B), err(eng->D.B);
+    cudaMemcpy(cnt.data(), eng->S.att_cnt, 4 * (size_t)eng->D.B, cudaMemcpyDeviceToHost);
+    cudaMemcpy(err.data(), eng->S.err, 4 * (size_t)eng->D.B, cudaMemcpyDeviceToHost);
+    int64_t n = 0;
+    for (int s = 0; s < eng->D.B; ++s) n += err[s] ? 0 : cnt[s];
+    return n;
 }
 
 int64_t pikv_exchange_bytes(pikv_engine* eng) { return (int64_t)eng->D.B * eng->X.bytes_per_stream; }
@@ -1211,7 +1296,7 @@ int pikv_prefill_synthetic(pikv_engine* eng, int64_t tokens, uint64_t seed) {
     eng->profiling = false;
     for (int64_t t = 0; t < tokens; ++t) {
         launch_synth(eng->D, eng->in_q, eng->in_k, eng->in_v, seed, (uint64_t)t, eng->stream);
-        if (eng->D.world == 1) {
+        if (eng->D.world == 1 || eng->comm) {  // the full step (with the collective when sharded)
             rc = run_step(eng, eng->in_q, eng->in_k, eng->in_v, nullptr, nullptr, false);
         } else {
             rc = enqueue_local(eng, eng->in_q, eng->in_k, eng->in_v, nullptr, false, nullptr);
@@ -1308,6 +1393,9 @@ int pikv_insert_bulk(pikv_engine* eng, int32_t stream, int64_t T, const void* k,
     if (need > eng->bulk_cap) {
         CUDA_TRY(cudaStreamSynchronize(st));
         if (eng->bulk_buf) cudaFree(eng->bulk_buf);
+    if (eng->rb_buf) cudaFree(eng->rb_buf);
+    if (eng->gathered) cudaFree(eng->gathered);
+    if (eng->comm && eng->own_comm) ncclCommDestroy(eng->comm);
         eng->bulk_buf = nullptr, eng->bulk_cap = 0;
         CUDA_TRY(cudaMalloc(&eng->bulk_buf, need));
         eng->bulk_cap = need;
@@ -1464,8 +1552,13 @@ int pikv_read_attended_host(pikv_engine* eng, int32_t stream, int64_t* token, in
     std::vector<int64_t> ht(m);
     std::vector<int32_t> he(m);
     {
-        uint8_t* buf = nullptr;
-        CUDA_TRY(cudaMalloc(&buf, 12 * (size_t)m));
+        if (eng->rb_cap < 12 * (size_t)m) {
+            if (eng->rb_buf) cudaFree(eng->rb_buf);
+            eng->rb_buf = nullptr, eng->rb_cap = 0;
+            CUDA_TRY(cudaMalloc(&eng->rb_buf, 12 * (size_t)m));
+            eng->rb_cap = 12 * (size_t)m;
+        }
+        uint8_t* buf = (uint8_t*)eng->rb_buf;
         launch_gather_slots(eng->S, eng->S.att_slot + base[0], m, (int64_t*)buf, (int32_t*)(buf + 8 * (size_t)m),
                             eng->stream);
         cudaError_t e = cudaGetLastError();
@@ -1473,7 +1566,6 @@ int pikv_read_attended_host(pikv_engine* eng, int32_t stream, int64_t* token, in
         if (e == cudaSuccess)
             e = cudaMemcpyAsync(he.data(), buf + 8 * (size_t)m, 4 * (size_t)m, cudaMemcpyDeviceToHost, eng->stream);
         if (e == cudaSuccess) e = cudaStreamSynchronize(eng->stream);
-        cudaFree(buf);
         if (e != cudaSuccess) return fail(PIKV_ERR_CUDA, std::string("read_attended: ") + cudaGetErrorString(e));
     }
     for (int i = 0; i < m; ++i) {
@@ -2153,7 +2245,7 @@ int pikv_group_create(const pikv_config* cfg, int32_t n_micro, int32_t attend_sm
     *out = nullptr;
     if (n_micro < 1 || cfg->batch % n_micro != 0)
         return fail(PIKV_ERR_INVALID_CONFIG, "batch must be a multiple of n_micro");
-    if (cfg->world_size != 1) return fail(PIKV_ERR_INVALID_CONFIG, "pikv_group: world_size must be 1");
+
     int rc = validate(*cfg);
     if (rc) return rc;
     CUDA_TRY(cudaSetDevice(cuda_device));
@@ -2294,6 +2386,17 @@ int pikv_group_submit(pikv_group* g, int32_t m, const void* q, const void* k, co
         }
         if (!host) {
             if (!rc) rc = run_step(e, dq, dk, dv, ds, dy, true, nullptr, kPartTail);
+        } else if (e->exchange_path()) {
+            // sharded over ranks: y is final only after the all-gather and the
+            // cross-rank merge (the fold part); its D2H follows the whole tail
+            if (!rc) CUDA_TRY(cudaStreamWaitEvent(st, g->y_done[m], 0));
+            if (!rc) rc = run_step(e, dq, dk, dv, ds, dy, true, nullptr, kPartTail);
+            if (!rc) {
+                CUDA_TRY(cudaEventRecord(g->y_ready[m], st));
+                CUDA_TRY(cudaStreamWaitEvent(g->side[m], g->y_ready[m], 0));
+                CUDA_TRY(cudaMemcpyAsync(y, e->out_y, g->y_bytes, cudaMemcpyDeviceToHost, g->side[m]));
+                CUDA_TRY(cudaEventRecord(g->y_done[m], g->side[m]));
+            }
         } else {
             // y leaves for the host on a side stream as soon as the merge wrote
             // it, while the fold-back runs: the caller's wait returns earlier
@@ -2313,6 +2416,15 @@ int pikv_group_submit(pikv_group* g, int32_t m, const void* q, const void* k, co
     if (rc) return rc;
     if (e->profiling && host) CUDA_TRY(cudaMemcpyAsync(y, e->out_y, g->y_bytes, cudaMemcpyDeviceToHost, st));
     if (!host || e->profiling) CUDA_TRY(cudaEventRecord(g->y_done[m], st));
+    return PIKV_OK;
+}
+
+int pikv_group_attach_nccl(pikv_group* g, const uint8_t* ids) {
+    if (!g || !ids) return fail(PIKV_ERR_INVALID_ARGUMENT, "NULL argument");
+    for (int m = 0; m < g->n; ++m) {  // one communicator per micro-batch stream
+        const int rc = pikv_engine_attach_nccl(g->eng[m], ids + (size_t)m * PIKV_NCCL_ID_BYTES);
+        if (rc) return rc;
+    }
     return PIKV_OK;
 }
 

@@ -254,7 +254,8 @@ void launch_route_one(const Dims& D, const Cfg& C, const State& S, int s, const 
     Dims d1 = D;
     d1.q_f64 = 1;
     const size_t smem = route_smem_bytes(d1, d1.route_ch);
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k_route_one, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // static shared memory counts against the 48 KB default too: always opt in
+    cudaFuncSetAttribute(k_route_one, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int threads = ((D.E + 31) / 32) * 32 + 32;
     k_route_one<<<1, threads, smem, st>>>(d1, C, S, s, q, logits);
 }
@@ -447,7 +448,8 @@ int pick_route_chunk(const Dims& D) {
 
 void launch_route(const Dims& D, const Cfg& C, const State& S, const void* q, cudaStream_t st) {
     const size_t smem = route_smem_bytes(D, D.route_ch);
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k_route, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // static shared memory counts against the 48 KB default too: always opt in
+    cudaFuncSetAttribute(k_route, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int threads = ((D.E + 31) / 32) * 32 + 32;
     launch_pdl(k_route, dim3(D.B), dim3(threads), smem, st, D, C, S, q);
 }

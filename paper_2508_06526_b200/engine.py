@@ -425,6 +425,21 @@ class Engine:
         check(lib().pikv_step_finish(self.h, _ptr(gathered), _ptr(y)))
         return y
 
+    # ---- multi-GPU: NCCL inside the library --------------------------------
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        check(lib().pikv_nccl_unique_id(buf))
+        return buf.raw
+
+    def attach_nccl(self, uid: bytes):
+        """ncclCommInitRank(world_size, uid, rank_id) -- collective over ranks."""
+        buf = ctypes.create_string_buffer(bytes(uid), 128)
+        check(lib().pikv_engine_attach_nccl(self.h, buf))
+
+    def local_attended(self) -> int:
+        return int(lib().pikv_local_attended(self.h))
+
     def stream_handle(self) -> int:
         return int(lib().pikv_engine_stream(self.h) or 0)
 
@@ -512,6 +527,11 @@ class EngineGroup:
 
     def kernel_launches(self) -> int:
         return sum(e.kernel_launches() for e in self.engines)
+
+    def attach_nccl(self, uids):
+        """One communicator per micro-batch (uids: n_micro unique ids)."""
+        buf = ctypes.create_string_buffer(b"".join(bytes(u) for u in uids), 128 * self.n)
+        check(lib().pikv_group_attach_nccl(self.h, buf))
 
     def read_step(self):
         """Concatenated (experts, gates, logits, summaries) over micro-batches."""

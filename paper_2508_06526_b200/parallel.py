@@ -11,8 +11,13 @@ shards, and the one real exchange of the path is the log-sum-exp merge
 (m, l, o[H][d'h], per-expert hit counts, step counters) and finishes the
 step locally (global y, global (m, l) for the alpha fold-back, misses).
 
-The collective is NCCL over NVLink on GPUs; the same code runs over gloo on
-CPU tensors for the multi-process tests.
+On GPUs the collective lives inside the library: ``attach_nccl`` creates
+the engine's NCCL communicator (rank 0's unique id broadcast over the
+caller's process group) and every ``Engine.step`` then runs the whole
+sharded step -- the all-gather enqueued on the engine stream inside the
+captured step graph.  ``ShardedStepper`` drives the same exchange through
+pikv_step_local / pikv_step_finish with torch.distributed as the transport
+(gloo: the multi-process tests, staged through host memory).
 """
 from __future__ import annotations
 
@@ -46,6 +51,22 @@ def all_gather_bytes(out: torch.Tensor, local: torch.Tensor, group=None):
     dist.all_gather(parts, loc, group=group)
     out.copy_(host)
     return out
+
+
+def attach_nccl(engine, group=None, n_comms: int = 1):
+    """Create the library-owned NCCL communicator(s) of `engine` (an Engine,
+    or an EngineGroup with one communicator per micro-batch): rank 0 draws
+    the unique ids, the process group broadcasts them."""
+    from .engine import Engine
+    ids = [Engine.nccl_unique_id() for _ in range(n_comms)] if dist.get_rank(group) == 0 else None
+    box = [ids]
+    dist.broadcast_object_list(box, src=0, group=group)
+    ids = box[0]
+    if n_comms == 1 and hasattr(engine, "attach_nccl") and not hasattr(engine, "engines"):
+        engine.attach_nccl(ids[0])
+    else:
+        engine.attach_nccl(ids)
+    return engine
 
 
 class ShardedStepper:

@@ -151,7 +151,7 @@ def test_snapshot_ordered_and_complete():  # test_kvstore.cpp:232-243
         st.insert(make_entry(t, t % 2, 4))
     snap = st.snapshot(6)
     assert len(snap) == 6
-    keys = [(int(r["device"]), int(r["shard"]), int(r["token_id"])) for r in snap]
+    keys = [(int(r["device"]), int(r["shard"]), int(r["token"])) for r in snap]
     assert keys == sorted(keys)
 
 

@@ -76,13 +76,14 @@ def group_rc(cfg, n_micro):
     return rc
 
 
-@pytest.mark.parametrize("batch,n_micro,world", [(3, 2, 1), (4, 0, 1), (4, 3, 1), (4, 2, 2)])
-def test_group_rejects_bad_split_before_cuda(batch, n_micro, world):
+@pytest.mark.parametrize("batch,n_micro,world,rank", [(3, 2, 1, 0), (4, 0, 1, 0), (4, 3, 1, 0),
+                                                     (4, 2, 2, 2)])
+def test_group_rejects_bad_split_before_cuda(batch, n_micro, world, rank):
     """pikv_group_create: the batch must split evenly into n_micro >= 1
-    micro-batches of a single-rank engine -> InvalidConfig, checked before
+    micro-batches, and rank_id < world_size -> InvalidConfig, checked before
     any CUDA call (include/pikv_b200.h, micro-batch pipeline)."""
     cfg = engine_config(batch=batch)
-    cfg.world_size = world
+    cfg.world_size, cfg.rank_id = world, rank
     assert _capi.ERRORS[group_rc(cfg, n_micro)] == "InvalidConfig"
 
 
