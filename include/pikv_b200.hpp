@@ -28,7 +28,6 @@
 #pragma once
 
 #include <algorithm>
-#include <charconv>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -897,23 +896,114 @@ class EngineGroup {
 };
 
 // ---- wire formats of the reference's run output (runner.cpp) --------------
-// nlohmann::json dump(): keys sorted, compact, doubles as shortest digits in
-// nlohmann's layout (fixed for decimal exponents -4 < n <= 15); see
-// paper_2508_06526_b200/wire.py for the grisu2 note.
+// nlohmann::json dump(): keys sorted, compact, doubles as nlohmann's grisu2
+// digits in its layout (fixed for decimal exponents -4 < n <= 15).
 namespace wire {
+
+// Grisu2 (Loitsch 2010) digits d1..dk and exponent (value = d1..dk 10^exp)
+// exactly as nlohmann's dtoa_impl generates them, including the doubles
+// where grisu2 is not the shortest form (1e23 -> 9.999999999999999e+22).
+inline void grisu2(double v, std::string& digits, int& dec_exp) {
+    struct Fp { std::uint64_t f; int e; };
+    struct Cached { std::uint64_t f; int e; int k; };
+    static const Cached pow10[] = {
+        {0xAB70FE17C79AC6CAULL, -1060, -300}, {0xFF77B1FCBEBCDC4FULL, -1034, -292}, {0xBE5691EF416BD60CULL, -1007, -284},
+        {0x8DD01FAD907FFC3CULL, -980, -276}, {0xD3515C2831559A83ULL, -954, -268}, {0x9D71AC8FADA6C9B5ULL, -927, -260},
+        {0xEA9C227723EE8BCBULL, -901, -252}, {0xAECC49914078536DULL, -874, -244}, {0x823C12795DB6CE57ULL, -847, -236},
+        {0xC21094364DFB5637ULL, -821, -228}, {0x9096EA6F3848984FULL, -794, -220}, {0xD77485CB25823AC7ULL, -768, -212},
+        {0xA086CFCD97BF97F4ULL, -741, -204}, {0xEF340A98172AACE5ULL, -715, -196}, {0xB23867FB2A35B28EULL, -688, -188},
+        {0x84C8D4DFD2C63F3BULL, -661, -180}, {0xC5DD44271AD3CDBAULL, -635, -172}, {0x936B9FCEBB25C996ULL, -608, -164},
+        {0xDBAC6C247D62A584ULL, -582, -156}, {0xA3AB66580D5FDAF6ULL, -555, -148}, {0xF3E2F893DEC3F126ULL, -529, -140},
+        {0xB5B5ADA8AAFF80B8ULL, -502, -132}, {0x87625F056C7C4A8BULL, -475, -124}, {0xC9BCFF6034C13053ULL, -449, -116},
+        {0x964E858C91BA2655ULL, -422, -108}, {0xDFF9772470297EBDULL, -396, -100}, {0xA6DFBD9FB8E5B88FULL, -369, -92},
+        {0xF8A95FCF88747D94ULL, -343, -84}, {0xB94470938FA89BCFULL, -316, -76}, {0x8A08F0F8BF0F156BULL, -289, -68},
+        {0xCDB02555653131B6ULL, -263, -60}, {0x993FE2C6D07B7FACULL, -236, -52}, {0xE45C10C42A2B3B06ULL, -210, -44},
+        {0xAA242499697392D3ULL, -183, -36}, {0xFD87B5F28300CA0EULL, -157, -28}, {0xBCE5086492111AEBULL, -130, -20},
+        {0x8CBCCC096F5088CCULL, -103, -12}, {0xD1B71758E219652CULL, -77, -4}, {0x9C40000000000000ULL, -50, 4},
+        {0xE8D4A51000000000ULL, -24, 12}, {0xAD78EBC5AC620000ULL, 3, 20}, {0x813F3978F8940984ULL, 30, 28},
+        {0xC097CE7BC90715B3ULL, 56, 36}, {0x8F7E32CE7BEA5C70ULL, 83, 44}, {0xD5D238A4ABE98068ULL, 109, 52},
+        {0x9F4F2726179A2245ULL, 136, 60}, {0xED63A231D4C4FB27ULL, 162, 68}, {0xB0DE65388CC8ADA8ULL, 189, 76},
+        {0x83C7088E1AAB65DBULL, 216, 84}, {0xC45D1DF942711D9AULL, 242, 92}, {0x924D692CA61BE758ULL, 269, 100},
+        {0xDA01EE641A708DEAULL, 295, 108}, {0xA26DA3999AEF774AULL, 322, 116}, {0xF209787BB47D6B85ULL, 348, 124},
+        {0xB454E4A179DD1877ULL, 375, 132}, {0x865B86925B9BC5C2ULL, 402, 140}, {0xC83553C5C8965D3DULL, 428, 148},
+        {0x952AB45CFA97A0B3ULL, 455, 156}, {0xDE469FBD99A05FE3ULL, 481, 164}, {0xA59BC234DB398C25ULL, 508, 172},
+        {0xF6C69A72A3989F5CULL, 534, 180}, {0xB7DCBF5354E9BECEULL, 561, 188}, {0x88FCF317F22241E2ULL, 588, 196},
+        {0xCC20CE9BD35C78A5ULL, 614, 204}, {0x98165AF37B2153DFULL, 641, 212}, {0xE2A0B5DC971F303AULL, 667, 220},
+        {0xA8D9D1535CE3B396ULL, 694, 228}, {0xFB9B7CD9A4A7443CULL, 720, 236}, {0xBB764C4CA7A44410ULL, 747, 244},
+        {0x8BAB8EEFB6409C1AULL, 774, 252}, {0xD01FEF10A657842CULL, 800, 260}, {0x9B10A4E5E9913129ULL, 827, 268},
+        {0xE7109BFBA19C0C9DULL, 853, 276}, {0xAC2820D9623BF429ULL, 880, 284}, {0x80444B5E7AA7CF85ULL, 907, 292},
+        {0xBF21E44003ACDD2DULL, 933, 300}, {0x8E679C2F5E44FF8FULL, 960, 308}, {0xD433179D9C8CB841ULL, 986, 316},
+        {0x9E19DB92B4E31BA9ULL, 1013, 324}};
+    auto normalize = [](Fp x) {
+        while (!(x.f >> 63)) x.f <<= 1, --x.e;
+        return x;
+    };
+    auto mul = [](Fp a, Fp b) {  // high 64 bits of the product, rounded half up
+        const unsigned __int128 p = (unsigned __int128)a.f * b.f + ((unsigned __int128)1 << 63);
+        return Fp{(std::uint64_t)(p >> 64), a.e + b.e + 64};
+    };
+    std::uint64_t bits;
+    std::memcpy(&bits, &v, 8);
+    const std::uint64_t E = bits >> 52, F = bits & ((1ULL << 52) - 1);
+    const Fp w0 = E == 0 ? Fp{F, 1 - 1075} : Fp{F + (1ULL << 52), static_cast<int>(E) - 1075};
+    const bool closer = F == 0 && E > 1;
+    const Fp mp = normalize(Fp{2 * w0.f + 1, w0.e - 1});
+    Fp mm = closer ? Fp{4 * w0.f - 1, w0.e - 2} : Fp{2 * w0.f - 1, w0.e - 1};
+    mm = Fp{mm.f << (mm.e - mp.e), mp.e};
+    const Fp w = normalize(w0);
+    const int fx = -60 - mp.e - 1;
+    const int k = fx * 78913 / (1 << 18) + (fx > 0);
+    const Cached c = pow10[(300 + k + 7) / 8];
+    const Fp cw = mul(w, {c.f, c.e}), cmm = mul(mm, {c.f, c.e}), cmp = mul(mp, {c.f, c.e});
+    const Fp Mm{cmm.f + 1, cmm.e}, Mp{cmp.f - 1, cmp.e};
+    dec_exp = -c.k;
+    std::uint64_t delta = Mp.f - Mm.f, dist = Mp.f - cw.f;
+    const int shift = -Mp.e;
+    const std::uint64_t one = 1ULL << shift;
+    std::uint32_t p1 = static_cast<std::uint32_t>(Mp.f >> shift);
+    std::uint64_t p2 = Mp.f & (one - 1);
+    digits.clear();
+    auto round = [&](std::uint64_t rest, std::uint64_t ten_k) {
+        while (rest < dist && delta - rest >= ten_k && (rest + ten_k < dist || dist - rest > rest + ten_k - dist)) {
+            --digits.back();
+            rest += ten_k;
+        }
+    };
+    int n = 1;
+    std::uint32_t p10 = 1;
+    while (p10 <= p1 / 10) p10 *= 10, ++n;
+    while (n > 0) {
+        digits.push_back(static_cast<char>('0' + p1 / p10));
+        p1 %= p10;
+        --n;
+        const std::uint64_t rest = (static_cast<std::uint64_t>(p1) << shift) + p2;
+        if (rest <= delta) {
+            dec_exp += n;
+            round(rest, static_cast<std::uint64_t>(p10) << shift);
+            return;
+        }
+        p10 /= 10;
+    }
+    int m = 0;
+    for (;;) {
+        p2 *= 10, delta *= 10, dist *= 10;
+        digits.push_back(static_cast<char>('0' + (p2 >> shift)));
+        p2 &= one - 1;
+        ++m;
+        if (p2 <= delta) break;
+    }
+    dec_exp -= m;
+    round(p2, one);
+}
 
 inline std::string json_double(double x) {
     if (x != x || x - x != 0.0) return "null";  // NaN, inf
     if (x == 0.0) return std::signbit(x) ? "-0.0" : "0.0";
-    char buf[64];
-    auto res = std::to_chars(buf, buf + sizeof(buf), x < 0 ? -x : x, std::chars_format::scientific);
-    std::string sci(buf, res.ptr);  // d[.ddd]e(+|-)XX, shortest round-trip digits
-    const auto epos = sci.find('e');
-    std::string ds = sci.substr(0, epos);
-    ds.erase(std::remove(ds.begin(), ds.end(), '.'), ds.end());
-    while (ds.size() > 1 && ds.back() == '0') ds.pop_back();
+    std::string ds;
+    int ex = 0;
+    grisu2(x < 0 ? -x : x, ds, ex);
     const int k = static_cast<int>(ds.size());
-    const int n = std::stoi(sci.substr(epos + 1)) + 1;  // value = 0.d1..dk * 10^n
+    const int n = k + ex;  // value = 0.d1..dk * 10^n
     std::string out = x < 0 ? "-" : "";
     if (k <= n && n <= 15) return out + ds + std::string(n - k, '0') + ".0";
     if (0 < n && n <= 15) return out + ds.substr(0, n) + "." + ds.substr(n);

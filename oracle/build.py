@@ -36,6 +36,12 @@ EXTRACTS = [
      "0b7a58bb7cf2a88e9dc9a5104abcacda680d760ba71f6d5b5c4e2ddb930bc5f2"),
     ("src/pipeline.cpp", 29, 57,  # QueryEncoder (the step's encode, pipeline.cpp:222)
      "94bea718658aadb9356db62905d46ab4460b919e090f97e3d4d0d2f1a581388a"),
+    # runner build only: strategy / scheme names (the parts of those files
+    # before their Eigen code)
+    ("src/scheduler.cpp", 14, 48,
+     "2d6cf5cf8afb020c51acd9485f85b5839f9669a547525bb53cae1c95c08640de"),
+    ("src/compressor.cpp", 117, 163,
+     "13f37d069754dcbe1e2a4f94c8d908497ef58acfe59848d75f962dcdca0b309d"),
 ]
 
 
@@ -104,6 +110,55 @@ def build_ref(force: bool = False) -> str | None:
     objs = []
     for s in srcs:
         o = os.path.join(REF_OUT, os.path.basename(s) + ".o")
+        _run(flags + ["-c", s, "-o", o])
+        objs.append(o)
+    _run(["g++", "-shared", "-o", out] + objs + ["-lpthread"])
+    return out
+
+
+def runner_lib_path() -> str:
+    return os.path.join(REF_OUT, "libpikv_runner.so")
+
+
+def build_runner(force: bool = False) -> str | None:
+    """oracle/_ref/libpikv_runner.so: the reference's run_experiment
+    (runner.cpp) with pipeline.cpp, runconfig.cpp, costmodel.cpp, trace.cpp,
+    kvstore.cpp, router.cpp, mathops.cpp compiled unchanged, the Eigen-free
+    scheduler.cpp / compressor.cpp extracts, nlohmann json.hpp from the
+    image's cudnn_frontend wheel, and oracle/ref_runner.cpp (Identity codec
+    + driver).  None when /root/reference or json.hpp is absent."""
+    out = runner_lib_path()
+    drv = os.path.join(HERE, "ref_runner.cpp")
+    if not os.path.isdir(REF):
+        return out if os.path.exists(out) else None
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= os.path.getmtime(drv):
+        return out
+    import glob
+    js = glob.glob(os.path.join(sys.prefix, "lib", "python3*", "site-packages", "include",
+                                "cudnn_frontend", "thirdparty", "nlohmann", "json.hpp"))
+    if not js:
+        return None
+    os.makedirs(REF_OUT, exist_ok=True)
+    inc = os.path.join(REF, "include")
+    hdr = ('#include "pikv/scheduler.hpp"\n#include <algorithm>\n#include <cmath>\n'
+           '#include "pikv/errors.hpp"\n#include "pikv/mathops.hpp"\n#include "pikv/rng.hpp"\n')
+    sched = (hdr + "namespace pikv {\n" + _extract(*EXTRACTS[4]) + _extract(*EXTRACTS[0]) +
+             _extract(*EXTRACTS[1]) + "}  // namespace pikv\n")
+    comp = ('#include "pikv/compressor.hpp"\n#include "pikv/errors.hpp"\nnamespace pikv {\n' +
+            _extract(*EXTRACTS[5]) + "}  // namespace pikv\n")
+    gen = {"runner_sched_extract.cpp": sched, "runner_comp_extract.cpp": comp}
+    for name, text in gen.items():
+        with open(os.path.join(REF_OUT, name), "w") as f:
+            f.write(text)
+    srcs = [os.path.join(REF, "src", s) for s in
+            ("mathops.cpp", "kvstore.cpp", "router.cpp", "costmodel.cpp", "trace.cpp",
+             "pipeline.cpp", "runconfig.cpp", "runner.cpp")]
+    srcs += [os.path.join(REF_OUT, n) for n in gen] + [drv]
+    flags = ["g++", "-std=c++20", "-O2", "-fPIC", "-include", "unordered_map", "-I", inc,
+             "-I", os.path.dirname(js[0])]
+    objs = []
+    for s in srcs:
+        o = os.path.join(REF_OUT, "runner_" + os.path.basename(s) + ".o")
         _run(flags + ["-c", s, "-o", o])
         objs.append(o)
     _run(["g++", "-shared", "-o", out] + objs + ["-lpthread"])

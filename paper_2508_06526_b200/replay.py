@@ -261,8 +261,10 @@ class MetricsAccumulator:
         mean = self.latency_total / len(self.lat) if self.lat else 0.0
         roof = io_and_roofline(m, self.hw, self.batch_tokens)
         mean_prefix = (0.0 if self.lookups == 0 else
-                       float(self.retrieved) / float(cfg.router.k) / float(steps))
-        io_model = (2.0 * self.head + self.d_stored) * mean_prefix * cfg.router.k * float(steps)
+                       float(self.retrieved) / float(m.k) / float(steps))
+        # runner.cpp:236-241 divides and multiplies by the MODEL's k (the
+        # cost model's active experts), not the router's
+        io_model = (2.0 * self.head + self.d_stored) * mean_prefix * m.k * float(steps)
         obj_lat, obj_mem, obj_hit = self.latency_total, float(self.peak_memory), hit_rate
         return {
             "type": "metrics", "steps": steps, "seed": self.seed,

@@ -116,3 +116,40 @@ def test_metrics_accumulator_on_oracle_replay():
     assert m["peak_memory_bytes"] > 0 and sum(m["expert_load"]) == 80 * cfg.router.k
     assert m["objective_value"] == (m["objective_latency_s"] + 1e-9 * m["objective_memory_bytes"]
                                     - 0.5 * m["objective_hit_rate"])
+
+
+# ------------------------------------ pinned to the reference's runner ----
+RUNNER_GOLD = sorted(glob.glob(os.path.join(HERE, "golden", "runner", "*.json")))
+
+
+def _runner_case(path):
+    import sys
+    sys.path.insert(0, os.path.join(HERE, "golden"))
+    from runner_cases import CASES, LAMBDA_HIT, LAMBDA_MEMORY, LAYERS, TOPO, D
+    doc = json.load(open(path))
+    c = CASES[doc["case"]]
+    spec = TraceSpec(steps=c["T"], width=D, vocab=c["vocab"], zipf_skew=c["skew"], seed=c["tseed"],
+                     layers=LAYERS)
+    topo = Topology.uniform(c["G"], TOPO["local"], TOPO["link"], TOPO["bw"])
+    return doc, c, spec, topo, LAMBDA_MEMORY, LAMBDA_HIT
+
+
+@pytest.mark.parametrize("path", RUNNER_GOLD, ids=[os.path.basename(p)[:-5] for p in RUNNER_GOLD])
+def test_oracle_replay_matches_reference_runner(path):
+    """MetricsAccumulator (runner.cpp:69-261 restated) fed by the oracle
+    engine reproduces the reference's own run_experiment output byte for
+    byte: report line, every event line, the store dump (goldens from
+    tests/golden/make_runner_golden.py)."""
+    doc, c, spec, topo, lm, lh = _runner_case(path)
+    from runner_cases import engine_cfg
+    from paper_2508_06526_b200 import wire
+    cfg = engine_cfg(c)
+    tr = generate_trace(spec)
+    acc = MetricsAccumulator(cfg, topo, c["home"], lm, lh, spec.seed)
+    gen = oracle_records(cfg, tr)
+    lines = [acc.step(t, next(gen)) for t in range(spec.steps)]
+    orc = next(gen)
+    report = acc.report(orc.router_state()["usage"])
+    assert lines == doc["events"]
+    assert wire.dumps(report) == doc["report"]
+    assert wire.store_dump_lines(orc.snapshot(spec.steps)) == doc["store"]

@@ -54,3 +54,37 @@ def test_run_trace_matches_oracle_replay(router, sched, kw):
             assert ja == jb
             assert np.allclose(ga, gb, rtol=1e-12, atol=0)
         assert outs[s].store_dump == wire.store_dump_lines(orc.snapshot(tr.spec.steps))
+
+
+# ------------------------------------ pinned to the reference's runner ----
+import glob  # noqa: E402
+import os  # noqa: E402
+import sys  # noqa: E402
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.join(_HERE, "golden"))
+from runner_cases import CASES  # noqa: E402
+
+_GPU_CASES = [p for p in sorted(glob.glob(os.path.join(_HERE, "golden", "runner", "*.json")))
+              if not CASES[os.path.basename(p)[:-5]].get("cpu_only")]
+
+
+@pytest.mark.parametrize("path", _GPU_CASES, ids=[os.path.basename(p)[:-5] for p in _GPU_CASES])
+def test_run_trace_matches_reference_runner(path):
+    """run_trace on the GPU == the reference's own run_experiment output
+    (tests/golden/runner, from tests/golden/make_runner_golden.py): report
+    line and store dump byte for byte, event lines byte for byte except the
+    gates (rel 1e-12: CUDA vs glibc exp)."""
+    from runner_cases import engine_cfg
+    from test_replay import _runner_case
+    doc, c, spec, topo, lm, lh = _runner_case(path)
+    out = run_trace(engine_cfg(c), [generate_trace(spec)], topo, home_device=c["home"], lambda_memory=lm,
+                    lambda_hit=lh, dump_store=True)[0]
+    assert out.report_line == doc["report"]
+    assert out.store_dump == doc["store"]
+    assert len(out.event_log) == len(doc["events"])
+    for a, b in zip(out.event_log, doc["events"]):
+        ja, jb = json.loads(a), json.loads(b)
+        ga, gb = ja.pop("gates"), jb.pop("gates")
+        assert ja == jb
+        assert np.allclose(ga, gb, rtol=1e-12, atol=0)

@@ -138,3 +138,36 @@ def test_cpp_facade_wire_lines_match_nlohmann(cpp_writer, name):
             non_byte += 1
             assert same_json(json.loads(a), json.loads(b)), (a, b)
     assert non_byte <= 2, non_byte
+
+
+def test_json_double_is_nlohmanns_grisu2():
+    """json_double == nlohmann::json::dump() for 6000 doubles across the whole
+    range (golden strings from tests/golden/make_grisu_golden.py), including
+    those where grisu2 is not the shortest representation."""
+    import os
+    import struct
+    from paper_2508_06526_b200.wire import json_double
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "wire",
+                        "doubles_nlohmann.txt")
+    n = 0
+    for line in open(path):
+        bits, text = line.split()
+        x = struct.unpack("<d", struct.pack("<Q", int(bits, 16)))[0]
+        assert json_double(x) == text, (bits, x, text)
+        n += 1
+    assert n >= 5000
+
+
+def test_cpp_facade_json_double_is_nlohmanns_grisu2(tmp_path):
+    """The C++ facade's wire::json_double against the same nlohmann golden."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = str(tmp_path / "test_grisu")
+    r = subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(root, "include"),
+                        os.path.join(root, "tests", "cpp", "test_grisu.cpp"), "-o", exe],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([exe, os.path.join(root, "tests", "golden", "wire", "doubles_nlohmann.txt")],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout
