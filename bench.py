@@ -81,6 +81,23 @@ def l2_note(kv_bytes_step):
             "parity / sweep point, not a bandwidth figure" % mb)
 
 
+def workload_config(name, w, world):
+    """The `config` object of the JSON line: the workload only (identical for
+    this engine's arm and the reference arm at the same N); run details of
+    this arm go to the line's `run` object."""
+    B = w["B"]
+    k, L, E, retain = w["k"], w["L"], w["E"], w.get("retain", 1.0)
+    elem = 2 if w["dtype"] == "bf16" else 4
+    # nominal KV read per step: B streams x (k^2 L / E) retained entries x entry bytes
+    nominal = B * (k * k * L / E) * retain * 2 * w["H"] * w["hd"] * elem
+    return {"workload": name, "description": WORKLOADS[name][0], "batch": B, "global_batch": B,
+            "context": L, "experts": E, "top_k": k, "heads": w["H"], "head_dim": w["hd"],
+            "codec": w["codec"], "kv_dtype": w["dtype"], "scheduler": "LRU page budget",
+            "retain": retain,
+            "placement": "%s-sharded over %d device(s)" % (w.get("placement", "expert"), world),
+            "parallelism": "ep%d" % world, "l2": l2_note(nominal)}
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -246,11 +263,11 @@ def cpu_reference(w, steps, threads=None, prefill=None):
     import ctypes
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from oracle import build as obuild
-    cfg = make_config(dict(w, H=1, hd=w["H"] * w["hd"]), world=1, rank=0, G=1)
+    cfg = make_config(dict(w, H=1, hd=w["H"] * w["hd"]), world=1, rank=0, G=w.get("G", 1))
     cfg.batch = 1
     cfg.kv_dtype = w["dtype"]
     cfg.compressor.scheme = "Identity"
-    threads = threads or min(os.cpu_count() or 1, 16)
+    threads = threads or max(1, min(os.cpu_count() or 1, w["B"]))  # one host thread per stream
     prefill = prefill if prefill is not None else w["L"]
     path = obuild.ref_lib_path()
     if os.path.exists(path):
@@ -293,12 +310,15 @@ def run_reference_arm(args, w, name):
     if rank != 0:
         return
     steps = max(1, args.steps)
-    res = cpu_reference(w, steps=min(steps, 3), prefill=None)
+    # the same K steps as this engine's arm (each = one decode token of
+    # every stream; the reference's streams run as parallel host threads)
+    res = cpu_reference(w, steps=steps, prefill=None)
     line = {"impl": "reference", "metric": "decode tokens/sec", "value": res["value"],
-            "unit": "tokens/s", "n_gpus": args.gpus, "steps": min(steps, 3),
+            "unit": "tokens/s", "n_gpus": args.gpus, "steps": steps,
+            "ms_per_step": res["seconds"] / steps * 1e3,
             "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": name, "description": w and WORKLOADS[name][0]},
+            "config": workload_config(name, w, args.gpus),
             "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": res["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -451,16 +471,11 @@ def run_group(args, w, name, cfg, n_micro, local):
         "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16" if cfg.kv_dtype == "bf16" else "f32",
         "data": "synthetic (device-generated N(0,1) q/k/v; store prefilled to L)",
-        "config": {"workload": name, "description": WORKLOADS[name][0], "batch": B,
-                   "context": w["L"], "experts": w["E"], "top_k": w["k"], "heads": w["H"],
-                   "head_dim": w["hd"], "codec": w["codec"], "scheduler": "LRU page budget",
-                   "placement": "expert-sharded over 1 GPU(s)", "global_batch": B,
-                   "parallelism": "ep1, %d micro-batches of %d streams pipelined "
-                                  "(control/fold-back of one overlap the other's attention)"
-                                  % (n_micro, Bm),
-                   "micro_batches": n_micro, "attend_sms": attend_sms,
-                   "l2": l2_note(kv_bytes_step),
-                   "prefill_s": round(prefill_s, 2)},
+        "config": workload_config(name, w, 1),
+        "run": {"pipeline": "%d micro-batches of %d streams pipelined (control/fold-back of one "
+                            "overlap the other's attention)" % (n_micro, Bm),
+                "micro_batches": n_micro, "attend_sms": attend_sms,
+                "l2_measured": l2_note(kv_bytes_step), "prefill_s": round(prefill_s, 2)},
         "kv_gbs": kv_bytes_step / (ms / args.steps * 1e-3) / 1e9,
         "kv_frac_of_hbm": kv_bytes_step / (ms / args.steps * 1e-3) / 1e9 / peak,
         "attended_per_step": att_last,
@@ -743,16 +758,11 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16"
         if cfg.kv_dtype == "bf16" else "f32",
         "data": "synthetic (device-generated N(0,1) q/k/v; store prefilled to L)",
-        "config": {"workload": name, "description": WORKLOADS[name][0], "batch": B,
-                   "context": w["L"], "experts": w["E"], "top_k": w["k"], "heads": w["H"],
-                   "head_dim": w["hd"], "codec": w["codec"], "scheduler": "LRU page budget",
-                   "placement": "%s-sharded over %d GPU(s) (n_tok=%d, n_exp=%d)" % (
-                       args.placement, world, cfg.store.n_tok, cfg.store.n_exp),
-                   "global_batch": B,
-                   "parallelism": "ep%d (experts over GPUs, LSE merge all-gather)" % world,
-                   "exchange": exchange,
-                   "l2": l2_note(att_last * entry_bytes),
-                   "prefill_s": round(prefill_s, 2)},
+        "config": workload_config(name, w, world),
+        "run": {"store": "n_tok=%d, n_exp=%d over %d GPU(s); LSE merge all-gather" % (
+                    cfg.store.n_tok, cfg.store.n_exp, world),
+                "exchange": exchange, "l2_measured": l2_note(att_last * entry_bytes),
+                "prefill_s": round(prefill_s, 2)},
         "kv_gbs": kv_bytes_step / (ms / args.steps * 1e-3) / 1e9,
         "kv_frac_of_hbm": kv_bytes_step / (ms / args.steps * 1e-3) / 1e9 / (peak * world),
         "attended_per_step": att_last,
