@@ -328,12 +328,15 @@ def run_reference_arm(args, w, name):
 DEFAULT_ATTEND_SMS = 0  # 0 = the library's default (all but 24 SMs; profiles/README.md sweep)
 
 
-def run_group(args, w, name, cfg, n_micro, local):
-    """N=1 with the micro-batch pipeline (pikv_group): the batch's streams are
-    split into n_micro engines; micro-batch m's control plane / fold-back
-    overlap micro-batch m-1's attention.  Same metric, config and timing rules
-    as the single-engine path."""
+def run_group(args, w, name, cfg, n_micro, local, world=1, rank=0, dist_on=False):
+    """The micro-batch pipeline (pikv_group): the batch's streams are split
+    into n_micro engines; micro-batch m's control plane / fold-back overlap
+    micro-batch m-1's attention.  Sharded (N ranks, or --sharded-rehearsal):
+    every micro-batch gets its own NCCL communicator inside the library, so
+    micro-batch m's all-gather overlaps m+1's attention; times are the max over
+    ranks.  Same metric, config and timing rules as the single-engine path."""
     import torch
+    import torch.distributed as dist
     from paper_2508_06526_b200.engine import EngineGroup
     attend_sms = args.attend_sms if args.attend_sms is not None else DEFAULT_ATTEND_SMS
     if attend_sms <= 0:  # the library default (pikv_group_create, attend_sms = 0)
@@ -346,6 +349,19 @@ def run_group(args, w, name, cfg, n_micro, local):
         rng = np.random.default_rng(0)
         basis = np.linalg.qr(rng.standard_normal((hd, hd)))[0][:, :r].T
         grp.set_codec(np.ascontiguousarray(np.repeat(basis[None], cfg.n_heads, 0), np.float32))
+    exchange = "none (one rank)"
+    if dist_on:
+        from paper_2508_06526_b200.parallel import attach_nccl
+        attach_nccl(grp, n_comms=n_micro)
+        exchange = "ncclAllGather inside libpikv_b200, one communicator per micro-batch"
+
+    def max_over_ranks(x):
+        if not dist_on:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     t0 = time.time()
     grp.prefill_synthetic(w["L"], seed=7)
     prefill_s = time.time() - t0
@@ -379,6 +395,9 @@ def run_group(args, w, name, cfg, n_micro, local):
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
+    if dist_on:
+        dist.barrier()
+        torch.cuda.synchronize()
     grp.set_timing(True)
     with ClockSampler(local) as clk:
         if args.ncu_window:
@@ -392,17 +411,26 @@ def run_group(args, w, name, cfg, n_micro, local):
         if args.ncu_window:
             torch.cuda.cudart().cudaProfilerStop()
     grp.set_timing(False)
-    ms = ev0.elapsed_time(ev1)
+    if dist_on:
+        dist.barrier()
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
     launches = grp.kernel_launches() - launches0
     att_ms, n_att = grp.read_timing()
     grp.sync()
     _, _, _, summ = grp.read_step()
-    att_last = sum(s["n_attended"] for s in summ)
+    att_last = sum(s["n_attended"] for s in summ)  # global (after the cross-rank merge)
+    local_att = sum(e.local_attended() for e in grp.engines)  # this rank's own shards
     entry_bytes = grp.engines[0].entry_bytes()
     peak, peak_kind = load_peaks()
     attend_avg_ms = att_ms / max(n_att, 1)
-    alg_per_launch = att_last * entry_bytes / n_micro
+    alg_per_launch = local_att * entry_bytes / n_micro
     achieved = alg_per_launch / (attend_avg_ms * 1e-3) / 1e9 if attend_avg_ms else 0.0
+    rank_bytes = None
+    if dist_on:  # this rank's KV bytes per step, max / min over ranks (balance)
+        mx_b = max_over_ranks(float(local_att * entry_bytes))
+        t = torch.tensor([float(local_att * entry_bytes)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        rank_bytes = {"max": mx_b, "min": float(t.item()), "this_rank": float(local_att * entry_bytes)}
 
     # per-kernel breakdown of one micro-batch engine (eager, events between kernels)
     e0 = grp.engines[0]
@@ -451,34 +479,39 @@ def run_group(args, w, name, cfg, n_micro, local):
     # the host loop is exposed to host scheduling jitter: median of 3 runs
     grp.read_timing()
     grp.set_timing(True)
+    if dist_on:
+        dist.barrier()
     e2e_runs = [e2e_run() for _ in range(3)]
     grp.set_timing(False)
     e2e_att_ms, _ = grp.read_timing()
-    e2e_ms = float(np.median(e2e_runs))
+    e2e_ms = max_over_ranks(float(np.median(e2e_runs)))
     e2e = {"value": B * args.steps / (e2e_ms * 1e-3), "unit": "tokens/s",
            "h2d_bytes_per_step": 3 * B * d * elem, "d2h_bytes_per_step": B * dp * 4,
            "ms_per_step": e2e_ms / args.steps,
            "api": "pikv_group_submit(host=1) / pikv_group_wait per micro-batch",
-           "runs_ms": [round(x, 3) for x in e2e_runs], "statistic": "median of 3 runs",
+           "runs_ms": [round(x, 3) for x in e2e_runs],
+           "statistic": "median of 3 runs" + (", max over ranks" if dist_on else ""),
            "attend_share": e2e_att_ms / sum(e2e_runs) if sum(e2e_runs) else None}
 
     tokens = B * args.steps
     kv_bytes_step = att_last * entry_bytes
     line = {
         "metric": "decode tokens/sec", "value": tokens / (ms * 1e-3), "unit": "tokens/s",
-        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16" if cfg.kv_dtype == "bf16" else "f32",
         "data": "synthetic (device-generated N(0,1) q/k/v; store prefilled to L)",
-        "config": workload_config(name, w, 1),
+        "config": workload_config(name, w, world),
         "run": {"pipeline": "%d micro-batches of %d streams pipelined (control/fold-back of one "
                             "overlap the other's attention)" % (n_micro, Bm),
-                "micro_batches": n_micro, "attend_sms": attend_sms,
+                "micro_batches": n_micro, "attend_sms": attend_sms, "exchange": exchange,
+                "store": "n_tok=%d, n_exp=%d over %d GPU(s)" % (cfg.store.n_tok, cfg.store.n_exp, world),
                 "l2_measured": l2_note(kv_bytes_step), "prefill_s": round(prefill_s, 2)},
         "kv_gbs": kv_bytes_step / (ms / args.steps * 1e-3) / 1e9,
-        "kv_frac_of_hbm": kv_bytes_step / (ms / args.steps * 1e-3) / 1e9 / peak,
+        "kv_frac_of_hbm": kv_bytes_step / (ms / args.steps * 1e-3) / 1e9 / (peak * world),
         "attended_per_step": att_last,
+        "kv_bytes_per_rank_step": rank_bytes,
         "stream_errors": sum(1 for x in summ if x["error"]),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak,
@@ -496,14 +529,23 @@ def run_group(args, w, name, cfg, n_micro, local):
         "clocks": clk.summary(),
         "e2e": e2e,
     }
-    if not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline:
         try:
             res = cpu_reference(w, steps=2)
             line["cpu_baseline"] = {k2: res[k2] for k2 in ("value", "unit", "cores", "kind",
                                                            "sample")}
         except Exception as ex:  # pragma: no cover
             line["cpu_baseline"] = {"value": None, "error": str(ex)}
-    print(json.dumps(line), flush=True)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist_on:  # explicit teardown (see main)
+        torch.cuda.synchronize()
+        dist.barrier()
+        dist.destroy_process_group()
+        grp.close()
+        sys.stdout.flush()
+        sys.stderr.flush()
+        os._exit(0)
     grp.close()
 
 
@@ -524,6 +566,8 @@ def main():
                     help="micro-batches pipelined on the GPU (default 2 at N=1 when B is even)")
     ap.add_argument("--attend-sms", type=int, default=None,
                     help="SMs of the persistent attention grid in the micro-batch pipeline")
+    ap.add_argument("--sharded-rehearsal", action="store_true",
+                    help="run the multi-GPU code path (NCCL exchange + merge) at N = 1")
     ap.add_argument("--placement", default="expert", choices=["expert", "token"],
                     help="shard_assign placement: expert (n_tok=1) or token-interleaved (n_tok=G)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -549,7 +593,15 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
-    if world > 1:
+    # --sharded-rehearsal: the multi-GPU code path at N = 1 (process group of
+    # one, the library's one-rank NCCL communicator, the exchange + merge
+    # kernels), so the path the 8-GPU run takes is exercised on one GPU
+    dist_on = world > 1 or args.sharded_rehearsal
+    if dist_on:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
         if args.dist_backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
@@ -563,11 +615,11 @@ def main():
         # the per-GPU KV read per step stays that of one GPU ("weak" scaling)
         w["B"] = w["B"] * world
     cfg = make_config(w, world=world, rank=rank)
-    n_micro = args.micro if args.micro is not None else (2 if world == 1 and w["B"] % 2 == 0 else 1)
-    if world > 1 or w["B"] % n_micro:
+    n_micro = args.micro if args.micro is not None else (2 if w["B"] % 2 == 0 else 1)
+    if w["B"] % n_micro:
         n_micro = 1
     if n_micro > 1:
-        run_group(args, w, name, cfg, n_micro, local)
+        run_group(args, w, name, cfg, n_micro, local, world, rank, dist_on)
         return
     eng = Engine(cfg, device=local)
     B, d, dp = cfg.batch, cfg.model.d, cfg.stored_width
@@ -578,7 +630,7 @@ def main():
         eng.set_codec(np.ascontiguousarray(np.repeat(basis[None], cfg.n_heads, 0), np.float32))
     stepper = None
     exchange = "none (one rank)"
-    if world > 1:
+    if dist_on:
         # the all-gather of the LSE records inside the library (NCCL on the
         # engine stream, captured in the step graph); torch.distributed as the
         # transport only if the library's communicator cannot be created
@@ -626,7 +678,7 @@ def main():
     # ---------------- timed region (device-resident inputs) ----------------
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    if world > 1:
+    if dist_on:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
@@ -639,12 +691,12 @@ def main():
         torch.cuda.synchronize()
         if args.ncu_window:
             torch.cuda.cudart().cudaProfilerStop()
-    if world > 1:
+    if dist_on:
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
     launches = eng.kernel_launches() - launches0
     t_ms = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
+    if dist_on:
         dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
     ms = float(t_ms.item())
     _, _, _, summ = eng.read_step()
@@ -663,7 +715,7 @@ def main():
     # KV bytes this rank's attention kernel read (its own count, not global / ranks)
     alg_bytes = att_total * entry_bytes
     rank_bytes = None
-    if world > 1:  # per-rank KV bytes per step: max and min over ranks (balance)
+    if dist_on:  # per-rank KV bytes per step: max and min over ranks (balance)
         t_b = torch.tensor([alg_bytes / max(nprof, 1)], dtype=torch.float64, device="cuda")
         mx, mn = t_b.clone(), t_b.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
@@ -704,11 +756,11 @@ def main():
             return e0.elapsed_time(e1)
 
         # a synchronous host loop is exposed to host scheduling jitter: median of 3 runs
-        if world > 1:
+        if dist_on:
             dist.barrier()
         e2e_runs = [e2e_run() for _ in range(3)]
         e2e_ms = float(np.median(e2e_runs))
-        if world > 1:  # max over ranks
+        if dist_on:  # max over ranks
             t_e2e = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
             dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
             e2e_ms = float(t_e2e.item())
@@ -790,7 +842,7 @@ def main():
             line["cpu_baseline"] = {"value": None, "error": str(ex)}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist_on:
         # explicit teardown: every rank done, group gone, engine freed -- then
         # leave without interpreter teardown (torch/NCCL/gloo destructors
         # racing the CUDA context aborted the rehearsal run after the result)

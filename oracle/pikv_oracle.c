@@ -732,6 +732,16 @@ int po_engine_read_payload(po_engine* e, int64_t gi, float* key, float* value) {
     return PIKV_OK;
 }
 
+/* Overwrite the stored K/V of live slot gi (test infrastructure: attend over
+ * exactly the values another store holds, e.g. the GPU's rounded projections). */
+int po_engine_write_payload(po_engine* e, int64_t gi, const float* key, const float* value) {
+    if (gi < 0 || gi >= po_engine_slot_count(e) || !e->slots[gi].id) return PIKV_ERR_INVALID_ARGUMENT;
+    float* p = slot_payload(e, (size_t)gi, 1);
+    memcpy(p, key, sizeof(float) * (size_t)e->dp);
+    memcpy(p + e->dp, value, sizeof(float) * (size_t)e->dp);
+    return PIKV_OK;
+}
+
 int po_engine_set_attn_mass(po_engine* e, const double* attn_mass, const double* per_layer) {
     int64_t n = po_engine_slot_count(e);
     for (int64_t i = 0; i < n; ++i)

@@ -167,6 +167,7 @@ struct pikv_engine {
     size_t rb_cap = 0;
     bool exchange_path() const { return D.world > 1 || comm != nullptr; }
     std::string attend_err;  // non-empty: the decode step cannot run this layout
+    cudaEvent_t y_final_event = nullptr;  // group host path, sharded: recorded after the merge
     double* enc_wt = nullptr;
     double* q64 = nullptr;
     double* in_emb = nullptr;
@@ -760,6 +761,14 @@ static int engine_create(const pikv_config* cfg, int32_t cuda_device, int attend
     CUDA_TRY(cudaMemsetAsync(S.id, 0, sizeof(uint64_t) * total_slots, st));
     CUDA_TRY(cudaMemsetAsync(S.attn_mass, 0, sizeof(double) * total_slots, st));
     CUDA_TRY(cudaMemsetAsync(S.has_pl, 0, total_slots, st));
+    // never-written slots read back as zeros (readback of whole slot arrays)
+    CUDA_TRY(cudaMemsetAsync(S.shard_seq, 0, sizeof(uint64_t) * total_slots, st));
+    CUDA_TRY(cudaMemsetAsync(S.token, 0, sizeof(int64_t) * total_slots, st));
+    CUDA_TRY(cudaMemsetAsync(S.expert, 0, sizeof(int32_t) * total_slots, st));
+    CUDA_TRY(cudaMemsetAsync(S.insert_step, 0, sizeof(uint64_t) * total_slots, st));
+    CUDA_TRY(cudaMemsetAsync(S.last_access, 0, sizeof(uint64_t) * total_slots, st));
+    CUDA_TRY(cudaMemsetAsync(S.freq, 0, sizeof(uint64_t) * total_slots, st));
+    CUDA_TRY(cudaMemsetAsync(S.per_layer, 0, sizeof(double) * total_slots * std::max(D.n_layers, 1), st));
     CUDA_TRY(cudaMemsetAsync(S.pr_cnt, 0, sizeof(int32_t) * rings * D.ppr_sched, st));
     CUDA_TRY(cudaMemsetAsync(S.pages_live, 0, sizeof(int32_t) * B * std::max(D.Gl, 1), st));
     CUDA_TRY(cudaMemsetAsync(S.pr_first, 0, sizeof(int32_t) * rings * D.ppr_sched, st));
@@ -946,6 +955,9 @@ static int enqueue_finish(pikv_engine* eng, const uint8_t* gathered, float* y, b
                           int granks) {
     const bool xp = eng->exchange_path();
     if (xp) launch_finish_merge(eng->D, eng->C, eng->S, eng->X, gathered, y, granks, eng->stream);
+    // y is final here (the cross-rank merge wrote it): a host-path group step
+    // starts its D2H while the fold-back runs
+    if (xp && eng->y_final_event) cudaEventRecord(eng->y_final_event, eng->stream);
     mark(eng, 10);
     // fold-back + feedback in one launch (last CTA runs the feedback); the
     // prefill (no attention) launches the feedback alone
@@ -2387,12 +2399,16 @@ int pikv_group_submit(pikv_group* g, int32_t m, const void* q, const void* k, co
         if (!host) {
             if (!rc) rc = run_step(e, dq, dk, dv, ds, dy, true, nullptr, kPartTail);
         } else if (e->exchange_path()) {
-            // sharded over ranks: y is final only after the all-gather and the
-            // cross-rank merge (the fold part); its D2H follows the whole tail
+            // sharded over ranks: y is final after the all-gather and the
+            // cross-rank merge, inside the fold part; the fold graph records
+            // y_ready right after the merge (y_final_event) and the D2H on
+            // the side stream overlaps the fold-back
             if (!rc) CUDA_TRY(cudaStreamWaitEvent(st, g->y_done[m], 0));
-            if (!rc) rc = run_step(e, dq, dk, dv, ds, dy, true, nullptr, kPartTail);
+            if (!rc) rc = run_step(e, dq, dk, dv, ds, dy, true, nullptr, kPartMerge);
+            e->y_final_event = g->y_ready[m];
+            if (!rc) rc = run_step(e, dq, dk, dv, ds, dy, true, nullptr, kPartFold);
+            e->y_final_event = nullptr;
             if (!rc) {
-                CUDA_TRY(cudaEventRecord(g->y_ready[m], st));
                 CUDA_TRY(cudaStreamWaitEvent(g->side[m], g->y_ready[m], 0));
                 CUDA_TRY(cudaMemcpyAsync(y, e->out_y, g->y_bytes, cudaMemcpyDeviceToHost, g->side[m]));
                 CUDA_TRY(cudaEventRecord(g->y_done[m], g->side[m]));

@@ -74,6 +74,7 @@ def oracle_lib():
         lib.po_engine_read_payload.argtypes = [ctypes.c_void_p, ctypes.c_int64,
                                                ctypes.POINTER(ctypes.c_float),
                                                ctypes.POINTER(ctypes.c_float)]
+        lib.po_engine_write_payload.argtypes = lib.po_engine_read_payload.argtypes
         lib.po_engine_step_embed.argtypes = [ctypes.c_void_p, c_double_p, c_double_p,
                                              ctypes.POINTER(PoStepOut), ctypes.c_int]
         lib.po_encoder_weights.argtypes = [ctypes.c_int, ctypes.c_uint64, c_double_p]
@@ -320,6 +321,17 @@ class OracleEngine(_StepMixin):
             self.lib.po_engine_read_payload(self.h, int(gi), k[i].ctypes.data_as(fp),
                                             v[i].ctypes.data_as(fp))
         return k, v
+
+    def write_payload(self, slots, k, v):
+        """Overwrite the stored K/V of live slots ([n][d'] float32 each)."""
+        fp = ctypes.POINTER(ctypes.c_float)
+        k = np.ascontiguousarray(k, dtype=np.float32)
+        v = np.ascontiguousarray(v, dtype=np.float32)
+        for i, gi in enumerate(slots):
+            rc = self.lib.po_engine_write_payload(self.h, int(gi), k[i].ctypes.data_as(fp),
+                                                  v[i].ctypes.data_as(fp))
+            if rc:
+                raise RuntimeError("write_payload: slot %d not live" % gi)
 
     def set_attn_mass(self, attn_mass, per_layer=None):
         a = np.ascontiguousarray(attn_mass, dtype=np.float64)

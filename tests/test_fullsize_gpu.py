@@ -18,8 +18,8 @@ the CPU oracle on identical inputs.
 Per step and stream, bit-exact: routing, hits/lookups, n_attended,
 fetch_elements, pages before/after, every eviction record in order, the
 attended (token, expert) set; tolerances (stated): gates rel 1e-12, alpha
-abs 1e-6 + rel 1e-4, y rel-L2 <= 2e-5 (low-rank: 1e-4, see
-test_fullsize_group).  After the build and after the last step: the whole
+abs 1e-6 + rel 1e-4, y rel-L2 <= 2e-5 (low-rank: after the store check the
+oracle attends over the GPU's stored projections, see test_fullsize_group).  After the build and after the last step: the whole
 slot metadata, and the stored K/V of sampled slots (exactly equal; low-rank:
 under 1 % of the values one bf16 ulp apart, the rounding of a 16-bit-basis
 tensor-core projection vs the fp64 one).
@@ -181,8 +181,17 @@ def test_fullsize_group(name):
         assert nd_gpu == nd_orc
         del kb, vb
         check_store(grp.engines[s], 0, orcs[s], lowrank=lowrank, seed=s)
+        if lowrank:
+            # the rounding check above bounds the stored projections; from here
+            # on both sides attend over the GPU's stored values, so the decode
+            # steps are held to the same 2e-5 as every other config
+            live = np.flatnonzero(grp.engines[s].slots(0)["id"] != 0)
+            for a in range(0, len(live), 8192):
+                sl = live[a:a + 8192]
+                gk, gv = grp.engines[s].read_entries(0, sl)
+                orcs[s].write_payload(sl, gk, gv)
     # -- decode steps through the pipeline (pinned host submits)
-    ytol = 1e-4 if lowrank else Y_TOL
+    ytol = Y_TOL
     hin = torch.empty(DECODE_STEPS, B, 3, d, dtype=torch.int16).pin_memory()
     hy = torch.zeros(DECODE_STEPS, B, cfg.stored_width, dtype=torch.float32).pin_memory()
     qkv = [make_stream(DECODE_STEPS, d, 300 + s, "bf16", 0) for s in range(B)]

@@ -85,6 +85,25 @@ def test_one_rank_nccl_group():
         torch.cuda.synchronize()
         assert torch.allclose(ya, yb, rtol=1e-5, atol=1e-6), t
         assert np.array_equal(ga.read_step()[0], gb.read_step()[0]), t
+    # pinned host submits: the sharded host path copies y out right after the
+    # cross-rank merge (an event inside the fold graph)
+    Bm = cfg.batch // 2
+    hin = torch.empty(6, 2, 3, Bm, cfg.model.d, dtype=torch.int16).pin_memory()
+    for t in range(6):
+        q, k, v = ins[t]
+        for m in range(2):
+            for j, x in enumerate((q, k, v)):
+                hin[t, m, j] = x[m * Bm:(m + 1) * Bm].cpu()
+    hya = torch.zeros(6, cfg.batch, cfg.stored_width).pin_memory()
+    hyb = torch.zeros(6, cfg.batch, cfg.stored_width).pin_memory()
+    for t in range(6):
+        for m in range(2):
+            for g, hy in ((ga, hya), (gb, hyb)):
+                g.submit(m, hin[t, m, 0].data_ptr(), hin[t, m, 1].data_ptr(), hin[t, m, 2].data_ptr(), None,
+                         hy[t, m * Bm].data_ptr(), host=True)
+    ga.sync(), gb.sync()
+    assert torch.allclose(hya, hyb, rtol=1e-5, atol=1e-6)
+    assert hyb.abs().sum() > 0
     ga.close(), gb.close()
 
 
