@@ -188,6 +188,7 @@ def make_config(w, world=1, rank=0, G=None):
     keep = min(1.15, retain * 1.15 + 0.05)
     c.pool_entries = int(B * (k * L * local_frac * keep + 4096 + 2 * E * ps))
     c.seed = 1
+    c.route_mode = w.get("route", "exact")
     return c
 
 
@@ -566,6 +567,8 @@ def main():
                     help="micro-batches pipelined on the GPU (default 2 at N=1 when B is even)")
     ap.add_argument("--attend-sms", type=int, default=None,
                     help="SMs of the persistent attention grid in the micro-batch pipeline")
+    ap.add_argument("--route", default="exact", choices=["exact", "fast"],
+                    help="router logits: exact sequential fp64 chain (parity mode) or fp64 tree (fast)")
     ap.add_argument("--sharded-rehearsal", action="store_true",
                     help="run the multi-GPU code path (NCCL exchange + merge) at N = 1")
     ap.add_argument("--placement", default="expert", choices=["expert", "token"],
@@ -582,6 +585,7 @@ def main():
     if args.retain is not None:
         w["retain"] = args.retain
     w["placement"] = args.placement
+    w["route"] = args.route
     if args.impl == "reference":
         run_reference_arm(args, w, name)
         return

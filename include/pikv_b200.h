@@ -124,7 +124,17 @@ typedef struct pikv_config {
     int32_t rank_id;
     int64_t pool_entries; /* KV page pool capacity in entries (0 = auto)     */
     uint64_t seed;        /* EngineConfig.seed: W_r = Rng(seed ^ kRouterSalt) */
+    /* PIKV_ROUTE_EXACT: logits as the reference's sequential fp64 sum
+     * (router.cpp:224-229, bit-exact routing); PIKV_ROUTE_FAST: the same fp64
+     * products reduced as a tree (FMA) -- rounding-order differences only,
+     * routing flips only on near-ties (tests report the rate), ~10x lower
+     * route latency. */
+    int32_t route_mode;
+    int32_t reserved0;
 } pikv_config;
+
+#define PIKV_ROUTE_EXACT 0
+#define PIKV_ROUTE_FAST 1
 
 /* One eviction record, scheduler.hpp:90-98 (+ the stream it belongs to). */
 typedef struct pikv_evict_record {

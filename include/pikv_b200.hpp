@@ -174,6 +174,7 @@ struct EngineConfig {  // pipeline.hpp:87-98 (+ B200 runtime fields)
     DType kv_dtype = DType::F32;
     long long pool_entries = 0;
     int cuda_device = 0;
+    bool fast_routing = false;  // PIKV_ROUTE_FAST (tree-reduced fp64 logits)
 
     pikv_config to_c() const {
         pikv_config c;
@@ -203,6 +204,7 @@ struct EngineConfig {  // pipeline.hpp:87-98 (+ B200 runtime fields)
         c.unbounded_budget = unbounded_budget, c.n_layers = n_layers, c.batch = batch;
         c.kv_dtype = kv_dtype == DType::BF16 ? PIKV_DTYPE_BF16 : PIKV_DTYPE_F32;
         c.world_size = 1, c.rank_id = 0, c.pool_entries = pool_entries, c.seed = seed;
+        c.route_mode = fast_routing ? PIKV_ROUTE_FAST : PIKV_ROUTE_EXACT;
         return c;
     }
 };

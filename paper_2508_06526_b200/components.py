@@ -316,8 +316,9 @@ class RouterState:
     """RouterState::init(experts, width, seed) (router.cpp:54-67) on the GPU:
     W_r = Rng(seed) N(0, 1/d); load / usage / miss / bandit bias in HBM."""
 
-    def __init__(self, experts: int, width: int, seed: int, device: int = 0):
+    def __init__(self, experts: int, width: int, seed: int, device: int = 0, route_mode: str = "exact"):
         self.experts, self.width, self.seed, self.device = experts, width, seed, device
+        self.route_mode = route_mode  # "fast": tree-reduced fp64 logits (PIKV_ROUTE_FAST)
         self._eng = None
         self._k = None
         self._cfg = None
@@ -340,6 +341,7 @@ class RouterState:
         c.router = rcfg
         c.unbounded_budget = True
         c.seed = self.seed ^ ROUTER_SALT  # W_r = Rng(cfg.seed ^ salt) = Rng(seed)
+        c.route_mode = self.route_mode
         c.batch, c.n_layers, c.pool_entries = 1, 0, 16
         if self._eng is not None:
             self._eng.close()

@@ -55,6 +55,7 @@ class PikvConfigC(ctypes.Structure):
         ("batch", ctypes.c_int32), ("kv_dtype", ctypes.c_int32),
         ("world_size", ctypes.c_int32), ("rank_id", ctypes.c_int32),
         ("pool_entries", ctypes.c_int64), ("seed", ctypes.c_uint64),
+        ("route_mode", ctypes.c_int32), ("reserved0", ctypes.c_int32),
     ]
 
 
@@ -132,6 +133,7 @@ class EngineConfig:                     # pipeline.hpp:87-98
     compressor: CompressorConfig = field(default_factory=CompressorConfig)
     unbounded_budget: bool = False
     seed: int = 1
+    route_mode: str = "exact"            # "fast": tree-reduced fp64 logits (PIKV_ROUTE_FAST)
     # ---- B200 runtime (no reference counterpart) ----
     n_heads: int = 1
     n_layers: int = 0
@@ -193,4 +195,5 @@ class EngineConfig:                     # pipeline.hpp:87-98
         c.batch, c.kv_dtype = self.batch, DTYPE[self.kv_dtype]
         c.world_size, c.rank_id, c.pool_entries = self.world_size, self.rank_id, self.pool_entries
         c.seed = self.seed & 0xFFFFFFFFFFFFFFFF
+        c.route_mode = {"exact": 0, "fast": 1}[self.route_mode]
         return c

@@ -458,6 +458,8 @@ static int validate(const pikv_config& c) {
         return fail(PIKV_ERR_INVALID_CONFIG, "bad world_size / rank_id");
     if (c.codec < PIKV_CODEC_IDENTITY || c.codec > PIKV_CODEC_INT4)
         return fail(PIKV_ERR_INVALID_CONFIG, "unknown codec");
+    if (c.route_mode != PIKV_ROUTE_EXACT && c.route_mode != PIKV_ROUTE_FAST)
+        return fail(PIKV_ERR_INVALID_CONFIG, "route_mode must be PIKV_ROUTE_EXACT or PIKV_ROUTE_FAST");
     if (c.kv_dtype != PIKV_DTYPE_F32 && c.kv_dtype != PIKV_DTYPE_BF16)
         return fail(PIKV_ERR_INVALID_CONFIG, "kv_dtype must be f32 or bf16");
     const int hd = c.d / c.n_heads;
@@ -487,6 +489,7 @@ static void fill_cfg(const pikv_config& c, Cfg& C) {
     std::memcpy(C.adakv_weights, c.adakv_weights, sizeof(C.adakv_weights));
     std::memcpy(C.flex_plan, c.flex_plan, sizeof(C.flex_plan));
     C.unbounded_budget = c.unbounded_budget, C.head_width = c.head_width;
+    C.route_mode = c.route_mode;
     // Page aggregates (scheduler.cpp:276-289) are summed in slot order.  When
     // every score is an integer multiple of 2^-10 and the page sum stays below
     // 2^42 in magnitude, each partial sum is exact, so any summation order is

@@ -156,7 +156,21 @@ __device__ __forceinline__ const int* route_body(const Dims& D, const Cfg& C, co
         for (int e = tid; e < D.E; e += blockDim.x) sm_logit[e] = logits_in[e];
         __syncthreads();
     }
-    if (!base && !logits_in) {
+    if (!base && !logits_in && C.route_mode == PIKV_ROUTE_FAST) {
+        // fast routing: the same fp64 products reduced as a tree (FMA, warp
+        // shuffles) instead of the reference's sequential sum -- logits differ
+        // in rounding order only; one warp per expert, W read from L2
+        const int warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+        const int CH = kRouteCH, rs = CH + 2;
+        for (int e = warp; e < D.E; e += nw) {
+            double acc = 0.0;
+            for (int i = lane; i < D.d; i += 32)
+                acc = fma(S.W[((size_t)(i / CH) * D.E + e) * rs + i % CH], sm_q[i], acc);
+            for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+            if (lane == 0) sm_logit[e] = acc;
+        }
+        __syncthreads();
+    } else if (!base && !logits_in) {
         const int E = D.E, CH = kRouteCH;
         const int nchunk = (D.d + CH - 1) / CH;
         const int warp = tid >> 5, lane = tid & 31;

@@ -79,6 +79,7 @@ struct Cfg {  // scalar config needed on device (copied by value into kernels)
     double flex_plan[32];
     int unbounded_budget, head_width;
     int exact_sum;  // page aggregates are exact in any order (see capi.cu)
+    int route_mode; // PIKV_ROUTE_EXACT (sequential fp64 chain) / PIKV_ROUTE_FAST (fp64 tree)
     int record_agg; // LRU / LRU+ with exact sums: aggregates from page records
 };
 

@@ -434,3 +434,24 @@ def test_lowrank_codec_matches_projection():  # compressor.cpp:318-340
     y = c.encode_vector(x)
     assert np.allclose(y, basis @ x, rtol=1e-5, atol=1e-5)
     assert np.allclose(c.decode_vector(y), basis.T @ (basis @ x), rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("E,k,d", [(16, 2, 4096), (64, 4, 1024)])
+def test_fast_routing_flip_rate(E, k, d):
+    """PIKV_ROUTE_FAST (tree-reduced fp64 logits) against the exact sequential
+    chain (router.cpp:224-229) on the same 4000 N(0,1) queries: logits agree
+    to rounding order (<= 1e-12 relative to the row norm), and the selected
+    experts flip only on near-ties (the rate is reported; bound 1e-3)."""
+    rng = np.random.default_rng(E)
+    ex, fa = RouterState(E, d, 7), RouterState(E, d, 7, route_mode="fast")
+    cfg = rc("TopK", k)
+    flips, worst = 0, 0.0
+    n = 4000
+    for q in rng.standard_normal((n, d)):
+        a, b = route(q, ex, cfg), route(q, fa, cfg)
+        la, lb = np.array(a.logits), np.array(b.logits)
+        worst = max(worst, float(np.max(np.abs(la - lb)) / max(np.linalg.norm(la), 1e-300)))
+        flips += a.experts != b.experts
+    print("fast routing E%d k%d d%d: %d / %d selections differ, logit rel diff %.2e" % (E, k, d, flips, n, worst))
+    assert worst <= 1e-12
+    assert flips / n <= 1e-3
