@@ -32,6 +32,9 @@ import time
 
 import numpy as np
 
+# one JSON line on stdout: NCCL prints its version banner there otherwise
+os.environ.setdefault("NCCL_DEBUG", "WARN")
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -270,6 +273,15 @@ def cpu_reference(w, steps, threads=None, prefill=None):
     cfg.compressor.scheme = "Identity"
     threads = threads or max(1, min(os.cpu_count() or 1, w["B"]))  # one host thread per stream
     prefill = prefill if prefill is not None else w["L"]
+    # the reference keeps every entry's K and V as fp64 vectors: bound the
+    # streams run at once by half the host's available memory (c3: 17 GB of
+    # KV per stream at 128K tokens)
+    try:
+        avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+        per_stream = prefill * w["k"] * 2 * w["H"] * w["hd"] * 8 * 1.3
+        threads = max(1, min(threads, int(0.5 * avail // max(per_stream, 1))))
+    except (ValueError, OSError, AttributeError):
+        pass
     path = obuild.ref_lib_path()
     if os.path.exists(path):
         from oracle_bind import ref_lib
@@ -507,6 +519,7 @@ def run_group(args, w, name, cfg, n_micro, local, world=1, rank=0, dist_on=False
         "run": {"pipeline": "%d micro-batches of %d streams pipelined (control/fold-back of one "
                             "overlap the other's attention)" % (n_micro, Bm),
                 "micro_batches": n_micro, "attend_sms": attend_sms, "exchange": exchange,
+                "route": w.get("route", "exact"),
                 "store": "n_tok=%d, n_exp=%d over %d GPU(s)" % (cfg.store.n_tok, cfg.store.n_exp, world),
                 "l2_measured": l2_note(kv_bytes_step), "prefill_s": round(prefill_s, 2)},
         "kv_gbs": kv_bytes_step / (ms / args.steps * 1e-3) / 1e9,
@@ -817,7 +830,8 @@ def main():
         "config": workload_config(name, w, world),
         "run": {"store": "n_tok=%d, n_exp=%d over %d GPU(s); LSE merge all-gather" % (
                     cfg.store.n_tok, cfg.store.n_exp, world),
-                "exchange": exchange, "l2_measured": l2_note(att_last * entry_bytes),
+                "exchange": exchange, "route": w.get("route", "exact"),
+                "l2_measured": l2_note(att_last * entry_bytes),
                 "prefill_s": round(prefill_s, 2)},
         "kv_gbs": kv_bytes_step / (ms / args.steps * 1e-3) / 1e9,
         "kv_frac_of_hbm": kv_bytes_step / (ms / args.steps * 1e-3) / 1e9 / (peak * world),
