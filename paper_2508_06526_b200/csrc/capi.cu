@@ -44,6 +44,7 @@ __global__ void k_lr_decode(const float*, const float*, const float*, int32_t, i
                             int32_t, float*);
 const char* attend_check(const Dims& D);
 int attend_entries_per_stage(const Dims& D);
+int attend_ctas_per_sm(const Dims& D);
 }  // namespace pikv_dev
 
 namespace {
@@ -581,7 +582,7 @@ static int engine_create(const pikv_config* cfg, int32_t cuda_device, int attend
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device);
     if (const char* v = std::getenv("PIKV_ATTEND_SMS")) attend_sms = std::atoi(v);
-    D.attend_ctas = 2 * (attend_sms > 0 ? std::min(attend_sms, sms) : sms);  // two CTAs per SM
+    D.attend_ctas = attend_ctas_per_sm(D) * (attend_sms > 0 ? std::min(attend_sms, sms) : sms);
     {
         const char* v = std::getenv("PIKV_ITEMS");
         D.items_per_cta = v ? std::max(1, std::atoi(v)) : items_per_cta;
@@ -960,7 +961,8 @@ static int enqueue_finish(pikv_engine* eng, const uint8_t* gathered, float* y, b
     if (xp) launch_finish_merge(eng->D, eng->C, eng->S, eng->X, gathered, y, granks, eng->stream);
     // y is final here (the cross-rank merge wrote it): a host-path group step
     // starts its D2H while the fold-back runs
-    if (xp && eng->y_final_event) cudaEventRecord(eng->y_final_event, eng->stream);
+    // (an external event node when captured: waited on outside the graph)
+    if (xp && eng->y_final_event) cudaEventRecordWithFlags(eng->y_final_event, eng->stream, cudaEventRecordExternal);
     mark(eng, 10);
     // fold-back + feedback in one launch (last CTA runs the feedback); the
     // prefill (no attention) launches the feedback alone

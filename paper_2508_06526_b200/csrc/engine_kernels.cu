@@ -160,12 +160,25 @@ __device__ __forceinline__ const int* route_body(const Dims& D, const Cfg& C, co
         // fast routing: the same fp64 products reduced as a tree (FMA, warp
         // shuffles) instead of the reference's sequential sum -- logits differ
         // in rounding order only; one warp per expert, W read from L2
+        // (k_route launches one warp per expert in this mode; four independent
+        // accumulators keep the L2 loads in flight)
         const int warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
         const int CH = kRouteCH, rs = CH + 2;
         for (int e = warp; e < D.E; e += nw) {
-            double acc = 0.0;
-            for (int i = lane; i < D.d; i += 32)
-                acc = fma(S.W[((size_t)(i / CH) * D.E + e) * rs + i % CH], sm_q[i], acc);
+            double a[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int c0 = 0; c0 < D.d; c0 += CH) {
+                const double* row = S.W + ((size_t)(c0 / CH) * D.E + e) * rs;
+                const double* qq = sm_q + c0;
+                const int w = min(CH, D.d - c0);
+                if (w == CH) {
+#pragma unroll
+                    for (int u = 0; u < kRouteCHMax / 32; ++u)
+                        if (u * 32 < CH) a[u & 3] = fma(row[lane + u * 32], qq[lane + u * 32], a[u & 3]);
+                } else {
+                    for (int i = lane; i < w; i += 32) a[0] = fma(row[i], qq[i], a[0]);
+                }
+            }
+            double acc = (a[0] + a[1]) + (a[2] + a[3]);
             for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
             if (lane == 0) sm_logit[e] = acc;
         }
@@ -464,7 +477,8 @@ void launch_route(const Dims& D, const Cfg& C, const State& S, const void* q, cu
     const size_t smem = route_smem_bytes(D, D.route_ch);
     // static shared memory counts against the 48 KB default too: always opt in
     cudaFuncSetAttribute(k_route, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const int threads = ((D.E + 31) / 32) * 32 + 32;
+    int threads = ((D.E + 31) / 32) * 32 + 32;
+    if (C.route_mode == PIKV_ROUTE_FAST) threads = std::max(threads, std::min(1024, 32 * D.E));
     launch_pdl(k_route, dim3(D.B), dim3(threads), smem, st, D, C, S, q);
 }
 

@@ -463,6 +463,10 @@ void launch_retr_count(const Dims& D, const State& S, cudaStream_t st);
 void launch_retr_scan(const Dims& D, const Cfg& C, const State& S, cudaStream_t st);
 void launch_retr_write(const Dims& D, const State& S, cudaStream_t st);
 void launch_attend(const Dims& D, const State& S, cudaStream_t st);
+bool attend_i4tc_applies(const Dims& D);  // int4 / 128-dim heads: the tensor-core kernel (attend_i4tc.cu)
+void launch_attend_i4tc(const Dims& D, const State& S, cudaStream_t st);
+int attend_i4tc_eps();
+int attend_i4tc_stages(const Dims& D);
 void launch_combine(const Dims& D, const Cfg& C, const State& S, const ExchangeLayout& X, float* y,
                     int direct, int attended, cudaStream_t st);
 void launch_finish_merge(const Dims& D, const Cfg& C, const State& S, const ExchangeLayout& X,

@@ -46,7 +46,7 @@ def rel_l2(a, b):
 
 
 def run_parity(cfg, T, seed, inject=True, basis=None, bias=None, kept=None, check_slots=True,
-               mutate=None, embed=False, no_saliency=False):
+               mutate=None, embed=False, no_saliency=False, stream_fn=None):
     B = cfg.batch
     eng = Engine(cfg)
     if basis is not None or bias is not None or kept is not None:
@@ -55,6 +55,8 @@ def run_parity(cfg, T, seed, inject=True, basis=None, bias=None, kept=None, chec
     orc = [OracleEngine(cfg, basis=ob, bias=bias, kept=kept) for _ in range(B)]
     streams = [make_stream(T, cfg.model.d, seed + 1000 * s, cfg.kv_dtype, cfg.n_layers)
                for s in range(B)]
+    if stream_fn is not None:
+        streams = [stream_fn(s, st) for s, st in enumerate(streams)]
     for t in range(T):
         if mutate is not None:
             mutate(t, orc)
@@ -262,6 +264,31 @@ def test_engine_c4_quant_shape_parity(codec):
                         codec=codec)
     cfg.model.head_width = 128
     run_parity(cfg, 60, 23, inject=False)
+
+
+@pytest.mark.parametrize("tc", ["1", "0"])
+def test_engine_int4_dynamic_range(monkeypatch, tc):
+    """int4 at the c4 head shape with a wide dynamic range: per-token K and V
+    magnitudes spread over 10^-2..10^2 and a sharpened q, so the running max
+    jumps and the V scales differ by orders of magnitude between entries --
+    the tensor-core kernel's weight epochs (attend_i4tc.cu) are re-based
+    many times per item.  Both kernels against the oracle, y within 2e-5."""
+    from oracle_bind import round_to
+    monkeypatch.setenv("PIKV_I4TC", tc)
+    cfg = engine_config(router="TopK", sched="LRU", d=4096, H=32, E=16, k=2, G=1, n_tok=1,
+                        n_exp=16, S=64, ps=16, budget=6, batch=2, dtype="bf16", n_layers=0,
+                        codec="Int4")
+    cfg.model.head_width = 128
+
+    def widen(s, st):
+        q, k, v, sal = st
+        rng = np.random.default_rng(77 + s)
+        T = q.shape[0]
+        ks = 10.0 ** rng.uniform(-1, 1, size=(T, 1))
+        vs = 10.0 ** rng.uniform(-2, 2, size=(T, 1))
+        return (round_to(q * 4.0, "bf16"), round_to(k * ks, "bf16"), round_to(v * vs, "bf16"), sal)
+
+    run_parity(cfg, 60, 29, inject=False, stream_fn=widen)
 
 
 def test_engine_full_context_invariants():
