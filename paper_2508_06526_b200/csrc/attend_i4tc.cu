@@ -48,6 +48,7 @@ constexpr int kPad = 32;           // smem entry stride = entry_bytes + kPad
 constexpr int kNQ = 4;             // work-item queue depth
 constexpr int kTau = 5;            // epoch headroom bits
 constexpr float kLim = 16777215.f;  // weights must round to < 2^24 (three u8 digits)
+constexpr int kEpochMax = 32768;    // entries per epoch: 255 * 240 * n < 2^31
 constexpr unsigned kFull = 0xffffffffu;
 // q digit planes of a head pair in smem: [head 2][plane 3][K word 16][even, odd],
 // planes padded to 36 words (bank spread of the per-lane LDS.128 reads)
@@ -61,6 +62,7 @@ struct I4Params {
     int stage_bytes;  // kEPS * stride
     int dyn;          // work items from the global ticket (1) or strided (0)
     float scale2;     // log2(e) / sqrt(128)
+    uint32_t c88, c0f;  // nibble masks (kernel parameters, so they stay in registers)
 };
 
 __device__ __forceinline__ void imma_u8s8(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
@@ -82,9 +84,24 @@ __device__ __forceinline__ float ex2a(float x) {  // 2^x, x <= 0
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
-// two's-complement nibbles -> u8 (c + 8): even nibbles of w, odd nibbles of w
-__device__ __forceinline__ uint32_t nib_lo(uint32_t w) { return (w ^ 0x88888888u) & 0x0F0F0F0Fu; }
-__device__ __forceinline__ uint32_t nib_hi(uint32_t w) { return ((w >> 4) & 0x0F0F0F0Fu) ^ 0x08080808u; }
+// two's-complement nibbles -> biased u8 lanes (c + 8), one LOP3 each with the
+// masks in registers (c88 = 0x88888888, c0f = 0x0F0F0F0F): even nibbles as
+// c + 8, odd nibbles as 16 (c + 8) (no shift; the x16 is removed in integers)
+__device__ __forceinline__ uint32_t nlo(uint32_t w, uint32_t c88, uint32_t c0f) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, 0x28;" : "=r"(d) : "r"(w), "r"(c88), "r"(c0f));  // (w ^ c88) & c0f
+    return d;
+}
+__device__ __forceinline__ uint32_t nhi(uint32_t w, uint32_t c88, uint32_t c0f) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, 0x14;" : "=r"(d) : "r"(w), "r"(c88), "r"(c0f));  // (w ^ c88) & ~c0f
+    return d;
+}
+__device__ __forceinline__ float rcpa(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 
 __global__ void __launch_bounds__(17 * 32, 1) k_attend_i4tc(Dims D, State S, I4Params P) {
     griddep_enter();
@@ -257,25 +274,29 @@ __global__ void __launch_bounds__(17 * 32, 1) k_attend_i4tc(Dims D, State S, I4P
             xs = __shfl_sync(kFull, qinv, hsrc) * P.scale2;
         }
         // B fragments of the q.k MMAs: column g = digit plane g of head h0
-        // (g < 3; MMAs 0-3) or g - 4 of head h1 (4 <= g < 7; MMAs 4-7), K words
-        // 4t..4t+3; inactive lanes read zeros
+        // (g < 3) or g - 4 of head h1 (4 <= g < 7); lane t reads the even / odd
+        // digits of K words 4t..4t+3; inactive lanes read zeros
         const uint4* qf0 = g < 3 ? (const uint4*)(qw + g * kQPlane + 8 * t) : qzero;
         const uint4* qf1 = (g >= 4 && g < 7) ? (const uint4*)(qw + (3 + g - 4) * kQPlane + 8 * t) : qzero;
+        float* scp = S.scores + (pos0 + 2 * g + odd) * H + hm;  // this lane's logit slot, stage 0
 
         float m = -INFINITY, l = 0.f, E = 1.f, invE = 1.f;
         bool have = false;
+        int since = 0;  // entries in the current epoch (s32 headroom of the x16 tiles)
         unsigned long long wsum = 0ull;
+        // p.v tiles: tile 4 wh + T rows g / g + 8 = d 64 wh + 8g + T / + 4;
+        // odd T are high nibbles (x16)
         int acc[8][4];
-        // o of head hm at d = 8g + T (t even) or 64 + 8g + T (t odd): the
-        // values this lane writes at the end of the item
+        // o of head hm at d = 64 wh + 8g + T (+ 4 for t odd): the values this
+        // lane writes at the end of the item
         float oF[8];
 #pragma unroll
         for (int T = 0; T < 8; ++T) {
             acc[T][0] = acc[T][1] = acc[T][2] = acc[T][3] = 0;
             oF[T] = 0.f;
         }
-        // fold the epoch's integer sums into oF: o = sum_p 256^p D_p - 8 sum w
-        // (exact in fp64), scaled by the epoch's E
+        // fold the epoch's integer sums into oF: o = sum_p 256^p D_p (/16 for
+        // high-nibble tiles) - 8 sum w, exact in fp64, scaled by the epoch's E
         auto fold = [&]() {
             unsigned long long W = wsum;
 #pragma unroll
@@ -285,81 +306,89 @@ __global__ void __launch_bounds__(17 * 32, 1) k_attend_i4tc(Dims D, State S, I4P
             const double Ed = (double)E;
 #pragma unroll
             for (int T = 0; T < 8; ++T) {
-                double v0 = (double)acc[T][0] * fa + (double)acc[T][1] * fb - cw;
-                double v1 = (double)acc[T][2] * fa + (double)acc[T][3] * fb - cw;
+                const double sc = (T & 1) ? 0.0625 : 1.0;
+                const double v0 = ((double)acc[T][0] * fa + (double)acc[T][1] * fb) * sc - cw;
+                const double v1 = ((double)acc[T][2] * fa + (double)acc[T][3] * fb) * sc - cw;
                 // t even keeps row g, t odd row g + 8: swap halves, then add
                 const double mine = odd ? v1 : v0, other = odd ? v0 : v1;
                 oF[T] += (float)((mine + __shfl_xor_sync(kFull, other, 1)) * Ed);
                 acc[T][0] = acc[T][1] = acc[T][2] = acc[T][3] = 0;
             }
             wsum = 0ull;
+            since = 0;
         };
+        const uint32_t c88 = P.c88, c0f = P.c0f;  // LOP3 operands (both masks in one op)
 
-        for (int b = 0; b < cnt; b += kEPS) {
-            const int n = min(kEPS, cnt - b);
-            mbar_wait_sleep(&full[stage], phase);
+        // one pass per stage, plus a final pass (b >= cnt) that only folds: the
+        // fold is inlined once
+        for (int b = 0;; b += kEPS, scp += kEPS * H) {
+            const bool fin = b >= cnt;
             const uint8_t* sb = stages + (size_t)stage * P.stage_bytes;
-            const uint8_t* r0 = sb + (size_t)(2 * g) * P.stride;  // entry 2g
-            const uint8_t* r1 = r0 + P.stride;                    // entry 2g + 1
-            // ---------------- q.k: 8 MMAs (4 K words x 2 heads) ----------------
-            int dq[4] = {0, 0, 0, 0};
-            {
-                uint32_t qB[8][2];
-                {
-                    const uint4 f0 = qf0[0], f1 = qf0[1], f2 = qf1[0], f3 = qf1[1];
-                    qB[0][0] = f0.x, qB[0][1] = f0.y, qB[1][0] = f0.z, qB[1][1] = f0.w;
-                    qB[2][0] = f1.x, qB[2][1] = f1.y, qB[3][0] = f1.z, qB[3][1] = f1.w;
-                    qB[4][0] = f2.x, qB[4][1] = f2.y, qB[5][0] = f2.z, qB[5][1] = f2.w;
-                    qB[6][0] = f3.x, qB[6][1] = f3.y, qB[7][0] = f3.z, qB[7][1] = f3.w;
+            float z0 = 0.f, z1 = 0.f, wf0 = 0.f, wf1 = 0.f;
+            bool need = false;
+            if (!fin) {
+                const int n = min(kEPS, cnt - b);
+                mbar_wait_sleep(&full[stage], phase);
+                const uint8_t* r0 = sb + (size_t)(2 * g) * P.stride;  // entry 2g
+                const uint8_t* r1 = r0 + P.stride;                    // entry 2g + 1
+                // ---------------- q.k: 8 MMAs ----------------
+                // per head: K words 4t..4t+3 of entries 2g, 2g+1; low nibbles (even
+                // d) and high nibbles (odd d, x16) in separate MMAs and accumulators
+                int dl[4] = {0, 0, 0, 0}, dh[4] = {0, 0, 0, 0};
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    const uint4 f0 = (hh ? qf1 : qf0)[0], f1 = (hh ? qf1 : qf0)[1];
+                    const uint4 ka = *(const uint4*)(r0 + (hh ? koff1 : koff0));
+                    const uint4 kb = *(const uint4*)(r1 + (hh ? koff1 : koff0));
+                    imma_u8s8(dl, nlo(ka.x, c88, c0f), nlo(kb.x, c88, c0f), nlo(ka.y, c88, c0f), nlo(kb.y, c88, c0f),
+                              f0.x, f0.z);
+                    imma_u8s8(dh, nhi(ka.x, c88, c0f), nhi(kb.x, c88, c0f), nhi(ka.y, c88, c0f), nhi(kb.y, c88, c0f),
+                              f0.y, f0.w);
+                    imma_u8s8(dl, nlo(ka.z, c88, c0f), nlo(kb.z, c88, c0f), nlo(ka.w, c88, c0f), nlo(kb.w, c88, c0f),
+                              f1.x, f1.z);
+                    imma_u8s8(dh, nhi(ka.z, c88, c0f), nhi(kb.z, c88, c0f), nhi(ka.w, c88, c0f), nhi(kb.w, c88, c0f),
+                              f1.y, f1.w);
                 }
-                const uint4 ka = *(const uint4*)(r0 + koff0), kb = *(const uint4*)(r1 + koff0);
-                const uint4 kc = *(const uint4*)(r0 + koff1), kd = *(const uint4*)(r1 + koff1);
-                imma_u8s8(dq, nib_lo(ka.x), nib_lo(kb.x), nib_hi(ka.x), nib_hi(kb.x), qB[0][0], qB[0][1]);
-                imma_u8s8(dq, nib_lo(ka.y), nib_lo(kb.y), nib_hi(ka.y), nib_hi(kb.y), qB[1][0], qB[1][1]);
-                imma_u8s8(dq, nib_lo(ka.z), nib_lo(kb.z), nib_hi(ka.z), nib_hi(kb.z), qB[2][0], qB[2][1]);
-                imma_u8s8(dq, nib_lo(ka.w), nib_lo(kb.w), nib_hi(ka.w), nib_hi(kb.w), qB[3][0], qB[3][1]);
-                imma_u8s8(dq, nib_lo(kc.x), nib_lo(kd.x), nib_hi(kc.x), nib_hi(kd.x), qB[4][0], qB[4][1]);
-                imma_u8s8(dq, nib_lo(kc.y), nib_lo(kd.y), nib_hi(kc.y), nib_hi(kd.y), qB[5][0], qB[5][1]);
-                imma_u8s8(dq, nib_lo(kc.z), nib_lo(kd.z), nib_hi(kc.z), nib_hi(kd.z), qB[6][0], qB[6][1]);
-                imma_u8s8(dq, nib_lo(kc.w), nib_lo(kd.w), nib_hi(kc.w), nib_hi(kd.w), qB[7][0], qB[7][1]);
-            }
-            const float sk0 = *(const float*)(r0 + 2 * pay + 4 * hm), sk1 = *(const float*)(r1 + 2 * pay + 4 * hm);
-            const float sv0 = *(const float*)(r0 + 2 * pay + 4 * (H + hm));
-            const float sv1 = *(const float*)(r1 + 2 * pay + 4 * (H + hm));
-            // column 2t (+ 2t + 1): planes 0, 1 (t even) or plane 2 (t odd) of head hm
-            const float fa = odd ? 65536.f : 1.f, fb = odd ? 0.f : 256.f;
-            float s0 = (float)(dq[0] - cA) * fa + (float)(dq[1] - cB) * fb;
-            float s1 = (float)(dq[2] - cA) * fa + (float)(dq[3] - cB) * fb;
-            s0 += __shfl_xor_sync(kFull, s0, 1);
-            s1 += __shfl_xor_sync(kFull, s1, 1);
-            const bool v0 = 2 * g < n, v1 = 2 * g + 1 < n;
-            const float x0 = v0 ? s0 * xs * sk0 : -INFINITY;
-            const float x1 = v1 ? s1 * xs * sk1 : -INFINITY;
-            {
-                float* scp = S.scores + (pos0 + b + 2 * g + odd) * H + hm;
+                const float sk0 = *(const float*)(r0 + 2 * pay + 4 * hm), sk1 = *(const float*)(r1 + 2 * pay + 4 * hm);
+                const float sv0 = *(const float*)(r0 + 2 * pay + 4 * (H + hm));
+                const float sv1 = *(const float*)(r1 + 2 * pay + 4 * (H + hm));
+                // column 2t (+ 2t + 1): planes 0, 1 (t even) or plane 2 (t odd) of head hm
+                const float fa = odd ? 65536.f : 1.f, fb = odd ? 0.f : 256.f;
+                float s0 = (float)(dl[0] + (dh[0] >> 4) - cA) * fa + (float)(dl[1] + (dh[1] >> 4) - cB) * fb;
+                float s1 = (float)(dl[2] + (dh[2] >> 4) - cA) * fa + (float)(dl[3] + (dh[3] >> 4) - cB) * fb;
+                s0 += __shfl_xor_sync(kFull, s0, 1);
+                s1 += __shfl_xor_sync(kFull, s1, 1);
+                const bool v0 = 2 * g < n, v1 = 2 * g + 1 < n;
+                const float x0 = v0 ? s0 * xs * sk0 : -INFINITY;
+                const float x1 = v1 ? s1 * xs * sk1 : -INFINITY;
                 if (odd ? v1 : v0) *scp = odd ? x1 : x0;
-            }
-            // ---------------- online softmax of head hm ----------------
-            float mx = fmaxf(x0, x1);
+                // ---------------- online softmax of head hm ----------------
+                float mx = fmaxf(x0, x1);
 #pragma unroll
-            for (int off = 4; off < 32; off <<= 1) mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, off));
-            if (mx > m) {
-                const float c = ex2a(m - mx);  // m = -inf -> 0
-                l *= c;
+                for (int off = 4; off < 32; off <<= 1) mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, off));
+                if (mx > m) {
+                    const float c = ex2a(m - mx);  // m = -inf -> 0
+                    l *= c;
 #pragma unroll
-                for (int T = 0; T < 8; ++T) oF[T] *= c;
-                E *= c;
-                invE = __frcp_rn(E);
-                m = mx;
+                    for (int T = 0; T < 8; ++T) oF[T] *= c;
+                    E *= c;
+                    invE = rcpa(E);
+                    m = mx;
+                }
+                const float p0 = ex2a(x0 - m), p1 = ex2a(x1 - m);
+                l += p0 + p1;
+                z0 = v0 ? p0 * sv0 : 0.f, z1 = v1 ? p1 * sv1 : 0.f;
+                wf0 = z0 * invE, wf1 = z1 * invE;
+                since += kEPS;
+                need = !have || !(wf0 < kLim) || !(wf1 < kLim) || since > kEpochMax;
             }
-            const float p0 = ex2a(x0 - m), p1 = ex2a(x1 - m);
-            l += p0 + p1;
-            const float z0 = v0 ? p0 * sv0 : 0.f, z1 = v1 ? p1 * sv1 : 0.f;
-            float wf0 = z0 * invE, wf1 = z1 * invE;
-            const bool need = !have || !(wf0 < kLim) || !(wf1 < kLim);
-            if (__any_sync(kFull, need)) {
-                // new epoch (first stage, or a weight outgrew the headroom)
+            if (__any_sync(kFull, fin || need)) {
+                // fold the epoch; then (unless the item is done) a new epoch:
+                // first stage, a weight outgrew the headroom, or the x16
+                // accumulators near their s32 range
                 if (have) fold();
+                if (fin) break;
+                since = kEPS;
                 float zm = fmaxf(z0, z1);
 #pragma unroll
                 for (int off = 4; off < 32; off <<= 1) zm = fmaxf(zm, __shfl_xor_sync(kFull, zm, off));
@@ -390,44 +419,47 @@ __global__ void __launch_bounds__(17 * 32, 1) k_attend_i4tc(Dims D, State S, I4P
                 pb1 = g < 4 ? 0u : pk;
             }
             // ---------------- p.v: 8 MMAs (16 d rows each, both heads) ----------------
-            // lane (g, t) transposes V words g and g + 8 (d 8g.., 64 + 8g..) of
-            // entries t + 4i for both heads: x[grp][k] = byte k of the 4 entries
-            uint32_t xr[4][4];
+            // lane (g, t) transposes V word g (wh = 0: d 8g..) and g + 8 (wh = 1:
+            // d 64 + 8g..) of entries t + 4i for both heads: x[hh][k] = byte k of
+            // the 4 entries (nibbles d 2k, 2k + 1 of the word)
 #pragma unroll
-            for (int grp = 0; grp < 4; ++grp) {
-                const int hh = grp < 2 ? h0 : h1;
-                const uint8_t* vb = sb + (size_t)t * P.stride + pay + hh * 64 + 4 * (g + ((grp & 1) ? 8 : 0));
-                const uint32_t w_0 = *(const uint32_t*)(vb);
-                const uint32_t w_1 = *(const uint32_t*)(vb + 4 * P.stride);
-                const uint32_t w_2 = *(const uint32_t*)(vb + 8 * P.stride);
-                const uint32_t w_3 = *(const uint32_t*)(vb + 12 * P.stride);
-                const uint32_t u01l = __byte_perm(w_0, w_1, 0x5140), u01h = __byte_perm(w_0, w_1, 0x7362);
-                const uint32_t u23l = __byte_perm(w_2, w_3, 0x5140), u23h = __byte_perm(w_2, w_3, 0x7362);
-                xr[grp][0] = __byte_perm(u01l, u23l, 0x5410);
-                xr[grp][1] = __byte_perm(u01l, u23l, 0x7632);
-                xr[grp][2] = __byte_perm(u01h, u23h, 0x5410);
-                xr[grp][3] = __byte_perm(u01h, u23h, 0x7632);
-            }
+            for (int wh = 0; wh < 2; ++wh) {
+                uint32_t xr[2][4];
 #pragma unroll
-            for (int T = 0; T < 8; ++T) {
-                const int k = T >> 1;
-                if (T & 1)
-                    imma_u8u8(acc[T], nib_hi(xr[0][k]), nib_hi(xr[1][k]), nib_hi(xr[2][k]), nib_hi(xr[3][k]), pb0, pb1);
-                else
-                    imma_u8u8(acc[T], nib_lo(xr[0][k]), nib_lo(xr[1][k]), nib_lo(xr[2][k]), nib_lo(xr[3][k]), pb0, pb1);
+                for (int hh = 0; hh < 2; ++hh) {
+                    const uint8_t* vb = sb + (size_t)t * P.stride + pay + (hh ? h1 : h0) * 64 + 4 * (g + 8 * wh);
+                    const uint32_t w_0 = *(const uint32_t*)(vb);
+                    const uint32_t w_1 = *(const uint32_t*)(vb + 4 * P.stride);
+                    const uint32_t w_2 = *(const uint32_t*)(vb + 8 * P.stride);
+                    const uint32_t w_3 = *(const uint32_t*)(vb + 12 * P.stride);
+                    const uint32_t u01l = __byte_perm(w_0, w_1, 0x5140), u01h = __byte_perm(w_0, w_1, 0x7362);
+                    const uint32_t u23l = __byte_perm(w_2, w_3, 0x5140), u23h = __byte_perm(w_2, w_3, 0x7362);
+                    xr[hh][0] = __byte_perm(u01l, u23l, 0x5410);
+                    xr[hh][1] = __byte_perm(u01l, u23l, 0x7632);
+                    xr[hh][2] = __byte_perm(u01h, u23h, 0x5410);
+                    xr[hh][3] = __byte_perm(u01h, u23h, 0x7632);
+                }
+                // tile T: rows g = d 8g + T (byte T/2), g + 8 = d 8g + T + 4 (byte T/2 + 2)
+                imma_u8u8(acc[4 * wh + 0], nlo(xr[0][0], c88, c0f), nlo(xr[0][2], c88, c0f), nlo(xr[1][0], c88, c0f),
+                          nlo(xr[1][2], c88, c0f), pb0, pb1);
+                imma_u8u8(acc[4 * wh + 1], nhi(xr[0][0], c88, c0f), nhi(xr[0][2], c88, c0f), nhi(xr[1][0], c88, c0f),
+                          nhi(xr[1][2], c88, c0f), pb0, pb1);
+                imma_u8u8(acc[4 * wh + 2], nlo(xr[0][1], c88, c0f), nlo(xr[0][3], c88, c0f), nlo(xr[1][1], c88, c0f),
+                          nlo(xr[1][3], c88, c0f), pb0, pb1);
+                imma_u8u8(acc[4 * wh + 3], nhi(xr[0][1], c88, c0f), nhi(xr[0][3], c88, c0f), nhi(xr[1][1], c88, c0f),
+                          nhi(xr[1][3], c88, c0f), pb0, pb1);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stage]);
             if (++stage == P.NST) stage = 0, phase ^= 1;
         }
         // ---- the item's partial (m, l, o) of heads h0, h1 ----
-        if (have) fold();
 #pragma unroll
         for (int off = 4; off < 32; off <<= 1) l += __shfl_xor_sync(kFull, l, off);
-        // lanes t even write d 8g.. (row g), t odd d 64 + 8g.. (row g + 8)
-        float4* po = (float4*)(S.part_o + ((int64_t)w * H + hm) * 128 + (odd ? 64 : 0) + 8 * g);
-        po[0] = make_float4(oF[0], oF[1], oF[2], oF[3]);
-        po[1] = make_float4(oF[4], oF[5], oF[6], oF[7]);
+        // tile 4 wh + T, T = 0..3: d 64 wh + 8g + T (+ 4 for t odd)
+        float* po = S.part_o + ((int64_t)w * H + hm) * 128 + 8 * g + (odd ? 4 : 0);
+        *(float4*)po = make_float4(oF[0], oF[1], oF[2], oF[3]);
+        *(float4*)(po + 64) = make_float4(oF[4], oF[5], oF[6], oF[7]);
         if (g == 0 && !odd) {
             S.part_m[(int64_t)w * H + hm] = m;
             S.part_l[(int64_t)w * H + hm] = l;
@@ -453,6 +485,8 @@ static I4Params i4_params(const Dims& D, size_t* smem) {
     int nst = budget / P.stage_bytes;
     P.NST = nst > 4 ? 4 : nst;
     P.scale2 = 1.4426950408889634f / sqrtf(128.f);
+    P.c88 = 0x88888888u;
+    P.c0f = 0x0F0F0F0Fu;
     const char* st = std::getenv("PIKV_ATT_STATIC");
     P.dyn = st && st[0] == '1' ? 0 : 1;
     if (smem) *smem = 256 + (size_t)q_area_bytes(D.H / 2) + (size_t)P.NST * P.stage_bytes;
