@@ -354,7 +354,10 @@ def run_group(args, w, name, cfg, n_micro, local, world=1, rank=0, dist_on=False
     attend_sms = args.attend_sms if args.attend_sms is not None else DEFAULT_ATTEND_SMS
     if attend_sms <= 0:  # the library default (pikv_group_create, attend_sms = 0)
         nsm = torch.cuda.get_device_properties(local).multi_processor_count
-        attend_sms = nsm - (12 if w["codec"] in ("Int8", "Int4") else 44)
+        # attention SMs vs SMs left to the other micro-batch's control kernels
+        # (profiles/scripts/r02_sms_sweep.sh: int4's tensor-core kernel is fast
+        # enough that the control tail needs more SMs than int8's)
+        attend_sms = nsm - {"Int8": 12, "Int4": 24}.get(w["codec"], 44)
     grp = EngineGroup(cfg, n_micro=n_micro, attend_sms=attend_sms, device=local)
     B, d, dp, Bm = cfg.batch, cfg.model.d, cfg.stored_width, grp.Bm
     if cfg.compressor.scheme in ("LowRank",):

@@ -157,7 +157,7 @@ def test_fullsize_group(name):
     cfg.pool_entries = B * (k_top * L + 4096 + 2 * w["E"] * 16)
     lowrank = cfg.compressor.scheme == "LowRank"
     nsm = torch.cuda.get_device_properties(0).multi_processor_count
-    attend_sms = nsm - (12 if w["codec"] in ("Int8", "Int4") else 44)
+    attend_sms = nsm - {"Int8": 12, "Int4": 24}.get(w["codec"], 44)  # as bench.py
     grp = EngineGroup(cfg, n_micro=2, attend_sms=attend_sms)
     basis = None
     if lowrank:  # bench.py's basis
