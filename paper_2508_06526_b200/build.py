@@ -14,7 +14,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpikv_b200.so")
-SOURCES = ["capi.cu", "engine_kernels.cu", "attend.cu", "attend_i4tc.cu", "ops.cu", "bulk_tc.cu", "components.cu"]
+SOURCES = ["capi.cu", "engine_kernels.cu", "attend.cu", "attend_i4tc.cu", "attend_bf16tc.cu", "ops.cu", "bulk_tc.cu", "components.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

@@ -667,6 +667,8 @@ void launch_dec(const Dims& D, const State& S, const Plan& pl, cudaStream_t st) 
 const char* attend_check(const Dims& D) {
     if (attend_i4tc_applies(D))
         return attend_i4tc_stages(D) < 2 ? "KV entry too large for the shared-memory ring" : nullptr;
+    if (attend_bf16tc_applies(D))
+        return attend_bf16tc_stages(D) < 2 ? "KV entry too large for the shared-memory ring" : nullptr;
     Plan pl = make_plan(D);
     int elem_x2 = D.codec == PIKV_CODEC_INT8 ? 2 : D.codec == PIKV_CODEC_INT4 ? 1
                                                  : (D.kv_dtype == PIKV_DTYPE_BF16 ? 4 : 8);
@@ -684,16 +686,22 @@ int attend_max_smem() { return kSmemBudget; }
 // entries per ring stage of the attention plan (work items are sized in
 // multiples of it so no item ends in a partly filled stage)
 int attend_entries_per_stage(const Dims& D) {
-    return attend_i4tc_applies(D) ? attend_i4tc_eps() : make_plan(D).P.EPS;
+    if (attend_i4tc_applies(D)) return attend_i4tc_eps();
+    if (attend_bf16tc_applies(D)) return attend_bf16tc_eps();
+    return make_plan(D).P.EPS;
 }
 
-// resident attention CTAs per SM: one 544-thread CTA for the tensor-core
-// int4 kernel, two 288-thread CTAs otherwise
-int attend_ctas_per_sm(const Dims& D) { return attend_i4tc_applies(D) ? 1 : 2; }
+// resident attention CTAs per SM: one CTA of up to 544 threads for the
+// tensor-core kernels, two 288-thread CTAs otherwise
+int attend_ctas_per_sm(const Dims& D) { return attend_i4tc_applies(D) || attend_bf16tc_applies(D) ? 1 : 2; }
 
 void launch_attend(const Dims& D, const State& S, cudaStream_t st) {
     if (attend_i4tc_applies(D)) {
         launch_attend_i4tc(D, S, st);
+        return;
+    }
+    if (attend_bf16tc_applies(D)) {
+        launch_attend_bf16tc(D, S, st);
         return;
     }
     Plan pl = make_plan(D);

@@ -37,15 +37,14 @@
 
 #include <cstdlib>
 
-#include "pikv_dev.cuh"
+#include "attend_ring.cuh"
 
 namespace pikv_dev {
 
 namespace {
 
-constexpr int kEPS = 16;           // entries per stage = MMA rows / k-slots per head
+constexpr int kEPS = kRingEPS;     // entries per stage = MMA rows / k-slots per head
 constexpr int kPad = 32;           // smem entry stride = entry_bytes + kPad
-constexpr int kNQ = 4;             // work-item queue depth
 constexpr int kTau = 5;            // epoch headroom bits
 constexpr float kLim = 16777215.f;  // weights must round to < 2^24 (three u8 digits)
 constexpr int kEpochMax = 32768;    // entries per epoch: 255 * 240 * n < 2^31
@@ -57,10 +56,7 @@ constexpr int kQWords = 2 * 3 * kQPlane;
 __host__ __device__ constexpr int q_area_bytes(int ncw) { return ((ncw * kQWords + 8) * 4 + 127) / 128 * 128; }
 
 struct I4Params {
-    int NST;          // ring stages
-    int stride;       // smem bytes per entry slot
-    int stage_bytes;  // kEPS * stride
-    int dyn;          // work items from the global ticket (1) or strided (0)
+    RingParams R;
     float scale2;     // log2(e) / sqrt(128)
     uint32_t c88, c0f;  // nibble masks (kernel parameters, so they stay in registers)
 };
@@ -106,11 +102,7 @@ __device__ __forceinline__ float rcpa(float x) {
 __global__ void __launch_bounds__(17 * 32, 1) k_attend_i4tc(Dims D, State S, I4Params P) {
     griddep_enter();
     extern __shared__ __align__(128) uint8_t smem[];
-    uint64_t* full = (uint64_t*)smem;  // [0, 4) stage ring
-    uint64_t* empty = full + 4;        // [4, 8)
-    uint64_t* ifull = full + 8;        // [8, 12) work-item queue
-    uint64_t* iempty = full + 12;      // [12, 16)
-    int* iq = (int*)(full + 16);
+    const RingSmem R = ring_smem(smem);
     const int H = D.H;
     const int ncw = H / 2;  // consumer warps
     // per consumer warp: its q digit planes in B-fragment order (kQWords),
@@ -120,84 +112,12 @@ __global__ void __launch_bounds__(17 * 32, 1) k_attend_i4tc(Dims D, State S, I4P
     uint8_t* stages = smem + 256 + q_area_bytes(ncw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid < 8) qsm[ncw * kQWords + tid] = 0u;
-    if (tid == 0) {
-        for (int i = 0; i < P.NST; ++i) {
-            mbar_init(&full[i], 1);
-            mbar_init(&empty[i], ncw);
-        }
-        for (int i = 0; i < kNQ; ++i) {
-            mbar_init(&ifull[i], 1);
-            mbar_init(&iempty[i], ncw);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
+    if (tid == 0) ring_init(R, P.R, ncw);
     __syncthreads();
     const int n_items = S.n_items[0];
-    const int eb = D.entry_bytes, pay = D.payload_bytes;
-
+    const int pay = D.payload_bytes;
     if (warp == ncw) {
-        // ================= producer warp (as k_attend) =================
-        const uint64_t pol = evict_first_policy();
-        int stage = 0;
-        uint32_t phase = 0;
-        auto item_of = [&](int w, int64_t& pos, int& cnt) {
-            if (w < n_items) {
-                pos = (int64_t)S.item_stream[w] * D.att_stride + S.item_begin[w];
-                cnt = S.item_end[w] - S.item_begin[w];
-            } else {
-                pos = 0, cnt = 0;
-            }
-        };
-        auto next_item = [&](int prev) -> int {
-            if (!P.dyn) return prev < 0 ? (int)blockIdx.x : prev + (int)gridDim.x;
-            int w = 0;
-            if (lane == 0) w = atomicAdd(&S.n_items[1], 1);
-            return __shfl_sync(kFull, w, 0);
-        };
-        int kq = 0;
-        auto publish = [&](int w) {
-            if (lane == 0) {
-                mbar_wait_sleep(&iempty[kq % kNQ], ((kq / kNQ) & 1) ^ 1);
-                *(volatile int*)&iq[kq % kNQ] = w;
-                mbar_arrive(&ifull[kq % kNQ]);
-            }
-            ++kq;
-        };
-        int64_t npos;
-        int ncnt;
-        int w = next_item(-1);
-        item_of(w, npos, ncnt);
-        int32_t nwin = lane < ncnt ? S.att_entry[npos + lane] : 0;
-        for (;;) {
-            publish(w);
-            if (w >= n_items) break;
-            const int64_t pos0 = npos;
-            const int cnt = ncnt;
-            auto win_load = [&](int w0) { return w0 + lane < cnt ? S.att_entry[pos0 + w0 + lane] : 0; };
-            int win = 0;
-            int32_t cur = nwin, nxt = win_load(32);
-            const int wn = next_item(w);
-            item_of(wn, npos, ncnt);
-            nwin = lane < ncnt ? S.att_entry[npos + lane] : 0;
-            for (int b = 0; b < cnt; b += kEPS) {
-                const int n = min(kEPS, cnt - b);
-                while (b >= win + 32) win += 32, cur = nxt, nxt = win_load(win + 32);
-                const int o = b - win + lane;
-                const int32_t e_cur = __shfl_sync(kFull, cur, o & 31);
-                const int32_t e_nxt = __shfl_sync(kFull, nxt, o & 31);
-                const int64_t ent = o < 32 ? e_cur : e_nxt;
-                if (lane == 0) {
-                    mbar_wait_sleep(&empty[stage], phase ^ 1);
-                    mbar_expect_tx(&full[stage], (uint32_t)(n * eb));
-                }
-                __syncwarp();
-                if (lane < n)
-                    bulk_g2s(stages + (size_t)stage * P.stage_bytes + (size_t)lane * P.stride,
-                             S.pool + ent * (int64_t)eb, (uint32_t)eb, &full[stage], pol);
-                if (++stage == P.NST) stage = 0, phase ^= 1;
-            }
-            w = wn;
-        }
+        ring_produce(D, S, P.R, R, stages, n_items, lane);
         return;
     }
     if (warp > ncw) return;
@@ -213,10 +133,7 @@ __global__ void __launch_bounds__(17 * 32, 1) k_attend_i4tc(Dims D, State S, I4P
     int stage = 0;
     uint32_t phase = 0;
     for (int kq = 0;; ++kq) {
-        mbar_wait_sleep(&ifull[kq % kNQ], (kq / kNQ) & 1);
-        const int w = *(volatile int*)&iq[kq % kNQ];
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&iempty[kq % kNQ]);
+        const int w = ring_next_item(R, kq, lane);
         if (w >= n_items) break;
         const int s = S.item_stream[w];
         const int64_t pos0 = (int64_t)s * D.att_stride + S.item_begin[w];
@@ -323,14 +240,14 @@ __global__ void __launch_bounds__(17 * 32, 1) k_attend_i4tc(Dims D, State S, I4P
         // fold is inlined once
         for (int b = 0;; b += kEPS, scp += kEPS * H) {
             const bool fin = b >= cnt;
-            const uint8_t* sb = stages + (size_t)stage * P.stage_bytes;
+            const uint8_t* sb = stages + (size_t)stage * P.R.stage_bytes;
             float z0 = 0.f, z1 = 0.f, wf0 = 0.f, wf1 = 0.f;
             bool need = false;
             if (!fin) {
                 const int n = min(kEPS, cnt - b);
-                mbar_wait_sleep(&full[stage], phase);
-                const uint8_t* r0 = sb + (size_t)(2 * g) * P.stride;  // entry 2g
-                const uint8_t* r1 = r0 + P.stride;                    // entry 2g + 1
+                mbar_wait_sleep(&R.full[stage], phase);
+                const uint8_t* r0 = sb + (size_t)(2 * g) * P.R.stride;  // entry 2g
+                const uint8_t* r1 = r0 + P.R.stride;                    // entry 2g + 1
                 // ---------------- q.k: 8 MMAs ----------------
                 // per head: K words 4t..4t+3 of entries 2g, 2g+1; low nibbles (even
                 // d) and high nibbles (odd d, x16) in separate MMAs and accumulators
@@ -427,11 +344,11 @@ __global__ void __launch_bounds__(17 * 32, 1) k_attend_i4tc(Dims D, State S, I4P
                 uint32_t xr[2][4];
 #pragma unroll
                 for (int hh = 0; hh < 2; ++hh) {
-                    const uint8_t* vb = sb + (size_t)t * P.stride + pay + (hh ? h1 : h0) * 64 + 4 * (g + 8 * wh);
+                    const uint8_t* vb = sb + (size_t)t * P.R.stride + pay + (hh ? h1 : h0) * 64 + 4 * (g + 8 * wh);
                     const uint32_t w_0 = *(const uint32_t*)(vb);
-                    const uint32_t w_1 = *(const uint32_t*)(vb + 4 * P.stride);
-                    const uint32_t w_2 = *(const uint32_t*)(vb + 8 * P.stride);
-                    const uint32_t w_3 = *(const uint32_t*)(vb + 12 * P.stride);
+                    const uint32_t w_1 = *(const uint32_t*)(vb + 4 * P.R.stride);
+                    const uint32_t w_2 = *(const uint32_t*)(vb + 8 * P.R.stride);
+                    const uint32_t w_3 = *(const uint32_t*)(vb + 12 * P.R.stride);
                     const uint32_t u01l = __byte_perm(w_0, w_1, 0x5140), u01h = __byte_perm(w_0, w_1, 0x7362);
                     const uint32_t u23l = __byte_perm(w_2, w_3, 0x5140), u23h = __byte_perm(w_2, w_3, 0x7362);
                     xr[hh][0] = __byte_perm(u01l, u23l, 0x5410);
@@ -450,8 +367,8 @@ __global__ void __launch_bounds__(17 * 32, 1) k_attend_i4tc(Dims D, State S, I4P
                           nhi(xr[1][3], c88, c0f), pb0, pb1);
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[stage]);
-            if (++stage == P.NST) stage = 0, phase ^= 1;
+            if (lane == 0) mbar_arrive(&R.empty[stage]);
+            if (++stage == P.R.NST) stage = 0, phase ^= 1;
         }
         // ---- the item's partial (m, l, o) of heads h0, h1 ----
 #pragma unroll
@@ -479,21 +396,16 @@ bool attend_i4tc_applies(const Dims& D) {
 
 static I4Params i4_params(const Dims& D, size_t* smem) {
     I4Params P{};
-    P.stride = D.entry_bytes + kPad;
-    P.stage_bytes = kEPS * P.stride;
-    const int budget = 227 * 1024 - 256 - q_area_bytes(D.H / 2);
-    int nst = budget / P.stage_bytes;
-    P.NST = nst > 4 ? 4 : nst;
+    P.R = ring_params(D, kEPS, kPad, q_area_bytes(D.H / 2));
+    if (P.R.NST > 4) P.R.NST = 4;
     P.scale2 = 1.4426950408889634f / sqrtf(128.f);
     P.c88 = 0x88888888u;
     P.c0f = 0x0F0F0F0Fu;
-    const char* st = std::getenv("PIKV_ATT_STATIC");
-    P.dyn = st && st[0] == '1' ? 0 : 1;
-    if (smem) *smem = 256 + (size_t)q_area_bytes(D.H / 2) + (size_t)P.NST * P.stage_bytes;
+    if (smem) *smem = 256 + (size_t)q_area_bytes(D.H / 2) + (size_t)P.R.NST * P.R.stage_bytes;
     return P;
 }
 
-int attend_i4tc_stages(const Dims& D) { return i4_params(D, nullptr).NST; }
+int attend_i4tc_stages(const Dims& D) { return i4_params(D, nullptr).R.NST; }
 int attend_i4tc_eps() { return kEPS; }
 
 void launch_attend_i4tc(const Dims& D, const State& S, cudaStream_t st) {

@@ -467,6 +467,10 @@ bool attend_i4tc_applies(const Dims& D);  // int4 / 128-dim heads: the tensor-co
 void launch_attend_i4tc(const Dims& D, const State& S, cudaStream_t st);
 int attend_i4tc_eps();
 int attend_i4tc_stages(const Dims& D);
+bool attend_bf16tc_applies(const Dims& D);  // 32-wide bf16 head slices: tensor cores (attend_bf16tc.cu)
+void launch_attend_bf16tc(const Dims& D, const State& S, cudaStream_t st);
+int attend_bf16tc_stages(const Dims& D);
+int attend_bf16tc_eps();
 void launch_combine(const Dims& D, const Cfg& C, const State& S, const ExchangeLayout& X, float* y,
                     int direct, int attended, cudaStream_t st);
 void launch_finish_merge(const Dims& D, const Cfg& C, const State& S, const ExchangeLayout& X,
