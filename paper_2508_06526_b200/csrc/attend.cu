@@ -145,6 +145,7 @@ struct AttParams {
     int stage_bytes;
     float scale2;     // log2(e) / sqrt(dph)
     int dyn;          // work items from the global ticket (1) or strided by CTA (0)
+    int merge;        // one bulk copy per run of pool-adjacent entries (PIKV_ATT_MERGE)
 };
 
 // Thread (sub, head, j) owns chunks j + i*LPH (i < CPT) of one head: the
@@ -258,13 +259,27 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
                     mbar_expect_tx(&full[stage], (uint32_t)(n * eb));
                 }
                 __syncwarp();
-                if (lane < n) {
+                // P.merge: entries adjacent in the pool (a page's run) go as one
+                // bulk copy from the run's first lane (the stage's slots are
+                // contiguous too)
+                int len = 1;
+                bool issue = lane < n;
+                if (P.merge) {
+                    const int64_t prev = __shfl_up_sync(0xffffffffu, ent, 1);
+                    const bool start = lane < n && (lane == 0 || ent != prev + 1);
+                    const uint32_t starts = __ballot_sync(0xffffffffu, start);
+                    const uint32_t later = starts & ~((2u << lane) - 1u);
+                    const int end = later ? __ffs(later) - 1 : n;
+                    len = (end < n ? end : n) - lane;
+                    issue = start;
+                }
+                if (issue) {
                     if (PIKV_ATTEND_NOHINT)
                         bulk_g2s_plain(stages + (size_t)stage * P.stage_bytes + (size_t)lane * eb,
-                                       S.pool + ent * (int64_t)eb, (uint32_t)eb, &full[stage]);
+                                       S.pool + ent * (int64_t)eb, (uint32_t)(len * eb), &full[stage]);
                     else
                         bulk_g2s(stages + (size_t)stage * P.stage_bytes + (size_t)lane * eb,
-                                 S.pool + ent * (int64_t)eb, (uint32_t)eb, &full[stage], pol);
+                                 S.pool + ent * (int64_t)eb, (uint32_t)(len * eb), &full[stage], pol);
                 }
                 if (++stage == P.NST) stage = 0, phase ^= 1;
             }
@@ -618,6 +633,8 @@ Plan make_plan(const Dims& D) {
     {
         const char* st = std::getenv("PIKV_ATT_STATIC");  // A/B experiments only
         pl.P.dyn = st && st[0] == '1' ? 0 : 1;
+        const char* mg = std::getenv("PIKV_ATT_MERGE");
+        pl.P.merge = mg && mg[0] == '1' ? 1 : 0;
     }
 
 
