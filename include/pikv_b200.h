@@ -528,6 +528,11 @@ int pikv_group_sync(pikv_group* grp);
  * (at most 8192 launches per micro-batch are kept between reads). */
 int pikv_group_set_timing(pikv_group* grp, int32_t on);
 int pikv_group_read_timing(pikv_group* grp, double* ms, int32_t* n);
+/* Debug probe (PIKV_GROUP_TIMELINE=1 when the group is created; device-pointer
+ * submits): rows of 6 doubles (micro-batch, control start, control end, cross-
+ * micro-batch wait satisfied, attention end, tail end) in ms relative to the
+ * first recorded submit; at most cap rows, clears the record. */
+int pikv_group_read_timeline(pikv_group* grp, double* out, int32_t cap, int32_t* n);
 
 #ifdef __cplusplus
 }

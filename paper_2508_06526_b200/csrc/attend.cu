@@ -216,6 +216,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
         // fewer items; P.dyn = 0 strides them statically (blockIdx + i*grid).
         auto next_item = [&](int prev) -> int {
             if (!P.dyn) return prev < 0 ? (int)blockIdx.x : prev + (int)gridDim.x;
+            if (D.att_share) {  // equal static shares: this CTA's items, then the sentinel
+                const int w = prev < 0 ? S.cta_first[blockIdx.x] : prev + 1;
+                return w < S.cta_first[blockIdx.x + 1] ? w : n_items;
+            }
             int w = 0;
             if (lane == 0) w = atomicAdd(&S.n_items[1], 1);
             return __shfl_sync(0xffffffffu, w, 0);
@@ -302,15 +306,24 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
     for (int i = 0; i < CPT; ++i) coff[i] = (head * P.CPH + j + i * LPH) * 16;
     int stage = 0;
     uint32_t phase = 0;
+    long long t_start = 0, n_ent = 0;  // PIKV_DEBUG_ATT
+    if (D.dbg_att && tid == 0) t_start = (long long)globaltimer();
     for (int kq = 0;; ++kq) {
         mbar_wait_sleep(&ifull[kq % NQ], (kq / NQ) & 1);
         const int w = *(volatile int*)&iq[kq % NQ];
         __syncwarp();
         if (lane == 0) mbar_arrive(&iempty[kq % NQ]);
-        if (w >= n_items) break;
+        if (w >= n_items) {
+            if (D.dbg_att && tid == 0) {
+                long long* d = S.dbg + 64 + 8 * D.B + 8 * blockIdx.x;
+                d[0] = t_start, d[1] = (long long)globaltimer(), d[2] = kq, d[3] = n_ent, d[4] = smid();
+            }
+            break;
+        }
         const int s = S.item_stream[w];
         const int64_t pos0 = (int64_t)s * D.att_stride + S.item_begin[w];
         const int cnt = S.item_end[w] - S.item_begin[w];
+        n_ent += cnt;
         f2 q[CPT][NP], o[CPT][NP];
         float m = -INFINITY, l = 0.f;
 #pragma unroll

@@ -74,6 +74,10 @@ __device__ __forceinline__ void ring_produce(const Dims& D, const State& S, cons
     };
     auto next_item = [&](int prev) -> int {
         if (!P.dyn) return prev < 0 ? (int)blockIdx.x : prev + (int)gridDim.x;
+        if (D.att_share) {  // equal static shares: this CTA's items, then the sentinel
+            const int w = prev < 0 ? S.cta_first[blockIdx.x] : prev + 1;
+            return w < S.cta_first[blockIdx.x + 1] ? w : n_items;
+        }
         int w = 0;
         if (lane == 0) w = atomicAdd(&S.n_items[1], 1);
         return __shfl_sync(kAll, w, 0);

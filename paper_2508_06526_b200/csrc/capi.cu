@@ -588,6 +588,12 @@ static int engine_create(const pikv_config* cfg, int32_t cuda_device, int attend
         D.items_per_cta = v ? std::max(1, std::atoi(v)) : items_per_cta;
         const char* dc = std::getenv("PIKV_DEBUG_CTL");
         D.dbg_ctl = dc && dc[0] == '1';
+        const char* da = std::getenv("PIKV_DEBUG_ATT");
+        D.dbg_att = da && da[0] == '1';
+        // attention work as equal static shares per CTA (default) or ticketed
+        // items (PIKV_ATT_SHARE=0, A/B): profiles/README.md "Round 2: balanced shares"
+        const char* sh = std::getenv("PIKV_ATT_SHARE");
+        D.att_share = !(sh && sh[0] == '0');
     }
     D.only_s = -1;  // scheduler kernels: all streams
     D.holes = 0;    // no arbitrary erase yet: page members are contiguous
@@ -713,6 +719,7 @@ static int engine_create(const pikv_config* cfg, int32_t cuda_device, int attend
     chk(S.item_end = eng->alloc<int32_t>(D.item_cap));
     chk(S.n_items = eng->alloc<int32_t>(2));  // [count, attention's dynamic item ticket]
     chk(S.item_first = eng->alloc<int32_t>(B + 1));
+    chk(S.cta_first = eng->alloc<int32_t>((size_t)D.attend_ctas + 1 + B + 1));  // + per-stream unit scratch
     chk(S.part_m = eng->alloc<float>((size_t)D.item_cap * D.H));
     chk(S.part_l = eng->alloc<float>((size_t)D.item_cap * D.H));
     chk(S.part_o = eng->alloc<float>((size_t)D.item_cap * D.H * D.dph));
@@ -720,7 +727,7 @@ static int engine_create(const pikv_config* cfg, int32_t cuda_device, int attend
     chk(S.gM = eng->alloc<float>((size_t)B * D.H));
     chk(S.gL = eng->alloc<float>((size_t)B * D.H));
     chk(S.summary = eng->alloc<pikv_step_summary>(B));
-    chk(S.dbg = eng->alloc<long long>(64 + 8 * (size_t)B));
+    chk(S.dbg = eng->alloc<long long>(64 + 8 * (size_t)B + 8 * (size_t)D.attend_ctas));
     chk(S.done_ctr = eng->alloc<unsigned>(1));
     chk(S.ctl_ctr = eng->alloc<unsigned>(4));
     const size_t in_elem = c.kv_dtype == PIKV_DTYPE_BF16 ? 2 : 4;
@@ -1009,7 +1016,12 @@ static int run_step(pikv_engine* eng, const void* q, const void* k, const void* 
         return fail(PIKV_ERR_INVALID_ARGUMENT,
                     "world_size > 1: attach NCCL (pikv_engine_attach_nccl) or use pikv_step_local / pikv_step_finish");
     cudaSetDevice(eng->device);
-    const bool use_graph = (eng->warmed_parts & parts) == parts && !eng->profiling;
+    static const bool att_eager = [] {  // A/B experiments only: attention part launched without a graph
+        const char* v = std::getenv("PIKV_ATT_EAGER");
+        return v && v[0] == '1';
+    }();
+    const bool use_graph = (eng->warmed_parts & parts) == parts && !eng->profiling &&
+                           !(att_eager && parts == kPartAttend);
     if (!use_graph) {
         rc = enqueue_step(eng, emb, q, k, v, sal, y, attend, parts);
         if (rc) return rc;
@@ -1720,7 +1732,8 @@ int64_t pikv_entry_bytes(pikv_engine* eng) { return eng->D.entry_bytes; }
 // Not part of the public header: debug timestamps written by kernels.
 int pikv_debug_read(pikv_engine* eng, long long* out, int n) {
     CUDA_TRY(cudaStreamSynchronize(eng->stream));
-    CUDA_TRY(cudaMemcpy(out, eng->S.dbg, sizeof(long long) * std::min(n, 64 + 8 * eng->D.B), cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(out, eng->S.dbg, sizeof(long long) * std::min(n, 64 + 8 * eng->D.B + 8 * eng->D.attend_ctas),
+                        cudaMemcpyDeviceToHost));
     return PIKV_OK;
 }
 int64_t pikv_kernel_launches(pikv_engine* eng) { return eng->launches; }
@@ -2255,6 +2268,15 @@ struct pikv_group {
     std::vector<std::vector<std::pair<cudaEvent_t, cudaEvent_t>>> tev;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tfree;
     size_t in_bytes = 0, y_bytes = 0, sal_elems = 0;  // per micro-batch
+    // timeline probe (PIKV_GROUP_TIMELINE=1 at create; pikv_group_read_timeline):
+    // per submit, events before / after the control graph, after the cross-
+    // micro-batch wait, after the attention graph, after the tail
+    bool timeline = false;
+    struct TL {
+        int m;
+        cudaEvent_t ev[5];
+    };
+    std::vector<TL> tl;
 };
 
 int pikv_group_create(const pikv_config* cfg, int32_t n_micro, int32_t attend_sms, int32_t cuda_device,
@@ -2319,6 +2341,7 @@ int pikv_group_create(const pikv_config* cfg, int32_t n_micro, int32_t attend_sm
     }
     cudaEventCreateWithFlags(&g->join, cudaEventDisableTiming);
     g->tev.resize(n_micro);
+    if (const char* tv = std::getenv("PIKV_GROUP_TIMELINE")) g->timeline = tv[0] == '1';
     const Dims& D = g->eng[0]->D;
     g->in_bytes = (size_t)D.B * D.d * (D.kv_dtype == PIKV_DTYPE_BF16 ? 2 : 4);
     g->y_bytes = sizeof(float) * (size_t)D.B * D.dp;
@@ -2339,6 +2362,8 @@ int pikv_group_destroy(pikv_group* g) {
         for (auto& p : v) cudaEventDestroy(p.first), cudaEventDestroy(p.second);
     for (auto& p : g->tfree) cudaEventDestroy(p.first), cudaEventDestroy(p.second);
     if (g->join) cudaEventDestroy(g->join);
+    for (auto& r : g->tl)
+        for (auto ev : r.ev) cudaEventDestroy(ev);
     delete g;
     return PIKV_OK;
 }
@@ -2347,6 +2372,14 @@ int pikv_group_size(pikv_group* g) { return g->n; }
 
 pikv_engine* pikv_group_engine(pikv_group* g, int32_t m) {
     return m >= 0 && m < g->n ? g->eng[m] : nullptr;
+}
+
+static thread_local cudaEvent_t* g_tl_rec = nullptr;
+static void Group_TL_begin(pikv_group* g, int m) {
+    pikv_group::TL r;
+    r.m = m;
+    for (auto& ev : r.ev) cudaEventCreate(&ev);
+    g->tl.push_back(r);
 }
 
 int pikv_group_submit(pikv_group* g, int32_t m, const void* q, const void* k, const void* v,
@@ -2381,10 +2414,18 @@ int pikv_group_submit(pikv_group* g, int32_t m, const void* q, const void* k, co
         // attention graph -> [record] -> tail graph; the ordering is stream
         // API calls between the graph launches.  (Attention on a separate
         // highest-priority stream measured slower: 37.5 vs 42.1 K tokens/s at c2.)
+        g_tl_rec = nullptr;
+        if (g->timeline && !host && g->tl.size() < 4096) {
+            Group_TL_begin(g, m);
+            g_tl_rec = g->tl.back().ev;
+            CUDA_TRY(cudaEventRecord(g_tl_rec[0], st));
+        }
         rc = run_step(e, dq, dk, dv, ds, dy, true, nullptr, kPartCtl);
+        if (g_tl_rec) CUDA_TRY(cudaEventRecord(g_tl_rec[1], st));
         if (!rc) {
             // (unordered attention launches measured: c2 43.8 vs 43.7 K, c5 145 vs 154 K)
             if (g->n > 1) CUDA_TRY(cudaStreamWaitEvent(st, g->att_done[(m + g->n - 1) % g->n], 0));
+            if (g_tl_rec) CUDA_TRY(cudaEventRecord(g_tl_rec[2], st));
             std::pair<cudaEvent_t, cudaEvent_t> p{nullptr, nullptr};
             if (g->timing && g->tev[m].size() < 8192) {  // bounded until pikv_group_read_timing
                 if (g->tfree.empty()) {
@@ -2400,9 +2441,11 @@ int pikv_group_submit(pikv_group* g, int32_t m, const void* q, const void* k, co
             rc = run_step(e, dq, dk, dv, ds, dy, true, nullptr, kPartAttend);
             if (p.second) CUDA_TRY(cudaEventRecord(p.second, st));
             CUDA_TRY(cudaEventRecord(g->att_done[m], st));
+            if (g_tl_rec) CUDA_TRY(cudaEventRecord(g_tl_rec[3], st));
         }
         if (!host) {
             if (!rc) rc = run_step(e, dq, dk, dv, ds, dy, true, nullptr, kPartTail);
+            if (!rc && g_tl_rec) CUDA_TRY(cudaEventRecord(g_tl_rec[4], st));
         } else if (e->exchange_path()) {
             // sharded over ranks: y is final after the all-gather and the
             // cross-rank merge, inside the fold part; the fold graph records
@@ -2509,6 +2552,31 @@ int pikv_group_read_timing(pikv_group* g, double* ms, int32_t* n) {
         v.clear();
     }
     if (ms) *ms = tot;
+    if (n) *n = cnt;
+    return PIKV_OK;
+}
+
+/* Debug probe: rows of (m, ctl_start, ctl_end, wait_done, attend_end, tail_end)
+ * in ms relative to the first recorded submit; clears the record. */
+int pikv_group_read_timeline(pikv_group* g, double* out, int32_t cap, int32_t* n) {
+    int cnt = 0;
+    if (!g->tl.empty()) {
+        CUDA_TRY(cudaEventSynchronize(g->tl.back().ev[4]));
+        for (auto& r : g->tl) {
+            if (cnt < cap) {
+                out[6 * cnt] = r.m;
+                for (int i = 0; i < 5; ++i) {
+                    float t = 0;
+                    CUDA_TRY(cudaEventElapsedTime(&t, g->tl[0].ev[0], r.ev[i]));
+                    out[6 * cnt + 1 + i] = t;
+                }
+                ++cnt;
+            }
+        }
+        for (auto& r : g->tl)
+            for (auto ev : r.ev) cudaEventDestroy(ev);
+        g->tl.clear();
+    }
     if (n) *n = cnt;
     return PIKV_OK;
 }

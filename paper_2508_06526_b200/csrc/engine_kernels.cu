@@ -1612,6 +1612,112 @@ __device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t* wsum, int
     return excl;
 }
 
+// The step's summary (StepResult counters) is complete before attention:
+// this rank's view, made global by k_finish_merge.
+__device__ __forceinline__ void write_summary(const Dims& D, const Cfg& C, const State& S, int s, int64_t n) {
+    int nev = S.n_ow[s], pb = 0, pa = 0, hits = 0;
+    for (int gl = 0; gl < D.Gl; ++gl) {
+        nev += S.n_ev[s * D.Gl + gl];
+        pb += S.pages_before[s * D.Gl + gl];
+        pa += S.pages_after[s * D.Gl + gl];
+    }
+    for (int j = 0; j < D.k; ++j) hits += S.found[(int64_t)s * D.k + j] > 0;
+    pikv_step_summary& sm = S.summary[s];
+    sm.step = S.now[s];
+    sm.inserts = D.k;
+    sm.lookups = D.k;
+    sm.hits = hits;
+    sm.n_attended = (int32_t)n;
+    const int hw = C.head_width < D.dp ? C.head_width : D.dp;  // pipeline.cpp:22-26, 262-264
+    sm.fetch_elements = (int64_t)n * (int64_t)(2 * hw + D.dp);
+    sm.n_evictions = nev;
+    sm.pages_before = pb;
+    sm.pages_after = pa;
+    sm.error = S.err[s];
+}
+
+// Equal static shares (D.att_share): every stream's list is cut into units of
+// one ring stage (att_eps entries, the last one partial), the units of all
+// streams are laid end to end (stream-major) and attention CTA c takes units
+// [floor(c U / Cn), floor((c + 1) U / Cn)) of the U in total.  A CTA's share
+// becomes one work item per stream it touches, so items stay stream-major
+// (item_first / k_combine unchanged), every CTA streams the same bytes (+-1
+// stage) and has no ticket round trips; cta_first[c] is CTA c's first item
+// (its items are cta_first[c] .. cta_first[c+1]-1).  Measured reason: with
+// ~2 ticketed items per CTA, CTAs that got one item idled for half the launch,
+// and a CTA's TMA ring streams at a fixed ~33 GB/s, so idle CTAs cost HBM
+// bandwidth (profiles/microbench/attend_ctas.py).
+__device__ __forceinline__ void build_items_shares(const Dims& D, const Cfg& C, const State& S, int64_t* wsum) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nt = blockDim.x, nw = nt >> 5;
+    const int64_t eps = D.att_eps > 0 ? D.att_eps : 1;
+    const int64_t Cg = D.attend_ctas;
+    // pass 1: units per stream -> U
+    int64_t U = 0;
+    for (int s0 = 0; s0 < D.B; s0 += nt) {
+        int64_t tot;
+        const int64_t n = s0 + tid < D.B ? (int64_t)S.att_cnt[s0 + tid] : 0;
+        block_excl_scan((n + eps - 1) / eps, wsum, &tot);
+        U += tot;
+    }
+    // Cn = min(CTAs, U) CTAs get shares (each >= 1 unit); the rest none.
+    // CTA of unit u: the largest c with floor(c U / Cn) <= u
+    const int64_t Cn = U < Cg ? U : Cg;
+    auto cta_of = [&](int64_t u) { return ((u + 1) * Cn + U - 1) / U - 1; };
+    // pass 2: items per stream (the CTAs its units span), item_first, summary
+    int64_t carry = 0, ucarry = 0;
+    for (int s0 = 0; s0 < D.B; s0 += nt) {
+        const int s = s0 + tid;
+        const int64_t n = s < D.B ? S.att_cnt[s] : 0;
+        const int64_t us = (n + eps - 1) / eps;
+        int64_t utot, tot;
+        const int64_t a = block_excl_scan(us, wsum, &utot) + ucarry;
+        const int64_t ni = us > 0 ? cta_of(a + us - 1) - cta_of(a) + 1 : 0;
+        const int64_t first = block_excl_scan(ni, wsum, &tot) + carry;
+        if (s < D.B) {
+            S.item_first[s] = (int32_t)first;
+            S.cta_first[Cg + 1 + s] = (int32_t)a;  // scratch: the stream's first unit
+            write_summary(D, C, S, s, n);
+        }
+        carry += tot;
+        ucarry += utot;
+    }
+    if (tid == 0) {
+        S.item_first[D.B] = (int32_t)carry;
+        S.n_items[0] = (int32_t)carry;
+        S.n_items[1] = 0;
+    }
+    for (int64_t c = Cn + tid; c <= Cg; c += nt) S.cta_first[c] = (int32_t)carry;  // no share
+    if (U == 0) {
+        __syncthreads();
+        return;
+    }
+    __syncthreads();
+    // pass 3 (warp per stream): its items, and cta_first of the CTAs whose
+    // share starts inside it (an empty share points at the next CTA's item)
+    for (int s = warp; s < D.B; s += nw) {
+        const int64_t n = S.att_cnt[s];
+        const int64_t us = (n + eps - 1) / eps;
+        const int64_t a = S.cta_first[Cg + 1 + s], b = a + us;
+        const int64_t f = S.item_first[s];
+        if (us == 0) continue;
+        const int64_t clo = cta_of(a), chi = cta_of(b - 1);
+        for (int64_t c = clo + lane; c <= chi; c += 32) {
+            const int64_t ulo = max(c * U / Cn, a), uhi = min((c + 1) * U / Cn, b);
+            const int64_t w = f + (c - clo);
+            S.item_stream[w] = s;
+            S.item_begin[w] = (int32_t)((ulo - a) * eps);
+            S.item_end[w] = (int32_t)min((uhi - a) * eps, n);
+        }
+        // CTAs c with floor(c U / Cn) in [a, b): c in [ceil(a Cn / U), ceil(b Cn / U))
+        const int64_t o0 = (a * Cn + U - 1) / U, o1 = (b * Cn + U - 1) / U;
+        for (int64_t c = o0 + lane; c < o1 && c < Cn; c += 32) {
+            const int64_t u = c * U / Cn;
+            S.cta_first[c] = (int32_t)(f + (cta_of(u) - clo));
+        }
+    }
+    __syncthreads();
+}
+
 // Attention work items from the per-stream attended counts (att_cnt): a
 // stream's list is cut into items of C entries, C sized so the persistent
 // attention grid gets ~items_per_cta items per CTA.  One CTA, any block size.
@@ -1623,6 +1729,10 @@ __device__ __forceinline__ void build_items(const Dims& D, const Cfg& C, const S
         int64_t tot;
         block_excl_scan(s0 + tid < D.B ? (int64_t)S.att_cnt[s0 + tid] : 0, wsum, &tot);
         N += tot;
+    }
+    if (D.att_share) {
+        build_items_shares(D, C, S, wsum);
+        return;
     }
     // entries per item: the smallest cs (>= 16) whose item count fits the
     // persistent attention grid (items_per_cta per CTA).  Each stream rounds
@@ -1662,27 +1772,7 @@ __device__ __forceinline__ void build_items(const Dims& D, const Cfg& C, const S
         const int64_t first = block_excl_scan((n + cs - 1) / cs, wsum, &tot) + carry;
         if (s < D.B) {
             S.item_first[s] = (int32_t)first;
-            // the step's summary (StepResult counters) is complete before
-            // attention: this rank's view, made global by k_finish_merge
-            int nev = S.n_ow[s], pb = 0, pa = 0, hits = 0;
-            for (int gl = 0; gl < D.Gl; ++gl) {
-                nev += S.n_ev[s * D.Gl + gl];
-                pb += S.pages_before[s * D.Gl + gl];
-                pa += S.pages_after[s * D.Gl + gl];
-            }
-            for (int j = 0; j < D.k; ++j) hits += S.found[(int64_t)s * D.k + j] > 0;
-            pikv_step_summary& sm = S.summary[s];
-            sm.step = S.now[s];
-            sm.inserts = D.k;
-            sm.lookups = D.k;
-            sm.hits = hits;
-            sm.n_attended = (int32_t)n;
-            const int hw = C.head_width < D.dp ? C.head_width : D.dp;  // pipeline.cpp:22-26, 262-264
-            sm.fetch_elements = (int64_t)n * (int64_t)(2 * hw + D.dp);
-            sm.n_evictions = nev;
-            sm.pages_before = pb;
-            sm.pages_after = pa;
-            sm.error = S.err[s];
+            write_summary(D, C, S, s, n);
         }
         carry += tot;
     }

@@ -64,7 +64,9 @@ struct Dims {
     int q_f64;          // the step's q is fp64 (QueryEncoder output), not kv_dtype
     int ctl_cl, ctl_smem;  // k_control cluster size and dynamic smem (control_geometry)
     int att_eps;           // k_attend entries per ring stage (item sizes are multiples)
+    int att_share;         // work items as equal static shares per attention CTA (cta_first), not tickets
     int dbg_ctl;        // k_control phase timestamps into dbg[64 + 8 s + p] (PIKV_DEBUG_CTL=1)
+    int dbg_att;        // k_attend per-CTA (start, end, items, entries, smid) into dbg[64 + 8 B + 8 cta] (PIKV_DEBUG_ATT=1)
     int only_s;         // >= 0: the scheduler kernels evict this stream only (pikv_evict_host)
     int holes;          // an arbitrary KVStore::erase happened: page members are not a
                         // contiguous range, membership is checked per slot
@@ -170,6 +172,7 @@ struct State {
     int32_t* item_end;
     int32_t* n_items;       // [2]: item count, k_attend's dynamic item ticket
     int32_t* item_first;    // [B+1] first work item of each stream
+    int32_t* cta_first;     // [attend_ctas+1] first work item of each attention CTA (att_share)
     float* part_m;          // [item_cap][H]
     float* part_l;
     float* part_o;          // [item_cap][H][dph]
@@ -199,6 +202,16 @@ __device__ __forceinline__ bool ring_can_hold(int raw, int e, int n_tok, int n_e
     return lhs >= 0 && lhs < n_tok;
 }
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ int smid() {
+    int r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
+}
 __device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
 
