@@ -25,6 +25,7 @@
 #include <cstdlib>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "pikv_dev.cuh"
 
@@ -44,7 +45,8 @@ namespace {
 
 constexpr int kConsumers = 256;
 constexpr int kThreads = kConsumers + 32;
-constexpr int kSmemBudget = 110 * 1024;  // two CTAs per SM
+constexpr int kSmemBudget = 110 * 1024;   // two CTAs per SM
+constexpr int kSmemBudget3 = 74 * 1024;   // three CTAs per SM (bf16 heads, PIKV_ATT_CPS=3)
 
 __device__ __forceinline__ void consumer_bar() {
     asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
@@ -158,8 +160,9 @@ __device__ __forceinline__ float ex2(float x) {  // 2^x, x <= 0 (flushes to 0 be
 }
 
 // LPHC: lanes per head as a compile-time constant (0 = P.LPH at run time)
-template <class Dec, int CPT, int NB, int LPHC>
-__global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttParams P) {
+template <class Dec, int CPT, int NB, int LPHC, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_attend(Dims D, State S, AttParams P) {
+    const long long t_entry = D.dbg_att && threadIdx.x == 0 ? (long long)globaltimer() : 0;  // PIKV_DEBUG_ATT
     griddep_enter();
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr int N = Dec::N, NP = N / 2;
@@ -306,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
     for (int i = 0; i < CPT; ++i) coff[i] = (head * P.CPH + j + i * LPH) * 16;
     int stage = 0;
     uint32_t phase = 0;
-    long long t_start = 0, n_ent = 0;  // PIKV_DEBUG_ATT
+    long long t_start = 0, n_ent = 0, t_first = 0;  // PIKV_DEBUG_ATT
     if (D.dbg_att && tid == 0) t_start = (long long)globaltimer();
     for (int kq = 0;; ++kq) {
         mbar_wait_sleep(&ifull[kq % NQ], (kq / NQ) & 1);
@@ -317,6 +320,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
             if (D.dbg_att && tid == 0) {
                 long long* d = S.dbg + 64 + 8 * D.B + 8 * blockIdx.x;
                 d[0] = t_start, d[1] = (long long)globaltimer(), d[2] = kq, d[3] = n_ent, d[4] = smid();
+                d[5] = t_entry, d[6] = t_first;
             }
             break;
         }
@@ -420,6 +424,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
         for (int b = 0; b < cnt; b += P.EPS) {
             const int n = min(P.EPS, cnt - b);
             mbar_wait_sleep(&full[stage], phase);
+            if (D.dbg_att && tid == 0 && t_first == 0) t_first = (long long)globaltimer();
             const uint8_t* sb = stages + (size_t)stage * P.stage_bytes;
             float* scp = S.scores + (pos0 + b) * H + head;  // this stage's logits, entry e at scp[e * H]
             // warp-uniform trip count (sub-groups of a warp see different entries)
@@ -600,11 +605,23 @@ __global__ void __launch_bounds__(kThreads, 2) k_attend(Dims D, State S, AttPara
 struct Plan {
     AttParams P;
     int cpt;
+    int cps;  // CTAs per SM (2, or 3 with a two-stage ring)
     size_t smem;
 };
 
+// Three CTAs per SM (PIKV_ATT_CPS=3; 72 registers, two-stage ring of ~32 KiB
+// stages): bf16 / f32 heads only (the int8 / int4 consumers spill at 72).
+int cps_of(const Dims& D) {
+    if (D.codec == PIKV_CODEC_INT8 || D.codec == PIKV_CODEC_INT4 || D.kv_dtype != PIKV_DTYPE_BF16) return 2;
+    const char* v = std::getenv("PIKV_ATT_CPS");
+    return v && v[0] == '3' ? 3 : 2;
+}
+
 Plan make_plan(const Dims& D) {
     Plan pl{};
+    pl.cps = cps_of(D);
+    const int budget = pl.cps == 3 ? kSmemBudget3 : kSmemBudget;
+    const int min_st = pl.cps == 3 ? 2 : 3;
     int elem_bytes_x2 = 0;  // payload bytes per element * 2
     switch (D.codec) {
         case PIKV_CODEC_INT8: elem_bytes_x2 = 2; break;
@@ -628,19 +645,19 @@ Plan make_plan(const Dims& D) {
     // entries per stage: ~32 KiB, at least one per sub-group when possible,
     // and small enough that the ring keeps >= 3 stages in flight
     const size_t redb = pl.P.EP > 1 ? sizeof(float) * (size_t)pl.P.EP * D.H * (D.dph + 2) : 0;
-    const int ring_max = (int)((kSmemBudget - 256 - redb) / D.entry_bytes);  // entries that fit
+    const int ring_max = (int)((budget - 256 - redb) / D.entry_bytes);  // entries that fit
     // a stage holds whole consumer batches (EP sub-groups x NB entries): a
     // partly filled batch still decodes and dots its K chunks
     const int nb = (D.codec == PIKV_CODEC_INT8 || D.codec == PIKV_CODEC_INT4 || cpt == 1) ? 4 : 2;  // BatchOf::NB
     const int batch = std::max(1, pl.P.EP * nb);
     int eps = (32 * 1024) / D.entry_bytes;
     eps = std::max(eps, std::min(batch, 32));
-    if (eps % batch && (eps / batch + 1) * batch <= std::max(1, ring_max / 3)) eps = (eps / batch + 1) * batch;
-    eps = std::min(eps, std::max(1, ring_max / 3));
+    if (eps % batch && (eps / batch + 1) * batch <= std::max(1, ring_max / min_st)) eps = (eps / batch + 1) * batch;
+    eps = std::min(eps, std::max(1, ring_max / min_st));
     eps = eps < 1 ? 1 : (eps > 32 ? 32 : eps);
     pl.P.EPS = eps;
     pl.P.stage_bytes = eps * D.entry_bytes;
-    int nst = (int)((kSmemBudget - 256 - redb) / pl.P.stage_bytes);
+    int nst = (int)((budget - 256 - redb) / pl.P.stage_bytes);
     pl.P.NST = nst > 8 ? 8 : nst;
     pl.P.scale2 = 1.4426950408889634f / sqrtf((float)D.dph);
     {
@@ -664,7 +681,9 @@ template <int CPT> struct BatchOf<DecI4, CPT> { static constexpr int NB = 4; };
 
 template <class Dec, int CPT, int LPHC>
 void launch_t(const Dims& D, const State& S, const Plan& pl, cudaStream_t st) {
-    auto kern = k_attend<Dec, CPT, BatchOf<Dec, CPT>::NB, LPHC>;
+    auto kern = k_attend<Dec, CPT, BatchOf<Dec, CPT>::NB, LPHC, 2>;
+    if constexpr (std::is_same<Dec, DecBF16>::value)
+        if (pl.cps == 3) kern = k_attend<Dec, CPT, BatchOf<Dec, CPT>::NB, LPHC, 3>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
     launch_pdl(kern, dim3(D.attend_ctas), dim3(kThreads), pl.smem, st, D, S, pl.P);
 }
@@ -723,7 +742,9 @@ int attend_entries_per_stage(const Dims& D) {
 
 // resident attention CTAs per SM: one CTA of up to 544 threads for the
 // tensor-core kernels, two 288-thread CTAs otherwise
-int attend_ctas_per_sm(const Dims& D) { return attend_i4tc_applies(D) || attend_bf16tc_applies(D) ? 1 : 2; }
+int attend_ctas_per_sm(const Dims& D) {
+    return attend_i4tc_applies(D) || attend_bf16tc_applies(D) ? 1 : make_plan(D).cps;
+}
 
 void launch_attend(const Dims& D, const State& S, cudaStream_t st) {
     if (attend_i4tc_applies(D)) {

@@ -44,7 +44,7 @@ y = torch.empty(cfg.batch, cfg.stored_width, dtype=torch.float32, device="cuda")
 L = lib()
 L.pikv_debug_read.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_longlong), ctypes.c_int]
 e0 = grp.engines[0]
-ctas = 2 * sms  # two CTAs per SM for the CUDA-core kernel
+ctas = (3 if os.environ.get("PIKV_ATT_CPS") == "3" else 2) * sms  # CTAs per SM of the CUDA-core kernel
 nbuf = 64 + 8 * Bm + 8 * ctas
 buf = (ctypes.c_longlong * nbuf)()
 eb = e0.entry_bytes()
@@ -59,14 +59,17 @@ for i in range(args.steps):
     L.pikv_debug_read(e0.h, buf, nbuf)
     a = np.array(buf[64 + 8 * Bm:], dtype=np.int64).reshape(ctas, 8)
     t0, t1, items, ents, sm = a[:, 0], a[:, 1], a[:, 2], a[:, 3], a[:, 4]
-    base = t0.min()
+    te, tf = a[:, 5], a[:, 6]
+    base = te.min()
     start, end = (t0 - base) / 1e3, (t1 - base) / 1e3
     per_sm = np.bincount(sm, minlength=nsm)
     dur = end.max()
     gbs = ents.sum() * eb / (dur * 1e-6) / 1e9
     rate = ents * eb / np.maximum(end - start, 1e-3) / 1e3  # GB/s per CTA
     two = per_sm[sm] >= 2
-    res.append(dict(launch_us=dur, gbs=gbs, start_max=start.max(), end_min=end.min(),
+    res.append(dict(entry_max=((te - base) / 1e3).max(), setup_p50=np.percentile((t0 - te) / 1e3, 50),
+                    first_data_p50=np.percentile((tf - base) / 1e3, 50),
+                    first_data_max=((tf - base) / 1e3).max(), launch_us=dur, gbs=gbs, start_max=start.max(), end_min=end.min(),
                     end_p50=np.percentile(end, 50), items_min=items.min(), items_max=items.max(),
                     sms_used=int((per_sm > 0).sum()), sms_with_2=int((per_sm >= 2).sum()),
                     rate_alone=rate[~two].mean() if (~two).any() else 0.0,
