@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_attend(Dims D, State S, AttP
     for (int i = 0; i < CPT; ++i) coff[i] = (head * P.CPH + j + i * LPH) * 16;
     int stage = 0;
     uint32_t phase = 0;
-    long long t_start = 0, n_ent = 0, t_first = 0;  // PIKV_DEBUG_ATT
+    long long t_start = 0, n_ent = 0, t_first = 0, t_wait = 0;  // PIKV_DEBUG_ATT
     if (D.dbg_att && tid == 0) t_start = (long long)globaltimer();
     for (int kq = 0;; ++kq) {
         mbar_wait_sleep(&ifull[kq % NQ], (kq / NQ) & 1);
@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_attend(Dims D, State S, AttP
             if (D.dbg_att && tid == 0) {
                 long long* d = S.dbg + 64 + 8 * D.B + 8 * blockIdx.x;
                 d[0] = t_start, d[1] = (long long)globaltimer(), d[2] = kq, d[3] = n_ent, d[4] = smid();
-                d[5] = t_entry, d[6] = t_first;
+                d[5] = t_entry, d[6] = t_first, d[7] = t_wait;
             }
             break;
         }
@@ -423,8 +423,15 @@ __global__ void __launch_bounds__(kThreads, MINB) k_attend(Dims D, State S, AttP
         }
         for (int b = 0; b < cnt; b += P.EPS) {
             const int n = min(P.EPS, cnt - b);
-            mbar_wait_sleep(&full[stage], phase);
-            if (D.dbg_att && tid == 0 && t_first == 0) t_first = (long long)globaltimer();
+            if (D.dbg_att && tid == 0) {
+                const long long t0 = (long long)globaltimer();
+                mbar_wait_sleep(&full[stage], phase);
+                const long long t1 = (long long)globaltimer();
+                if (t_first == 0) t_first = t1;
+                else t_wait += t1 - t0;
+            } else {
+                mbar_wait_sleep(&full[stage], phase);
+            }
             const uint8_t* sb = stages + (size_t)stage * P.stage_bytes;
             float* scp = S.scores + (pos0 + b) * H + head;  // this stage's logits, entry e at scp[e * H]
             // warp-uniform trip count (sub-groups of a warp see different entries)
@@ -742,6 +749,17 @@ int attend_entries_per_stage(const Dims& D) {
 
 // resident attention CTAs per SM: one CTA of up to 544 threads for the
 // tensor-core kernels, two 288-thread CTAs otherwise
+// SMs the micro-batch pipeline leaves free of attention CTAs for the other
+// micro-batch's control plane (profiles/README.md sweeps): the int8 / int4
+// consumers need more issue slots per byte than the control tail, the HMMA
+// low-rank kernel sustains more per SM than the CUDA-core bf16 kernel.
+int attend_reserve_sms(const Dims& D) {
+    if (attend_i4tc_applies(D)) return 24;
+    if (attend_bf16tc_applies(D)) return 32;
+    if (D.codec == PIKV_CODEC_INT8 || D.codec == PIKV_CODEC_INT4) return 12;
+    return 44;
+}
+
 int attend_ctas_per_sm(const Dims& D) {
     return attend_i4tc_applies(D) || attend_bf16tc_applies(D) ? 1 : make_plan(D).cps;
 }

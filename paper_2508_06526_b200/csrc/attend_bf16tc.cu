@@ -22,7 +22,8 @@
 //    k-slots 8-15 / columns 4-6 (block-diagonal B).
 // Ring: attend_ring.cuh, 3 stages x 16 entries (PIKV_BF16TC_EPS=8: 7 x 8),
 // slot stride = entry + 16 B (ldmatrix's 8 row addresses fall in 8 different
-// 16-B bank groups).  Opt-in (PIKV_BF16TC=1), see attend_bf16tc_applies.
+// 16-B bank groups).  Default for these layouts (PIKV_BF16TC=0: the CUDA-core
+// kernel), see attend_bf16tc_applies.
 #include <cuda_runtime.h>
 
 #include <cstdlib>
@@ -86,6 +87,8 @@ __device__ __forceinline__ uint32_t pack_part(const Parts3& a, const Parts3& b, 
 // (q.k rows g + 8 repeat rows g; one p.v MMA per d tile; twice the stages)
 template <int EPS>
 __global__ void __launch_bounds__(17 * 32, 1) k_attend_bf16tc(Dims D, State S, BTcParams P) {
+    const long long t_entry = D.dbg_att && threadIdx.x == 0 ? (long long)globaltimer() : 0;  // PIKV_DEBUG_ATT
+    long long t_wait = 0, n_stage = 0, n_ent = 0;
     griddep_enter();
     extern __shared__ __align__(128) uint8_t smem[];
     const RingSmem R = ring_smem(smem);
@@ -127,10 +130,18 @@ __global__ void __launch_bounds__(17 * 32, 1) k_attend_bf16tc(Dims D, State S, B
     uint32_t phase = 0;
     for (int kq = 0;; ++kq) {
         const int w = ring_next_item(R, kq, lane);
-        if (w >= n_items) break;
+        if (w >= n_items) {
+            if (D.dbg_att && tid == 0) {
+                long long* d = S.dbg + 64 + 8 * D.B + 8 * blockIdx.x;
+                d[0] = t_entry, d[1] = (long long)globaltimer(), d[2] = kq, d[3] = n_ent, d[4] = smid();
+                d[5] = t_entry, d[6] = t_wait, d[7] = n_stage;
+            }
+            break;
+        }
         const int s = S.item_stream[w];
         const int64_t pos0 = (int64_t)s * D.att_stride + S.item_begin[w];
         const int cnt = S.item_end[w] - S.item_begin[w];
+        n_ent += cnt;
         // q.k B fragments: MMA i covers dims 8i..8i+7 of both heads; b0 = head
         // h0 dims 8i + 2t, +1 (k-slots 2t, 2t+1), b1 = head h1 (k-slots 8 + 2t)
         uint32_t qB[kDPH / 8][2];
@@ -154,7 +165,13 @@ __global__ void __launch_bounds__(17 * 32, 1) k_attend_bf16tc(Dims D, State S, B
 
         for (int b = 0; b < cnt; b += EPS, scp += EPS * H) {
             const int n = min(EPS, cnt - b);
-            mbar_wait_sleep(&R.full[stage], phase);
+            if (D.dbg_att && tid == 0) {
+                const long long t0 = (long long)globaltimer();
+                mbar_wait_sleep(&R.full[stage], phase);
+                t_wait += (long long)globaltimer() - t0, ++n_stage;
+            } else {
+                mbar_wait_sleep(&R.full[stage], phase);
+            }
             const uint8_t* sb = stages + (size_t)stage * P.R.stage_bytes;
             // ---------------- q.k ----------------
             float dq[4] = {0.f, 0.f, 0.f, 0.f};
@@ -251,16 +268,16 @@ __global__ void __launch_bounds__(17 * 32, 1) k_attend_bf16tc(Dims D, State S, B
 }  // namespace
 
 // bf16 stored head slices of width 32 (rank-32 projections or 32-dim heads),
-// even H <= 32, when PIKV_BF16TC=1.  Opt-in: at c4-lowrank it needs ~0.5x the
-// CUDA-core kernel's instructions per entry but sustains less HBM per SM with
-// one CTA per SM (0.206 vs 0.197 ms per launch on the default 104 attention
-// SMs; 0.184 vs 0.192 at 124; profiles/README.md), so the step is faster on
-// the CUDA-core kernel.
+// even H <= 32; default (PIKV_BF16TC=0 selects the CUDA-core kernel).  With
+// equal static work shares the HMMA kernel beats the CUDA-core one at
+// c4-lowrank: 73.6-74.4 K vs 71.1-73.3 K tokens/s, e2e 72-73 K vs 64-66 K
+// (three runs each), attention frac 0.87-0.89 on 116 SMs
+// (profiles/scripts/r02_lowrank_rep.sh, profiles/README.md).
 bool attend_bf16tc_applies(const Dims& D) {
     if (D.codec == PIKV_CODEC_INT8 || D.codec == PIKV_CODEC_INT4) return false;
     if (D.kv_dtype != PIKV_DTYPE_BF16 || D.dph != kDPH || D.H < 2 || D.H > 32 || (D.H & 1)) return false;
     const char* v = std::getenv("PIKV_BF16TC");  // read at engine creation and graph capture
-    return v && v[0] == '1';
+    return !(v && v[0] == '0');
 }
 
 static int btc_eps() {

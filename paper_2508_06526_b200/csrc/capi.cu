@@ -45,6 +45,7 @@ __global__ void k_lr_decode(const float*, const float*, const float*, int32_t, i
 const char* attend_check(const Dims& D);
 int attend_entries_per_stage(const Dims& D);
 int attend_ctas_per_sm(const Dims& D);
+int attend_reserve_sms(const Dims& D);
 }  // namespace pikv_dev
 
 namespace {
@@ -582,7 +583,11 @@ static int engine_create(const pikv_config* cfg, int32_t cuda_device, int attend
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device);
     if (const char* v = std::getenv("PIKV_ATTEND_SMS")) attend_sms = std::atoi(v);
-    D.attend_ctas = attend_ctas_per_sm(D) * (attend_sms > 0 ? std::min(attend_sms, sms) : sms);
+    // attend_sms > 0: that many SMs; 0: all; < 0: all but the pipeline's
+    // control-plane reserve for this layout (attend_reserve_sms)
+    const int use_sms = attend_sms > 0 ? std::min(attend_sms, sms)
+                        : attend_sms < 0 ? std::max(1, sms - attend_reserve_sms(D)) : sms;
+    D.attend_ctas = attend_ctas_per_sm(D) * use_sms;
     {
         const char* v = std::getenv("PIKV_ITEMS");
         D.items_per_cta = v ? std::max(1, std::atoi(v)) : items_per_cta;
@@ -590,10 +595,14 @@ static int engine_create(const pikv_config* cfg, int32_t cuda_device, int attend
         D.dbg_ctl = dc && dc[0] == '1';
         const char* da = std::getenv("PIKV_DEBUG_ATT");
         D.dbg_att = da && da[0] == '1';
-        // attention work as equal static shares per CTA (default) or ticketed
-        // items (PIKV_ATT_SHARE=0, A/B): profiles/README.md "Round 2: balanced shares"
+        // attention work as equal static shares per CTA or ticketed items
+        // (PIKV_ATT_SHARE=1 / 0 overrides).  Shares win where the attention
+        // CTAs start together (c2 44.1-44.4 vs 43.1-43.5 K tokens/s, c3, c4);
+        // with more than 16 streams per engine the other micro-batch's control
+        // kernels delay some CTAs' start and tickets let those run less (c5,
+        // 32 streams per micro-batch: 152-156 vs 151-153 K); profiles/README.md
         const char* sh = std::getenv("PIKV_ATT_SHARE");
-        D.att_share = !(sh && sh[0] == '0');
+        D.att_share = sh ? sh[0] != '0' : D.B <= 16;
     }
     D.only_s = -1;  // scheduler kernels: all streams
     D.holes = 0;    // no arbitrary erase yet: page members are contiguous
@@ -2294,18 +2303,11 @@ int pikv_group_create(const pikv_config* cfg, int32_t n_micro, int32_t attend_sm
     pikv_config c = *cfg;
     c.batch = cfg->batch / n_micro;
     if (cfg->pool_entries > 0) c.pool_entries = cfg->pool_entries / n_micro;
-    if (attend_sms <= 0 && n_micro > 1) {
-        // leave SMs to the control plane of the other micro-batch (sweeps in
-        // profiles/README.md): 44 for bf16/f32/low-rank attention (c2 flat at
-        // 44 K from 100 to 116 SMs, c3 42.7 K at 100 vs 39.9 K at 124,
-        // c4-low-rank 71.8 K at 104 vs 68.9 K at 120), 12 for int8/int4 whose
-        // attention needs more issue slots per byte (c4-int8 39.7 K at 136 vs
-        // 36.6 K at 148 and 37.7 K at 124; c4-int4 35.0 K at 136 vs 33.2 K at 148)
-        int sms = 148;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device);
-        const bool quant = cfg->codec == PIKV_CODEC_INT8 || cfg->codec == PIKV_CODEC_INT4;
-        attend_sms = std::max(1, sms - (quant ? 12 : 44));
-    }
+    // leave SMs to the control plane of the other micro-batch: all but
+    // attend_reserve_sms(layout) (sweeps in profiles/README.md: c2 flat at
+    // 44 K from 100 to 116 SMs, c4-int8 39.7 K at 136 vs 36.6 K at 148,
+    // c4-low-rank on the HMMA kernel 74 K at 116 vs 72.3 K at 124)
+    if (attend_sms <= 0 && n_micro > 1) attend_sms = -1;
     for (int m = 0; m < n_micro; ++m) {
         pikv_engine* e = nullptr;
         // 2 work items per attention CTA in the pipeline (c2: 1 -> 37.6 K,

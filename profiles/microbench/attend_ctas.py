@@ -44,7 +44,8 @@ y = torch.empty(cfg.batch, cfg.stored_width, dtype=torch.float32, device="cuda")
 L = lib()
 L.pikv_debug_read.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_longlong), ctypes.c_int]
 e0 = grp.engines[0]
-ctas = (3 if os.environ.get("PIKV_ATT_CPS") == "3" else 2) * sms  # CTAs per SM of the CUDA-core kernel
+tc = os.environ.get("PIKV_BF16TC") == "1"  # the HMMA kernel: one CTA per SM, wait ns in slot 6
+ctas = (1 if tc else 3 if os.environ.get("PIKV_ATT_CPS") == "3" else 2) * sms
 nbuf = 64 + 8 * Bm + 8 * ctas
 buf = (ctypes.c_longlong * nbuf)()
 eb = e0.entry_bytes()
@@ -60,6 +61,9 @@ for i in range(args.steps):
     a = np.array(buf[64 + 8 * Bm:], dtype=np.int64).reshape(ctas, 8)
     t0, t1, items, ents, sm = a[:, 0], a[:, 1], a[:, 2], a[:, 3], a[:, 4]
     te, tf = a[:, 5], a[:, 6]
+    wait = a[:, 6] if tc else a[:, 7]
+    if tc:
+        tf = te
     base = te.min()
     start, end = (t0 - base) / 1e3, (t1 - base) / 1e3
     per_sm = np.bincount(sm, minlength=nsm)
@@ -67,7 +71,7 @@ for i in range(args.steps):
     gbs = ents.sum() * eb / (dur * 1e-6) / 1e9
     rate = ents * eb / np.maximum(end - start, 1e-3) / 1e3  # GB/s per CTA
     two = per_sm[sm] >= 2
-    res.append(dict(entry_max=((te - base) / 1e3).max(), setup_p50=np.percentile((t0 - te) / 1e3, 50),
+    res.append(dict(wait_frac_p50=np.percentile(wait / np.maximum(t1 - t0, 1), 50), entry_max=((te - base) / 1e3).max(), setup_p50=np.percentile((t0 - te) / 1e3, 50),
                     first_data_p50=np.percentile((tf - base) / 1e3, 50),
                     first_data_max=((tf - base) / 1e3).max(), launch_us=dur, gbs=gbs, start_max=start.max(), end_min=end.min(),
                     end_p50=np.percentile(end, 50), items_min=items.min(), items_max=items.max(),
