@@ -600,9 +600,11 @@ static int engine_create(const pikv_config* cfg, int32_t cuda_device, int attend
         // CTAs start together (c2 44.1-44.4 vs 43.1-43.5 K tokens/s, c3, c4);
         // with more than 16 streams per engine the other micro-batch's control
         // kernels delay some CTAs' start and tickets let those run less (c5,
-        // 32 streams per micro-batch: 152-156 vs 151-153 K); profiles/README.md
+        // 32 streams per micro-batch: 152-156 vs 151-153 K); a single stream's
+        // latency-bound step builds ticketed items faster (c1: 70.2 vs 72.4 us);
+        // profiles/README.md
         const char* sh = std::getenv("PIKV_ATT_SHARE");
-        D.att_share = sh ? sh[0] != '0' : D.B <= 16;
+        D.att_share = sh ? sh[0] != '0' : D.B >= 2 && D.B <= 16;
     }
     D.only_s = -1;  // scheduler kernels: all streams
     D.holes = 0;    // no arbitrary erase yet: page members are contiguous

@@ -1659,9 +1659,12 @@ __device__ __forceinline__ void build_items_shares(const Dims& D, const Cfg& C, 
         block_excl_scan((n + eps - 1) / eps, wsum, &tot);
         U += tot;
     }
-    // Cn = min(CTAs, U) CTAs get shares (each >= 1 unit); the rest none.
+    // Cn CTAs get shares of >= mu units (>= 16 entries, as the ticketed items:
+    // small steps would otherwise spread over many one-stage partials that the
+    // merge then reads back); the rest none.
     // CTA of unit u: the largest c with floor(c U / Cn) <= u
-    const int64_t Cn = U < Cg ? U : Cg;
+    const int64_t mu = (16 + eps - 1) / eps;
+    const int64_t Cn = U / mu < Cg ? (U / mu > 0 ? U / mu : 1) : Cg;
     auto cta_of = [&](int64_t u) { return ((u + 1) * Cn + U - 1) / U - 1; };
     // pass 2: items per stream (the CTAs its units span), item_first, summary
     int64_t carry = 0, ucarry = 0;
