@@ -41,7 +41,21 @@ constexpr unsigned kAllB = 0xffffffffu;
 struct BTcParams {
     RingParams R;
     float scale2;  // log2(e) / sqrt(dph)
+    int early;     // release each stage once its fragments are in registers (PIKV_BF16TC_EARLY=1; default after the math)
 };
+
+// Scoreboard wait on every loaded fragment register (an empty asm that reads
+// them): the ldmatrix reads of the stage are complete before it is released.
+template <int A, int J, int T>
+__device__ __forceinline__ void regs_ready(const uint32_t (&ka)[A][4], const uint32_t (&va)[J][T][4]) {
+#pragma unroll
+    for (int i = 0; i < A; ++i) asm volatile("" ::"r"(ka[i][0]), "r"(ka[i][1]), "r"(ka[i][2]), "r"(ka[i][3]) : "memory");
+#pragma unroll
+    for (int j = 0; j < J; ++j)
+#pragma unroll
+        for (int t = 0; t < T; ++t)
+            asm volatile("" ::"r"(va[j][t][0]), "r"(va[j][t][1]), "r"(va[j][t][2]), "r"(va[j][t][3]) : "memory");
+}
 
 __device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -86,7 +100,7 @@ __device__ __forceinline__ uint32_t pack_part(const Parts3& a, const Parts3& b, 
 // EPS entries per ring stage: 16 (q.k rows g / g + 8, p.v two halves) or 8
 // (q.k rows g + 8 repeat rows g; one p.v MMA per d tile; twice the stages)
 template <int EPS>
-__global__ void __launch_bounds__(17 * 32, 1) k_attend_bf16tc(Dims D, State S, BTcParams P) {
+__global__ void __launch_bounds__(18 * 32, 1) k_attend_bf16tc(Dims D, State S, BTcParams P) {
     const long long t_entry = D.dbg_att && threadIdx.x == 0 ? (long long)globaltimer() : 0;  // PIKV_DEBUG_ATT
     long long t_wait = 0, n_stage = 0, n_ent = 0;
     griddep_enter();
@@ -100,11 +114,11 @@ __global__ void __launch_bounds__(17 * 32, 1) k_attend_bf16tc(Dims D, State S, B
     __syncthreads();
     const int n_items = S.n_items[0];
     const int pay = D.payload_bytes;
-    if (warp == ncw) {
-        ring_produce(D, S, P.R, R, stages, n_items, lane);
+    if (warp >= ncw) {  // producers: two with static shares (ring_produce)
+        const int nprod = P.R.nprod;
+        if (warp - ncw < nprod) ring_produce(D, S, P.R, R, stages, n_items, lane, warp - ncw, nprod);
         return;
     }
-    if (warp > ncw) return;
 
     // MMA fragment coordinates: g = lane / 4, t = lane % 4.  q.k tile rows g /
     // g + 8 = entries g / g + 8 of the stage; lanes t = 0, 1 hold head h0,
@@ -173,14 +187,27 @@ __global__ void __launch_bounds__(17 * 32, 1) k_attend_bf16tc(Dims D, State S, B
                 mbar_wait_sleep(&R.full[stage], phase);
             }
             const uint8_t* sb = stages + (size_t)stage * P.R.stage_bytes;
+            // The stage's K and V^T fragments go to registers first and the
+            // stage is released before any math: the ring slot is busy for the
+            // ldmatrix round trip only, not the whole q.k -> softmax -> p.v
+            // chain (consumers waited 26-33 % of the time for data with the
+            // release after the math: profiles/README.md)
+            uint32_t ka[kDPH / 8][4], va[EPS / 8][kDPH / 16][4];
+#pragma unroll
+            for (int i = 0; i < kDPH / 8; ++i) ldsm_x4(ka[i], sb + qk_off + 16 * i);
+#pragma unroll
+            for (int j = 0; j < EPS / 8; ++j)
+#pragma unroll
+                for (int T = 0; T < kDPH / 16; ++T) ldsm_x4_t(va[j][T], sb + pv_off + (8 * j) * P.R.stride + 32 * T);
+            if (P.early) {
+                regs_ready(ka, va);  // the loads have landed before the slot is handed back
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&R.empty[stage]);
+            }
             // ---------------- q.k ----------------
             float dq[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-            for (int i = 0; i < kDPH / 8; ++i) {
-                uint32_t a[4];
-                ldsm_x4(a, sb + qk_off + 16 * i);
-                hmma(dq, a, qB[i][0], qB[i][1]);
-            }
+            for (int i = 0; i < kDPH / 8; ++i) hmma(dq, ka[i], qB[i][0], qB[i][1]);
             // column 2t (+1): hi + mid (t even) or lo (t odd) of head hm
             float s0 = dq[0] + dq[1], s1 = dq[2] + dq[3];
             s0 += __shfl_xor_sync(kAllB, s0, 1);
@@ -227,8 +254,7 @@ __global__ void __launch_bounds__(17 * 32, 1) k_attend_bf16tc(Dims D, State S, B
                 const uint32_t b0 = pk & bm0, b1 = pk & ~bm0;
 #pragma unroll
                 for (int T = 0; T < kDPH / 16; ++T) {
-                    uint32_t a[4];
-                    ldsm_x4_t(a, sb + pv_off + (8 * j) * P.R.stride + 32 * T);
+                    uint32_t* a = va[j][T];
                     if (n < EPS) {
                         // a partly filled stage: the unused slots hold stale bytes
                         // (NaN patterns included) -- zero their V so 0 * NaN cannot
@@ -237,14 +263,16 @@ __global__ void __launch_bounds__(17 * 32, 1) k_attend_bf16tc(Dims D, State S, B
                                             (8 * j + 2 * t + 1 < n ? 0xFFFF0000u : 0u);
                         a[0] &= vm, a[1] &= vm, a[2] &= vm, a[3] &= vm;
                     }
-                    hmma(st[T], a, b0, b1);
+                    hmma(st[T], va[j][T], b0, b1);
                 }
             }
 #pragma unroll
             for (int T = 0; T < kDPH / 16; ++T)
                 acc[T][0] += st[T][0], acc[T][1] += st[T][1], acc[T][2] += st[T][2], acc[T][3] += st[T][3];
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&R.empty[stage]);
+            if (!P.early) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&R.empty[stage]);
+            }
             if (++stage == P.R.NST) stage = 0, phase ^= 1;
         }
         // ---- the item's partial (m, l, o) of heads h0, h1 ----
@@ -289,6 +317,10 @@ static BTcParams btc_params(const Dims& D, size_t* smem) {
     BTcParams P{};
     P.R = ring_params(D, btc_eps(), kPadB, 0);
     P.scale2 = 1.4426950408889634f / sqrtf((float)D.dph);
+    // release after the math (default: c4-lowrank 0.185 vs 0.190 ms per launch
+    // with the release right after the fragment loads, PIKV_BF16TC_EARLY=1)
+    const char* ea = std::getenv("PIKV_BF16TC_EARLY");  // A/B experiments only
+    P.early = ea && ea[0] == '1';
     if (smem) *smem = 256 + (size_t)P.R.NST * P.R.stage_bytes;
     return P;
 }
@@ -301,7 +333,7 @@ void launch_attend_bf16tc(const Dims& D, const State& S, cudaStream_t st) {
     const BTcParams P = btc_params(D, &smem);
     auto kern = P.R.eps == 16 ? k_attend_bf16tc<16> : k_attend_bf16tc<8>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    launch_pdl(kern, dim3(D.attend_ctas), dim3((D.H / 2 + 1) * 32), smem, st, D, S, P);
+    launch_pdl(kern, dim3(D.attend_ctas), dim3((D.H / 2 + P.R.nprod) * 32), smem, st, D, S, P);
 }
 
 }  // namespace pikv_dev

@@ -99,7 +99,7 @@ __device__ __forceinline__ float rcpa(float x) {
     return y;
 }
 
-__global__ void __launch_bounds__(17 * 32, 1) k_attend_i4tc(Dims D, State S, I4Params P) {
+__global__ void __launch_bounds__(18 * 32, 1) k_attend_i4tc(Dims D, State S, I4Params P) {
     griddep_enter();
     extern __shared__ __align__(128) uint8_t smem[];
     const RingSmem R = ring_smem(smem);
@@ -116,11 +116,11 @@ __global__ void __launch_bounds__(17 * 32, 1) k_attend_i4tc(Dims D, State S, I4P
     __syncthreads();
     const int n_items = S.n_items[0];
     const int pay = D.payload_bytes;
-    if (warp == ncw) {
-        ring_produce(D, S, P.R, R, stages, n_items, lane);
+    if (warp >= ncw) {  // producers: two with static shares (ring_produce)
+        const int nprod = P.R.nprod;
+        if (warp - ncw < nprod) ring_produce(D, S, P.R, R, stages, n_items, lane, warp - ncw, nprod);
         return;
     }
-    if (warp > ncw) return;
 
     // ================= consumer warps: heads h0, h1 =================
     // MMA fragment coordinates: g = lane / 4 (row / column group), t = lane % 4
@@ -412,7 +412,7 @@ void launch_attend_i4tc(const Dims& D, const State& S, cudaStream_t st) {
     size_t smem = 0;
     const I4Params P = i4_params(D, &smem);
     cudaFuncSetAttribute(k_attend_i4tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    launch_pdl(k_attend_i4tc, dim3(D.attend_ctas), dim3((D.H / 2 + 1) * 32), smem, st, D, S, P);
+    launch_pdl(k_attend_i4tc, dim3(D.attend_ctas), dim3((D.H / 2 + P.R.nprod) * 32), smem, st, D, S, P);
 }
 
 }  // namespace pikv_dev

@@ -26,6 +26,7 @@ struct RingParams {
     int stride;       // smem bytes per entry slot (entry_bytes + pad)
     int stage_bytes;  // eps * stride
     int dyn;          // work items from the global ticket (1) or strided by CTA (0)
+    int nprod;        // producer warps (ring_produce)
 };
 
 // smem header: barriers and the item queue (256 B at the start of the
@@ -57,12 +58,16 @@ __device__ __forceinline__ void ring_init(const RingSmem& R, const RingParams& P
 
 // The producer warp's whole life: items until the ticket runs out, then the
 // sentinel item (w >= n_items) that ends the consumers.
+// With static work shares (D.att_share) nprod producer warps split the stages
+// (producer `me` fills stages k = me mod nprod) and producer 0 alone publishes
+// the items: one warp's wait-expect-issue loop per stage limited a one-CTA ring
+// of 16-entry stages to ~6.1-6.6 TB/s (profiles/microbench/ring_sweep.cu).
 __device__ __forceinline__ void ring_produce(const Dims& D, const State& S, const RingParams& P, const RingSmem& R,
-                                             uint8_t* stages, int n_items, int lane) {
+                                             uint8_t* stages, int n_items, int lane, int me = 0, int nprod = 1) {
     constexpr unsigned kAll = 0xffffffffu;
     const int eb = D.entry_bytes;
     const uint64_t pol = evict_first_policy();
-    int stage = 0;
+    int stage = 0, ks = 0;
     uint32_t phase = 0;
     auto item_of = [&](int w, int64_t& pos, int& cnt) {
         if (w < n_items) {
@@ -84,7 +89,7 @@ __device__ __forceinline__ void ring_produce(const Dims& D, const State& S, cons
     };
     int kq = 0;
     auto publish = [&](int w) {
-        if (lane == 0) {
+        if (lane == 0 && me == 0) {
             mbar_wait_sleep(&R.iempty[kq % kRingNQ], ((kq / kRingNQ) & 1) ^ 1);
             *(volatile int*)&R.iq[kq % kRingNQ] = w;
             mbar_arrive(&R.ifull[kq % kRingNQ]);
@@ -117,14 +122,16 @@ __device__ __forceinline__ void ring_produce(const Dims& D, const State& S, cons
             const int32_t e_cur = __shfl_sync(kAll, cur, o & 31);
             const int32_t e_nxt = __shfl_sync(kAll, nxt, o & 31);
             const int64_t ent = o < 32 ? e_cur : e_nxt;
-            if (lane == 0) {
-                mbar_wait_sleep(&R.empty[stage], phase ^ 1);
-                mbar_expect_tx(&R.full[stage], (uint32_t)(n * eb));
+            if (ks++ % nprod == me) {
+                if (lane == 0) {
+                    mbar_wait_sleep(&R.empty[stage], phase ^ 1);
+                    mbar_expect_tx(&R.full[stage], (uint32_t)(n * eb));
+                }
+                __syncwarp();
+                if (lane < n)
+                    bulk_g2s(stages + (size_t)stage * P.stage_bytes + (size_t)lane * P.stride,
+                             S.pool + ent * (int64_t)eb, (uint32_t)eb, &R.full[stage], pol);
             }
-            __syncwarp();
-            if (lane < n)
-                bulk_g2s(stages + (size_t)stage * P.stage_bytes + (size_t)lane * P.stride, S.pool + ent * (int64_t)eb,
-                         (uint32_t)eb, &R.full[stage], pol);
             if (++stage == P.NST) stage = 0, phase ^= 1;
         }
         w = wn;
@@ -152,6 +159,10 @@ inline RingParams ring_params(const Dims& D, int eps, int pad, int extra) {
     P.NST = nst > kRingMaxStages ? kRingMaxStages : nst;
     const char* st = std::getenv("PIKV_ATT_STATIC");  // A/B experiments only
     P.dyn = st && st[0] == '1' ? 0 : 1;
+    // two producer warps when the work items are static shares (both walk the
+    // same items), one with ticketed items; PIKV_RING_PROD=1 forces one (A/B)
+    const char* rp = std::getenv("PIKV_RING_PROD");
+    P.nprod = D.att_share && !(rp && rp[0] == '1') ? 2 : 1;
     return P;
 }
 

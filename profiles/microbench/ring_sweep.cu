@@ -38,36 +38,42 @@ __device__ __forceinline__ void bulk(void* dst, const void* src, unsigned n, uin
         : "memory");
 }
 
-constexpr size_t kBlk = 16384;
 
-__global__ void __launch_bounds__(288) k_ring(const uint8_t* base, const int* perm, int nblk, int nst, int eps,
-                                              unsigned* out) {
+__global__ void __launch_bounds__(640) k_ring(const uint8_t* base, const int* perm, int nblk, int nst, int eps,
+                                              unsigned* out, int kBlk, int pad, int nthr, int nprod) {
     extern __shared__ __align__(128) uint8_t sm[];
     uint64_t* full = (uint64_t*)sm;
     uint64_t* empty = full + 16;
     uint8_t* st = sm + 256;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const size_t per = eps * kBlk;
+    const int ncw = nthr / 32 - nprod;  // consumer warps; the last nprod warps produce (stage i: warp ncw + i % nprod)
+    const size_t slot = kBlk + pad;
+    const size_t per = eps * slot;
     if (tid == 0) {
-        for (int i = 0; i < nst; ++i) mbar_init(&full[i], 1), mbar_init(&empty[i], 8);
+        for (int i = 0; i < nst; ++i) mbar_init(&full[i], 1), mbar_init(&empty[i], ncw);
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
     __syncthreads();
     const long long nstage = (long long)((nblk / eps + gridDim.x - 1 - blockIdx.x) / gridDim.x);
-    if (warp == 8) {
+    if (warp >= ncw) {
+        const int me = warp - ncw;
         uint64_t pol;
         asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
         int s = 0;
         unsigned ph = 0;
         for (long long p = 0; p < nstage; ++p) {
+            if (p % nprod != me) {
+                if (++s == nst) s = 0, ph ^= 1;
+                continue;
+            }
             if (lane == 0) {
                 mbar_wait(&empty[s], ph ^ 1);
-                mbar_expect_tx(&full[s], (unsigned)per);
+                mbar_expect_tx(&full[s], (unsigned)(eps * kBlk));
             }
             __syncwarp();
             const long long g = blockIdx.x + p * gridDim.x;
             if (lane < eps)
-                bulk(st + s * per + lane * kBlk, base + (size_t)perm[g * eps + lane] * kBlk, (unsigned)kBlk, &full[s],
+                bulk(st + s * per + lane * slot, base + (size_t)perm[g * eps + lane] * kBlk, (unsigned)kBlk, &full[s],
                      pol);
             if (++s == nst) s = 0, ph ^= 1;
         }
@@ -79,7 +85,7 @@ __global__ void __launch_bounds__(288) k_ring(const uint8_t* base, const int* pe
     for (long long p = 0; p < nstage; ++p) {
         mbar_wait(&full[s], ph);
         const uint4* v = (const uint4*)(st + s * per);
-        for (int i = tid; i < (int)(per / 16); i += 256) {
+        for (int i = tid; i < (int)(per / 16); i += ncw * 32) {
             const uint4 x = v[i];
             acc.x ^= x.x, acc.y ^= x.y, acc.z ^= x.z, acc.w ^= x.w;
         }
@@ -97,41 +103,44 @@ int main() {
     uint8_t* p;
     if (cudaMalloc(&p, bytes) != cudaSuccess) return 1;
     cudaMemset(p, 1, bytes);
-    const int nblk_all = (int)(bytes / kBlk), nblk = (int)((2ull << 30) / kBlk);
-    std::vector<int> perm(nblk_all);
-    for (int i = 0; i < nblk_all; ++i) perm[i] = i;
-    std::shuffle(perm.begin(), perm.end(), std::mt19937(1));
-    int* dperm;
-    cudaMalloc(&dperm, sizeof(int) * nblk);
-    cudaMemcpy(dperm, perm.data(), sizeof(int) * nblk, cudaMemcpyHostToDevice);
     cudaFuncSetAttribute(k_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     struct G {
-        int cps, nst, eps;
+        int blk, cps, nst, eps, pad, nthr, nprod;
     };
-    const G geos[] = {{2, 3, 2}, {2, 6, 1}, {1, 6, 2}, {1, 13, 1}, {1, 3, 4}, {3, 4, 1}, {3, 2, 2}, {4, 3, 1}};
-    for (int sms : {104, 116, 124, 136, 148}) {
+    // 16 KB entries (c2) and 4 KB entries (rank-32 low-rank: the HMMA kernel's
+    // 1 CTA x 3 stages x 16 entries with a 16-byte slot pad, 16 consumer warps)
+    const G geos[] = {{16384, 2, 3, 2, 0, 288, 1},  {4096, 2, 3, 8, 16, 288, 1},  {4096, 1, 3, 16, 16, 544, 1},
+                      {4096, 1, 3, 16, 16, 576, 2}, {4096, 1, 6, 8, 16, 544, 1},   {4096, 1, 6, 8, 16, 576, 2},
+                      {4096, 1, 6, 8, 16, 608, 3}};
+    for (int sms : {104, 116, 148}) {
         for (const G& g : geos) {
-            const size_t smem = 256 + (size_t)g.nst * g.eps * kBlk;
+            const int nblk_all = (int)(bytes / g.blk), nblk = (int)((2ull << 30) / g.blk);
+            std::vector<int> perm(nblk_all);
+            for (int i = 0; i < nblk_all; ++i) perm[i] = i;
+            std::shuffle(perm.begin(), perm.end(), std::mt19937(1));
+            int* dperm;
+            cudaMalloc(&dperm, sizeof(int) * nblk);
+            cudaMemcpy(dperm, perm.data(), sizeof(int) * nblk, cudaMemcpyHostToDevice);
+            const size_t smem = 256 + (size_t)g.nst * g.eps * (g.blk + g.pad);
             float best = 1e9f;
-            for (int r = 0; r < 6; ++r) {
+            for (int r = 0; r < 5; ++r) {
                 cudaEventRecord(a);
-                k_ring<<<sms * g.cps, 288, smem>>>(p, dperm, nblk, g.nst, g.eps, o);
+                k_ring<<<sms * g.cps, g.nthr, smem>>>(p, dperm, nblk, g.nst, g.eps, o, g.blk, g.pad, g.nthr, g.nprod);
                 cudaEventRecord(b);
                 cudaEventSynchronize(b);
                 float ms;
                 cudaEventElapsedTime(&ms, a, b);
                 best = std::min(best, ms);
             }
-            int occ = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ring, 288, smem);
-            printf("{\"sms\": %d, \"ctas_per_sm\": %d, \"resident\": %d, \"stages\": %d, \"stage_kb\": %zu, "
-                   "\"ring_kb_per_sm\": %zu, \"gbs\": %.1f, \"err\": \"%s\"}\n",
-                   sms, g.cps, occ, g.nst, g.eps * kBlk / 1024, g.cps * g.nst * g.eps * kBlk / 1024,
-                   (double)nblk * kBlk / (best * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
+            printf("{\"sms\": %d, \"entry\": %d, \"ctas_per_sm\": %d, \"threads\": %d, \"stages\": %d, \"entries_per_stage\": %d, "
+                   "\"slot_pad\": %d, \"gbs\": %.1f, \"err\": \"%s\"}\n",
+                   sms, g.blk, g.cps, g.nthr, g.nst, g.eps, g.pad, (double)nblk * g.blk / (best * 1e-3) / 1e9,
+                   cudaGetErrorString(cudaGetLastError()));
             fflush(stdout);
+            cudaFree(dperm);
         }
     }
     return 0;
