@@ -100,7 +100,7 @@ __device__ __forceinline__ uint32_t pack_part(const Parts3& a, const Parts3& b, 
 // EPS entries per ring stage: 16 (q.k rows g / g + 8, p.v two halves) or 8
 // (q.k rows g + 8 repeat rows g; one p.v MMA per d tile; twice the stages)
 template <int EPS>
-__global__ void __launch_bounds__(18 * 32, 1) k_attend_bf16tc(Dims D, State S, BTcParams P) {
+__global__ void __launch_bounds__(19 * 32, 1) k_attend_bf16tc(Dims D, State S, BTcParams P) {
     const long long t_entry = D.dbg_att && threadIdx.x == 0 ? (long long)globaltimer() : 0;  // PIKV_DEBUG_ATT
     long long t_wait = 0, n_stage = 0, n_ent = 0;
     griddep_enter();

@@ -99,7 +99,7 @@ __device__ __forceinline__ float rcpa(float x) {
     return y;
 }
 
-__global__ void __launch_bounds__(18 * 32, 1) k_attend_i4tc(Dims D, State S, I4Params P) {
+__global__ void __launch_bounds__(19 * 32, 1) k_attend_i4tc(Dims D, State S, I4Params P) {
     griddep_enter();
     extern __shared__ __align__(128) uint8_t smem[];
     const RingSmem R = ring_smem(smem);

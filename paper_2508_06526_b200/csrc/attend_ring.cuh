@@ -160,9 +160,9 @@ inline RingParams ring_params(const Dims& D, int eps, int pad, int extra) {
     const char* st = std::getenv("PIKV_ATT_STATIC");  // A/B experiments only
     P.dyn = st && st[0] == '1' ? 0 : 1;
     // two producer warps when the work items are static shares (both walk the
-    // same items), one with ticketed items; PIKV_RING_PROD=1 forces one (A/B)
+    // same items), one with ticketed items; PIKV_RING_PROD=1..3 (A/B)
     const char* rp = std::getenv("PIKV_RING_PROD");
-    P.nprod = D.att_share && !(rp && rp[0] == '1') ? 2 : 1;
+    P.nprod = D.att_share ? (rp && rp[0] >= '1' && rp[0] <= '3' ? rp[0] - '0' : 2) : 1;
     return P;
 }
 
