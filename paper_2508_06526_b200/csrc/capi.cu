@@ -469,9 +469,9 @@ static int validate(const pikv_config& c) {
         return fail(PIKV_ERR_INVALID_CONFIG, "codec rank must be in [1, head_dim]");
     if (c.n_layers < 0) return fail(PIKV_ERR_INVALID_CONFIG, "n_layers must be >= 0");
     if (c.d > 16384) return fail(PIKV_ERR_INVALID_CONFIG, "d must be <= 16384 (router stages q in smem)");
-    // k_foldback stages the per-(stream, head) global (m, l) in shared memory
-    if (8.0 * c.batch * c.n_heads + 4.0 * c.batch > 227.0 * 1024)
-        return fail(PIKV_ERR_INVALID_CONFIG, "batch x n_heads too large (fold-back: 8 B H + 4 B <= 227 KB)");
+    // k_foldback stages one stream's global (m, 1/l) per head in shared memory
+    if (8.0 * c.n_heads > 227.0 * 1024)
+        return fail(PIKV_ERR_INVALID_CONFIG, "n_heads too large (fold-back: 8 H <= 227 KB)");
     if (128 + 8.0 * c.d + 5.0 * c.E * (32 * 8 + 16) > 200 * 1024)
         return fail(PIKV_ERR_INVALID_CONFIG, "router: E x d too large for the shared-memory W ring");
     return PIKV_OK;
