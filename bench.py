@@ -359,7 +359,7 @@ def run_group(args, w, name, cfg, n_micro, local, world=1, rank=0, dist_on=False
         # enough that the control tail needs more SMs than int8's)
         # (the library's attend_reserve_sms: the HMMA low-rank kernel is
         # default for 32-wide bf16 slices)
-        attend_sms = nsm - {"Int8": 12, "Int4": 24, "LowRank": 32}.get(w["codec"], 44)
+        attend_sms = nsm - {"Int8": 12, "Int4": 32, "LowRank": 40}.get(w["codec"], 44)
     grp = EngineGroup(cfg, n_micro=n_micro, attend_sms=attend_sms, device=local)
     B, d, dp, Bm = cfg.batch, cfg.model.d, cfg.stored_width, grp.Bm
     if cfg.compressor.scheme in ("LowRank",):

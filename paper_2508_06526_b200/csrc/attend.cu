@@ -754,8 +754,11 @@ int attend_entries_per_stage(const Dims& D) {
 // consumers need more issue slots per byte than the control tail, the HMMA
 // low-rank kernel sustains more per SM than the CUDA-core bf16 kernel.
 int attend_reserve_sms(const Dims& D) {
-    if (attend_i4tc_applies(D)) return 24;
-    if (attend_bf16tc_applies(D)) return 32;
+    // (with static shares and two ring producers, profiles/scripts/r02_tc_sms.sh:
+    // c4-int4 72.3 K at 116 SMs vs 71.1 K at 124; c4-lowrank 77.6-78.0 K at 108
+    // vs 76.2-76.9 K at 116)
+    if (attend_i4tc_applies(D)) return 32;
+    if (attend_bf16tc_applies(D)) return 40;
     if (D.codec == PIKV_CODEC_INT8 || D.codec == PIKV_CODEC_INT4) return 12;
     return 44;
 }

@@ -2308,7 +2308,7 @@ int pikv_group_create(const pikv_config* cfg, int32_t n_micro, int32_t attend_sm
     // leave SMs to the control plane of the other micro-batch: all but
     // attend_reserve_sms(layout) (sweeps in profiles/README.md: c2 flat at
     // 44 K from 100 to 116 SMs, c4-int8 39.7 K at 136 vs 36.6 K at 148,
-    // c4-low-rank on the HMMA kernel 74 K at 116 vs 72.3 K at 124)
+    // c4-low-rank on the HMMA kernel 77.6-78.0 K at 108 vs 76.2-76.9 K at 116)
     if (attend_sms <= 0 && n_micro > 1) attend_sms = -1;
     for (int m = 0; m < n_micro; ++m) {
         pikv_engine* e = nullptr;
