@@ -611,49 +611,6 @@ __device__ __forceinline__ void encode_row(const Dims& D, const State& S, const 
     }
 }
 
-// int8 / int4 encode of one K or V row by threads [t0, t0 + nt) (whole warps)
-// while warp 0 runs the insert bookkeeping: the same arithmetic as
-// encode_row's quantized case, synchronised with named barrier 1 over the nt
-// encoding threads instead of __syncthreads.
-__device__ __forceinline__ void encode_quant_warps(const Dims& D, const void* x, int s, uint8_t* dst,
-                                                   float* scales_out, float* tmp, int t0, int nt) {
-    const int H = D.H, hd = D.d / H;
-    const int64_t base = (int64_t)s * D.d;
-    const int bits = D.codec == PIKV_CODEC_INT8 ? 8 : 4;
-    const float qmax = bits == 8 ? 127.0f : 7.0f;
-    const int tid = threadIdx.x - t0;
-    for (int i = tid; i < D.d; i += nt) tmp[i] = load_in(x, D.kv_dtype, base + i);
-    asm volatile("bar.sync 1, %0;" ::"r"(nt) : "memory");
-    const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
-    for (int h = warp; h < H; h += nw) {
-        float amax = 0.f;
-        for (int i = lane; i < hd; i += 32) amax = fmaxf(amax, fabsf(tmp[h * hd + i]));
-        for (int off = 16; off; off >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
-        float inv = 0.f, scale = 0.f;
-        if (amax > 0.f) {
-            scale = __fdiv_rn(amax, qmax);
-            inv = __fdiv_rn(qmax, amax);
-        }
-        if (lane == 0) scales_out[h] = scale;
-        if (bits == 8) {
-            for (int i = lane; i < hd; i += 32) {
-                float c = rintf(__fmul_rn(tmp[h * hd + i], inv));
-                c = fminf(fmaxf(c, -qmax), qmax);
-                ((int8_t*)dst)[h * hd + i] = (int8_t)(int)c;
-            }
-        } else {
-            for (int i2 = lane; i2 < hd / 2; i2 += 32) {
-                float c0 = rintf(__fmul_rn(tmp[h * hd + 2 * i2], inv));
-                float c1 = rintf(__fmul_rn(tmp[h * hd + 2 * i2 + 1], inv));
-                c0 = fminf(fmaxf(c0, -qmax), qmax);
-                c1 = fminf(fmaxf(c1, -qmax), qmax);
-                dst[(h * hd) / 2 + i2] = (uint8_t)(((int)c0 & 0xF) | (((int)c1 & 0xF) << 4));
-            }
-        }
-    }
-    asm volatile("bar.sync 1, %0;" ::"r"(nt) : "memory");  // tmp is reused by the next row
-}
-
 // KVStore::insert of stream s's k entries by the calling CTA (k_insert,
 // k_control); sm_entry = dynamic smem of insert_smem_bytes().  `sel` = the
 // step's experts in shared memory when the caller has them (k_control),
@@ -993,19 +950,7 @@ __device__ __forceinline__ void insert_body(const Dims& D, const Cfg& C, const S
         }  // LowRank / LoRAPlus: q_attn written by k_project
     };
     const bool overlap = D.codec == PIKV_CODEC_IDENTITY && (D.d * esz) % 16 == 0 && blockDim.x >= 64;
-    const bool quant = D.codec == PIKV_CODEC_INT8 || D.codec == PIKV_CODEC_INT4;
-    if (quant && blockDim.x >= 64 && blockDim.x % 32 == 0) {
-        // warp 0: bookkeeping; warps 1..: quantize K and V, the query
-        if (warp == 0) {
-            insert_book(D, S, s, sel, saliency, sm_dst, &sm_n);
-        } else {
-            const int t0 = 32, nt = blockDim.x - 32;
-            float* ksc = (float*)(sm_entry + 2 * pay);
-            encode_quant_warps(D, kin, s, sm_entry, ksc, tmp, t0, nt);
-            encode_quant_warps(D, vin, s, sm_entry + pay, ksc + D.H, tmp, t0, nt);
-            query(tid - t0, nt);
-        }
-    } else if (overlap) {
+    if (overlap) {
         // warp 0: bookkeeping; warps 1..: K/V rows -> smem entry, query
         if (warp == 0) {
             insert_book(D, S, s, sel, saliency, sm_dst, &sm_n);
