@@ -449,3 +449,59 @@ def test_engine_single_pass_retrieval(monkeypatch, sched, kw):
     monkeypatch.setenv("PIKV_CONTROL", "0")
     cfg = engine_config(router="TopK", sched=sched, batch=3, **kw)
     run_parity(cfg, 50, 61)
+
+
+@pytest.mark.parametrize("share", ["1", "0"])
+@pytest.mark.parametrize("batch", [2, 20])
+@pytest.mark.parametrize("codec", ["none", "Int4"])
+def test_work_distribution_parity(monkeypatch, share, batch, codec):
+    """Attention work as equal static shares per CTA (build_items_shares,
+    cta_first; two ring producer warps in the tensor-core kernels) or as
+    ticketed items, forced both ways at 2 and 20 streams (default: shares for
+    2..16 streams), on the c2 head shape (CUDA-core k_attend) and int4 codes
+    (IMMA kernel): every step against the oracle -- experts, evictions and
+    attended sets bit-exact, y within 2e-5.  Small rings leave fewer stage
+    units than attention CTAs, so the share builder's short-grid path (CTAs
+    without a share) runs too."""
+    monkeypatch.setenv("PIKV_ATT_SHARE", share)
+    H, hd = 32, 128
+    cfg = engine_config(router="TopK", sched="LRU", d=H * hd, H=H, E=16, k=2, G=1, n_tok=1, n_exp=16,
+                        S=64, ps=16, budget=6, batch=batch, dtype="bf16", n_layers=0,
+                        codec="Identity" if codec == "none" else codec)
+    cfg.model.head_width = hd
+    run_parity(cfg, 24 if batch > 2 else 40, 41, inject=False)
+
+
+@pytest.mark.parametrize("batch", [2, 20])
+def test_work_distribution_lowrank_modes_agree(monkeypatch, batch):
+    """Rank-32 low-rank slices (HMMA kernel): static shares with two ring
+    producers and ticketed items with one give the same step -- experts,
+    evictions and attended counts identical, y within 1e-6 (only the order of
+    the partial-softmax merge differs).  Compared GPU to GPU: against the
+    fp64 oracle the low-rank y also carries the fp32-vs-fp64 projection's
+    occasional one-ulp bf16 storage differences (test_engine_rank32_shape_parity)."""
+    H, hd, r = 32, 128, 32
+    cfg = engine_config(router="TopK", sched="LRU", d=H * hd, H=H, E=16, k=2, G=1, n_tok=1, n_exp=16,
+                        S=64, ps=16, budget=6, batch=batch, dtype="bf16", n_layers=0, codec="LowRank", rank=r)
+    cfg.model.head_width = hd
+    rng = np.random.default_rng(5)
+    basis = np.ascontiguousarray(
+        np.stack([np.linalg.qr(rng.standard_normal((hd, hd)))[0][:, :r].T for _ in range(H)]), np.float32)
+    engines = []
+    for share in ("1", "0"):
+        monkeypatch.setenv("PIKV_ATT_SHARE", share)
+        e = Engine(cfg)
+        e.set_codec(basis, None, None)
+        engines.append(e)
+    streams = [make_stream(24, cfg.model.d, 41 + 1000 * s, cfg.kv_dtype, 0) for s in range(batch)]
+    for t in range(24):
+        q, k, v = (np.stack([streams[s][i][t] for s in range(batch)]) for i in range(3))
+        out = []
+        for e in engines:
+            y = e.step_host(to_kv(q, cfg.kv_dtype), to_kv(k, cfg.kv_dtype), to_kv(v, cfg.kv_dtype), None)
+            experts, _, _, summ = e.read_step()
+            out.append((y, experts, [x["n_attended"] for x in summ], e.read_evictions()))
+        (y1, x1, n1, ev1), (y0, x0, n0, ev0) = out
+        assert np.array_equal(x1, x0) and n1 == n0 and ev1 == ev0, t
+        for s in range(batch):
+            assert rel_l2(y1[s].astype(np.float64), y0[s].astype(np.float64)) <= 1e-6, (t, s)
