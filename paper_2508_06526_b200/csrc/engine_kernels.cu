@@ -2587,8 +2587,11 @@ void launch_finish_merge(const Dims& D, const Cfg& C, const State& S, const Exch
 void launch_foldback(const Dims& D, const Cfg& C, const State& S, cudaStream_t st) {
     const size_t smem = sizeof(float) * 2 * (size_t)D.H;
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_foldback, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    // ~4 CTAs of 256 threads per B200 SM (148) in all, split over the streams
-    const int x = std::max(1, (4 * 148 + D.B - 1) / D.B);
+    // ~4 CTAs of 256 threads per B200 SM (148) in all, split over the streams,
+    // and no more per stream than its attended region can fill (small steps:
+    // c1's single stream would otherwise launch 592 mostly idle CTAs)
+    const int64_t fill = (D.att_stride + 255) / 256;
+    const int x = (int)std::max<int64_t>(1, std::min<int64_t>((4 * 148 + D.B - 1) / D.B, fill));
     launch_pdl(k_foldback, dim3(x, D.B), dim3(256), smem, st, D, C, S);
 }
 void launch_feedback(const Dims& D, const Cfg& C, const State& S, cudaStream_t st) {
