@@ -8,8 +8,10 @@
 // entry's per-head logit for the alpha fold-back (pipeline.cpp:302-312).
 //
 // Design (B200):
-//  * persistent grid: one 288-thread CTA per SM; work items = (stream, run of
-//    C consecutive retrieved entries), strided over CTAs;
+//  * persistent grid: two 288-thread CTAs per SM; work items = (stream, run of
+//    consecutive retrieved entries): each CTA's equal static share of all the
+//    streams' entries (build_items_shares; 2..16 streams per engine), else
+//    items taken from a global ticket;
 //  * warp 8 is the producer: lanes issue one cp.async.bulk (TMA bulk copy,
 //    SASS UBLKCP) per KV entry -- K, V (and scales) are contiguous in the
 //    paged pool, 16 KiB at 32x128 bf16 -- into an NST-stage shared-memory
@@ -218,11 +220,11 @@ __global__ void __launch_bounds__(kThreads, MINB) k_attend(Dims D, State S, AttP
         // busy with the previous micro-batch's tail kernels -- simply run
         // fewer items; P.dyn = 0 strides them statically (blockIdx + i*grid).
         auto next_item = [&](int prev) -> int {
-            if (!P.dyn) return prev < 0 ? (int)blockIdx.x : prev + (int)gridDim.x;
             if (D.att_share) {  // equal static shares: this CTA's items, then the sentinel
                 const int w = prev < 0 ? S.cta_first[blockIdx.x] : prev + 1;
                 return w < S.cta_first[blockIdx.x + 1] ? w : n_items;
             }
+            if (!P.dyn) return prev < 0 ? (int)blockIdx.x : prev + (int)gridDim.x;
             int w = 0;
             if (lane == 0) w = atomicAdd(&S.n_items[1], 1);
             return __shfl_sync(0xffffffffu, w, 0);

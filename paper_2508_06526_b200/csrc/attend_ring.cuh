@@ -1,12 +1,13 @@
 // SPDX-License-Identifier: Apache-2.0
 //
 // The TMA ring shared by the tensor-core attention kernels (attend_i4tc.cu,
-// attend_bf16tc.cu): one CTA per SM, `ncw` consumer warps + one producer
-// warp.  The producer takes work items (stream, run of retrieved entries)
-// from the global ticket, hands each to the consumers through a small smem
-// queue, and streams the item's entries into an NST-stage ring of kRingEPS
-// entries per stage (one cp.async.bulk per entry, slot stride padded for the
-// consumers' bank pattern; full/empty mbarriers).  Same protocol as k_attend
+// attend_bf16tc.cu): one CTA per SM, `ncw` consumer warps + one or two
+// producer warps.  The producers take work items (stream, run of retrieved
+// entries) -- the CTA's static share, or from the global ticket -- hand each
+// to the consumers through a small smem queue, and stream the items' entries
+// into an NST-stage ring of kRingEPS entries per stage (one cp.async.bulk per
+// entry, slot stride padded for the consumers' bank pattern; full/empty
+// mbarriers).  Same protocol as k_attend
 // (attend.cu), which keeps its own copy for its 2-CTA geometry.
 #pragma once
 
@@ -78,11 +79,11 @@ __device__ __forceinline__ void ring_produce(const Dims& D, const State& S, cons
         }
     };
     auto next_item = [&](int prev) -> int {
-        if (!P.dyn) return prev < 0 ? (int)blockIdx.x : prev + (int)gridDim.x;
         if (D.att_share) {  // equal static shares: this CTA's items, then the sentinel
             const int w = prev < 0 ? S.cta_first[blockIdx.x] : prev + 1;
             return w < S.cta_first[blockIdx.x + 1] ? w : n_items;
         }
+        if (!P.dyn) return prev < 0 ? (int)blockIdx.x : prev + (int)gridDim.x;
         int w = 0;
         if (lane == 0) w = atomicAdd(&S.n_items[1], 1);
         return __shfl_sync(kAll, w, 0);
