@@ -495,8 +495,10 @@ int pikv_column_variance_host(const double* rows, int32_t n, int32_t d, double* 
  * exactly the reference's step sequence; results equal those of the
  * micro-batch engines stepped one after another.
  * attend_sms > 0 limits the persistent attention grid to that many SMs so
- * the other micro-batch's control kernels find free SMs (0 = auto: all but
- * 44 SMs when n_micro > 1, all but 12 for int8/int4; measured on B200). */
+ * the other micro-batch's control kernels find free SMs (0 = auto when
+ * n_micro > 1: all but 44 SMs for bf16 / f32 heads, 12 for int8, 32 for the
+ * int4 IMMA kernel, 40 for the HMMA kernel of 32-wide bf16 slices; measured
+ * on B200). */
 typedef struct pikv_group pikv_group;
 int pikv_group_create(const pikv_config* cfg, int32_t n_micro, int32_t attend_sms,
                       int32_t cuda_device, pikv_group** out);
