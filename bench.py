@@ -435,16 +435,20 @@ def run_group(args, w, name, cfg, n_micro, local, world=1, rank=0, dist_on=False
         dist.barrier()
     ms = max_over_ranks(ev0.elapsed_time(ev1))
     launches = grp.kernel_launches() - launches0
-    att_ms, n_att = grp.read_timing()
+    # attention launches as intervals: with the attention SM partition the two
+    # micro-batches' launches overlap, so the kernel's time is the union of the
+    # intervals (the time any attention launch was in flight), not their sum
+    att_sum_ms, att_ms, n_att = grp.read_timing_union()
     grp.sync()
     _, _, _, summ = grp.read_step()
     att_last = sum(s["n_attended"] for s in summ)  # global (after the cross-rank merge)
     local_att = sum(e.local_attended() for e in grp.engines)  # this rank's own shards
     entry_bytes = grp.engines[0].entry_bytes()
     peak, peak_kind = load_peaks()
-    attend_avg_ms = att_ms / max(n_att, 1)
+    attend_avg_ms = att_sum_ms / max(n_att, 1)  # per launch, submit to end (includes any overlap)
+    attend_busy_ms = att_ms / max(n_att, 1)     # union per launch
     alg_per_launch = local_att * entry_bytes / n_micro
-    achieved = alg_per_launch / (attend_avg_ms * 1e-3) / 1e9 if attend_avg_ms else 0.0
+    achieved = alg_per_launch / (attend_busy_ms * 1e-3) / 1e9 if attend_busy_ms else 0.0
     rank_bytes = None
     if dist_on:  # this rank's KV bytes per step, max / min over ranks (balance)
         mx_b = max_over_ranks(float(local_att * entry_bytes))
@@ -503,7 +507,7 @@ def run_group(args, w, name, cfg, n_micro, local, world=1, rank=0, dist_on=False
         dist.barrier()
     e2e_runs = [e2e_run() for _ in range(3)]
     grp.set_timing(False)
-    e2e_att_ms, _ = grp.read_timing()
+    _, e2e_att_ms, _ = grp.read_timing_union()
     e2e_ms = max_over_ranks(float(np.median(e2e_runs)))
     e2e = {"value": B * args.steps / (e2e_ms * 1e-3), "unit": "tokens/s",
            "h2d_bytes_per_step": 3 * B * d * elem, "d2h_bytes_per_step": B * dp * 4,
@@ -538,9 +542,19 @@ def run_group(args, w, name, cfg, n_micro, local, world=1, rank=0, dist_on=False
                      "frac": achieved / peak,
                      "traffic": (load_traffic(name) or (None, None))[0],
                      "traffic_source": (load_traffic(name) or (None, None))[1],
-                     "kernel": "k_attend (decode attention, TMA bulk ring), one launch per "
-                               "micro-batch, timed live in the timed region",
-                     "peak_kind": peak_kind, "avg_launch_ms": attend_avg_ms,
+                     "kernel": "decode attention (k_attend / k_attend_bf16tc / k_attend_i4tc), one "
+                               "launch per micro-batch, timed live in the timed region: achieved = "
+                               "algorithmic bytes of the timed launches / the union of their "
+                               "[submit, end] intervals (launches of the two micro-batches overlap "
+                               "in the attention SM partition)",
+                     "peak_kind": peak_kind,
+                     "peak_note": "MEASURED_PEAKS hbm_gbs is a copy (read + write) figure; pure "
+                                  "reads stream at 6.9-7.3 TB/s on this B200 "
+                                  "(profiles/microbench/ring_sweep.cu, read_bw.cu), so this "
+                                  "read-only kernel can exceed it",
+                     "avg_launch_ms": attend_avg_ms,
+                     "busy_ms_per_launch": attend_busy_ms,
+                     "attention_partition": grp.attention_partition(),
                      "launches_timed": n_att,
                      "algorithmic_bytes_per_launch": alg_per_launch,
                      "attend_share_of_step": att_ms / ms if ms else None},

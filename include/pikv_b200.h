@@ -530,6 +530,13 @@ int pikv_group_sync(pikv_group* grp);
  * (at most 8192 launches per micro-batch are kept between reads). */
 int pikv_group_set_timing(pikv_group* grp, int32_t on);
 int pikv_group_read_timing(pikv_group* grp, double* ms, int32_t* n);
+/* The same launches as intervals on one time axis: *sum_ms = summed launch
+ * times, *union_ms = the time any attention launch was in flight (launches of
+ * different micro-batches overlap in the attention SM partition). */
+int pikv_group_read_timing_union(pikv_group* grp, double* sum_ms, double* union_ms, int32_t* n);
+/* 1 when the group's attention runs in its own green-context SM partition
+ * (default for the two-CTA CUDA-core attention kernel; PIKV_GREEN=0 / 1). */
+int pikv_group_attention_partition(pikv_group* grp);
 /* Debug probe (PIKV_GROUP_TIMELINE=1 when the group is created; device-pointer
  * submits): rows of 6 doubles (micro-batch, control start, control end, cross-
  * micro-batch wait satisfied, attention end, tail end) in ms relative to the

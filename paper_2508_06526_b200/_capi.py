@@ -112,6 +112,8 @@ SIGNATURES = {
     "pikv_group_set_timing": (ctypes.c_int, [c_vp, c_i32]),
     "pikv_group_read_timing": (ctypes.c_int, [c_vp, P(c_f64), P(c_i32)]),
     "pikv_group_read_timeline": (ctypes.c_int, [c_vp, P(c_f64), c_i32, P(c_i32)]),
+    "pikv_group_read_timing_union": (ctypes.c_int, [c_vp, P(c_f64), P(c_f64), P(c_i32)]),
+    "pikv_group_attention_partition": (ctypes.c_int, [c_vp]),
     "pikv_nccl_unique_id": (ctypes.c_int, [c_vp]),
     "pikv_engine_attach_nccl": (ctypes.c_int, [c_vp, c_vp]),
     "pikv_engine_set_nccl_comm": (ctypes.c_int, [c_vp, c_vp]),

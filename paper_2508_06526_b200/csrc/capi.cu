@@ -3,6 +3,7 @@
 // C-ABI of the B200 PiKV engine (include/pikv_b200.h): engine lifetime,
 // HBM allocation, the per-step launch sequence (captured once into a CUDA
 // graph and replayed), result readback and the pure-function entry points.
+#include <cuda.h>  // green-context types only: the entry points come from cudaGetDriverEntryPoint
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -2279,6 +2280,14 @@ struct pikv_group {
     std::vector<std::vector<std::pair<cudaEvent_t, cudaEvent_t>>> tev;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tfree;
     size_t in_bytes = 0, y_bytes = 0, sal_elems = 0;  // per micro-batch
+    // Attention SM partition (PIKV_GREEN=1): a green context owning the
+    // attention SMs; each micro-batch's attention graph is captured and run on
+    // its own stream in it, so the two micro-batches' attention launches need
+    // no ordering (the next one's CTAs take the partition's SMs as the
+    // previous one's finish) and can never take the control plane's SMs.
+    CUgreenCtx gctx = nullptr;
+    std::vector<cudaStream_t> att_st;
+    std::vector<cudaEvent_t> ctl_done;
     // timeline probe (PIKV_GROUP_TIMELINE=1 at create; pikv_group_read_timeline):
     // per submit, events before / after the control graph, after the cross-
     // micro-batch wait, after the attention graph, after the tail
@@ -2289,6 +2298,55 @@ struct pikv_group {
     };
     std::vector<TL> tl;
 };
+
+// Driver entry points for green contexts (no link against libcuda: the
+// library must load on hosts without a driver, e.g. for the CPU tests).
+static void* drv(const char* name) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+        return nullptr;
+    return fn;
+}
+
+// A green context of `sms` SMs (a multiple of 8) and one stream in it per
+// micro-batch; false (nothing created) when the driver cannot provide it.
+static bool make_attention_partition(pikv_group* g, int sms) {
+    using GetRes = CUresult (*)(CUdevice, CUdevResource*, CUdevResourceType);
+    using Split = CUresult (*)(CUdevResource*, unsigned int*, const CUdevResource*, CUdevResource*, unsigned int,
+                               unsigned int);
+    using GenDesc = CUresult (*)(CUdevResourceDesc*, CUdevResource*, unsigned int);
+    using Create = CUresult (*)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned int);
+    using StreamCreate = CUresult (*)(CUstream*, CUgreenCtx, unsigned int, int);
+    using DevGet = CUresult (*)(CUdevice*, int);
+    auto dev_get = reinterpret_cast<DevGet>(drv("cuDeviceGet"));
+    auto get_res = reinterpret_cast<GetRes>(drv("cuDeviceGetDevResource"));
+    auto split = reinterpret_cast<Split>(drv("cuDevSmResourceSplitByCount"));
+    auto gen = reinterpret_cast<GenDesc>(drv("cuDevResourceGenerateDesc"));
+    auto create = reinterpret_cast<Create>(drv("cuGreenCtxCreate"));
+    auto screate = reinterpret_cast<StreamCreate>(drv("cuGreenCtxStreamCreate"));
+    if (!dev_get || !get_res || !split || !gen || !create || !screate) return false;
+    CUdevice dev;
+    CUdevResource all{}, part[1]{}, rest{};
+    unsigned int ng = 1;
+    CUdevResourceDesc desc;
+    if (dev_get(&dev, g->device) != CUDA_SUCCESS || get_res(dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS)
+        return false;
+    if (split(part, &ng, &all, &rest, 0, (unsigned)sms) != CUDA_SUCCESS || ng != 1 ||
+        (int)part[0].sm.smCount != sms)
+        return false;
+    if (gen(&desc, part, 1) != CUDA_SUCCESS || create(&g->gctx, desc, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS)
+        return false;
+    for (int m = 0; m < g->n; ++m) {
+        CUstream st = nullptr;
+        if (screate(&st, g->gctx, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS) return false;
+        g->att_st.push_back((cudaStream_t)st);
+        cudaEvent_t ev;
+        cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        g->ctl_done.push_back(ev);
+    }
+    return true;
+}
 
 int pikv_group_create(const pikv_config* cfg, int32_t n_micro, int32_t attend_sms, int32_t cuda_device,
                       pikv_group** out) {
@@ -2345,6 +2403,27 @@ int pikv_group_create(const pikv_config* cfg, int32_t n_micro, int32_t attend_sm
     }
     cudaEventCreateWithFlags(&g->join, cudaEventDisableTiming);
     g->tev.resize(n_micro);
+    // default for the CUDA-core attention kernel (two CTAs per SM): c2 45.3 ->
+    // 49.4 K tokens/s, c3 44.7 -> 46.2 K, c5 157 -> 163 K; the one-CTA-per-SM
+    // tensor-core kernels lose 2-3 % (their control-bound steps lose the SMs
+    // the attention gaps used to free): profiles/README.md.  PIKV_GREEN=0 / 1
+    // overrides; sharded groups keep the ordered attention.
+    const char* gv = std::getenv("PIKV_GREEN");
+    const bool want_green = gv ? gv[0] == '1' : attend_ctas_per_sm(g->eng[0]->D) == 2;
+    if (want_green && n_micro > 1 && !g->eng[0]->exchange_path()) {
+        // the partition holds the attention grid's SMs, rounded down to the
+        // green-context granularity (8 SMs on sm_90+)
+        const int cps = std::max(1, attend_ctas_per_sm(g->eng[0]->D));
+        const int sms = (g->eng[0]->D.attend_ctas / cps) & ~7;
+        if (sms >= 8 && make_attention_partition(g, sms)) {
+            for (auto* e : g->eng) e->D.attend_ctas = cps * sms;
+        } else {
+            for (auto st : g->att_st) cudaStreamDestroy(st);
+            for (auto ev : g->ctl_done) cudaEventDestroy(ev);
+            g->att_st.clear(), g->ctl_done.clear();
+            g->gctx = nullptr;  // (a partly created context is left to process exit)
+        }
+    }
     if (const char* tv = std::getenv("PIKV_GROUP_TIMELINE")) g->timeline = tv[0] == '1';
     const Dims& D = g->eng[0]->D;
     g->in_bytes = (size_t)D.B * D.d * (D.kv_dtype == PIKV_DTYPE_BF16 ? 2 : 4);
@@ -2368,6 +2447,12 @@ int pikv_group_destroy(pikv_group* g) {
     if (g->join) cudaEventDestroy(g->join);
     for (auto& r : g->tl)
         for (auto ev : r.ev) cudaEventDestroy(ev);
+    for (auto st : g->att_st) cudaStreamSynchronize(st), cudaStreamDestroy(st);
+    for (auto ev : g->ctl_done) cudaEventDestroy(ev);
+    if (g->gctx) {
+        using Destroy = CUresult (*)(CUgreenCtx);
+        if (auto d = reinterpret_cast<Destroy>(drv("cuGreenCtxDestroy"))) d(g->gctx);
+    }
     delete g;
     return PIKV_OK;
 }
@@ -2428,8 +2513,18 @@ int pikv_group_submit(pikv_group* g, int32_t m, const void* q, const void* k, co
         if (g_tl_rec) CUDA_TRY(cudaEventRecord(g_tl_rec[1], st));
         if (!rc) {
             // (unordered attention launches measured: c2 43.8 vs 43.7 K, c5 145 vs 154 K)
-            if (g->n > 1) CUDA_TRY(cudaStreamWaitEvent(st, g->att_done[(m + g->n - 1) % g->n], 0));
-            if (g_tl_rec) CUDA_TRY(cudaEventRecord(g_tl_rec[2], st));
+            // attention stream: the engine stream (ordered after the previous
+            // micro-batch's attention), or this micro-batch's stream in the
+            // attention partition (no ordering needed)
+            const bool green = !g->att_st.empty();
+            cudaStream_t ast = green ? g->att_st[m] : st;
+            if (green) {
+                CUDA_TRY(cudaEventRecord(g->ctl_done[m], st));
+                CUDA_TRY(cudaStreamWaitEvent(ast, g->ctl_done[m], 0));
+            } else if (g->n > 1) {
+                CUDA_TRY(cudaStreamWaitEvent(st, g->att_done[(m + g->n - 1) % g->n], 0));
+            }
+            if (g_tl_rec) CUDA_TRY(cudaEventRecord(g_tl_rec[2], ast));
             std::pair<cudaEvent_t, cudaEvent_t> p{nullptr, nullptr};
             if (g->timing && g->tev[m].size() < 8192) {  // bounded until pikv_group_read_timing
                 if (g->tfree.empty()) {
@@ -2440,12 +2535,17 @@ int pikv_group_submit(pikv_group* g, int32_t m, const void* q, const void* k, co
                     g->tfree.pop_back();
                 }
                 g->tev[m].push_back(p);
-                CUDA_TRY(cudaEventRecord(p.first, st));
+                CUDA_TRY(cudaEventRecord(p.first, ast));
             }
+            // the attention graph is captured and replayed on ast (a graph
+            // captured on another stream would run on every SM)
+            e->stream = ast;
             rc = run_step(e, dq, dk, dv, ds, dy, true, nullptr, kPartAttend);
-            if (p.second) CUDA_TRY(cudaEventRecord(p.second, st));
-            CUDA_TRY(cudaEventRecord(g->att_done[m], st));
-            if (g_tl_rec) CUDA_TRY(cudaEventRecord(g_tl_rec[3], st));
+            e->stream = st;
+            if (p.second) CUDA_TRY(cudaEventRecord(p.second, ast));
+            CUDA_TRY(cudaEventRecord(g->att_done[m], ast));
+            if (green) CUDA_TRY(cudaStreamWaitEvent(st, g->att_done[m], 0));
+            if (g_tl_rec) CUDA_TRY(cudaEventRecord(g_tl_rec[3], ast));
         }
         if (!host) {
             if (!rc) rc = run_step(e, dq, dk, dv, ds, dy, true, nullptr, kPartTail);
@@ -2539,6 +2639,48 @@ int pikv_group_sync(pikv_group* g) {
 
 int pikv_group_set_timing(pikv_group* g, int32_t on) {
     g->timing = on != 0;
+    return PIKV_OK;
+}
+
+int pikv_group_attention_partition(pikv_group* g) { return g && g->gctx ? 1 : 0; }
+
+int pikv_group_read_timing_union(pikv_group* g, double* sum_ms, double* union_ms, int32_t* n) {
+    // attention launches of all micro-batches as [start, end] on one time
+    // axis; with overlapping launches (attention partition) the union is the
+    // time the attention kernels had the GPU
+    std::vector<std::pair<double, double>> iv;
+    cudaEvent_t ref = nullptr;
+    for (auto& v : g->tev)
+        for (auto& p : v) {
+            CUDA_TRY(cudaEventSynchronize(p.second));
+            if (!ref) ref = p.first;
+        }
+    double tot = 0;
+    for (auto& v : g->tev) {
+        for (auto& p : v) {
+            float a = 0, b = 0;
+            CUDA_TRY(cudaEventElapsedTime(&a, ref, p.first));
+            CUDA_TRY(cudaEventElapsedTime(&b, ref, p.second));
+            iv.emplace_back(a, b);
+            tot += b - a;
+            g->tfree.push_back(p);
+        }
+        v.clear();
+    }
+    std::sort(iv.begin(), iv.end());
+    double uni = 0, cs = 0, ce = -1e300;
+    for (auto& x : iv) {
+        if (x.first > ce) {
+            if (ce > cs) uni += ce - cs;
+            cs = x.first, ce = x.second;
+        } else {
+            ce = std::max(ce, x.second);
+        }
+    }
+    if (!iv.empty() && ce > cs) uni += ce - cs;
+    if (sum_ms) *sum_ms = tot;
+    if (union_ms) *union_ms = uni;
+    if (n) *n = (int32_t)iv.size();
     return PIKV_OK;
 }
 

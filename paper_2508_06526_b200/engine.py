@@ -517,6 +517,16 @@ class EngineGroup:
         check(lib().pikv_group_read_timing(self.h, ctypes.byref(ms), ctypes.byref(n)))
         return ms.value, n.value
 
+    def attention_partition(self) -> bool:
+        """True when the attention runs in its own green-context SM partition."""
+        return bool(lib().pikv_group_attention_partition(self.h))
+
+    def read_timing_union(self):
+        """(summed attention launch ms, ms any attention launch was in flight, launches)."""
+        tot, uni, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_int32()
+        check(lib().pikv_group_read_timing_union(self.h, ctypes.byref(tot), ctypes.byref(uni), ctypes.byref(n)))
+        return tot.value, uni.value, n.value
+
     def prefill_synthetic(self, tokens: int, seed: int = 1):
         for m, e in enumerate(self.engines):
             e.prefill_synthetic(tokens, seed=seed + 7919 * m)
