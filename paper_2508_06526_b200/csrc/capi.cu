@@ -2416,7 +2416,15 @@ int pikv_group_create(const pikv_config* cfg, int32_t n_micro, int32_t attend_sm
         const int cps = std::max(1, attend_ctas_per_sm(g->eng[0]->D));
         const int sms = (g->eng[0]->D.attend_ctas / cps) & ~7;
         if (sms >= 8 && make_attention_partition(g, sms)) {
-            for (auto* e : g->eng) e->D.attend_ctas = cps * sms;
+            // with the partition the static shares win at every batch (c5, 32
+            // streams per engine: 165.5 vs 162.9 K tokens/s with tickets; c4-int8
+            // 39.6 vs 38.5-39.1 K): no other micro-batch's control kernels hold
+            // attention SMs, so the CTAs start together
+            const bool share_env = std::getenv("PIKV_ATT_SHARE") != nullptr;
+            for (auto* e : g->eng) {
+                e->D.attend_ctas = cps * sms;
+                if (!share_env && e->D.B >= 2) e->D.att_share = 1;
+            }
         } else {
             for (auto st : g->att_st) cudaStreamDestroy(st);
             for (auto ev : g->ctl_done) cudaEventDestroy(ev);
