@@ -654,10 +654,10 @@ def main():
         w["B"] = w["B"] * world
     cfg = make_config(w, world=world, rank=rank)
     # micro-batches: 4 where the attention runs in its own SM partition (the
-    # two-CTA CUDA-core kernel, one rank: launches overlap, so quarter-batch
+    # two-CTA CUDA-core kernel: launches overlap, so quarter-batch
     # launches cost no tail -- c2 49.5 -> 51.0 K, c3 46.2 -> 48.3 K, c5 166 ->
     # 177 K tokens/s), else 2 (profiles/README.md)
-    part = world == 1 and not args.sharded_rehearsal and w["codec"] == "Identity"
+    part = w["codec"] == "Identity"
     default_micro = 4 if part and w["B"] % 4 == 0 and w["B"] >= 16 else 2
     n_micro = args.micro if args.micro is not None else (default_micro if w["B"] % 2 == 0 else 1)
     if w["B"] % n_micro:

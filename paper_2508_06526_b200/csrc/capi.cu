@@ -2407,10 +2407,11 @@ int pikv_group_create(const pikv_config* cfg, int32_t n_micro, int32_t attend_sm
     // 49.4 K tokens/s, c3 44.7 -> 46.2 K, c5 157 -> 163 K; the one-CTA-per-SM
     // tensor-core kernels lose 2-3 % (their control-bound steps lose the SMs
     // the attention gaps used to free): profiles/README.md.  PIKV_GREEN=0 / 1
-    // overrides; sharded groups keep the ordered attention.
+    // overrides.  Sharded groups too: the attention part has no collective
+    // (the all-gather follows in the merge part, on the engine stream).
     const char* gv = std::getenv("PIKV_GREEN");
     const bool want_green = gv ? gv[0] == '1' : attend_ctas_per_sm(g->eng[0]->D) == 2;
-    if (want_green && n_micro > 1 && !g->eng[0]->exchange_path()) {
+    if (want_green && n_micro > 1) {
         // the partition holds the attention grid's SMs, rounded down to the
         // green-context granularity (8 SMs on sm_90+)
         const int cps = std::max(1, attend_ctas_per_sm(g->eng[0]->D));
