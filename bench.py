@@ -653,12 +653,11 @@ def main():
         # the per-GPU KV read per step stays that of one GPU ("weak" scaling)
         w["B"] = w["B"] * world
     cfg = make_config(w, world=world, rank=rank)
-    # micro-batches: 4 where the attention runs in its own SM partition (the
-    # two-CTA CUDA-core kernel: launches overlap, so quarter-batch
-    # launches cost no tail -- c2 49.5 -> 51.0 K, c3 46.2 -> 48.3 K, c5 166 ->
-    # 177 K tokens/s), else 2 (profiles/README.md)
-    part = w["codec"] == "Identity"
-    default_micro = 4 if part and w["B"] % 4 == 0 and w["B"] >= 16 else 2
+    # micro-batches: 4 with the attention in its own SM partition (launches
+    # overlap, so quarter-batch launches cost no tail -- c2 49.5 -> 51.0 K, c3
+    # 46.2 -> 48.3 K, c5 166 -> 177 K, c4-lowrank 77.8 -> 81.9 K, c4-int4 72.1 ->
+    # 74.8 K tokens/s; int8 even), else 2 (profiles/README.md)
+    default_micro = 4 if w["B"] % 4 == 0 and w["B"] >= 16 else 2
     n_micro = args.micro if args.micro is not None else (default_micro if w["B"] % 2 == 0 else 1)
     if w["B"] % n_micro:
         n_micro = 1

@@ -2409,8 +2409,11 @@ int pikv_group_create(const pikv_config* cfg, int32_t n_micro, int32_t attend_sm
     // the attention gaps used to free): profiles/README.md.  PIKV_GREEN=0 / 1
     // overrides.  Sharded groups too: the attention part has no collective
     // (the all-gather follows in the merge part, on the engine stream).
+    // The one-CTA-per-SM tensor-core kernels gain from it from four
+    // micro-batches on (c4-lowrank 77.8 -> 81.9 K, c4-int4 72.1 -> 74.8 K
+    // tokens/s), not with two.
     const char* gv = std::getenv("PIKV_GREEN");
-    const bool want_green = gv ? gv[0] == '1' : attend_ctas_per_sm(g->eng[0]->D) == 2;
+    const bool want_green = gv ? gv[0] == '1' : (attend_ctas_per_sm(g->eng[0]->D) == 2 || n_micro >= 4);
     if (want_green && n_micro > 1) {
         // the partition holds the attention grid's SMs, rounded down to the
         // green-context granularity (8 SMs on sm_90+)
