@@ -2412,8 +2412,20 @@ int pikv_group_create(const pikv_config* cfg, int32_t n_micro, int32_t attend_sm
     // The one-CTA-per-SM tensor-core kernels gain from it from four
     // micro-batches on (c4-lowrank 77.8 -> 81.9 K, c4-int4 72.1 -> 74.8 K
     // tokens/s), not with two.
+    // Not by default under a CUDA tool that injects itself (the environment
+    // variables ncu / nsys / compute-sanitizer set): ncu cannot prepare every
+    // kernel of a green context for profiling (an all-kernel launch list
+    // failed with an unknown error), and the tools' kernel lists must not
+    // depend on it.
     const char* gv = std::getenv("PIKV_GREEN");
-    const bool want_green = gv ? gv[0] == '1' : (attend_ctas_per_sm(g->eng[0]->D) == 2 || n_micro >= 4);
+    bool tool = false;  // injected by ncu / nsys / compute-sanitizer / CUPTI injection
+    for (const char* var : {"CUDA_INJECTION64_PATH", "NV_TPS_LAUNCH_TOKEN", "NV_NSIGHT_INJECTION_TRANSPORT_TYPE",
+                            "NVIDIA_PROCESS_INJECTION_CRASH_REPORTING"}) {
+        const char* v = std::getenv(var);
+        tool = tool || (v && v[0]);
+    }
+    const bool want_green =
+        gv ? gv[0] == '1' : !tool && (attend_ctas_per_sm(g->eng[0]->D) == 2 || n_micro >= 4);
     if (want_green && n_micro > 1) {
         // the partition holds the attention grid's SMs, rounded down to the
         // green-context granularity (8 SMs on sm_90+)
