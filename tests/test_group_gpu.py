@@ -115,3 +115,40 @@ def test_group_step_full_batch_buffers():
         assert torch.equal(ya, yb)
     a.close()
     b.close()
+
+
+@pytest.mark.parametrize("n_micro", [2, 4])
+def test_attention_partition_changes_only_the_schedule(monkeypatch, n_micro):
+    """The attention SM partition (green context; launches of different
+    micro-batches unordered and overlapping) against the ordered pipeline on
+    all SMs, same attention grid (104 SMs, a multiple of 8): y, experts and
+    attended counts bit-identical every step at the c2 head shape (32 x 128
+    bf16, E16 top-2); the partition is reported active only when asked for."""
+    B, T, d = 8, 12, 4096
+    cfg = engine_config(router="TopK", sched="LRU", d=d, H=32, E=16, k=2, S=64, G=1, n_tok=1,
+                        n_exp=16, budget=6, ps=16, n_layers=0, dtype="bf16", batch=B)
+    cfg.model.head_width = 128
+    rng = np.random.default_rng(9)
+    x = torch.from_numpy(bf16_bits(rng.standard_normal((T, 3, B, d))).view(np.int16)).cuda()
+    out = []
+    for green in ("1", "0"):
+        monkeypatch.setenv("PIKV_GREEN", green)
+        grp = EngineGroup(cfg, n_micro=n_micro, attend_sms=104)
+        assert grp.attention_partition() == (green == "1")
+        Bm = B // n_micro
+        ys = torch.zeros(T, B, cfg.stored_width, dtype=torch.float32, device="cuda")
+        rec = []
+        for t in range(T):
+            for m in range(n_micro):
+                sl = slice(m * Bm, (m + 1) * Bm)
+                grp.submit(m, x[t, 0, sl], x[t, 1, sl], x[t, 2, sl], None, ys[t, sl])
+            grp.sync()
+            steps = [e.read_step() for e in grp.engines]
+            rec.append((np.concatenate([s[0] for s in steps]),
+                        [x_["n_attended"] for s in steps for x_ in s[3]]))
+        out.append((ys.cpu().numpy(), rec))
+        grp.close()
+    (y1, r1), (y0, r0) = out
+    assert np.array_equal(y1.view(np.uint32), y0.view(np.uint32))
+    for t in range(T):
+        assert np.array_equal(r1[t][0], r0[t][0]) and r1[t][1] == r0[t][1], t
